@@ -1,0 +1,1080 @@
+/*
+ * ipm_oracle.c — plain fp64 CPU oracle of the IPM hot path (arXiv 1912.09238).
+ *
+ * TEST INFRASTRUCTURE ONLY (see ipm_oracle.h).  Citations "PAPER.md:n" are
+ * lines of the paper's LaTeX source; "reading k" refers to the numbered
+ * readings of SURVEY.md §8(c), copied into DESIGN.md.
+ *
+ * Style: every routine is the textbook form of the paper's formula.  Loops are
+ * written in the paper's index order; nothing is blocked, fused or reordered.
+ * OpenMP only distributes independent spatial cells (the dual
+ * problem needs no communication).
+ */
+#include "ipm_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define PI_ 3.14159265358979323846
+
+struct orc_ctx {
+  orc_problem P;
+  int N, Q, m, d, F, cells;
+  int32_t *idx;   /* [N][p] multi-indices, graded then lexicographically descending */
+  double *xi;     /* [Q][p] nodes */
+  double *omega;  /* [Q]    w_k f_Xi(xi_k) */
+  double *Phi;    /* [Q][N] phi_i(xi_k) */
+  int32_t *nbr;   /* [cells][F] neighbour, or -1-tag on the boundary */
+  double *nrm;    /* [cells][F][2] outward unit normal */
+  double *coef;   /* [cells][F] |e| / |Omega_j| */
+  double *area;   /* [cells] */
+  double *perim;  /* [cells] */
+  double *xc;     /* [cells][2] cell centre (1D/cart) */
+  double *bc_u;   /* [4][Q][m] ghost states of STATE boundaries */
+  int32_t *level; /* [cells] refinement level index (adaptivity) */
+  int n_levels;
+  int Nl[8];      /* N at each level */
+};
+
+/* ------------------------------------------------------------------------ */
+/* Random space: Legendre polynomials, Gauss-Legendre rule, total-degree basis */
+/* ------------------------------------------------------------------------ */
+
+/* P_0..P_n at x by the three-term recurrence (k+1)P_{k+1} = (2k+1)x P_k - k P_{k-1}. */
+static void legendre_P(int n, double x, double *P) {
+  P[0] = 1.0;
+  if (n >= 1) P[1] = x;
+  for (int k = 1; k < n; ++k) P[k + 1] = ((2.0 * k + 1.0) * x * P[k] - k * P[k - 1]) / (k + 1.0);
+}
+
+/* Orthonormal Legendre w.r.t. the density 1/2 on [-1,1]: sqrt(2i+1) P_i. */
+static double phi_1d(int i, double x) {
+  double P[64];
+  legendre_P(i, x, P);
+  return sqrt(2.0 * i + 1.0) * P[i];
+}
+
+/* Gauss-Legendre nodes (ascending) and weights (sum 2): Newton on P_q. */
+void orc_gauss_legendre(int q, double *x, double *w) {
+  double P[256];
+  for (int i = 0; i < q; ++i) {
+    double z = cos(PI_ * (i + 0.75) / (q + 0.5));
+    for (int it = 0; it < 100; ++it) {
+      legendre_P(q, z, P);
+      double dP = q * (z * P[q] - P[q - 1]) / (z * z - 1.0);
+      double dz = P[q] / dP;
+      z -= dz;
+      if (fabs(dz) < 1e-16) break;
+    }
+    legendre_P(q, z, P);
+    double dP = q * (z * P[q] - P[q - 1]) / (z * z - 1.0);
+    x[q - 1 - i] = z;
+    w[q - 1 - i] = 2.0 / ((1.0 - z * z) * dP * dP);
+  }
+}
+
+/* N = binom(M+p, p). */
+int orc_num_basis(int p, int M) {
+  double r = 1.0;
+  for (int k = 1; k <= p; ++k) r = r * (M + k) / k;
+  return (int)(r + 0.5);
+}
+
+/* All multi-indices |i| <= M, graded by |i|, then lexicographically descending within a degree
+ * (reading: SURVEY §8c step 1; e.g. p=2, degree 2 -> (2,0),(1,1),(0,2)). */
+static void gen_degree(int p, int pos, int rem, int32_t *cur, int32_t *idx, int *n) {
+  if (pos == p - 1) {
+    cur[pos] = rem;
+    for (int k = 0; k < p; ++k) idx[*n * p + k] = cur[k];
+    ++*n;
+    return;
+  }
+  for (int v = rem; v >= 0; --v) {
+    cur[pos] = v;
+    gen_degree(p, pos + 1, rem - v, cur, idx, n);
+  }
+}
+
+void orc_multi_indices(int p, int M, int32_t *idx) {
+  int n = 0;
+  int32_t cur[8];
+  for (int deg = 0; deg <= M; ++deg) gen_degree(p, 0, deg, cur, idx, &n);
+}
+
+/* ------------------------------------------------------------------------ */
+/* Closures: u_s = (grad s)^{-1}, its Jacobian, s_* */
+/* ------------------------------------------------------------------------ */
+
+/* BASELINE scaling U = -rho S/(gamma-1), S = ln p - gamma ln rho (reading 11):
+ *   ln rho = v1 - |v_m|^2/(2 v_E) - (gamma + ln(-v_E))/(gamma-1), p = rho/(-v_E), w = -v_m/v_E. */
+static int euler_u(double gamma, int d, const double *v, double *u) {
+  int m = d + 2;
+  double vE = v[m - 1];
+  if (!(vE < 0.0)) return 0;
+  double vm2 = 0.0;
+  for (int k = 0; k < d; ++k) vm2 += v[1 + k] * v[1 + k];
+  double lnrho = v[0] - vm2 / (2.0 * vE) - (gamma + log(-vE)) / (gamma - 1.0);
+  double rho = exp(lnrho);
+  double p = rho / (-vE);
+  double w2 = 0.0;
+  u[0] = rho;
+  for (int k = 0; k < d; ++k) {
+    double wk = -v[1 + k] / vE;
+    u[1 + k] = rho * wk;
+    w2 += wk * wk;
+  }
+  u[m - 1] = p / (gamma - 1.0) + 0.5 * rho * w2;
+  for (int k = 0; k < m; ++k)
+    if (!isfinite(u[k])) return 0;
+  return rho > 0.0;
+}
+
+/* du/dv = A0 (symmetric), H = (E+p)/rho, c^2 = gamma p / rho. */
+static int euler_du(double gamma, int d, const double *v, double *J) {
+  int m = d + 2;
+  double u[4];
+  if (!euler_u(gamma, d, v, u)) return 0;
+  double rho = u[0], E = u[m - 1];
+  double mm2 = 0.0;
+  for (int k = 0; k < d; ++k) mm2 += u[1 + k] * u[1 + k];
+  double p = (gamma - 1.0) * (E - 0.5 * mm2 / rho);
+  double H = (E + p) / rho;
+  double c2 = gamma * p / rho;
+  J[0 * m + 0] = rho;
+  for (int k = 0; k < d; ++k) {
+    J[0 * m + 1 + k] = u[1 + k];
+    J[(1 + k) * m + 0] = u[1 + k];
+    for (int l = 0; l < d; ++l) J[(1 + k) * m + 1 + l] = u[1 + k] * u[1 + l] / rho + (k == l ? p : 0.0);
+    J[(1 + k) * m + m - 1] = u[1 + k] * H;
+    J[(m - 1) * m + 1 + k] = u[1 + k] * H;
+  }
+  J[0 * m + m - 1] = E;
+  J[(m - 1) * m + 0] = E;
+  J[(m - 1) * m + m - 1] = rho * H * H - c2 * p / (gamma - 1.0);
+  return 1;
+}
+
+/* forward map v = grad U(u) (BASELINE scaling). */
+static int euler_grad(double gamma, int d, const double *u, double *v) {
+  int m = d + 2;
+  double rho = u[0];
+  double mm2 = 0.0;
+  for (int k = 0; k < d; ++k) mm2 += u[1 + k] * u[1 + k];
+  double p = (gamma - 1.0) * (u[m - 1] - 0.5 * mm2 / rho);
+  if (!(rho > 0.0) || !(p > 0.0)) return 0;
+  double S = log(p) - gamma * log(rho);
+  double w2 = mm2 / (rho * rho);
+  v[0] = (gamma - S) / (gamma - 1.0) - rho * w2 / (2.0 * p);
+  for (int k = 0; k < d; ++k) v[1 + k] = rho * (u[1 + k] / rho) / p;
+  v[m - 1] = -rho / p;
+  return 1;
+}
+
+/* App. B, paper scaling s = -rho ln(rho^{-gamma}(E - |m|^2/(2 rho))),
+ * with dS/dE corrected to -rho/(E - |m|^2/(2 rho)) (reading 9). */
+void orc_euler_paper_grad_s(double gamma, int d, const double *u, double *Lam) {
+  int m = d + 2;
+  double rho = u[0], E = u[m - 1];
+  double mm2 = 0.0;
+  for (int k = 0; k < d; ++k) mm2 += u[1 + k] * u[1 + k];
+  double eps = E - mm2 / (2.0 * rho);
+  Lam[0] = -log(pow(rho, -gamma) * eps) + mm2 / (-2.0 * rho * E + mm2) + gamma;
+  for (int k = 0; k < d; ++k) Lam[1 + k] = -2.0 * rho * u[1 + k] / (-2.0 * rho * E + mm2);
+  Lam[m - 1] = -rho / eps;
+}
+
+/* App. B alpha(Lambda) with the gamma-term sign corrected to +2 Lambda_4 gamma
+ * (reading 10). */
+int orc_euler_paper_u(double gamma, int d, const double *L, double *u) {
+  int m = d + 2;
+  double L4 = L[m - 1];
+  if (!(L4 < 0.0)) return 0;
+  double Lm2 = 0.0;
+  for (int k = 0; k < d; ++k) Lm2 += L[1 + k] * L[1 + k];
+  double alpha = exp((Lm2 - 2.0 * L[0] * L4 + 2.0 * L4 * gamma) / (2.0 * L4 * (1.0 - gamma))) *
+                 pow(-L4, 1.0 / (1.0 - gamma));
+  u[0] = alpha;
+  for (int k = 0; k < d; ++k) u[1 + k] = -L[1 + k] * alpha / L4;
+  u[m - 1] = -alpha * (-Lm2 + 2.0 * L4) / (2.0 * L4 * L4);
+  return isfinite(alpha) && alpha > 0.0;
+}
+
+static double sigmoid(double L) {
+  if (L >= 0.0) return 1.0 / (1.0 + exp(-L));
+  double e = exp(L);
+  return e / (1.0 + e);
+}
+
+int orc_closure_u(const orc_ctx *c, const double *L, double *u) {
+  const orc_problem *P = &c->P;
+  switch (P->closure) {
+    case ORC_CL_QUADRATIC: /* s = u^2/2: u_s(Lambda) = Lambda */
+      for (int a = 0; a < c->m; ++a) u[a] = L[a];
+      return 1;
+    case ORC_CL_BARRIER: /* u_s = u- + (u+ - u-) sigma(Lambda) (BASELINE cfg 1) */
+      u[0] = P->umin + (P->umax - P->umin) * sigmoid(L[0]);
+      return isfinite(u[0]);
+    default:
+      return euler_u(P->gamma, c->m - 2, L, u);
+  }
+}
+
+int orc_closure_du(const orc_ctx *c, const double *L, double *J) {
+  const orc_problem *P = &c->P;
+  switch (P->closure) {
+    case ORC_CL_QUADRATIC:
+      for (int a = 0; a < c->m; ++a)
+        for (int b = 0; b < c->m; ++b) J[a * c->m + b] = (a == b) ? 1.0 : 0.0;
+      return 1;
+    case ORC_CL_BARRIER: {
+      double s = sigmoid(L[0]);
+      J[0] = (P->umax - P->umin) * s * (1.0 - s);
+      return 1;
+    }
+    default:
+      return euler_du(P->gamma, c->m - 2, L, J);
+  }
+}
+
+/* Legendre transform s_* (only used by the dual objective L). */
+double orc_closure_sstar(const orc_ctx *c, const double *L) {
+  const orc_problem *P = &c->P;
+  switch (P->closure) {
+    case ORC_CL_QUADRATIC: {
+      double s = 0.0;
+      for (int a = 0; a < c->m; ++a) s += 0.5 * L[a] * L[a];
+      return s;
+    }
+    case ORC_CL_BARRIER: {
+      double D = P->umax - P->umin;
+      double softplus = (L[0] > 0.0 ? L[0] : 0.0) + log1p(exp(-fabs(L[0])));
+      return P->umin * L[0] + D * softplus - D * log(D);
+    }
+    default: {
+      double u[4];
+      if (!euler_u(P->gamma, c->m - 2, L, u)) return NAN;
+      return u[0]; /* U_*(v) = rho(v) */
+    }
+  }
+}
+
+int orc_closure_grad_s(const orc_ctx *c, const double *u, double *L) {
+  const orc_problem *P = &c->P;
+  switch (P->closure) {
+    case ORC_CL_QUADRATIC:
+      for (int a = 0; a < c->m; ++a) L[a] = u[a];
+      return 1;
+    case ORC_CL_BARRIER: /* s'(u) = ln((u-u-)/(u+-u)) */
+      if (!(u[0] > P->umin && u[0] < P->umax)) return 0;
+      L[0] = log((u[0] - P->umin) / (P->umax - u[0]));
+      return 1;
+    default:
+      return euler_grad(P->gamma, c->m - 2, u, L);
+  }
+}
+
+/* ------------------------------------------------------------------------ */
+/* Physics: physical flux, wave speed, two-point numerical fluxes g           */
+/* ------------------------------------------------------------------------ */
+
+/* Euler physical flux along unit normal n: (rho v_n, m v_n + p n, (E+p) v_n). */
+static void euler_flux_n(double gamma, int d, const double *u, const double *n, double *f,
+                         double *vn_out, double *c_out) {
+  int m = d + 2;
+  double rho = u[0], E = u[m - 1];
+  double mm2 = 0.0, vn = 0.0;
+  for (int k = 0; k < d; ++k) {
+    mm2 += u[1 + k] * u[1 + k];
+    vn += u[1 + k] / rho * n[k];
+  }
+  double p = (gamma - 1.0) * (E - 0.5 * mm2 / rho);
+  f[0] = rho * vn;
+  for (int k = 0; k < d; ++k) f[1 + k] = u[1 + k] * vn + p * n[k];
+  f[m - 1] = (E + p) * vn;
+  if (vn_out) *vn_out = vn;
+  if (c_out) *c_out = sqrt(gamma * p / rho);
+}
+
+/* g(u_l, u_r; n) at one node.  cfg 1: global LF g = (u_l^2+u_r^2)/4 - dx/(2dt) (u_r-u_l)
+ * (PAPER.md:870); HLL with Davis speeds (reading 14); Rusanov (reading 14). */
+void orc_flux_g(const orc_ctx *c, const double *ul, const double *ur, const double *n,
+                double dx_over_dt, double *g) {
+  const orc_problem *P = &c->P;
+  int m = c->m;
+  if (P->flux == ORC_FLUX_LF_GLOBAL) {
+    /* scalar Burgers, 1D, n = +1 */
+    g[0] = 0.25 * (ul[0] * ul[0] + ur[0] * ur[0]) - 0.5 * dx_over_dt * (ur[0] - ul[0]);
+    return;
+  }
+  int d = m - 2;
+  double fl[4], fr[4], vl, vr, cl, cr;
+  euler_flux_n(P->gamma, d, ul, n, fl, &vl, &cl);
+  euler_flux_n(P->gamma, d, ur, n, fr, &vr, &cr);
+  if (P->flux == ORC_FLUX_HLL) {
+    double SL = fmin(vl - cl, vr - cr);
+    double SR = fmax(vl + cl, vr + cr);
+    for (int a = 0; a < m; ++a) {
+      if (SL >= 0.0)
+        g[a] = fl[a];
+      else if (SR <= 0.0)
+        g[a] = fr[a];
+      else
+        g[a] = (SR * fl[a] - SL * fr[a] + SL * SR * (ur[a] - ul[a])) / (SR - SL);
+    }
+    return;
+  }
+  double al = fabs(vl) + cl, ar = fabs(vr) + cr;
+  double amax = al > ar ? al : ar;
+  for (int a = 0; a < m; ++a) g[a] = 0.5 * (fl[a] + fr[a]) - 0.5 * amax * (ur[a] - ul[a]);
+}
+
+/* wave speed s = |f'(u)| along one direction (Burgers |u|; Euler |v_n|+c) */
+static double wave_speed(const orc_ctx *c, const double *u, const double *n) {
+  if (c->P.closure != ORC_CL_EULER && c->m == 1) return fabs(u[0]);
+  int d = c->m - 2;
+  double f[4], vn, cs;
+  euler_flux_n(c->P.gamma, d, u, n, f, &vn, &cs);
+  return fabs(vn) + cs;
+}
+
+static double speed_norm(const orc_ctx *c, const double *u) {
+  if (c->m == 1) return fabs(u[0]);
+  int d = c->m - 2;
+  double v2 = 0.0;
+  for (int k = 0; k < d; ++k) v2 += (u[1 + k] / u[0]) * (u[1 + k] / u[0]);
+  double n0[2] = {1.0, 0.0}, f[4], vn, cs;
+  euler_flux_n(c->P.gamma, d, u, n0, f, &vn, &cs);
+  return sqrt(v2) + cs;
+}
+
+/* primitive -> conserved */
+static void prim_to_cons(const orc_ctx *c, const double *q, double *u) {
+  if (c->m == 1) {
+    u[0] = q[0];
+    return;
+  }
+  int d = c->m - 2;
+  double rho = q[0], p = q[d + 1], v2 = 0.0;
+  u[0] = rho;
+  for (int k = 0; k < d; ++k) {
+    u[1 + k] = rho * q[1 + k];
+    v2 += q[1 + k] * q[1 + k];
+  }
+  u[d + 1] = p / (c->P.gamma - 1.0) + 0.5 * rho * v2;
+}
+
+/* conserved state of a state spec at node xi */
+static void spec_state(const orc_ctx *c, const orc_state_spec *s, const double *xi, double *u) {
+  int p = c->P.p;
+  double q[5] = {0, 0, 0, 0, 0};
+  if (s->kind == ORC_SPEC_FREESTREAM) {
+    double rho = s->q0[0], pr = s->q0[1];
+    double Ma = s->q0[2] + s->q0[3] * xi[s->dim_a];
+    double th = (s->q0[4] + s->q0[5] * xi[s->dim_b]) * PI_ / 180.0;
+    double cs = sqrt(c->P.gamma * pr / rho);
+    q[0] = rho;
+    q[1] = Ma * cs * cos(th);
+    q[2] = Ma * cs * sin(th);
+    q[3] = pr;
+  } else {
+    int nq = (c->m == 1) ? 1 : c->m;
+    for (int k = 0; k < nq; ++k) {
+      q[k] = s->q0[k];
+      for (int dd = 0; dd < p && dd < 3; ++dd) q[k] += s->q1[k][dd] * xi[dd];
+    }
+  }
+  prim_to_cons(c, q, u);
+}
+
+/* ghost state at node k for boundary tag t (reading 16) */
+static void ghost_state(const orc_ctx *c, int tag, int k, const double *uin, const double *n,
+                        double *ug) {
+  int m = c->m;
+  int kind = c->P.bc_kind[tag];
+  if (kind == ORC_BC_STATE) {
+    memcpy(ug, c->bc_u + ((size_t)tag * c->Q + k) * m, sizeof(double) * m);
+  } else if (kind == ORC_BC_SLIP) {
+    int d = m - 2;
+    double mn = 0.0;
+    for (int q = 0; q < d; ++q) mn += uin[1 + q] * n[q];
+    ug[0] = uin[0];
+    for (int q = 0; q < d; ++q) ug[1 + q] = uin[1 + q] - 2.0 * mn * n[q];
+    ug[m - 1] = uin[m - 1];
+  } else {
+    memcpy(ug, uin, sizeof(double) * m);
+  }
+}
+
+/* ------------------------------------------------------------------------ */
+/* Context: basis, quadrature, mesh geometry                                  */
+/* ------------------------------------------------------------------------ */
+
+typedef struct {
+  int64_t key;
+  int32_t t, e;
+} edge_t;
+
+static int edge_cmp(const void *x, const void *y) {
+  const edge_t *a = (const edge_t *)x, *b = (const edge_t *)y;
+  if (a->key != b->key) return a->key < b->key ? -1 : 1;
+  return (a->t * 3 + a->e) - (b->t * 3 + b->e);
+}
+
+static void build_geometry(orc_ctx *c) {
+  const orc_problem *P = &c->P;
+  int F = c->F, n = c->cells;
+  c->nbr = (int32_t *)malloc(sizeof(int32_t) * n * F);
+  c->nrm = (double *)calloc((size_t)n * F * 2, sizeof(double));
+  c->coef = (double *)malloc(sizeof(double) * n * F);
+  c->area = (double *)malloc(sizeof(double) * n);
+  c->perim = (double *)malloc(sizeof(double) * n);
+  c->xc = (double *)calloc((size_t)n * 2, sizeof(double));
+  if (P->mesh_kind == ORC_MESH_1D) {
+    double dx = (P->x1 - P->x0) / P->nx;
+    for (int j = 0; j < n; ++j) {
+      c->nbr[j * 2 + 0] = (j > 0) ? j - 1 : (P->periodic ? n - 1 : -1 - 0);
+      c->nbr[j * 2 + 1] = (j < n - 1) ? j + 1 : (P->periodic ? 0 : -1 - 1);
+      c->nrm[(j * 2 + 0) * 2] = -1.0;
+      c->nrm[(j * 2 + 1) * 2] = 1.0;
+      c->coef[j * 2 + 0] = c->coef[j * 2 + 1] = 1.0 / dx;
+      c->area[j] = dx;
+      c->perim[j] = 2.0;
+      c->xc[j * 2] = P->x0 + (j + 0.5) * dx;
+    }
+  } else if (P->mesh_kind == ORC_MESH_CART2D) {
+    double dx = (P->x1 - P->x0) / P->nx, dy = (P->y1 - P->y0) / P->ny;
+    for (int iy = 0; iy < P->ny; ++iy)
+      for (int ix = 0; ix < P->nx; ++ix) {
+        int j = iy * P->nx + ix;
+        int nx = P->nx, ny = P->ny;
+        c->nbr[j * 4 + 0] = ix > 0 ? j - 1 : (P->periodic ? iy * nx + nx - 1 : -1 - 0);
+        c->nbr[j * 4 + 1] = ix < nx - 1 ? j + 1 : (P->periodic ? iy * nx : -1 - 1);
+        c->nbr[j * 4 + 2] = iy > 0 ? j - nx : (P->periodic ? (ny - 1) * nx + ix : -1 - 2);
+        c->nbr[j * 4 + 3] = iy < ny - 1 ? j + nx : (P->periodic ? ix : -1 - 3);
+        double nn[4][2] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}};
+        for (int f = 0; f < 4; ++f) {
+          c->nrm[(j * 4 + f) * 2 + 0] = nn[f][0];
+          c->nrm[(j * 4 + f) * 2 + 1] = nn[f][1];
+        }
+        c->coef[j * 4 + 0] = c->coef[j * 4 + 1] = 1.0 / dx;
+        c->coef[j * 4 + 2] = c->coef[j * 4 + 3] = 1.0 / dy;
+        c->area[j] = dx * dy;
+        c->perim[j] = 2.0 * (dx + dy);
+        c->xc[j * 2] = P->x0 + (ix + 0.5) * dx;
+        c->xc[j * 2 + 1] = P->y0 + (iy + 0.5) * dy;
+      }
+  } else {
+    /* triangles: neighbour across edge e = (v_e, v_{e+1}) found by brute-force edge matching
+     * (sorted edge keys); outward normal of a counter-clockwise triangle is (dy, -dx)/|e|. */
+    int T = P->n_tri;
+    edge_t *E = (edge_t *)malloc(sizeof(edge_t) * 3 * T);
+    for (int t = 0; t < T; ++t)
+      for (int e = 0; e < 3; ++e) {
+        int a = P->tri[t * 3 + e], b = P->tri[t * 3 + (e + 1) % 3];
+        int lo = a < b ? a : b, hi = a < b ? b : a;
+        E[t * 3 + e].key = (int64_t)lo * P->n_vert + hi;
+        E[t * 3 + e].t = t;
+        E[t * 3 + e].e = e;
+      }
+    qsort(E, 3 * T, sizeof(edge_t), edge_cmp);
+    for (int t = 0; t < T; ++t)
+      for (int e = 0; e < 3; ++e) c->nbr[t * 3 + e] = -1 - (P->tri_tag[t * 3 + e] < 0 ? 0 : P->tri_tag[t * 3 + e]);
+    for (int i = 0; i + 1 < 3 * T; ++i)
+      if (E[i].key == E[i + 1].key) {
+        c->nbr[E[i].t * 3 + E[i].e] = E[i + 1].t;
+        c->nbr[E[i + 1].t * 3 + E[i + 1].e] = E[i].t;
+      }
+    free(E);
+    for (int t = 0; t < T; ++t) {
+      const double *A = P->vert + 2 * P->tri[t * 3 + 0];
+      const double *B = P->vert + 2 * P->tri[t * 3 + 1];
+      const double *C = P->vert + 2 * P->tri[t * 3 + 2];
+      double ar = 0.5 * ((B[0] - A[0]) * (C[1] - A[1]) - (C[0] - A[0]) * (B[1] - A[1]));
+      c->area[t] = ar;
+      c->perim[t] = 0.0;
+      c->xc[t * 2] = (A[0] + B[0] + C[0]) / 3.0;
+      c->xc[t * 2 + 1] = (A[1] + B[1] + C[1]) / 3.0;
+      for (int e = 0; e < 3; ++e) {
+        const double *V0 = P->vert + 2 * P->tri[t * 3 + e];
+        const double *V1 = P->vert + 2 * P->tri[t * 3 + (e + 1) % 3];
+        double dx = V1[0] - V0[0], dy = V1[1] - V0[1];
+        double len = sqrt(dx * dx + dy * dy);
+        c->nrm[(t * 3 + e) * 2 + 0] = dy / len;
+        c->nrm[(t * 3 + e) * 2 + 1] = -dx / len;
+        c->coef[t * 3 + e] = len / ar;
+        c->perim[t] += len;
+      }
+    }
+  }
+}
+
+orc_ctx *orc_create(const orc_problem *P) {
+  orc_ctx *c = (orc_ctx *)calloc(1, sizeof(orc_ctx));
+  c->P = *P;
+  int p = P->p;
+  c->N = orc_num_basis(p, P->M);
+  c->Q = 1;
+  for (int d = 0; d < p; ++d) c->Q *= P->q1d;
+  c->m = P->m;
+  c->d = (P->mesh_kind == ORC_MESH_1D) ? 1 : 2;
+  c->F = (P->mesh_kind == ORC_MESH_1D) ? 2 : (P->mesh_kind == ORC_MESH_CART2D ? 4 : 3);
+  c->cells = (P->mesh_kind == ORC_MESH_1D) ? P->nx : (P->mesh_kind == ORC_MESH_CART2D ? P->nx * P->ny : P->n_tri);
+  int N = c->N, Q = c->Q;
+  c->idx = (int32_t *)malloc(sizeof(int32_t) * N * p);
+  orc_multi_indices(p, P->M, c->idx);
+  /* tensor Gauss-Legendre rule, last dimension fastest; omega_k = prod w_{k_d} / 2 (f_Xi = 2^-p) */
+  double x1[128], w1[128];
+  orc_gauss_legendre(P->q1d, x1, w1);
+  c->xi = (double *)malloc(sizeof(double) * Q * p);
+  c->omega = (double *)malloc(sizeof(double) * Q);
+  c->Phi = (double *)malloc(sizeof(double) * Q * N);
+  for (int k = 0; k < Q; ++k) {
+    int r = k;
+    double om = 1.0;
+    for (int d = p - 1; d >= 0; --d) {
+      int kd = r % P->q1d;
+      r /= P->q1d;
+      c->xi[k * p + d] = x1[kd];
+      om *= w1[kd] / 2.0;
+    }
+    c->omega[k] = om;
+    for (int i = 0; i < N; ++i) {
+      double v = 1.0;
+      for (int d = 0; d < p; ++d) v *= phi_1d(c->idx[i * p + d], c->xi[k * p + d]);
+      c->Phi[k * N + i] = v;
+    }
+  }
+  build_geometry(c);
+  c->bc_u = (double *)calloc((size_t)4 * Q * c->m, sizeof(double));
+  for (int t = 0; t < 4; ++t)
+    if (P->bc_kind[t] == ORC_BC_STATE)
+      for (int k = 0; k < Q; ++k) spec_state(c, &P->bc_state[t], c->xi + k * p, c->bc_u + ((size_t)t * Q + k) * c->m);
+  c->level = (int32_t *)calloc(c->cells, sizeof(int32_t));
+  c->n_levels = P->n_levels;
+  if (c->n_levels > 0) {
+    for (int l = 0; l < c->n_levels; ++l) c->Nl[l] = orc_num_basis(p, P->level_M[l]);
+  } else {
+    c->Nl[0] = N;
+  }
+#ifdef _OPENMP
+  if (P->n_threads > 0) omp_set_num_threads(P->n_threads);
+#endif
+  return c;
+}
+
+void orc_destroy(orc_ctx *c) {
+  if (!c) return;
+  free(c->idx); free(c->xi); free(c->omega); free(c->Phi);
+  free(c->nbr); free(c->nrm); free(c->coef); free(c->area); free(c->perim); free(c->xc);
+  free(c->bc_u); free(c->level);
+  free(c);
+}
+
+int orc_N(const orc_ctx *c) { return c->N; }
+int orc_Q(const orc_ctx *c) { return c->Q; }
+int orc_cells(const orc_ctx *c) { return c->cells; }
+
+void orc_get_quadrature(const orc_ctx *c, double *xi, double *omega, double *Phi) {
+  if (xi) memcpy(xi, c->xi, sizeof(double) * c->Q * c->P.p);
+  if (omega) memcpy(omega, c->omega, sizeof(double) * c->Q);
+  if (Phi) memcpy(Phi, c->Phi, sizeof(double) * c->Q * c->N);
+}
+
+void orc_get_geometry(const orc_ctx *c, int32_t *nbr, double *nrm, double *coef, double *area) {
+  int n = c->cells, F = c->F;
+  if (nbr) memcpy(nbr, c->nbr, sizeof(int32_t) * n * F);
+  if (nrm) memcpy(nrm, c->nrm, sizeof(double) * n * F * 2);
+  if (coef) memcpy(coef, c->coef, sizeof(double) * n * F);
+  if (area) memcpy(area, c->area, sizeof(double) * n);
+}
+
+static int cell_N(const orc_ctx *c, int j) { return c->n_levels > 0 ? c->Nl[c->level[j]] : c->N; }
+
+/* ------------------------------------------------------------------------ */
+/* Dual problem                                           */
+/* ------------------------------------------------------------------------ */
+
+/* Lambda_k = sum_i lambda_i phi_i(xi_k)  (lambda^T phi at node k) */
+static void reconstruct(const orc_ctx *c, int Nl, const double *lam, int k, double *Lk) {
+  int m = c->m, N = c->N;
+  for (int a = 0; a < m; ++a) {
+    double s = 0.0;
+    for (int i = 0; i < Nl; ++i) s += lam[i * m + a] * c->Phi[k * N + i];
+    Lk[a] = s;
+  }
+}
+
+/* L(lambda; uhat) = <s_*(lambda^T phi)>_Q - sum_i lambda_i^T uhat_i */
+int orc_dual_objective(const orc_ctx *c, int Nl, const double *lam, const double *uhat, double *L) {
+  int m = c->m;
+  double Lk[4], s = 0.0;
+  for (int k = 0; k < c->Q; ++k) {
+    reconstruct(c, Nl, lam, k, Lk);
+    s += c->omega[k] * orc_closure_sstar(c, Lk);
+  }
+  for (int i = 0; i < Nl; ++i)
+    for (int a = 0; a < m; ++a) s -= lam[i * m + a] * uhat[i * m + a];
+  *L = s;
+  return isfinite(s);
+}
+
+/* grad L = <u_s(lambda^T phi) phi^T>_Q^T - uhat */
+int orc_dual_gradient(const orc_ctx *c, int Nl, const double *lam, const double *uhat, double *g) {
+  int m = c->m, N = c->N;
+  double Lk[4], uk[4];
+  for (int i = 0; i < Nl; ++i)
+    for (int a = 0; a < m; ++a) g[i * m + a] = 0.0;
+  for (int k = 0; k < c->Q; ++k) {
+    reconstruct(c, Nl, lam, k, Lk);
+    if (!orc_closure_u(c, Lk, uk)) return 0;
+    for (int i = 0; i < Nl; ++i)
+      for (int a = 0; a < m; ++a) g[i * m + a] += c->omega[k] * uk[a] * c->Phi[k * N + i];
+  }
+  int ok = 1;
+  for (int i = 0; i < Nl; ++i)
+    for (int a = 0; a < m; ++a) {
+      g[i * m + a] -= uhat[i * m + a];
+      if (!isfinite(g[i * m + a])) ok = 0;
+    }
+  return ok;
+}
+
+/* h(lambda) = <u_s(lambda^T phi) phi^T>_Q^T */
+int orc_moments_from_dual(const orc_ctx *c, int Nl, const double *lam, double *uhat) {
+  int n = Nl * c->m;
+  double *zero = (double *)calloc(n, sizeof(double));
+  int ok = orc_dual_gradient(c, Nl, lam, zero, uhat);
+  free(zero);
+  return ok;
+}
+
+/* H = <grad u_s(lambda^T phi) (x) phi phi^T>_Q^T, full n x n, vec index (i,a) -> i*m+a */
+int orc_dual_hessian(const orc_ctx *c, int Nl, const double *lam, double *H) {
+  int m = c->m, N = c->N, n = Nl * m;
+  double Lk[4], J[16];
+  for (int r = 0; r < n * n; ++r) H[r] = 0.0;
+  for (int k = 0; k < c->Q; ++k) {
+    reconstruct(c, Nl, lam, k, Lk);
+    if (!orc_closure_du(c, Lk, J)) return 0;
+    for (int i = 0; i < Nl; ++i)
+      for (int a = 0; a < m; ++a)
+        for (int j = 0; j < Nl; ++j)
+          for (int b = 0; b < m; ++b)
+            H[(i * m + a) * n + (j * m + b)] += c->omega[k] * J[a * m + b] * c->Phi[k * N + i] * c->Phi[k * N + j];
+  }
+  return 1;
+}
+
+/* stopping quantity sum_a ||g_{.,a}||_2 (reading 1) */
+static double crit_of(const double *g, int Nl, int m) {
+  double s = 0.0;
+  for (int a = 0; a < m; ++a) {
+    double q = 0.0;
+    for (int i = 0; i < Nl; ++i) q += g[i * m + a] * g[i * m + a];
+    s += sqrt(q);
+  }
+  return s;
+}
+
+/* Textbook Cholesky H = L L^T, then L L^T d = -g */
+static int cholesky_solve(double *H, int n, const double *g, double *d) {
+  for (int j = 0; j < n; ++j) {
+    double s = H[j * n + j];
+    for (int k = 0; k < j; ++k) s -= H[j * n + k] * H[j * n + k];
+    if (!(s > 0.0) || !isfinite(s)) return 0;
+    double Ljj = sqrt(s);
+    H[j * n + j] = Ljj;
+    for (int i = j + 1; i < n; ++i) {
+      double t = H[i * n + j];
+      for (int k = 0; k < j; ++k) t -= H[i * n + k] * H[j * n + k];
+      H[i * n + j] = t / Ljj;
+    }
+  }
+  /* forward: L y = -g */
+  for (int i = 0; i < n; ++i) {
+    double t = -g[i];
+    for (int k = 0; k < i; ++k) t -= H[i * n + k] * d[k];
+    d[i] = t / H[i * n + i];
+  }
+  /* backward: L^T d = y */
+  for (int i = n - 1; i >= 0; --i) {
+    double t = d[i];
+    for (int k = i + 1; k < n; ++k) t -= H[k * n + i] * d[k];
+    d[i] = t / H[i * n + i];
+  }
+  return 1;
+}
+
+/* L together with the magnitude of the terms it sums (rounding scale of L):
+ *   scale = <|s_*(lambda^T phi)|>_Q + sum_i |lambda_i^T uhat_i|  */
+static int objective_and_scale(const orc_ctx *c, int Nl, const double *lam, const double *uhat,
+                               double *L, double *scale) {
+  int m = c->m;
+  double Lk[4], s = 0.0, sc = 0.0;
+  for (int k = 0; k < c->Q; ++k) {
+    reconstruct(c, Nl, lam, k, Lk);
+    double sk = orc_closure_sstar(c, Lk);
+    s += c->omega[k] * sk;
+    sc += c->omega[k] * fabs(sk);
+  }
+  for (int i = 0; i < Nl; ++i)
+    for (int a = 0; a < m; ++a) {
+      s -= lam[i * m + a] * uhat[i * m + a];
+      sc += fabs(lam[i * m + a] * uhat[i * m + a]);
+    }
+  *L = s;
+  *scale = sc;
+  return isfinite(s);
+}
+
+/* Newton iteration lambda^{(l+1)} = d(lambda^{(l)}; uhat) until the stopping
+ * criterion holds (FULL, Alg. 1 lines 7-10) or once (ONE_STEP, Alg. 2 line 5),
+ * globalised by Armijo backtracking on the dual objective L with a rounding
+ * allowance (reading 3'):  accept alpha if the trial is admissible and
+ *     L(lambda + alpha d) <= L(lambda) + c alpha grad L . d + 1e-12 scale(L). */
+int orc_dual_solve_cell(const orc_ctx *c, int Nl, int mode, const double *uhat, double *lam,
+                        int32_t *iters, double *crit_out) {
+  const orc_problem *P = &c->P;
+  int m = c->m, n = Nl * m;
+  double *g = (double *)malloc(sizeof(double) * n);
+  double *dd = (double *)malloc(sizeof(double) * n);
+  double *lt = (double *)malloc(sizeof(double) * n);
+  double *H = (double *)malloc(sizeof(double) * n * n);
+  int status = ORC_OK, l = 0;
+  double crit = INFINITY;
+  if (!orc_dual_gradient(c, Nl, lam, uhat, g)) {
+    status = ORC_INADMISSIBLE;
+    goto done;
+  }
+  for (;;) {
+    crit = crit_of(g, Nl, m);
+    if (crit < P->tau) break;
+    if (mode == ORC_NEWTON_ONE_STEP && l == 1) break;
+    if (l == P->max_newton) {
+      status = ORC_NONCONVERGENCE;
+      break;
+    }
+    if (!orc_dual_hessian(c, Nl, lam, H) || !cholesky_solve(H, n, g, dd)) {
+      status = ORC_ILLCONDITIONED;
+      break;
+    }
+    double L0, scale;
+    objective_and_scale(c, Nl, lam, uhat, &L0, &scale);
+    double slope = 0.0;
+    for (int r = 0; r < n; ++r) slope += g[r] * dd[r];
+    double alpha = 1.0;
+    int accepted = 0;
+    for (int h = 0; h <= P->max_halvings; ++h) {
+      for (int r = 0; r < n; ++r) lt[r] = lam[r] + alpha * dd[r];
+      double Lt, sct;
+      if (objective_and_scale(c, Nl, lt, uhat, &Lt, &sct) &&
+          Lt <= L0 + P->armijo_c * alpha * slope + 1e-12 * scale && orc_dual_gradient(c, Nl, lt, uhat, g)) {
+        accepted = 1;
+        break;
+      }
+      alpha *= 0.5;
+    }
+    if (!accepted) {
+      status = ORC_LINESEARCH;
+      break;
+    }
+    memcpy(lam, lt, sizeof(double) * n);
+    ++l;
+  }
+done:
+  if (iters) *iters = l;
+  if (crit_out) *crit_out = crit;
+  free(g); free(dd); free(lt); free(H);
+  return status;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Whole-field operations                                                     */
+/* ------------------------------------------------------------------------ */
+
+static double clamp01(double x) { return x < 0.0 ? 0.0 : (x > 1.0 ? 1.0 : x); }
+
+/* u_j^0 = (1/|Omega_j|) int <u_IC phi>_Q dx with exact cell averages of the piecewise-constant IC
+ * at every node (Alg. 1 line 2; reading 17). */
+void orc_project_ic(const orc_ctx *c, const orc_ic *ic, double *uhat) {
+  const orc_problem *P = &c->P;
+  int N = c->N, Q = c->Q, m = c->m, p = P->p;
+#pragma omp parallel for schedule(static)
+  for (int j = 0; j < c->cells; ++j) {
+    int Nl = cell_N(c, j);
+    double *uj = uhat + (size_t)j * N * m;
+    for (int r = 0; r < N * m; ++r) uj[r] = 0.0;
+    for (int k = 0; k < Q; ++k) {
+      const double *xi = c->xi + k * p;
+      double ub[4] = {0, 0, 0, 0}, us[4][4];
+      if (ic->kind == ORC_IC_UNIFORM) {
+        spec_state(c, &ic->state[0], xi, ub);
+      } else {
+        double xs = ic->xs0, ys = ic->ys0;
+        for (int d = 0; d < p && d < 3; ++d) {
+          xs += ic->xs1[d] * xi[d];
+          ys += ic->ys1[d] * xi[d];
+        }
+        int nreg = ic->kind == ORC_IC_STEP1D ? 2 : 4;
+        for (int r = 0; r < nreg; ++r) spec_state(c, &ic->state[r], xi, us[r]);
+        if (P->mesh_kind == ORC_MESH_1D) {
+          double dx = (P->x1 - P->x0) / P->nx;
+          double xl = P->x0 + j * dx;
+          double fl = clamp01((xs - xl) / dx); /* fraction of the cell left of x_s */
+          for (int a = 0; a < m; ++a) ub[a] = fl * us[0][a] + (1.0 - fl) * us[1][a];
+        } else {
+          int ix = j % P->nx, iy = j / P->nx;
+          double dx = (P->x1 - P->x0) / P->nx, dy = (P->y1 - P->y0) / P->ny;
+          double fx = clamp01((xs - (P->x0 + ix * dx)) / dx); /* fraction with x < x_s */
+          double fy = clamp01((ys - (P->y0 + iy * dy)) / dy); /* fraction with y < y_s */
+          for (int a = 0; a < m; ++a)
+            ub[a] = (1.0 - fx) * (1.0 - fy) * us[0][a] + fx * (1.0 - fy) * us[1][a] + fx * fy * us[2][a] +
+                    (1.0 - fx) * fy * us[3][a];
+        }
+      }
+      for (int i = 0; i < Nl; ++i)
+        for (int a = 0; a < m; ++a) uj[i * m + a] += c->omega[k] * ub[a] * c->Phi[k * N + i];
+    }
+  }
+}
+
+/* lambda^(0) at t=0: e_0 (x) grad s(uhat_0) (reading 6) */
+void orc_warm_start(const orc_ctx *c, const double *uhat, double *lam) {
+  int N = c->N, m = c->m;
+  for (int j = 0; j < c->cells; ++j) {
+    double *lj = lam + (size_t)j * N * m;
+    for (int r = 0; r < N * m; ++r) lj[r] = 0.0;
+    orc_closure_grad_s(c, uhat + (size_t)j * N * m, lj);
+  }
+}
+
+void orc_set_levels(orc_ctx *c, const int32_t *levels) { memcpy(c->level, levels, sizeof(int32_t) * c->cells); }
+void orc_get_levels(const orc_ctx *c, int32_t *levels) { memcpy(levels, c->level, sizeof(int32_t) * c->cells); }
+
+/* Alg. 1 lines 4-10 (FULL) / Alg. 2 line 5 (ONE_STEP) for every cell */
+void orc_dual_solve_all(const orc_ctx *c, const double *uhat, double *lam, int32_t *iters,
+                        int32_t *status, double *crit) {
+  int N = c->N, m = c->m;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int j = 0; j < c->cells; ++j) {
+    int32_t it = 0;
+    double cr = 0.0;
+    int st = orc_dual_solve_cell(c, cell_N(c, j), c->P.newton_mode, uhat + (size_t)j * N * m,
+                                 lam + (size_t)j * N * m, &it, &cr);
+    if (iters) iters[j] = it;
+    if (status) status[j] = st;
+    if (crit) crit[j] = cr;
+  }
+}
+
+/* node states u_k^{(j)} = u_s(lambda_j^T phi(xi_k)) for all cells */
+static int node_states(const orc_ctx *c, const double *lam, double *U) {
+  int N = c->N, m = c->m, Q = c->Q, bad = 0;
+#pragma omp parallel for schedule(static) reduction(+ : bad)
+  for (int j = 0; j < c->cells; ++j) {
+    double Lk[4];
+    for (int k = 0; k < Q; ++k) {
+      reconstruct(c, cell_N(c, j), lam + (size_t)j * N * m, k, Lk);
+      if (!orc_closure_u(c, Lk, U + ((size_t)j * Q + k) * m)) bad++;
+    }
+  }
+  return bad == 0;
+}
+
+/* CFL time step from the largest wave speed over all cells, nodes and ghost states (reading 15). */
+static double dt_from_states(const orc_ctx *c, const double *U, double t_remaining) {
+  const orc_problem *P = &c->P;
+  int Q = c->Q, m = c->m, F = c->F;
+  double rate = 0.0;
+  for (int j = 0; j < c->cells; ++j) {
+    for (int k = 0; k < Q; ++k) {
+      const double *u = U + ((size_t)j * Q + k) * m;
+      double r;
+      if (P->mesh_kind == ORC_MESH_1D) {
+        double n1[2] = {1.0, 0.0};
+        r = wave_speed(c, u, n1) * c->coef[j * 2];
+      } else if (P->mesh_kind == ORC_MESH_CART2D) {
+        double nx[2] = {1.0, 0.0}, ny[2] = {0.0, 1.0};
+        r = wave_speed(c, u, nx) * c->coef[j * 4 + 0] + wave_speed(c, u, ny) * c->coef[j * 4 + 2];
+      } else {
+        r = speed_norm(c, u) * c->perim[j] / c->area[j];
+      }
+      if (r > rate) rate = r;
+      /* ghost states of boundary faces of this cell */
+      for (int f = 0; f < F; ++f) {
+        int nb = c->nbr[j * F + f];
+        if (nb >= 0) continue;
+        double ug[4];
+        ghost_state(c, -1 - nb, k, u, c->nrm + (j * F + f) * 2, ug);
+        double rg;
+        if (P->mesh_kind == ORC_MESH_1D) {
+          double n1[2] = {1.0, 0.0};
+          rg = wave_speed(c, ug, n1) * c->coef[j * 2];
+        } else if (P->mesh_kind == ORC_MESH_CART2D) {
+          double nx[2] = {1.0, 0.0}, ny[2] = {0.0, 1.0};
+          rg = wave_speed(c, ug, nx) * c->coef[j * 4 + 0] + wave_speed(c, ug, ny) * c->coef[j * 4 + 2];
+        } else {
+          rg = speed_norm(c, ug) * c->perim[j] / c->area[j];
+        }
+        if (rg > rate) rate = rg;
+      }
+    }
+  }
+  double dt = P->cfl / rate;
+  return dt < t_remaining ? dt : t_remaining;
+}
+
+double orc_compute_dt(const orc_ctx *c, const double *lam, double t_remaining) {
+  double *U = (double *)malloc(sizeof(double) * (size_t)c->cells * c->Q * c->m);
+  double dt = node_states(c, lam, U) ? dt_from_states(c, U, t_remaining) : NAN;
+  free(U);
+  return dt;
+}
+
+/* Moment update:
+ *   r_{j,k} = 1D:   (g(u_j,u_{j+1}) - g(u_{j-1},u_j)) / dx                        (eq. IPMDiscretization)
+ *             cart: (G_{i+1/2}-G_{i-1/2})/dx + (H_{j+1/2}-H_{j-1/2})/dy           (dimension by dimension)
+ *             tri:  sum_e |e|/|Omega_j| g(u_j, u_nb; n_e)                          (edge sum)
+ *   CONSERVATIVE: uhat^{n+1} = uhat^n - dt <r phi^T>_Q^T                          (reading 13)
+ *   PAPER_C:      uhat^{n+1} = <(u^{(j)} - dt r) phi_{l^{n+1}}^T>_Q^T */
+static void flux_update_states(const orc_ctx *c, const double *U, const int32_t *new_level,
+                               const double *uhat_old, double *uhat_new, double dt) {
+  const orc_problem *P = &c->P;
+  int N = c->N, m = c->m, Q = c->Q, F = c->F;
+  double dx_over_dt = (P->mesh_kind == ORC_MESH_1D) ? ((P->x1 - P->x0) / P->nx) / dt : 0.0;
+#pragma omp parallel for schedule(static)
+  for (int j = 0; j < c->cells; ++j) {
+    int Nnew = c->n_levels > 0 ? c->Nl[new_level[j]] : N;
+    double *un = uhat_new + (size_t)j * N * m;
+    const double *uo = uhat_old + (size_t)j * N * m;
+    double acc[224 * 4];
+    for (int r = 0; r < N * m; ++r) acc[r] = 0.0;
+    for (int k = 0; k < Q; ++k) {
+      const double *uj = U + ((size_t)j * Q + k) * m;
+      double nb_u[4][4];
+      for (int f = 0; f < F; ++f) {
+        int nb = c->nbr[j * F + f];
+        if (nb >= 0)
+          memcpy(nb_u[f], U + ((size_t)nb * Q + k) * m, sizeof(double) * m);
+        else
+          ghost_state(c, -1 - nb, k, uj, c->nrm + (j * F + f) * 2, nb_u[f]);
+      }
+      double r[4] = {0, 0, 0, 0}, gp[4], gm[4];
+      if (P->mesh_kind == ORC_MESH_1D) {
+        double n1[2] = {1.0, 0.0};
+        orc_flux_g(c, uj, nb_u[1], n1, dx_over_dt, gp);    /* g_{j+1/2} = g(u_j, u_{j+1}) */
+        orc_flux_g(c, nb_u[0], uj, n1, dx_over_dt, gm);    /* g_{j-1/2} = g(u_{j-1}, u_j) */
+        for (int a = 0; a < m; ++a) r[a] = (gp[a] - gm[a]) * c->coef[j * 2];
+      } else if (P->mesh_kind == ORC_MESH_CART2D) {
+        double nx[2] = {1.0, 0.0}, ny[2] = {0.0, 1.0};
+        orc_flux_g(c, uj, nb_u[1], nx, 0.0, gp);
+        orc_flux_g(c, nb_u[0], uj, nx, 0.0, gm);
+        for (int a = 0; a < m; ++a) r[a] = (gp[a] - gm[a]) * c->coef[j * 4 + 0];
+        orc_flux_g(c, uj, nb_u[3], ny, 0.0, gp);
+        orc_flux_g(c, nb_u[2], uj, ny, 0.0, gm);
+        for (int a = 0; a < m; ++a) r[a] += (gp[a] - gm[a]) * c->coef[j * 4 + 2];
+      } else {
+        for (int f = 0; f < F; ++f) {
+          orc_flux_g(c, uj, nb_u[f], c->nrm + (j * F + f) * 2, 0.0, gp);
+          for (int a = 0; a < m; ++a) r[a] += c->coef[j * F + f] * gp[a];
+        }
+      }
+      for (int i = 0; i < Nnew; ++i)
+        for (int a = 0; a < m; ++a) {
+          if (P->update_form == ORC_UPDATE_PAPER_C)
+            acc[i * m + a] += c->omega[k] * (uj[a] - dt * r[a]) * c->Phi[k * N + i];
+          else
+            acc[i * m + a] += c->omega[k] * r[a] * c->Phi[k * N + i];
+        }
+    }
+    for (int i = 0; i < N; ++i)
+      for (int a = 0; a < m; ++a) {
+        double v;
+        if (i >= Nnew)
+          v = 0.0;
+        else if (P->update_form == ORC_UPDATE_PAPER_C)
+          v = acc[i * m + a];
+        else
+          v = uo[i * m + a] - dt * acc[i * m + a];
+        un[i * m + a] = v;
+      }
+  }
+}
+
+void orc_flux_update(orc_ctx *c, const double *lam, const double *uhat_old, double *uhat_new, double dt) {
+  double *U = (double *)malloc(sizeof(double) * (size_t)c->cells * c->Q * c->m);
+  node_states(c, lam, U);
+  flux_update_states(c, U, c->level, uhat_old, uhat_new, dt);
+  free(U);
+}
+
+/* smoothness indicator on the first state component (reading 19-20):
+ *   S = sum_{M_{l-1} < |i| <= M_l} h_{i,0}^2 / sum_{|i| <= M_l} h_{i,0}^2 */
+double orc_indicator(const orc_ctx *c, int lvl, const double *h) {
+  int m = c->m;
+  int Nl = c->Nl[lvl];
+  int Nprev = lvl > 0 ? c->Nl[lvl - 1] : orc_num_basis(c->P.p, c->P.level_M[0] - 1);
+  double num = 0.0, den = 0.0;
+  for (int i = 0; i < Nl; ++i) {
+    den += h[i * m] * h[i * m];
+    if (i >= Nprev) num += h[i * m] * h[i * m];
+  }
+  return den > 0.0 ? num / den : 0.0;
+}
+
+/* One step of Algorithm 1 (FULL) / 2 (ONE_STEP) / 3-4 structure (levels), PAPER.md:196-217,
+ * 252-269, 400-450 (without retardation). */
+int orc_step(orc_ctx *c, double *uhat, double *lam, double t_remaining, int32_t *iters,
+             int32_t *status, double *dt_used, double *residual) {
+  int N = c->N, m = c->m, Q = c->Q, cells = c->cells;
+  int32_t *st = (int32_t *)malloc(sizeof(int32_t) * cells);
+  int32_t *newlev = (int32_t *)malloc(sizeof(int32_t) * cells);
+  orc_dual_solve_all(c, uhat, lam, iters, st, NULL);
+  int worst = 0;
+  for (int j = 0; j < cells; ++j) {
+    if (st[j] > worst) worst = st[j];
+    if (status) status[j] = st[j];
+  }
+  /* refinement level l^{n+1} from h(lambda^{n+1}) at level l^n (Alg. 3 line 15) */
+  memcpy(newlev, c->level, sizeof(int32_t) * cells);
+  if (c->n_levels > 0) {
+#pragma omp parallel for schedule(static)
+    for (int j = 0; j < cells; ++j) {
+      int lvl = c->level[j];
+      double h[224 * 4];
+      orc_moments_from_dual(c, c->Nl[lvl], lam + (size_t)j * N * m, h);
+      double S = orc_indicator(c, lvl, h);
+      int nl = lvl;
+      if (S < c->P.delta_dec && lvl > 0) nl = lvl - 1;
+      else if (S > c->P.delta_inc && lvl < c->n_levels - 1) nl = lvl + 1;
+      newlev[j] = nl;
+    }
+  }
+  double *U = (double *)malloc(sizeof(double) * (size_t)cells * Q * m);
+  if (!node_states(c, lam, U)) {
+    if (worst < ORC_INADMISSIBLE) worst = ORC_INADMISSIBLE;
+  }
+  double dt = dt_from_states(c, U, t_remaining);
+  double *unew = (double *)malloc(sizeof(double) * (size_t)cells * N * m);
+  flux_update_states(c, U, newlev, uhat, unew, dt);
+  /* steady residual on the zeroth moment of the first state (reading 23) */
+  double res = 0.0;
+  for (int j = 0; j < cells; ++j) res += c->area[j] * fabs(unew[(size_t)j * N * m] - uhat[(size_t)j * N * m]);
+  memcpy(uhat, unew, sizeof(double) * (size_t)cells * N * m);
+  /* lambda zero-padded (refine) or truncated (coarsen) to the new level */
+  if (c->n_levels > 0) {
+    for (int j = 0; j < cells; ++j) {
+      int Nn = c->Nl[newlev[j]];
+      for (int r = Nn * m; r < N * m; ++r) lam[(size_t)j * N * m + r] = 0.0;
+    }
+    memcpy(c->level, newlev, sizeof(int32_t) * cells);
+  }
+  if (dt_used) *dt_used = dt;
+  if (residual) *residual = res;
+  free(U); free(unew); free(st); free(newlev);
+  return worst;
+}

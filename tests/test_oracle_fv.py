@@ -1,0 +1,351 @@
+"""Oracle pins: kinetic flux and finite-volume moment update (PAPER.md:116-146, 182-194, 228-270,
+366-425, 855-881) against closed forms, textbook solvers written here, and invariants."""
+import math
+
+import numpy as np
+import pytest
+
+from inputs import configs
+from inputs.generators import bump_channel_mesh
+
+G = 1.4
+
+
+def euler_flux(u, n):
+    # PAPER.md:471-489 projected on the unit normal n
+    d = len(u) - 2
+    rho, mom, E = u[0], np.asarray(u[1:1 + d]), u[1 + d]
+    v = mom / rho
+    p = (G - 1) * (E - 0.5 * rho * v @ v)
+    vn = v @ np.asarray(n[:d])
+    return np.concatenate([[rho * vn], mom * vn + p * np.asarray(n[:d]), [(E + p) * vn]])
+
+
+def rand_state(rng, d):
+    rho, v, p = rng.uniform(0.2, 1.5), rng.uniform(-1, 1, d), rng.uniform(0.1, 1.5)
+    return np.concatenate([[rho], rho * v, [p / (G - 1) + 0.5 * rho * v @ v]])
+
+
+# ------------------------------------------------------------------ fluxes
+@pytest.mark.parametrize("name,d", [("cfg2", 1), ("cfg3", 2)])
+def test_flux_consistency(oracle_mod, name, d):
+    o = oracle_mod.Oracle(configs.get(name, mesh=dict(nx=2, ny=2)))
+    rng = np.random.default_rng(0)
+    for _ in range(100):
+        u = rand_state(rng, d)
+        th = rng.uniform(0, 2 * np.pi)
+        n = np.array([np.cos(th), np.sin(th)]) if d == 2 else np.array([1.0, 0.0])
+        np.testing.assert_allclose(o.flux_g(u, u, n), euler_flux(u, n), rtol=1e-13, atol=1e-13)
+
+
+def test_burgers_global_lf_is_printed_formula(oracle_mod):
+    o = oracle_mod.Oracle(configs.get("cfg1", mesh=dict(nx=2)))
+    # g(1,-1) with dx/dt = 1 -> (1+1)/4 - 1/2 (-2) = 1.5 ; consistency g(u,u) = u^2/2
+    assert o.flux_g(np.array([1.0]), np.array([-1.0]), dx_over_dt=1.0)[0] == 1.5
+    assert o.flux_g(np.array([3.0]), np.array([3.0]), dx_over_dt=7.0)[0] == 4.5
+
+
+def test_rusanov_rotational_invariance(oracle_mod):
+    o = oracle_mod.Oracle(configs.get("cfg3", mesh=dict(nx=2, ny=2)))
+    rng = np.random.default_rng(1)
+    for _ in range(50):
+        ul, ur = rand_state(rng, 2), rand_state(rng, 2)
+        th = rng.uniform(0, 2 * np.pi)
+        c, s = np.cos(th), np.sin(th)
+        R = np.array([[1, 0, 0, 0], [0, c, s, 0], [0, -s, c, 0], [0, 0, 0, 1.0]])
+        g_n = o.flux_g(ul, ur, np.array([c, s]))
+        g_x = o.flux_g(R @ ul, R @ ur, np.array([1.0, 0.0]))
+        np.testing.assert_allclose(g_n, R.T @ g_x, rtol=1e-12, atol=1e-12)
+
+
+def test_hll_supersonic_is_upwind(oracle_mod):
+    o = oracle_mod.Oracle(configs.get("cfg2", mesh=dict(nx=2)))
+    rho, v, p = 1.0, 3.0, 1.0  # Mach > 2: S_L > 0
+    u = np.array([rho, rho * v, p / (G - 1) + 0.5 * rho * v * v])
+    u2 = np.array([0.8, 0.8 * 3.2, 0.9 / (G - 1) + 0.5 * 0.8 * 3.2 ** 2])
+    np.testing.assert_allclose(o.flux_g(u, u2), euler_flux(u, [1.0, 0.0]), rtol=1e-14)
+    um = u * np.array([1, -1, 1])
+    u2m = u2 * np.array([1, -1, 1])
+    np.testing.assert_allclose(o.flux_g(u2m, um), euler_flux(um, [1.0, 0.0]), rtol=1e-14)
+
+
+# ------------------------------------------------------------------ App. A: kinetic == analytic SG
+@pytest.mark.parametrize("M", [1, 3, 5, 8])
+def test_kinetic_flux_equals_analytic_sg_flux(oracle_mod, M):
+    """App. A: with the quadratic entropy, the kinetic LF flux equals
+    G_i = 1/4 (u_l^T C_i u_l + u_r^T C_i u_r) - dx/(2dt)(u_r - u_l)_i once the quadrature is exact
+    for degree 3M, i.e. Gauss-LEGENDRE with Q >= ceil((3M+1)/2) (reading 26)."""
+    Q = math.ceil((3 * M + 1) / 2)
+    cfg = configs.get("cfg1", closure="quadratic", M=M, q1d=Q, mesh=dict(nx=5, periodic=True))
+    o = oracle_mod.Oracle(cfg)
+    N = M + 1
+    # C_i = <phi phi^T phi_i> from an independent 64-point rule (numpy)
+    x, w = np.polynomial.legendre.leggauss(64)
+    P = np.stack([np.sqrt(2 * i + 1) * np.polynomial.legendre.legval(x, np.eye(N)[i]) for i in range(N)])
+    Cten = np.einsum("k,ik,jk,lk->lij", w / 2, P, P, P)
+    rng = np.random.default_rng(M)
+    uhat = np.zeros((5, N, 1))
+    uhat[:, :, 0] = rng.standard_normal((5, N)) * 0.5
+    uhat[:, 0, 0] += 2.0
+    dt = 1e-3
+    dx = (cfg["mesh"]["x1"] - cfg["mesh"]["x0"]) / 5
+    new = o.flux_update(uhat.copy(), uhat, dt)  # quadratic closure: lambda = uhat
+
+    def Gsg(ul, ur):
+        return np.array([0.25 * (ul @ Cten[i] @ ul + ur @ Cten[i] @ ur) for i in range(N)]) - dx / (2 * dt) * (ur - ul)
+
+    for j in range(5):
+        ul, uc, ur = uhat[j - 1, :, 0], uhat[j, :, 0], uhat[(j + 1) % 5, :, 0]
+        ref = uc - dt / dx * (Gsg(uc, ur) - Gsg(ul, uc))
+        np.testing.assert_allclose(new[j, :, 0], ref, rtol=0, atol=1e-12)
+
+
+# ------------------------------------------------------------------ steps
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3"])
+def test_uniform_state_is_preserved_bit_exactly(oracle_mod, name):
+    # periodic, so every cell sees the same reconstruction (a Dirichlet ghost differs from
+    # u_s(grad s(u)) by rounding)
+    cfg = configs.get(name, mesh=dict(nx=8, ny=6, periodic=True))
+    cfg["ic"] = dict(kind="uniform", states=[cfg["ic"]["states"][0]])
+    o = oracle_mod.Oracle(cfg)
+    u = o.project_ic()
+    u0 = u.copy()
+    lam = o.warm_start(u)
+    for _ in range(3):
+        w, it, _, dt, _ = o.step(u, lam)
+        assert w == 0 and (it == 0).all() and dt > 0
+    np.testing.assert_array_equal(u, u0)
+
+
+def hll_fv_sod(nx, t_end, cfl=0.4):
+    """Deterministic first-order FV with the HLL flux (Davis speeds), transmissive ends — written
+    here independently of the oracle as the xi-independent reference."""
+    dx = 1.0 / nx
+    x = (np.arange(nx) + 0.5) * dx
+    U = np.where(x[:, None] < 0.5, [1.0, 0.0, 1.0 / (G - 1)], [0.125, 0.0, 0.1 / (G - 1)])
+    t = 0.0
+
+    def prim(U):
+        rho, m, E = U[:, 0], U[:, 1], U[:, 2]
+        v = m / rho
+        p = (G - 1) * (E - 0.5 * rho * v * v)
+        return rho, v, p, np.sqrt(G * p / rho)
+
+    dts = []
+    while t < t_end * (1 - 1e-14):
+        rho, v, p, c = prim(U)
+        dt = min(cfl * dx / np.max(np.abs(v) + c), t_end - t)
+        Ue = np.vstack([U[:1], U, U[-1:]])
+        rho, v, p, c = prim(Ue)
+        F = np.stack([rho * v, rho * v * v + p, (Ue[:, 2] + p) * v], axis=1)
+        SL = np.minimum(v[:-1] - c[:-1], v[1:] - c[1:])[:, None]
+        SR = np.maximum(v[:-1] + c[:-1], v[1:] + c[1:])[:, None]
+        Fh = np.where(SL >= 0, F[:-1], np.where(SR <= 0, F[1:],
+                      (SR * F[:-1] - SL * F[1:] + SL * SR * (Ue[1:] - Ue[:-1])) / (SR - SL)))
+        U = U - dt / dx * (Fh[1:] - Fh[:-1])
+        t += dt
+        dts.append(dt)
+    return U, dts
+
+
+def test_xi_independent_ic_is_deterministic_fv(oracle_mod):
+    cfg = configs.get("cfg2", mesh=dict(nx=100), t_end=0.05, M=3, q1d=6)
+    cfg["ic"]["xs1"] = (0.0,)
+    o = oracle_mod.Oracle(cfg)
+    u, lam, info = o.run(record=True)
+    ref, dts = hll_fv_sod(100, 0.05)
+    assert info["steps"] == len(dts)
+    # same scheme; differences are rounding of u_s(grad s(u)) and quadrature sums over ~80 steps
+    np.testing.assert_allclose(u[:, 0, :], ref, rtol=1e-10, atol=1e-10)
+    assert np.abs(u[:, 1:, :]).max() < 1e-14
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg3"])
+def test_periodic_domain_conserves_zeroth_moment(oracle_mod, name):
+    cfg = configs.get(name, mesh=dict(nx=40 if name == "cfg1" else 12, ny=10, periodic=True))
+    o = oracle_mod.Oracle(cfg)
+    u = o.project_ic()
+    lam = o.warm_start(u)
+    _, _, _, area = o.geometry()
+    tot0 = (area[:, None] * u[:, 0, :]).sum(axis=0)
+    for _ in range(20):
+        w, *_ = o.step(u, lam)
+        assert w == 0
+    tot = (area[:, None] * u[:, 0, :]).sum(axis=0)
+    np.testing.assert_allclose(tot, tot0, rtol=1e-12, atol=1e-12)
+
+
+# ------------------------------------------------------------------ exact solutions
+def burgers_exact_expectation(x, t):
+    # shock speed (12+3)/2 = 7.5; E[u](x,t) = 3 + 9 P(xi > (x - 0.5 - 7.5 t)/0.2)
+    z = (x - 0.5 - 7.5 * t) / 0.2
+    return 3.0 + 9.0 * np.clip((1.0 - z) / 2.0, 0.0, 1.0)
+
+
+def test_burgers_expectation_converges_to_exact(oracle_mod):
+    errs = []
+    for nx in (100, 200, 400):
+        o = oracle_mod.Oracle(configs.get("cfg1", mesh=dict(nx=nx)))
+        u, _, info = o.run()
+        assert abs(info["t"] - 0.11) < 1e-14
+        dx = 3.0 / nx
+        x = (np.arange(nx) + 0.5) * dx
+        errs.append(np.sum(np.abs(u[:, 0, 0] - burgers_exact_expectation(x, 0.11))) * dx)
+    assert errs[0] > errs[1] > errs[2]
+    assert errs[2] / errs[0] < 0.7
+    assert errs[1] < 0.12
+
+
+def sod_exact(xt):
+    """Exact Riemann solution of Sod (1,0,1)|(0.125,0,0.1) at x/t (Toro's two-shock/rarefaction
+    solver with Newton on p*)."""
+    rl, ul, pl, rr, ur, pr = 1.0, 0.0, 1.0, 0.125, 0.0, 0.1
+    cl, cr = np.sqrt(G * pl / rl), np.sqrt(G * pr / rr)
+
+    def f(p, r, pk, ck):
+        if p > pk:
+            A, B = 2 / ((G + 1) * r), (G - 1) / (G + 1) * pk
+            return (p - pk) * np.sqrt(A / (p + B))
+        return 2 * ck / (G - 1) * ((p / pk) ** ((G - 1) / (2 * G)) - 1)
+
+    p = 0.5 * (pl + pr)
+    for _ in range(100):
+        F = f(p, rl, pl, cl) + f(p, rr, pr, cr) + ur - ul
+        h = 1e-8
+        dF = (f(p + h, rl, pl, cl) + f(p + h, rr, pr, cr) - f(p - h, rl, pl, cl) - f(p - h, rr, pr, cr)) / (2 * h)
+        p -= F / dF
+    us = 0.5 * (ul + ur) + 0.5 * (f(p, rr, pr, cr) - f(p, rl, pl, cl))
+    rsl = rl * (p / pl) ** (1 / G)
+    rsr = rr * ((p / pr + (G - 1) / (G + 1)) / ((G - 1) / (G + 1) * p / pr + 1))
+    S = ur + cr * np.sqrt((G + 1) / (2 * G) * p / pr + (G - 1) / (2 * G))
+    csl = cl * (p / pl) ** ((G - 1) / (2 * G))
+    out = np.empty_like(xt)
+    for i, s in enumerate(xt):
+        if s < ul - cl:
+            out[i] = rl
+        elif s < us - csl:
+            out[i] = rl * (2 / (G + 1) + (G - 1) / ((G + 1) * cl) * (ul - s)) ** (2 / (G - 1))
+        elif s < us:
+            out[i] = rsl
+        elif s < S:
+            out[i] = rsr
+        else:
+            out[i] = rr
+    return out, (p, us, rsl, rsr, S)
+
+
+def test_sod_star_state_matches_textbook():
+    _, (p, u, rl, rr, S) = sod_exact(np.array([0.0]))
+    # Toro, Riemann Solvers, Table 4.3 / SPEC.md:256
+    assert abs(p - 0.30313) < 1e-5 and abs(u - 0.92745) < 1e-5
+    assert abs(rl - 0.42632) < 1e-5 and abs(rr - 0.26557) < 1e-5 and abs(S - 1.75216) < 1e-5
+
+
+@pytest.mark.slow
+def test_sod_expectation_close_to_exact(oracle_mod):
+    nx, t = 400, 0.14
+    o = oracle_mod.Oracle(configs.get("cfg2", mesh=dict(nx=nx)))
+    u, _, info = o.run()
+    x = (np.arange(nx) + 0.5) / nx
+    xg, wg = np.polynomial.legendre.leggauss(200)
+    E = np.zeros(nx)
+    for xi, w in zip(xg, wg):
+        E += 0.5 * w * sod_exact((x - 0.5 - 0.05 * xi) / t)[0]
+    err = np.sum(np.abs(u[:, 0, 0] - E)) / nx
+    assert err < 0.01, err
+
+
+# ------------------------------------------------------------------ One-Shot (Theorems 1-2)
+def _steady(oracle_mod, mode):
+    o = oracle_mod.Oracle(configs.steady1d(mode))
+    u = o.project_ic()
+    lam = o.warm_start(u)
+    res1, total = None, 0
+    for n in range(5000):
+        w, it, _, _, res = o.step(u, lam)
+        assert w == 0
+        total += int(it.sum())
+        res1 = res if res1 is None else res1
+        if res <= 1e-8 * res1:
+            return u, total
+    raise AssertionError("no steady state")
+
+
+def test_one_shot_reaches_the_ipm_fixed_point_with_fewer_newton_steps(oracle_mod):
+    u_full, n_full = _steady(oracle_mod, "full")
+    u_os, n_os = _steady(oracle_mod, "one_step")
+    assert n_os < n_full
+    np.testing.assert_allclose(u_os, u_full, atol=1e-6)
+    # the fixed point is the inflow state u_L = 9 + 2 xi: E = 9, u_1 = 2/sqrt(3)
+    np.testing.assert_allclose(u_full[:, 0, 0], 9.0, atol=1e-6)
+    np.testing.assert_allclose(u_full[:, 1, 0], 2 / np.sqrt(3), atol=1e-5)
+
+
+# ------------------------------------------------------------------ adaptivity
+def test_indicator_examples(oracle_mod):
+    cfg = configs.get("cfg4")
+    o = oracle_mod.Oracle(cfg, bump_channel_mesh(6, 4, 1))
+    h = np.zeros((21, 4))
+    h[:6, 0] = [1.0, 0.3, 0.2, 0, 0, 0]
+    assert o.indicator(0, h) == 0.0  # nothing in the degree-2 band
+    h = np.zeros((21, 4))
+    h[20, 0] = 1.0
+    assert o.indicator(3, h) == 1.0  # only top-degree moment
+    h = np.zeros((21, 4))
+    h[0, 0], h[15, 0] = 2.0, 1.0
+    assert abs(o.indicator(3, h) - 0.2) < 1e-15  # 1/(4+1)
+
+
+def test_single_level_ladder_is_bit_identical(oracle_mod):
+    base = configs.parity_variant("cfg4")
+    mesh = bump_channel_mesh(base["mesh"]["nx_pts"], base["mesh"]["ny_pts"], base["mesh"]["seed"])
+    a = oracle_mod.Oracle(dict(base, levels=None, M=3, q1d=6), mesh)
+    b = oracle_mod.Oracle(dict(base, levels=[3], M=3, q1d=6, initial_level=0), mesh)
+    ua, ub = a.project_ic(), b.project_ic()
+    la, lb = a.warm_start(ua), b.warm_start(ub)
+    for _ in range(4):
+        wa, ita, *_ = a.step(ua, la)
+        wb, itb, *_ = b.step(ub, lb)
+        assert wa == wb == 0
+        np.testing.assert_array_equal(ita, itb)
+    np.testing.assert_array_equal(ua, ub)
+    np.testing.assert_array_equal(la, lb)
+
+
+def test_adaptive_levels_rise_where_the_state_varies(oracle_mod):
+    cfg = configs.parity_variant("cfg4")
+    mesh = bump_channel_mesh(cfg["mesh"]["nx_pts"], cfg["mesh"]["ny_pts"], cfg["mesh"]["seed"])
+    o = oracle_mod.Oracle(cfg, mesh)
+    u = o.project_ic()
+    lam = o.warm_start(u)
+    for _ in range(10):
+        w, *_ = o.step(u, lam)
+        assert w == 0
+    lv = o.levels()
+    assert lv.min() >= 0 and lv.max() <= 3
+    N = np.array([6, 10, 15, 21])[lv]
+    for j in range(o.cells):  # moments above the cell's level are zero
+        assert np.all(u[j, N[j]:] == 0.0) and np.all(lam[j, N[j]:] == 0.0)
+
+
+# ------------------------------------------------------------------ unstructured geometry
+def test_triangle_mesh_geometry(oracle_mod):
+    cfg = configs.parity_variant("cfg4")
+    mesh = bump_channel_mesh(cfg["mesh"]["nx_pts"], cfg["mesh"]["ny_pts"], cfg["mesh"]["seed"])
+    o = oracle_mod.Oracle(cfg, mesh)
+    nbr, nrm, coef, area = o.geometry()
+    assert (area > 0).all()
+    # closed polygons: sum_e |e| n_e = 0
+    s = (coef[:, :, None] * area[:, None, None] * nrm).sum(axis=1)
+    assert np.abs(s).max() < 1e-14
+    # neighbour relation is symmetric with opposite normals
+    for t in range(o.cells):
+        for e in range(3):
+            nb = nbr[t, e]
+            if nb >= 0:
+                back = np.nonzero(nbr[nb] == t)[0]
+                assert len(back) == 1
+                np.testing.assert_allclose(nrm[nb, back[0]], -nrm[t, e], atol=1e-14)
+    # total area = channel minus the piecewise-linear bump (circular segment 0.0672...)
+    seg = 1.3 ** 2 * np.arccos(1.2 / 1.3) - 1.2 * np.sqrt(1.3 ** 2 - 1.2 ** 2)
+    assert abs(area.sum() - (3.0 - seg)) < 2e-3
