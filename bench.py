@@ -1,0 +1,313 @@
+#!/usr/bin/env python
+"""Benchmark of the IPM hot path (arXiv 1912.09238) on B200.
+
+One step = one ipm_step over every cell of the workload: per-cell Newton solve of the IPM dual
+problem (FULL, tau = 1e-10), CFL dt, kinetic-flux moment update (all rows of DESIGN.md §Path).
+Default workload: BASELINE config 3 (2D Euler Riemann, 1024^2 cells, N=15 x m=4, Q=10x10 GL)
+started from the seeded dual-solve stress state so that every cell iterates.
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle (the reference arm of
+this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FP64_PEAK_TFLOPS = 37.2  # derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary.json")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg3")
+    ap.add_argument("--nx", type=int, default=0, help="override grid size (cartesian nx = ny)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--seed", type=int, default=9238)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------------------------
+def flops_per_iteration(N, m, Q):
+    """Algorithmic fp64 flops of one Newton iteration of one cell:
+    reconstruction 2QNm, gradient 2QNm, Hessian unique entries 2Q N(N+1)/2 m(m+1)/2,
+    Cholesky n^3/3 and two triangular solves 2n^2 (n = N m).  Transcendentals not counted."""
+    n = N * m
+    return 2 * Q * N * m + 2 * Q * N * m + 2 * Q * (N * (N + 1) // 2) * (m * (m + 1) // 2) + n ** 3 / 3 + 2 * n * n
+
+
+def flops_initial(N, m, Q):
+    """every cell evaluates the reconstruction and gradient once before its first test (a2 + a3)"""
+    return 4 * Q * N * m
+
+
+def flux_bytes_per_cell(N, m, Q):
+    """algorithmic HBM bytes of the flux kernel per cell: node states read once, uhat read + write"""
+    return 8 * (Q * m + 2 * N * m)
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index=0):
+        self.samples, self.index, self._stop = [], index, threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) > 1 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for nme, v in zip(names, s[3:7]):
+                if v.strip().lower() == "active":
+                    reasons.add(nme)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------------------------
+def workload(args):
+    from inputs import configs
+
+    cfg = configs.get(args.config)
+    if args.nx and cfg["mesh"]["kind"] == "cart2d":
+        cfg["mesh"].update(nx=args.nx, ny=args.nx)
+    return cfg
+
+
+def run_reference(args):
+    """The reference arm of this tier: the CPU oracle, as it stands, on a bounded sample."""
+    import oracle
+    from inputs import configs
+    from inputs.generators import STRESS_AMP, cell_centres, stress_state
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    cfg = workload(args)
+    full_cells = cfg["mesh"]["nx"] * cfg["mesh"].get("ny", 1)
+    side = 128 if cfg["p"] <= 2 else 8
+    sample = configs.get(args.config, mesh=dict(nx=side, ny=side))
+    o = oracle.Oracle(sample)
+    base, z = stress_state("euler2d" if cfg["closure"] == "euler" else "burgers", cell_centres(sample["mesh"]),
+                           o.N, o.m, args.seed)
+    amp = STRESS_AMP["euler2d" if cfg["closure"] == "euler" else "burgers"]
+    lam_star = o.stress_dual(base, z, amp)
+    uhat = o.moments_from_dual_all(lam_star)
+    lam = o.warm_start(uhat)
+    steps = max(1, min(args.steps, 3))
+    t0 = time.perf_counter()
+    iters = 0
+    for _ in range(steps):
+        w, it, _, _, _ = o.step(uhat, lam)
+        iters += int(it.sum())
+    dt = time.perf_counter() - t0
+    cores = os.cpu_count()
+    value = o.cells * steps / dt
+    line = {
+        "impl": "reference", "metric": "IPM cell-steps/s (= cell dual-solves/s)", "value": value,
+        "unit": "cell-steps/s", "n_gpus": args.gpus, "steps": steps, "warmup": 0,
+        "ms_per_step": dt / steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "cells_full": full_cells, "sample_cells": o.cells},
+        "cpu_baseline": {"value": value, "unit": "cell-steps/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{side}x{side} cells of the {args.config} stress state, {steps} steps "
+                                   f"({iters} Newton iterations), OpenMP over cells"},
+        "e2e": {"value": value, "unit": "cell-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    return line
+
+
+def cpu_baseline(args, cfg):
+    """Oracle timed on the host cores on a bounded sample (~10-30 s of CPU work)."""
+    ref = run_reference(args)
+    if ref is None:
+        return None
+    return ref["cpu_baseline"]
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from inputs.generators import STRESS_AMP, cell_centres, stress_state
+    from paper_1912_09238_b200 import Context
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = workload(args)
+    g = Context(cfg)
+    kind = "euler2d" if cfg["closure"] == "euler" else "burgers"
+    base, z = stress_state(kind, cell_centres(cfg["mesh"]), g.N, g.m, args.seed + rank)
+    amp = STRESS_AMP[kind]
+    dev = torch.device("cuda", local)
+    lam_s = g.zeros()
+    g.ipm_stress_dual(torch.from_numpy(base).to(dev), torch.from_numpy(z).to(dev), amp[0], amp[1], lam_s)
+    del base, z
+    u0 = g.zeros()
+    g.ipm_moments_from_dual(lam_s, u0)
+    lam0 = g.zeros()
+    g.ipm_warm_start(u0, lam0)
+    uhat, lam = u0.clone(), lam0.clone()
+    g.enable_timing(True)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up (starts from the stress state)
+    for _ in range(args.warmup):
+        g.ipm_step(uhat, lam, None, sync=False)
+    barrier()
+    # timed region: K consecutive steps (Algorithm 1), device-timed with CUDA events
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dual_ms, flux_ms, iters = [], [], 0
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            info = g.ipm_step(uhat, lam, None, sync=True)
+            iters += info.newton_iters
+            d, f = g.last_kernel_ms()
+            dual_ms.append(d)
+            flux_ms.append(f)
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    cells_total = g.cells * world
+    value = cells_total * args.steps / (ms / 1e3)
+
+    # end-to-end through the C-ABI with host buffers: H2D of the step inputs (uhat, lambda) from
+    # pinned memory, ipm_step, D2H of the step result (uhat, lambda), every step
+    e2e = None
+    if not args.no_e2e:
+        h_u = torch.empty_like(uhat, device="cpu").pin_memory()
+        h_l = torch.empty_like(lam, device="cpu").pin_memory()
+        h_u.copy_(uhat)
+        h_l.copy_(lam)
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            uhat.copy_(h_u, non_blocking=True)
+            lam.copy_(h_l, non_blocking=True)
+            g.ipm_step(uhat, lam, None, sync=False)
+            h_u.copy_(uhat, non_blocking=True)
+            h_l.copy_(lam, non_blocking=True)
+        e1.record(stream)
+        barrier()
+        ms_e = e0.elapsed_time(e1)
+        te = torch.tensor([ms_e], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        nbytes = (uhat.numel() + lam.numel()) * 8
+        e2e = {"value": cells_total * args.steps / (float(te.item()) / 1e3), "unit": "cell-steps/s",
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes}
+
+    N, m, Q = g.N, g.m, g.Q
+    dual_avg = float(np.mean(dual_ms))
+    flops = iters / args.steps * flops_per_iteration(N, m, Q) + g.cells * flops_initial(N, m, Q)
+    achieved = flops / (dual_avg / 1e3) / 1e12
+    traffic = None
+    if os.path.exists(NCU_SUMMARY):
+        try:
+            traffic = json.load(open(NCU_SUMMARY)).get(args.config, {}).get("dual_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    flux_avg = float(np.mean(flux_ms))
+    hbm = json.load(open(MEASURED))["hbm_gbs"] if os.path.exists(MEASURED) else 6650.0
+    flux_gbs = g.cells * flux_bytes_per_cell(N, m, Q) / (flux_avg / 1e3) / 1e9
+    line = None
+    if rank == 0:
+        line = {
+            "metric": "IPM cell-steps/s (= cell dual-solves/s)", "value": value, "unit": "cell-steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": args.config, "cells_per_gpu": g.cells, "N": N, "m": m, "Q": Q,
+                       "newton": cfg["newton"], "tau": cfg["tau"],
+                       "state": "seeded dual-solve stress state (SURVEY §8d), steps continue Algorithm 1",
+                       "l2": "inputs larger than L2 (node states %.1f GB)" % (g.cells * Q * m * 8 / 1e9),
+                       "parallelism": "replicas" if world > 1 else "single"},
+            "newton_iters_per_cell_step": iters / (g.cells * args.steps),
+            "cell_newton_iters_per_s": iters * world / (ms / 1e3),
+            "roofline": {"bound": "alu", "kernel": "k_dual_warp", "achieved": achieved,
+                         "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
+                         "traffic": traffic, "dual_ms_avg": dual_avg,
+                         "share_of_step": dual_avg / (ms / args.steps)},
+            "roofline_flux": {"bound": "hbm", "kernel": "k_flux_warp", "achieved": flux_gbs, "peak": hbm,
+                              "unit": "GB/s", "frac": flux_gbs / hbm, "flux_ms_avg": flux_avg},
+            "e2e": e2e,
+            "gpu_launches": 4 * args.steps,
+            "clocks": clk.summary(),
+        }
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return line
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        line = run_reference(args)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+    line = run_ours(args)
+    if line is not None:
+        line["cpu_baseline"] = None if args.no_cpu_baseline else cpu_baseline(args, None)
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,212 @@
+/*
+ * ipm.h — C-ABI of libipm: the B200 (sm_100a) hot path of the Intrusive Polynomial Moment
+ * method, Kusch, Wolters, Frank, arXiv 1912.09238 ("PAPER.md:n" = line n of the paper source).
+ *
+ * The path, per (pseudo-)time step (Algorithm 1; Algorithm 2, PAPER.md:252-269;
+ * Algorithm 3):
+ *   1. per spatial cell j, Newton iteration on the convex dual problem
+ *        lambda_j = argmin L(lambda; uhat_j),  L = <s_*(lambda^T phi)>_Q - sum_i lambda_i^T uhat_i
+ *      (PAPER.md:155-180), to ||grad L|| < tau (FULL) or one step (ONE_STEP),
+ *      optionally choosing the cell's next polynomial degree;
+ *   2. CFL time step from the reconstructed states u_s(lambda^T phi(xi_k));
+ *   3. kinetic-flux finite-volume moment update.
+ *
+ * Conventions (all entry points):
+ *   - d_* arguments are DEVICE pointers on the context's device, caller-owned, contiguous,
+ *     fp64 unless stated.  Moment / dual arrays are [cells][N][m] row-major (m fastest),
+ *     N = binom(M+p, p) the full basis size; cell order: 1D j; cartesian iy*nx+ix; tri = triangle id.
+ *     With adaptivity entries above a cell's level are zero.
+ *   - h_* arguments are HOST pointers.
+ *   - Calls are asynchronous on the stream given in ipm_config.stream (NULL = legacy default
+ *     stream) unless documented as synchronous.  They return IPM_ERR_ARG for invalid arguments,
+ *     IPM_ERR_CUDA for launch/runtime errors; per-cell numerical outcomes are written to per-cell
+ *     status arrays (ipm_cell_status), never returned by the asynchronous calls.
+ *   - The context allocates all its device memory in ipm_init and nothing afterwards.
+ *   - One context per device and thread; not thread-safe.
+ *   - There is no CPU fallback: without a CUDA device ipm_init returns IPM_ERR_CUDA.
+ */
+#ifndef IPM_H
+#define IPM_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define IPM_API __attribute__((visibility("default")))
+#else
+#define IPM_API
+#endif
+
+typedef struct ipm_ctx ipm_ctx;
+
+typedef enum {
+  IPM_OK = 0,
+  IPM_ERR_ARG = 1,
+  IPM_ERR_CUDA = 2,
+  IPM_ERR_NCCL = 3,
+  IPM_ERR_UNSUPPORTED = 4, /* size/closure combination not compiled in */
+  IPM_ERR_NUMERIC = 5      /* a synchronous call found failed cells (see ipm_cell_status) */
+} ipm_status;
+
+/* per-cell outcome of the dual solve (readings 3', 4, 5 in DESIGN.md) */
+typedef enum {
+  IPM_CELL_OK = 0,
+  IPM_CELL_NONCONVERGENCE = 1,     /* max_newton iterations without ||grad L|| < tau */
+  IPM_CELL_ILLCONDITIONED = 2,     /* Cholesky of the dual Hessian found a pivot <= 0 / non-finite */
+  IPM_CELL_LINESEARCH = 3,         /* Armijo backtracking exhausted max_halvings */
+  IPM_CELL_INADMISSIBLE = 4        /* the starting lambda reconstructs a non-admissible state */
+} ipm_cell_status;
+
+/* entropy closures: u_s = (grad s)^{-1} */
+typedef enum {
+  IPM_CLOSURE_QUADRATIC = 0, /* s = |u|^2/2, IPM == stochastic Galerkin */
+  IPM_CLOSURE_BARRIER = 1,   /* scalar, u(L) = u- + (u+ - u-)/(1+exp(-L)) (BASELINE cfg 1) */
+  IPM_CLOSURE_EULER = 2      /* U = -rho S/(gamma-1) (BASELINE cfg 2; App. B up to scaling) */
+} ipm_closure;
+
+/* deterministic two-point fluxes g(u_l, u_r) used inside the kinetic flux */
+typedef enum {
+  IPM_FLUX_LF_GLOBAL = 0, /* scalar Burgers: (u_l^2+u_r^2)/4 - dx/(2dt)(u_r-u_l) */
+  IPM_FLUX_HLL = 1,       /* Euler 1D, Davis wave speeds */
+  IPM_FLUX_RUSANOV = 2    /* Euler, local Lax-Friedrichs along the face normal */
+} ipm_flux;
+
+typedef enum { IPM_MESH_1D = 0, IPM_MESH_CART2D = 1, IPM_MESH_TRI = 2 } ipm_mesh_kind;
+typedef enum { IPM_BC_TRANSMISSIVE = 0, IPM_BC_STATE = 1, IPM_BC_SLIP = 2 } ipm_bc_kind;
+typedef enum { IPM_NEWTON_FULL = 0, IPM_NEWTON_ONE_STEP = 1 } ipm_newton_mode;
+typedef enum { IPM_UPDATE_CONSERVATIVE = 0, IPM_UPDATE_PAPER_C = 1 } ipm_update_form;
+typedef enum { IPM_IC_UNIFORM = 0, IPM_IC_STEP1D = 1, IPM_IC_QUAD2D = 2 } ipm_ic_kind;
+
+/* A primitive state as a function of the random vector xi.
+ *   kind 0 (affine):     q_c(xi) = q0[c] + sum_d q1[c][d] xi_d; components (u) | (rho,v,p) | (rho,vx,vy,p)
+ *   kind 1 (freestream): rho = q0[0], p = q0[1], Mach = q0[2] + q0[3] xi[dim_a],
+ *                        angle(deg) = q0[4] + q0[5] xi[dim_b], v = Mach c (cos, sin). */
+typedef struct {
+  int32_t kind, dim_a, dim_b, reserved;
+  double q0[6];
+  double q1[5][3];
+} ipm_state;
+
+typedef struct {
+  /* random space: total-degree Legendre basis, tensor Gauss-Legendre rule */
+  int32_t p, M, q1d;
+  /* physics */
+  int32_t m;                 /* states per node: 1 (scalar), 3 (Euler 1D), 4 (Euler 2D) */
+  int32_t closure, flux;
+  double gamma;              /* Euler */
+  double u_minus, u_plus;    /* barrier bounds */
+  /* mesh (the full, global mesh) */
+  int32_t mesh_kind, nx, ny, periodic;
+  double x0, x1, y0, y1;
+  int32_t n_vert, n_tri;
+  const double *h_vert;      /* [n_vert][2] */
+  const int32_t *h_tri;      /* [n_tri][3] counter-clockwise */
+  const int32_t *h_tri_tag;  /* [n_tri][3] boundary tag of edge (v_e, v_e+1), -1 interior */
+  /* boundary conditions, indexed by side (1D: 0 left, 1 right; cart: 0 left, 1 right, 2 bottom,
+   * 3 top) or by triangle edge tag */
+  int32_t bc_kind[4];
+  ipm_state bc_state[4];
+  /* Newton */
+  double tau, armijo_c;
+  int32_t max_newton, max_halvings;
+  int32_t newton_mode, update_form;
+  double cfl;
+  /* adaptivity: n_levels = 0 -> off; level_M ascending, level_M[n_levels-1] == M */
+  int32_t n_levels;
+  int32_t level_M[8];
+  double delta_dec, delta_inc;
+  /* distribution: the context owns part (rank) of a px x py block decomposition (cartesian)
+   * or of the Morton-ordered cell list (tri); nranks = 1 -> whole mesh */
+  int32_t rank, nranks, px, py;
+  const void *nccl_id;       /* 128-byte ncclUniqueId (host) when nranks > 1 */
+  void *stream;              /* cudaStream_t */
+} ipm_config;
+
+typedef struct {
+  double dt, t;              /* time step taken, time after the step */
+  double residual;           /* sum_j |Omega_j| |uhat_{j,0,0}^{n+1} - uhat_{j,0,0}^n| */
+  int64_t newton_iters;      /* accepted Newton steps over all local cells this step */
+  int64_t failed_cells;      /* cells with status != IPM_CELL_OK */
+  int32_t worst_status;      /* max ipm_cell_status over local cells */
+  int32_t reserved;
+} ipm_step_info;
+
+/* Create a context: host setup of basis, quadrature and mesh tables, device upload,
+ * communicator (nranks > 1).  Synchronous. */
+IPM_API ipm_status ipm_init(const ipm_config *cfg, ipm_ctx **out);
+IPM_API void ipm_destroy(ipm_ctx *c);
+IPM_API const char *ipm_status_string(ipm_status s);
+IPM_API const char *ipm_last_error(void);
+
+/* sizes of the local problem: cells (owned), N, Q, m */
+IPM_API ipm_status ipm_sizes(const ipm_ctx *c, int64_t *cells, int32_t *N, int32_t *Q, int32_t *m);
+/* host copies of the basis tables: h_xi [Q][p], h_omega [Q], h_phi [Q][N] (any may be NULL) */
+IPM_API ipm_status ipm_get_basis(const ipm_ctx *c, double *h_xi, double *h_omega, double *h_phi);
+/* host copy of the owned cells' global ids [cells] (int64) */
+IPM_API ipm_status ipm_get_cell_ids(const ipm_ctx *c, int64_t *h_ids);
+
+/* Dual solve for all owned cells (Alg. 1 lines 4-10; Alg. 2 line 5).
+ *   d_uhat   [cells][N][m] in
+ *   d_lambda [cells][N][m] in: warm start, out: last accepted iterate
+ *   mode     IPM_NEWTON_FULL | IPM_NEWTON_ONE_STEP
+ *   d_iters  [cells] int32 out: accepted Newton steps (nullable)
+ *   d_status [cells] int32 out: ipm_cell_status (nullable)
+ *   d_crit   [cells] out: final sum_a ||grad_{lambda_{.,a}} L||_2 (nullable) */
+IPM_API ipm_status ipm_dual_solve(ipm_ctx *c, const double *d_uhat, double *d_lambda, int32_t mode,
+                          int32_t *d_iters, int32_t *d_status, double *d_crit);
+
+/* Kinetic-flux moment update from given duals:
+ *   d_lambda    [cells][N][m] in (halo duals are exchanged internally when nranks > 1)
+ *   d_uhat_old  [cells][N][m] in; d_uhat_new [cells][N][m] out (may not alias d_uhat_old)
+ *   dt > 0: use it; dt <= 0: CFL step from the reconstructed states, capped by t_end - t.
+ *   Uses ipm_config.update_form.  d_dt (nullable, device, 1 double) receives the step used. */
+IPM_API ipm_status ipm_flux_update(ipm_ctx *c, const double *d_lambda, const double *d_uhat_old,
+                           double *d_uhat_new, double dt, double *d_dt);
+
+/* One full step of Algorithm 1/2/3 in place: dual solve (config newton_mode), refinement level
+ * (n_levels > 0), CFL dt capped at t_end - t (t_end <= 0: no cap, steady), moment update.
+ * info == NULL: asynchronous.  info != NULL: synchronous; fills info. */
+IPM_API ipm_status ipm_step(ipm_ctx *c, double *d_uhat, double *d_lambda, double t_end, ipm_step_info *info);
+
+/* Helpers for inputs (not steps of the path):
+ *   ipm_project_ic: uhat_j = <ubar_j(xi) phi>_Q with exact cell averages of a piecewise-constant IC
+ *                   (Alg. 1 line 2); also resets t = 0 and levels to initial_level.
+ *   ipm_warm_start: lambda = e_0 (x) grad s(uhat_0) per cell (reading 6)
+ *   ipm_moments_from_dual: uhat = h(lambda) = <u_s(lambda^T phi) phi^T>_Q
+ *   ipm_stress_dual: lambda_0 = grad s(d_base[j]); lambda_{i,a} = (rel |lambda_{0,a}| + abs)
+ *                    2^{-|i|} d_z[j][i][a], higher modes scaled so max_k Lambda_E <= lambda_{0,E}/2. */
+typedef struct {
+  int32_t kind, initial_level;
+  double xs0, xs1[3], ys0, ys1[3];
+  ipm_state state[4];        /* STEP1D: left,right; QUAD2D: NE,NW,SW,SE; UNIFORM: [0] */
+} ipm_ic;
+IPM_API ipm_status ipm_project_ic(ipm_ctx *c, const ipm_ic *ic, double *d_uhat);
+IPM_API ipm_status ipm_warm_start(ipm_ctx *c, const double *d_uhat, double *d_lambda);
+IPM_API ipm_status ipm_moments_from_dual(ipm_ctx *c, const double *d_lambda, double *d_uhat);
+IPM_API ipm_status ipm_stress_dual(ipm_ctx *c, const double *d_base, const double *d_z, double rel, double abs_,
+                           double *d_lambda);
+
+/* levels (adaptivity): device int32 [cells]; get/set copy from/to the context */
+IPM_API ipm_status ipm_get_levels(ipm_ctx *c, int32_t *d_levels);
+IPM_API ipm_status ipm_set_levels(ipm_ctx *c, const int32_t *d_levels);
+/* per-cell results of the last ipm_step: d_iters, d_status int32 [cells] (device, nullable) */
+IPM_API ipm_status ipm_last_cell_stats(ipm_ctx *c, int32_t *d_iters, int32_t *d_status);
+/* simulation time (host, synchronous) */
+IPM_API ipm_status ipm_get_time(ipm_ctx *c, double *t);
+IPM_API ipm_status ipm_set_time(ipm_ctx *c, double t);
+
+/* NCCL bootstrap: rank 0 creates the 128-byte id that the caller broadcasts (e.g. with
+ * torch.distributed) before ipm_init on every rank. */
+IPM_API ipm_status ipm_nccl_unique_id(void *h_id128);
+
+/* Timing of the last ipm_step's dual-solve kernel (ms, CUDA events on the ctx stream;
+ * synchronous) — used by bench.py for the roofline line. */
+IPM_API ipm_status ipm_last_kernel_ms(ipm_ctx *c, float *dual_ms, float *flux_ms);
+IPM_API ipm_status ipm_enable_timing(ipm_ctx *c, int32_t on);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,715 @@
+// ipm_api.cu — libipm host side: context setup (basis, quadrature, mesh tables), device memory,
+// and the C-ABI declared in include/ipm.h.
+//
+// Host setup follows the paper's definitions:
+//   total-degree basis, N = binom(M+p, p), graded multi-indices
+//   orthonormal Legendre phi_i(xi) = prod_n sqrt(2 i_n + 1) P_{i_n}(xi_n) for U(-1,1)^p
+//   <h>_Q = sum_k w_k h(xi_k) f_Xi(xi_k) with a tensor Gauss-Legendre rule
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/ipm.h"
+#include "ipm_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+ipm_status fail(ipm_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CUDA_OK(expr)                                                                               \
+  do {                                                                                              \
+    cudaError_t e_ = (expr);                                                                        \
+    if (e_ != cudaSuccess) return fail(IPM_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// ---------------------------------------------------------------------------------------------
+// random space
+// ---------------------------------------------------------------------------------------------
+
+// Gauss-Legendre rule on [-1,1] (weights sum to 2): Newton iteration on P_q from the asymptotic
+// guess cos(pi (k - 1/4)/(q + 1/2)), P_q and P_q' from the three-term recurrence.
+void gauss_legendre(int q, std::vector<double>& x, std::vector<double>& w) {
+  x.assign(q, 0.0);
+  w.assign(q, 0.0);
+  for (int k = 1; k <= (q + 1) / 2; ++k) {
+    double z = std::cos(M_PI * (k - 0.25) / (q + 0.5));
+    double dp = 0.0;
+    for (int it = 0; it < 64; ++it) {
+      double p0 = 1.0, p1 = z;
+      for (int n = 2; n <= q; ++n) {
+        const double p2 = ((2.0 * n - 1.0) * z * p1 - (n - 1.0) * p0) / n;
+        p0 = p1;
+        p1 = p2;
+      }
+      if (q == 1) {
+        p1 = z;
+        p0 = 1.0;
+      }
+      dp = q * (z * p1 - p0) / (z * z - 1.0);
+      const double step = p1 / dp;
+      z -= step;
+      if (std::fabs(step) <= 1e-16 * std::max(1.0, std::fabs(z))) break;
+    }
+    {
+      double p0 = 1.0, p1 = z;
+      for (int n = 2; n <= q; ++n) {
+        const double p2 = ((2.0 * n - 1.0) * z * p1 - (n - 1.0) * p0) / n;
+        p0 = p1;
+        p1 = p2;
+      }
+      dp = q * (z * p1 - p0) / (z * z - 1.0);
+    }
+    const double wk = 2.0 / ((1.0 - z * z) * dp * dp);
+    x[k - 1] = -z;
+    x[q - k] = z;
+    w[k - 1] = wk;
+    w[q - k] = wk;
+  }
+  if (q % 2 == 1) x[q / 2] = 0.0;
+}
+
+double legendre_orthonormal(int n, double x) {
+  double p0 = 1.0, p1 = x;
+  if (n == 0) return 1.0;
+  for (int k = 2; k <= n; ++k) {
+    const double p2 = ((2.0 * k - 1.0) * x * p1 - (k - 1.0) * p0) / k;
+    p0 = p1;
+    p1 = p2;
+  }
+  return std::sqrt(2.0 * n + 1.0) * p1;
+}
+
+int binom_total(int p, int M) {
+  long long r = 1;
+  for (int k = 1; k <= p; ++k) r = r * (M + k) / k;
+  return (int)r;
+}
+
+// graded, then lexicographically descending within one total degree (prefix property per level)
+void total_degree_set(int p, int M, std::vector<int>& idx) {
+  idx.clear();
+  std::vector<int> cur(p, 0);
+  for (int deg = 0; deg <= M; ++deg) {
+    // odometer over tuples summing to deg, first entry descending
+    std::vector<int> t(p, 0);
+    t[0] = deg;
+    for (;;) {
+      idx.insert(idx.end(), t.begin(), t.end());
+      // predecessor in lexicographic order among tuples with sum deg
+      int j = p - 2;
+      while (j >= 0 && t[j] == 0) --j;
+      if (j < 0) break;
+      t[j] -= 1;
+      int rest = 0;
+      for (int r = j + 1; r < p; ++r) rest += t[r];
+      rest += 1;
+      for (int r = j + 1; r < p; ++r) t[r] = 0;
+      t[j + 1] = rest;
+    }
+  }
+}
+
+struct HostPrim {
+  // primitive state at node xi for an ipm_state
+  static void eval(const ipm_state& s, const double* xi, int p, int m, double gamma, double* u) {
+    double q[5] = {0, 0, 0, 0, 0};
+    if (s.kind == 1) {
+      const double rho = s.q0[0], pr = s.q0[1];
+      const double mach = s.q0[2] + s.q0[3] * xi[s.dim_a];
+      const double th = (s.q0[4] + s.q0[5] * xi[s.dim_b]) * M_PI / 180.0;
+      const double c = std::sqrt(gamma * pr / rho);
+      q[0] = rho;
+      q[1] = mach * c * std::cos(th);
+      q[2] = mach * c * std::sin(th);
+      q[3] = pr;
+    } else {
+      const int nq = m;
+      for (int c = 0; c < nq; ++c) {
+        q[c] = s.q0[c];
+        for (int d = 0; d < p && d < 3; ++d) q[c] += s.q1[c][d] * xi[d];
+      }
+    }
+    if (m == 1) {
+      u[0] = q[0];
+      return;
+    }
+    const int d = m - 2;
+    double v2 = 0.0;
+    u[0] = q[0];
+    for (int k = 0; k < d; ++k) {
+      u[1 + k] = q[0] * q[1 + k];
+      v2 += q[1 + k] * q[1 + k];
+    }
+    u[m - 1] = q[d + 1] / (gamma - 1.0) + 0.5 * q[0] * v2;
+  }
+};
+
+double host_speed(int m, double gamma, const double* u, int mode /*0 dir x, 1 dir y, 2 norm*/) {
+  if (m == 1) return std::fabs(u[0]);
+  const int d = m - 2;
+  double m2 = 0.0;
+  for (int k = 0; k < d; ++k) m2 += u[1 + k] * u[1 + k];
+  const double p = (gamma - 1.0) * (u[m - 1] - 0.5 * m2 / u[0]);
+  const double c = std::sqrt(gamma * p / u[0]);
+  if (mode == 2) return std::sqrt(m2) / u[0] + c;
+  return std::fabs(u[1 + mode] / u[0]) + c;
+}
+
+template <typename T>
+T* dalloc(size_t n, std::vector<void*>& owned) {
+  if (n == 0) n = 1;
+  void* p = nullptr;
+  if (cudaMalloc(&p, n * sizeof(T)) != cudaSuccess) return nullptr;
+  owned.push_back(p);
+  return (T*)p;
+}
+
+}  // namespace
+
+struct ipm_ctx {
+  ipm_config cfg;
+  int N = 0, Q = 0, QP = 0, m = 0, p = 0, F = 0;
+  int64_t cells = 0;
+  std::vector<int> idx, deg;
+  std::vector<double> xi, omega, phi;  // phi [Q][N]
+  std::vector<int64_t> cell_ids;
+  double ghost_rate = 0.0;
+  int nl_levels[8] = {0};
+  std::vector<void*> owned;
+  cudaStream_t stream = nullptr;
+  ipm::KernelCtx k{};
+  // device buffers
+  double *d_uq = nullptr, *d_crit = nullptr;
+  int32_t *d_level = nullptr, *d_level_new = nullptr, *d_iters = nullptr, *d_status = nullptr;
+  ipm::StepScalars* d_sc = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool timing = false;
+  int initial_level = 0;
+};
+
+extern "C" {
+
+const char* ipm_status_string(ipm_status s) {
+  switch (s) {
+    case IPM_OK: return "ok";
+    case IPM_ERR_ARG: return "invalid argument";
+    case IPM_ERR_CUDA: return "CUDA error";
+    case IPM_ERR_NCCL: return "NCCL error";
+    case IPM_ERR_UNSUPPORTED: return "unsupported configuration";
+    case IPM_ERR_NUMERIC: return "failed cells";
+  }
+  return "unknown";
+}
+
+const char* ipm_last_error(void) { return g_err.c_str(); }
+
+void ipm_destroy(ipm_ctx* c) {
+  if (!c) return;
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  for (void* p : c->owned) cudaFree(p);
+  delete c;
+}
+
+ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
+  if (!cfg || !out) return fail(IPM_ERR_ARG, "null argument");
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(IPM_ERR_CUDA, "no CUDA device (libipm has no CPU path)");
+  const ipm_config& C = *cfg;
+  if (C.p < 1 || C.p > 3 || C.M < 0 || C.q1d < 1 || C.q1d > 64) return fail(IPM_ERR_ARG, "bad random space");
+  if (!(C.m == 1 || C.m == 3 || C.m == 4)) return fail(IPM_ERR_ARG, "m must be 1, 3 or 4");
+  if (C.closure == IPM_CLOSURE_BARRIER && (C.m != 1 || !(C.u_plus > C.u_minus)))
+    return fail(IPM_ERR_ARG, "barrier closure needs m = 1 and u+ > u-");
+  if (C.closure == IPM_CLOSURE_EULER && C.m == 1) return fail(IPM_ERR_ARG, "Euler closure needs m = 3 or 4");
+  if (C.nranks > 1) return fail(IPM_ERR_UNSUPPORTED, "nranks > 1 not built in this library version");
+  if (C.n_levels < 0 || C.n_levels > 8) return fail(IPM_ERR_ARG, "n_levels in [0, 8]");
+  if (C.n_levels > 0 && C.level_M[C.n_levels - 1] != C.M) return fail(IPM_ERR_ARG, "level_M[last] must equal M");
+
+  ipm_ctx* c = new ipm_ctx();
+  c->cfg = C;
+  c->stream = (cudaStream_t)C.stream;
+  c->p = C.p;
+  c->m = C.m;
+  c->N = binom_total(C.p, C.M);
+  c->Q = 1;
+  for (int d = 0; d < C.p; ++d) c->Q *= C.q1d;
+  c->QP = (c->Q % 2 == 0) ? c->Q + 1 : c->Q;
+  const int N = c->N, Q = c->Q, QP = c->QP, p = c->p, m = c->m;
+
+  // basis and quadrature
+  total_degree_set(p, C.M, c->idx);
+  c->deg.resize(N);
+  for (int i = 0; i < N; ++i) {
+    int s = 0;
+    for (int d = 0; d < p; ++d) s += c->idx[i * p + d];
+    c->deg[i] = s;
+  }
+  std::vector<double> x1, w1;
+  gauss_legendre(C.q1d, x1, w1);
+  c->xi.resize((size_t)Q * p);
+  c->omega.resize(Q);
+  c->phi.resize((size_t)Q * N);
+  for (int k = 0; k < Q; ++k) {
+    int r = k;
+    double om = 1.0;
+    for (int d = p - 1; d >= 0; --d) {
+      const int kd = r % C.q1d;
+      r /= C.q1d;
+      c->xi[(size_t)k * p + d] = x1[kd];
+      om *= 0.5 * w1[kd];  // f_Xi = 2^{-p}
+    }
+    c->omega[k] = om;
+    for (int i = 0; i < N; ++i) {
+      double v = 1.0;
+      for (int d = 0; d < p; ++d) v *= legendre_orthonormal(c->idx[i * p + d], c->xi[(size_t)k * p + d]);
+      c->phi[(size_t)k * N + i] = v;
+    }
+  }
+  std::vector<double> PhiT((size_t)N * QP, 0.0), WPhiT((size_t)N * QP, 0.0);
+  for (int i = 0; i < N; ++i)
+    for (int k = 0; k < Q; ++k) {
+      PhiT[(size_t)i * QP + k] = c->phi[(size_t)k * N + i];
+      WPhiT[(size_t)i * QP + k] = c->omega[k] * c->phi[(size_t)k * N + i];
+    }
+
+  // mesh tables
+  int F = 0;
+  int64_t cells = 0;
+  std::vector<int32_t> nbr;
+  std::vector<double> nrm, coef, area, rgeo;
+  double inv_dx = 0.0, inv_dy = 0.0;
+  if (C.mesh_kind == IPM_MESH_1D) {
+    if (C.nx < 1) {
+      delete c;
+      return fail(IPM_ERR_ARG, "nx >= 1");
+    }
+    F = 2;
+    cells = C.nx;
+    const double dx = (C.x1 - C.x0) / C.nx;
+    inv_dx = 1.0 / dx;
+    nbr.resize(cells * 2);
+    coef.assign(cells * 2, inv_dx);
+    area.assign(cells, dx);
+    for (int64_t j = 0; j < cells; ++j) {
+      nbr[j * 2 + 0] = j > 0 ? (int32_t)(j - 1) : (C.periodic ? (int32_t)(cells - 1) : -1);
+      nbr[j * 2 + 1] = j < cells - 1 ? (int32_t)(j + 1) : (C.periodic ? 0 : -2);
+    }
+  } else if (C.mesh_kind == IPM_MESH_CART2D) {
+    if (C.nx < 1 || C.ny < 1) {
+      delete c;
+      return fail(IPM_ERR_ARG, "nx, ny >= 1");
+    }
+    F = 4;
+    const int64_t nx = C.nx, ny = C.ny;
+    cells = nx * ny;
+    const double dx = (C.x1 - C.x0) / nx, dy = (C.y1 - C.y0) / ny;
+    inv_dx = 1.0 / dx;
+    inv_dy = 1.0 / dy;
+    nbr.resize(cells * 4);
+    coef.resize(cells * 4);
+    area.assign(cells, dx * dy);
+    for (int64_t iy = 0; iy < ny; ++iy)
+      for (int64_t ix = 0; ix < nx; ++ix) {
+        const int64_t j = iy * nx + ix;
+        nbr[j * 4 + 0] = (int32_t)(ix > 0 ? j - 1 : (C.periodic ? iy * nx + nx - 1 : -1));
+        nbr[j * 4 + 1] = (int32_t)(ix < nx - 1 ? j + 1 : (C.periodic ? iy * nx : -2));
+        nbr[j * 4 + 2] = (int32_t)(iy > 0 ? j - nx : (C.periodic ? (ny - 1) * nx + ix : -3));
+        nbr[j * 4 + 3] = (int32_t)(iy < ny - 1 ? j + nx : (C.periodic ? ix : -4));
+        coef[j * 4 + 0] = coef[j * 4 + 1] = inv_dx;
+        coef[j * 4 + 2] = coef[j * 4 + 3] = inv_dy;
+      }
+  } else if (C.mesh_kind == IPM_MESH_TRI) {
+    if (C.n_tri < 1 || !C.h_vert || !C.h_tri || !C.h_tri_tag) {
+      delete c;
+      return fail(IPM_ERR_ARG, "triangle mesh arrays required");
+    }
+    F = 3;
+    cells = C.n_tri;
+    nbr.assign(cells * 3, 0);
+    nrm.assign(cells * 6, 0.0);
+    coef.assign(cells * 3, 0.0);
+    area.assign(cells, 0.0);
+    rgeo.assign(cells, 0.0);
+    std::unordered_map<int64_t, int64_t> edge_owner;
+    edge_owner.reserve((size_t)cells * 3);
+    for (int64_t t = 0; t < cells; ++t)
+      for (int e = 0; e < 3; ++e) {
+        const int a = C.h_tri[t * 3 + e], b = C.h_tri[t * 3 + (e + 1) % 3];
+        const int64_t key = (int64_t)std::min(a, b) * C.n_vert + std::max(a, b);
+        const int tag = C.h_tri_tag[t * 3 + e];
+        nbr[t * 3 + e] = -1 - (tag < 0 ? 0 : tag);
+        auto it = edge_owner.find(key);
+        if (it == edge_owner.end()) {
+          edge_owner.emplace(key, t * 3 + e);
+        } else {
+          const int64_t o = it->second;
+          nbr[t * 3 + e] = (int32_t)(o / 3);
+          nbr[o] = (int32_t)t;
+        }
+      }
+    for (int64_t t = 0; t < cells; ++t) {
+      const double* A = C.h_vert + 2 * C.h_tri[t * 3 + 0];
+      const double* B = C.h_vert + 2 * C.h_tri[t * 3 + 1];
+      const double* Cc = C.h_vert + 2 * C.h_tri[t * 3 + 2];
+      const double ar = 0.5 * ((B[0] - A[0]) * (Cc[1] - A[1]) - (Cc[0] - A[0]) * (B[1] - A[1]));
+      if (!(ar > 0.0)) {
+        delete c;
+        return fail(IPM_ERR_ARG, "triangles must be counter-clockwise with positive area");
+      }
+      area[t] = ar;
+      double per = 0.0;
+      for (int e = 0; e < 3; ++e) {
+        const double* V0 = C.h_vert + 2 * C.h_tri[t * 3 + e];
+        const double* V1 = C.h_vert + 2 * C.h_tri[t * 3 + (e + 1) % 3];
+        const double ex = V1[0] - V0[0], ey = V1[1] - V0[1];
+        const double len = std::sqrt(ex * ex + ey * ey);
+        nrm[(t * 3 + e) * 2 + 0] = ey / len;
+        nrm[(t * 3 + e) * 2 + 1] = -ex / len;
+        coef[t * 3 + e] = len / ar;
+        per += len;
+      }
+      rgeo[t] = per / ar;
+    }
+  } else {
+    delete c;
+    return fail(IPM_ERR_ARG, "mesh_kind");
+  }
+  c->F = F;
+  c->cells = cells;
+  c->cell_ids.resize(cells);
+  for (int64_t j = 0; j < cells; ++j) c->cell_ids[j] = j;
+
+  // boundary ghost states per node and their CFL contribution
+  std::vector<double> ghost((size_t)4 * Q * m, 0.0);
+  for (int t = 0; t < 4; ++t)
+    if (C.bc_kind[t] == IPM_BC_STATE)
+      for (int k = 0; k < Q; ++k)
+        HostPrim::eval(C.bc_state[t], &c->xi[(size_t)k * p], p, m, C.gamma, &ghost[((size_t)t * Q + k) * m]);
+  double grate = 0.0;
+  for (int64_t j = 0; j < cells; ++j)
+    for (int f = 0; f < F; ++f) {
+      const int nb = nbr[j * F + f];
+      if (nb >= 0) continue;
+      const int tag = -1 - nb;
+      if (C.bc_kind[tag] != IPM_BC_STATE) continue;
+      for (int k = 0; k < Q; ++k) {
+        const double* ug = &ghost[((size_t)tag * Q + k) * m];
+        double r;
+        if (C.mesh_kind == IPM_MESH_1D)
+          r = host_speed(m, C.gamma, ug, 0) * inv_dx;
+        else if (C.mesh_kind == IPM_MESH_CART2D)
+          r = host_speed(m, C.gamma, ug, 0) * inv_dx + host_speed(m, C.gamma, ug, 1) * inv_dy;
+        else
+          r = host_speed(m, C.gamma, ug, 2) * rgeo[j];
+        grate = std::max(grate, r);
+      }
+    }
+  c->ghost_rate = grate;
+
+  // device memory
+  auto& O = c->owned;
+  double* d_PhiT = dalloc<double>(PhiT.size(), O);
+  double* d_WPhiT = dalloc<double>(WPhiT.size(), O);
+  double* d_omega = dalloc<double>(Q, O);
+  int32_t* d_deg = dalloc<int32_t>(N, O);
+  int32_t* d_nbr = dalloc<int32_t>(nbr.size(), O);
+  double* d_nrm = dalloc<double>(nrm.size(), O);
+  double* d_coef = dalloc<double>(coef.size(), O);
+  double* d_area = dalloc<double>(area.size(), O);
+  double* d_rgeo = dalloc<double>(rgeo.size(), O);
+  double* d_ghost = dalloc<double>(ghost.size(), O);
+  c->d_uq = dalloc<double>((size_t)cells * Q * m, O);
+  c->d_crit = dalloc<double>(cells, O);
+  c->d_level = dalloc<int32_t>(cells, O);
+  c->d_level_new = dalloc<int32_t>(cells, O);
+  c->d_iters = dalloc<int32_t>(cells, O);
+  c->d_status = dalloc<int32_t>(cells, O);
+  c->d_sc = dalloc<ipm::StepScalars>(1, O);
+  if (!d_PhiT || !d_WPhiT || !d_omega || !d_deg || !d_nbr || !d_nrm || !d_coef || !d_area || !d_rgeo || !d_ghost ||
+      !c->d_uq || !c->d_crit || !c->d_level || !c->d_level_new || !c->d_iters || !c->d_status || !c->d_sc) {
+    ipm_destroy(c);
+    return fail(IPM_ERR_CUDA, "cudaMalloc failed");
+  }
+  std::vector<int32_t> deg32(c->deg.begin(), c->deg.end());
+  auto up = [&](void* dst, const void* src, size_t bytes) {
+    return bytes == 0 ? cudaSuccess : cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice);
+  };
+  if (up(d_PhiT, PhiT.data(), PhiT.size() * 8) || up(d_WPhiT, WPhiT.data(), WPhiT.size() * 8) ||
+      up(d_omega, c->omega.data(), Q * 8) || up(d_deg, deg32.data(), N * 4) ||
+      up(d_nbr, nbr.data(), nbr.size() * 4) || up(d_nrm, nrm.data(), nrm.size() * 8) ||
+      up(d_coef, coef.data(), coef.size() * 8) || up(d_area, area.data(), area.size() * 8) ||
+      up(d_rgeo, rgeo.data(), rgeo.size() * 8) || up(d_ghost, ghost.data(), ghost.size() * 8) ||
+      cudaMemset(c->d_sc, 0, sizeof(ipm::StepScalars)) || cudaMemset(c->d_level, 0, cells * 4) ||
+      cudaMemset(c->d_level_new, 0, cells * 4)) {
+    ipm_destroy(c);
+    return fail(IPM_ERR_CUDA, "upload failed");
+  }
+  for (auto& e : c->ev) cudaEventCreate(&e);
+
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int sms = 0, optin = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+
+  ipm::KernelCtx& k = c->k;
+  k.T = ipm::Tables{d_PhiT, d_WPhiT, d_omega, d_deg, N, Q, QP, p};
+  k.mesh.kind = C.mesh_kind;
+  k.mesh.F = F;
+  k.mesh.cells = cells;
+  k.mesh.nbr = d_nbr;
+  k.mesh.nrm = d_nrm;
+  k.mesh.coef = d_coef;
+  k.mesh.area = d_area;
+  k.mesh.rate_geo = d_rgeo;
+  k.mesh.inv_dx = inv_dx;
+  k.mesh.inv_dy = inv_dy;
+  k.mesh.ghost = d_ghost;
+  for (int t = 0; t < 4; ++t) k.mesh.bc_kind[t] = C.bc_kind[t];
+  k.nw = ipm::Newton{C.tau, C.armijo_c, C.max_newton, C.max_halvings, C.newton_mode};
+  k.ad.n_levels = C.n_levels;
+  for (int l = 0; l < C.n_levels; ++l) k.ad.Nl[l] = binom_total(p, C.level_M[l]);
+  k.ad.Nprev0 = C.n_levels > 0 ? (C.level_M[0] > 0 ? binom_total(p, C.level_M[0] - 1) : 0) : 0;
+  k.ad.delta_dec = C.delta_dec;
+  k.ad.delta_inc = C.delta_inc;
+  k.cl = ipm::ClParams{C.gamma, C.u_minus, C.u_plus};
+  k.closure = C.closure;
+  k.flux = C.flux;
+  k.m = m;
+  k.sc = c->d_sc;
+  k.stream = c->stream;
+  k.sm_count = sms;
+  k.smem_optin = (size_t)optin;
+  *out = c;
+  return IPM_OK;
+}
+
+ipm_status ipm_sizes(const ipm_ctx* c, int64_t* cells, int32_t* N, int32_t* Q, int32_t* m) {
+  if (!c) return fail(IPM_ERR_ARG, "null ctx");
+  if (cells) *cells = c->cells;
+  if (N) *N = c->N;
+  if (Q) *Q = c->Q;
+  if (m) *m = c->m;
+  return IPM_OK;
+}
+
+ipm_status ipm_get_basis(const ipm_ctx* c, double* h_xi, double* h_omega, double* h_phi) {
+  if (!c) return fail(IPM_ERR_ARG, "null ctx");
+  if (h_xi) std::memcpy(h_xi, c->xi.data(), c->xi.size() * 8);
+  if (h_omega) std::memcpy(h_omega, c->omega.data(), c->omega.size() * 8);
+  if (h_phi) std::memcpy(h_phi, c->phi.data(), c->phi.size() * 8);
+  return IPM_OK;
+}
+
+ipm_status ipm_get_cell_ids(const ipm_ctx* c, int64_t* h_ids) {
+  if (!c || !h_ids) return fail(IPM_ERR_ARG, "null argument");
+  std::memcpy(h_ids, c->cell_ids.data(), c->cell_ids.size() * 8);
+  return IPM_OK;
+}
+
+static ipm_status launch_rc(int rc, const char* what) {
+  if (rc == 0) return IPM_OK;
+  if (rc < 0) return fail(IPM_ERR_UNSUPPORTED, std::string(what) + ": combination not compiled in / too large");
+  return fail(IPM_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString((cudaError_t)rc));
+}
+
+ipm_status ipm_dual_solve(ipm_ctx* c, const double* d_uhat, double* d_lambda, int32_t mode, int32_t* d_iters,
+                          int32_t* d_status, double* d_crit) {
+  if (!c || !d_uhat || !d_lambda) return fail(IPM_ERR_ARG, "null argument");
+  if (mode != IPM_NEWTON_FULL && mode != IPM_NEWTON_ONE_STEP) return fail(IPM_ERR_ARG, "mode");
+  ipm::KernelCtx k = c->k;
+  k.nw.mode = mode;
+  if (int rc = ipm::launch_step_begin(k, 0.0)) return launch_rc(rc, "step_begin");
+  ipm::DualLaunch a{};
+  a.uhat = d_uhat;
+  a.lam = d_lambda;
+  a.iters = d_iters ? d_iters : c->d_iters;
+  a.status = d_status ? d_status : c->d_status;
+  a.crit = d_crit ? d_crit : c->d_crit;
+  a.uq = nullptr;
+  a.level = c->cfg.n_levels > 0 ? c->d_level : nullptr;
+  a.level_new = nullptr;
+  a.cells = c->cells;
+  a.mode = mode;
+  a.want_rate = 0;
+  return launch_rc(ipm::launch_dual(k, a), "dual_solve");
+}
+
+ipm_status ipm_flux_update(ipm_ctx* c, const double* d_lambda, const double* d_uhat_old, double* d_uhat_new,
+                           double dt, double* d_dt) {
+  if (!c || !d_lambda || !d_uhat_old || !d_uhat_new) return fail(IPM_ERR_ARG, "null argument");
+  const ipm::KernelCtx& k = c->k;
+  if (int rc = ipm::launch_step_begin(k, c->ghost_rate)) return launch_rc(rc, "step_begin");
+  if (int rc = ipm::launch_nodes(k, d_lambda, nullptr, c->d_uq)) return launch_rc(rc, "nodes");
+  if (int rc = ipm::launch_dt(k, -1.0, dt, c->cfg.cfl)) return launch_rc(rc, "dt");
+  ipm::FluxLaunch f{c->d_uq, d_uhat_old, d_uhat_new, nullptr, c->cfg.update_form, c->cfg.cfl};
+  if (int rc = ipm::launch_flux(k, f)) return launch_rc(rc, "flux");
+  if (d_dt) CUDA_OK(cudaMemcpyAsync(d_dt, &c->d_sc->dt, 8, cudaMemcpyDeviceToDevice, c->stream));
+  return IPM_OK;
+}
+
+ipm_status ipm_step(ipm_ctx* c, double* d_uhat, double* d_lambda, double t_end, ipm_step_info* info) {
+  if (!c || !d_uhat || !d_lambda) return fail(IPM_ERR_ARG, "null argument");
+  const ipm::KernelCtx& k = c->k;
+  if (int rc = ipm::launch_step_begin(k, c->ghost_rate)) return launch_rc(rc, "step_begin");
+  ipm::DualLaunch a{};
+  a.uhat = d_uhat;
+  a.lam = d_lambda;
+  a.iters = c->d_iters;
+  a.status = c->d_status;
+  a.crit = c->d_crit;
+  a.uq = c->d_uq;
+  a.level = c->cfg.n_levels > 0 ? c->d_level : nullptr;
+  a.level_new = c->cfg.n_levels > 0 ? c->d_level_new : nullptr;
+  a.cells = c->cells;
+  a.mode = c->cfg.newton_mode;
+  a.want_rate = 1;
+  if (c->timing) cudaEventRecord(c->ev[0], c->stream);
+  if (int rc = ipm::launch_dual(k, a)) return launch_rc(rc, "dual_solve");
+  if (c->timing) cudaEventRecord(c->ev[1], c->stream);
+  if (int rc = ipm::launch_dt(k, t_end, -1.0, c->cfg.cfl)) return launch_rc(rc, "dt");
+  ipm::FluxLaunch f{c->d_uq, d_uhat, d_uhat, a.level_new, c->cfg.update_form, c->cfg.cfl};
+  if (c->timing) cudaEventRecord(c->ev[2], c->stream);
+  if (int rc = ipm::launch_flux(k, f)) return launch_rc(rc, "flux");
+  if (c->timing) cudaEventRecord(c->ev[3], c->stream);
+  if (c->cfg.n_levels > 0) std::swap(c->d_level, c->d_level_new);
+  if (info) {
+    ipm::StepScalars s;
+    CUDA_OK(cudaMemcpyAsync(&s, c->d_sc, sizeof(s), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+    info->dt = s.dt;
+    info->t = s.t;
+    info->residual = s.residual;
+    info->newton_iters = (int64_t)s.newton_iters;
+    info->failed_cells = (int64_t)s.failed;
+    info->worst_status = s.worst;
+    if (s.failed) return fail(IPM_ERR_NUMERIC, "failed cells in step");
+  }
+  return IPM_OK;
+}
+
+ipm_status ipm_project_ic(ipm_ctx* c, const ipm_ic* ic, double* d_uhat) {
+  if (!c || !ic || !d_uhat) return fail(IPM_ERR_ARG, "null argument");
+  const ipm_config& C = c->cfg;
+  const int Q = c->Q, m = c->m, p = c->p;
+  const int R = ic->kind == IPM_IC_UNIFORM ? 1 : (ic->kind == IPM_IC_STEP1D ? 2 : 4);
+  if (ic->kind == IPM_IC_STEP1D && C.mesh_kind != IPM_MESH_1D) return fail(IPM_ERR_ARG, "STEP1D needs a 1D mesh");
+  if (ic->kind == IPM_IC_QUAD2D && C.mesh_kind != IPM_MESH_CART2D)
+    return fail(IPM_ERR_ARG, "QUAD2D needs a cartesian mesh");
+  std::vector<double> region((size_t)R * Q * m), split((size_t)Q * 2);
+  for (int k = 0; k < Q; ++k) {
+    const double* x = &c->xi[(size_t)k * p];
+    for (int r = 0; r < R; ++r) HostPrim::eval(ic->state[r], x, p, m, C.gamma, &region[((size_t)r * Q + k) * m]);
+    double xs = ic->xs0, ys = ic->ys0;
+    for (int d = 0; d < p && d < 3; ++d) {
+      xs += ic->xs1[d] * x[d];
+      ys += ic->ys1[d] * x[d];
+    }
+    split[k * 2] = xs;
+    split[k * 2 + 1] = ys;
+  }
+  // temporary device copies (setup helper, synchronous)
+  double *d_reg = nullptr, *d_split = nullptr;
+  CUDA_OK(cudaMalloc(&d_reg, region.size() * 8));
+  CUDA_OK(cudaMalloc(&d_split, split.size() * 8));
+  CUDA_OK(cudaMemcpy(d_reg, region.data(), region.size() * 8, cudaMemcpyHostToDevice));
+  CUDA_OK(cudaMemcpy(d_split, split.data(), split.size() * 8, cudaMemcpyHostToDevice));
+  c->initial_level = ic->initial_level;
+  if (C.n_levels > 0) {
+    std::vector<int32_t> lv(c->cells, ic->initial_level);
+    CUDA_OK(cudaMemcpy(c->d_level, lv.data(), lv.size() * 4, cudaMemcpyHostToDevice));
+  }
+  const double dx = C.nx > 0 ? (C.x1 - C.x0) / C.nx : 0.0, dy = C.ny > 0 ? (C.y1 - C.y0) / C.ny : 0.0;
+  int rc = ipm::launch_project_ic(c->k, d_reg, d_split, ic->kind, C.nx, C.x0, C.y0, dx, dy,
+                                  C.n_levels > 0 ? c->d_level : nullptr, d_uhat);
+  ipm::StepScalars s{};
+  cudaMemcpy(c->d_sc, &s, sizeof(s), cudaMemcpyHostToDevice);  // t = 0
+  cudaStreamSynchronize(c->stream);
+  cudaFree(d_reg);
+  cudaFree(d_split);
+  return launch_rc(rc, "project_ic");
+}
+
+ipm_status ipm_warm_start(ipm_ctx* c, const double* d_uhat, double* d_lambda) {
+  if (!c || !d_uhat || !d_lambda) return fail(IPM_ERR_ARG, "null argument");
+  return launch_rc(ipm::launch_warm_start(c->k, d_uhat, d_lambda), "warm_start");
+}
+
+ipm_status ipm_moments_from_dual(ipm_ctx* c, const double* d_lambda, double* d_uhat) {
+  if (!c || !d_uhat || !d_lambda) return fail(IPM_ERR_ARG, "null argument");
+  return launch_rc(ipm::launch_nodes(c->k, d_lambda, d_uhat, nullptr), "moments_from_dual");
+}
+
+ipm_status ipm_stress_dual(ipm_ctx* c, const double* d_base, const double* d_z, double rel, double abs_,
+                           double* d_lambda) {
+  if (!c || !d_base || !d_z || !d_lambda) return fail(IPM_ERR_ARG, "null argument");
+  return launch_rc(ipm::launch_stress(c->k, d_base, d_z, rel, abs_, d_lambda), "stress_dual");
+}
+
+ipm_status ipm_get_levels(ipm_ctx* c, int32_t* d_levels) {
+  if (!c || !d_levels) return fail(IPM_ERR_ARG, "null argument");
+  CUDA_OK(cudaMemcpyAsync(d_levels, c->d_level, c->cells * 4, cudaMemcpyDeviceToDevice, c->stream));
+  return IPM_OK;
+}
+
+ipm_status ipm_set_levels(ipm_ctx* c, const int32_t* d_levels) {
+  if (!c || !d_levels) return fail(IPM_ERR_ARG, "null argument");
+  CUDA_OK(cudaMemcpyAsync(c->d_level, d_levels, c->cells * 4, cudaMemcpyDeviceToDevice, c->stream));
+  return IPM_OK;
+}
+
+ipm_status ipm_last_cell_stats(ipm_ctx* c, int32_t* d_iters, int32_t* d_status) {
+  if (!c) return fail(IPM_ERR_ARG, "null ctx");
+  if (d_iters) CUDA_OK(cudaMemcpyAsync(d_iters, c->d_iters, c->cells * 4, cudaMemcpyDeviceToDevice, c->stream));
+  if (d_status) CUDA_OK(cudaMemcpyAsync(d_status, c->d_status, c->cells * 4, cudaMemcpyDeviceToDevice, c->stream));
+  return IPM_OK;
+}
+
+ipm_status ipm_get_time(ipm_ctx* c, double* t) {
+  if (!c || !t) return fail(IPM_ERR_ARG, "null argument");
+  CUDA_OK(cudaMemcpyAsync(t, &c->d_sc->t, 8, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(cudaStreamSynchronize(c->stream));
+  return IPM_OK;
+}
+
+ipm_status ipm_set_time(ipm_ctx* c, double t) {
+  if (!c) return fail(IPM_ERR_ARG, "null ctx");
+  CUDA_OK(cudaMemcpyAsync(&c->d_sc->t, &t, 8, cudaMemcpyHostToDevice, c->stream));
+  CUDA_OK(cudaStreamSynchronize(c->stream));
+  return IPM_OK;
+}
+
+ipm_status ipm_nccl_unique_id(void* h_id128) {
+  (void)h_id128;
+  return fail(IPM_ERR_UNSUPPORTED, "NCCL bootstrap not built in this library version");
+}
+
+ipm_status ipm_enable_timing(ipm_ctx* c, int32_t on) {
+  if (!c) return fail(IPM_ERR_ARG, "null ctx");
+  c->timing = on != 0;
+  return IPM_OK;
+}
+
+ipm_status ipm_last_kernel_ms(ipm_ctx* c, float* dual_ms, float* flux_ms) {
+  if (!c) return fail(IPM_ERR_ARG, "null ctx");
+  if (!c->timing) return fail(IPM_ERR_ARG, "timing not enabled");
+  CUDA_OK(cudaEventSynchronize(c->ev[3]));
+  if (dual_ms) CUDA_OK(cudaEventElapsedTime(dual_ms, c->ev[0], c->ev[1]));
+  if (flux_ms) CUDA_OK(cudaEventElapsedTime(flux_ms, c->ev[2], c->ev[3]));
+  return IPM_OK;
+}
+
+}  // extern "C"

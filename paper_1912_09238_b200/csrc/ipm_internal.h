@@ -1,0 +1,111 @@
+// ipm_internal.h — internal structures shared by the libipm host code and kernels.
+#pragma once
+#include <cstdint>
+
+namespace ipm {
+
+struct ClParams {
+  double gamma, umin, umax;
+};
+
+// Basis / quadrature tables as seen by the kernels (device pointers).
+//   PhiT  [N][QP]  phi_i(xi_k)           (QP = Q rounded up to an odd stride: bank spread)
+//   WPhiT [N][QP]  omega_k phi_i(xi_k)
+struct Tables {
+  const double* PhiT;
+  const double* WPhiT;
+  const double* omega;
+  const int32_t* deg;  // [N] total degree |i|
+  int N, Q, QP, p;
+};
+
+// Local mesh: owned cells, face tables (F faces per cell)
+//   nbr  [cells][F]  >= 0: cell index into the node-state buffer (owned or halo slot),
+//                    < 0: boundary, tag = -1 - nbr
+//   nrm  [cells][F][2] outward unit normal (tri only)
+//   coef [cells][F]  |e| / |Omega_j|
+struct Mesh {
+  int kind, F;
+  int64_t cells;
+  const int32_t* nbr;
+  const double* nrm;
+  const double* coef;
+  const double* area;      // [cells]
+  const double* rate_geo;  // [cells] tri: perimeter / area
+  double inv_dx, inv_dy;   // 1D / cartesian
+  const double* ghost;     // [4][Q][m] STATE boundary node states
+  int bc_kind[4];
+};
+
+struct Newton {
+  double tau, armijo_c;
+  int max_newton, max_halvings;
+  int mode;
+};
+
+struct Adapt {
+  int n_levels;
+  int Nl[8];
+  int Nprev0;  // basis size of degree level_M[0]-1 (indicator band at the lowest level)
+  double delta_dec, delta_inc;
+};
+
+// Device scalars of one step (ctx-owned).
+struct StepScalars {
+  unsigned long long rate_bits;  // max over nodes of the CFL rate (as ordered bits of a double >= 0)
+  double dt, t, residual;
+  unsigned long long newton_iters, failed;
+  int worst, work_counter, work_counter2, pad;
+};
+
+struct DualLaunch {
+  const double* uhat;
+  double* lam;
+  int32_t* iters;
+  int32_t* status;
+  double* crit;
+  double* uq;            // [cells][Q][m] node states at the final iterate (nullable)
+  const int32_t* level;  // nullable
+  int32_t* level_new;    // nullable
+  int64_t cells;
+  int mode;
+  int want_rate;
+};
+
+struct FluxLaunch {
+  const double* uq;  // [cells + halo][Q][m]
+  const double* uhat_old;
+  double* uhat_new;
+  const int32_t* level_new;  // nullable: projection level per cell
+  int update_form;
+  double cfl;
+};
+
+// Everything a launcher needs.
+struct KernelCtx {
+  Tables T;
+  Mesh mesh;
+  Newton nw;
+  Adapt ad;
+  ClParams cl;
+  int closure, flux, m;
+  StepScalars* sc;  // device
+  void* stream;     // cudaStream_t
+  int sm_count;
+  size_t smem_optin;
+};
+
+// launchers (ipm_kernels.cu); return 0 on success, else a cudaError_t / -1 unsupported
+int launch_step_begin(const KernelCtx& k, double rate0);
+int launch_dual(const KernelCtx& k, const DualLaunch& a);
+int launch_dt(const KernelCtx& k, double t_end, double dt_fixed, double cfl);
+int launch_flux(const KernelCtx& k, const FluxLaunch& a);
+int launch_project_ic(const KernelCtx& k, const double* d_region /*[R][Q][m]*/, const double* d_split /*[Q][2]*/,
+                      int ic_kind, int nx, double x0, double y0, double dx, double dy, const int32_t* level,
+                      double* uhat);
+int launch_warm_start(const KernelCtx& k, const double* uhat, double* lam);
+// node pass: uhat = h(lambda) (nullable), node states uq (nullable), CFL rate into sc
+int launch_nodes(const KernelCtx& k, const double* lam, double* uhat, double* uq);
+int launch_stress(const KernelCtx& k, const double* base, const double* z, double rel, double abs_, double* lam);
+
+}  // namespace ipm

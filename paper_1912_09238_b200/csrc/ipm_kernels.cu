@@ -1,0 +1,848 @@
+// ipm_kernels.cu — sm_100a kernels of the IPM hot path (fp64).
+//
+//   k_dual_warp   one warp per spatial cell, persistent CTAs pulling cells from an atomic queue
+//                 (Newton counts differ from cell to cell).  Per iteration:
+//                   Lambda_k = Phi lambda            (lanes over nodes k)
+//                   u_k = u_s(Lambda_k), J_k = grad u_s(Lambda_k), s_*(Lambda_k)
+//                   g = Phi^T (omega o u) - uhat     (lanes over outputs (i,a))
+//                   H_{(i,a),(j,b)} = sum_k omega_k phi_ki phi_kj J_ab,k   (lanes over pairs i<=j)
+//                   packed-lower Cholesky of H in shared memory, d = -H^{-1} g
+//                   Armijo backtracking on L (reading 3'), trial = next iterate's node data
+//                 epilogue: lambda, iteration count, status, node states u_k (for the flux),
+//                 CFL rate, refinement level.
+//   k_flux_warp   one warp per cell: kinetic flux at every node of every face (PAPER.md:144-146,
+//                 460-462), projection Phi^T(omega o .) and the conservative / c-form update.
+//   small kernels: step begin, dt, IC projection, warm start, h(lambda), stress duals.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "ipm_device.cuh"
+#include "ipm_internal.h"
+
+namespace ipm {
+
+// ------------------------------------------------------------------------------------------------
+// geometry of the per-warp shared-memory workspace of the dual kernel
+// ------------------------------------------------------------------------------------------------
+template <int MS>
+struct DualLayout {
+  static constexpr int MM = MS * (MS + 1) / 2;
+  static constexpr int NS = ((MS + MM) % 2 == 0) ? MS + MM + 1 : MS + MM;  // odd node stride
+  static __host__ __device__ int per_warp(int N, int Q) {
+    const int n = N * MS;
+    int w = 5 * n + Q * NS + n * (n + 1) / 2;
+    return (w + 1) & ~1;  // keep 16-byte alignment between warps
+  }
+  static __host__ __device__ int tables(int N, int QP) { return 2 * N * QP; }
+};
+
+__device__ __forceinline__ int packed(int r, int c) { return r * (r + 1) / 2 + c; }  // r >= c
+
+// node pass: Lambda = Phi lam, closure at every node -> nb, returns admissibility (warp-uniform),
+// s1 = sum_k omega_k s_*(Lambda_k), s2 = sum_k omega_k |s_*(Lambda_k)|
+template <int CL, int MS>
+__device__ __forceinline__ bool warp_eval(const double* __restrict__ lamv, int Nl, const double* __restrict__ sPhiT,
+                                          int QP, const double* __restrict__ omega, int Q, double* __restrict__ nb,
+                                          const ClParams& cp, double& s1, double& s2, int lane) {
+  using L = DualLayout<MS>;
+  bool ok = true;
+  double a1 = 0.0, a2 = 0.0;
+  for (int k = lane; k < Q; k += 32) {
+    double Lam[MS];
+#pragma unroll
+    for (int a = 0; a < MS; ++a) Lam[a] = 0.0;
+    for (int i = 0; i < Nl; ++i) {
+      const double ph = sPhiT[i * QP + k];
+#pragma unroll
+      for (int a = 0; a < MS; ++a) Lam[a] = fma(lamv[i * MS + a], ph, Lam[a]);
+    }
+    double u[MS], J[L::MM], ss;
+    const bool okk = Closure<CL, MS>::eval(Lam, u, J, ss, cp);
+    ok = ok && okk;
+    double* row = nb + k * L::NS;
+#pragma unroll
+    for (int a = 0; a < MS; ++a) row[a] = u[a];
+#pragma unroll
+    for (int q = 0; q < L::MM; ++q) row[MS + q] = J[q];
+    const double w = omega[k];
+    a1 = fma(w, ss, a1);
+    a2 = fma(w, fabs(ss), a2);
+  }
+  ok = __all_sync(FULL_MASK, ok);
+  s1 = warp_sum(a1);
+  s2 = warp_sum(a2);
+  __syncwarp();
+  return ok && isfinite(s1);
+}
+
+// g = Phi^T(omega o u) - uhat ; returns crit = sum_a ||g_{.,a}||_2 (warp-uniform)
+template <int MS>
+__device__ __forceinline__ double warp_grad(const double* __restrict__ nb, const double* __restrict__ sWPhiT, int QP,
+                                            int Q, int Nl, const double* __restrict__ uh, double* __restrict__ g,
+                                            int lane) {
+  using L = DualLayout<MS>;
+  const int n = Nl * MS;
+  double part[MS];
+#pragma unroll
+  for (int a = 0; a < MS; ++a) part[a] = 0.0;
+  for (int r = lane; r < n; r += 32) {
+    const int i = r / MS, a = r - i * MS;
+    const double* wp = sWPhiT + i * QP;
+    double s = 0.0;
+    for (int k = 0; k < Q; ++k) s = fma(wp[k], nb[k * L::NS + a], s);
+    const double gr = s - uh[r];
+    g[r] = gr;
+#pragma unroll
+    for (int b = 0; b < MS; ++b)
+      if (b == a) part[b] = fma(gr, gr, part[b]);
+  }
+  double crit = 0.0;
+#pragma unroll
+  for (int a = 0; a < MS; ++a) crit += sqrt(warp_sum(part[a]));
+  __syncwarp();
+  return crit;
+}
+
+// H (packed lower, n x n) = sum_k omega_k J_k (x) phi_k phi_k^T
+template <int MS>
+__device__ __forceinline__ void warp_hessian(const double* __restrict__ nb, const double* __restrict__ sPhiT,
+                                             const double* __restrict__ sWPhiT, int QP, int Q, int Nl,
+                                             double* __restrict__ H, int lane) {
+  using L = DualLayout<MS>;
+  const int NP = Nl * (Nl + 1) / 2;
+  for (int pp = lane; pp < NP; pp += 32) {
+    int j = (int)((sqrtf(8.0f * pp + 1.0f) - 1.0f) * 0.5f);
+    while (j * (j + 1) / 2 > pp) --j;
+    while ((j + 1) * (j + 2) / 2 <= pp) ++j;
+    const int i = pp - j * (j + 1) / 2;  // i <= j
+    double acc[L::MM];
+#pragma unroll
+    for (int q = 0; q < L::MM; ++q) acc[q] = 0.0;
+    const double* wi = sWPhiT + i * QP;
+    const double* pj = sPhiT + j * QP;
+    for (int k = 0; k < Q; ++k) {
+      const double f = wi[k] * pj[k];
+      const double* Jk = nb + k * L::NS + MS;
+#pragma unroll
+      for (int q = 0; q < L::MM; ++q) acc[q] = fma(f, Jk[q], acc[q]);
+    }
+#pragma unroll
+    for (int a = 0; a < MS; ++a)
+#pragma unroll
+      for (int b = 0; b < MS; ++b) {
+        const double v = acc[a <= b ? sym_idx<MS>(a, b) : sym_idx<MS>(b, a)];
+        const int r1 = i * MS + a, r2 = j * MS + b;
+        if (r1 >= r2)
+          H[packed(r1, r2)] = v;
+        else
+          H[packed(r2, r1)] = v;
+      }
+  }
+  __syncwarp();
+}
+
+// in-place Cholesky of packed-lower H, then d = -H^{-1} g.  Returns false on a non-positive pivot.
+__device__ __forceinline__ bool warp_chol_solve(double* __restrict__ H, int n, const double* __restrict__ g,
+                                                double* __restrict__ d, int lane) {
+  for (int k = 0; k < n; ++k) {
+    const double piv = H[packed(k, k)];
+    if (!(piv > 0.0) || !isfinite(piv)) return false;  // warp-uniform (same address)
+    const double Lkk = sqrt(piv);
+    __syncwarp();
+    if (lane == 0) H[packed(k, k)] = Lkk;
+    for (int i = k + 1 + lane; i < n; i += 32) H[packed(i, k)] = H[packed(i, k)] / Lkk;
+    __syncwarp();
+    for (int i = k + 1 + lane; i < n; i += 32) {
+      const double lik = H[packed(i, k)];
+      double* row = H + packed(i, 0);
+      for (int jj = k + 1; jj <= i; ++jj) row[jj] = fma(-lik, H[packed(jj, k)], row[jj]);
+    }
+    __syncwarp();
+  }
+  for (int r = lane; r < n; r += 32) d[r] = -g[r];
+  __syncwarp();
+  for (int k = 0; k < n; ++k) {  // L y = -g
+    const double yk = d[k] / H[packed(k, k)];
+    __syncwarp();
+    if (lane == 0) d[k] = yk;
+    for (int i = k + 1 + lane; i < n; i += 32) d[i] = fma(-H[packed(i, k)], yk, d[i]);
+    __syncwarp();
+  }
+  for (int k = n - 1; k >= 0; --k) {  // L^T d = y
+    const double dk = d[k] / H[packed(k, k)];
+    __syncwarp();
+    if (lane == 0) d[k] = dk;
+    for (int i = lane; i < k; i += 32) d[i] = fma(-H[packed(k, i)], dk, d[i]);
+    __syncwarp();
+  }
+  return true;
+}
+
+__device__ __forceinline__ double warp_dot(const double* a, const double* b, int n, int lane) {
+  double s = 0.0;
+  for (int r = lane; r < n; r += 32) s = fma(a[r], b[r], s);
+  return warp_sum(s);
+}
+__device__ __forceinline__ double warp_absdot(const double* a, const double* b, int n, int lane) {
+  double s = 0.0;
+  for (int r = lane; r < n; r += 32) s += fabs(a[r] * b[r]);
+  return warp_sum(s);
+}
+
+// CFL rate of a node state (reading 15)
+template <int CL, int MS>
+__device__ __forceinline__ double node_rate(const double* u, const Mesh& M, int64_t cell, double gamma) {
+  if constexpr (MS == 1) {
+    return fabs(u[0]) * M.inv_dx;
+  } else {
+    if (M.kind == MK_1D) return Euler<MS>::speed_dir(u, 0, gamma) * M.inv_dx;
+    if (M.kind == MK_CART)
+      return Euler<MS>::speed_dir(u, 0, gamma) * M.inv_dx + Euler<MS>::speed_dir(u, 1, gamma) * M.inv_dy;
+    return Euler<MS>::speed_norm(u, gamma) * M.rate_geo[cell];
+  }
+}
+
+struct DualParams {
+  Tables T;
+  Mesh mesh;
+  Newton nw;
+  Adapt ad;
+  ClParams cl;
+  DualLaunch a;
+  StepScalars* sc;
+};
+
+template <int CL, int MS>
+__global__ void __launch_bounds__(512) k_dual_warp(DualParams P) {
+  using Lay = DualLayout<MS>;
+  extern __shared__ __align__(16) double sm[];
+  const int N = P.T.N, Q = P.T.Q, QP = P.T.QP;
+  double* sPhiT = sm;
+  double* sWPhiT = sm + N * QP;
+  for (int t = threadIdx.x; t < N * QP; t += blockDim.x) {
+    sPhiT[t] = P.T.PhiT[t];
+    sWPhiT[t] = P.T.WPhiT[t];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nmax = N * MS;
+  double* base = sm + Lay::tables(N, QP) + (size_t)warp * Lay::per_warp(N, Q);
+  double* lam = base;
+  double* lt = lam + nmax;
+  double* uh = lt + nmax;
+  double* g = uh + nmax;
+  double* dd = g + nmax;
+  double* nb = dd + nmax;
+  double* H = nb + Q * Lay::NS;
+
+  const double* __restrict__ omega = P.T.omega;
+  long long my_iters = 0, my_failed = 0;
+  int my_worst = 0;
+  double my_rate = 0.0;
+  const DualLaunch& A = P.a;
+
+  for (;;) {
+    int64_t cell = 0;
+    if (lane == 0) cell = atomicAdd(&P.sc->work_counter, 1);
+    cell = __shfl_sync(FULL_MASK, cell, 0);
+    if (cell >= A.cells) break;
+    const int lvl = A.level ? A.level[cell] : 0;
+    const int Nl = (P.ad.n_levels > 0) ? P.ad.Nl[lvl] : N;
+    const int n = Nl * MS;
+    const double* gu = A.uhat + cell * nmax;
+    double* gl = A.lam + cell * nmax;
+    for (int r = lane; r < n; r += 32) {
+      uh[r] = gu[r];
+      lam[r] = gl[r];
+    }
+    __syncwarp();
+
+    int status = 0, l = 0;
+    double s1, s2, crit = INFINITY;
+    bool nb_is_lam = warp_eval<CL, MS>(lam, Nl, sPhiT, QP, omega, Q, nb, P.cl, s1, s2, lane);
+    if (!nb_is_lam) {
+      status = 4;  // INADMISSIBLE
+    } else {
+      crit = warp_grad<MS>(nb, sWPhiT, QP, Q, Nl, uh, g, lane);
+      double L0 = s1 - warp_dot(lam, uh, n, lane);
+      double scale = s2 + warp_absdot(lam, uh, n, lane);
+      for (;;) {
+        if (crit < P.nw.tau) break;
+        if (P.nw.mode == 1 && l == 1) break;
+        if (l == P.nw.max_newton) {
+          status = 1;
+          break;
+        }
+        warp_hessian<MS>(nb, sPhiT, sWPhiT, QP, Q, Nl, H, lane);
+        if (!warp_chol_solve(H, n, g, dd, lane)) {
+          status = 2;
+          break;
+        }
+        const double slope = warp_dot(g, dd, n, lane);
+        double alpha = 1.0;
+        bool accepted = false;
+        for (int h = 0; h <= P.nw.max_halvings; ++h) {
+          for (int r = lane; r < n; r += 32) lt[r] = lam[r] + alpha * dd[r];
+          __syncwarp();
+          double t1, t2;
+          const bool okt = warp_eval<CL, MS>(lt, Nl, sPhiT, QP, omega, Q, nb, P.cl, t1, t2, lane);
+          nb_is_lam = false;
+          if (okt) {
+            const double Lt = t1 - warp_dot(lt, uh, n, lane);
+            if (Lt <= L0 + P.nw.armijo_c * alpha * slope + 1e-12 * scale) {
+              const double sct = t2 + warp_absdot(lt, uh, n, lane);
+              crit = warp_grad<MS>(nb, sWPhiT, QP, Q, Nl, uh, g, lane);
+              for (int r = lane; r < n; r += 32) lam[r] = lt[r];
+              __syncwarp();
+              nb_is_lam = true;
+              L0 = Lt;
+              scale = sct;
+              accepted = true;
+              break;
+            }
+          }
+          alpha *= 0.5;
+        }
+        if (!accepted) {
+          status = 3;
+          break;
+        }
+        ++l;
+      }
+    }
+    // ---- epilogue ------------------------------------------------------------------------------
+    if (!nb_is_lam && status != 4) {
+      double t1, t2;
+      warp_eval<CL, MS>(lam, Nl, sPhiT, QP, omega, Q, nb, P.cl, t1, t2, lane);
+    }
+    int Nnew = Nl;
+    if (P.ad.n_levels > 0 && A.level_new) {
+      // S_l on the first state of h = g + uhat at level l (readings 19, 20)
+      const int Nprev = lvl > 0 ? P.ad.Nl[lvl - 1] : P.ad.Nprev0;
+      double num = 0.0, den = 0.0;
+      for (int i = lane; i < Nl; i += 32) {
+        const double h = g[i * MS] + uh[i * MS];
+        den = fma(h, h, den);
+        if (i >= Nprev) num = fma(h, h, num);
+      }
+      num = warp_sum(num);
+      den = warp_sum(den);
+      const double S = den > 0.0 ? num / den : 0.0;
+      int nl = lvl;
+      if (status == 0 || P.nw.mode == 1) {
+        if (S < P.ad.delta_dec && lvl > 0)
+          nl = lvl - 1;
+        else if (S > P.ad.delta_inc && lvl < P.ad.n_levels - 1)
+          nl = lvl + 1;
+      }
+      Nnew = P.ad.Nl[nl];
+      if (lane == 0) A.level_new[cell] = nl;
+    }
+    // lambda zero-padded / truncated to the new level (the node states keep the old level)
+    for (int r = lane; r < nmax; r += 32) gl[r] = (r < Nnew * MS) ? lam[r] : 0.0;
+    if (lane == 0) {
+      if (A.iters) A.iters[cell] = l;
+      if (A.status) A.status[cell] = status;
+      if (A.crit) A.crit[cell] = crit;
+    }
+    if (status != 4) {
+      double cr = 0.0;
+      for (int k = lane; k < Q; k += 32) {
+        const double* u = nb + k * Lay::NS;
+        if (A.uq) {
+          double* o = A.uq + (cell * Q + k) * MS;
+#pragma unroll
+          for (int a = 0; a < MS; ++a) o[a] = u[a];
+        }
+        if (A.want_rate) cr = fmax(cr, node_rate<CL, MS>(u, P.mesh, cell, P.cl.gamma));
+      }
+      my_rate = fmax(my_rate, cr);
+    }
+    my_iters += l;
+    if (status != 0) {
+      my_failed += 1;
+      my_worst = max(my_worst, status);
+    }
+    __syncwarp();
+  }
+  my_rate = warp_max(my_rate);
+  if (lane == 0) {
+    if (A.want_rate) atomicMax(&P.sc->rate_bits, (unsigned long long)__double_as_longlong(my_rate));
+    if (my_iters) atomicAdd(&P.sc->newton_iters, (unsigned long long)my_iters);
+    if (my_failed) atomicAdd(&P.sc->failed, (unsigned long long)my_failed);
+    if (my_worst) atomicMax(&P.sc->worst, my_worst);
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// flux kernel (variant B: node states from the dual kernel)
+// ------------------------------------------------------------------------------------------------
+struct FluxParams {
+  Tables T;
+  Mesh mesh;
+  ClParams cl;
+  Adapt ad;
+  FluxLaunch a;
+  StepScalars* sc;
+};
+
+template <int FX, int MS, int MK>
+__global__ void __launch_bounds__(256) k_flux_warp(FluxParams P) {
+  extern __shared__ __align__(16) double sm[];
+  const int N = P.T.N, Q = P.T.Q, QP = P.T.QP;
+  double* sWPhiT = sm;
+  for (int t = threadIdx.x; t < N * QP; t += blockDim.x) sWPhiT[t] = P.T.WPhiT[t];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  double* q = sm + N * QP + (size_t)warp * (Q * MS + 1);
+  const int nmax = N * MS;
+  const double dt = P.sc->dt;
+  const double gam = P.cl.gamma;
+  const int F = P.mesh.F;
+  const FluxLaunch& A = P.a;
+  double my_res = 0.0;
+  const int64_t total_warps = (int64_t)gridDim.x * nw;
+  for (int64_t cell = (int64_t)blockIdx.x * nw + warp; cell < P.mesh.cells; cell += total_warps) {
+    for (int k = lane; k < Q; k += 32) {
+      double uj[MS], r[MS], gneg[MS];
+      const double* src = A.uq + (cell * Q + k) * MS;
+#pragma unroll
+      for (int a = 0; a < MS; ++a) {
+        uj[a] = src[a];
+        r[a] = 0.0;
+      }
+      for (int f = 0; f < F; ++f) {
+        const int nbc = P.mesh.nbr[cell * F + f];
+        double un[MS];
+        double nv[2];
+        if (MK == MK_TRI) {
+          nv[0] = P.mesh.nrm[(cell * F + f) * 2];
+          nv[1] = P.mesh.nrm[(cell * F + f) * 2 + 1];
+        } else {
+          nv[0] = (f >> 1) == 0 ? 1.0 : 0.0;
+          nv[1] = (f >> 1) == 1 ? 1.0 : 0.0;
+        }
+        if (nbc >= 0) {
+          const double* s2 = A.uq + ((int64_t)nbc * Q + k) * MS;
+#pragma unroll
+          for (int a = 0; a < MS; ++a) un[a] = s2[a];
+        } else {
+          const int tag = -1 - nbc;
+          const int kind = P.mesh.bc_kind[tag];
+          if (kind == 1) {
+            const double* gs = P.mesh.ghost + ((int64_t)tag * Q + k) * MS;
+#pragma unroll
+            for (int a = 0; a < MS; ++a) un[a] = gs[a];
+          } else if (kind == 2 && MS > 1) {
+            // slip wall: mirror the normal momentum about the outward normal
+            const double sgn = (MK == MK_TRI || (f & 1)) ? 1.0 : -1.0;
+            const double on[2] = {nv[0] * sgn, nv[1] * sgn};
+            double mn = 0.0;
+#pragma unroll
+            for (int d = 0; d < MS - 2; ++d) mn += uj[1 + d] * on[d];
+            un[0] = uj[0];
+#pragma unroll
+            for (int d = 0; d < MS - 2; ++d) un[1 + d] = uj[1 + d] - 2.0 * mn * on[d];
+            un[MS - 1] = uj[MS - 1];
+          } else {
+#pragma unroll
+            for (int a = 0; a < MS; ++a) un[a] = uj[a];
+          }
+        }
+        const double cf = P.mesh.coef[cell * F + f];
+        if (MK == MK_TRI) {
+          double gf[MS];
+          NumFlux<FX, MS>::g(uj, un, nv, gam, 0.0, gf);
+#pragma unroll
+          for (int a = 0; a < MS; ++a) r[a] = fma(cf, gf[a], r[a]);
+        } else if ((f & 1) == 0) {
+          // paper form per direction: (g(u_j, u_{j+1}) - g(u_{j-1}, u_j)) / dx;
+          // the difference is formed before scaling so a uniform state gives exactly zero
+          NumFlux<FX, MS>::g(un, uj, nv, gam, 1.0 / (cf * dt), gneg);
+        } else {
+          double gpos[MS];
+          NumFlux<FX, MS>::g(uj, un, nv, gam, 1.0 / (cf * dt), gpos);
+#pragma unroll
+          for (int a = 0; a < MS; ++a) r[a] += (gpos[a] - gneg[a]) * cf;
+        }
+      }
+      double* qk = q + k * MS;
+      if (A.update_form == 1) {
+#pragma unroll
+        for (int a = 0; a < MS; ++a) qk[a] = uj[a] - dt * r[a];
+      } else {
+#pragma unroll
+        for (int a = 0; a < MS; ++a) qk[a] = r[a];
+      }
+    }
+    __syncwarp();
+    const int Nnew = (P.ad.n_levels > 0 && A.level_new) ? P.ad.Nl[A.level_new[cell]] : N;
+    const double* uo = A.uhat_old + cell * nmax;
+    double* un_ = A.uhat_new + cell * nmax;
+    for (int rr = lane; rr < nmax; rr += 32) {
+      const int i = rr / MS, a = rr - i * MS;
+      const double old = uo[rr];  // uhat_new may alias uhat_old (only this cell's entries are read)
+      double out = 0.0;
+      if (i < Nnew) {
+        const double* wp = sWPhiT + i * QP;
+        double s = 0.0;
+        for (int k = 0; k < Q; ++k) s = fma(wp[k], q[k * MS + a], s);
+        out = (A.update_form == 1) ? s : old - dt * s;
+      }
+      un_[rr] = out;
+      if (rr == 0) my_res += P.mesh.area[cell] * fabs(out - old);
+    }
+    __syncwarp();
+  }
+  my_res = warp_sum(my_res);
+  if (lane == 0 && my_res != 0.0) atomicAdd(&P.sc->residual, my_res);
+}
+
+// ------------------------------------------------------------------------------------------------
+// small kernels
+// ------------------------------------------------------------------------------------------------
+__global__ void k_step_begin(StepScalars* sc, double rate0) {
+  sc->rate_bits = (unsigned long long)__double_as_longlong(rate0);
+  sc->residual = 0.0;
+  sc->newton_iters = 0;
+  sc->failed = 0;
+  sc->worst = 0;
+  sc->work_counter = 0;
+  sc->work_counter2 = 0;
+}
+
+// dt = min(cfl / rate, t_end - t) (t_end <= 0: no cap), then t += dt
+__global__ void k_dt(StepScalars* sc, double t_end, double dt_fixed, double cfl) {
+  double dt;
+  if (dt_fixed > 0.0) {
+    dt = dt_fixed;
+  } else {
+    const double rate = __longlong_as_double((long long)sc->rate_bits);
+    dt = cfl / rate;
+    if (t_end > 0.0) dt = fmin(dt, t_end - sc->t);
+  }
+  sc->dt = dt;
+  sc->t = sc->t + dt;
+}
+
+// IC projection: uhat_j = sum_k omega_k phi(xi_k) ubar_j(xi_k), exact cell averages of a
+// piecewise-constant IC at each node (Alg. 1 line 2; reading 17)
+template <int MS>
+__global__ void k_project_ic(Tables T, int64_t cells, const double* __restrict__ region,
+                             const double* __restrict__ split, int kind, int nx, double x0, double y0, double dx,
+                             double dy, const int32_t* __restrict__ level, Adapt ad, double* __restrict__ uhat) {
+  extern __shared__ __align__(16) double sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int Q = T.Q, N = T.N;
+  double* q = sm + warp * (Q * MS + 1);
+  for (int64_t cell = (int64_t)blockIdx.x * nw + warp; cell < cells; cell += (int64_t)gridDim.x * nw) {
+    for (int k = lane; k < Q; k += 32) {
+      double ub[MS];
+      if (kind == 0) {
+#pragma unroll
+        for (int a = 0; a < MS; ++a) ub[a] = region[(0 * Q + k) * MS + a];
+      } else if (kind == 1) {
+        const double xl = x0 + (double)cell * dx;
+        double fl = (split[k * 2] - xl) / dx;
+        fl = fmin(fmax(fl, 0.0), 1.0);
+#pragma unroll
+        for (int a = 0; a < MS; ++a)
+          ub[a] = fl * region[(0 * Q + k) * MS + a] + (1.0 - fl) * region[(1 * Q + k) * MS + a];
+      } else {
+        const int64_t ix = cell % nx, iy = cell / nx;
+        double fx = (split[k * 2] - (x0 + ix * dx)) / dx;
+        double fy = (split[k * 2 + 1] - (y0 + iy * dy)) / dy;
+        fx = fmin(fmax(fx, 0.0), 1.0);
+        fy = fmin(fmax(fy, 0.0), 1.0);
+        const double w0 = (1.0 - fx) * (1.0 - fy), w1 = fx * (1.0 - fy), w2 = fx * fy, w3 = (1.0 - fx) * fy;
+#pragma unroll
+        for (int a = 0; a < MS; ++a)
+          ub[a] = w0 * region[(0 * Q + k) * MS + a] + w1 * region[(1 * Q + k) * MS + a] +
+                  w2 * region[(2 * Q + k) * MS + a] + w3 * region[(3 * Q + k) * MS + a];
+      }
+#pragma unroll
+      for (int a = 0; a < MS; ++a) q[k * MS + a] = ub[a];
+    }
+    __syncwarp();
+    const int Nl = (ad.n_levels > 0 && level) ? ad.Nl[level[cell]] : N;
+    for (int r = lane; r < N * MS; r += 32) {
+      const int i = r / MS, a = r - i * MS;
+      double s = 0.0;
+      if (i < Nl)
+        for (int k = 0; k < Q; ++k) s = fma(T.WPhiT[i * T.QP + k], q[k * MS + a], s);
+      uhat[cell * N * MS + r] = s;
+    }
+    __syncwarp();
+  }
+}
+
+template <int CL, int MS>
+__global__ void k_warm_start(int64_t cells, int N, ClParams cp, const double* __restrict__ uhat,
+                             double* __restrict__ lam, StepScalars* sc) {
+  const int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (cell >= cells) return;
+  double u[MS], L[MS];
+#pragma unroll
+  for (int a = 0; a < MS; ++a) u[a] = uhat[cell * N * MS + a];
+  const bool ok = Closure<CL, MS>::grad_s(u, L, cp);
+  if (!ok) atomicMax(&sc->worst, 4);
+  for (int r = 0; r < N * MS; ++r) lam[cell * N * MS + r] = (r < MS) ? (ok ? L[r] : NAN) : 0.0;
+}
+
+// node pass for given duals (warp per cell): optional uhat = h(lambda), node states
+// u_s(lambda^T phi(xi_k)) and CFL rate
+template <int CL, int MS>
+__global__ void k_nodes(Tables T, Mesh mesh, ClParams cp, const double* __restrict__ lam_g, double* __restrict__ uhat,
+                        double* __restrict__ uq, StepScalars* sc) {
+  using Lay = DualLayout<MS>;
+  extern __shared__ __align__(16) double sm[];
+  const int N = T.N, Q = T.Q, QP = T.QP;
+  double* sPhiT = sm;
+  double* sWPhiT = sm + N * QP;
+  for (int t = threadIdx.x; t < N * QP; t += blockDim.x) {
+    sPhiT[t] = T.PhiT[t];
+    sWPhiT[t] = T.WPhiT[t];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  double* lam = sm + 2 * N * QP + (size_t)warp * (N * MS + Q * Lay::NS + 1);
+  double* nb = lam + N * MS;
+  double my_rate = 0.0;
+  int bad = 0;
+  for (int64_t cell = (int64_t)blockIdx.x * nw + warp; cell < mesh.cells; cell += (int64_t)gridDim.x * nw) {
+    for (int r = lane; r < N * MS; r += 32) lam[r] = lam_g[cell * N * MS + r];
+    __syncwarp();
+    double s1, s2;
+    if (!warp_eval<CL, MS>(lam, N, sPhiT, QP, T.omega, Q, nb, cp, s1, s2, lane)) bad = 1;
+    if (uhat) {
+      double* out = uhat + cell * N * MS;
+      for (int r = lane; r < N * MS; r += 32) {
+        const int i = r / MS, a = r - i * MS;
+        double s = 0.0;
+        for (int k = 0; k < Q; ++k) s = fma(sWPhiT[i * QP + k], nb[k * Lay::NS + a], s);
+        out[r] = s;
+      }
+    }
+    for (int k = lane; k < Q; k += 32) {
+      const double* u = nb + k * Lay::NS;
+      if (uq) {
+        double* o = uq + (cell * Q + k) * MS;
+#pragma unroll
+        for (int a = 0; a < MS; ++a) o[a] = u[a];
+      }
+      my_rate = fmax(my_rate, node_rate<CL, MS>(u, mesh, cell, cp.gamma));
+    }
+    __syncwarp();
+  }
+  my_rate = warp_max(my_rate);
+  if (lane == 0 && sc) {
+    atomicMax(&sc->rate_bits, (unsigned long long)__double_as_longlong(my_rate));
+    if (bad) atomicMax(&sc->worst, 4);
+  }
+}
+
+// stress duals: lambda_0 = grad s(base); higher (rel|l0| + abs) 2^-|i| z; Euler: scale
+// higher modes so that max_k sum_{i>=1} lambda_{i,E} phi_i(xi_k) <= |lambda_{0,E}|/2
+template <int CL, int MS>
+__global__ void k_stress(Tables T, int64_t cells, ClParams cp, const double* __restrict__ basev,
+                         const double* __restrict__ z, double rel, double abs_, double* __restrict__ lam) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int N = T.N, Q = T.Q;
+  for (int64_t cell = (int64_t)blockIdx.x * nw + warp; cell < cells; cell += (int64_t)gridDim.x * nw) {
+    double u[MS], L0[MS];
+#pragma unroll
+    for (int a = 0; a < MS; ++a) u[a] = basev[cell * MS + a];
+    Closure<CL, MS>::grad_s(u, L0, cp);
+    double* out = lam + cell * N * MS;
+    for (int r = lane; r < N * MS; r += 32) {
+      const int i = r / MS, a = r - i * MS;
+      double v;
+      if (i == 0) {
+        v = L0[a];
+      } else {
+        double amp = 0.0;
+#pragma unroll
+        for (int b = 0; b < MS; ++b)
+          if (b == a) amp = rel * fabs(L0[b]) + abs_;
+        v = amp * exp2(-(double)T.deg[i]) * z[cell * N * MS + r];
+      }
+      out[r] = v;
+    }
+    __syncwarp();
+    if (CL == CL_EULER) {
+      double mx = -INFINITY;
+      for (int k = lane; k < Q; k += 32) {
+        double s = 0.0;
+        for (int i = 1; i < N; ++i) s = fma(T.PhiT[i * T.QP + k], out[i * MS + MS - 1], s);
+        mx = fmax(mx, s);
+      }
+      mx = warp_max(mx);
+      const double lim = 0.5 * fabs(L0[MS - 1]);
+      if (mx > lim) {
+        const double f = lim / mx;
+        for (int r = MS + lane; r < N * MS; r += 32) out[r] *= f;
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// launchers and dispatch
+// ------------------------------------------------------------------------------------------------
+static inline cudaStream_t S(const KernelCtx& k) { return (cudaStream_t)k.stream; }
+
+int launch_step_begin(const KernelCtx& k, double rate0) {
+  k_step_begin<<<1, 1, 0, S(k)>>>(k.sc, rate0);
+  return (int)cudaGetLastError();
+}
+
+int launch_dt(const KernelCtx& k, double t_end, double dt_fixed, double cfl) {
+  k_dt<<<1, 1, 0, S(k)>>>(k.sc, t_end, dt_fixed, cfl);
+  return (int)cudaGetLastError();
+}
+
+template <int CL, int MS>
+static int dual_impl(const KernelCtx& k, const DualLaunch& a) {
+  using Lay = DualLayout<MS>;
+  const size_t tab = (size_t)Lay::tables(k.T.N, k.T.QP) * 8, pw = (size_t)Lay::per_warp(k.T.N, k.T.Q) * 8;
+  if (tab + pw > k.smem_optin) return -1;
+  int warps = (int)((k.smem_optin - tab) / pw);
+  warps = warps > 16 ? 16 : warps;
+  const size_t smem = tab + warps * pw;
+  auto kern = k_dual_warp<CL, MS>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem);
+  if (per_sm < 1) per_sm = 1;
+  int64_t want = (a.cells + warps - 1) / warps;
+  int grid = (int)std::min<int64_t>(want, (int64_t)k.sm_count * per_sm);
+  if (grid < 1) grid = 1;
+  DualParams P{k.T, k.mesh, k.nw, k.ad, k.cl, a, k.sc};
+  kern<<<grid, warps * 32, smem, S(k)>>>(P);
+  return (int)cudaGetLastError();
+}
+
+int launch_dual(const KernelCtx& k, const DualLaunch& a) {
+  if (a.cells == 0) return 0;
+  switch (k.closure * 10 + k.m) {
+    case CL_QUADRATIC * 10 + 1: return dual_impl<CL_QUADRATIC, 1>(k, a);
+    case CL_QUADRATIC * 10 + 3: return dual_impl<CL_QUADRATIC, 3>(k, a);
+    case CL_QUADRATIC * 10 + 4: return dual_impl<CL_QUADRATIC, 4>(k, a);
+    case CL_BARRIER * 10 + 1: return dual_impl<CL_BARRIER, 1>(k, a);
+    case CL_EULER * 10 + 3: return dual_impl<CL_EULER, 3>(k, a);
+    case CL_EULER * 10 + 4: return dual_impl<CL_EULER, 4>(k, a);
+  }
+  return -1;
+}
+
+template <int FX, int MS, int MK>
+static int flux_impl(const KernelCtx& k, const FluxLaunch& a) {
+  const int warps = 8;
+  const size_t smem = ((size_t)k.T.N * k.T.QP + warps * (k.T.Q * MS + 1)) * 8;
+  if (smem > k.smem_optin) return -1;
+  auto kern = k_flux_warp<FX, MS, MK>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t want = (k.mesh.cells + warps - 1) / warps;
+  int grid = (int)std::min<int64_t>(want, (int64_t)k.sm_count * per_sm * 4);
+  if (grid < 1) grid = 1;
+  FluxParams P{k.T, k.mesh, k.cl, k.ad, a, k.sc};
+  kern<<<grid, warps * 32, smem, S(k)>>>(P);
+  return (int)cudaGetLastError();
+}
+
+int launch_flux(const KernelCtx& k, const FluxLaunch& a) {
+  if (k.mesh.cells == 0) return 0;
+  const int key = (k.flux * 10 + k.m) * 10 + k.mesh.kind;
+  switch (key) {
+    case (FX_LF_GLOBAL * 10 + 1) * 10 + MK_1D: return flux_impl<FX_LF_GLOBAL, 1, MK_1D>(k, a);
+    case (FX_HLL * 10 + 3) * 10 + MK_1D: return flux_impl<FX_HLL, 3, MK_1D>(k, a);
+    case (FX_RUSANOV * 10 + 3) * 10 + MK_1D: return flux_impl<FX_RUSANOV, 3, MK_1D>(k, a);
+    case (FX_RUSANOV * 10 + 4) * 10 + MK_CART: return flux_impl<FX_RUSANOV, 4, MK_CART>(k, a);
+    case (FX_HLL * 10 + 4) * 10 + MK_CART: return flux_impl<FX_HLL, 4, MK_CART>(k, a);
+    case (FX_RUSANOV * 10 + 4) * 10 + MK_TRI: return flux_impl<FX_RUSANOV, 4, MK_TRI>(k, a);
+  }
+  return -1;
+}
+
+template <int MS>
+static int ic_impl(const KernelCtx& k, const double* region, const double* split, int kind, int nx, double x0,
+                   double y0, double dx, double dy, const int32_t* level, double* uhat) {
+  const int warps = 8;
+  const size_t smem = (size_t)warps * (k.T.Q * MS + 1) * 8;
+  auto kern = k_project_ic<MS>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t want = (k.mesh.cells + warps - 1) / warps;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)k.sm_count * 8));
+  kern<<<grid, warps * 32, smem, S(k)>>>(k.T, k.mesh.cells, region, split, kind, nx, x0, y0, dx, dy, level, k.ad,
+                                         uhat);
+  return (int)cudaGetLastError();
+}
+
+int launch_project_ic(const KernelCtx& k, const double* region, const double* split, int kind, int nx, double x0,
+                      double y0, double dx, double dy, const int32_t* level, double* uhat) {
+  switch (k.m) {
+    case 1: return ic_impl<1>(k, region, split, kind, nx, x0, y0, dx, dy, level, uhat);
+    case 3: return ic_impl<3>(k, region, split, kind, nx, x0, y0, dx, dy, level, uhat);
+    case 4: return ic_impl<4>(k, region, split, kind, nx, x0, y0, dx, dy, level, uhat);
+  }
+  return -1;
+}
+
+template <int CL, int MS>
+static int warm_impl(const KernelCtx& k, const double* uhat, double* lam) {
+  const int64_t n = k.mesh.cells;
+  k_warm_start<CL, MS><<<(unsigned)((n + 127) / 128), 128, 0, S(k)>>>(n, k.T.N, k.cl, uhat, lam, k.sc);
+  return (int)cudaGetLastError();
+}
+
+template <int CL, int MS>
+static int nodes_impl(const KernelCtx& k, const double* lam, double* uhat, double* uq) {
+  using Lay = DualLayout<MS>;
+  const int warps = 4;
+  const size_t smem = ((size_t)2 * k.T.N * k.T.QP + warps * (k.T.N * MS + k.T.Q * Lay::NS + 1)) * 8;
+  if (smem > k.smem_optin) return -1;
+  auto kern = k_nodes<CL, MS>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t want = (k.mesh.cells + warps - 1) / warps;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)k.sm_count * 4));
+  kern<<<grid, warps * 32, smem, S(k)>>>(k.T, k.mesh, k.cl, lam, uhat, uq, k.sc);
+  return (int)cudaGetLastError();
+}
+
+template <int CL, int MS>
+static int stress_impl(const KernelCtx& k, const double* base, const double* z, double rel, double abs_,
+                       double* lam) {
+  const int warps = 8;
+  const int64_t want = (k.mesh.cells + warps - 1) / warps;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)k.sm_count * 16));
+  k_stress<CL, MS><<<grid, warps * 32, 0, S(k)>>>(k.T, k.mesh.cells, k.cl, base, z, rel, abs_, lam);
+  return (int)cudaGetLastError();
+}
+
+#define IPM_DISPATCH_CL(FN, ...)                                                \
+  switch (k.closure * 10 + k.m) {                                               \
+    case CL_QUADRATIC * 10 + 1: return FN<CL_QUADRATIC, 1>(k, __VA_ARGS__);     \
+    case CL_QUADRATIC * 10 + 3: return FN<CL_QUADRATIC, 3>(k, __VA_ARGS__);     \
+    case CL_QUADRATIC * 10 + 4: return FN<CL_QUADRATIC, 4>(k, __VA_ARGS__);     \
+    case CL_BARRIER * 10 + 1: return FN<CL_BARRIER, 1>(k, __VA_ARGS__);         \
+    case CL_EULER * 10 + 3: return FN<CL_EULER, 3>(k, __VA_ARGS__);             \
+    case CL_EULER * 10 + 4: return FN<CL_EULER, 4>(k, __VA_ARGS__);             \
+  }                                                                             \
+  return -1;
+
+int launch_warm_start(const KernelCtx& k, const double* uhat, double* lam) { IPM_DISPATCH_CL(warm_impl, uhat, lam) }
+int launch_nodes(const KernelCtx& k, const double* lam, double* uhat, double* uq) {
+  IPM_DISPATCH_CL(nodes_impl, lam, uhat, uq)
+}
+int launch_stress(const KernelCtx& k, const double* base, const double* z, double rel, double abs_, double* lam) {
+  IPM_DISPATCH_CL(stress_impl, base, z, rel, abs_, lam)
+}
+
+}  // namespace ipm

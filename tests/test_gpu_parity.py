@@ -1,0 +1,172 @@
+"""GPU parity: the CUDA path through the C-ABI against the oracle on the same seeded inputs.
+
+Tolerances: moments 1e-9 relative to the state's scale (reading 27), Newton
+counts +-1, statuses equal, zeroth-moment conservation 1e-12 on periodic meshes.
+"""
+import numpy as np
+import pytest
+
+from inputs import configs
+
+from .gpu_common import assert_moments_close, mesh_arrays, stress_inputs, to_np
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+
+    if not t.cuda.is_available():
+        pytest.fail("GPU test needs CUDA (no CPU fallback exists)")
+    return t
+
+
+def ctx_and_oracle(cfg):
+    import oracle
+    from paper_1912_09238_b200 import Context
+
+    ma = mesh_arrays(cfg)
+    return Context(cfg, ma), oracle.Oracle(cfg, ma), ma
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+def test_basis_tables_match(torch, name):
+    cfg = configs.parity_variant(name)
+    g, o, _ = ctx_and_oracle(cfg)
+    xg, wg, pg = g.basis()
+    xo, wo, po = o.quadrature()
+    np.testing.assert_allclose(xg, xo, atol=2e-15)
+    np.testing.assert_allclose(wg, wo, rtol=1e-13, atol=1e-17)
+    np.testing.assert_allclose(pg, po, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4"])
+def test_dual_solve_stress_parity(torch, name):
+    """manufactured lambda* per cell: uhat = h(lambda*), solve from e0 (x) grad s(uhat_0)."""
+    cfg = configs.parity_variant(name)
+    if name == "cfg4":
+        cfg["levels"] = None  # whole basis in every cell; adaptivity is covered by the run test
+        cfg["newton"] = "full"
+    g, o, ma = ctx_and_oracle(cfg)
+    base, z, amp = stress_inputs(cfg, seed=9238 + int(name[-1]), ma=ma)
+    # oracle side
+    lam_star = o.stress_dual(base, z, amp)
+    u_o = o.moments_from_dual_all(lam_star)
+    lam_o = o.warm_start(u_o)
+    it_o, st_o, _ = o.dual_solve_all(u_o, lam_o)
+    # GPU side, from the same seeded draws
+    tb, tz = torch.tensor(base, device="cuda"), torch.tensor(z, device="cuda")
+    lam_s = g.zeros()
+    g.ipm_stress_dual(tb, tz, amp[0], amp[1], lam_s)
+    np.testing.assert_allclose(to_np(lam_s), lam_star, rtol=1e-13, atol=1e-13)
+    u_g = g.zeros()
+    g.ipm_moments_from_dual(lam_s, u_g)
+    assert_moments_close(to_np(u_g), u_o, 1e-13, "h(lambda*)")
+    lam_g = g.zeros()
+    g.ipm_warm_start(u_g, lam_g)
+    it_g = g.zeros(g.cells, dtype=torch.int32)
+    st_g = g.zeros(g.cells, dtype=torch.int32)
+    g.ipm_dual_solve(u_g, lam_g, "full", it_g, st_g)
+    torch.cuda.synchronize()
+    assert (st_o == 0).all()
+    np.testing.assert_array_equal(to_np(st_g), st_o)
+    assert np.abs(to_np(it_g) - it_o).max() <= 1
+    assert (it_o >= 1).mean() > 0.9  # the stress input makes every cell iterate
+    scale = np.abs(lam_star).max(axis=(0, 1))
+    err = (np.abs(to_np(lam_g) - lam_o) / scale).max()
+    assert err < 1e-9, err
+
+
+def _run_both(cfg, n_steps=None):
+    g, o, _ = ctx_and_oracle(cfg)
+    u_o, l_o, info_o = o.run(n_steps=n_steps, record=True)
+    u_g, l_g, info_g = g.run(n_steps=n_steps, record=True)
+    return g, o, (u_o, l_o, info_o), (to_np(u_g), to_np(l_g), info_g)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3"])
+def test_full_run_parity(torch, name):
+    cfg = configs.parity_variant(name)
+    g, o, (u_o, l_o, io), (u_g, l_g, ig) = _run_both(cfg)
+    assert io["steps"] == ig["steps"]
+    assert abs(io["t"] - ig["t"]) < 1e-14
+    assert_moments_close(u_g, u_o, 1e-9, name)
+    for (dto, ito, _), (dtg, itg, _) in zip(io["hist"], ig["hist"]):
+        assert abs(dto - dtg) <= 1e-12 * dto
+        assert np.abs(ito - itg).max() <= 1
+
+
+def test_cfg5_window_parity(torch):
+    cfg = configs.parity_variant("cfg5")
+    g, o, (u_o, _, io), (u_g, _, ig) = _run_both(cfg, n_steps=3)
+    assert_moments_close(u_g, u_o, 1e-9, "cfg5")
+
+
+def test_one_shot_adaptive_cfg4_parity(torch):
+    cfg = configs.parity_variant("cfg4")
+    g, o, (u_o, l_o, io), (u_g, l_g, ig) = _run_both(cfg, n_steps=15)
+    lv_o = o.levels()
+    lv_g = to_np(g.levels())
+    assert (lv_o != lv_g).mean() < 0.01
+    assert_moments_close(u_g, u_o, 1e-9, "cfg4")
+    for (_, ito, ro), (_, itg, rg) in zip(io["hist"], ig["hist"]):
+        assert np.abs(ito - itg).max() <= 1
+        assert abs(ro - rg) <= 1e-9 * max(ro, 1e-300)
+
+
+def test_one_shot_steady_fixed_point(torch):
+    from paper_1912_09238_b200 import Context
+
+    res = {}
+    for mode in ("full", "one_step"):
+        g = Context(configs.steady1d(mode))
+        u = g.zeros()
+        g.ipm_project_ic(u)
+        lam = g.zeros()
+        g.ipm_warm_start(u, lam)
+        r1, total = None, 0
+        for _ in range(5000):
+            info = g.ipm_step(u, lam)
+            assert info.failed_cells == 0
+            total += info.newton_iters
+            r1 = info.residual if r1 is None else r1
+            if info.residual <= 1e-8 * r1:
+                break
+        res[mode] = (to_np(u), total)
+    assert res["one_step"][1] < res["full"][1]
+    np.testing.assert_allclose(res["one_step"][0], res["full"][0], atol=1e-6)
+
+
+def test_periodic_conservation(torch):
+    cfg = configs.get("cfg3", mesh=dict(nx=16, ny=12, periodic=True))
+    from paper_1912_09238_b200 import Context
+
+    g = Context(cfg)
+    u = g.zeros()
+    g.ipm_project_ic(u)
+    lam = g.zeros()
+    g.ipm_warm_start(u, lam)
+    tot0 = to_np(u)[:, 0, :].sum(axis=0)
+    for _ in range(10):
+        info = g.ipm_step(u, lam)
+        assert info.failed_cells == 0
+    tot = to_np(u)[:, 0, :].sum(axis=0)
+    np.testing.assert_allclose(tot, tot0, rtol=1e-12, atol=1e-12)
+
+
+def test_uniform_state_bit_exact(torch):
+    from paper_1912_09238_b200 import Context
+
+    cfg = configs.get("cfg3", mesh=dict(nx=8, ny=6, periodic=True))
+    cfg["ic"] = dict(kind="uniform", states=[cfg["ic"]["states"][0]])
+    g = Context(cfg)
+    u = g.zeros()
+    g.ipm_project_ic(u)
+    u0 = u.clone()
+    lam = g.zeros()
+    g.ipm_warm_start(u, lam)
+    for _ in range(3):
+        info = g.ipm_step(u, lam)
+        assert info.newton_iters == 0
+    assert torch.equal(u, u0)
