@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <unordered_map>
@@ -485,7 +486,7 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   k.ad.Nprev0 = C.n_levels > 0 ? (C.level_M[0] > 0 ? binom_total(p, C.level_M[0] - 1) : 0) : 0;
   k.ad.delta_dec = C.delta_dec;
   k.ad.delta_inc = C.delta_inc;
-  k.cl = ipm::ClParams{C.gamma, C.u_minus, C.u_plus};
+  k.cl = ipm::ClParams{C.gamma, C.u_minus, C.u_plus, C.gamma > 1.0 ? 1.0 / (C.gamma - 1.0) : 0.0};
   k.closure = C.closure;
   k.flux = C.flux;
   k.m = m;
@@ -493,6 +494,9 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   k.stream = c->stream;
   k.sm_count = sms;
   k.smem_optin = (size_t)optin;
+  // IPM_DUAL_KERNEL=warp selects the warp-per-cell dual kernel (comparison / tests)
+  const char* dk = std::getenv("IPM_DUAL_KERNEL");
+  k.force_warp_kernel = (dk && std::strcmp(dk, "warp") == 0) ? 1 : 0;
   *out = c;
   return IPM_OK;
 }

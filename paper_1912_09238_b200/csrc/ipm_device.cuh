@@ -109,7 +109,8 @@ struct Closure<CL_EULER, MS> {
 #pragma unroll
     for (int k = 0; k < D; ++k) vm2 = fma(v[1 + k], v[1 + k], vm2);
     const double inv_vE = 1.0 / vE;
-    const double lnrho = v[0] - 0.5 * vm2 * inv_vE - (g + log(-vE)) / (g - 1.0);
+    const double igm1 = c.inv_gm1;
+    const double lnrho = v[0] - 0.5 * vm2 * inv_vE - (g + log(-vE)) * igm1;
     const double rho = exp(lnrho);
     const double p = -rho * inv_vE;
     double w[D], w2 = 0.0;
@@ -118,14 +119,15 @@ struct Closure<CL_EULER, MS> {
       w[k] = -v[1 + k] * inv_vE;
       w2 = fma(w[k], w[k], w2);
     }
-    const double E = p / (g - 1.0) + 0.5 * rho * w2;
+    const double E = p * igm1 + 0.5 * rho * w2;
     u[0] = rho;
 #pragma unroll
     for (int k = 0; k < D; ++k) u[1 + k] = rho * w[k];
     u[MS - 1] = E;
     sstar = rho;
     // A0 = du/dv: H = (E+p)/rho, c^2 = gamma p / rho
-    const double H = (E + p) / rho;
+    const double irho = 1.0 / rho;
+    const double H = (E + p) * irho;
     J[sym_idx<MS>(0, 0)] = rho;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
@@ -135,7 +137,7 @@ struct Closure<CL_EULER, MS> {
       J[sym_idx<MS>(1 + k, MS - 1)] = u[1 + k] * H;
     }
     J[sym_idx<MS>(0, MS - 1)] = E;
-    J[sym_idx<MS>(MS - 1, MS - 1)] = rho * H * H - g * p * p / (rho * (g - 1.0));
+    J[sym_idx<MS>(MS - 1, MS - 1)] = rho * H * H - g * p * p * irho * igm1;
     return rho > 0.0 && isfinite(rho) && isfinite(E);
   }
   // v = ((gamma - S)/(gamma-1) - rho|w|^2/(2p), rho w/p, -rho/p), S = ln p - gamma ln rho

@@ -5,7 +5,7 @@
 namespace ipm {
 
 struct ClParams {
-  double gamma, umin, umax;
+  double gamma, umin, umax, inv_gm1;  // inv_gm1 = 1/(gamma-1)
 };
 
 // Basis / quadrature tables as seen by the kernels (device pointers).
@@ -93,6 +93,7 @@ struct KernelCtx {
   void* stream;     // cudaStream_t
   int sm_count;
   size_t smem_optin;
+  int force_warp_kernel;  // 1: always use the warp-per-cell dual kernel (tests, comparison)
 };
 
 // launchers (ipm_kernels.cu); return 0 on success, else a cudaError_t / -1 unsupported

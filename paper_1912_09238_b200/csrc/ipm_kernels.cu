@@ -376,6 +376,8 @@ __global__ void __launch_bounds__(512) k_dual_warp(DualParams P) {
   }
 }
 
+#include "ipm_dual_group.cuh"
+
 // ------------------------------------------------------------------------------------------------
 // flux kernel (variant B: node states from the dual kernel)
 // ------------------------------------------------------------------------------------------------
@@ -726,8 +728,54 @@ static int dual_impl(const KernelCtx& k, const DualLaunch& a) {
   return (int)cudaGetLastError();
 }
 
+template <int CL, int MS, int G>
+static int dual_group_impl(const KernelCtx& k, const DualLaunch& a) {
+  using Lay = GroupLayout<MS>;
+  const size_t tab = (size_t)2 * k.T.N * k.T.QP * 8, pg = (size_t)Lay::per_group(k.T.N, k.T.Q, G) * 8;
+  if (tab + pg > k.smem_optin) return -1;
+  int groups = (int)((k.smem_optin - tab) / pg);
+  groups = std::min(groups, 768 / G);
+  const size_t smem = tab + groups * pg;
+  auto kern = k_dual_group<CL, MS, G>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, groups * G, smem);
+  if (per_sm < 1) return -1;
+  const int64_t want = (a.cells + groups - 1) / groups;
+  int grid = (int)std::min<int64_t>(want, (int64_t)k.sm_count * per_sm);
+  if (grid < 1) grid = 1;
+  DualParams P{k.T, k.mesh, k.nw, k.ad, k.cl, a, k.sc};
+  kern<<<grid, groups * G, smem, S(k)>>>(P);
+  return (int)cudaGetLastError();
+}
+
+// group size: the smallest of 32/64/128/256 threads that owns every m x m Hessian block
+static int group_size(int N) {
+  const int NP = N * (N + 1) / 2;
+  for (int G : {32, 64, 128, 256})
+    if (NP <= G) return G;
+  return 0;
+}
+
 int launch_dual(const KernelCtx& k, const DualLaunch& a) {
   if (a.cells == 0) return 0;
+  if (!k.force_warp_kernel) {
+    const int G = group_size(k.T.N);
+    const int key = (k.closure * 10 + k.m) * 1000 + G;
+    int rc = -1;
+    switch (key) {
+      case (CL_BARRIER * 10 + 1) * 1000 + 32: rc = dual_group_impl<CL_BARRIER, 1, 32>(k, a); break;
+      case (CL_BARRIER * 10 + 1) * 1000 + 64: rc = dual_group_impl<CL_BARRIER, 1, 64>(k, a); break;
+      case (CL_QUADRATIC * 10 + 1) * 1000 + 32: rc = dual_group_impl<CL_QUADRATIC, 1, 32>(k, a); break;
+      case (CL_EULER * 10 + 3) * 1000 + 64: rc = dual_group_impl<CL_EULER, 3, 64>(k, a); break;
+      case (CL_EULER * 10 + 3) * 1000 + 128: rc = dual_group_impl<CL_EULER, 3, 128>(k, a); break;
+      case (CL_EULER * 10 + 4) * 1000 + 32: rc = dual_group_impl<CL_EULER, 4, 32>(k, a); break;
+      case (CL_EULER * 10 + 4) * 1000 + 64: rc = dual_group_impl<CL_EULER, 4, 64>(k, a); break;
+      case (CL_EULER * 10 + 4) * 1000 + 128: rc = dual_group_impl<CL_EULER, 4, 128>(k, a); break;
+      case (CL_EULER * 10 + 4) * 1000 + 256: rc = dual_group_impl<CL_EULER, 4, 256>(k, a); break;
+    }
+    if (rc != -1) return rc;
+  }
   switch (k.closure * 10 + k.m) {
     case CL_QUADRATIC * 10 + 1: return dual_impl<CL_QUADRATIC, 1>(k, a);
     case CL_QUADRATIC * 10 + 3: return dual_impl<CL_QUADRATIC, 3>(k, a);
