@@ -206,6 +206,11 @@ IPM_API ipm_status ipm_nccl_unique_id(void *h_id128);
 IPM_API ipm_status ipm_last_kernel_ms(ipm_ctx *c, float *dual_ms, float *flux_ms);
 IPM_API ipm_status ipm_enable_timing(ipm_ctx *c, int32_t on);
 
+/* Debug: per-phase clock64 cycle totals of the dual kernel (builds with -DIPM_PHASE_TIMERS;
+ * zeros otherwise).  h_out[8]: 0 eval/grad/line search, 1 Hessian, 2 Cholesky, 3 back-substitution,
+ * 4 final line search, 7 epilogue + cell fetch.  Synchronous; resets the counters. */
+IPM_API ipm_status ipm_debug_phase_cycles(uint64_t *h_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -25,17 +25,24 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, timers: bool = False, variant: str = "",
+          defines=()) -> str:
+    """variant/defines: experimental builds (libipm_<variant>.so), never the product default."""
+    name = "libipm_timers.so" if timers else (f"libipm_{variant}.so" if variant else "libipm.so")
+    lib = os.path.join(HERE, name)
+    if not force and not timers and not variant and not stale():
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp]
+    tmp = lib + f".tmp{os.getpid()}"
+    extra = (["-DIPM_PHASE_TIMERS"] if timers else []) + [f"-D{d}" for d in defines]
+    cmd = [NVCC, *FLAGS, *extra, *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    var = next((a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--variant=")), "")
+    print(build(force="--force" in sys.argv, verbose=True, timers="--timers" in sys.argv, variant=var, defines=defs))

@@ -279,6 +279,17 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
       c->phi[(size_t)k * N + i] = v;
     }
   }
+  // 1D pair table for the sum-factorised Hessian: LL[k][pr] = (w_k/2) L_a(x_k) L_b(x_k), a <= b <= M
+  const int npr = (C.M + 1) * (C.M + 2) / 2;
+  std::vector<double> LL((size_t)C.q1d * npr);
+  for (int k = 0; k < C.q1d; ++k) {
+    int pr = 0;
+    for (int aa = 0; aa <= C.M; ++aa)
+      for (int bb = aa; bb <= C.M; ++bb, ++pr)
+        LL[(size_t)k * npr + pr] =
+            0.5 * w1[k] * legendre_orthonormal(aa, x1[k]) * legendre_orthonormal(bb, x1[k]);
+  }
+  std::vector<int32_t> idx32(c->idx.begin(), c->idx.end());
   std::vector<double> PhiT((size_t)N * QP, 0.0), WPhiT((size_t)N * QP, 0.0);
   for (int i = 0; i < N; ++i)
     for (int k = 0; k < Q; ++k) {
@@ -426,6 +437,8 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   double* d_WPhiT = dalloc<double>(WPhiT.size(), O);
   double* d_omega = dalloc<double>(Q, O);
   int32_t* d_deg = dalloc<int32_t>(N, O);
+  double* d_LL = dalloc<double>(LL.size(), O);
+  int32_t* d_idx = dalloc<int32_t>(idx32.size(), O);
   int32_t* d_nbr = dalloc<int32_t>(nbr.size(), O);
   double* d_nrm = dalloc<double>(nrm.size(), O);
   double* d_coef = dalloc<double>(coef.size(), O);
@@ -439,7 +452,7 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   c->d_iters = dalloc<int32_t>(cells, O);
   c->d_status = dalloc<int32_t>(cells, O);
   c->d_sc = dalloc<ipm::StepScalars>(1, O);
-  if (!d_PhiT || !d_WPhiT || !d_omega || !d_deg || !d_nbr || !d_nrm || !d_coef || !d_area || !d_rgeo || !d_ghost ||
+  if (!d_PhiT || !d_WPhiT || !d_omega || !d_deg || !d_LL || !d_idx || !d_nbr || !d_nrm || !d_coef || !d_area || !d_rgeo || !d_ghost ||
       !c->d_uq || !c->d_crit || !c->d_level || !c->d_level_new || !c->d_iters || !c->d_status || !c->d_sc) {
     ipm_destroy(c);
     return fail(IPM_ERR_CUDA, "cudaMalloc failed");
@@ -450,6 +463,7 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   };
   if (up(d_PhiT, PhiT.data(), PhiT.size() * 8) || up(d_WPhiT, WPhiT.data(), WPhiT.size() * 8) ||
       up(d_omega, c->omega.data(), Q * 8) || up(d_deg, deg32.data(), N * 4) ||
+      up(d_LL, LL.data(), LL.size() * 8) || up(d_idx, idx32.data(), idx32.size() * 4) ||
       up(d_nbr, nbr.data(), nbr.size() * 4) || up(d_nrm, nrm.data(), nrm.size() * 8) ||
       up(d_coef, coef.data(), coef.size() * 8) || up(d_area, area.data(), area.size() * 8) ||
       up(d_rgeo, rgeo.data(), rgeo.size() * 8) || up(d_ghost, ghost.data(), ghost.size() * 8) ||
@@ -467,7 +481,7 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
 
   ipm::KernelCtx& k = c->k;
-  k.T = ipm::Tables{d_PhiT, d_WPhiT, d_omega, d_deg, N, Q, QP, p};
+  k.T = ipm::Tables{d_PhiT, d_WPhiT, d_omega, d_deg, N, Q, QP, p, d_LL, d_idx, C.q1d, npr};
   k.mesh.kind = C.mesh_kind;
   k.mesh.F = F;
   k.mesh.cells = cells;
@@ -713,6 +727,14 @@ ipm_status ipm_last_kernel_ms(ipm_ctx* c, float* dual_ms, float* flux_ms) {
   CUDA_OK(cudaEventSynchronize(c->ev[3]));
   if (dual_ms) CUDA_OK(cudaEventElapsedTime(dual_ms, c->ev[0], c->ev[1]));
   if (flux_ms) CUDA_OK(cudaEventElapsedTime(flux_ms, c->ev[2], c->ev[3]));
+  return IPM_OK;
+}
+
+ipm_status ipm_debug_phase_cycles(uint64_t* h_out) {
+  if (!h_out) return fail(IPM_ERR_ARG, "null argument");
+  unsigned long long v[8];
+  if (int rc = ipm::debug_phase_cycles(v)) return launch_rc(rc, "debug_phase_cycles");
+  for (int i = 0; i < 8; ++i) h_out[i] = v[i];
   return IPM_OK;
 }
 

@@ -15,6 +15,9 @@
 //   Armijo    on L(lambda) with the rounding allowance of reading 3'; the accepted trial's node data
 //             and gradient are the next iteration's.
 #pragma once
+#ifndef IPM_GROUP_THREADS
+#define IPM_GROUP_THREADS 512  // CTA size bound: 512 -> <= 128 registers / thread
+#endif
 // (included inside namespace ipm by ipm_kernels.cu, after DualParams and node_rate)
 
 template <int MS>
@@ -23,11 +26,19 @@ struct GroupLayout {
   static constexpr int NS = ((MS + MM) % 2 == 0) ? MS + MM + 1 : MS + MM;
   static constexpr int TB = MS * MS;  // doubles per block (stored column-major)
   static constexpr int RS = MS > 2 ? MS : 2;  // values per reduction slot
-  // doubles per group: 5 vectors + union(node buffer, L blocks) + reduction scratch + control
-  static __host__ __device__ int per_group(int N, int Q, int G) {
-    const int n = N * MS, NP = N * (N + 1) / 2;
+  // doubles per group: 5 vectors + node buffer / L blocks / sum-factorisation stage + reduction + control
+  //   direct (SF = 0): union(node buffer, L blocks)
+  //   SF > 0:          node buffer, then union(T stage [q][npr][MM], L blocks)
+  static __host__ __device__ int region(int N, int Q, int SF, int q1d) {
+    const int NP = N * (N + 1) / 2;
     const int nb = Q * NS, lb = NP * TB;
-    int w = 5 * n + (nb > lb ? nb : lb) + 2 * RS * (G / 32) + 4;
+    if (SF == 0) return nb > lb ? nb : lb;
+    const int tb = q1d * (SF * (SF + 1) / 2) * MM;
+    return nb + (tb > lb ? tb : lb);
+  }
+  static __host__ __device__ int per_group(int N, int Q, int G, int SF = 0, int q1d = 0) {
+    const int n = N * MS;
+    int w = 5 * n + region(N, Q, SF, q1d) + N * TB + 2 * RS * (G / 32) + 4;
     return (w + 1) & ~1;
   }
 };
@@ -36,8 +47,26 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-template <int CL, int MS, int G>
-__global__ void __launch_bounds__(768) k_dual_group(DualParams P) {
+#ifdef IPM_PHASE_TIMERS
+__device__ unsigned long long g_phase_cycles[8];
+#define PHASE_MARK(i)                                  \
+  do {                                                 \
+    const long long now_ = clock64();                  \
+    if (t == 0) ph_acc[i] += (unsigned long long)(now_ - ph_t0); \
+    ph_t0 = now_;                                      \
+  } while (0)
+#else
+#define PHASE_MARK(i) \
+  do {                \
+  } while (0)
+#endif
+
+template <int CL, int MS, int G, int SF, int T>
+__global__ void __launch_bounds__(IPM_GROUP_THREADS) k_dual_group(DualParams P) {
+#ifdef IPM_PHASE_TIMERS
+  unsigned long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long ph_t0 = clock64();
+#endif
   using Lay = GroupLayout<MS>;
   constexpr int NW = G / 32;
   constexpr int MM = Lay::MM, NS = Lay::NS, TB = Lay::TB;
@@ -46,25 +75,32 @@ __global__ void __launch_bounds__(768) k_dual_group(DualParams P) {
   const int N = P.T.N, Q = P.T.Q, QP = P.T.QP;
   double* sPhiT = sm;
   double* sWPhiT = sm + N * QP;
+  constexpr int NPR = SF * (SF + 1) / 2;
+  double* sLL = sm + 2 * N * QP;  // [q1d][NPR] (SF > 0)
+  const int q1 = P.T.q1d;
+  const int tabsz = 2 * N * QP + ((SF > 0) ? ((q1 * NPR + 1) & ~1) : 0);
   for (int x = threadIdx.x; x < N * QP; x += blockDim.x) {
     sPhiT[x] = P.T.PhiT[x];
     sWPhiT[x] = P.T.WPhiT[x];
   }
+  if (SF > 0)
+    for (int x = threadIdx.x; x < q1 * NPR; x += blockDim.x) sLL[x] = P.T.LL[x];
   __syncthreads();
   const int grp = threadIdx.x / G, t = threadIdx.x - grp * G;
   const int wig = t >> 5, lane = t & 31;
   const int bar = 1 + grp;
   const int nmax = N * MS;
-  double* base = sm + 2 * N * QP + (size_t)grp * Lay::per_group(N, Q, G);
+  double* base = sm + tabsz + (size_t)grp * Lay::per_group(N, Q, G, SF, q1);
   double* lam = base;
   double* lt = lam + nmax;
   double* uh = lt + nmax;
   double* g = uh + nmax;
   double* dd = g + nmax;
-  double* nb = dd + nmax;  // node buffer, union with the L blocks
-  double* Ls = nb;
-  const int nbsize = Q * NS > (N * (N + 1) / 2) * TB ? Q * NS : (N * (N + 1) / 2) * TB;
-  double* red = nb + nbsize;  // [2 slots][RS][NW]
+  double* nb = dd + nmax;                   // node buffer
+  double* Ls = (SF > 0) ? nb + Q * NS : nb;  // L blocks (union with nb, or with the T stage)
+  double* Tt = Ls;                          // sum-factorisation stage T[k1][pr][ab] (SF > 0)
+  double* Linv = nb + Lay::region(N, Q, SF, q1);  // [N] inverses of the diagonal Cholesky blocks
+  double* red = Linv + (size_t)N * TB;  // [2 slots][RS][NW]
   int* ctl = (int*)(red + 2 * Lay::RS * NW);
 
   const double* __restrict__ omega = P.T.omega;
@@ -188,22 +224,31 @@ __global__ void __launch_bounds__(768) k_dual_group(DualParams P) {
     ad = sa;
   };
 
-  // block (I, J) owned by this thread: row-major lower enumeration p = I(I+1)/2 + J
-  int bI = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
-  while (bI * (bI + 1) / 2 > t) --bI;
-  while ((bI + 1) * (bI + 2) / 2 <= t) ++bI;
-  const int bJ = t - bI * (bI + 1) / 2;
+  // blocks (I, J) owned by this thread: p = t + s G, row-major lower enumeration p = I(I+1)/2 + J
+  int bIa[T], bJa[T];
+#pragma unroll
+  for (int s = 0; s < T; ++s) {
+    const int pp = t + s * G;
+    int bI = (int)((sqrtf(8.0f * pp + 1.0f) - 1.0f) * 0.5f);
+    while (bI * (bI + 1) / 2 > pp) --bI;
+    while ((bI + 1) * (bI + 2) / 2 <= pp) ++bI;
+    bIa[s] = bI;
+    bJa[s] = pp - bI * (bI + 1) / 2;
+  }
 
   for (;;) {
     if (t == 0) ctl[0] = atomicAdd(&P.sc->work_counter, 1);
     gsync();
     const int64_t cell = ctl[0];
     if (cell >= A.cells) break;
+    PHASE_MARK(7);
     const int lvl = A.level ? A.level[cell] : 0;
     const int Nl = (P.ad.n_levels > 0) ? P.ad.Nl[lvl] : N;
     const int n = Nl * MS;
     const int NPl = Nl * (Nl + 1) / 2;
-    const bool own = t < NPl;
+    bool owna[T];
+#pragma unroll
+    for (int q = 0; q < T; ++q) owna[q] = (t + q * G) < NPl;
     const double* gu = A.uhat + cell * nmax;
     double* gl = A.lam + cell * nmax;
     for (int r = t; r < n; r += G) {
@@ -233,163 +278,238 @@ __global__ void __launch_bounds__(768) k_dual_group(DualParams P) {
           status = 1;
           break;
         }
+        PHASE_MARK(0);  // eval / gradient / line search of the previous iteration
         // ---- Hessian block in registers -------------------------------------------------------
-        double blk[MS][MS];
-        if (own) {
-          double acc[MM];
+        double blk[T][MS][MS];
+        if constexpr (SF > 0) {
+          // sum factorisation over the tensor rule (p = 2), k = k1 q + k2:
+          //   T_ab[k1][(i2,j2)] = sum_k2 LL[k2][(i2,j2)] J_ab(k1,k2)
+          //   H_ab[I][J]       = sum_k1 LL[k1][(i1,j1)] T_ab[k1][(i2,j2)]
+          for (int e = t; e < q1 * MM; e += G) {
+            const int k1 = e / MM, ab = e - k1 * MM;
+            double acc[NPR];
 #pragma unroll
-          for (int q = 0; q < MM; ++q) acc[q] = 0.0;
-          const double* wi = sWPhiT + bI * QP;
-          const double* pj = sPhiT + bJ * QP;
-          for (int k = 0; k < Q; ++k) {
-            const double f = wi[k] * pj[k];
-            const double* Jk = nb + k * NS + MS;
+            for (int pr = 0; pr < NPR; ++pr) acc[pr] = 0.0;
+            for (int k2 = 0; k2 < q1; ++k2) {
+              const double jv = nb[(k1 * q1 + k2) * NS + MS + ab];
+              const double* ll = sLL + k2 * NPR;
 #pragma unroll
-            for (int q = 0; q < MM; ++q) acc[q] = fma(f, Jk[q], acc[q]);
-          }
-#pragma unroll
-          for (int a = 0; a < MS; ++a)
-#pragma unroll
-            for (int b = 0; b < MS; ++b) blk[a][b] = acc[a <= b ? sym_idx<MS>(a, b) : sym_idx<MS>(b, a)];
-        }
-        gsync();  // node buffer dead from here: L blocks reuse it
-        // ---- blocked Cholesky ------------------------------------------------------------------
-        bool chol_ok = true;
-        for (int K = 0; K < Nl; ++K) {
-          if (own && bI == K && bJ == K) {
-            bool ok = true;
-#pragma unroll
-            for (int c = 0; c < MS; ++c) {
-              double s = blk[c][c];
-#pragma unroll
-              for (int x = 0; x < c; ++x) s = fma(-blk[c][x], blk[c][x], s);
-              if (!(s > 0.0) || !isfinite(s)) ok = false;
-              const double lcc = sqrt(s);
-              const double inv = 1.0 / lcc;
-              blk[c][c] = lcc;
-#pragma unroll
-              for (int r = c + 1; r < MS; ++r) {
-                double v = blk[r][c];
-#pragma unroll
-                for (int x = 0; x < c; ++x) v = fma(-blk[r][x], blk[c][x], v);
-                blk[r][c] = v * inv;
-              }
+              for (int pr = 0; pr < NPR; ++pr) acc[pr] = fma(ll[pr], jv, acc[pr]);
             }
-            double* o = Ls + (size_t)t * TB;
+#pragma unroll
+            for (int pr = 0; pr < NPR; ++pr) Tt[(k1 * NPR + pr) * MM + ab] = acc[pr];
+          }
+          gsync();
+#pragma unroll
+          for (int q = 0; q < T; ++q) {
+            if (!owna[q]) continue;
+            int a1 = P.T.idx[bIa[q] * 2], a2 = P.T.idx[bIa[q] * 2 + 1];
+            int b1 = P.T.idx[bJa[q] * 2], b2 = P.T.idx[bJa[q] * 2 + 1];
+            if (a1 > b1) { const int x = a1; a1 = b1; b1 = x; }
+            if (a2 > b2) { const int x = a2; a2 = b2; b2 = x; }
+            const int pr1 = a1 * SF - a1 * (a1 - 1) / 2 + (b1 - a1);
+            const int pr2 = a2 * SF - a2 * (a2 - 1) / 2 + (b2 - a2);
+            double acc[MM];
+#pragma unroll
+            for (int z = 0; z < MM; ++z) acc[z] = 0.0;
+            for (int k1 = 0; k1 < q1; ++k1) {
+              const double lv = sLL[k1 * NPR + pr1];
+              const double* Tk = Tt + (k1 * NPR + pr2) * MM;
+#pragma unroll
+              for (int z = 0; z < MM; ++z) acc[z] = fma(lv, Tk[z], acc[z]);
+            }
 #pragma unroll
             for (int a = 0; a < MS; ++a)
 #pragma unroll
-              for (int b = 0; b < MS; ++b) o[LIDX(a, b)] = (b <= a) ? blk[a][b] : 0.0;
-            ctl[1] = ok ? 0 : 1;
+              for (int b = 0; b < MS; ++b) blk[q][a][b] = acc[a <= b ? sym_idx<MS>(a, b) : sym_idx<MS>(b, a)];
           }
-          gsync();
+        } else {
+#pragma unroll
+          for (int q = 0; q < T; ++q) {
+            if (!owna[q]) continue;
+            double acc[MM];
+#pragma unroll
+            for (int z = 0; z < MM; ++z) acc[z] = 0.0;
+            const double* wi = sWPhiT + bIa[q] * QP;
+            const double* pj = sPhiT + bJa[q] * QP;
+            for (int k = 0; k < Q; ++k) {
+              const double f = wi[k] * pj[k];
+              const double* Jk = nb + k * NS + MS;
+#pragma unroll
+              for (int z = 0; z < MM; ++z) acc[z] = fma(f, Jk[z], acc[z]);
+            }
+#pragma unroll
+            for (int a = 0; a < MS; ++a)
+#pragma unroll
+              for (int b = 0; b < MS; ++b) blk[q][a][b] = acc[a <= b ? sym_idx<MS>(a, b) : sym_idx<MS>(b, a)];
+          }
+        }
+        for (int r = t; r < n; r += G) dd[r] = -g[r];
+        gsync();  // node buffer / T stage dead from here: L blocks reuse them
+        PHASE_MARK(1);
+        // ---- blocked Cholesky with the forward solve folded in ---------------------------------
+        // step K: (1) owner of (K,K): L_KK = chol(A_KK), Linv_K = L_KK^{-1}, y_K = Linv_K b_K
+        //         (2) owners of (I,K), I > K: L_IK = A_IK Linv_K^T, b_I -= L_IK y_K
+        //         (3) owners of (I,J), I >= J > K: A_IJ -= L_IK L_JK^T
+        // b = -g lives in dd and becomes y = L^{-1}(-g) in place.
+        // diagonal step: owner of (K,K) factors its (fully updated) block, publishes L_KK and
+        // Linv_K, and turns b_K into y_K = Linv_K b_K.  Called for K = 0 up front and for K + 1
+        // inside the trailing phase of step K (look-ahead), right after that block's own update.
+        auto diag_step = [&](int q, int K) {
+          bool ok = true;
+          double inv[MS];
+#pragma unroll
+          for (int c = 0; c < MS; ++c) {
+            double sv = blk[q][c][c];
+#pragma unroll
+            for (int x = 0; x < c; ++x) sv = fma(-blk[q][c][x], blk[q][c][x], sv);
+            if (!(sv > 0.0) || !isfinite(sv)) ok = false;
+            const double rs = rsqrt(sv);
+            inv[c] = rs;
+            blk[q][c][c] = sv * rs;
+#pragma unroll
+            for (int r = c + 1; r < MS; ++r) {
+              double v = blk[q][r][c];
+#pragma unroll
+              for (int x = 0; x < c; ++x) v = fma(-blk[q][r][x], blk[q][c][x], v);
+              blk[q][r][c] = v * rs;
+            }
+          }
+          // Linv (lower): Linv[c][c] = 1/L[c][c]; Linv[r][c] = -Linv[r][r] sum_{x=c}^{r-1} L[r][x] Linv[x][c]
+          double li[MS][MS];
+#pragma unroll
+          for (int c = 0; c < MS; ++c) {
+            li[c][c] = inv[c];
+#pragma unroll
+            for (int r = c + 1; r < MS; ++r) {
+              double v = 0.0;
+#pragma unroll
+              for (int x = c; x < r; ++x) v = fma(blk[q][r][x], li[x][c], v);
+              li[r][c] = -inv[r] * v;
+            }
+          }
+          double* o = Ls + (size_t)(t + q * G) * TB;
+          double* oi = Linv + (size_t)K * TB;
+#pragma unroll
+          for (int aa = 0; aa < MS; ++aa)
+#pragma unroll
+            for (int bb = 0; bb < MS; ++bb) {
+              o[LIDX(aa, bb)] = (bb <= aa) ? blk[q][aa][bb] : 0.0;
+              oi[LIDX(aa, bb)] = (bb <= aa) ? li[aa][bb] : 0.0;
+            }
+          double bk[MS];
+#pragma unroll
+          for (int aa = 0; aa < MS; ++aa) bk[aa] = dd[K * MS + aa];
+#pragma unroll
+          for (int aa = 0; aa < MS; ++aa) {
+            double v = 0.0;
+#pragma unroll
+            for (int x = 0; x <= aa; ++x) v = fma(li[aa][x], bk[x], v);
+            dd[K * MS + aa] = v;
+          }
+          ctl[1] = ok ? 0 : 1;
+        };
+        bool chol_ok = true;
+#pragma unroll
+        for (int q = 0; q < T; ++q)
+          if (owna[q] && bIa[q] == 0 && bJa[q] == 0) diag_step(q, 0);
+        gsync();
+        for (int K = 0; K < Nl; ++K) {
           if (ctl[1]) {
             chol_ok = false;
             break;
           }
-          const double* Lkk = Ls + (size_t)(K * (K + 1) / 2 + K) * TB;
-          if (own && bJ == K && bI > K) {
-            // X = A_IK L_KK^{-T}: x_c = (a_c - sum_{x<c} x_x L_KK[c][x]) / L_KK[c][c]
-            double inv[MS];
+          // (2) panel
+          const double* Li = Linv + (size_t)K * TB;
 #pragma unroll
-            for (int c = 0; c < MS; ++c) inv[c] = 1.0 / Lkk[LIDX(c, c)];
+          for (int q = 0; q < T; ++q) {
+            if (!(owna[q] && bJa[q] == K && bIa[q] > K)) continue;
+            double X[MS][MS];
 #pragma unroll
             for (int r = 0; r < MS; ++r)
 #pragma unroll
               for (int c = 0; c < MS; ++c) {
-                double v = blk[r][c];
+                double v = 0.0;
 #pragma unroll
-                for (int x = 0; x < c; ++x) v = fma(-blk[r][x], Lkk[LIDX(c, x)], v);
-                blk[r][c] = v * inv[c];
+                for (int x = 0; x <= c; ++x) v = fma(blk[q][r][x], Li[LIDX(c, x)], v);
+                X[r][c] = v;
               }
-            double* o = Ls + (size_t)t * TB;
+            double yk[MS];
 #pragma unroll
-            for (int a = 0; a < MS; ++a)
+            for (int x = 0; x < MS; ++x) yk[x] = dd[K * MS + x];
+            double* o = Ls + (size_t)(t + q * G) * TB;
+            const int bI = bIa[q];
 #pragma unroll
-              for (int b = 0; b < MS; ++b) o[LIDX(a, b)] = blk[a][b];
+            for (int r = 0; r < MS; ++r) {
+              double v = dd[bI * MS + r];
+#pragma unroll
+              for (int c = 0; c < MS; ++c) {
+                o[LIDX(r, c)] = X[r][c];
+                v = fma(-X[r][c], yk[c], v);
+              }
+              dd[bI * MS + r] = v;
+            }
           }
           gsync();
-          if (own && bJ > K) {
-            const double* Lik = Ls + (size_t)(bI * (bI + 1) / 2 + K) * TB;
-            const double* Ljk = Ls + (size_t)(bJ * (bJ + 1) / 2 + K) * TB;
-            // rank-1 updates by column x of L_IK and L_JK (contiguous in column-major blocks)
+          // (3) trailing update; the owner of (K+1,K+1) then factors it at once (look-ahead)
+#pragma unroll
+          for (int q = 0; q < T; ++q) {
+            if (!(owna[q] && bJa[q] > K)) continue;
+            const double* Lik = Ls + (size_t)(bIa[q] * (bIa[q] + 1) / 2 + K) * TB;
+            const double* Ljk = Ls + (size_t)(bJa[q] * (bJa[q] + 1) / 2 + K) * TB;
 #pragma unroll
             for (int x = 0; x < MS; ++x) {
               double ci[MS], cj[MS];
 #pragma unroll
-              for (int a = 0; a < MS; ++a) {
-                ci[a] = Lik[LIDX(a, x)];
-                cj[a] = Ljk[LIDX(a, x)];
+              for (int aa = 0; aa < MS; ++aa) {
+                ci[aa] = Lik[LIDX(aa, x)];
+                cj[aa] = Ljk[LIDX(aa, x)];
               }
 #pragma unroll
               for (int r = 0; r < MS; ++r)
 #pragma unroll
-                for (int c = 0; c < MS; ++c) blk[r][c] = fma(-ci[r], cj[c], blk[r][c]);
+                for (int c = 0; c < MS; ++c) blk[q][r][c] = fma(-ci[r], cj[c], blk[q][r][c]);
             }
+            if (bIa[q] == K + 1 && bJa[q] == K + 1) diag_step(q, K + 1);
           }
+          gsync();
         }
         if (!chol_ok) {
           status = 2;
           break;
         }
-        // ---- triangular solves by warp 0: L y = -g, L^T d = y ---------------------------------
+        PHASE_MARK(2);
+        // ---- back substitution L^T d = y by warp 0 (column oriented, Linv_K^T per block) ------
         if (wig == 0) {
-          for (int r = lane; r < n; r += 32) dd[r] = -g[r];
-          __syncwarp();
-          for (int K = 0; K < Nl; ++K) {
-            const double* Lkk = Ls + (size_t)(K * (K + 1) / 2 + K) * TB;
-            double y[MS];
+          for (int K = Nl - 1; K >= 0; --K) {
+            const double* Li = Linv + (size_t)K * TB;
+            double dk[MS];
 #pragma unroll
             for (int c = 0; c < MS; ++c) {
-              double v = dd[K * MS + c];
+              double v = 0.0;
 #pragma unroll
-              for (int x = 0; x < c; ++x) v = fma(-Lkk[LIDX(c, x)], y[x], v);
-              y[c] = v / Lkk[LIDX(c, c)];
+              for (int x = c; x < MS; ++x) v = fma(Li[LIDX(x, c)], dd[K * MS + x], v);
+              dk[c] = v;
             }
             __syncwarp();
             if (lane < MS) {
 #pragma unroll
               for (int c = 0; c < MS; ++c)
-                if (c == lane) dd[K * MS + c] = y[c];
-            }
-            for (int e = lane; e < (Nl - 1 - K) * MS; e += 32) {
-              const int I = K + 1 + e / MS, c = e - (e / MS) * MS;
-              const double* Lik = Ls + (size_t)(I * (I + 1) / 2 + K) * TB;
-              double v = dd[I * MS + c];
-#pragma unroll
-              for (int x = 0; x < MS; ++x) v = fma(-Lik[LIDX(c, x)], y[x], v);
-              dd[I * MS + c] = v;
-            }
-            __syncwarp();
-          }
-          for (int K = Nl - 1; K >= 0; --K) {
-            const double* Lkk = Ls + (size_t)(K * (K + 1) / 2 + K) * TB;
-            double x_[MS];
-#pragma unroll
-            for (int c = MS - 1; c >= 0; --c) {
-              double v = dd[K * MS + c];
-#pragma unroll
-              for (int x = c + 1; x < MS; ++x) v = fma(-Lkk[LIDX(x, c)], x_[x], v);
-              x_[c] = v / Lkk[LIDX(c, c)];
-            }
-            __syncwarp();
-            if (lane < MS) {
-#pragma unroll
-              for (int c = 0; c < MS; ++c)
-                if (c == lane) dd[K * MS + c] = x_[c];
+                if (c == lane) dd[K * MS + c] = dk[c];
             }
             for (int e = lane; e < K * MS; e += 32) {
               const int J = e / MS, c = e - J * MS;
               const double* Lkj = Ls + (size_t)(K * (K + 1) / 2 + J) * TB;
               double v = dd[J * MS + c];
 #pragma unroll
-              for (int x = 0; x < MS; ++x) v = fma(-Lkj[LIDX(x, c)], x_[x], v);
+              for (int x = 0; x < MS; ++x) v = fma(-Lkj[LIDX(x, c)], dk[x], v);
               dd[J * MS + c] = v;
             }
             __syncwarp();
           }
         }
         gsync();
+        PHASE_MARK(3);
         // ---- Armijo backtracking on L (reading 3') ---------------------------------------------
         double slope, dummy;
         dot2(g, dd, n, slope, dummy);
@@ -425,6 +545,7 @@ __global__ void __launch_bounds__(768) k_dual_group(DualParams P) {
         gsync();
       }
     }
+    PHASE_MARK(4);
     // ---- epilogue ------------------------------------------------------------------------------
     gsync();
     if (!nb_is_lam && status != 4) {
@@ -476,6 +597,11 @@ __global__ void __launch_bounds__(768) k_dual_group(DualParams P) {
     }
     gsync();
   }
+  PHASE_MARK(5);
+#ifdef IPM_PHASE_TIMERS
+  if (t == 0)
+    for (int i = 0; i < 8; ++i) atomicAdd(&g_phase_cycles[i], ph_acc[i]);
+#endif
   my_rate = warp_max(my_rate);
   if (lane == 0) {
     if (A.want_rate) atomicMax(&P.sc->rate_bits, (unsigned long long)__double_as_longlong(my_rate));

@@ -17,6 +17,12 @@ struct Tables {
   const double* omega;
   const int32_t* deg;  // [N] total degree |i|
   int N, Q, QP, p;
+  // sum factorisation over the tensor Gauss-Legendre rule (p == 2):
+  //   LL [q1d][npr] = (w_k/2) L_a(x_k) L_b(x_k) for 1D degree pairs a <= b <= M
+  //   idx [N][p]    multi-indices
+  const double* LL;
+  const int32_t* idx;
+  int q1d, npr;
 };
 
 // Local mesh: owned cells, face tables (F faces per cell)
@@ -98,6 +104,7 @@ struct KernelCtx {
 
 // launchers (ipm_kernels.cu); return 0 on success, else a cudaError_t / -1 unsupported
 int launch_step_begin(const KernelCtx& k, double rate0);
+int debug_phase_cycles(unsigned long long* out);
 int launch_dual(const KernelCtx& k, const DualLaunch& a);
 int launch_dt(const KernelCtx& k, double t_end, double dt_fixed, double cfl);
 int launch_flux(const KernelCtx& k, const FluxLaunch& a);

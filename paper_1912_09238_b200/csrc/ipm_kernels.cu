@@ -16,6 +16,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 #include <cstdio>
 
 #include "ipm_device.cuh"
@@ -697,6 +699,18 @@ __global__ void k_stress(Tables T, int64_t cells, ClParams cp, const double* __r
 // ------------------------------------------------------------------------------------------------
 static inline cudaStream_t S(const KernelCtx& k) { return (cudaStream_t)k.stream; }
 
+int debug_phase_cycles(unsigned long long* out) {
+#ifdef IPM_PHASE_TIMERS
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_phase_cycles, 8 * sizeof(unsigned long long));
+  unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+  return (int)e;
+#else
+  for (int i = 0; i < 8; ++i) out[i] = 0;
+  return 0;
+#endif
+}
+
 int launch_step_begin(const KernelCtx& k, double rate0) {
   k_step_begin<<<1, 1, 0, S(k)>>>(k.sc, rate0);
   return (int)cudaGetLastError();
@@ -728,15 +742,17 @@ static int dual_impl(const KernelCtx& k, const DualLaunch& a) {
   return (int)cudaGetLastError();
 }
 
-template <int CL, int MS, int G>
+template <int CL, int MS, int G, int SF, int T>
 static int dual_group_impl(const KernelCtx& k, const DualLaunch& a) {
   using Lay = GroupLayout<MS>;
-  const size_t tab = (size_t)2 * k.T.N * k.T.QP * 8, pg = (size_t)Lay::per_group(k.T.N, k.T.Q, G) * 8;
+  const int npr = SF * (SF + 1) / 2;
+  const size_t tab = ((size_t)2 * k.T.N * k.T.QP + (SF > 0 ? ((k.T.q1d * npr + 1) & ~1) : 0)) * 8;
+  const size_t pg = (size_t)Lay::per_group(k.T.N, k.T.Q, G, SF, k.T.q1d) * 8;
   if (tab + pg > k.smem_optin) return -1;
   int groups = (int)((k.smem_optin - tab) / pg);
-  groups = std::min(groups, 768 / G);
+  groups = std::min(groups, IPM_GROUP_THREADS / G);
   const size_t smem = tab + groups * pg;
-  auto kern = k_dual_group<CL, MS, G>;
+  auto kern = k_dual_group<CL, MS, G, SF, T>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, groups * G, smem);
@@ -749,30 +765,52 @@ static int dual_group_impl(const KernelCtx& k, const DualLaunch& a) {
   return (int)cudaGetLastError();
 }
 
-// group size: the smallest of 32/64/128/256 threads that owns every m x m Hessian block
-static int group_size(int N) {
+// group size G and blocks per thread T: T = 2 (fewer threads per cell, more cells per SM) with the
+// smallest G such that G T covers every m x m Hessian block; IPM_GROUP_T=1 forces one block per thread
+static void group_shape(int N, int& G, int& T) {
   const int NP = N * (N + 1) / 2;
-  for (int G : {32, 64, 128, 256})
-    if (NP <= G) return G;
-  return 0;
+  const char* e = std::getenv("IPM_GROUP_T");
+  const int tmax = (e && e[0] == '1') ? 1 : 2;
+  G = 0;
+  T = 0;
+  for (int t = tmax; t >= 1 && G == 0; --t)
+    for (int g : {32, 64, 128, 256})
+      if (NP <= g * t) {
+        G = g;
+        T = t;
+        break;
+      }
 }
 
 int launch_dual(const KernelCtx& k, const DualLaunch& a) {
   if (a.cells == 0) return 0;
   if (!k.force_warp_kernel) {
-    const int G = group_size(k.T.N);
-    const int key = (k.closure * 10 + k.m) * 1000 + G;
+    int G, T;
+    group_shape(k.T.N, G, T);
+    // sum factorisation for p = 2 tensor rules (SF = M + 1); opt-in with IPM_SUMFACT=1 (it costs
+    // shared memory, i.e. cells in flight, which measured slower on cfg 3)
+    const char* sfe = std::getenv("IPM_SUMFACT");
+    const int SF = (k.T.p == 2 && (sfe && sfe[0] == '1')) ? (int)std::lround((std::sqrt(8.0 * k.T.npr + 1) - 1) / 2) : 0;
+    const int key = (((k.closure * 10 + k.m) * 1000 + G) * 10 + SF) * 10 + T;
     int rc = -1;
     switch (key) {
-      case (CL_BARRIER * 10 + 1) * 1000 + 32: rc = dual_group_impl<CL_BARRIER, 1, 32>(k, a); break;
-      case (CL_BARRIER * 10 + 1) * 1000 + 64: rc = dual_group_impl<CL_BARRIER, 1, 64>(k, a); break;
-      case (CL_QUADRATIC * 10 + 1) * 1000 + 32: rc = dual_group_impl<CL_QUADRATIC, 1, 32>(k, a); break;
-      case (CL_EULER * 10 + 3) * 1000 + 64: rc = dual_group_impl<CL_EULER, 3, 64>(k, a); break;
-      case (CL_EULER * 10 + 3) * 1000 + 128: rc = dual_group_impl<CL_EULER, 3, 128>(k, a); break;
-      case (CL_EULER * 10 + 4) * 1000 + 32: rc = dual_group_impl<CL_EULER, 4, 32>(k, a); break;
-      case (CL_EULER * 10 + 4) * 1000 + 64: rc = dual_group_impl<CL_EULER, 4, 64>(k, a); break;
-      case (CL_EULER * 10 + 4) * 1000 + 128: rc = dual_group_impl<CL_EULER, 4, 128>(k, a); break;
-      case (CL_EULER * 10 + 4) * 1000 + 256: rc = dual_group_impl<CL_EULER, 4, 256>(k, a); break;
+#define IPM_GCASE(CLV, MSV, GV, SFV, TV) \
+  case (((CLV * 10 + MSV) * 1000 + GV) * 10 + SFV) * 10 + TV: rc = dual_group_impl<CLV, MSV, GV, SFV, TV>(k, a); break;
+      IPM_GCASE(CL_BARRIER, 1, 32, 0, 1)
+      IPM_GCASE(CL_BARRIER, 1, 32, 0, 2)
+      IPM_GCASE(CL_QUADRATIC, 1, 32, 0, 1)
+      IPM_GCASE(CL_EULER, 3, 32, 0, 2)
+      IPM_GCASE(CL_EULER, 3, 64, 0, 1)
+      IPM_GCASE(CL_EULER, 4, 64, 0, 2)
+      IPM_GCASE(CL_EULER, 4, 64, 5, 2)
+      IPM_GCASE(CL_EULER, 4, 128, 0, 1)
+      IPM_GCASE(CL_EULER, 4, 128, 5, 1)
+      IPM_GCASE(CL_EULER, 4, 128, 0, 2)
+      IPM_GCASE(CL_EULER, 4, 128, 6, 2)
+      IPM_GCASE(CL_EULER, 4, 256, 6, 1)
+      IPM_GCASE(CL_EULER, 4, 32, 3, 2)
+      IPM_GCASE(CL_EULER, 4, 64, 4, 2)
+#undef IPM_GCASE
     }
     if (rc != -1) return rc;
   }

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libipm.so")
+LIB_PATH = os.environ.get("IPM_LIB", os.path.join(HERE, "libipm.so"))
 
 CLOSURE = {"quadratic": 0, "barrier": 1, "euler": 2}
 FLUX = {"lf_global": 0, "hll": 1, "rusanov": 2}
@@ -29,6 +29,7 @@ EXPORTS = [
     "ipm_get_cell_ids", "ipm_dual_solve", "ipm_flux_update", "ipm_step", "ipm_project_ic", "ipm_warm_start",
     "ipm_moments_from_dual", "ipm_stress_dual", "ipm_get_levels", "ipm_set_levels", "ipm_last_cell_stats",
     "ipm_get_time", "ipm_set_time", "ipm_nccl_unique_id", "ipm_last_kernel_ms", "ipm_enable_timing",
+    "ipm_debug_phase_cycles",
 ]
 
 
@@ -110,6 +111,7 @@ def lib():
             "ipm_nccl_unique_id": (st, [P]),
             "ipm_last_kernel_ms": (st, [P, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
             "ipm_enable_timing": (st, [P, C.c_int32]),
+            "ipm_debug_phase_cycles": (st, [P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -304,6 +306,11 @@ class Context:
         a, b = C.c_float(), C.c_float()
         check(lib().ipm_last_kernel_ms(self.h, C.byref(a), C.byref(b)), "ipm_last_kernel_ms")
         return a.value, b.value
+
+    def debug_phase_cycles(self):
+        out = np.zeros(8, np.uint64)
+        check(lib().ipm_debug_phase_cycles(out.ctypes.data), "ipm_debug_phase_cycles")
+        return out
 
     def run(self, uhat=None, lam=None, t_end=None, n_steps=None, record=False):
         """Algorithm 1 from the IC (or a given state) until t_end or for n_steps (synchronous steps)."""
