@@ -23,22 +23,27 @@
 template <int MS>
 struct GroupLayout {
   static constexpr int MM = MS * (MS + 1) / 2;
-  static constexpr int NS = ((MS + MM) % 2 == 0) ? MS + MM + 1 : MS + MM;
+  // node-buffer row stride: even (16-byte aligned rows for vector loads), not a multiple of 16 doubles
+  static constexpr int NS0 = (MS + MM + 1) & ~1;
+  static constexpr int NS = (NS0 % 16 == 0) ? NS0 + 2 : NS0;
   static constexpr int TB = MS * MS;  // doubles per block (stored column-major)
+  // block stride in shared memory: padded so that lanes reading the same element of different
+  // blocks fall into different banks (a 128-byte stride would put them all in one bank)
+  static constexpr int TBP = (TB % 2 == 0) ? ((TB % 16 == 0) ? TB + 2 : TB) : TB + 1;
   static constexpr int RS = MS > 2 ? MS : 2;  // values per reduction slot
   // doubles per group: 5 vectors + node buffer / L blocks / sum-factorisation stage + reduction + control
   //   direct (SF = 0): union(node buffer, L blocks)
   //   SF > 0:          node buffer, then union(T stage [q][npr][MM], L blocks)
   static __host__ __device__ int region(int N, int Q, int SF, int q1d) {
     const int NP = N * (N + 1) / 2;
-    const int nb = Q * NS, lb = NP * TB;
+    const int nb = Q * NS, lb = NP * TBP;
     if (SF == 0) return nb > lb ? nb : lb;
     const int tb = q1d * (SF * (SF + 1) / 2) * MM;
     return nb + (tb > lb ? tb : lb);
   }
   static __host__ __device__ int per_group(int N, int Q, int G, int SF = 0, int q1d = 0) {
     const int n = N * MS;
-    int w = 5 * n + region(N, Q, SF, q1d) + N * TB + 2 * RS * (G / 32) + 4;
+    int w = 5 * n + region(N, Q, SF, q1d) + N * TBP + 2 * RS * (G / 32) + 4;
     return (w + 1) & ~1;
   }
 };
@@ -69,7 +74,7 @@ __global__ void __launch_bounds__(IPM_GROUP_THREADS) k_dual_group(DualParams P) 
 #endif
   using Lay = GroupLayout<MS>;
   constexpr int NW = G / 32;
-  constexpr int MM = Lay::MM, NS = Lay::NS, TB = Lay::TB;
+  constexpr int MM = Lay::MM, NS = Lay::NS, TB = Lay::TBP;
 #define LIDX(a, b) ((b) * MS + (a))  // element (a, b) of a column-major block
   extern __shared__ __align__(16) double sm[];
   const int N = P.T.N, Q = P.T.Q, QP = P.T.QP;
@@ -324,25 +329,39 @@ __global__ void __launch_bounds__(IPM_GROUP_THREADS) k_dual_group(DualParams P) 
               for (int b = 0; b < MS; ++b) blk[q][a][b] = acc[a <= b ? sym_idx<MS>(a, b) : sym_idx<MS>(b, a)];
           }
         } else {
+          // direct: H_IJ = sum_k (omega_k phi_kI phi_kJ) J_k; the J_k row is loaded once for all of
+          // this thread's blocks
+          double acc[T][MM];
+#pragma unroll
+          for (int q = 0; q < T; ++q)
+#pragma unroll
+            for (int z = 0; z < MM; ++z) acc[q][z] = 0.0;
+          const double* wi[T];
+          const double* pj[T];
 #pragma unroll
           for (int q = 0; q < T; ++q) {
-            if (!owna[q]) continue;
-            double acc[MM];
+            wi[q] = sWPhiT + (owna[q] ? bIa[q] : 0) * QP;
+            pj[q] = sPhiT + (owna[q] ? bJa[q] : 0) * QP;
+          }
+          for (int k = 0; k < Q; ++k) {
+            const double* Jk = nb + k * NS + MS;
+            double jv[MM];
 #pragma unroll
-            for (int z = 0; z < MM; ++z) acc[z] = 0.0;
-            const double* wi = sWPhiT + bIa[q] * QP;
-            const double* pj = sPhiT + bJa[q] * QP;
-            for (int k = 0; k < Q; ++k) {
-              const double f = wi[k] * pj[k];
-              const double* Jk = nb + k * NS + MS;
+            for (int z = 0; z < MM; ++z) jv[z] = Jk[z];
 #pragma unroll
-              for (int z = 0; z < MM; ++z) acc[z] = fma(f, Jk[z], acc[z]);
+            for (int q = 0; q < T; ++q) {
+              const double f = wi[q][k] * pj[q][k];
+#pragma unroll
+              for (int z = 0; z < MM; ++z) acc[q][z] = fma(f, jv[z], acc[q][z]);
             }
+          }
+#pragma unroll
+          for (int q = 0; q < T; ++q)
 #pragma unroll
             for (int a = 0; a < MS; ++a)
 #pragma unroll
-              for (int b = 0; b < MS; ++b) blk[q][a][b] = acc[a <= b ? sym_idx<MS>(a, b) : sym_idx<MS>(b, a)];
-          }
+              for (int b = 0; b < MS; ++b)
+                blk[q][a][b] = acc[q][a <= b ? sym_idx<MS>(a, b) : sym_idx<MS>(b, a)];
         }
         for (int r = t; r < n; r += G) dd[r] = -g[r];
         gsync();  // node buffer / T stage dead from here: L blocks reuse them
