@@ -508,6 +508,16 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   k.stream = c->stream;
   k.sm_count = sms;
   k.smem_optin = (size_t)optin;
+  // large cells (the on-chip group kernel needs <= 256 threads x 2 blocks): L2-resident scratch
+  if (N * (N + 1) / 2 > 512 && m == 4) {
+    k.big_ctas = sms;
+    const size_t nd = ipm::big_scratch_doubles(N, Q, m) * (size_t)sms;
+    k.big_scratch = dalloc<double>(nd, c->owned);
+    if (!k.big_scratch) {
+      ipm_destroy(c);
+      return fail(IPM_ERR_CUDA, "cudaMalloc (big-cell scratch) failed");
+    }
+  }
   // IPM_DUAL_KERNEL=warp selects the warp-per-cell dual kernel (comparison / tests)
   const char* dk = std::getenv("IPM_DUAL_KERNEL");
   k.force_warp_kernel = (dk && std::strcmp(dk, "warp") == 0) ? 1 : 0;

@@ -1,0 +1,450 @@
+// ipm_dual_big.cuh — dual solve for large cells (config 5: N = 56, m = 4, n = 224, Q = 1000).
+// (included inside namespace ipm by ipm_kernels.cu)
+//
+// One CTA (NT threads) per cell, persistent over an atomic cell queue.  The per-cell working set
+// (node data Q x (m + m(m+1)/2), Hessian blocks N(N+1)/2 x m^2, diagonal inverses) does not fit on
+// chip, so it lives in a per-CTA global scratch slice that stays L2-resident (148 CTAs x ~330 KB);
+// the basis tables are read from global memory (L2).  Vectors (lambda, trial, uhat, g, d) are in
+// shared memory.  Same method as k_dual_group: eval / gradient / Hessian blocks / blocked Cholesky
+// with the forward solve folded in / back substitution / Armijo on L (reading 3').
+#pragma once
+
+template <int MS>
+struct BigLayout {
+  static constexpr int MM = MS * (MS + 1) / 2;
+  static constexpr int NS = MS + MM;
+  static constexpr int TB = MS * MS;
+  // per-CTA global scratch (doubles)
+  static __host__ __device__ size_t scratch(int N, int Q) {
+    return (size_t)Q * NS + (size_t)(N * (N + 1) / 2) * TB + (size_t)N * TB + 64;
+  }
+};
+
+template <int CL, int MS, int NT>
+__global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restrict__ scratch) {
+  using Lay = BigLayout<MS>;
+  constexpr int NW = NT / 32;
+  constexpr int MM = Lay::MM, NS = Lay::NS, TB = Lay::TB;
+#define BIDX(a, b) ((b) * MS + (a))
+  extern __shared__ __align__(16) double sm[];
+  const int N = P.T.N, Q = P.T.Q, QP = P.T.QP;
+  const double* __restrict__ PhiT = P.T.PhiT;
+  const double* __restrict__ WPhiT = P.T.WPhiT;
+  const double* __restrict__ omega = P.T.omega;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int nmax = N * MS;
+  double* lam = sm;
+  double* lt = lam + nmax;
+  double* uh = lt + nmax;
+  double* g = uh + nmax;
+  double* dd = g + nmax;
+  double* red = dd + nmax;  // [2][4][NW]
+  int* ctl = (int*)(red + 8 * NW);
+  double* nb = scratch + (size_t)blockIdx.x * Lay::scratch(N, Q);
+  double* Hb = nb + (size_t)Q * NS;                 // blocks, row-major lower enumeration
+  double* Linv = Hb + (size_t)(N * (N + 1) / 2) * TB;
+  const DualLaunch& A = P.a;
+  long long my_iters = 0, my_failed = 0;
+  int my_worst = 0;
+  double my_rate = 0.0;
+  int slot = 0;
+
+  auto bsum = [&](double* v, int cnt) {  // block-wide sums of cnt (<= 4) values
+    double* r = red + slot * 4 * NW;
+    slot ^= 1;
+    for (int a = 0; a < cnt; ++a) {
+      const double s = warp_sum(v[a]);
+      if (lane == 0) r[a * NW + wid] = s;
+    }
+    __syncthreads();
+    for (int a = 0; a < cnt; ++a) {
+      double s = 0.0;
+      for (int w = 0; w < NW; ++w) s += r[a * NW + w];
+      v[a] = s;
+    }
+  };
+  auto eval = [&](const double* lamv, int Nl, double& s1, double& s2) -> bool {
+    double v[2] = {0.0, 0.0};
+    bool bad = false;
+    for (int k = t; k < Q; k += NT) {
+      double Lam[MS];
+#pragma unroll
+      for (int a = 0; a < MS; ++a) Lam[a] = 0.0;
+      for (int i = 0; i < Nl; ++i) {
+        const double ph = PhiT[(size_t)i * QP + k];
+#pragma unroll
+        for (int a = 0; a < MS; ++a) Lam[a] = fma(lamv[i * MS + a], ph, Lam[a]);
+      }
+      double u[MS], J[MM], ss;
+      if (!Closure<CL, MS>::eval(Lam, u, J, ss, P.cl)) bad = true;
+      double* row = nb + (size_t)k * NS;
+#pragma unroll
+      for (int a = 0; a < MS; ++a) row[a] = u[a];
+#pragma unroll
+      for (int q = 0; q < MM; ++q) row[MS + q] = J[q];
+      v[0] = fma(omega[k], ss, v[0]);
+      v[1] = fma(omega[k], fabs(ss), v[1]);
+    }
+    if (bad) v[1] = INFINITY;
+    bsum(v, 2);
+    s1 = v[0];
+    s2 = v[1];
+    return isfinite(v[0]) && isfinite(v[1]);
+  };
+  auto grad = [&](int Nl) -> double {
+    const int n = Nl * MS;
+    double part[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int r = t; r < n; r += NT) {
+      const int i = r / MS, a = r - i * MS;
+      const double* wp = WPhiT + (size_t)i * QP;
+      double s0 = 0.0, s1 = 0.0;
+      int k = 0;
+      for (; k + 1 < Q; k += 2) {
+        s0 = fma(wp[k], nb[(size_t)k * NS + a], s0);
+        s1 = fma(wp[k + 1], nb[(size_t)(k + 1) * NS + a], s1);
+      }
+      if (k < Q) s0 = fma(wp[k], nb[(size_t)k * NS + a], s0);
+      const double gr = (s0 + s1) - uh[r];
+      g[r] = gr;
+      part[a] = fma(gr, gr, part[a]);
+    }
+    bsum(part, MS);
+    double crit = 0.0;
+    for (int a = 0; a < MS; ++a) crit += sqrt(part[a]);
+    return crit;
+  };
+  auto dot2 = [&](const double* x, const double* y, int n, double& d, double& ad) {
+    double v[2] = {0.0, 0.0};
+    for (int r = t; r < n; r += NT) {
+      const double p = x[r] * y[r];
+      v[0] += p;
+      v[1] += fabs(p);
+    }
+    bsum(v, 2);
+    d = v[0];
+    ad = v[1];
+  };
+  auto blk_ij = [](int p, int& I, int& J) {
+    I = (int)((sqrtf(8.0f * p + 1.0f) - 1.0f) * 0.5f);
+    while (I * (I + 1) / 2 > p) --I;
+    while ((I + 1) * (I + 2) / 2 <= p) ++I;
+    J = p - I * (I + 1) / 2;
+  };
+
+  for (;;) {
+    if (t == 0) ctl[0] = atomicAdd(&P.sc->work_counter, 1);
+    __syncthreads();
+    const int64_t cell = ctl[0];
+    if (cell >= A.cells) break;
+    const int lvl = A.level ? A.level[cell] : 0;
+    const int Nl = (P.ad.n_levels > 0) ? P.ad.Nl[lvl] : N;
+    const int n = Nl * MS, NPl = Nl * (Nl + 1) / 2;
+    const double* gu = A.uhat + cell * nmax;
+    double* gl = A.lam + cell * nmax;
+    for (int r = t; r < n; r += NT) {
+      uh[r] = gu[r];
+      lam[r] = gl[r];
+    }
+    __syncthreads();
+    int status = 0, l = 0;
+    double s1, s2, crit = INFINITY;
+    bool nb_is_lam = eval(lam, Nl, s1, s2);
+    if (!nb_is_lam) {
+      status = 4;
+    } else {
+      crit = grad(Nl);
+      double L0, scale;
+      {
+        double d1, d2;
+        dot2(lam, uh, n, d1, d2);
+        L0 = s1 - d1;
+        scale = s2 + d2;
+      }
+      for (;;) {
+        if (crit < P.nw.tau) break;
+        if (P.nw.mode == 1 && l == 1) break;
+        if (l == P.nw.max_newton) {
+          status = 1;
+          break;
+        }
+        // Hessian blocks H_IJ = sum_k omega_k phi_kI phi_kJ J_k
+        for (int p = t; p < NPl; p += NT) {
+          int I, J;
+          blk_ij(p, I, J);
+          double acc[MM];
+#pragma unroll
+          for (int z = 0; z < MM; ++z) acc[z] = 0.0;
+          const double* wi = WPhiT + (size_t)I * QP;
+          const double* pj = PhiT + (size_t)J * QP;
+          for (int k = 0; k < Q; ++k) {
+            const double f = wi[k] * pj[k];
+            const double* Jk = nb + (size_t)k * NS + MS;
+#pragma unroll
+            for (int z = 0; z < MM; ++z) acc[z] = fma(f, Jk[z], acc[z]);
+          }
+          double* o = Hb + (size_t)p * TB;
+#pragma unroll
+          for (int a = 0; a < MS; ++a)
+#pragma unroll
+            for (int b = 0; b < MS; ++b) o[BIDX(a, b)] = acc[a <= b ? sym_idx<MS>(a, b) : sym_idx<MS>(b, a)];
+        }
+        for (int r = t; r < n; r += NT) dd[r] = -g[r];
+        __syncthreads();
+        // blocked right-looking Cholesky, blocks resident in the scratch slice; forward solve folded
+        bool chol_ok = true;
+        for (int K = 0; K < Nl; ++K) {
+          if (t == 0) {
+            double* Bk = Hb + (size_t)(K * (K + 1) / 2 + K) * TB;
+            double L[MS][MS], li[MS][MS], inv[MS];
+            bool ok = true;
+#pragma unroll
+            for (int a = 0; a < MS; ++a)
+#pragma unroll
+              for (int b = 0; b < MS; ++b) L[a][b] = Bk[BIDX(a, b)];
+#pragma unroll
+            for (int c = 0; c < MS; ++c) {
+              double sv = L[c][c];
+#pragma unroll
+              for (int x = 0; x < c; ++x) sv = fma(-L[c][x], L[c][x], sv);
+              if (!(sv > 0.0) || !isfinite(sv)) ok = false;
+              const double rs = rsqrt(sv);
+              inv[c] = rs;
+              L[c][c] = sv * rs;
+#pragma unroll
+              for (int r = c + 1; r < MS; ++r) {
+                double v = L[r][c];
+#pragma unroll
+                for (int x = 0; x < c; ++x) v = fma(-L[r][x], L[c][x], v);
+                L[r][c] = v * rs;
+              }
+            }
+#pragma unroll
+            for (int c = 0; c < MS; ++c) {
+              li[c][c] = inv[c];
+#pragma unroll
+              for (int r = c + 1; r < MS; ++r) {
+                double v = 0.0;
+#pragma unroll
+                for (int x = c; x < r; ++x) v = fma(L[r][x], li[x][c], v);
+                li[r][c] = -inv[r] * v;
+              }
+            }
+            double* oi = Linv + (size_t)K * TB;
+#pragma unroll
+            for (int a = 0; a < MS; ++a)
+#pragma unroll
+              for (int b = 0; b < MS; ++b) {
+                Bk[BIDX(a, b)] = (b <= a) ? L[a][b] : 0.0;
+                oi[BIDX(a, b)] = (b <= a) ? li[a][b] : 0.0;
+              }
+            double bk[MS];
+#pragma unroll
+            for (int a = 0; a < MS; ++a) bk[a] = dd[K * MS + a];
+#pragma unroll
+            for (int a = 0; a < MS; ++a) {
+              double v = 0.0;
+#pragma unroll
+              for (int x = 0; x <= a; ++x) v = fma(li[a][x], bk[x], v);
+              dd[K * MS + a] = v;
+            }
+            ctl[1] = ok ? 0 : 1;
+          }
+          __syncthreads();
+          if (ctl[1]) {
+            chol_ok = false;
+            break;
+          }
+          const double* Li = Linv + (size_t)K * TB;
+          for (int I = K + 1 + t; I < Nl; I += NT) {
+            double* Bik = Hb + (size_t)(I * (I + 1) / 2 + K) * TB;
+            double A_[MS][MS], X[MS][MS], yk[MS];
+#pragma unroll
+            for (int a = 0; a < MS; ++a)
+#pragma unroll
+              for (int b = 0; b < MS; ++b) A_[a][b] = Bik[BIDX(a, b)];
+#pragma unroll
+            for (int r = 0; r < MS; ++r)
+#pragma unroll
+              for (int c = 0; c < MS; ++c) {
+                double v = 0.0;
+#pragma unroll
+                for (int x = 0; x <= c; ++x) v = fma(A_[r][x], Li[BIDX(c, x)], v);
+                X[r][c] = v;
+              }
+#pragma unroll
+            for (int x = 0; x < MS; ++x) yk[x] = dd[K * MS + x];
+#pragma unroll
+            for (int r = 0; r < MS; ++r) {
+              double v = dd[I * MS + r];
+#pragma unroll
+              for (int c = 0; c < MS; ++c) {
+                Bik[BIDX(r, c)] = X[r][c];
+                v = fma(-X[r][c], yk[c], v);
+              }
+              dd[I * MS + r] = v;
+            }
+          }
+          __syncthreads();
+          // trailing: blocks (I, J) with I >= J > K
+          const int R = Nl - 1 - K, ntr = R * (R + 1) / 2;
+          for (int e = t; e < ntr; e += NT) {
+            int a_, b_;
+            blk_ij(e, a_, b_);
+            const int I = K + 1 + a_, J = K + 1 + b_;
+            const double* Lik = Hb + (size_t)(I * (I + 1) / 2 + K) * TB;
+            const double* Ljk = Hb + (size_t)(J * (J + 1) / 2 + K) * TB;
+            double* Bij = Hb + (size_t)(I * (I + 1) / 2 + J) * TB;
+            double acc[MS][MS];
+#pragma unroll
+            for (int a = 0; a < MS; ++a)
+#pragma unroll
+              for (int b = 0; b < MS; ++b) acc[a][b] = Bij[BIDX(a, b)];
+#pragma unroll
+            for (int x = 0; x < MS; ++x) {
+              double ci[MS], cj[MS];
+#pragma unroll
+              for (int a = 0; a < MS; ++a) {
+                ci[a] = Lik[BIDX(a, x)];
+                cj[a] = Ljk[BIDX(a, x)];
+              }
+#pragma unroll
+              for (int r = 0; r < MS; ++r)
+#pragma unroll
+                for (int c = 0; c < MS; ++c) acc[r][c] = fma(-ci[r], cj[c], acc[r][c]);
+            }
+#pragma unroll
+            for (int a = 0; a < MS; ++a)
+#pragma unroll
+              for (int b = 0; b < MS; ++b) Bij[BIDX(a, b)] = acc[a][b];
+          }
+          __syncthreads();
+        }
+        if (!chol_ok) {
+          status = 2;
+          break;
+        }
+        // back substitution L^T d = y (warp 0)
+        if (wid == 0) {
+          for (int K = Nl - 1; K >= 0; --K) {
+            const double* Li = Linv + (size_t)K * TB;
+            double dk[MS];
+#pragma unroll
+            for (int c = 0; c < MS; ++c) {
+              double v = 0.0;
+#pragma unroll
+              for (int x = c; x < MS; ++x) v = fma(Li[BIDX(x, c)], dd[K * MS + x], v);
+              dk[c] = v;
+            }
+            __syncwarp();
+            if (lane < MS) {
+#pragma unroll
+              for (int c = 0; c < MS; ++c)
+                if (c == lane) dd[K * MS + c] = dk[c];
+            }
+            for (int e = lane; e < K * MS; e += 32) {
+              const int J = e / MS, c = e - J * MS;
+              const double* Lkj = Hb + (size_t)(K * (K + 1) / 2 + J) * TB;
+              double v = dd[J * MS + c];
+#pragma unroll
+              for (int x = 0; x < MS; ++x) v = fma(-Lkj[BIDX(x, c)], dk[x], v);
+              dd[J * MS + c] = v;
+            }
+            __syncwarp();
+          }
+        }
+        __syncthreads();
+        double slope, dummy;
+        dot2(g, dd, n, slope, dummy);
+        double alpha = 1.0;
+        bool accepted = false;
+        for (int h = 0; h <= P.nw.max_halvings; ++h) {
+          for (int r = t; r < n; r += NT) lt[r] = lam[r] + alpha * dd[r];
+          __syncthreads();
+          double t1, t2;
+          const bool okt = eval(lt, Nl, t1, t2);
+          nb_is_lam = false;
+          if (okt) {
+            double d1, d2;
+            dot2(lt, uh, n, d1, d2);
+            const double Lt = t1 - d1;
+            if (Lt <= L0 + P.nw.armijo_c * alpha * slope + 1e-12 * scale) {
+              crit = grad(Nl);
+              for (int r = t; r < n; r += NT) lam[r] = lt[r];
+              nb_is_lam = true;
+              L0 = Lt;
+              scale = t2 + d2;
+              accepted = true;
+              break;
+            }
+          }
+          alpha *= 0.5;
+        }
+        if (!accepted) {
+          status = 3;
+          break;
+        }
+        ++l;
+        __syncthreads();
+      }
+    }
+    __syncthreads();
+    if (!nb_is_lam && status != 4) {
+      double t1, t2;
+      eval(lam, Nl, t1, t2);
+    }
+    int Nnew = Nl;
+    if (P.ad.n_levels > 0 && A.level_new) {
+      const int Nprev = lvl > 0 ? P.ad.Nl[lvl - 1] : P.ad.Nprev0;
+      double v[2] = {0.0, 0.0};
+      for (int i = t; i < Nl; i += NT) {
+        const double h = g[i * MS] + uh[i * MS];
+        v[1] = fma(h, h, v[1]);
+        if (i >= Nprev) v[0] = fma(h, h, v[0]);
+      }
+      bsum(v, 2);
+      const double S = v[1] > 0.0 ? v[0] / v[1] : 0.0;
+      int nl = lvl;
+      if (status == 0 || P.nw.mode == 1) {
+        if (S < P.ad.delta_dec && lvl > 0)
+          nl = lvl - 1;
+        else if (S > P.ad.delta_inc && lvl < P.ad.n_levels - 1)
+          nl = lvl + 1;
+      }
+      Nnew = P.ad.Nl[nl];
+      if (t == 0) A.level_new[cell] = nl;
+    }
+    for (int r = t; r < nmax; r += NT) gl[r] = (r < Nnew * MS) ? lam[r] : 0.0;
+    if (t == 0) {
+      if (A.iters) A.iters[cell] = l;
+      if (A.status) A.status[cell] = status;
+      if (A.crit) A.crit[cell] = crit;
+      my_iters += l;
+      if (status != 0) {
+        my_failed += 1;
+        my_worst = max(my_worst, status);
+      }
+    }
+    if (status != 4) {
+      for (int k = t; k < Q; k += NT) {
+        const double* u = nb + (size_t)k * NS;
+        if (A.uq) {
+          double* o = A.uq + (cell * Q + k) * MS;
+#pragma unroll
+          for (int a = 0; a < MS; ++a) o[a] = u[a];
+        }
+        if (A.want_rate) my_rate = fmax(my_rate, node_rate<CL, MS>(u, P.mesh, cell, P.cl.gamma));
+      }
+    }
+    __syncthreads();
+  }
+  my_rate = warp_max(my_rate);
+  if (lane == 0) {
+    if (A.want_rate) atomicMax(&P.sc->rate_bits, (unsigned long long)__double_as_longlong(my_rate));
+    if (t == 0) {
+      if (my_iters) atomicAdd(&P.sc->newton_iters, (unsigned long long)my_iters);
+      if (my_failed) atomicAdd(&P.sc->failed, (unsigned long long)my_failed);
+      if (my_worst) atomicMax(&P.sc->worst, my_worst);
+    }
+  }
+#undef BIDX
+}

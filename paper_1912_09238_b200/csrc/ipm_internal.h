@@ -100,10 +100,13 @@ struct KernelCtx {
   int sm_count;
   size_t smem_optin;
   int force_warp_kernel;  // 1: always use the warp-per-cell dual kernel (tests, comparison)
+  double* big_scratch;    // per-CTA scratch of the large-cell dual kernel (config 5), or null
+  int big_ctas;
 };
 
 // launchers (ipm_kernels.cu); return 0 on success, else a cudaError_t / -1 unsupported
 int launch_step_begin(const KernelCtx& k, double rate0);
+size_t big_scratch_doubles(int N, int Q, int m);
 int debug_phase_cycles(unsigned long long* out);
 int launch_dual(const KernelCtx& k, const DualLaunch& a);
 int launch_dt(const KernelCtx& k, double t_end, double dt_fixed, double cfl);

@@ -379,6 +379,7 @@ __global__ void __launch_bounds__(512) k_dual_warp(DualParams P) {
 }
 
 #include "ipm_dual_group.cuh"
+#include "ipm_dual_big.cuh"
 
 // ------------------------------------------------------------------------------------------------
 // flux kernel (variant B: node states from the dual kernel)
@@ -390,18 +391,22 @@ struct FluxParams {
   Adapt ad;
   FluxLaunch a;
   StepScalars* sc;
+  int tables_in_smem;
 };
 
 template <int FX, int MS, int MK>
 __global__ void __launch_bounds__(256) k_flux_warp(FluxParams P) {
   extern __shared__ __align__(16) double sm[];
   const int N = P.T.N, Q = P.T.Q, QP = P.T.QP;
-  double* sWPhiT = sm;
-  for (int t = threadIdx.x; t < N * QP; t += blockDim.x) sWPhiT[t] = P.T.WPhiT[t];
-  __syncthreads();
+  // basis table staged in shared memory when it fits (P.tables_in_smem), else read from L2
+  const double* sWPhiT = P.tables_in_smem ? sm : P.T.WPhiT;
+  if (P.tables_in_smem) {
+    for (int t = threadIdx.x; t < N * QP; t += blockDim.x) sm[t] = P.T.WPhiT[t];
+    __syncthreads();
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
-  double* q = sm + N * QP + (size_t)warp * (Q * MS + 1);
+  double* q = sm + (P.tables_in_smem ? N * QP : 0) + (size_t)warp * (Q * MS + 1);
   const int nmax = N * MS;
   const double dt = P.sc->dt;
   const double gam = P.cl.gamma;
@@ -600,19 +605,21 @@ __global__ void k_warm_start(int64_t cells, int N, ClParams cp, const double* __
 // u_s(lambda^T phi(xi_k)) and CFL rate
 template <int CL, int MS>
 __global__ void k_nodes(Tables T, Mesh mesh, ClParams cp, const double* __restrict__ lam_g, double* __restrict__ uhat,
-                        double* __restrict__ uq, StepScalars* sc) {
+                        double* __restrict__ uq, StepScalars* sc, int tables_in_smem) {
   using Lay = DualLayout<MS>;
   extern __shared__ __align__(16) double sm[];
   const int N = T.N, Q = T.Q, QP = T.QP;
-  double* sPhiT = sm;
-  double* sWPhiT = sm + N * QP;
-  for (int t = threadIdx.x; t < N * QP; t += blockDim.x) {
-    sPhiT[t] = T.PhiT[t];
-    sWPhiT[t] = T.WPhiT[t];
+  const double* sPhiT = tables_in_smem ? sm : T.PhiT;
+  const double* sWPhiT = tables_in_smem ? sm + N * QP : T.WPhiT;
+  if (tables_in_smem) {
+    for (int t = threadIdx.x; t < N * QP; t += blockDim.x) {
+      sm[t] = T.PhiT[t];
+      sm[N * QP + t] = T.WPhiT[t];
+    }
+    __syncthreads();
   }
-  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  double* lam = sm + 2 * N * QP + (size_t)warp * (N * MS + Q * Lay::NS + 1);
+  double* lam = sm + (tables_in_smem ? 2 * N * QP : 0) + (size_t)warp * (N * MS + Q * Lay::NS + 1);
   double* nb = lam + N * MS;
   double my_rate = 0.0;
   int bad = 0;
@@ -782,6 +789,10 @@ static void group_shape(int N, int& G, int& T) {
       }
 }
 
+size_t big_scratch_doubles(int N, int Q, int m) {
+  return m == 4 ? BigLayout<4>::scratch(N, Q) : 0;
+}
+
 int launch_dual(const KernelCtx& k, const DualLaunch& a) {
   if (a.cells == 0) return 0;
   if (!k.force_warp_kernel) {
@@ -813,6 +824,17 @@ int launch_dual(const KernelCtx& k, const DualLaunch& a) {
 #undef IPM_GCASE
     }
     if (rc != -1) return rc;
+    // cells too large for the on-chip group kernel (config 5): CTA per cell, L2-resident scratch
+    if (k.big_scratch && k.closure == CL_EULER && k.m == 4) {
+      constexpr int NT = 512;
+      const size_t smem = ((size_t)5 * k.T.N * 4 + 8 * (NT / 32) + 8) * 8;
+      auto kern = k_dual_big<CL_EULER, 4, NT>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      const int grid = (int)std::min<int64_t>(a.cells, (int64_t)k.big_ctas);
+      DualParams P{k.T, k.mesh, k.nw, k.ad, k.cl, a, k.sc};
+      kern<<<grid, NT, smem, S(k)>>>(P, k.big_scratch);
+      return (int)cudaGetLastError();
+    }
   }
   switch (k.closure * 10 + k.m) {
     case CL_QUADRATIC * 10 + 1: return dual_impl<CL_QUADRATIC, 1>(k, a);
@@ -827,9 +849,12 @@ int launch_dual(const KernelCtx& k, const DualLaunch& a) {
 
 template <int FX, int MS, int MK>
 static int flux_impl(const KernelCtx& k, const FluxLaunch& a) {
-  const int warps = 8;
-  const size_t smem = ((size_t)k.T.N * k.T.QP + warps * (k.T.Q * MS + 1)) * 8;
-  if (smem > k.smem_optin) return -1;
+  const size_t tab = (size_t)k.T.N * k.T.QP * 8, pw = (size_t)(k.T.Q * MS + 1) * 8;
+  int in_smem = (tab + 4 * pw <= k.smem_optin) ? 1 : 0;
+  const size_t base = in_smem ? tab : 0;
+  int warps = (int)std::min<size_t>(8, (k.smem_optin - base) / pw);
+  if (warps < 1) return -1;
+  const size_t smem = base + warps * pw;
   auto kern = k_flux_warp<FX, MS, MK>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 1;
@@ -838,7 +863,7 @@ static int flux_impl(const KernelCtx& k, const FluxLaunch& a) {
   const int64_t want = (k.mesh.cells + warps - 1) / warps;
   int grid = (int)std::min<int64_t>(want, (int64_t)k.sm_count * per_sm * 4);
   if (grid < 1) grid = 1;
-  FluxParams P{k.T, k.mesh, k.cl, k.ad, a, k.sc};
+  FluxParams P{k.T, k.mesh, k.cl, k.ad, a, k.sc, in_smem};
   kern<<<grid, warps * 32, smem, S(k)>>>(P);
   return (int)cudaGetLastError();
 }
@@ -860,8 +885,10 @@ int launch_flux(const KernelCtx& k, const FluxLaunch& a) {
 template <int MS>
 static int ic_impl(const KernelCtx& k, const double* region, const double* split, int kind, int nx, double x0,
                    double y0, double dx, double dy, const int32_t* level, double* uhat) {
-  const int warps = 8;
-  const size_t smem = (size_t)warps * (k.T.Q * MS + 1) * 8;
+  const size_t pw = (size_t)(k.T.Q * MS + 1) * 8;
+  const int warps = (int)std::min<size_t>(8, k.smem_optin / pw);
+  if (warps < 1) return -1;
+  const size_t smem = (size_t)warps * pw;
   auto kern = k_project_ic<MS>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t want = (k.mesh.cells + warps - 1) / warps;
@@ -891,14 +918,17 @@ static int warm_impl(const KernelCtx& k, const double* uhat, double* lam) {
 template <int CL, int MS>
 static int nodes_impl(const KernelCtx& k, const double* lam, double* uhat, double* uq) {
   using Lay = DualLayout<MS>;
-  const int warps = 4;
-  const size_t smem = ((size_t)2 * k.T.N * k.T.QP + warps * (k.T.N * MS + k.T.Q * Lay::NS + 1)) * 8;
-  if (smem > k.smem_optin) return -1;
+  const size_t tab = (size_t)2 * k.T.N * k.T.QP * 8, pw = (size_t)(k.T.N * MS + k.T.Q * Lay::NS + 1) * 8;
+  const int in_smem = (tab + 4 * pw <= k.smem_optin) ? 1 : 0;
+  const size_t base = in_smem ? tab : 0;
+  const int warps = (int)std::min<size_t>(4, (k.smem_optin - base) / pw);
+  if (warps < 1) return -1;
+  const size_t smem = base + warps * pw;
   auto kern = k_nodes<CL, MS>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t want = (k.mesh.cells + warps - 1) / warps;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)k.sm_count * 4));
-  kern<<<grid, warps * 32, smem, S(k)>>>(k.T, k.mesh, k.cl, lam, uhat, uq, k.sc);
+  kern<<<grid, warps * 32, smem, S(k)>>>(k.T, k.mesh, k.cl, lam, uhat, uq, k.sc, in_smem);
   return (int)cudaGetLastError();
 }
 
