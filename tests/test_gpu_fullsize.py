@@ -1,0 +1,165 @@
+"""Full-size parity in the launch configuration bench.py times (BASELINE configs 3-5 sizes):
+the CUDA path runs on the whole mesh; the oracle recomputes sampled cells one by one.
+
+  dual solve   : sampled cells, oracle dual_solve_cell from the same seeded stress state
+  flux update  : sampled interior cells with a fixed dt; the oracle solves the cell and its
+                 neighbours itself and applies its own update on a one-cell stencil mesh
+"""
+import numpy as np
+import pytest
+
+from inputs import configs
+from inputs.generators import bump_channel_mesh
+
+from .gpu_common import stress_inputs, to_np
+
+pytestmark = pytest.mark.gpu
+
+N_SAMPLE = 48
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+
+    if not t.cuda.is_available():
+        pytest.fail("GPU test needs CUDA")
+    return t
+
+
+def _setup(torch, cfg, ma=None):
+    import oracle
+    from paper_1912_09238_b200 import Context
+
+    g = Context(cfg, ma)
+    base, z, amp = stress_inputs(cfg, seed=77, ma=ma)
+    lam_s = g.zeros()
+    g.ipm_stress_dual(torch.from_numpy(base).cuda(), torch.from_numpy(z).cuda(), amp[0], amp[1], lam_s)
+    u = g.zeros()
+    g.ipm_moments_from_dual(lam_s, u)
+    lam0 = g.zeros()
+    g.ipm_warm_start(u, lam0)
+    return g, base, z, amp, u, lam0
+
+
+def _oracle_cells(cfg, base, z, amp, cells, ma_small=None):
+    """oracle on a context whose cells are the sampled ones (geometry irrelevant for the dual solve)"""
+    import oracle
+
+    small = dict(cfg)
+    small["mesh"] = dict(kind="1d", nx=len(cells), x0=0.0, x1=1.0)
+    small["levels"] = None
+    o = oracle.Oracle(small)
+    lam_star = o.stress_dual(base[cells], z[cells], amp)
+    u = o.moments_from_dual_all(lam_star)
+    lam = o.warm_start(u)
+    return o, u, lam
+
+
+@pytest.mark.parametrize("name,nx", [("cfg3", 1024), ("cfg5", 96)])
+def test_dual_solve_full_size_sampled(torch, name, nx):
+    cfg = configs.get(name, mesh=dict(nx=nx, ny=nx))
+    g, base, z, amp, u, lam0 = _setup(torch, cfg)
+    it = g.zeros(g.cells, dtype=torch.int32)
+    st = g.zeros(g.cells, dtype=torch.int32)
+    lam = lam0.clone()
+    g.ipm_dual_solve(u, lam, "full", it, st)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(5)
+    cells = np.sort(rng.choice(g.cells, size=N_SAMPLE if name == "cfg3" else 12, replace=False))
+    o, u_o, lam_o = _oracle_cells(cfg, base, z, amp, cells)
+    it_o, st_o, _ = o.dual_solve_all(u_o, lam_o)
+    lg, itg, stg = to_np(lam)[cells], to_np(it)[cells], to_np(st)[cells]
+    np.testing.assert_array_equal(stg, st_o)
+    assert np.abs(itg - it_o).max() <= 1
+    scale = np.abs(lam_o).max(axis=(0, 1))
+    assert (np.abs(lg - lam_o) / scale).max() < 1e-9
+    assert (to_np(st) == 0).all()
+
+
+def test_flux_update_full_size_sampled_cart(torch):
+    import oracle
+
+    cfg = configs.get("cfg3")
+    nx = cfg["mesh"]["nx"]
+    g, base, z, amp, u, lam0 = _setup(torch, cfg)
+    lam = lam0.clone()
+    g.ipm_dual_solve(u, lam, "full")
+    dt = 2e-5
+    unew = g.zeros()
+    g.ipm_flux_update(lam, u, unew, dt)
+    torch.cuda.synchronize()
+    un = to_np(unew)
+    rng = np.random.default_rng(6)
+    h = 1.0 / nx
+    for _ in range(12):
+        ix, iy = rng.integers(1, nx - 1, size=2)
+        ids = [(iy + dy) * nx + (ix + dx) for dy in (-1, 0, 1) for dx in (-1, 0, 1)]
+        small = configs.get("cfg3", mesh=dict(nx=3, ny=3, x0=(ix - 1) * h, x1=(ix + 2) * h,
+                                               y0=(iy - 1) * h, y1=(iy + 2) * h))
+        o = oracle.Oracle(small)
+        lam_star = o.stress_dual(base[ids], z[ids], amp)
+        uo = o.moments_from_dual_all(lam_star)
+        lo = o.warm_start(uo)
+        o.dual_solve_all(uo, lo)
+        new_o = o.flux_update(lo, uo, dt)
+        ref = new_o[4]
+        sc = np.maximum(np.abs(ref[0]), 1e-300)
+        err = (np.abs(un[ids[4]] - ref) / sc).max()
+        assert err < 1e-9, (ix, iy, err)
+
+
+def test_cfg4_full_mesh_one_shot_sampled(torch):
+    """cfg 4 at its full 200k-triangle mesh: one One-Shot dual step (adaptive levels at the initial
+    degree) on the seeded stress state, then the c-form update with fixed dt on sampled cells."""
+    import oracle
+    from paper_1912_09238_b200 import Context
+
+    cfg = configs.get("cfg4")
+    m = cfg["mesh"]
+    vert, tri, tags = bump_channel_mesh(m["nx_pts"], m["ny_pts"], m["seed"])
+    cfg_nl = dict(cfg, levels=None)  # whole degree-5 basis in every cell for the sampled check
+    g, base, z, amp, u, lam0 = _setup(torch, cfg_nl, (vert, tri, tags))
+    assert g.cells > 190_000
+    lam = lam0.clone()
+    it = g.zeros(g.cells, dtype=torch.int32)
+    g.ipm_dual_solve(u, lam, "one_step", it)
+    dt = 1e-4
+    unew = g.zeros()
+    g.ipm_flux_update(lam, u, unew, dt)
+    torch.cuda.synchronize()
+    un, itg = to_np(unew), to_np(it)
+    # neighbours by shared edges (test-side, numpy)
+    from collections import defaultdict
+
+    edges = defaultdict(list)
+    for t_ in range(tri.shape[0]):
+        for e in range(3):
+            a, b = sorted((tri[t_, e], tri[t_, (e + 1) % 3]))
+            edges[(a, b)].append(t_)
+    rng = np.random.default_rng(7)
+    checked = 0
+    while checked < 10:
+        c = int(rng.integers(0, tri.shape[0]))
+        nbrs = []
+        for e in range(3):
+            a, b = sorted((tri[c, e], tri[c, (e + 1) % 3]))
+            nbrs += [x for x in edges[(a, b)] if x != c]
+        if len(nbrs) != 3:
+            continue
+        ids = [c] + nbrs
+        vid = np.unique(tri[ids].ravel())
+        remap = {v: i for i, v in enumerate(vid)}
+        sub_tri = np.array([[remap[v] for v in tri[t_]] for t_ in ids], dtype=np.int32)
+        sub_tags = tags[ids].copy()
+        o = oracle.Oracle(dict(cfg_nl, newton="one_step"), (vert[vid], sub_tri, sub_tags))
+        lam_star = o.stress_dual(base[ids], z[ids], amp)
+        uo = o.moments_from_dual_all(lam_star)
+        lo = o.warm_start(uo)
+        ito, _, _ = o.dual_solve_all(uo, lo)
+        assert abs(int(ito[0]) - int(itg[c])) <= 1
+        new_o = o.flux_update(lo, uo, dt)
+        sc = np.maximum(np.abs(new_o[0][0]), 1e-300)
+        err = (np.abs(un[c] - new_o[0]) / sc).max()
+        assert err < 1e-9, (c, err)
+        checked += 1
