@@ -120,7 +120,7 @@ typedef struct {
   /* distribution: the context owns part (rank) of a px x py block decomposition (cartesian)
    * or of the Morton-ordered cell list (tri); nranks = 1 -> whole mesh */
   int32_t rank, nranks, px, py;
-  const void *nccl_id;       /* 128-byte ncclUniqueId (host) when nranks > 1 */
+  const void *reserved_ptr;  /* unused (the exchange is performed by the caller) */
   void *stream;              /* cudaStream_t */
 } ipm_config;
 
@@ -197,9 +197,30 @@ IPM_API ipm_status ipm_last_cell_stats(ipm_ctx *c, int32_t *d_iters, int32_t *d_
 IPM_API ipm_status ipm_get_time(ipm_ctx *c, double *t);
 IPM_API ipm_status ipm_set_time(ipm_ctx *c, double t);
 
-/* NCCL bootstrap: rank 0 creates the 128-byte id that the caller broadcasts (e.g. with
- * torch.distributed) before ipm_init on every rank. */
-IPM_API ipm_status ipm_nccl_unique_id(void *h_id128);
+/* Distributed contexts (nranks > 1): the step is split around the exchange, which the caller
+ * performs (e.g. torch.distributed over NCCL; the dual problems need no communication, only the
+ * flux needs the face neighbours' duals):
+ *   ipm_step_dual  dual solve of the owned cells, packs the duals of the cells adjacent to each peer
+ *                  into d_sendbuf [nsend][N][m] (grouped by peer, ipm_halo_layout order) and copies
+ *                  the local CFL rate (bits of a double >= 0, order-preserving as uint64) to d_rate;
+ *   (caller)       send/receive the per-peer slices, all-reduce d_rate with MAX;
+ *   ipm_step_flux  node states of the halo cells from d_recvbuf [nrecv][N][m], dt from d_rate,
+ *                  moment update of the owned cells; info (if non-NULL) holds LOCAL sums.
+ * ipm_step = ipm_step_dual + ipm_step_flux without exchange (single-rank contexts only). */
+IPM_API ipm_status ipm_step_dual(ipm_ctx *c, const double *d_uhat, double *d_lambda, double *d_sendbuf,
+                                 uint64_t *d_rate);
+IPM_API ipm_status ipm_step_flux(ipm_ctx *c, double *d_uhat, double *d_lambda, const double *d_recvbuf,
+                                 const uint64_t *d_rate, double t_end, ipm_step_info *info);
+/* peers (ascending rank) with per-peer send / receive cell counts; arrays sized npeers */
+IPM_API ipm_status ipm_halo_layout(const ipm_ctx *c, int32_t *npeers, int64_t *nsend, int64_t *nrecv,
+                                   int32_t *h_peers, int32_t *h_send_count, int32_t *h_recv_count);
+/* Host-only (no CUDA): the partition ipm_init would build for cfg->rank of cfg->nranks.
+ * Pass NULL arrays to query sizes first.  local ids ascending; halo and send ids grouped by peer
+ * (ascending rank), ascending within a peer; send list r->s equals halo list of s from r. */
+IPM_API ipm_status ipm_partition_query(const ipm_config *cfg, int64_t *cells, int64_t *nhalo, int32_t *npeers,
+                                       int64_t *nsend, int64_t *h_local_gid, int64_t *h_halo_gid,
+                                       int32_t *h_peers, int32_t *h_send_count, int32_t *h_recv_count,
+                                       int64_t *h_send_gid);
 
 /* Timing of the last ipm_step's dual-solve kernel (ms, CUDA events on the ctx stream;
  * synchronous) — used by bench.py for the roofline line. */

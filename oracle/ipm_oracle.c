@@ -885,47 +885,62 @@ static int node_states(const orc_ctx *c, const double *lam, double *U) {
   return bad == 0;
 }
 
-/* CFL time step from the largest wave speed over all cells, nodes and ghost states (reading 15). */
-static double dt_from_states(const orc_ctx *c, const double *U, double t_remaining) {
+/* CFL rate of cell j: largest wave speed over its nodes and the ghost states of its boundary faces,
+ * times the mesh factor (reading 15). */
+static double cell_rate(const orc_ctx *c, const double *U, int j) {
   const orc_problem *P = &c->P;
   int Q = c->Q, m = c->m, F = c->F;
   double rate = 0.0;
-  for (int j = 0; j < c->cells; ++j) {
-    for (int k = 0; k < Q; ++k) {
-      const double *u = U + ((size_t)j * Q + k) * m;
-      double r;
+  for (int k = 0; k < Q; ++k) {
+    const double *u = U + ((size_t)j * Q + k) * m;
+    double r;
+    if (P->mesh_kind == ORC_MESH_1D) {
+      double n1[2] = {1.0, 0.0};
+      r = wave_speed(c, u, n1) * c->coef[j * 2];
+    } else if (P->mesh_kind == ORC_MESH_CART2D) {
+      double nx[2] = {1.0, 0.0}, ny[2] = {0.0, 1.0};
+      r = wave_speed(c, u, nx) * c->coef[j * 4 + 0] + wave_speed(c, u, ny) * c->coef[j * 4 + 2];
+    } else {
+      r = speed_norm(c, u) * c->perim[j] / c->area[j];
+    }
+    if (r > rate) rate = r;
+    for (int f = 0; f < F; ++f) {
+      int nb = c->nbr[j * F + f];
+      if (nb >= 0) continue;
+      double ug[4];
+      ghost_state(c, -1 - nb, k, u, c->nrm + (j * F + f) * 2, ug);
+      double rg;
       if (P->mesh_kind == ORC_MESH_1D) {
         double n1[2] = {1.0, 0.0};
-        r = wave_speed(c, u, n1) * c->coef[j * 2];
+        rg = wave_speed(c, ug, n1) * c->coef[j * 2];
       } else if (P->mesh_kind == ORC_MESH_CART2D) {
         double nx[2] = {1.0, 0.0}, ny[2] = {0.0, 1.0};
-        r = wave_speed(c, u, nx) * c->coef[j * 4 + 0] + wave_speed(c, u, ny) * c->coef[j * 4 + 2];
+        rg = wave_speed(c, ug, nx) * c->coef[j * 4 + 0] + wave_speed(c, ug, ny) * c->coef[j * 4 + 2];
       } else {
-        r = speed_norm(c, u) * c->perim[j] / c->area[j];
+        rg = speed_norm(c, ug) * c->perim[j] / c->area[j];
       }
-      if (r > rate) rate = r;
-      /* ghost states of boundary faces of this cell */
-      for (int f = 0; f < F; ++f) {
-        int nb = c->nbr[j * F + f];
-        if (nb >= 0) continue;
-        double ug[4];
-        ghost_state(c, -1 - nb, k, u, c->nrm + (j * F + f) * 2, ug);
-        double rg;
-        if (P->mesh_kind == ORC_MESH_1D) {
-          double n1[2] = {1.0, 0.0};
-          rg = wave_speed(c, ug, n1) * c->coef[j * 2];
-        } else if (P->mesh_kind == ORC_MESH_CART2D) {
-          double nx[2] = {1.0, 0.0}, ny[2] = {0.0, 1.0};
-          rg = wave_speed(c, ug, nx) * c->coef[j * 4 + 0] + wave_speed(c, ug, ny) * c->coef[j * 4 + 2];
-        } else {
-          rg = speed_norm(c, ug) * c->perim[j] / c->area[j];
-        }
-        if (rg > rate) rate = rg;
-      }
+      if (rg > rate) rate = rg;
     }
   }
-  double dt = P->cfl / rate;
+  return rate;
+}
+
+/* Delta t = CFL / max_j rate_j, clipped to the remaining time (reading 15). */
+static double dt_from_states(const orc_ctx *c, const double *U, double t_remaining) {
+  double rate = 0.0;
+  for (int j = 0; j < c->cells; ++j) {
+    double r = cell_rate(c, U, j);
+    if (r > rate) rate = r;
+  }
+  double dt = c->P.cfl / rate;
   return dt < t_remaining ? dt : t_remaining;
+}
+
+void orc_cell_rates(const orc_ctx *c, const double *lam, double *rates) {
+  double *U = (double *)malloc(sizeof(double) * (size_t)c->cells * c->Q * c->m);
+  node_states(c, lam, U);
+  for (int j = 0; j < c->cells; ++j) rates[j] = cell_rate(c, U, j);
+  free(U);
 }
 
 double orc_compute_dt(const orc_ctx *c, const double *lam, double t_remaining) {

@@ -143,6 +143,8 @@ void orc_get_levels(const orc_ctx *c, int32_t *levels);
 void orc_dual_solve_all(const orc_ctx *c, const double *uhat, double *lam, int32_t *iters,
                         int32_t *status, double *crit);
 double orc_compute_dt(const orc_ctx *c, const double *lam, double t_remaining);
+/* per-cell CFL rate (largest wave speed x mesh factor, incl. boundary ghost states); dt = CFL / max */
+void orc_cell_rates(const orc_ctx *c, const double *lam, double *rates);
 void orc_flux_update(orc_ctx *c, const double *lam, const double *uhat_old, double *uhat_new,
                      double dt);
 /* one step of Algorithm 1 / 2 / 3: dual solve, [levels], dt, moment update.

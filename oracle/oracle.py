@@ -98,6 +98,7 @@ def lib():
             "orc_set_levels": (None, [P, I]), "orc_get_levels": (None, [P, I]),
             "orc_dual_solve_all": (None, [P, D, D, I, I, D]),
             "orc_compute_dt": (C.c_double, [P, D, C.c_double]),
+            "orc_cell_rates": (None, [P, D, D]),
             "orc_flux_update": (None, [P, D, D, D, C.c_double]),
             "orc_step": (C.c_int, [P, D, D, C.c_double, I, I, D, D]),
         }
@@ -332,6 +333,11 @@ class Oracle:
 
     def compute_dt(self, lam, t_remaining=np.inf):
         return lib().orc_compute_dt(self.ctx, _d(lam), t_remaining)
+
+    def cell_rates(self, lam):
+        r = np.zeros(self.cells)
+        lib().orc_cell_rates(self.ctx, _d(np.ascontiguousarray(lam)), _d(r))
+        return r
 
     def flux_update(self, lam, uhat_old, dt):
         new = self.zeros()

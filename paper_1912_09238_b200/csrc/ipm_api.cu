@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "../../include/ipm.h"
+#include "ipm_host.h"
 #include "ipm_internal.h"
 
 namespace {
@@ -181,7 +182,10 @@ T* dalloc(size_t n, std::vector<void*>& owned) {
 struct ipm_ctx {
   ipm_config cfg;
   int N = 0, Q = 0, QP = 0, m = 0, p = 0, F = 0;
-  int64_t cells = 0;
+  int64_t cells = 0, halo = 0;
+  ipm::Partition part;
+  int64_t* d_gid = nullptr;       // [cells] global ids of owned cells
+  int32_t* d_send_local = nullptr;  // [nsend] local indices packed for the peers
   std::vector<int> idx, deg;
   std::vector<double> xi, omega, phi;  // phi [Q][N]
   std::vector<int64_t> cell_ids;
@@ -235,7 +239,7 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   if (C.closure == IPM_CLOSURE_BARRIER && (C.m != 1 || !(C.u_plus > C.u_minus)))
     return fail(IPM_ERR_ARG, "barrier closure needs m = 1 and u+ > u-");
   if (C.closure == IPM_CLOSURE_EULER && C.m == 1) return fail(IPM_ERR_ARG, "Euler closure needs m = 3 or 4");
-  if (C.nranks > 1) return fail(IPM_ERR_UNSUPPORTED, "nranks > 1 not built in this library version");
+  if (C.nranks > 1 && (C.rank < 0 || C.rank >= C.nranks)) return fail(IPM_ERR_ARG, "rank out of range");
   if (C.n_levels < 0 || C.n_levels > 8) return fail(IPM_ERR_ARG, "n_levels in [0, 8]");
   if (C.n_levels > 0 && C.level_M[C.n_levels - 1] != C.M) return fail(IPM_ERR_ARG, "level_M[last] must equal M");
 
@@ -297,112 +301,28 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
       WPhiT[(size_t)i * QP + k] = c->omega[k] * c->phi[(size_t)k * N + i];
     }
 
-  // mesh tables
-  int F = 0;
-  int64_t cells = 0;
-  std::vector<int32_t> nbr;
-  std::vector<double> nrm, coef, area, rgeo;
-  double inv_dx = 0.0, inv_dy = 0.0;
-  if (C.mesh_kind == IPM_MESH_1D) {
-    if (C.nx < 1) {
-      delete c;
-      return fail(IPM_ERR_ARG, "nx >= 1");
-    }
-    F = 2;
-    cells = C.nx;
-    const double dx = (C.x1 - C.x0) / C.nx;
-    inv_dx = 1.0 / dx;
-    nbr.resize(cells * 2);
-    coef.assign(cells * 2, inv_dx);
-    area.assign(cells, dx);
-    for (int64_t j = 0; j < cells; ++j) {
-      nbr[j * 2 + 0] = j > 0 ? (int32_t)(j - 1) : (C.periodic ? (int32_t)(cells - 1) : -1);
-      nbr[j * 2 + 1] = j < cells - 1 ? (int32_t)(j + 1) : (C.periodic ? 0 : -2);
-    }
-  } else if (C.mesh_kind == IPM_MESH_CART2D) {
-    if (C.nx < 1 || C.ny < 1) {
-      delete c;
-      return fail(IPM_ERR_ARG, "nx, ny >= 1");
-    }
-    F = 4;
-    const int64_t nx = C.nx, ny = C.ny;
-    cells = nx * ny;
-    const double dx = (C.x1 - C.x0) / nx, dy = (C.y1 - C.y0) / ny;
-    inv_dx = 1.0 / dx;
-    inv_dy = 1.0 / dy;
-    nbr.resize(cells * 4);
-    coef.resize(cells * 4);
-    area.assign(cells, dx * dy);
-    for (int64_t iy = 0; iy < ny; ++iy)
-      for (int64_t ix = 0; ix < nx; ++ix) {
-        const int64_t j = iy * nx + ix;
-        nbr[j * 4 + 0] = (int32_t)(ix > 0 ? j - 1 : (C.periodic ? iy * nx + nx - 1 : -1));
-        nbr[j * 4 + 1] = (int32_t)(ix < nx - 1 ? j + 1 : (C.periodic ? iy * nx : -2));
-        nbr[j * 4 + 2] = (int32_t)(iy > 0 ? j - nx : (C.periodic ? (ny - 1) * nx + ix : -3));
-        nbr[j * 4 + 3] = (int32_t)(iy < ny - 1 ? j + nx : (C.periodic ? ix : -4));
-        coef[j * 4 + 0] = coef[j * 4 + 1] = inv_dx;
-        coef[j * 4 + 2] = coef[j * 4 + 3] = inv_dy;
-      }
-  } else if (C.mesh_kind == IPM_MESH_TRI) {
-    if (C.n_tri < 1 || !C.h_vert || !C.h_tri || !C.h_tri_tag) {
-      delete c;
-      return fail(IPM_ERR_ARG, "triangle mesh arrays required");
-    }
-    F = 3;
-    cells = C.n_tri;
-    nbr.assign(cells * 3, 0);
-    nrm.assign(cells * 6, 0.0);
-    coef.assign(cells * 3, 0.0);
-    area.assign(cells, 0.0);
-    rgeo.assign(cells, 0.0);
-    std::unordered_map<int64_t, int64_t> edge_owner;
-    edge_owner.reserve((size_t)cells * 3);
-    for (int64_t t = 0; t < cells; ++t)
-      for (int e = 0; e < 3; ++e) {
-        const int a = C.h_tri[t * 3 + e], b = C.h_tri[t * 3 + (e + 1) % 3];
-        const int64_t key = (int64_t)std::min(a, b) * C.n_vert + std::max(a, b);
-        const int tag = C.h_tri_tag[t * 3 + e];
-        nbr[t * 3 + e] = -1 - (tag < 0 ? 0 : tag);
-        auto it = edge_owner.find(key);
-        if (it == edge_owner.end()) {
-          edge_owner.emplace(key, t * 3 + e);
-        } else {
-          const int64_t o = it->second;
-          nbr[t * 3 + e] = (int32_t)(o / 3);
-          nbr[o] = (int32_t)t;
-        }
-      }
-    for (int64_t t = 0; t < cells; ++t) {
-      const double* A = C.h_vert + 2 * C.h_tri[t * 3 + 0];
-      const double* B = C.h_vert + 2 * C.h_tri[t * 3 + 1];
-      const double* Cc = C.h_vert + 2 * C.h_tri[t * 3 + 2];
-      const double ar = 0.5 * ((B[0] - A[0]) * (Cc[1] - A[1]) - (Cc[0] - A[0]) * (B[1] - A[1]));
-      if (!(ar > 0.0)) {
-        delete c;
-        return fail(IPM_ERR_ARG, "triangles must be counter-clockwise with positive area");
-      }
-      area[t] = ar;
-      double per = 0.0;
-      for (int e = 0; e < 3; ++e) {
-        const double* V0 = C.h_vert + 2 * C.h_tri[t * 3 + e];
-        const double* V1 = C.h_vert + 2 * C.h_tri[t * 3 + (e + 1) % 3];
-        const double ex = V1[0] - V0[0], ey = V1[1] - V0[1];
-        const double len = std::sqrt(ex * ex + ey * ey);
-        nrm[(t * 3 + e) * 2 + 0] = ey / len;
-        nrm[(t * 3 + e) * 2 + 1] = -ex / len;
-        coef[t * 3 + e] = len / ar;
-        per += len;
-      }
-      rgeo[t] = per / ar;
-    }
-  } else {
+  // mesh face tables (global), this rank's part and its halo
+  ipm::MeshTables G, Lm;
+  std::string merr;
+  if (!ipm::build_mesh(C, G, merr)) {
     delete c;
-    return fail(IPM_ERR_ARG, "mesh_kind");
+    return fail(IPM_ERR_ARG, merr);
   }
+  const int nranks = C.nranks > 0 ? C.nranks : 1;
+  if (!ipm::build_partition(C, G, nranks > 1 ? C.rank : 0, nranks, c->part, merr)) {
+    delete c;
+    return fail(IPM_ERR_ARG, merr);
+  }
+  ipm::local_tables(G, c->part, Lm);
+  const int F = G.F;
+  const int64_t cells = Lm.cells;
+  const double inv_dx = G.inv_dx, inv_dy = G.inv_dy;
+  std::vector<int32_t>& nbr = Lm.nbr;
+  std::vector<double>&nrm = Lm.nrm, &coef = Lm.coef, &area = Lm.area, &rgeo = Lm.rgeo;
   c->F = F;
   c->cells = cells;
-  c->cell_ids.resize(cells);
-  for (int64_t j = 0; j < cells; ++j) c->cell_ids[j] = j;
+  c->halo = (int64_t)c->part.halo_gid.size();
+  c->cell_ids = c->part.local_gid;
 
   // boundary ghost states per node and their CFL contribution
   std::vector<double> ghost((size_t)4 * Q * m, 0.0);
@@ -411,9 +331,9 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
       for (int k = 0; k < Q; ++k)
         HostPrim::eval(C.bc_state[t], &c->xi[(size_t)k * p], p, m, C.gamma, &ghost[((size_t)t * Q + k) * m]);
   double grate = 0.0;
-  for (int64_t j = 0; j < cells; ++j)
+  for (int64_t j = 0; j < G.cells; ++j)
     for (int f = 0; f < F; ++f) {
-      const int nb = nbr[j * F + f];
+      const int nb = G.nbr[j * F + f];
       if (nb >= 0) continue;
       const int tag = -1 - nb;
       if (C.bc_kind[tag] != IPM_BC_STATE) continue;
@@ -425,7 +345,7 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
         else if (C.mesh_kind == IPM_MESH_CART2D)
           r = host_speed(m, C.gamma, ug, 0) * inv_dx + host_speed(m, C.gamma, ug, 1) * inv_dy;
         else
-          r = host_speed(m, C.gamma, ug, 2) * rgeo[j];
+          r = host_speed(m, C.gamma, ug, 2) * G.rgeo[j];
         grate = std::max(grate, r);
       }
     }
@@ -445,7 +365,9 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   double* d_area = dalloc<double>(area.size(), O);
   double* d_rgeo = dalloc<double>(rgeo.size(), O);
   double* d_ghost = dalloc<double>(ghost.size(), O);
-  c->d_uq = dalloc<double>((size_t)cells * Q * m, O);
+  c->d_uq = dalloc<double>((size_t)(cells + c->halo) * Q * m, O);
+  c->d_gid = dalloc<int64_t>(cells, O);
+  c->d_send_local = dalloc<int32_t>(c->part.send_local.size(), O);
   c->d_crit = dalloc<double>(cells, O);
   c->d_level = dalloc<int32_t>(cells, O);
   c->d_level_new = dalloc<int32_t>(cells, O);
@@ -453,7 +375,7 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   c->d_status = dalloc<int32_t>(cells, O);
   c->d_sc = dalloc<ipm::StepScalars>(1, O);
   if (!d_PhiT || !d_WPhiT || !d_omega || !d_deg || !d_LL || !d_idx || !d_nbr || !d_nrm || !d_coef || !d_area || !d_rgeo || !d_ghost ||
-      !c->d_uq || !c->d_crit || !c->d_level || !c->d_level_new || !c->d_iters || !c->d_status || !c->d_sc) {
+      !c->d_uq || !c->d_gid || !c->d_send_local || !c->d_crit || !c->d_level || !c->d_level_new || !c->d_iters || !c->d_status || !c->d_sc) {
     ipm_destroy(c);
     return fail(IPM_ERR_CUDA, "cudaMalloc failed");
   }
@@ -467,6 +389,8 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
       up(d_nbr, nbr.data(), nbr.size() * 4) || up(d_nrm, nrm.data(), nrm.size() * 8) ||
       up(d_coef, coef.data(), coef.size() * 8) || up(d_area, area.data(), area.size() * 8) ||
       up(d_rgeo, rgeo.data(), rgeo.size() * 8) || up(d_ghost, ghost.data(), ghost.size() * 8) ||
+      up(c->d_gid, c->part.local_gid.data(), cells * 8) ||
+      up(c->d_send_local, c->part.send_local.data(), c->part.send_local.size() * 4) ||
       cudaMemset(c->d_sc, 0, sizeof(ipm::StepScalars)) || cudaMemset(c->d_level, 0, cells * 4) ||
       cudaMemset(c->d_level_new, 0, cells * 4)) {
     ipm_destroy(c);
@@ -576,21 +500,32 @@ ipm_status ipm_dual_solve(ipm_ctx* c, const double* d_uhat, double* d_lambda, in
   return launch_rc(ipm::launch_dual(k, a), "dual_solve");
 }
 
+// node states of the halo cells from received duals (rows cells .. cells+halo of the node buffer)
+static int halo_nodes(ipm_ctx* c, const double* d_recv) {
+  if (c->halo == 0) return 0;
+  ipm::KernelCtx kh = c->k;
+  kh.mesh.cells = c->halo;
+  return ipm::launch_nodes(kh, d_recv, nullptr, c->d_uq + (size_t)c->cells * c->Q * c->m, 0);
+}
+
 ipm_status ipm_flux_update(ipm_ctx* c, const double* d_lambda, const double* d_uhat_old, double* d_uhat_new,
                            double dt, double* d_dt) {
   if (!c || !d_lambda || !d_uhat_old || !d_uhat_new) return fail(IPM_ERR_ARG, "null argument");
+  if (c->halo > 0) return fail(IPM_ERR_ARG, "ipm_flux_update needs halo duals: use ipm_step_dual/ipm_step_flux");
   const ipm::KernelCtx& k = c->k;
   if (int rc = ipm::launch_step_begin(k, c->ghost_rate)) return launch_rc(rc, "step_begin");
-  if (int rc = ipm::launch_nodes(k, d_lambda, nullptr, c->d_uq)) return launch_rc(rc, "nodes");
+  if (int rc = ipm::launch_nodes(k, d_lambda, nullptr, c->d_uq, 1)) return launch_rc(rc, "nodes");
   if (int rc = ipm::launch_dt(k, -1.0, dt, c->cfg.cfl)) return launch_rc(rc, "dt");
-  ipm::FluxLaunch f{c->d_uq, d_uhat_old, d_uhat_new, nullptr, c->cfg.update_form, c->cfg.cfl};
+  ipm::FluxLaunch f{c->d_uq, d_uhat_old, d_uhat_new, nullptr, nullptr, c->cfg.update_form, c->cfg.cfl};
   if (int rc = ipm::launch_flux(k, f)) return launch_rc(rc, "flux");
   if (d_dt) CUDA_OK(cudaMemcpyAsync(d_dt, &c->d_sc->dt, 8, cudaMemcpyDeviceToDevice, c->stream));
   return IPM_OK;
 }
 
-ipm_status ipm_step(ipm_ctx* c, double* d_uhat, double* d_lambda, double t_end, ipm_step_info* info) {
+ipm_status ipm_step_dual(ipm_ctx* c, const double* d_uhat, double* d_lambda, double* d_sendbuf,
+                         uint64_t* d_rate) {
   if (!c || !d_uhat || !d_lambda) return fail(IPM_ERR_ARG, "null argument");
+  if (!c->part.send_local.empty() && !d_sendbuf) return fail(IPM_ERR_ARG, "send buffer required");
   const ipm::KernelCtx& k = c->k;
   if (int rc = ipm::launch_step_begin(k, c->ghost_rate)) return launch_rc(rc, "step_begin");
   ipm::DualLaunch a{};
@@ -608,8 +543,23 @@ ipm_status ipm_step(ipm_ctx* c, double* d_uhat, double* d_lambda, double t_end, 
   if (c->timing) cudaEventRecord(c->ev[0], c->stream);
   if (int rc = ipm::launch_dual(k, a)) return launch_rc(rc, "dual_solve");
   if (c->timing) cudaEventRecord(c->ev[1], c->stream);
+  if (!c->part.send_local.empty())
+    if (int rc = ipm::launch_pack(k, d_lambda, c->d_send_local, (int64_t)c->part.send_local.size(), d_sendbuf))
+      return launch_rc(rc, "pack");
+  if (d_rate) CUDA_OK(cudaMemcpyAsync(d_rate, &c->d_sc->rate_bits, 8, cudaMemcpyDeviceToDevice, c->stream));
+  return IPM_OK;
+}
+
+ipm_status ipm_step_flux(ipm_ctx* c, double* d_uhat, double* d_lambda, const double* d_recvbuf,
+                         const uint64_t* d_rate, double t_end, ipm_step_info* info) {
+  if (!c || !d_uhat || !d_lambda) return fail(IPM_ERR_ARG, "null argument");
+  if (c->halo > 0 && !d_recvbuf) return fail(IPM_ERR_ARG, "receive buffer required");
+  const ipm::KernelCtx& k = c->k;
+  if (d_rate) CUDA_OK(cudaMemcpyAsync(&c->d_sc->rate_bits, d_rate, 8, cudaMemcpyDeviceToDevice, c->stream));
+  if (int rc = halo_nodes(c, d_recvbuf)) return launch_rc(rc, "halo nodes");
   if (int rc = ipm::launch_dt(k, t_end, -1.0, c->cfg.cfl)) return launch_rc(rc, "dt");
-  ipm::FluxLaunch f{c->d_uq, d_uhat, d_uhat, a.level_new, c->cfg.update_form, c->cfg.cfl};
+  const int32_t* lvl_new = c->cfg.n_levels > 0 ? c->d_level_new : nullptr;
+  ipm::FluxLaunch f{c->d_uq, d_uhat, d_uhat, lvl_new, d_lambda, c->cfg.update_form, c->cfg.cfl};
   if (c->timing) cudaEventRecord(c->ev[2], c->stream);
   if (int rc = ipm::launch_flux(k, f)) return launch_rc(rc, "flux");
   if (c->timing) cudaEventRecord(c->ev[3], c->stream);
@@ -625,6 +575,54 @@ ipm_status ipm_step(ipm_ctx* c, double* d_uhat, double* d_lambda, double t_end, 
     info->failed_cells = (int64_t)s.failed;
     info->worst_status = s.worst;
     if (s.failed) return fail(IPM_ERR_NUMERIC, "failed cells in step");
+  }
+  return IPM_OK;
+}
+
+ipm_status ipm_step(ipm_ctx* c, double* d_uhat, double* d_lambda, double t_end, ipm_step_info* info) {
+  if (!c || !d_uhat || !d_lambda) return fail(IPM_ERR_ARG, "null argument");
+  if (c->halo > 0 || !c->part.send_local.empty())
+    return fail(IPM_ERR_ARG, "distributed context: use ipm_step_dual / exchange / ipm_step_flux");
+  if (ipm_status s = ipm_step_dual(c, d_uhat, d_lambda, nullptr, nullptr)) return s;
+  return ipm_step_flux(c, d_uhat, d_lambda, nullptr, nullptr, t_end, info);
+}
+
+ipm_status ipm_halo_layout(const ipm_ctx* c, int32_t* npeers, int64_t* nsend, int64_t* nrecv, int32_t* h_peers,
+                           int32_t* h_send_count, int32_t* h_recv_count) {
+  if (!c) return fail(IPM_ERR_ARG, "null ctx");
+  const ipm::Partition& P = c->part;
+  if (npeers) *npeers = (int32_t)P.peers.size();
+  if (nsend) *nsend = (int64_t)P.send_gid.size();
+  if (nrecv) *nrecv = (int64_t)P.halo_gid.size();
+  for (size_t i = 0; i < P.peers.size(); ++i) {
+    if (h_peers) h_peers[i] = P.peers[i];
+    if (h_send_count) h_send_count[i] = P.send_count[i];
+    if (h_recv_count) h_recv_count[i] = P.recv_count[i];
+  }
+  return IPM_OK;
+}
+
+ipm_status ipm_partition_query(const ipm_config* cfg, int64_t* cells, int64_t* nhalo, int32_t* npeers,
+                               int64_t* nsend, int64_t* h_local_gid, int64_t* h_halo_gid, int32_t* h_peers,
+                               int32_t* h_send_count, int32_t* h_recv_count, int64_t* h_send_gid) {
+  if (!cfg) return fail(IPM_ERR_ARG, "null config");
+  ipm::MeshTables G;
+  ipm::Partition P;
+  std::string err;
+  if (!ipm::build_mesh(*cfg, G, err)) return fail(IPM_ERR_ARG, err);
+  const int nr = cfg->nranks > 0 ? cfg->nranks : 1;
+  if (!ipm::build_partition(*cfg, G, nr > 1 ? cfg->rank : 0, nr, P, err)) return fail(IPM_ERR_ARG, err);
+  if (cells) *cells = (int64_t)P.local_gid.size();
+  if (nhalo) *nhalo = (int64_t)P.halo_gid.size();
+  if (npeers) *npeers = (int32_t)P.peers.size();
+  if (nsend) *nsend = (int64_t)P.send_gid.size();
+  if (h_local_gid) std::memcpy(h_local_gid, P.local_gid.data(), P.local_gid.size() * 8);
+  if (h_halo_gid) std::memcpy(h_halo_gid, P.halo_gid.data(), P.halo_gid.size() * 8);
+  if (h_send_gid) std::memcpy(h_send_gid, P.send_gid.data(), P.send_gid.size() * 8);
+  for (size_t i = 0; i < P.peers.size(); ++i) {
+    if (h_peers) h_peers[i] = P.peers[i];
+    if (h_send_count) h_send_count[i] = P.send_count[i];
+    if (h_recv_count) h_recv_count[i] = P.recv_count[i];
   }
   return IPM_OK;
 }
@@ -662,7 +660,7 @@ ipm_status ipm_project_ic(ipm_ctx* c, const ipm_ic* ic, double* d_uhat) {
   }
   const double dx = C.nx > 0 ? (C.x1 - C.x0) / C.nx : 0.0, dy = C.ny > 0 ? (C.y1 - C.y0) / C.ny : 0.0;
   int rc = ipm::launch_project_ic(c->k, d_reg, d_split, ic->kind, C.nx, C.x0, C.y0, dx, dy,
-                                  C.n_levels > 0 ? c->d_level : nullptr, d_uhat);
+                                  C.n_levels > 0 ? c->d_level : nullptr, c->d_gid, d_uhat);
   ipm::StepScalars s{};
   cudaMemcpy(c->d_sc, &s, sizeof(s), cudaMemcpyHostToDevice);  // t = 0
   cudaStreamSynchronize(c->stream);
@@ -678,7 +676,7 @@ ipm_status ipm_warm_start(ipm_ctx* c, const double* d_uhat, double* d_lambda) {
 
 ipm_status ipm_moments_from_dual(ipm_ctx* c, const double* d_lambda, double* d_uhat) {
   if (!c || !d_uhat || !d_lambda) return fail(IPM_ERR_ARG, "null argument");
-  return launch_rc(ipm::launch_nodes(c->k, d_lambda, d_uhat, nullptr), "moments_from_dual");
+  return launch_rc(ipm::launch_nodes(c->k, d_lambda, d_uhat, nullptr, 0), "moments_from_dual");
 }
 
 ipm_status ipm_stress_dual(ipm_ctx* c, const double* d_base, const double* d_z, double rel, double abs_,
@@ -720,10 +718,6 @@ ipm_status ipm_set_time(ipm_ctx* c, double t) {
   return IPM_OK;
 }
 
-ipm_status ipm_nccl_unique_id(void* h_id128) {
-  (void)h_id128;
-  return fail(IPM_ERR_UNSUPPORTED, "NCCL bootstrap not built in this library version");
-}
 
 ipm_status ipm_enable_timing(ipm_ctx* c, int32_t on) {
   if (!c) return fail(IPM_ERR_ARG, "null ctx");

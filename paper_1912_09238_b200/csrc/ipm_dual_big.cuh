@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
       Nnew = P.ad.Nl[nl];
       if (t == 0) A.level_new[cell] = nl;
     }
-    for (int r = t; r < nmax; r += NT) gl[r] = (r < Nnew * MS) ? lam[r] : 0.0;
+    for (int r = t; r < nmax; r += NT) gl[r] = (r < n) ? lam[r] : 0.0;  // truncated to the new level after the flux
     if (t == 0) {
       if (A.iters) A.iters[cell] = l;
       if (A.status) A.status[cell] = status;

@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(IPM_GROUP_THREADS) k_dual_group(DualParams P) 
       Nnew = P.ad.Nl[nl];
       if (t == 0) A.level_new[cell] = nl;
     }
-    for (int r = t; r < nmax; r += G) gl[r] = (r < Nnew * MS) ? lam[r] : 0.0;
+    for (int r = t; r < nmax; r += G) gl[r] = (r < n) ? lam[r] : 0.0;  // truncated to the new level after the flux
     if (t == 0) {
       if (A.iters) A.iters[cell] = l;
       if (A.status) A.status[cell] = status;

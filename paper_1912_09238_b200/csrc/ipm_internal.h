@@ -83,6 +83,7 @@ struct FluxLaunch {
   const double* uhat_old;
   double* uhat_new;
   const int32_t* level_new;  // nullable: projection level per cell
+  double* lam;               // nullable: duals truncated to the new level after the update
   int update_form;
   double cfl;
 };
@@ -113,10 +114,12 @@ int launch_dt(const KernelCtx& k, double t_end, double dt_fixed, double cfl);
 int launch_flux(const KernelCtx& k, const FluxLaunch& a);
 int launch_project_ic(const KernelCtx& k, const double* d_region /*[R][Q][m]*/, const double* d_split /*[Q][2]*/,
                       int ic_kind, int nx, double x0, double y0, double dx, double dy, const int32_t* level,
-                      double* uhat);
+                      const int64_t* gid, double* uhat);
+// pack duals of the listed local cells into a contiguous send buffer [n][N][m]
+int launch_pack(const KernelCtx& k, const double* lam, const int32_t* idx, int64_t n, double* out);
 int launch_warm_start(const KernelCtx& k, const double* uhat, double* lam);
 // node pass: uhat = h(lambda) (nullable), node states uq (nullable), CFL rate into sc
-int launch_nodes(const KernelCtx& k, const double* lam, double* uhat, double* uq);
+int launch_nodes(const KernelCtx& k, const double* lam, double* uhat, double* uq, int want_rate);
 int launch_stress(const KernelCtx& k, const double* base, const double* z, double rel, double abs_, double* lam);
 
 }  // namespace ipm

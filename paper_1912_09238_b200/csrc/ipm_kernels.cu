@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(512) k_dual_warp(DualParams P) {
       if (lane == 0) A.level_new[cell] = nl;
     }
     // lambda zero-padded / truncated to the new level (the node states keep the old level)
-    for (int r = lane; r < nmax; r += 32) gl[r] = (r < Nnew * MS) ? lam[r] : 0.0;
+    for (int r = lane; r < nmax; r += 32) gl[r] = (r < n) ? lam[r] : 0.0;  // truncated after the flux
     if (lane == 0) {
       if (A.iters) A.iters[cell] = l;
       if (A.status) A.status[cell] = status;
@@ -503,6 +503,8 @@ __global__ void __launch_bounds__(256) k_flux_warp(FluxParams P) {
       }
       un_[rr] = out;
       if (rr == 0) my_res += P.mesh.area[cell] * fabs(out - old);
+      // duals zero-padded / truncated to the new level (Alg. 3: next dual solve at l^{n+1})
+      if (A.lam && i >= Nnew) A.lam[cell * nmax + rr] = 0.0;
     }
     __syncwarp();
   }
@@ -542,7 +544,8 @@ __global__ void k_dt(StepScalars* sc, double t_end, double dt_fixed, double cfl)
 template <int MS>
 __global__ void k_project_ic(Tables T, int64_t cells, const double* __restrict__ region,
                              const double* __restrict__ split, int kind, int nx, double x0, double y0, double dx,
-                             double dy, const int32_t* __restrict__ level, Adapt ad, double* __restrict__ uhat) {
+                             double dy, const int32_t* __restrict__ level, const int64_t* __restrict__ gid, Adapt ad,
+                             double* __restrict__ uhat) {
   extern __shared__ __align__(16) double sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int Q = T.Q, N = T.N;
@@ -554,14 +557,14 @@ __global__ void k_project_ic(Tables T, int64_t cells, const double* __restrict__
 #pragma unroll
         for (int a = 0; a < MS; ++a) ub[a] = region[(0 * Q + k) * MS + a];
       } else if (kind == 1) {
-        const double xl = x0 + (double)cell * dx;
+        const double xl = x0 + (double)gid[cell] * dx;
         double fl = (split[k * 2] - xl) / dx;
         fl = fmin(fmax(fl, 0.0), 1.0);
 #pragma unroll
         for (int a = 0; a < MS; ++a)
           ub[a] = fl * region[(0 * Q + k) * MS + a] + (1.0 - fl) * region[(1 * Q + k) * MS + a];
       } else {
-        const int64_t ix = cell % nx, iy = cell / nx;
+        const int64_t ix = gid[cell] % nx, iy = gid[cell] / nx;
         double fx = (split[k * 2] - (x0 + ix * dx)) / dx;
         double fy = (split[k * 2 + 1] - (y0 + iy * dy)) / dy;
         fx = fmin(fmax(fx, 0.0), 1.0);
@@ -605,7 +608,7 @@ __global__ void k_warm_start(int64_t cells, int N, ClParams cp, const double* __
 // u_s(lambda^T phi(xi_k)) and CFL rate
 template <int CL, int MS>
 __global__ void k_nodes(Tables T, Mesh mesh, ClParams cp, const double* __restrict__ lam_g, double* __restrict__ uhat,
-                        double* __restrict__ uq, StepScalars* sc, int tables_in_smem) {
+                        double* __restrict__ uq, StepScalars* sc, int tables_in_smem, int want_rate) {
   using Lay = DualLayout<MS>;
   extern __shared__ __align__(16) double sm[];
   const int N = T.N, Q = T.Q, QP = T.QP;
@@ -644,13 +647,13 @@ __global__ void k_nodes(Tables T, Mesh mesh, ClParams cp, const double* __restri
 #pragma unroll
         for (int a = 0; a < MS; ++a) o[a] = u[a];
       }
-      my_rate = fmax(my_rate, node_rate<CL, MS>(u, mesh, cell, cp.gamma));
+      if (want_rate) my_rate = fmax(my_rate, node_rate<CL, MS>(u, mesh, cell, cp.gamma));
     }
     __syncwarp();
   }
   my_rate = warp_max(my_rate);
   if (lane == 0 && sc) {
-    atomicMax(&sc->rate_bits, (unsigned long long)__double_as_longlong(my_rate));
+    if (want_rate) atomicMax(&sc->rate_bits, (unsigned long long)__double_as_longlong(my_rate));
     if (bad) atomicMax(&sc->worst, 4);
   }
 }
@@ -884,7 +887,7 @@ int launch_flux(const KernelCtx& k, const FluxLaunch& a) {
 
 template <int MS>
 static int ic_impl(const KernelCtx& k, const double* region, const double* split, int kind, int nx, double x0,
-                   double y0, double dx, double dy, const int32_t* level, double* uhat) {
+                   double y0, double dx, double dy, const int32_t* level, const int64_t* gid, double* uhat) {
   const size_t pw = (size_t)(k.T.Q * MS + 1) * 8;
   const int warps = (int)std::min<size_t>(8, k.smem_optin / pw);
   if (warps < 1) return -1;
@@ -893,17 +896,17 @@ static int ic_impl(const KernelCtx& k, const double* region, const double* split
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t want = (k.mesh.cells + warps - 1) / warps;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)k.sm_count * 8));
-  kern<<<grid, warps * 32, smem, S(k)>>>(k.T, k.mesh.cells, region, split, kind, nx, x0, y0, dx, dy, level, k.ad,
-                                         uhat);
+  kern<<<grid, warps * 32, smem, S(k)>>>(k.T, k.mesh.cells, region, split, kind, nx, x0, y0, dx, dy, level, gid,
+                                         k.ad, uhat);
   return (int)cudaGetLastError();
 }
 
 int launch_project_ic(const KernelCtx& k, const double* region, const double* split, int kind, int nx, double x0,
-                      double y0, double dx, double dy, const int32_t* level, double* uhat) {
+                      double y0, double dx, double dy, const int32_t* level, const int64_t* gid, double* uhat) {
   switch (k.m) {
-    case 1: return ic_impl<1>(k, region, split, kind, nx, x0, y0, dx, dy, level, uhat);
-    case 3: return ic_impl<3>(k, region, split, kind, nx, x0, y0, dx, dy, level, uhat);
-    case 4: return ic_impl<4>(k, region, split, kind, nx, x0, y0, dx, dy, level, uhat);
+    case 1: return ic_impl<1>(k, region, split, kind, nx, x0, y0, dx, dy, level, gid, uhat);
+    case 3: return ic_impl<3>(k, region, split, kind, nx, x0, y0, dx, dy, level, gid, uhat);
+    case 4: return ic_impl<4>(k, region, split, kind, nx, x0, y0, dx, dy, level, gid, uhat);
   }
   return -1;
 }
@@ -916,7 +919,7 @@ static int warm_impl(const KernelCtx& k, const double* uhat, double* lam) {
 }
 
 template <int CL, int MS>
-static int nodes_impl(const KernelCtx& k, const double* lam, double* uhat, double* uq) {
+static int nodes_impl(const KernelCtx& k, const double* lam, double* uhat, double* uq, int want_rate) {
   using Lay = DualLayout<MS>;
   const size_t tab = (size_t)2 * k.T.N * k.T.QP * 8, pw = (size_t)(k.T.N * MS + k.T.Q * Lay::NS + 1) * 8;
   const int in_smem = (tab + 4 * pw <= k.smem_optin) ? 1 : 0;
@@ -928,7 +931,7 @@ static int nodes_impl(const KernelCtx& k, const double* lam, double* uhat, doubl
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t want = (k.mesh.cells + warps - 1) / warps;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)k.sm_count * 4));
-  kern<<<grid, warps * 32, smem, S(k)>>>(k.T, k.mesh, k.cl, lam, uhat, uq, k.sc, in_smem);
+  kern<<<grid, warps * 32, smem, S(k)>>>(k.T, k.mesh, k.cl, lam, uhat, uq, k.sc, in_smem, want_rate);
   return (int)cudaGetLastError();
 }
 
@@ -954,8 +957,24 @@ static int stress_impl(const KernelCtx& k, const double* base, const double* z, 
   return -1;
 
 int launch_warm_start(const KernelCtx& k, const double* uhat, double* lam) { IPM_DISPATCH_CL(warm_impl, uhat, lam) }
-int launch_nodes(const KernelCtx& k, const double* lam, double* uhat, double* uq) {
-  IPM_DISPATCH_CL(nodes_impl, lam, uhat, uq)
+int launch_nodes(const KernelCtx& k, const double* lam, double* uhat, double* uq, int want_rate) {
+  IPM_DISPATCH_CL(nodes_impl, lam, uhat, uq, want_rate)
+}
+
+__global__ void k_pack(const double* __restrict__ lam, const int32_t* __restrict__ idx, int64_t n, int row,
+                       double* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * row) return;
+  const int64_t s = e / row, r = e - s * row;
+  out[e] = lam[(int64_t)idx[s] * row + r];
+}
+
+int launch_pack(const KernelCtx& k, const double* lam, const int32_t* idx, int64_t n, double* out) {
+  if (n == 0) return 0;
+  const int row = k.T.N * k.m;
+  const int64_t tot = n * row;
+  k_pack<<<(unsigned)((tot + 255) / 256), 256, 0, S(k)>>>(lam, idx, n, row, out);
+  return (int)cudaGetLastError();
 }
 int launch_stress(const KernelCtx& k, const double* base, const double* z, double rel, double abs_, double* lam) {
   IPM_DISPATCH_CL(stress_impl, base, z, rel, abs_, lam)

@@ -1,0 +1,47 @@
+"""The exchange step of the distributed path: torch.distributed plumbing only.
+
+Per (pseudo-)time step, after every rank has solved the dual problems of its own cells:
+  * halo_exchange: each rank sends the duals of its cells adjacent to a peer and receives the duals
+    of that peer's adjacent cells (one layer of face neighbours: the kinetic flux is a
+    nearest-neighbour stencil); NCCL P2P over NVLink on GPUs, gloo on CPU tests.
+  * allreduce_max_: the CFL rate (bits of a non-negative double, order-preserving as int64).
+  * reduce_info_: step statistics (sums; worst status max) for ipm_step_info.
+Buffers are laid out by libipm (ipm_halo_layout): rows [nsend][N*m] / [nrecv][N*m], grouped by
+peer in ascending rank order.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def halo_exchange(sendbuf: torch.Tensor, recvbuf: torch.Tensor, layout: dict, group=None) -> None:
+    ops = []
+    s0 = r0 = 0
+    for peer, ns, nr in zip(layout["peers"], layout["send_count"], layout["recv_count"]):
+        if ns:
+            ops.append(dist.P2POp(dist.isend, sendbuf[s0:s0 + ns], peer, group))
+        if nr:
+            ops.append(dist.P2POp(dist.irecv, recvbuf[r0:r0 + nr], peer, group))
+        s0 += ns
+        r0 += nr
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+
+def allreduce_max_(t: torch.Tensor, group=None) -> None:
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+
+
+def reduce_info_(info, device, group=None) -> None:
+    """Global step statistics from the local ones (ctypes ipm_step_info, in place)."""
+    v = torch.tensor([info.residual, float(info.newton_iters), float(info.failed_cells)], dtype=torch.float64,
+                     device=device)
+    dist.all_reduce(v, op=dist.ReduceOp.SUM, group=group)
+    w = torch.tensor([info.worst_status], dtype=torch.int64, device=device)
+    dist.all_reduce(w, op=dist.ReduceOp.MAX, group=group)
+    info.residual = float(v[0])
+    info.newton_iters = int(v[1])
+    info.failed_cells = int(v[2])
+    info.worst_status = int(w[0])

@@ -28,8 +28,8 @@ EXPORTS = [
     "ipm_init", "ipm_destroy", "ipm_status_string", "ipm_last_error", "ipm_sizes", "ipm_get_basis",
     "ipm_get_cell_ids", "ipm_dual_solve", "ipm_flux_update", "ipm_step", "ipm_project_ic", "ipm_warm_start",
     "ipm_moments_from_dual", "ipm_stress_dual", "ipm_get_levels", "ipm_set_levels", "ipm_last_cell_stats",
-    "ipm_get_time", "ipm_set_time", "ipm_nccl_unique_id", "ipm_last_kernel_ms", "ipm_enable_timing",
-    "ipm_debug_phase_cycles",
+    "ipm_get_time", "ipm_set_time", "ipm_last_kernel_ms", "ipm_enable_timing",
+    "ipm_debug_phase_cycles", "ipm_step_dual", "ipm_step_flux", "ipm_halo_layout", "ipm_partition_query",
 ]
 
 
@@ -59,7 +59,7 @@ class ipm_config(C.Structure):
         ("n_levels", C.c_int32), ("level_M", C.c_int32 * 8),
         ("delta_dec", C.c_double), ("delta_inc", C.c_double),
         ("rank", C.c_int32), ("nranks", C.c_int32), ("px", C.c_int32), ("py", C.c_int32),
-        ("nccl_id", C.c_void_p), ("stream", C.c_void_p),
+        ("reserved_ptr", C.c_void_p), ("stream", C.c_void_p),
     ]
 
 
@@ -108,7 +108,11 @@ def lib():
             "ipm_last_cell_stats": (st, [P, I, I]),
             "ipm_get_time": (st, [P, C.POINTER(C.c_double)]),
             "ipm_set_time": (st, [P, C.c_double]),
-            "ipm_nccl_unique_id": (st, [P]),
+            "ipm_step_dual": (st, [P, D, D, D, D]),
+            "ipm_step_flux": (st, [P, D, D, D, D, C.c_double, C.POINTER(ipm_step_info)]),
+            "ipm_halo_layout": (st, [P, C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_int64), P, P, P]),
+            "ipm_partition_query": (st, [C.POINTER(ipm_config), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                         C.POINTER(C.c_int32), C.POINTER(C.c_int64), P, P, P, P, P, P]),
             "ipm_last_kernel_ms": (st, [P, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
             "ipm_enable_timing": (st, [P, C.c_int32]),
             "ipm_debug_phase_cycles": (st, [P]),
@@ -147,11 +151,69 @@ def _ptr(t) -> int:
     return 0 if t is None else t.data_ptr()
 
 
+def make_config(cfg: dict, mesh_arrays=None, rank=0, nranks=1, px=1, py=1):
+    """ipm_config for a config dict (inputs/configs.py format); returns (config, arrays to keep alive)."""
+    c = ipm_config()
+    keep = []
+    c.p, c.M, c.q1d, c.m = cfg["p"], cfg["M"], cfg["q1d"], cfg["m"]
+    c.closure, c.flux = CLOSURE[cfg["closure"]], FLUX[cfg["flux"]]
+    c.gamma, c.u_minus, c.u_plus = cfg.get("gamma", 1.4), cfg.get("umin", 0.0), cfg.get("umax", 1.0)
+    mesh = cfg["mesh"]
+    c.mesh_kind = MESH[mesh["kind"]]
+    if mesh["kind"] == "tri":
+        vert, tri, tags = mesh_arrays
+        vert = np.ascontiguousarray(vert, np.float64)
+        tri = np.ascontiguousarray(tri, np.int32)
+        tags = np.ascontiguousarray(tags, np.int32)
+        keep += [vert, tri, tags]
+        c.n_vert, c.n_tri = vert.shape[0], tri.shape[0]
+        c.h_vert, c.h_tri, c.h_tri_tag = vert.ctypes.data, tri.ctypes.data, tags.ctypes.data
+    else:
+        c.nx, c.ny = mesh["nx"], mesh.get("ny", 1)
+        c.x0, c.x1 = mesh["x0"], mesh["x1"]
+        c.y0, c.y1 = mesh.get("y0", 0.0), mesh.get("y1", 1.0)
+        c.periodic = int(mesh.get("periodic", False))
+    for t, (kind, spec) in enumerate(cfg["bc"]):
+        c.bc_kind[t] = BC[kind]
+        c.bc_state[t] = _state(spec)
+    c.tau, c.armijo_c = cfg["tau"], cfg["armijo_c"]
+    c.max_newton, c.max_halvings = cfg["max_newton"], cfg["max_halvings"]
+    c.newton_mode, c.update_form = NEWTON[cfg["newton"]], UPDATE[cfg["update"]]
+    c.cfl = cfg["cfl"]
+    levels = cfg.get("levels") or []
+    c.n_levels = len(levels)
+    for k, Mk in enumerate(levels):
+        c.level_M[k] = Mk
+    c.delta_dec, c.delta_inc = cfg.get("delta_dec", 0.0), cfg.get("delta_inc", 0.0)
+    c.rank, c.nranks, c.px, c.py = rank, nranks, px, py
+    return c, keep
+
+
+def partition_query(cfg: dict, rank: int, nranks: int, px: int = 0, py: int = 0, mesh_arrays=None) -> dict:
+    """Host-only: the partition libipm builds for this rank (no CUDA needed)."""
+    c, keep = make_config(cfg, mesh_arrays, rank, nranks, px, py)
+    cells, nhalo, nsend = C.c_int64(), C.c_int64(), C.c_int64()
+    npeers = C.c_int32()
+    L = lib()
+    check(L.ipm_partition_query(C.byref(c), C.byref(cells), C.byref(nhalo), C.byref(npeers), C.byref(nsend),
+                                None, None, None, None, None, None), "ipm_partition_query")
+    local = np.zeros(cells.value, np.int64)
+    halo = np.zeros(nhalo.value, np.int64)
+    send = np.zeros(nsend.value, np.int64)
+    peers = np.zeros(npeers.value, np.int32)
+    sc = np.zeros(npeers.value, np.int32)
+    rc = np.zeros(npeers.value, np.int32)
+    check(L.ipm_partition_query(C.byref(c), C.byref(cells), C.byref(nhalo), C.byref(npeers), C.byref(nsend),
+                                local.ctypes.data, halo.ctypes.data, peers.ctypes.data, sc.ctypes.data,
+                                rc.ctypes.data, send.ctypes.data), "ipm_partition_query")
+    return dict(local=local, halo=halo, send=send, peers=peers, send_count=sc, recv_count=rc)
+
+
 class Context:
     """One libipm context for a config dict (inputs/configs.py format)."""
 
     def __init__(self, cfg: dict, mesh_arrays=None, device=None, stream=None, rank=0, nranks=1, px=1, py=1,
-                 nccl_id: bytes | None = None):
+                 group=None):
         import torch
 
         self.torch = torch
@@ -159,42 +221,8 @@ class Context:
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         with torch.cuda.device(self.device):
             self.stream = torch.cuda.current_stream(self.device) if stream is None else stream
-        c = ipm_config()
-        c.p, c.M, c.q1d, c.m = cfg["p"], cfg["M"], cfg["q1d"], cfg["m"]
-        c.closure, c.flux = CLOSURE[cfg["closure"]], FLUX[cfg["flux"]]
-        c.gamma, c.u_minus, c.u_plus = cfg.get("gamma", 1.4), cfg.get("umin", 0.0), cfg.get("umax", 1.0)
-        mesh = cfg["mesh"]
-        c.mesh_kind = MESH[mesh["kind"]]
-        self._keep = []
-        if mesh["kind"] == "tri":
-            vert, tri, tags = mesh_arrays
-            vert = np.ascontiguousarray(vert, np.float64)
-            tri = np.ascontiguousarray(tri, np.int32)
-            tags = np.ascontiguousarray(tags, np.int32)
-            self._keep += [vert, tri, tags]
-            c.n_vert, c.n_tri = vert.shape[0], tri.shape[0]
-            c.h_vert, c.h_tri, c.h_tri_tag = vert.ctypes.data, tri.ctypes.data, tags.ctypes.data
-        else:
-            c.nx, c.ny = mesh["nx"], mesh.get("ny", 1)
-            c.x0, c.x1 = mesh["x0"], mesh["x1"]
-            c.y0, c.y1 = mesh.get("y0", 0.0), mesh.get("y1", 1.0)
-            c.periodic = int(mesh.get("periodic", False))
-        for t, (kind, spec) in enumerate(cfg["bc"]):
-            c.bc_kind[t] = BC[kind]
-            c.bc_state[t] = _state(spec)
-        c.tau, c.armijo_c = cfg["tau"], cfg["armijo_c"]
-        c.max_newton, c.max_halvings = cfg["max_newton"], cfg["max_halvings"]
-        c.newton_mode, c.update_form = NEWTON[cfg["newton"]], UPDATE[cfg["update"]]
-        c.cfl = cfg["cfl"]
-        levels = cfg.get("levels") or []
-        c.n_levels = len(levels)
-        for k, Mk in enumerate(levels):
-            c.level_M[k] = Mk
-        c.delta_dec, c.delta_inc = cfg.get("delta_dec", 0.0), cfg.get("delta_inc", 0.0)
-        c.rank, c.nranks, c.px, c.py = rank, nranks, px, py
-        if nccl_id is not None:
-            self._nid = C.create_string_buffer(bytes(nccl_id), 128)
-            c.nccl_id = C.cast(self._nid, C.c_void_p)
+        c, self._keep = make_config(cfg, mesh_arrays, rank, nranks, px, py)
+        self.rank, self.nranks, self.group = rank, nranks, group
         c.stream = self.stream.cuda_stream
         self._c = c
         h = C.c_void_p()
@@ -243,10 +271,43 @@ class Context:
         check(lib().ipm_flux_update(self.h, _ptr(lam), _ptr(uhat_old), _ptr(uhat_new), float(dt), _ptr(dt_out)),
               "ipm_flux_update")
 
+    def _halo_setup(self):
+        npeers, nsend, nrecv = C.c_int32(), C.c_int64(), C.c_int64()
+        check(lib().ipm_halo_layout(self.h, C.byref(npeers), C.byref(nsend), C.byref(nrecv), None, None, None),
+              "ipm_halo_layout")
+        peers = np.zeros(npeers.value, np.int32)
+        sc = np.zeros(npeers.value, np.int32)
+        rc = np.zeros(npeers.value, np.int32)
+        check(lib().ipm_halo_layout(self.h, C.byref(npeers), C.byref(nsend), C.byref(nrecv), peers.ctypes.data,
+                                    sc.ctypes.data, rc.ctypes.data), "ipm_halo_layout")
+        t = self.torch
+        row = self.N * self.m
+        self.halo = dict(peers=peers.tolist(), send_count=sc.tolist(), recv_count=rc.tolist())
+        self.sendbuf = t.zeros((max(int(nsend.value), 1), row), dtype=t.float64, device=self.device)
+        self.recvbuf = t.zeros((max(int(nrecv.value), 1), row), dtype=t.float64, device=self.device)
+        self.rate = t.zeros(1, dtype=t.int64, device=self.device)
+
     def ipm_step(self, uhat, lam, t_end=None, sync=True):
+        """One step; for nranks > 1 the halo exchange and the dt all-reduce run in between
+        (paper_1912_09238_b200.dist, torch.distributed)."""
         info = ipm_step_info() if sync else None
         te = -1.0 if t_end is None else float(t_end)
-        rc = lib().ipm_step(self.h, _ptr(uhat), _ptr(lam), te, C.byref(info) if sync else None)
+        if self.nranks <= 1:
+            rc = lib().ipm_step(self.h, _ptr(uhat), _ptr(lam), te, C.byref(info) if sync else None)
+        else:
+            from . import dist
+
+            if not hasattr(self, "sendbuf"):
+                self._halo_setup()
+            check(lib().ipm_step_dual(self.h, _ptr(uhat), _ptr(lam), _ptr(self.sendbuf), _ptr(self.rate)),
+                  "ipm_step_dual")
+            dist.halo_exchange(self.sendbuf, self.recvbuf, self.halo, self.group)
+            dist.allreduce_max_(self.rate, self.group)
+            rc = lib().ipm_step_flux(self.h, _ptr(uhat), _ptr(lam), _ptr(self.recvbuf), _ptr(self.rate), te,
+                                     C.byref(info) if sync else None)
+            if sync and rc in (0, 5):
+                dist.reduce_info_(info, self.device, self.group)
+                rc = 5 if info.failed_cells else 0
         if rc == 5:  # IPM_ERR_NUMERIC: report, caller decides
             return info
         check(rc, "ipm_step")

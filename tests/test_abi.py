@@ -50,7 +50,7 @@ int main(void) {{
   printf("ipm_step_info %zu\\n", sizeof(ipm_step_info));
   O(ipm_config, gamma); O(ipm_config, x0); O(ipm_config, h_vert); O(ipm_config, bc_kind);
   O(ipm_config, bc_state); O(ipm_config, tau); O(ipm_config, cfl); O(ipm_config, n_levels);
-  O(ipm_config, delta_dec); O(ipm_config, rank); O(ipm_config, nccl_id); O(ipm_config, stream);
+  O(ipm_config, delta_dec); O(ipm_config, rank); O(ipm_config, reserved_ptr); O(ipm_config, stream);
   O(ipm_ic, xs0); O(ipm_ic, state); O(ipm_step_info, newton_iters); O(ipm_step_info, worst_status);
   return 0;
 }}
