@@ -801,10 +801,9 @@ int launch_dual(const KernelCtx& k, const DualLaunch& a) {
   if (!k.force_warp_kernel) {
     int G, T;
     group_shape(k.T.N, G, T);
-    // sum factorisation for p = 2 tensor rules (SF = M + 1); opt-in with IPM_SUMFACT=1 (it costs
-    // shared memory, i.e. cells in flight, which measured slower on cfg 3)
+    // sum factorisation for p = 2 tensor rules (SF = M + 1); IPM_SUMFACT=0 selects the direct sum
     const char* sfe = std::getenv("IPM_SUMFACT");
-    const int SF = (k.T.p == 2 && (sfe && sfe[0] == '1')) ? (int)std::lround((std::sqrt(8.0 * k.T.npr + 1) - 1) / 2) : 0;
+    const int SF = (k.T.p == 2 && !(sfe && sfe[0] == '0')) ? (int)std::lround((std::sqrt(8.0 * k.T.npr + 1) - 1) / 2) : 0;
     const int key = (((k.closure * 10 + k.m) * 1000 + G) * 10 + SF) * 10 + T;
     int rc = -1;
     switch (key) {
