@@ -34,12 +34,15 @@ struct GroupLayout {
   // doubles per group: 5 vectors + node buffer / L blocks / sum-factorisation stage + reduction + control
   //   direct (SF = 0): union(node buffer, L blocks)
   //   SF > 0:          node buffer, then union(T stage [q][npr][MM], L blocks)
+  // sum factorisation builds T_ab[k1][pr][ab] in NCH chunks of CHW ab-components so that
+  // (node buffer + one T chunk) fits where the L blocks go later
+  static constexpr int NCH = (MM >= 6) ? 2 : 1;
+  static constexpr int CHW = (MM + NCH - 1) / NCH;
   static __host__ __device__ int region(int N, int Q, int SF, int q1d) {
     const int NP = N * (N + 1) / 2;
     const int nb = Q * NS, lb = NP * TBP;
-    if (SF == 0) return nb > lb ? nb : lb;
-    const int tb = q1d * (SF * (SF + 1) / 2) * MM;
-    return nb + (tb > lb ? tb : lb);
+    const int used = (SF == 0) ? nb : nb + q1d * (SF * (SF + 1) / 2) * CHW;
+    return used > lb ? used : lb;
   }
   static __host__ __device__ int per_group(int N, int Q, int G, int SF = 0, int q1d = 0) {
     const int n = N * MS;
@@ -102,8 +105,8 @@ __global__ void __launch_bounds__(IPM_GROUP_THREADS) k_dual_group(DualParams P) 
   double* g = uh + nmax;
   double* dd = g + nmax;
   double* nb = dd + nmax;                   // node buffer
-  double* Ls = (SF > 0) ? nb + Q * NS : nb;  // L blocks (union with nb, or with the T stage)
-  double* Tt = Ls;                          // sum-factorisation stage T[k1][pr][ab] (SF > 0)
+  double* Ls = nb;           // L blocks (union with the node buffer and the T stage)
+  double* Tt = nb + Q * NS;  // sum-factorisation stage chunk T[k1][pr][c] (SF > 0)
   double* Linv = nb + Lay::region(N, Q, SF, q1);  // [N] inverses of the diagonal Cholesky blocks
   double* red = Linv + (size_t)N * TB;  // [2 slots][RS][NW]
   int* ctl = (int*)(red + 2 * Lay::RS * NW);
@@ -229,17 +232,23 @@ __global__ void __launch_bounds__(IPM_GROUP_THREADS) k_dual_group(DualParams P) 
     ad = sa;
   };
 
-  // blocks (I, J) owned by this thread: p = t + s G, row-major lower enumeration p = I(I+1)/2 + J
+  // blocks (I, J) owned by this thread: rank r = t + s G in the order J descending, then I
+  // ascending.  The blocks still updated in late Cholesky steps (large J) are then packed into the
+  // first threads, so the other warps skip those phases instead of issuing them for idle lanes.
+  // Shared-memory blocks are stored at the row-major lower index I(I+1)/2 + J.
   int bIa[T], bJa[T];
+  auto assign_blocks = [&](int Nl) {
 #pragma unroll
-  for (int s = 0; s < T; ++s) {
-    const int pp = t + s * G;
-    int bI = (int)((sqrtf(8.0f * pp + 1.0f) - 1.0f) * 0.5f);
-    while (bI * (bI + 1) / 2 > pp) --bI;
-    while ((bI + 1) * (bI + 2) / 2 <= pp) ++bI;
-    bIa[s] = bI;
-    bJa[s] = pp - bI * (bI + 1) / 2;
-  }
+    for (int q = 0; q < T; ++q) {
+      int r = t + q * G, J = Nl - 1;
+      while (J > 0 && r >= Nl - J) {
+        r -= Nl - J;
+        --J;
+      }
+      bJa[q] = J;
+      bIa[q] = J + r;
+    }
+  };
 
   for (;;) {
     if (t == 0) ctl[0] = atomicAdd(&P.sc->work_counter, 1);
@@ -254,6 +263,7 @@ __global__ void __launch_bounds__(IPM_GROUP_THREADS) k_dual_group(DualParams P) 
     bool owna[T];
 #pragma unroll
     for (int q = 0; q < T; ++q) owna[q] = (t + q * G) < NPl;
+    assign_blocks(Nl);
     const double* gu = A.uhat + cell * nmax;
     double* gl = A.lam + cell * nmax;
     for (int r = t; r < n; r += G) {
@@ -287,47 +297,65 @@ __global__ void __launch_bounds__(IPM_GROUP_THREADS) k_dual_group(DualParams P) 
         // ---- Hessian block in registers -------------------------------------------------------
         double blk[T][MS][MS];
         if constexpr (SF > 0) {
-          // sum factorisation over the tensor rule (p = 2), k = k1 q + k2:
+          // sum factorisation over the tensor rule (p = 2), k = k1 q + k2, in ab-chunks:
           //   T_ab[k1][(i2,j2)] = sum_k2 LL[k2][(i2,j2)] J_ab(k1,k2)
           //   H_ab[I][J]       = sum_k1 LL[k1][(i1,j1)] T_ab[k1][(i2,j2)]
-          for (int e = t; e < q1 * MM; e += G) {
-            const int k1 = e / MM, ab = e - k1 * MM;
-            double acc[NPR];
+          constexpr int NCH = Lay::NCH, CHW = Lay::CHW;
+          double acc[T][MM];
 #pragma unroll
-            for (int pr = 0; pr < NPR; ++pr) acc[pr] = 0.0;
-            for (int k2 = 0; k2 < q1; ++k2) {
-              const double jv = nb[(k1 * q1 + k2) * NS + MS + ab];
-              const double* ll = sLL + k2 * NPR;
+          for (int q = 0; q < T; ++q)
 #pragma unroll
-              for (int pr = 0; pr < NPR; ++pr) acc[pr] = fma(ll[pr], jv, acc[pr]);
-            }
-#pragma unroll
-            for (int pr = 0; pr < NPR; ++pr) Tt[(k1 * NPR + pr) * MM + ab] = acc[pr];
-          }
-          gsync();
+            for (int z = 0; z < MM; ++z) acc[q][z] = 0.0;
+          int pr1[T], pr2[T];
 #pragma unroll
           for (int q = 0; q < T; ++q) {
-            if (!owna[q]) continue;
-            int a1 = P.T.idx[bIa[q] * 2], a2 = P.T.idx[bIa[q] * 2 + 1];
-            int b1 = P.T.idx[bJa[q] * 2], b2 = P.T.idx[bJa[q] * 2 + 1];
+            const int I = owna[q] ? bIa[q] : 0, J = owna[q] ? bJa[q] : 0;
+            int a1 = P.T.idx[I * 2], a2 = P.T.idx[I * 2 + 1], b1 = P.T.idx[J * 2], b2 = P.T.idx[J * 2 + 1];
             if (a1 > b1) { const int x = a1; a1 = b1; b1 = x; }
             if (a2 > b2) { const int x = a2; a2 = b2; b2 = x; }
-            const int pr1 = a1 * SF - a1 * (a1 - 1) / 2 + (b1 - a1);
-            const int pr2 = a2 * SF - a2 * (a2 - 1) / 2 + (b2 - a2);
-            double acc[MM];
+            pr1[q] = a1 * SF - a1 * (a1 - 1) / 2 + (b1 - a1);
+            pr2[q] = a2 * SF - a2 * (a2 - 1) / 2 + (b2 - a2);
+          }
 #pragma unroll
-            for (int z = 0; z < MM; ++z) acc[z] = 0.0;
-            for (int k1 = 0; k1 < q1; ++k1) {
-              const double lv = sLL[k1 * NPR + pr1];
-              const double* Tk = Tt + (k1 * NPR + pr2) * MM;
+          for (int ch = 0; ch < NCH; ++ch) {
+            const int ab0 = ch * CHW;
+            const int nab = (MM - ab0) < CHW ? (MM - ab0) : CHW;
+            for (int e = t; e < q1 * nab; e += G) {
+              const int k1 = e / nab, c = e - k1 * nab;
+              double at[NPR];
 #pragma unroll
-              for (int z = 0; z < MM; ++z) acc[z] = fma(lv, Tk[z], acc[z]);
+              for (int pr = 0; pr < NPR; ++pr) at[pr] = 0.0;
+              const double* jrow = nb + (k1 * q1) * NS + MS + ab0 + c;
+              for (int k2 = 0; k2 < q1; ++k2) {
+                const double jv = jrow[k2 * NS];
+                const double* ll = sLL + k2 * NPR;
+#pragma unroll
+                for (int pr = 0; pr < NPR; ++pr) at[pr] = fma(ll[pr], jv, at[pr]);
+              }
+#pragma unroll
+              for (int pr = 0; pr < NPR; ++pr) Tt[(k1 * NPR + pr) * CHW + c] = at[pr];
             }
+            gsync();
+#pragma unroll
+            for (int q = 0; q < T; ++q) {
+              if (!owna[q]) continue;
+              for (int k1 = 0; k1 < q1; ++k1) {
+                const double lv = sLL[k1 * NPR + pr1[q]];
+                const double* Tk = Tt + (k1 * NPR + pr2[q]) * CHW;
+#pragma unroll
+                for (int c = 0; c < CHW; ++c)
+                  if (ab0 + c < MM) acc[q][ab0 + c] = fma(lv, Tk[c], acc[q][ab0 + c]);
+              }
+            }
+            if (ch + 1 < NCH) gsync();  // T chunk is rewritten by the next chunk
+          }
+#pragma unroll
+          for (int q = 0; q < T; ++q)
 #pragma unroll
             for (int a = 0; a < MS; ++a)
 #pragma unroll
-              for (int b = 0; b < MS; ++b) blk[q][a][b] = acc[a <= b ? sym_idx<MS>(a, b) : sym_idx<MS>(b, a)];
-          }
+              for (int b = 0; b < MS; ++b)
+                blk[q][a][b] = acc[q][a <= b ? sym_idx<MS>(a, b) : sym_idx<MS>(b, a)];
         } else {
           // direct: H_IJ = sum_k (omega_k phi_kI phi_kJ) J_k; the J_k row is loaded once for all of
           // this thread's blocks
@@ -407,7 +435,7 @@ __global__ void __launch_bounds__(IPM_GROUP_THREADS) k_dual_group(DualParams P) 
               li[r][c] = -inv[r] * v;
             }
           }
-          double* o = Ls + (size_t)(t + q * G) * TB;
+          double* o = Ls + (size_t)(bIa[q] * (bIa[q] + 1) / 2 + bJa[q]) * TB;
           double* oi = Linv + (size_t)K * TB;
 #pragma unroll
           for (int aa = 0; aa < MS; ++aa)
@@ -456,7 +484,7 @@ __global__ void __launch_bounds__(IPM_GROUP_THREADS) k_dual_group(DualParams P) 
             double yk[MS];
 #pragma unroll
             for (int x = 0; x < MS; ++x) yk[x] = dd[K * MS + x];
-            double* o = Ls + (size_t)(t + q * G) * TB;
+            double* o = Ls + (size_t)(bIa[q] * (bIa[q] + 1) / 2 + bJa[q]) * TB;
             const int bI = bIa[q];
 #pragma unroll
             for (int r = 0; r < MS; ++r) {
