@@ -103,8 +103,9 @@ struct Closure<CL_EULER, MS> {
   static constexpr int D = MS - 2;
   static constexpr int MM = MS * (MS + 1) / 2;
   __device__ static bool eval(const double* v, double* u, double* J, double& sstar, const ClParams& c) {
+    // branch-free (an early exit would leave u, J partly unwritten and force them to local memory);
+    // vE >= 0 makes log(-vE) NaN and the state inadmissible
     const double g = c.gamma, vE = v[MS - 1];
-    if (!(vE < 0.0)) return false;
     double vm2 = 0.0;
 #pragma unroll
     for (int k = 0; k < D; ++k) vm2 = fma(v[1 + k], v[1 + k], vm2);
@@ -138,7 +139,7 @@ struct Closure<CL_EULER, MS> {
     }
     J[sym_idx<MS>(0, MS - 1)] = E;
     J[sym_idx<MS>(MS - 1, MS - 1)] = rho * H * H - g * p * p * irho * igm1;
-    return rho > 0.0 && isfinite(rho) && isfinite(E);
+    return vE < 0.0 && rho > 0.0 && isfinite(rho) && isfinite(E);
   }
   // v = ((gamma - S)/(gamma-1) - rho|w|^2/(2p), rho w/p, -rho/p), S = ln p - gamma ln rho
   __device__ static bool grad_s(const double* u, double* v, const ClParams& c) {

@@ -1,0 +1,797 @@
+// ipm_dual_mma.cuh — dual solve with a register-resident, DMMA-blocked Cholesky (sm_100a, fp64).
+//
+// Same method as k_dual_group (Algorithm 1 / 2, reading 3' line search), with the
+// Newton system solved on the fp64 tensor path:
+//   * a group of W warps owns one spatial cell at a time (cells from an atomic queue);
+//   * the Hessian H = sum_k omega_k (phi_k phi_k^T) (x) J_k is built as the
+//     N(N+1)/2 x m(m+1)/2 table S[ab][pair] of its unique entries (sum factorised over the tensor
+//     Gauss-Legendre rule when p = 2, else the direct sum), then gathered into 8 x 8 blocks of the
+//     padded n x n matrix (n = N m, padded with the identity to NB*8);
+//   * every lower-triangular 8 x 8 block lives in the registers of one warp in the accumulator
+//     layout of mma.sync.m8n8k4.f64 (lane l: row l/4, columns 2(l%4), 2(l%4)+1);
+//   * right-looking blocked Cholesky, one block column K per step:
+//       diag     owner of (K,K): unblocked factor by quad shuffles, Linv_K = L_KK^{-1} formed on the
+//                fly; y_K = Linv_K b_K (forward solve folded in);
+//       panel    owners of (I,K): L_IK = A_IK Linv_K^T (2 DMMA), b_I -= L_IK y_K, L_IK published to
+//                shared memory in operand (A-fragment) order;
+//       trailing owners of (I,J), J > K: A_IJ -= L_IK L_JK^T (2 DMMA); the owner of (K+1,K+1)
+//                updates and factors it first (look-ahead);
+//   * back substitution L^T d = y with the register blocks (Linv_K^T on the diagonal, L_KJ^T below).
+#pragma once
+// (included inside namespace ipm by ipm_kernels.cu, after DualParams and node_rate)
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+// ordered shared-memory load (volatile: not hoisted across the DMMAs, which bounds register use)
+__device__ __forceinline__ double lds_ord(const double* p) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return v;
+}
+__device__ __forceinline__ double dneg(double x) {
+  return __longlong_as_double(__double_as_longlong(x) ^ (long long)0x8000000000000000ULL);
+}
+
+// column-major enumeration of the lower block triangle: r -> (I, J), J = 0.., I = J..NB-1
+__host__ __device__ constexpr int cmJ(int r, int NB) {
+  int J = 0;
+  while (r >= NB - J) {
+    r -= NB - J;
+    ++J;
+  }
+  return J;
+}
+__host__ __device__ constexpr int cmI(int r, int NB) {
+  int J = 0;
+  while (r >= NB - J) {
+    r -= NB - J;
+    ++J;
+  }
+  return J + r;
+}
+
+template <int MS>
+struct MmaLayout {
+  static constexpr int MM = MS * (MS + 1) / 2;
+  static constexpr int NCH = (MM >= 6) ? 2 : 1;  // ab chunks of the sum factorisation
+  static constexpr int CHW = (MM + NCH - 1) / NCH;
+  static constexpr int RSX = MS > 4 ? MS : 4;  // values per group reduction
+  // region (per group):  [node buffer u[MS][Q], J[MM][Q]]  overlapped by  S[MM][NPP]
+  //                      [T chunk q1 x NPR x CHW] at offset TO (SF only)
+  // S may overlap the dead part of the node buffer chunk by chunk (see s_base)
+  static __host__ __device__ int npp(int N) { return N * (N + 1) / 2; }
+  static __host__ __device__ int node(int Q) { return Q * (MS + MM); }
+  static __host__ __device__ bool s_overlaps(int N, int Q, int SF) {
+    if (SF == 0) return false;  // the direct sum reads J until the end
+    for (int ch = 0; ch + 1 < NCH; ++ch)
+      if ((ch + 1) * CHW * npp(N) > (MS + (ch + 1) * CHW) * Q) return false;
+    return true;
+  }
+  static __host__ __device__ int t_off(int N, int Q, int SF) {
+    const int s = s_overlaps(N, Q, SF) ? MM * npp(N) : 0;
+    return ((node(Q) > s ? node(Q) : s) + 1) & ~1;
+  }
+  static __host__ __device__ int s_base(int N, int Q, int SF, int q1d) {
+    if (s_overlaps(N, Q, SF)) return 0;
+    const int t = (SF > 0) ? q1d * (SF * (SF + 1) / 2) * CHW : 0;
+    return (t_off(N, Q, SF) + t + 1) & ~1;
+  }
+  static __host__ __device__ int region(int N, int Q, int SF, int q1d, int NB) {
+    int r = s_base(N, Q, SF, q1d) + MM * npp(N);
+    const int t = t_off(N, Q, SF) + ((SF > 0) ? q1d * (SF * (SF + 1) / 2) * CHW : 0);
+    if (t > r) r = t;
+    const int c = (2 * NB + 1) * 64;  // Cholesky: panel [NB][64], Linv fragment [64], diagonal [NB][64]
+    if (c > r) r = c;
+    return (r + 1) & ~1;
+  }
+  static __host__ __device__ int per_group(int N, int Q, int W, int SF, int q1d, int NB) {
+    const int nv = NB * 8;  // padded vector length
+    int w = 5 * nv + region(N, Q, SF, q1d, NB) + 2 * RSX * W + 4;
+    return (w + 1) & ~1;
+  }
+};
+
+template <int CL, int MS, int NB, int W, int SF>
+struct DualMma {
+  using Lay = MmaLayout<MS>;
+  static constexpr int MM = Lay::MM;
+  static constexpr int G = 32 * W;
+  static constexpr int NBT = NB * (NB + 1) / 2;
+  
+  // ---- 8x8 diagonal block: in C-fragment layout A (lower part used); out: Linv = L^{-1} -------
+  __device__ static bool diag_factor(double& a0, double& a1, int lane) {
+    const int r = lane >> 2, q = lane & 3;
+    double x0 = (r == 2 * q) ? 1.0 : 0.0, x1 = (r == 2 * q + 1) ? 1.0 : 0.0;
+    bool ok = true;
+#pragma unroll 1
+    for (int c = 0; c < 8; ++c) {
+      const int cq = c >> 1;
+      const double mine = (c & 1) ? a1 : a0;
+      const double d = __shfl_sync(FULL_MASK, mine, c * 4 + cq);
+      const double arc = __shfl_sync(FULL_MASK, mine, r * 4 + cq);
+      const double a0c = __shfl_sync(FULL_MASK, mine, (2 * q) * 4 + cq);
+      const double a1c = __shfl_sync(FULL_MASK, mine, (2 * q + 1) * 4 + cq);
+      if (!(d > 0.0) || !isfinite(d)) ok = false;
+      const double rs = rsqrt(d);
+      const double lrc = arc * rs;
+      if (2 * q > c) a0 = fma(-lrc, a0c * rs, a0);
+      if (2 * q + 1 > c) a1 = fma(-lrc, a1c * rs, a1);
+      if (r == c) {
+        x0 *= rs;
+        x1 *= rs;
+      }
+      const double xc0 = __shfl_sync(FULL_MASK, x0, c * 4 + q);
+      const double xc1 = __shfl_sync(FULL_MASK, x1, c * 4 + q);
+      if (r > c) {
+        x0 = fma(-lrc, xc0, x0);
+        x1 = fma(-lrc, xc1, x1);
+      }
+    }
+    a0 = x0;
+    a1 = x1;
+    return ok;
+  }
+
+  // C-fragment -> A-fragment (lane l: row l/4, column l%4 + 4 kk)
+  __device__ static void to_afrag(double c0, double c1, int lane, double& f0, double& f1) {
+    const int r = lane >> 2, q = lane & 3;
+    const int s0 = r * 4 + (q >> 1), s1 = s0 + 2;
+    const double u0 = __shfl_sync(FULL_MASK, c0, s0), u1 = __shfl_sync(FULL_MASK, c1, s0);
+    const double v0 = __shfl_sync(FULL_MASK, c0, s1), v1 = __shfl_sync(FULL_MASK, c1, s1);
+    f0 = (q & 1) ? u1 : u0;
+    f1 = (q & 1) ? v1 : v0;
+  }
+  // store a C-fragment block into operand (A-fragment) order: element (r, c) at (c/4)*32 + r*4 + c%4
+  __device__ static void store_afrag(double* dst, double c0, double c1, int lane) {
+    const int r = lane >> 2, q = lane & 3;
+    double2* p = reinterpret_cast<double2*>(dst + (q >> 1) * 32 + r * 4 + 2 * (q & 1));
+    *p = make_double2(c0, c1);
+  }
+
+  // H entry (R, C) from the unique-entry table S[ab][pair(i >= j)]; identity outside n x n
+  __device__ static double hval(const double* S, int npp, int n, int R, int C) {
+    if (R >= n || C >= n) return (R == C) ? 1.0 : 0.0;
+    if (R < C) {
+      const int x = R;
+      R = C;
+      C = x;
+    }
+    const int i = R / MS, a = R - i * MS, j = C / MS, b = C - j * MS;
+    const int ab = (a <= b) ? sym_idx<MS>(a, b) : sym_idx<MS>(b, a);
+    return S[ab * npp + i * (i + 1) / 2 + j];
+  }
+
+  // Gather H (unique-entry table S[ab][pair]) into 8x8 blocks, factor, solve.
+  //   strictly-lower blocks: registers of warp (column-major rank) % W, C-fragment layout; the
+  //                          (I, J) of slot s of warp wr is byte s of ijp (packed 4 per word)
+  //   diagonal blocks:       shared memory dg[K][lane][2] (C-fragment order), owned by warp K % W;
+  //                          after the factorisation they hold Linv_K
+  //   pan[I] (A-fragment order): the current panel L_IK;  linvf: Linv_K in A-fragment order
+  // dd: in -b (padded with zeros to NB*8), out: the Newton direction.  Returns SPD.
+  static constexpr int NBO = NB * (NB - 1) / 2;               // strictly-lower blocks
+  static constexpr int NBW2 = NBO > 0 ? (NBO + W - 1) / W : 1;  // per warp (upper bound)
+  static constexpr int NDW = (NB + W - 1) / W;                // diagonal blocks per warp
+  static constexpr int NIJ = (NBW2 + 3) / 4;                  // packed slot words
+  __host__ __device__ static constexpr int oJ(int r) { return cmJ(r, NB - 1); }
+  __host__ __device__ static constexpr int oI(int r) { return cmI(r, NB - 1) + 1; }
+  // slot table for warp wr: byte s = I << 4 | J, 0xff = empty
+  __host__ __device__ static unsigned slot_word(int wr, int w4) {
+    unsigned v = 0;
+    for (int k = 0; k < 4; ++k) {
+      const int s = 4 * w4 + k, br = s * W + wr;
+      const unsigned b = (s < NBW2 && br < NBO) ? (unsigned)((oI(br) << 4) | oJ(br)) : 0xffu;
+      v |= b << (8 * k);
+    }
+    return v;
+  }
+
+  __device__ static bool chol_solve(const double* S, int npp, double* dd, double* reg, int* ctl, int n, int NBl,
+                                    int lane, int wr, int bar, const unsigned* ijtab) {
+    const int r = lane >> 2, q = lane & 3;
+    double* pan = reg;                // [NB][64]
+    double* linvf = reg + NB * 64;    // [64]
+    double* dg = reg + NB * 64 + 64;  // [NB][64]
+    unsigned ijp[NIJ];
+#pragma unroll
+    for (int w4 = 0; w4 < NIJ; ++w4) ijp[w4] = ijtab[wr * NIJ + w4];
+    auto slotI = [&](int s) -> int { return (ijp[s >> 2] >> (8 * (s & 3) + 4)) & 15; };
+    auto slotJ = [&](int s) -> int { return (ijp[s >> 2] >> (8 * (s & 3))) & 15; };
+    auto slotOk = [&](int s) -> bool { return ((ijp[s >> 2] >> (8 * (s & 3))) & 0xff) != 0xff; };
+#ifdef IPM_PHASE_TIMERS
+    long long ct0 = clock64();
+#define CPH(i)                                                                                  \
+  do {                                                                                          \
+    const long long now_ = clock64();                                                           \
+    if (lane == 0 && wr == 0) atomicAdd(&g_phase_cycles[i], (unsigned long long)(now_ - ct0)); \
+    ct0 = now_;                                                                                 \
+  } while (0)
+#else
+#define CPH(i) \
+  do {         \
+  } while (0)
+#endif
+    double blk[NBW2][2];
+    double dtmp[NDW][2];
+    // ---- gather ------------------------------------------------------------------------------
+    if constexpr (MS == 4) {
+      // 8x8 block (I, J) = basis functions (2I + r/4, 2J + c/4): S offsets from lane constants
+      const int hi = r >> 2, a = r & 3, hq = q >> 1;
+      int abn[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int b = 2 * (q & 1) + e;
+        abn[e] = ((a <= b) ? sym_idx<4>(a, b) : sym_idx<4>(b, a)) * npp;
+      }
+      const int hmx = hi > hq ? hi : hq, hmn = hi + hq - hmx;
+#pragma unroll
+      for (int s = 0; s < NBW2; ++s) {
+        if (slotOk(s)) {
+          const int I = slotI(s), J = slotJ(s);
+          const int o = I * (2 * I + 1) + hi * (2 * I + 1) + 2 * J + hq;
+          const bool rin = 8 * I + r < n;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) blk[s][e] = (rin && 8 * J + 2 * q + e < n) ? S[abn[e] + o] : 0.0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < NDW; ++u) {
+        const int K = u * W + wr;
+        if (K < NB) {
+          const int o = K * (2 * K + 1) + hmx * (2 * K + 1) + 2 * K + hmn;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int R = 8 * K + r, C = 8 * K + 2 * q + e;
+            dtmp[u][e] = (R < n && C < n) ? S[abn[e] + o] : ((R == C) ? 1.0 : 0.0);
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int s = 0; s < NBW2; ++s) {
+        if (slotOk(s)) {
+          const int I = slotI(s), J = slotJ(s);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) blk[s][e] = hval(S, npp, n, 8 * I + r, 8 * J + 2 * q + e);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < NDW; ++u) {
+        const int K = u * W + wr;
+        if (K < NB) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) dtmp[u][e] = hval(S, npp, n, 8 * K + r, 8 * K + 2 * q + e);
+        }
+      }
+    }
+    if (lane == 0 && wr == 0) ctl[1] = 0;
+    named_sync(bar, G);  // S is dead: the Cholesky buffers reuse it
+#pragma unroll
+    for (int u = 0; u < NDW; ++u) {
+      const int K = u * W + wr;
+      if (K < NB) *reinterpret_cast<double2*>(dg + K * 64 + 2 * lane) = make_double2(dtmp[u][0], dtmp[u][1]);
+    }
+    named_sync(bar, G);
+    CPH(4);
+    bool ok = true;
+    // K = -1 only factors the first diagonal block (look-ahead of the loop)
+#pragma unroll 1
+    for (int K = -1; K < NBl; ++K) {
+      if (ctl[1]) {
+        ok = false;
+        break;
+      }
+      // ---- panel: L_IK = A_IK Linv_K^T, b_I -= L_IK y_K ---------------------------------------
+      if (K >= 0) {
+        const double lf0 = linvf[lane], lf1 = linvf[32 + lane];
+        const double y0 = dd[K * 8 + 2 * q], y1 = dd[K * 8 + 2 * q + 1];
+#pragma unroll
+        for (int s = 0; s < NBW2; ++s) {
+          if (!slotOk(s)) continue;
+          const int I = slotI(s), J = slotJ(s);
+          if (J != K || I >= NBl) continue;
+          double f0, f1;
+          to_afrag(blk[s][0], blk[s][1], lane, f0, f1);
+          double x0 = 0.0, x1 = 0.0;
+          dmma884(x0, x1, f0, lf0);
+          dmma884(x0, x1, f1, lf1);
+          blk[s][0] = x0;
+          blk[s][1] = x1;
+          store_afrag(pan + I * 64, x0, x1, lane);
+          double v = fma(x0, y0, x1 * y1);
+          v += __shfl_xor_sync(FULL_MASK, v, 1);
+          v += __shfl_xor_sync(FULL_MASK, v, 2);
+          if (q == 0) dd[I * 8 + r] -= v;
+        }
+        named_sync(bar, G);
+      }
+      // ---- trailing update; (K+1, K+1) first, then factored at once (look-ahead) ---------------
+      if (K + 1 < NBl && (K + 1) % W == wr) {
+        double2 v = *reinterpret_cast<const double2*>(dg + (K + 1) * 64 + 2 * lane);
+        if (K >= 0) {
+          const double p0 = lds_ord(pan + (K + 1) * 64 + lane), p1 = lds_ord(pan + (K + 1) * 64 + 32 + lane);
+          dmma884(v.x, v.y, dneg(p0), p0);
+          dmma884(v.x, v.y, dneg(p1), p1);
+        }
+        // Linv_{K+1} (kept in dg), its operand copy, y_{K+1} = Linv b_{K+1}
+        double a0 = v.x, a1 = v.y;
+        const bool okd = diag_factor(a0, a1, lane);
+        *reinterpret_cast<double2*>(dg + (K + 1) * 64 + 2 * lane) = make_double2(a0, a1);
+        store_afrag(linvf, a0, a1, lane);
+        const double b0 = dd[(K + 1) * 8 + 2 * q], b1 = dd[(K + 1) * 8 + 2 * q + 1];
+        double y = fma(a0, b0, a1 * b1);
+        y += __shfl_xor_sync(FULL_MASK, y, 1);
+        y += __shfl_xor_sync(FULL_MASK, y, 2);
+        __syncwarp();
+        if (q == 0) dd[(K + 1) * 8 + r] = y;
+        if (lane == 0 && !okd) ctl[1] = 1;
+      }
+      if (K >= 0) {
+#pragma unroll
+        for (int u = 0; u < NDW; ++u) {
+          const int Jd = u * W + wr;
+          if (Jd <= K + 1 || Jd >= NBl) continue;
+          double2 v = *reinterpret_cast<const double2*>(dg + Jd * 64 + 2 * lane);
+          const double p0 = lds_ord(pan + Jd * 64 + lane), p1 = lds_ord(pan + Jd * 64 + 32 + lane);
+          dmma884(v.x, v.y, dneg(p0), p0);
+          dmma884(v.x, v.y, dneg(p1), p1);
+          *reinterpret_cast<double2*>(dg + Jd * 64 + 2 * lane) = v;
+        }
+#pragma unroll
+        for (int s = 0; s < NBW2; ++s) {
+          if (!slotOk(s)) continue;
+          const int I = slotI(s), J = slotJ(s);
+          if (J <= K || I >= NBl) continue;
+          const double a0 = dneg(lds_ord(pan + I * 64 + lane)), a1 = dneg(lds_ord(pan + I * 64 + 32 + lane));
+          const double b0 = lds_ord(pan + J * 64 + lane), b1 = lds_ord(pan + J * 64 + 32 + lane);
+          dmma884(blk[s][0], blk[s][1], a0, b0);
+          dmma884(blk[s][0], blk[s][1], a1, b1);
+        }
+      }
+      named_sync(bar, G);
+    }
+    CPH(5);
+    if (!ok) return false;
+    // ---- back substitution: d_K = Linv_K^T z_K; z_J -= L_KJ^T d_K (J < K) --------------------------
+#pragma unroll 1
+    for (int K = NBl - 1; K >= 0; --K) {
+      if (K % W == wr) {
+        const double2 li = *reinterpret_cast<const double2*>(dg + K * 64 + 2 * lane);
+        const double z = dd[K * 8 + r];
+        double v0 = li.x * z, v1 = li.y * z;
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+          v0 += __shfl_xor_sync(FULL_MASK, v0, o);
+          v1 += __shfl_xor_sync(FULL_MASK, v1, o);
+        }
+        __syncwarp();
+        if (r == 0) {
+          dd[K * 8 + 2 * q] = v0;
+          dd[K * 8 + 2 * q + 1] = v1;
+        }
+      }
+      named_sync(bar, G);
+      if (K == 0) break;
+#pragma unroll
+      for (int s = 0; s < NBW2; ++s) {
+        if (!slotOk(s)) continue;
+        const int I = slotI(s), J = slotJ(s);
+        if (I != K) continue;
+        const double dk = dd[K * 8 + r];
+        double v0 = blk[s][0] * dk, v1 = blk[s][1] * dk;
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+          v0 += __shfl_xor_sync(FULL_MASK, v0, o);
+          v1 += __shfl_xor_sync(FULL_MASK, v1, o);
+        }
+        if (r == 0) {
+          dd[J * 8 + 2 * q] -= v0;
+          dd[J * 8 + 2 * q + 1] -= v1;
+        }
+      }
+      named_sync(bar, G);
+    }
+    CPH(6);
+    return true;
+#undef CPH
+  }
+};
+
+#ifdef IPM_PHASE_TIMERS
+#define MPHASE(i)                                                  \
+  do {                                                             \
+    const long long now_ = clock64();                              \
+    if (t == 0) ph_acc[i] += (unsigned long long)(now_ - ph_t0);   \
+    ph_t0 = now_;                                                  \
+  } while (0)
+#else
+#define MPHASE(i) \
+  do {            \
+  } while (0)
+#endif
+
+template <int CL, int MS, int NB, int W, int SF>
+#ifndef IPM_MMA_THREADS
+#define IPM_MMA_THREADS 512
+#endif
+__global__ void __launch_bounds__(IPM_MMA_THREADS) k_dual_mma(DualParams P) {
+#ifdef IPM_PHASE_TIMERS
+  unsigned long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long ph_t0 = clock64();
+#endif
+  using D = DualMma<CL, MS, NB, W, SF>;
+  using Lay = MmaLayout<MS>;
+  constexpr int G = D::G, MM = Lay::MM, NV = NB * 8;
+  extern __shared__ __align__(16) double sm[];
+  const int N = P.T.N, Q = P.T.Q, QP = P.T.QP;
+  constexpr int NPR = SF * (SF + 1) / 2;
+  double* sPhiT = sm;
+  double* sWPhiT = sm + N * QP;
+  double* sLL = sm + 2 * N * QP;  // [q1d][NPR] (SF > 0)
+  const int q1 = P.T.q1d;
+  unsigned* sIJ = (unsigned*)(sm + 2 * N * QP + ((SF > 0) ? ((q1 * NPR + 1) & ~1) : 0));  // [W][NIJ]
+  const int tabsz = 2 * N * QP + ((SF > 0) ? ((q1 * NPR + 1) & ~1) : 0) + ((W * D::NIJ + 3) / 4) * 2;
+  for (int x = threadIdx.x; x < N * QP; x += blockDim.x) {
+    sPhiT[x] = P.T.PhiT[x];
+    sWPhiT[x] = P.T.WPhiT[x];
+  }
+  if (SF > 0)
+    for (int x = threadIdx.x; x < q1 * NPR; x += blockDim.x) sLL[x] = P.T.LL[x];
+  if (threadIdx.x < W * D::NIJ) sIJ[threadIdx.x] = D::slot_word(threadIdx.x / D::NIJ, threadIdx.x % D::NIJ);
+  __syncthreads();
+  const int grp = threadIdx.x / G, t = threadIdx.x - grp * G;
+  const int wig = t >> 5, lane = t & 31;
+  const int bar = 1 + grp;
+  const int nmax = N * MS;
+  const int npp = Lay::npp(N);
+  double* base = sm + tabsz + (size_t)grp * Lay::per_group(N, Q, W, SF, q1, NB);
+  double* lam = base;
+  double* lt = lam + NV;
+  double* uh = lt + NV;
+  double* g = uh + NV;
+  double* dd = g + NV;
+  double* nb = dd + NV;  // node buffer: u[a][k] at nb[a Q + k], J[z][k] at nb[(MS + z) Q + k]
+  double* red = nb + Lay::region(N, Q, SF, q1, NB);  // [2 slots][RSX][W]
+  int* ctl = (int*)(red + 2 * Lay::RSX * W);
+
+  const double* __restrict__ omega = P.T.omega;
+  const DualLaunch& A = P.a;
+  long long my_iters = 0, my_failed = 0;
+  int my_worst = 0;
+  double my_rate = 0.0;
+  int slot = 0;
+
+  auto gsync = [&]() { named_sync(bar, G); };
+  // group-wide sums of RS values (alternating scratch slots)
+  auto gsum = [&](auto& v) {
+    constexpr int RS = sizeof(v) / sizeof(double);
+    double* rr = red + slot * Lay::RSX * W;
+    slot ^= 1;
+#pragma unroll
+    for (int a = 0; a < RS; ++a) {
+      v[a] = warp_sum(v[a]);
+      if (W > 1 && lane == 0) rr[a * W + wig] = v[a];
+    }
+    gsync();
+    if (W > 1) {
+#pragma unroll
+      for (int a = 0; a < RS; ++a) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) s += rr[a * W + w];
+        v[a] = s;
+      }
+    }
+  };
+
+  // Hessian unique entries S[ab][pair(i >= j)]
+  auto hessian = [&](int Nl) {
+    double* Tt = nb + Lay::t_off(N, Q, SF);
+    double* Sx = nb + Lay::s_base(N, Q, SF, q1);
+    const int NPl = Nl * (Nl + 1) / 2;
+    if constexpr (SF > 0) {
+      constexpr int NCH = Lay::NCH, CHW = Lay::CHW;
+#pragma unroll 1
+      for (int ch = 0; ch < NCH; ++ch) {
+        const int ab0 = ch * CHW;
+        const int nab = (MM - ab0) < CHW ? (MM - ab0) : CHW;
+        // stage 1: T[k1][pr2][c] = sum_k2 LL[k2][pr2] J_{ab0+c}(k1, k2)
+#pragma unroll 1
+        for (int e = t; e < q1 * nab; e += G) {
+          const int k1 = e / nab, c = e - k1 * nab;
+          double at[NPR];
+#pragma unroll
+          for (int pr = 0; pr < NPR; ++pr) at[pr] = 0.0;
+          const double* jrow = nb + (MS + ab0 + c) * Q + k1 * q1;
+#pragma unroll 2
+          for (int k2 = 0; k2 < q1; ++k2) {
+            const double jv = jrow[k2];
+            const double* ll = sLL + k2 * NPR;
+#pragma unroll
+            for (int pr = 0; pr < NPR; ++pr) at[pr] = fma(ll[pr], jv, at[pr]);
+          }
+#pragma unroll
+          for (int pr = 0; pr < NPR; ++pr) Tt[(k1 * NPR + pr) * CHW + c] = at[pr];
+        }
+        gsync();
+        // stage 2: S[ab0+c][pair] = sum_k1 LL[k1][pr1] T[k1][pr2][c]
+#pragma unroll 1
+        for (int p = t; p < NPl; p += G) {
+          int i = (int)((sqrtf(8.0f * p + 1.0f) - 1.0f) * 0.5f);
+          if ((i + 1) * (i + 2) / 2 <= p) ++i;
+          if (i * (i + 1) / 2 > p) --i;
+          const int j = p - i * (i + 1) / 2;
+          int a1 = P.T.idx[i * 2], a2 = P.T.idx[i * 2 + 1], b1 = P.T.idx[j * 2], b2 = P.T.idx[j * 2 + 1];
+          if (a1 > b1) { const int x = a1; a1 = b1; b1 = x; }
+          if (a2 > b2) { const int x = a2; a2 = b2; b2 = x; }
+          const int pr1 = a1 * SF - a1 * (a1 - 1) / 2 + (b1 - a1);
+          const int pr2 = a2 * SF - a2 * (a2 - 1) / 2 + (b2 - a2);
+          double acc[CHW];
+#pragma unroll
+          for (int c = 0; c < CHW; ++c) acc[c] = 0.0;
+#pragma unroll 2
+          for (int k1 = 0; k1 < q1; ++k1) {
+            const double lv = sLL[k1 * NPR + pr1];
+            const double* Tk = Tt + (k1 * NPR + pr2) * CHW;
+#pragma unroll
+            for (int c = 0; c < CHW; ++c) acc[c] = fma(lv, Tk[c], acc[c]);
+          }
+#pragma unroll
+          for (int c = 0; c < CHW; ++c)
+            if (c < nab) Sx[(ab0 + c) * npp + p] = acc[c];
+        }
+        gsync();  // T chunk is rewritten by the next chunk; S complete after the last
+      }
+    } else {
+      // direct: S[ab][pair] = sum_k (omega_k phi_ki phi_kj) J_ab,k
+#pragma unroll 1
+      for (int p = t; p < NPl; p += G) {
+        int i = (int)((sqrtf(8.0f * p + 1.0f) - 1.0f) * 0.5f);
+        if ((i + 1) * (i + 2) / 2 <= p) ++i;
+        if (i * (i + 1) / 2 > p) --i;
+        const int j = p - i * (i + 1) / 2;
+        const double* wi = sWPhiT + i * QP;
+        const double* pj = sPhiT + j * QP;
+        double acc[MM];
+#pragma unroll
+        for (int z = 0; z < MM; ++z) acc[z] = 0.0;
+#pragma unroll 1
+        for (int k = 0; k < Q; ++k) {
+          const double f = wi[k] * pj[k];
+#pragma unroll
+          for (int z = 0; z < MM; ++z) acc[z] = fma(f, nb[(MS + z) * Q + k], acc[z]);
+        }
+#pragma unroll
+        for (int z = 0; z < MM; ++z) Sx[z * npp + p] = acc[z];
+      }
+      gsync();
+    }
+  };
+
+  for (;;) {
+    if (t == 0) ctl[0] = atomicAdd(&P.sc->work_counter, 1);
+    gsync();
+    const int64_t cell = ctl[0];
+    if (cell >= A.cells) break;
+    MPHASE(7);
+    const int lvl = A.level ? A.level[cell] : 0;
+    const int Nl = (P.ad.n_levels > 0) ? P.ad.Nl[lvl] : N;
+    const int n = Nl * MS;
+    const int NBl = (n + 7) / 8;
+    {
+      const double* gu = A.uhat + cell * nmax;
+      const double* gl = A.lam + cell * nmax;
+      for (int r = t; r < n; r += G) {
+        uh[r] = gu[r];
+        lam[r] = gl[r];
+      }
+    }
+    gsync();
+
+    // Newton iteration with Armijo backtracking on L (reading 3') as one loop with a single
+    // evaluation site: mode 0 = first evaluation at lambda, 1 = line-search trial at lt,
+    // 2 = re-evaluation of the final lambda (node states for the flux)
+    int status = 0, l = 0, h = 0, mode = 0;
+    double crit = INFINITY, L0 = 0.0, scale = 0.0, slope = 0.0, alpha = 1.0;
+    bool nb_is_lam = false;
+    for (;;) {
+      const double* x = (mode == 1) ? lt : lam;
+      // ---- a2: Lambda = Phi x, u = u_s(Lambda), J = grad u_s, s_* (node buffer) --------------------
+      double sv[2] = {0.0, 0.0}, dv[2] = {0.0, 0.0};
+      bool bad = false;
+#pragma unroll 1
+      for (int k = t; k < Q; k += G) {
+        double Lam[MS];
+#pragma unroll
+        for (int a = 0; a < MS; ++a) Lam[a] = 0.0;
+#pragma unroll 4
+        for (int i = 0; i < Nl; ++i) {
+          const double ph = sPhiT[i * QP + k];
+#pragma unroll
+          for (int a = 0; a < MS; ++a) Lam[a] = fma(x[i * MS + a], ph, Lam[a]);
+        }
+        double u[MS], J[MM], ss;
+        if (!Closure<CL, MS>::eval(Lam, u, J, ss, P.cl)) bad = true;
+#pragma unroll
+        for (int a = 0; a < MS; ++a) nb[a * Q + k] = u[a];
+#pragma unroll
+        for (int z = 0; z < MM; ++z) nb[(MS + z) * Q + k] = J[z];
+        const double w = omega[k];
+        sv[0] = fma(w, ss, sv[0]);
+        sv[1] = fma(w, fabs(ss), sv[1]);
+      }
+      if (bad) sv[1] = INFINITY;
+      // x . uhat (and its magnitude) for L(x) = <s_*> - x . uhat
+      for (int r = t; r < n; r += G) {
+        const double v = x[r] * uh[r];
+        dv[0] += v;
+        dv[1] += fabs(v);
+      }
+      double red4[4] = {sv[0], sv[1], dv[0], dv[1]};
+      gsum(red4);
+      if (mode == 2) {
+        nb_is_lam = true;
+        break;
+      }
+      const bool ok = isfinite(red4[0]) && isfinite(red4[1]);
+      const double Lt = red4[0] - red4[2];
+      bool accept;
+      if (mode == 0) {
+        if (!ok) {
+          status = 4;
+          break;
+        }
+        accept = true;
+      } else {
+        accept = ok && (Lt <= L0 + P.nw.armijo_c * alpha * slope + 1e-12 * scale);
+      }
+      bool finish = false;
+      if (accept) {
+        // ---- a3: gradient g = Phi^T (omega o u) - uhat, crit = sum_a ||g_.a|| -----------------------
+        double part[MS];
+#pragma unroll
+        for (int a = 0; a < MS; ++a) part[a] = 0.0;
+#pragma unroll 1
+        for (int r = t; r < n; r += G) {
+          const int i = r / MS, a = r - i * MS;
+          const double* wp = sWPhiT + i * QP;
+          const double* ua = nb + a * Q;
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+          int k = 0;
+#pragma unroll 1
+          for (; k + 4 <= Q; k += 4) {
+            s0 = fma(wp[k], ua[k], s0);
+            s1 = fma(wp[k + 1], ua[k + 1], s1);
+            s2 = fma(wp[k + 2], ua[k + 2], s2);
+            s3 = fma(wp[k + 3], ua[k + 3], s3);
+          }
+          for (; k < Q; ++k) s0 = fma(wp[k], ua[k], s0);
+          const double gr = ((s0 + s1) + (s2 + s3)) - uh[r];
+          g[r] = gr;
+          if (mode == 1) lam[r] = lt[r];
+#pragma unroll
+          for (int b = 0; b < MS; ++b)
+            if (b == a) part[b] = fma(gr, gr, part[b]);
+        }
+        gsum(part);
+        crit = 0.0;
+#pragma unroll
+        for (int a = 0; a < MS; ++a) crit += sqrt(part[a]);
+        if (mode == 1) ++l;
+        nb_is_lam = true;
+        L0 = Lt;
+        scale = red4[1] + red4[3];
+        // ---- a7: stopping tests -------------------------------------------------------------------
+        if (crit < P.nw.tau || (P.nw.mode == 1 && l == 1)) break;
+        if (l == P.nw.max_newton) {
+          status = 1;
+          break;
+        }
+        MPHASE(0);
+        // ---- a4-a5: Hessian, Cholesky, d = -H^{-1} g ----------------------------------------------
+        hessian(Nl);
+        nb_is_lam = false;
+        for (int r = t; r < NBl * 8; r += G) dd[r] = (r < n) ? -g[r] : 0.0;
+        gsync();
+        MPHASE(1);
+        const bool chol_ok = D::chol_solve(nb + Lay::s_base(N, Q, SF, q1), npp, dd, nb, ctl, n, NBl, lane, wig, bar,
+                                           sIJ);
+        MPHASE(2);
+        if (!chol_ok) {
+          status = 2;
+          finish = true;
+        } else {
+          double sl[1] = {0.0};
+          for (int r = t; r < n; r += G) sl[0] = fma(g[r], dd[r], sl[0]);
+          gsum(sl);
+          slope = sl[0];
+          alpha = 1.0;
+          h = 0;
+        }
+      } else {
+        nb_is_lam = false;
+        alpha *= 0.5;
+        if (++h > P.nw.max_halvings) {
+          status = 3;
+          finish = true;
+        }
+      }
+      if (finish) {
+        if (nb_is_lam) break;
+        mode = 2;  // re-evaluate the last accepted iterate
+      } else {
+        for (int r = t; r < n; r += G) lt[r] = lam[r] + alpha * dd[r];
+        mode = 1;
+      }
+      gsync();
+      MPHASE(3);
+    }
+    MPHASE(4);
+    // ---- epilogue --------------------------------------------------------------------------------
+    gsync();
+    if (P.ad.n_levels > 0 && A.level_new) {
+      const int Nprev = lvl > 0 ? P.ad.Nl[lvl - 1] : P.ad.Nprev0;
+      double nd[2] = {0.0, 0.0};
+      for (int i = t; i < Nl; i += G) {
+        const double hv = g[i * MS] + uh[i * MS];
+        nd[1] = fma(hv, hv, nd[1]);
+        if (i >= Nprev) nd[0] = fma(hv, hv, nd[0]);
+      }
+      gsum(nd);
+      const double Sv = nd[1] > 0.0 ? nd[0] / nd[1] : 0.0;
+      int nl = lvl;
+      if (status == 0 || P.nw.mode == 1) {
+        if (Sv < P.ad.delta_dec && lvl > 0)
+          nl = lvl - 1;
+        else if (Sv > P.ad.delta_inc && lvl < P.ad.n_levels - 1)
+          nl = lvl + 1;
+      }
+      if (t == 0) A.level_new[cell] = nl;
+    }
+    {
+      double* gl = A.lam + cell * nmax;
+      for (int r = t; r < nmax; r += G) gl[r] = (r < n) ? lam[r] : 0.0;
+    }
+    if (t == 0) {
+      if (A.iters) A.iters[cell] = l;
+      if (A.status) A.status[cell] = status;
+      if (A.crit) A.crit[cell] = crit;
+      my_iters += l;
+      if (status != 0) {
+        my_failed += 1;
+        my_worst = max(my_worst, status);
+      }
+    }
+    if (status != 4) {
+      for (int k = t; k < Q; k += G) {
+        double u[MS];
+#pragma unroll
+        for (int a = 0; a < MS; ++a) u[a] = nb[a * Q + k];
+        if (A.uq) {
+          double* o = A.uq + (cell * Q + k) * MS;
+#pragma unroll
+          for (int a = 0; a < MS; ++a) o[a] = u[a];
+        }
+        if (A.want_rate) my_rate = fmax(my_rate, node_rate<CL, MS>(u, P.mesh, cell, P.cl.gamma));
+      }
+    }
+    gsync();
+  }
+  MPHASE(5);
+#ifdef IPM_PHASE_TIMERS
+  if (t == 0)
+    for (int i = 0; i < 8; ++i) atomicAdd(&g_phase_cycles[i], ph_acc[i]);
+#endif
+  my_rate = warp_max(my_rate);
+  if (lane == 0) {
+    if (A.want_rate) atomicMax(&P.sc->rate_bits, (unsigned long long)__double_as_longlong(my_rate));
+    if (t == 0) {
+      if (my_iters) atomicAdd(&P.sc->newton_iters, (unsigned long long)my_iters);
+      if (my_failed) atomicAdd(&P.sc->failed, (unsigned long long)my_failed);
+      if (my_worst) atomicMax(&P.sc->worst, my_worst);
+    }
+  }
+}
+#undef MPHASE

@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
+#include <string>
 
 #include "ipm_device.cuh"
 #include "ipm_internal.h"
@@ -379,6 +380,7 @@ __global__ void __launch_bounds__(512) k_dual_warp(DualParams P) {
 }
 
 #include "ipm_dual_group.cuh"
+#include "ipm_dual_mma.cuh"
 #include "ipm_dual_big.cuh"
 
 // ------------------------------------------------------------------------------------------------
@@ -796,8 +798,66 @@ size_t big_scratch_doubles(int N, int Q, int m) {
   return m == 4 ? BigLayout<4>::scratch(N, Q) : 0;
 }
 
+template <int CL, int MS, int NB, int W, int SF>
+static int dual_mma_impl(const KernelCtx& k, const DualLaunch& a) {
+  using Lay = MmaLayout<MS>;
+  constexpr int G = 32 * W;
+  const int npr = SF * (SF + 1) / 2;
+  const size_t tab = ((size_t)2 * k.T.N * k.T.QP + (SF > 0 ? ((k.T.q1d * npr + 1) & ~1) : 0) +
+                      ((W * DualMma<CL, MS, NB, W, SF>::NIJ + 3) / 4) * 2) * 8;
+  const size_t pg = (size_t)Lay::per_group(k.T.N, k.T.Q, W, SF, k.T.q1d, NB) * 8;
+  if (tab + pg > k.smem_optin) return -1;
+  int groups = (int)((k.smem_optin - tab) / pg);
+  groups = std::min(groups, std::min(512 / G, 15));  // named barriers 1..15 (0 = __syncthreads)
+  const size_t smem = tab + groups * pg;
+  auto kern = k_dual_mma<CL, MS, NB, W, SF>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, groups * G, smem);
+  if (per_sm < 1) return -1;
+  const int64_t want = (a.cells + groups - 1) / groups;
+  int grid = (int)std::min<int64_t>(want, (int64_t)k.sm_count * per_sm);
+  if (grid < 1) grid = 1;
+  DualParams P{k.T, k.mesh, k.nw, k.ad, k.cl, a, k.sc};
+  kern<<<grid, groups * G, smem, S(k)>>>(P);
+  return (int)cudaGetLastError();
+}
+
+// DMMA-Cholesky kernel: 8x8 blocks of the padded n x n Hessian, W warps per cell so that the
+// register blocks fit (<= 18 blocks per warp)
+static int dual_mma_dispatch(const KernelCtx& k, const DualLaunch& a, int SF) {
+  const int n = k.T.N * k.m, NB = (n + 7) / 8;
+  const int key = ((k.closure * 10 + k.m) * 100 + NB) * 10 + SF;
+  const char* we = std::getenv("IPM_MMA_W");
+  if (we && we[0] == '4' && key == ((CL_EULER * 10 + 4) * 100 + 8) * 10 + 5)
+    return dual_mma_impl<CL_EULER, 4, 8, 4, 5>(k, a);
+  switch (key) {
+#define IPM_MCASE(CLV, MSV, NBV, WV, SFV) \
+  case ((CLV * 10 + MSV) * 100 + NBV) * 10 + SFV: return dual_mma_impl<CLV, MSV, NBV, WV, SFV>(k, a);
+    IPM_MCASE(CL_BARRIER, 1, 1, 1, 0)
+    IPM_MCASE(CL_QUADRATIC, 1, 1, 1, 0)
+    IPM_MCASE(CL_EULER, 3, 4, 1, 0)
+    IPM_MCASE(CL_EULER, 4, 3, 1, 3)
+    IPM_MCASE(CL_EULER, 4, 5, 1, 4)
+    IPM_MCASE(CL_EULER, 4, 8, 2, 5)
+    IPM_MCASE(CL_EULER, 4, 8, 2, 0)
+    IPM_MCASE(CL_EULER, 4, 11, 4, 6)
+#undef IPM_MCASE
+  }
+  return -1;
+}
+
 int launch_dual(const KernelCtx& k, const DualLaunch& a) {
   if (a.cells == 0) return 0;
+  // the DMMA-Cholesky kernel is opt-in (IPM_DUAL_KERNEL=mma) until it beats the group kernel
+  const char* dk = std::getenv("IPM_DUAL_KERNEL");
+  const bool use_mma = dk && (std::string(dk) == "mma");
+  if (!k.force_warp_kernel && use_mma) {
+    const char* sfe = std::getenv("IPM_SUMFACT");
+    const int SF = (k.T.p == 2 && !(sfe && sfe[0] == '0')) ? (int)std::lround((std::sqrt(8.0 * k.T.npr + 1) - 1) / 2) : 0;
+    const int rc = dual_mma_dispatch(k, a, SF);
+    if (rc != -1) return rc;
+  }
   if (!k.force_warp_kernel) {
     int G, T;
     group_shape(k.T.N, G, T);

@@ -41,8 +41,15 @@ def test_basis_tables_match(torch, name):
     np.testing.assert_allclose(pg, po, rtol=1e-12, atol=1e-12)
 
 
+@pytest.fixture(params=["group", "mma"])
+def dual_kernel(request, monkeypatch):
+    """both dual-solve kernels (IPM_DUAL_KERNEL is read at every launch)"""
+    monkeypatch.setenv("IPM_DUAL_KERNEL", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4"])
-def test_dual_solve_stress_parity(torch, name):
+def test_dual_solve_stress_parity(torch, name, dual_kernel):
     """manufactured lambda* per cell: uhat = h(lambda*), solve from e0 (x) grad s(uhat_0)."""
     cfg = configs.parity_variant(name)
     if name == "cfg4":
@@ -86,7 +93,7 @@ def _run_both(cfg, n_steps=None):
 
 
 @pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3"])
-def test_full_run_parity(torch, name):
+def test_full_run_parity(torch, name, dual_kernel):
     cfg = configs.parity_variant(name)
     g, o, (u_o, l_o, io), (u_g, l_g, ig) = _run_both(cfg)
     assert io["steps"] == ig["steps"]
