@@ -302,11 +302,11 @@ def run_ours(args):
                        else "single", "global_cells": g.cells * world},
             "newton_iters_per_cell_step": iters / (g.cells * args.steps),
             "cell_newton_iters_per_s": iters * world / (ms / 1e3),
-            "roofline": {"bound": "alu", "kernel": "k_dual_warp", "achieved": achieved,
+            "roofline": {"bound": "alu", "kernel": Context.last_dual_kernel(), "achieved": achieved,
                          "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
                          "traffic": traffic, "dual_ms_avg": dual_avg,
                          "share_of_step": dual_avg / (ms / args.steps)},
-            "roofline_flux": {"bound": "hbm", "kernel": "k_flux_warp", "achieved": flux_gbs, "peak": hbm,
+            "roofline_flux": {"bound": "hbm", "kernel": "k_flux_cart" if cfg["mesh"]["kind"] != "tri" else "k_flux_warp", "achieved": flux_gbs, "peak": hbm,
                               "unit": "GB/s", "frac": flux_gbs / hbm, "flux_ms_avg": flux_avg},
             "e2e": e2e,
             "gpu_launches": (4 if world == 1 else 6) * args.steps,

@@ -227,6 +227,11 @@ IPM_API ipm_status ipm_partition_query(const ipm_config *cfg, int64_t *cells, in
 IPM_API ipm_status ipm_last_kernel_ms(ipm_ctx *c, float *dual_ms, float *flux_ms);
 IPM_API ipm_status ipm_enable_timing(ipm_ctx *c, int32_t on);
 
+/* Name of the dual-solve kernel the last dual launch of this process used ("k_dual_mma",
+ * "k_dual_group", "k_dual_warp", "k_dual_big"; "" before the first launch).  Host only, never fails;
+ * the string is static. */
+IPM_API const char *ipm_last_dual_kernel(void);
+
 /* Debug: per-phase clock64 cycle totals of the dual kernel (builds with -DIPM_PHASE_TIMERS;
  * zeros otherwise).  h_out[8]: 0 eval/grad/line search, 1 Hessian, 2 Cholesky, 3 back-substitution,
  * 4 final line search, 7 epilogue + cell fetch.  Synchronous; resets the counters. */

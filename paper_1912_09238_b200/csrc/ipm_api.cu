@@ -300,6 +300,15 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
       PhiT[(size_t)i * QP + k] = c->phi[(size_t)k * N + i];
       WPhiT[(size_t)i * QP + k] = c->omega[k] * c->phi[(size_t)k * N + i];
     }
+  // the same table in DMMA A-fragment order (projection of the flux kernel)
+  const int MT = (N + 7) / 8, KS = (Q + 3) / 4;
+  std::vector<double> WPhiF((size_t)MT * KS * 32, 0.0);
+  for (int mt = 0; mt < MT; ++mt)
+    for (int ks = 0; ks < KS; ++ks)
+      for (int l = 0; l < 32; ++l) {
+        const int i = 8 * mt + l / 4, k = 4 * ks + l % 4;
+        if (i < N && k < Q) WPhiF[((size_t)mt * KS + ks) * 32 + l] = WPhiT[(size_t)i * QP + k];
+      }
 
   // mesh face tables (global), this rank's part and its halo
   ipm::MeshTables G, Lm;
@@ -355,6 +364,7 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   auto& O = c->owned;
   double* d_PhiT = dalloc<double>(PhiT.size(), O);
   double* d_WPhiT = dalloc<double>(WPhiT.size(), O);
+  double* d_WPhiF = dalloc<double>(WPhiF.size(), O);
   double* d_omega = dalloc<double>(Q, O);
   int32_t* d_deg = dalloc<int32_t>(N, O);
   double* d_LL = dalloc<double>(LL.size(), O);
@@ -374,7 +384,7 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   c->d_iters = dalloc<int32_t>(cells, O);
   c->d_status = dalloc<int32_t>(cells, O);
   c->d_sc = dalloc<ipm::StepScalars>(1, O);
-  if (!d_PhiT || !d_WPhiT || !d_omega || !d_deg || !d_LL || !d_idx || !d_nbr || !d_nrm || !d_coef || !d_area || !d_rgeo || !d_ghost ||
+  if (!d_PhiT || !d_WPhiT || !d_WPhiF || !d_omega || !d_deg || !d_LL || !d_idx || !d_nbr || !d_nrm || !d_coef || !d_area || !d_rgeo || !d_ghost ||
       !c->d_uq || !c->d_gid || !c->d_send_local || !c->d_crit || !c->d_level || !c->d_level_new || !c->d_iters || !c->d_status || !c->d_sc) {
     ipm_destroy(c);
     return fail(IPM_ERR_CUDA, "cudaMalloc failed");
@@ -384,6 +394,7 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
     return bytes == 0 ? cudaSuccess : cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice);
   };
   if (up(d_PhiT, PhiT.data(), PhiT.size() * 8) || up(d_WPhiT, WPhiT.data(), WPhiT.size() * 8) ||
+      up(d_WPhiF, WPhiF.data(), WPhiF.size() * 8) ||
       up(d_omega, c->omega.data(), Q * 8) || up(d_deg, deg32.data(), N * 4) ||
       up(d_LL, LL.data(), LL.size() * 8) || up(d_idx, idx32.data(), idx32.size() * 4) ||
       up(d_nbr, nbr.data(), nbr.size() * 4) || up(d_nrm, nrm.data(), nrm.size() * 8) ||
@@ -405,7 +416,7 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
 
   ipm::KernelCtx& k = c->k;
-  k.T = ipm::Tables{d_PhiT, d_WPhiT, d_omega, d_deg, N, Q, QP, p, d_LL, d_idx, C.q1d, npr};
+  k.T = ipm::Tables{d_PhiT, d_WPhiT, d_omega, d_deg, N, Q, QP, p, d_LL, d_idx, C.q1d, npr, d_WPhiF, MT, KS};
   k.mesh.kind = C.mesh_kind;
   k.mesh.F = F;
   k.mesh.cells = cells;
@@ -733,6 +744,8 @@ ipm_status ipm_last_kernel_ms(ipm_ctx* c, float* dual_ms, float* flux_ms) {
   if (flux_ms) CUDA_OK(cudaEventElapsedTime(flux_ms, c->ev[2], c->ev[3]));
   return IPM_OK;
 }
+
+const char* ipm_last_dual_kernel(void) { return ipm::last_dual_kernel(); }
 
 ipm_status ipm_debug_phase_cycles(uint64_t* h_out) {
   if (!h_out) return fail(IPM_ERR_ARG, "null argument");

@@ -18,6 +18,7 @@
 //                updates and factors it first (look-ahead);
 //   * back substitution L^T d = y with the register blocks (Linv_K^T on the diagonal, L_KJ^T below).
 #pragma once
+#include <utility>
 // (included inside namespace ipm by ipm_kernels.cu, after DualParams and node_rate)
 
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
@@ -33,6 +34,16 @@ __device__ __forceinline__ double lds_ord(const double* p) {
 }
 __device__ __forceinline__ double dneg(double x) {
   return __longlong_as_double(__double_as_longlong(x) ^ (long long)0x8000000000000000ULL);
+}
+
+// compile-time loop: f(std::integral_constant<int, i>) for i = 0..N-1 (indices are constants in f)
+template <class F, int... Is>
+__device__ __forceinline__ void static_for_impl(F&& f, std::integer_sequence<int, Is...>) {
+  (f(std::integral_constant<int, Is>{}), ...);
+}
+template <int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  static_for_impl(f, std::make_integer_sequence<int, N>{});
 }
 
 // column-major enumeration of the lower block triangle: r -> (I, J), J = 0.., I = J..NB-1
@@ -108,6 +119,7 @@ struct DualMma {
     bool ok = true;
 #pragma unroll 1
     for (int c = 0; c < 8; ++c) {
+      __syncwarp();  // the warp is converged here: lets the compiler drop divergent-shuffle fallbacks
       const int cq = c >> 1;
       const double mine = (c & 1) ? a1 : a0;
       const double d = __shfl_sync(FULL_MASK, mine, c * 4 + cq);
@@ -119,10 +131,9 @@ struct DualMma {
       const double lrc = arc * rs;
       if (2 * q > c) a0 = fma(-lrc, a0c * rs, a0);
       if (2 * q + 1 > c) a1 = fma(-lrc, a1c * rs, a1);
-      if (r == c) {
-        x0 *= rs;
-        x1 *= rs;
-      }
+      const double xs = (r == c) ? rs : 1.0;
+      x0 *= xs;
+      x1 *= xs;
       const double xc0 = __shfl_sync(FULL_MASK, x0, c * 4 + q);
       const double xc1 = __shfl_sync(FULL_MASK, x1, c * 4 + q);
       if (r > c) {
@@ -188,18 +199,16 @@ struct DualMma {
     return v;
   }
 
+  // WR: the warp role (compile time, so every slot's block (I, J) and every step's work list are
+  // constants: the factorisation is straight-line code without per-slot predicates)
+  template <int WR>
   __device__ static bool chol_solve(const double* S, int npp, double* dd, double* reg, int* ctl, int n, int NBl,
-                                    int lane, int wr, int bar, const unsigned* ijtab) {
+                                    int lane, int bar) {
+    constexpr int wr = WR;
     const int r = lane >> 2, q = lane & 3;
     double* pan = reg;                // [NB][64]
     double* linvf = reg + NB * 64;    // [64]
     double* dg = reg + NB * 64 + 64;  // [NB][64]
-    unsigned ijp[NIJ];
-#pragma unroll
-    for (int w4 = 0; w4 < NIJ; ++w4) ijp[w4] = ijtab[wr * NIJ + w4];
-    auto slotI = [&](int s) -> int { return (ijp[s >> 2] >> (8 * (s & 3) + 4)) & 15; };
-    auto slotJ = [&](int s) -> int { return (ijp[s >> 2] >> (8 * (s & 3))) & 15; };
-    auto slotOk = [&](int s) -> bool { return ((ijp[s >> 2] >> (8 * (s & 3))) & 0xff) != 0xff; };
 #ifdef IPM_PHASE_TIMERS
     long long ct0 = clock64();
 #define CPH(i)                                                                                  \
@@ -226,16 +235,16 @@ struct DualMma {
         abn[e] = ((a <= b) ? sym_idx<4>(a, b) : sym_idx<4>(b, a)) * npp;
       }
       const int hmx = hi > hq ? hi : hq, hmn = hi + hq - hmx;
-#pragma unroll
-      for (int s = 0; s < NBW2; ++s) {
-        if (slotOk(s)) {
-          const int I = slotI(s), J = slotJ(s);
+      static_for<NBW2>([&](auto sc) {
+        constexpr int s = decltype(sc)::value, br = s * W + WR;
+        if constexpr (br < NBO) {
+          constexpr int I = oI(br), J = oJ(br);
           const int o = I * (2 * I + 1) + hi * (2 * I + 1) + 2 * J + hq;
           const bool rin = 8 * I + r < n;
 #pragma unroll
           for (int e = 0; e < 2; ++e) blk[s][e] = (rin && 8 * J + 2 * q + e < n) ? S[abn[e] + o] : 0.0;
         }
-      }
+      });
 #pragma unroll
       for (int u = 0; u < NDW; ++u) {
         const int K = u * W + wr;
@@ -249,14 +258,14 @@ struct DualMma {
         }
       }
     } else {
-#pragma unroll
-      for (int s = 0; s < NBW2; ++s) {
-        if (slotOk(s)) {
-          const int I = slotI(s), J = slotJ(s);
+      static_for<NBW2>([&](auto sc) {
+        constexpr int s = decltype(sc)::value, br = s * W + WR;
+        if constexpr (br < NBO) {
+          constexpr int I = oI(br), J = oJ(br);
 #pragma unroll
           for (int e = 0; e < 2; ++e) blk[s][e] = hval(S, npp, n, 8 * I + r, 8 * J + 2 * q + e);
         }
-      }
+      });
 #pragma unroll
       for (int u = 0; u < NDW; ++u) {
         const int K = u * W + wr;
@@ -275,124 +284,181 @@ struct DualMma {
     }
     named_sync(bar, G);
     CPH(4);
-    bool ok = true;
+    // Fragment orders (mma.m8n8k4.f64; lane l, r = l/4, q = l%4):
+    //   C: (r, 2q + e), e = 0, 1          A: (r, q + 4kk)          B: (q + 4kk, r)
+    // Conversions go through shared memory (store in A order, reload), not shuffles.
+    //   blk[s]  C-fragment of the trailing block A_IJ; after its panel step the B-fragment of L_IJ
+    //   pan[I]  L_IK of the current panel, A order;  linvf: Linv_K, A order
+    //   dg[K]   C-fragment of A_KK; after the factorisation the B-fragment of Linv_K
+    auto afrag_ld = [&](const double* src, double& f0, double& f1) {
+      f0 = src[lane];
+      f1 = src[32 + lane];
+    };
+    // B-fragment of a block stored in A order: element (row, c) sits at (c/4)*32 + row*4 + c%4
+    auto bfrag_ld = [&](const double* src, double& f0, double& f1) {
+      f0 = src[(r >> 2) * 32 + q * 4 + (r & 3)];
+      f1 = src[(r >> 2) * 32 + (q + 4) * 4 + (r & 3)];
+    };
+    // vector as an operand: column 0 of B or row 0 of A (lanes 0-3)
+    auto vec_frag = [&](const double* v, double& f0, double& f1) {
+      f0 = (lane < 4) ? v[lane] : 0.0;
+      f1 = (lane < 4) ? v[4 + lane] : 0.0;
+    };
+    bool live = true;  // false after a failed pivot or past the cell's level (adaptive)
     // K = -1 only factors the first diagonal block (look-ahead of the loop)
-#pragma unroll 1
-    for (int K = -1; K < NBl; ++K) {
-      if (ctl[1]) {
-        ok = false;
-        break;
+    static_for<NB + 1>([&](auto kc) {
+      constexpr int K = decltype(kc)::value - 1;
+      if (!live) return;
+      if (K >= NBl || ctl[1]) {
+        live = false;
+        return;
       }
       // ---- panel: L_IK = A_IK Linv_K^T, b_I -= L_IK y_K ---------------------------------------
-      if (K >= 0) {
-        const double lf0 = linvf[lane], lf1 = linvf[32 + lane];
-        const double y0 = dd[K * 8 + 2 * q], y1 = dd[K * 8 + 2 * q + 1];
-#pragma unroll
-        for (int s = 0; s < NBW2; ++s) {
-          if (!slotOk(s)) continue;
-          const int I = slotI(s), J = slotJ(s);
-          if (J != K || I >= NBl) continue;
+      // batched over the warp's panel blocks so the shared-memory round trips overlap:
+      //   C -> A order via pan[I];  X = A_IK Linv^T;  X -> pan[I] (A order);  B-fragment of X kept
+      if constexpr (K >= 0) {
+        auto each_panel = [&](auto&& fn) {
+          static_for<NBW2>([&](auto sc) {
+            constexpr int s = decltype(sc)::value, br = s * W + WR;
+            if constexpr (br < NBO) {
+              constexpr int I = oI(br), J = oJ(br);
+              if constexpr (J == K) {
+                if (I < NBl) fn(s, pan + I * 64, I);
+              }
+            }
+          });
+        };
+        each_panel([&](int s, double* pI, int) { store_afrag(pI, blk[s][0], blk[s][1], lane); });
+        __syncwarp();
+        double lf0, lf1;
+        afrag_ld(linvf, lf0, lf1);
+        each_panel([&](int s, double* pI, int) {
           double f0, f1;
-          to_afrag(blk[s][0], blk[s][1], lane, f0, f1);
+          afrag_ld(pI, f0, f1);
           double x0 = 0.0, x1 = 0.0;
           dmma884(x0, x1, f0, lf0);
           dmma884(x0, x1, f1, lf1);
           blk[s][0] = x0;
           blk[s][1] = x1;
-          store_afrag(pan + I * 64, x0, x1, lane);
-          double v = fma(x0, y0, x1 * y1);
-          v += __shfl_xor_sync(FULL_MASK, v, 1);
-          v += __shfl_xor_sync(FULL_MASK, v, 2);
-          if (q == 0) dd[I * 8 + r] -= v;
-        }
+        });
+        __syncwarp();
+        each_panel([&](int s, double* pI, int) { store_afrag(pI, blk[s][0], blk[s][1], lane); });
+        __syncwarp();
+        double yf0, yf1;
+        vec_frag(dd + K * 8, yf0, yf1);
+        each_panel([&](int s, double* pI, int I) {
+          double f0, f1;
+          afrag_ld(pI, f0, f1);
+          bfrag_ld(pI, blk[s][0], blk[s][1]);
+          double v0 = 0.0, v1 = 0.0;
+          dmma884(v0, v1, f0, yf0);
+          dmma884(v0, v1, f1, yf1);
+          if (q == 0) dd[I * 8 + r] -= v0;
+        });
         named_sync(bar, G);
       }
       // ---- trailing update; (K+1, K+1) first, then factored at once (look-ahead) ---------------
-      if (K + 1 < NBl && (K + 1) % W == wr) {
-        double2 v = *reinterpret_cast<const double2*>(dg + (K + 1) * 64 + 2 * lane);
-        if (K >= 0) {
-          const double p0 = lds_ord(pan + (K + 1) * 64 + lane), p1 = lds_ord(pan + (K + 1) * 64 + 32 + lane);
-          dmma884(v.x, v.y, dneg(p0), p0);
-          dmma884(v.x, v.y, dneg(p1), p1);
+      if constexpr (K + 1 < NB && (K + 1) % W == WR) {
+        constexpr int K1 = K + 1;
+        if (K1 < NBl) {
+          double2 v = *reinterpret_cast<const double2*>(dg + K1 * 64 + 2 * lane);
+          if constexpr (K >= 0) {
+            double p0, p1;
+            afrag_ld(pan + K1 * 64, p0, p1);
+            dmma884(v.x, v.y, dneg(p0), p0);
+            dmma884(v.x, v.y, dneg(p1), p1);
+          }
+          double a0 = v.x, a1 = v.y;
+          const bool okd = diag_factor(a0, a1, lane);
+          store_afrag(linvf, a0, a1, lane);
+          __syncwarp();
+          // y_K1 = Linv b_K1;  dg[K1] <- B-fragment of Linv (back substitution)
+          double f0, f1, bf0, bf1, g0, g1;
+          afrag_ld(linvf, f0, f1);
+          vec_frag(dd + K1 * 8, bf0, bf1);
+          bfrag_ld(linvf, g0, g1);
+          double y0 = 0.0, y1 = 0.0;
+          dmma884(y0, y1, f0, bf0);
+          dmma884(y0, y1, f1, bf1);
+          *reinterpret_cast<double2*>(dg + K1 * 64 + 2 * lane) = make_double2(g0, g1);
+          __syncwarp();
+          if (q == 0) dd[K1 * 8 + r] = y0;
+          if (lane == 0 && !okd) ctl[1] = 1;
         }
-        // Linv_{K+1} (kept in dg), its operand copy, y_{K+1} = Linv b_{K+1}
-        double a0 = v.x, a1 = v.y;
-        const bool okd = diag_factor(a0, a1, lane);
-        *reinterpret_cast<double2*>(dg + (K + 1) * 64 + 2 * lane) = make_double2(a0, a1);
-        store_afrag(linvf, a0, a1, lane);
-        const double b0 = dd[(K + 1) * 8 + 2 * q], b1 = dd[(K + 1) * 8 + 2 * q + 1];
-        double y = fma(a0, b0, a1 * b1);
-        y += __shfl_xor_sync(FULL_MASK, y, 1);
-        y += __shfl_xor_sync(FULL_MASK, y, 2);
-        __syncwarp();
-        if (q == 0) dd[(K + 1) * 8 + r] = y;
-        if (lane == 0 && !okd) ctl[1] = 1;
       }
-      if (K >= 0) {
-#pragma unroll
-        for (int u = 0; u < NDW; ++u) {
-          const int Jd = u * W + wr;
-          if (Jd <= K + 1 || Jd >= NBl) continue;
-          double2 v = *reinterpret_cast<const double2*>(dg + Jd * 64 + 2 * lane);
-          const double p0 = lds_ord(pan + Jd * 64 + lane), p1 = lds_ord(pan + Jd * 64 + 32 + lane);
-          dmma884(v.x, v.y, dneg(p0), p0);
-          dmma884(v.x, v.y, dneg(p1), p1);
-          *reinterpret_cast<double2*>(dg + Jd * 64 + 2 * lane) = v;
-        }
-#pragma unroll
-        for (int s = 0; s < NBW2; ++s) {
-          if (!slotOk(s)) continue;
-          const int I = slotI(s), J = slotJ(s);
-          if (J <= K || I >= NBl) continue;
-          const double a0 = dneg(lds_ord(pan + I * 64 + lane)), a1 = dneg(lds_ord(pan + I * 64 + 32 + lane));
-          const double b0 = lds_ord(pan + J * 64 + lane), b1 = lds_ord(pan + J * 64 + 32 + lane);
-          dmma884(blk[s][0], blk[s][1], a0, b0);
-          dmma884(blk[s][0], blk[s][1], a1, b1);
-        }
+      if constexpr (K >= 0) {
+        static_for<NDW>([&](auto uc) {
+          constexpr int Jd = decltype(uc)::value * W + WR;
+          if constexpr (Jd > K + 1 && Jd < NB) {
+            if (Jd < NBl) {
+              double2 v = *reinterpret_cast<const double2*>(dg + Jd * 64 + 2 * lane);
+              double p0, p1;
+              afrag_ld(pan + Jd * 64, p0, p1);
+              dmma884(v.x, v.y, dneg(p0), p0);
+              dmma884(v.x, v.y, dneg(p1), p1);
+              *reinterpret_cast<double2*>(dg + Jd * 64 + 2 * lane) = v;
+            }
+          }
+        });
+        static_for<NBW2>([&](auto sc) {
+          constexpr int s = decltype(sc)::value, br = s * W + WR;
+          if constexpr (br < NBO) {
+            constexpr int I = oI(br), J = oJ(br);
+            if constexpr (J > K) {
+              if (I < NBl) {
+                double a0, a1, b0, b1;
+                afrag_ld(pan + I * 64, a0, a1);
+                afrag_ld(pan + J * 64, b0, b1);
+                dmma884(blk[s][0], blk[s][1], dneg(a0), b0);
+                dmma884(blk[s][0], blk[s][1], dneg(a1), b1);
+              }
+            }
+          }
+        });
       }
       named_sync(bar, G);
-    }
+    });
     CPH(5);
-    if (!ok) return false;
-    // ---- back substitution: d_K = Linv_K^T z_K; z_J -= L_KJ^T d_K (J < K) --------------------------
-#pragma unroll 1
-    for (int K = NBl - 1; K >= 0; --K) {
-      if (K % W == wr) {
+    if (ctl[1]) return false;
+    // ---- back substitution: d_K = Linv_K^T z_K; z_J -= L_KJ^T d_K (J < K), as row-vector DMMAs --------
+    static_for<NB>([&](auto kc) {
+      constexpr int K = NB - 1 - decltype(kc)::value;
+      if (K >= NBl) return;
+      if constexpr (K % W == WR) {
         const double2 li = *reinterpret_cast<const double2*>(dg + K * 64 + 2 * lane);
-        const double z = dd[K * 8 + r];
-        double v0 = li.x * z, v1 = li.y * z;
-#pragma unroll
-        for (int o = 4; o < 32; o <<= 1) {
-          v0 += __shfl_xor_sync(FULL_MASK, v0, o);
-          v1 += __shfl_xor_sync(FULL_MASK, v1, o);
-        }
+        double z0, z1;
+        vec_frag(dd + K * 8, z0, z1);
+        double v0 = 0.0, v1 = 0.0;
+        dmma884(v0, v1, z0, li.x);
+        dmma884(v0, v1, z1, li.y);
         __syncwarp();
-        if (r == 0) {
+        if (lane < 4) {
           dd[K * 8 + 2 * q] = v0;
           dd[K * 8 + 2 * q + 1] = v1;
         }
       }
       named_sync(bar, G);
-      if (K == 0) break;
-#pragma unroll
-      for (int s = 0; s < NBW2; ++s) {
-        if (!slotOk(s)) continue;
-        const int I = slotI(s), J = slotJ(s);
-        if (I != K) continue;
-        const double dk = dd[K * 8 + r];
-        double v0 = blk[s][0] * dk, v1 = blk[s][1] * dk;
-#pragma unroll
-        for (int o = 4; o < 32; o <<= 1) {
-          v0 += __shfl_xor_sync(FULL_MASK, v0, o);
-          v1 += __shfl_xor_sync(FULL_MASK, v1, o);
-        }
-        if (r == 0) {
-          dd[J * 8 + 2 * q] -= v0;
-          dd[J * 8 + 2 * q + 1] -= v1;
-        }
+      if constexpr (K > 0) {
+        double d0, d1;
+        vec_frag(dd + K * 8, d0, d1);
+        static_for<NBW2>([&](auto sc) {
+          constexpr int s = decltype(sc)::value, br = s * W + WR;
+          if constexpr (br < NBO) {
+            constexpr int I = oI(br), J = oJ(br);
+            if constexpr (I == K) {
+              double v0 = 0.0, v1 = 0.0;
+              dmma884(v0, v1, d0, blk[s][0]);
+              dmma884(v0, v1, d1, blk[s][1]);
+              if (lane < 4) {
+                dd[J * 8 + 2 * q] -= v0;
+                dd[J * 8 + 2 * q + 1] -= v1;
+              }
+            }
+          }
+        });
+        named_sync(bar, G);
       }
-      named_sync(bar, G);
-    }
+    });
     CPH(6);
     return true;
 #undef CPH
@@ -469,6 +535,7 @@ __global__ void __launch_bounds__(IPM_MMA_THREADS) k_dual_mma(DualParams P) {
     constexpr int RS = sizeof(v) / sizeof(double);
     double* rr = red + slot * Lay::RSX * W;
     slot ^= 1;
+    __syncwarp();
 #pragma unroll
     for (int a = 0; a < RS; ++a) {
       v[a] = warp_sum(v[a]);
@@ -696,8 +763,22 @@ __global__ void __launch_bounds__(IPM_MMA_THREADS) k_dual_mma(DualParams P) {
         for (int r = t; r < NBl * 8; r += G) dd[r] = (r < n) ? -g[r] : 0.0;
         gsync();
         MPHASE(1);
-        const bool chol_ok = D::chol_solve(nb + Lay::s_base(N, Q, SF, q1), npp, dd, nb, ctl, n, NBl, lane, wig, bar,
-                                           sIJ);
+        const double* Sx = nb + Lay::s_base(N, Q, SF, q1);
+        bool chol_ok;
+if constexpr (W == 1) {
+          chol_ok = D::template chol_solve<0>(Sx, npp, dd, nb, ctl, n, NBl, lane, bar);
+        } else if constexpr (W == 2) {
+          chol_ok = (wig == 0) ? D::template chol_solve<0>(Sx, npp, dd, nb, ctl, n, NBl, lane, bar)
+                               : D::template chol_solve<1>(Sx, npp, dd, nb, ctl, n, NBl, lane, bar);
+        } else {
+          static_assert(W == 4, "W in {1, 2, 4}");
+          switch (wig) {
+            case 0: chol_ok = D::template chol_solve<0>(Sx, npp, dd, nb, ctl, n, NBl, lane, bar); break;
+            case 1: chol_ok = D::template chol_solve<1>(Sx, npp, dd, nb, ctl, n, NBl, lane, bar); break;
+            case 2: chol_ok = D::template chol_solve<2>(Sx, npp, dd, nb, ctl, n, NBl, lane, bar); break;
+            default: chol_ok = D::template chol_solve<3>(Sx, npp, dd, nb, ctl, n, NBl, lane, bar); break;
+          }
+        }
         MPHASE(2);
         if (!chol_ok) {
           status = 2;

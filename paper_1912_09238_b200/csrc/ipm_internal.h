@@ -23,6 +23,10 @@ struct Tables {
   const double* LL;
   const int32_t* idx;
   int q1d, npr;
+  // omega Phi^T in mma.m8n8k4 A-fragment order: WPhiF[(mt * KS + ks) * 32 + l] =
+  //   omega_k phi_i(xi_k), i = 8 mt + l/4, k = 4 ks + l%4 (zero outside N x Q); MT = ceil(N/8), KS = ceil(Q/4)
+  const double* WPhiF;
+  int MT, KS;
 };
 
 // Local mesh: owned cells, face tables (F faces per cell)
@@ -110,6 +114,7 @@ int launch_step_begin(const KernelCtx& k, double rate0);
 size_t big_scratch_doubles(int N, int Q, int m);
 int debug_phase_cycles(unsigned long long* out);
 int launch_dual(const KernelCtx& k, const DualLaunch& a);
+const char* last_dual_kernel();
 int launch_dt(const KernelCtx& k, double t_end, double dt_fixed, double cfl);
 int launch_flux(const KernelCtx& k, const FluxLaunch& a);
 int launch_project_ic(const KernelCtx& k, const double* d_region /*[R][Q][m]*/, const double* d_split /*[Q][2]*/,

@@ -515,6 +515,186 @@ __global__ void __launch_bounds__(256) k_flux_warp(FluxParams P) {
 }
 
 // ------------------------------------------------------------------------------------------------
+// flux kernel for 1D / cartesian meshes: CPW = 8/m cells per warp so that the projection
+// Phi^T(omega o r) of all of them is one set of DMMAs (columns = (cell, state) pairs):
+//   flux    lanes over (cell, node): the node's physical flux along each direction is formed once
+//           (Rusanov) and combined with the neighbours' at the two faces of that direction, in the
+//           paper's difference form (g(u_j, u_{j+1}) - g(u_{j-1}, u_j)) / dx;
+//   project C[i][(c,a)] = sum_k (omega phi_i)(xi_k) r_k[(c,a)], A = WPhiF (fragment order, shared
+//           memory), B = r staged per warp;  the update uhat^{n+1} = uhat^n - dt C (CONSERVATIVE) or
+//           Phi^T(omega o (u - dt r)) (c-form).
+// ------------------------------------------------------------------------------------------------
+// Rusanov flux ingredients of one node state along coordinate direction dir (Euler, m = d + 2)
+template <int MS>
+struct RusNode {
+  static constexpr int D = MS - 2;
+  double irho, p, c;
+  __device__ void init(const double* u, double gamma) {
+    irho = 1.0 / u[0];
+    double m2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) m2 = fma(u[1 + k], u[1 + k], m2);
+    p = (gamma - 1.0) * (u[MS - 1] - 0.5 * m2 * irho);
+    c = sqrt(gamma * p * irho);
+  }
+  // F_dir(u) and |v_dir| + c
+  __device__ void flux(const double* u, int dir, double* f, double& s) const {
+    const double vn = u[1 + dir] * irho;
+    f[0] = u[1 + dir];
+#pragma unroll
+    for (int k = 0; k < D; ++k) f[1 + k] = (k == dir) ? fma(u[1 + k], vn, p) : u[1 + k] * vn;
+    f[MS - 1] = (u[MS - 1] + p) * vn;
+    s = fabs(vn) + c;
+  }
+};
+
+template <int FX, int MS, int MK>
+__global__ void __launch_bounds__(256) k_flux_cart(FluxParams P) {
+  constexpr int CPW = 8 / MS;              // cells per warp (DMMA columns = CPW * MS <= 8)
+  constexpr int F = (MK == MK_CART) ? 4 : 2;
+  constexpr int ND = F / 2;                // directions
+  constexpr bool FAST = (FX == FX_RUSANOV && MS >= 3);
+  extern __shared__ __align__(16) double sm[];
+  const int N = P.T.N, Q = P.T.Q, MT = P.T.MT, KS = P.T.KS;
+  double* sA = sm;  // [MT][KS][32]
+  for (int x = threadIdx.x; x < MT * KS * 32; x += blockDim.x) sA[x] = P.T.WPhiF[x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  double* rb = sm + MT * KS * 32 + (size_t)warp * KS * 32;  // [KS*4][8]: rows k >= Q and unused columns stay 0
+  for (int x = lane; x < KS * 32; x += 32) rb[x] = 0.0;
+  __syncthreads();
+  const int nmax = N * MS;
+  const double dt = P.sc->dt;
+  const double gam = P.cl.gamma;
+  const FluxLaunch& A = P.a;
+  const int64_t cells = P.mesh.cells;
+  double my_res = 0.0;
+  const int64_t groups = (cells + CPW - 1) / CPW;
+  for (int64_t grp = (int64_t)blockIdx.x * nw + warp; grp < groups; grp += (int64_t)gridDim.x * nw) {
+    const int64_t cell0 = grp * CPW;
+    // ---- a11: kinetic flux at every node of every face ------------------------------------------
+    for (int it = lane; it < CPW * Q; it += 32) {
+      const int c = it / Q, k = it - c * Q;
+      const int64_t cell = cell0 + c;
+      if (cell >= cells) continue;
+      double uj[MS], r[MS];
+      const double* src = A.uq + (cell * Q + k) * MS;
+#pragma unroll
+      for (int a = 0; a < MS; ++a) {
+        uj[a] = src[a];
+        r[a] = 0.0;
+      }
+      // all neighbour node states first: their loads are independent and overlap
+      double un[F][MS];
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        const int nbc = P.mesh.nbr[cell * F + f];
+        if (nbc >= 0) {
+          const double* s2 = A.uq + ((int64_t)nbc * Q + k) * MS;
+#pragma unroll
+          for (int a = 0; a < MS; ++a) un[f][a] = s2[a];
+        } else {
+          const int tag = -1 - nbc;
+          const int kind = P.mesh.bc_kind[tag];
+          if (kind == 1) {
+            const double* gs = P.mesh.ghost + ((int64_t)tag * Q + k) * MS;
+#pragma unroll
+            for (int a = 0; a < MS; ++a) un[f][a] = gs[a];
+          } else if (kind == 2 && MS > 1) {
+            // slip wall: mirror the normal momentum
+#pragma unroll
+            for (int a = 0; a < MS; ++a) un[f][a] = uj[a];
+            un[f][1 + f / 2] = -uj[1 + f / 2];
+          } else {
+#pragma unroll
+            for (int a = 0; a < MS; ++a) un[f][a] = uj[a];
+          }
+        }
+      }
+      RusNode<MS> nj;
+      if constexpr (FAST) nj.init(uj, gam);
+#pragma unroll
+      for (int d = 0; d < ND; ++d) {
+        double fj[MS], sj = 0.0, gneg[MS];
+        if constexpr (FAST) nj.flux(uj, d, fj, sj);
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+          const int f = 2 * d + side;
+          const double cf = P.mesh.coef[cell * F + f];
+          double gf[MS];
+          if constexpr (FAST) {
+            RusNode<MS> nn;
+            nn.init(un[f], gam);
+            double fn[MS], sn;
+            nn.flux(un[f], d, fn, sn);
+            const double amax = fmax(side == 0 ? sn : sj, side == 0 ? sj : sn);
+            // g(uL, uR) = (F(uL) + F(uR))/2 - a (uR - uL)/2, uL = west/south state
+#pragma unroll
+            for (int a = 0; a < MS; ++a) {
+              const double fl = side == 0 ? fn[a] : fj[a], fr = side == 0 ? fj[a] : fn[a];
+              const double ul = side == 0 ? un[f][a] : uj[a], ur = side == 0 ? uj[a] : un[f][a];
+              gf[a] = 0.5 * (fl + fr) - 0.5 * amax * (ur - ul);
+            }
+          } else {
+            double nv[2] = {d == 0 ? 1.0 : 0.0, d == 1 ? 1.0 : 0.0};
+            if (side == 0)
+              NumFlux<FX, MS>::g(un[f], uj, nv, gam, 1.0 / (cf * dt), gf);
+            else
+              NumFlux<FX, MS>::g(uj, un[f], nv, gam, 1.0 / (cf * dt), gf);
+          }
+          if (side == 0) {
+#pragma unroll
+            for (int a = 0; a < MS; ++a) gneg[a] = gf[a];
+          } else {
+#pragma unroll
+            for (int a = 0; a < MS; ++a) r[a] += (gf[a] - gneg[a]) * cf;
+          }
+        }
+      }
+      double* o = rb + k * 8 + c * MS;
+      if (A.update_form == 1) {
+#pragma unroll
+        for (int a = 0; a < MS; ++a) o[a] = uj[a] - dt * r[a];
+      } else {
+#pragma unroll
+        for (int a = 0; a < MS; ++a) o[a] = r[a];
+      }
+    }
+    __syncwarp();
+    // ---- projection on the fp64 tensor path and the update ---------------------------------------
+    const int rr = lane >> 2, q = lane & 3;
+    for (int mt = 0; mt < MT; ++mt) {
+      double c0 = 0.0, c1 = 0.0;
+      const double* a = sA + (size_t)mt * KS * 32 + lane;
+      const double* b = rb + (lane & 3) * 8 + (lane >> 2);
+#pragma unroll 5
+      for (int ks = 0; ks < KS; ++ks) {
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c0), "+d"(c1)
+                     : "d"(a[ks * 32]), "d"(b[ks * 32]));
+      }
+      const int i = 8 * mt + rr;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = 2 * q + e, c = col / MS, av = col - c * MS;
+        const int64_t cell = cell0 + c;
+        if (col >= CPW * MS || i >= N || cell >= cells) continue;
+        const int Nnew = (P.ad.n_levels > 0 && A.level_new) ? P.ad.Nl[A.level_new[cell]] : N;
+        const int64_t idx = cell * nmax + i * MS + av;
+        const double old = A.uhat_old[idx];
+        double out = 0.0;
+        if (i < Nnew) out = (A.update_form == 1) ? (e == 0 ? c0 : c1) : old - dt * (e == 0 ? c0 : c1);
+        A.uhat_new[idx] = out;
+        if (i == 0 && av == 0) my_res += P.mesh.area[cell] * fabs(out - old);
+        if (A.lam && i >= Nnew) A.lam[idx] = 0.0;
+      }
+    }
+    __syncwarp();
+  }
+  my_res = warp_sum(my_res);
+  if (lane == 0 && my_res != 0.0) atomicAdd(&P.sc->residual, my_res);
+}
+
+// ------------------------------------------------------------------------------------------------
 // small kernels
 // ------------------------------------------------------------------------------------------------
 __global__ void k_step_begin(StepScalars* sc, double rate0) {
@@ -847,16 +1027,23 @@ static int dual_mma_dispatch(const KernelCtx& k, const DualLaunch& a, int SF) {
   return -1;
 }
 
+static const char* g_last_dual = "";
+const char* last_dual_kernel() { return g_last_dual; }
+
 int launch_dual(const KernelCtx& k, const DualLaunch& a) {
   if (a.cells == 0) return 0;
-  // the DMMA-Cholesky kernel is opt-in (IPM_DUAL_KERNEL=mma) until it beats the group kernel
+  // default: the DMMA-Cholesky kernel where it is instantiated; IPM_DUAL_KERNEL=group selects the
+  // 4x4-register-block kernel (comparison, tests)
   const char* dk = std::getenv("IPM_DUAL_KERNEL");
-  const bool use_mma = dk && (std::string(dk) == "mma");
+  const bool use_mma = !(dk && (std::string(dk) == "group"));
   if (!k.force_warp_kernel && use_mma) {
     const char* sfe = std::getenv("IPM_SUMFACT");
     const int SF = (k.T.p == 2 && !(sfe && sfe[0] == '0')) ? (int)std::lround((std::sqrt(8.0 * k.T.npr + 1) - 1) / 2) : 0;
     const int rc = dual_mma_dispatch(k, a, SF);
-    if (rc != -1) return rc;
+    if (rc != -1) {
+      g_last_dual = "k_dual_mma";
+      return rc;
+    }
   }
   if (!k.force_warp_kernel) {
     int G, T;
@@ -885,7 +1072,10 @@ int launch_dual(const KernelCtx& k, const DualLaunch& a) {
       IPM_GCASE(CL_EULER, 4, 64, 4, 2)
 #undef IPM_GCASE
     }
-    if (rc != -1) return rc;
+    if (rc != -1) {
+      g_last_dual = "k_dual_group";
+      return rc;
+    }
     // cells too large for the on-chip group kernel (config 5): CTA per cell, L2-resident scratch
     if (k.big_scratch && k.closure == CL_EULER && k.m == 4) {
       constexpr int NT = 512;
@@ -895,9 +1085,11 @@ int launch_dual(const KernelCtx& k, const DualLaunch& a) {
       const int grid = (int)std::min<int64_t>(a.cells, (int64_t)k.big_ctas);
       DualParams P{k.T, k.mesh, k.nw, k.ad, k.cl, a, k.sc};
       kern<<<grid, NT, smem, S(k)>>>(P, k.big_scratch);
+      g_last_dual = "k_dual_big";
       return (int)cudaGetLastError();
     }
   }
+  g_last_dual = "k_dual_warp";
   switch (k.closure * 10 + k.m) {
     case CL_QUADRATIC * 10 + 1: return dual_impl<CL_QUADRATIC, 1>(k, a);
     case CL_QUADRATIC * 10 + 3: return dual_impl<CL_QUADRATIC, 3>(k, a);
@@ -930,9 +1122,42 @@ static int flux_impl(const KernelCtx& k, const FluxLaunch& a) {
   return (int)cudaGetLastError();
 }
 
+template <int FX, int MS, int MK>
+static int flux_cart_impl(const KernelCtx& k, const FluxLaunch& a) {
+  constexpr int CPW = 8 / MS;
+  const size_t tab = (size_t)k.T.MT * k.T.KS * 32 * 8, pw = (size_t)k.T.KS * 32 * 8;
+  if (tab + pw > k.smem_optin) return -1;
+  const int warps = (int)std::min<size_t>(8, (k.smem_optin - tab) / pw);
+  const size_t smem = tab + warps * pw;
+  auto kern = k_flux_cart<FX, MS, MK>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t groups = (k.mesh.cells + CPW - 1) / CPW;
+  const int64_t want = (groups + warps - 1) / warps;
+  int grid = (int)std::min<int64_t>(want, (int64_t)k.sm_count * per_sm);
+  if (grid < 1) grid = 1;
+  FluxParams P{k.T, k.mesh, k.cl, k.ad, a, k.sc, 1};
+  kern<<<grid, warps * 32, smem, S(k)>>>(P);
+  return (int)cudaGetLastError();
+}
+
 int launch_flux(const KernelCtx& k, const FluxLaunch& a) {
   if (k.mesh.cells == 0) return 0;
   const int key = (k.flux * 10 + k.m) * 10 + k.mesh.kind;
+  const char* fk = std::getenv("IPM_FLUX_KERNEL");
+  if (!(fk && std::string(fk) == "warp")) {
+    int rc = -1;
+    switch (key) {
+      case (FX_LF_GLOBAL * 10 + 1) * 10 + MK_1D: rc = flux_cart_impl<FX_LF_GLOBAL, 1, MK_1D>(k, a); break;
+      case (FX_HLL * 10 + 3) * 10 + MK_1D: rc = flux_cart_impl<FX_HLL, 3, MK_1D>(k, a); break;
+      case (FX_RUSANOV * 10 + 3) * 10 + MK_1D: rc = flux_cart_impl<FX_RUSANOV, 3, MK_1D>(k, a); break;
+      case (FX_RUSANOV * 10 + 4) * 10 + MK_CART: rc = flux_cart_impl<FX_RUSANOV, 4, MK_CART>(k, a); break;
+      case (FX_HLL * 10 + 4) * 10 + MK_CART: rc = flux_cart_impl<FX_HLL, 4, MK_CART>(k, a); break;
+    }
+    if (rc != -1) return rc;
+  }
   switch (key) {
     case (FX_LF_GLOBAL * 10 + 1) * 10 + MK_1D: return flux_impl<FX_LF_GLOBAL, 1, MK_1D>(k, a);
     case (FX_HLL * 10 + 3) * 10 + MK_1D: return flux_impl<FX_HLL, 3, MK_1D>(k, a);

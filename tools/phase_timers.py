@@ -19,7 +19,7 @@ g.enable_timing(True)
 info = g.ipm_step(u, l0)
 d, f = g.last_kernel_ms()
 c = g.debug_phase_cycles().astype(float)
-names = (["eval/grad/linesearch", "hessian", "cholesky", "backsub", "final linesearch", "end", "-", "epilogue+fetch"] if os.environ.get("IPM_DUAL_KERNEL") != "mma" else ["top (eval/grad)", "hessian", "chol+solve", "linesearch", "[gather+diag0]", "[factor loop]", "[backsub]", "epilogue+fetch"])
+names = (["eval/grad/linesearch", "hessian", "cholesky", "backsub", "final linesearch", "end", "-", "epilogue+fetch"] if os.environ.get("IPM_DUAL_KERNEL") == "group" else ["top (eval/grad)", "hessian", "chol+solve", "linesearch", "[gather+diag0]", "[factor loop]", "[backsub]", "epilogue+fetch"])
 tot = c.sum()
 print(json.dumps({"cfg": name, "cells": g.cells, "iters": int(info.newton_iters), "dual_ms": d,
                   "cycles_per_cell_iter": tot / max(1, info.newton_iters),
