@@ -112,14 +112,35 @@ struct DualMma {
   static constexpr int G = 32 * W;
   static constexpr int NBT = NB * (NB + 1) / 2;
   
+  // 1/sqrt(x): hardware approximation + two Newton steps (rounding-level accuracy for the positive
+  // normal pivots of an SPD matrix; shorter latency than the library rsqrt, which also handles
+  // special operands, on the Cholesky's critical path)
+  __device__ static double rsqrt_nr(double x) {
+#ifdef IPM_DIAG_LIBRSQRT
+    return rsqrt(x);
+#else
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double h = 0.5 * x;
+    double e = fma(-h * y, y, 0.5);
+    y = fma(y, e, y);
+    e = fma(-h * y, y, 0.5);
+    return fma(y, e, y);
+#endif
+  }
+
   // ---- 8x8 diagonal block: in C-fragment layout A (lower part used); out: Linv = L^{-1} -------
   __device__ static bool diag_factor(double& a0, double& a1, int lane) {
     const int r = lane >> 2, q = lane & 3;
     double x0 = (r == 2 * q) ? 1.0 : 0.0, x1 = (r == 2 * q + 1) ? 1.0 : 0.0;
     bool ok = true;
+    __syncwarp();  // the warp is converged here: lets the compiler drop divergent-shuffle fallbacks
+#ifdef IPM_DIAG_UNROLL1
 #pragma unroll 1
+#else
+#pragma unroll
+#endif
     for (int c = 0; c < 8; ++c) {
-      __syncwarp();  // the warp is converged here: lets the compiler drop divergent-shuffle fallbacks
       const int cq = c >> 1;
       const double mine = (c & 1) ? a1 : a0;
       const double d = __shfl_sync(FULL_MASK, mine, c * 4 + cq);
@@ -127,7 +148,7 @@ struct DualMma {
       const double a0c = __shfl_sync(FULL_MASK, mine, (2 * q) * 4 + cq);
       const double a1c = __shfl_sync(FULL_MASK, mine, (2 * q + 1) * 4 + cq);
       if (!(d > 0.0) || !isfinite(d)) ok = false;
-      const double rs = rsqrt(d);
+      const double rs = rsqrt_nr(d);
       const double lrc = arc * rs;
       if (2 * q > c) a0 = fma(-lrc, a0c * rs, a0);
       if (2 * q + 1 > c) a1 = fma(-lrc, a1c * rs, a1);
