@@ -135,10 +135,10 @@ struct DualMma {
     double x0 = (r == 2 * q) ? 1.0 : 0.0, x1 = (r == 2 * q + 1) ? 1.0 : 0.0;
     bool ok = true;
     __syncwarp();  // the warp is converged here: lets the compiler drop divergent-shuffle fallbacks
-#ifdef IPM_DIAG_UNROLL1
-#pragma unroll 1
-#else
+#ifdef IPM_DIAG_UNROLL
 #pragma unroll
+#else
+#pragma unroll 1  // smaller code beats the extra ILP (instruction-cache bound kernel)
 #endif
     for (int c = 0; c < 8; ++c) {
       const int cq = c >> 1;
@@ -206,20 +206,8 @@ struct DualMma {
   static constexpr int NBO = NB * (NB - 1) / 2;               // strictly-lower blocks
   static constexpr int NBW2 = NBO > 0 ? (NBO + W - 1) / W : 1;  // per warp (upper bound)
   static constexpr int NDW = (NB + W - 1) / W;                // diagonal blocks per warp
-  static constexpr int NIJ = (NBW2 + 3) / 4;                  // packed slot words
   __host__ __device__ static constexpr int oJ(int r) { return cmJ(r, NB - 1); }
   __host__ __device__ static constexpr int oI(int r) { return cmI(r, NB - 1) + 1; }
-  // slot table for warp wr: byte s = I << 4 | J, 0xff = empty
-  __host__ __device__ static unsigned slot_word(int wr, int w4) {
-    unsigned v = 0;
-    for (int k = 0; k < 4; ++k) {
-      const int s = 4 * w4 + k, br = s * W + wr;
-      const unsigned b = (s < NBW2 && br < NBO) ? (unsigned)((oI(br) << 4) | oJ(br)) : 0xffu;
-      v |= b << (8 * k);
-    }
-    return v;
-  }
-
   // WR: the warp role (compile time, so every slot's block (I, J) and every step's work list are
   // constants: the factorisation is straight-line code without per-slot predicates)
   template <int WR>
@@ -518,15 +506,16 @@ __global__ void __launch_bounds__(IPM_MMA_THREADS) k_dual_mma(DualParams P) {
   double* sWPhiT = sm + N * QP;
   double* sLL = sm + 2 * N * QP;  // [q1d][NPR] (SF > 0)
   const int q1 = P.T.q1d;
-  unsigned* sIJ = (unsigned*)(sm + 2 * N * QP + ((SF > 0) ? ((q1 * NPR + 1) & ~1) : 0));  // [W][NIJ]
-  const int tabsz = 2 * N * QP + ((SF > 0) ? ((q1 * NPR + 1) & ~1) : 0) + ((W * D::NIJ + 3) / 4) * 2;
+  const int KS = P.T.KS, MTT = P.T.MT;
+  double* sWF = sm + 2 * N * QP + ((SF > 0) ? ((q1 * NPR + 1) & ~1) : 0);  // [MT][KS][32] omega Phi^T fragments
+  const int tabsz = 2 * N * QP + ((SF > 0) ? ((q1 * NPR + 1) & ~1) : 0) + MTT * KS * 32;
   for (int x = threadIdx.x; x < N * QP; x += blockDim.x) {
     sPhiT[x] = P.T.PhiT[x];
     sWPhiT[x] = P.T.WPhiT[x];
   }
   if (SF > 0)
     for (int x = threadIdx.x; x < q1 * NPR; x += blockDim.x) sLL[x] = P.T.LL[x];
-  if (threadIdx.x < W * D::NIJ) sIJ[threadIdx.x] = D::slot_word(threadIdx.x / D::NIJ, threadIdx.x % D::NIJ);
+  for (int x = threadIdx.x; x < MTT * KS * 32; x += blockDim.x) sWF[x] = P.T.WPhiF[x];
   __syncthreads();
   const int grp = threadIdx.x / G, t = threadIdx.x - grp * G;
   const int wig = t >> 5, lane = t & 31;
@@ -738,30 +727,40 @@ __global__ void __launch_bounds__(IPM_MMA_THREADS) k_dual_mma(DualParams P) {
       bool finish = false;
       if (accept) {
         // ---- a3: gradient g = Phi^T (omega o u) - uhat, crit = sum_a ||g_.a|| -----------------------
+        // on the fp64 tensor path: C[i][a] = sum_k (omega phi_i)(xi_k) u_a(xi_k), A = omega Phi^T in
+        // fragment order (shared memory), B = the node buffer's u rows; warps split the row tiles
         double part[MS];
 #pragma unroll
         for (int a = 0; a < MS; ++a) part[a] = 0.0;
+        {
+          const int MTl = (Nl + 7) >> 3, bn = lane >> 2, bk = lane & 3;
+          const bool bval = bn < MS;
+          const double* bsrc = nb + (bval ? bn : 0) * Q + bk;
 #pragma unroll 1
-        for (int r = t; r < n; r += G) {
-          const int i = r / MS, a = r - i * MS;
-          const double* wp = sWPhiT + i * QP;
-          const double* ua = nb + a * Q;
-          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-          int k = 0;
-#pragma unroll 1
-          for (; k + 4 <= Q; k += 4) {
-            s0 = fma(wp[k], ua[k], s0);
-            s1 = fma(wp[k + 1], ua[k + 1], s1);
-            s2 = fma(wp[k + 2], ua[k + 2], s2);
-            s3 = fma(wp[k + 3], ua[k + 3], s3);
-          }
-          for (; k < Q; ++k) s0 = fma(wp[k], ua[k], s0);
-          const double gr = ((s0 + s1) + (s2 + s3)) - uh[r];
-          g[r] = gr;
-          if (mode == 1) lam[r] = lt[r];
+          for (int mt = wig; mt < MTl; mt += W) {
+            double c0 = 0.0, c1 = 0.0;
+            const double* asrc = sWF + mt * KS * 32 + lane;
+#pragma unroll 5
+            for (int ks = 0; ks < KS; ++ks) {
+              const double bv = (bval && 4 * ks + bk < Q) ? bsrc[4 * ks] : 0.0;
+              dmma884(c0, c1, asrc[ks * 32], bv);
+            }
+            const int i = 8 * mt + (lane >> 2);
 #pragma unroll
-          for (int b = 0; b < MS; ++b)
-            if (b == a) part[b] = fma(gr, gr, part[b]);
+            for (int e = 0; e < 2; ++e) {
+              const int a = 2 * (lane & 3) + e;
+              if (a < MS && i < Nl) {
+                const int rr = i * MS + a;
+                const double gr = (e == 0 ? c0 : c1) - uh[rr];
+                g[rr] = gr;
+#pragma unroll
+                for (int b = 0; b < MS; ++b)
+                  if (b == a) part[b] = fma(gr, gr, part[b]);
+              }
+            }
+          }
+          if (mode == 1)
+            for (int r = t; r < n; r += G) lam[r] = lt[r];
         }
         gsum(part);
         crit = 0.0;
