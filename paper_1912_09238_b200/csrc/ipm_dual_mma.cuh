@@ -130,7 +130,8 @@ struct DualMma {
   }
 
   // ---- 8x8 diagonal block: in C-fragment layout A (lower part used); out: Linv = L^{-1} -------
-  __device__ static bool diag_factor(double& a0, double& a1, int lane) {
+  // ncol: columns to factor (the rest of the block is identity padding beyond n)
+  __device__ static bool diag_factor(double& a0, double& a1, int lane, int ncol = 8) {
     const int r = lane >> 2, q = lane & 3;
     double x0 = (r == 2 * q) ? 1.0 : 0.0, x1 = (r == 2 * q + 1) ? 1.0 : 0.0;
     bool ok = true;
@@ -140,7 +141,7 @@ struct DualMma {
 #else
 #pragma unroll 1  // smaller code beats the extra ILP (instruction-cache bound kernel)
 #endif
-    for (int c = 0; c < 8; ++c) {
+    for (int c = 0; c < ncol; ++c) {
       const int cq = c >> 1;
       const double mine = (c & 1) ? a1 : a0;
       const double d = __shfl_sync(FULL_MASK, mine, c * 4 + cq);
@@ -378,7 +379,7 @@ struct DualMma {
             dmma884(v.x, v.y, dneg(p1), p1);
           }
           double a0 = v.x, a1 = v.y;
-          const bool okd = diag_factor(a0, a1, lane);
+          const bool okd = diag_factor(a0, a1, lane, min(8, n - 8 * K1));
           store_afrag(linvf, a0, a1, lane);
           __syncwarp();
           // y_K1 = Linv b_K1;  dg[K1] <- B-fragment of Linv (back substitution)
