@@ -446,7 +446,7 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   // large cells (the on-chip group kernel needs <= 256 threads x 2 blocks): L2-resident scratch
   if (N * (N + 1) / 2 > 512 && m == 4) {
     k.big_ctas = sms;
-    const size_t nd = ipm::big_scratch_doubles(N, Q, m) * (size_t)sms;
+    const size_t nd = ipm::big_scratch_doubles(N, Q, m, C.q1d, npr, p) * (size_t)sms;
     k.big_scratch = dalloc<double>(nd, c->owned);
     if (!k.big_scratch) {
       ipm_destroy(c);

@@ -14,9 +14,18 @@ struct BigLayout {
   static constexpr int MM = MS * (MS + 1) / 2;
   static constexpr int NS = MS + MM;
   static constexpr int TB = MS * MS;
-  // per-CTA global scratch (doubles)
-  static __host__ __device__ size_t scratch(int N, int Q) {
-    return (size_t)Q * NS + (size_t)(N * (N + 1) / 2) * TB + (size_t)N * TB + 64;
+  // per-CTA global scratch (doubles): node data, Hessian blocks (also the first sum-factorisation
+  // stage T1, which fits inside them), diagonal inverses, second stage T2 (p = 3)
+  static __host__ __device__ size_t hb_size(int N, int q1, int npr, int p) {
+    const size_t hb = (size_t)(N * (N + 1) / 2) * TB;
+    const size_t t1 = (p == 3) ? (size_t)q1 * q1 * npr * MM : 0;
+    return hb > t1 ? hb : t1;
+  }
+  static __host__ __device__ size_t t2_size(int q1, int npr, int p) {
+    return (p == 3) ? (size_t)q1 * npr * npr * MM : 0;
+  }
+  static __host__ __device__ size_t scratch(int N, int Q, int q1, int npr, int p) {
+    return (size_t)Q * NS + hb_size(N, q1, npr, p) + (size_t)N * TB + t2_size(q1, npr, p) + 64;
   }
 };
 
@@ -39,10 +48,16 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
   double* g = uh + nmax;
   double* dd = g + nmax;
   double* red = dd + nmax;  // [2][4][NW]
-  int* ctl = (int*)(red + 8 * NW);
-  double* nb = scratch + (size_t)blockIdx.x * Lay::scratch(N, Q);
+  double* sLL = red + 8 * NW;  // [q1][npr] 1D pair table (sum factorisation)
+  int* ctl = (int*)(sLL + ((P.T.q1d * P.T.npr + 1) & ~1));
+  for (int x = threadIdx.x; x < P.T.q1d * P.T.npr; x += NT) sLL[x] = P.T.LL[x];
+  __syncthreads();
+  const int q1 = P.T.q1d, npr = P.T.npr, pdim = P.T.p;
+  double* nb = scratch + (size_t)blockIdx.x * Lay::scratch(N, Q, q1, npr, pdim);
   double* Hb = nb + (size_t)Q * NS;                 // blocks, row-major lower enumeration
-  double* Linv = Hb + (size_t)(N * (N + 1) / 2) * TB;
+  double* Linv = Hb + Lay::hb_size(N, q1, npr, pdim);
+  double* T2 = Linv + (size_t)N * TB;               // [k1][pr2][pr3][ab] (p = 3)
+  double* T1 = Hb;                                  // [k1 k2][pr3][ab]   (p = 3), dead before Hb is written
   const DualLaunch& A = P.a;
   long long my_iters = 0, my_failed = 0;
   int my_worst = 0;
@@ -168,6 +183,75 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
           break;
         }
         // Hessian blocks H_IJ = sum_k omega_k phi_kI phi_kJ J_k
+        if (pdim == 3 && npr <= 32) {
+          // sum factorisation over the tensor rule, k = (k1 q1 + k2) q1 + k3, LL[k][(a,b)] =
+          // (w_k/2) L_a L_b (x_k):  T1 = sum_k3 LL J,  T2 = sum_k2 LL T1,  H = sum_k1 LL T2
+          const int SF = (int)((sqrtf(8.0f * npr + 1.0f) - 1.0f) * 0.5f + 0.5f);
+          for (int e = t; e < q1 * q1 * MM; e += NT) {
+            const int k12 = e / MM, ab = e - k12 * MM;
+            double at[32];
+#pragma unroll
+            for (int x = 0; x < 32; ++x) at[x] = 0.0;
+            const double* jr = nb + (size_t)k12 * q1 * NS + MS + ab;
+            for (int k3 = 0; k3 < q1; ++k3) {
+              const double jv = jr[(size_t)k3 * NS];
+              const double* ll = sLL + k3 * npr;
+#pragma unroll
+              for (int x = 0; x < 32; ++x)
+                if (x < npr) at[x] = fma(ll[x], jv, at[x]);
+            }
+#pragma unroll
+            for (int x = 0; x < 32; ++x)
+              if (x < npr) T1[((size_t)k12 * npr + x) * MM + ab] = at[x];
+          }
+          __syncthreads();
+          for (int e = t; e < q1 * npr * MM; e += NT) {
+            const int k1 = e / (npr * MM), rem = e - k1 * npr * MM, pr3 = rem / MM, ab = rem - pr3 * MM;
+            double at[32];
+#pragma unroll
+            for (int x = 0; x < 32; ++x) at[x] = 0.0;
+            for (int k2 = 0; k2 < q1; ++k2) {
+              const double tv = T1[(((size_t)k1 * q1 + k2) * npr + pr3) * MM + ab];
+              const double* ll = sLL + k2 * npr;
+#pragma unroll
+              for (int x = 0; x < 32; ++x)
+                if (x < npr) at[x] = fma(ll[x], tv, at[x]);
+            }
+#pragma unroll
+            for (int x = 0; x < 32; ++x)
+              if (x < npr) T2[(((size_t)k1 * npr + x) * npr + pr3) * MM + ab] = at[x];
+          }
+          __syncthreads();
+          for (int p = t; p < NPl; p += NT) {
+            int I, J;
+            blk_ij(p, I, J);
+            int pr[3];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              int a = P.T.idx[I * 3 + d], b = P.T.idx[J * 3 + d];
+              if (a > b) {
+                const int x = a;
+                a = b;
+                b = x;
+              }
+              pr[d] = a * SF - a * (a - 1) / 2 + (b - a);
+            }
+            double acc[MM];
+#pragma unroll
+            for (int z = 0; z < MM; ++z) acc[z] = 0.0;
+            for (int k1 = 0; k1 < q1; ++k1) {
+              const double lv = sLL[k1 * npr + pr[0]];
+              const double* tv = T2 + (((size_t)k1 * npr + pr[1]) * npr + pr[2]) * MM;
+#pragma unroll
+              for (int z = 0; z < MM; ++z) acc[z] = fma(lv, tv[z], acc[z]);
+            }
+            double* o = Hb + (size_t)p * TB;
+#pragma unroll
+            for (int a = 0; a < MS; ++a)
+#pragma unroll
+              for (int b = 0; b < MS; ++b) o[BIDX(a, b)] = acc[a <= b ? sym_idx<MS>(a, b) : sym_idx<MS>(b, a)];
+          }
+        } else
         for (int p = t; p < NPl; p += NT) {
           int I, J;
           blk_ij(p, I, J);

@@ -111,7 +111,7 @@ struct KernelCtx {
 
 // launchers (ipm_kernels.cu); return 0 on success, else a cudaError_t / -1 unsupported
 int launch_step_begin(const KernelCtx& k, double rate0);
-size_t big_scratch_doubles(int N, int Q, int m);
+size_t big_scratch_doubles(int N, int Q, int m, int q1d, int npr, int p);
 int debug_phase_cycles(unsigned long long* out);
 int launch_dual(const KernelCtx& k, const DualLaunch& a);
 const char* last_dual_kernel();

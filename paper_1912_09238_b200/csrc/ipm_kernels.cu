@@ -974,8 +974,8 @@ static void group_shape(int N, int& G, int& T) {
       }
 }
 
-size_t big_scratch_doubles(int N, int Q, int m) {
-  return m == 4 ? BigLayout<4>::scratch(N, Q) : 0;
+size_t big_scratch_doubles(int N, int Q, int m, int q1d, int npr, int p) {
+  return m == 4 ? BigLayout<4>::scratch(N, Q, q1d, npr, p) : 0;
 }
 
 template <int CL, int MS, int NB, int W, int SF>
@@ -1079,7 +1079,7 @@ int launch_dual(const KernelCtx& k, const DualLaunch& a) {
     // cells too large for the on-chip group kernel (config 5): CTA per cell, L2-resident scratch
     if (k.big_scratch && k.closure == CL_EULER && k.m == 4) {
       constexpr int NT = 512;
-      const size_t smem = ((size_t)5 * k.T.N * 4 + 8 * (NT / 32) + 8) * 8;
+      const size_t smem = ((size_t)5 * k.T.N * 4 + 8 * (NT / 32) + ((k.T.q1d * k.T.npr + 1) & ~1) + 8) * 8;
       auto kern = k_dual_big<CL_EULER, 4, NT>;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       const int grid = (int)std::min<int64_t>(a.cells, (int64_t)k.big_ctas);
