@@ -29,7 +29,7 @@ struct BigLayout {
   }
 };
 
-template <int CL, int MS, int NT>
+template <int CL, int MS, int NT, bool HBS>
 __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restrict__ scratch) {
   using Lay = BigLayout<MS>;
   constexpr int NW = NT / 32;
@@ -54,10 +54,15 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
   __syncthreads();
   const int q1 = P.T.q1d, npr = P.T.npr, pdim = P.T.p;
   double* nb = scratch + (size_t)blockIdx.x * Lay::scratch(N, Q, q1, npr, pdim);
-  double* Hb = nb + (size_t)Q * NS;                 // blocks, row-major lower enumeration
-  double* Linv = Hb + Lay::hb_size(N, q1, npr, pdim);
+  double* T1 = nb + (size_t)Q * NS;                 // [k1 k2][pr3][ab] (p = 3); Hb when not in smem
+  double* Linv = T1 + Lay::hb_size(N, q1, npr, pdim);
   double* T2 = Linv + (size_t)N * TB;               // [k1][pr2][pr3][ab] (p = 3)
-  double* T1 = Hb;                                  // [k1 k2][pr3][ab]   (p = 3), dead before Hb is written
+  // Hessian blocks (row-major lower enumeration): in shared memory when they fit (config 5: 204 KB),
+  // so the blocked Cholesky works on-chip; else in the L2-resident scratch slice
+  // (HBS: a compile-time choice, so the Cholesky's accesses are shared-memory instructions)
+  double* Hb = HBS ? sLL + ((P.T.q1d * P.T.npr + 1) & ~1) + 8 : T1;  // after ctl (8 doubles)
+  if (HBS) Linv = Hb + (size_t)(N * (N + 1) / 2) * TB;
+
   const DualLaunch& A = P.a;
   long long my_iters = 0, my_failed = 0;
   int my_worst = 0;

@@ -1079,8 +1079,11 @@ int launch_dual(const KernelCtx& k, const DualLaunch& a) {
     // cells too large for the on-chip group kernel (config 5): CTA per cell, L2-resident scratch
     if (k.big_scratch && k.closure == CL_EULER && k.m == 4) {
       constexpr int NT = 512;
-      const size_t smem = ((size_t)5 * k.T.N * 4 + 8 * (NT / 32) + ((k.T.q1d * k.T.npr + 1) & ~1) + 8) * 8;
-      auto kern = k_dual_big<CL_EULER, 4, NT>;
+      const size_t smem0 = ((size_t)5 * k.T.N * 4 + 8 * (NT / 32) + ((k.T.q1d * k.T.npr + 1) & ~1) + 8) * 8;
+      const size_t hbl = ((size_t)(k.T.N * (k.T.N + 1) / 2) * 16 + (size_t)k.T.N * 16) * 8;
+      const int hb_in_smem = (smem0 + hbl <= k.smem_optin) ? 1 : 0;
+      const size_t smem = smem0 + (hb_in_smem ? hbl : 0);
+      auto kern = hb_in_smem ? k_dual_big<CL_EULER, 4, NT, true> : k_dual_big<CL_EULER, 4, NT, false>;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       const int grid = (int)std::min<int64_t>(a.cells, (int64_t)k.big_ctas);
       DualParams P{k.T, k.mesh, k.nw, k.ad, k.cl, a, k.sc};
