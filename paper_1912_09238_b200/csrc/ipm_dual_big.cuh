@@ -35,6 +35,10 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
   constexpr int NW = NT / 32;
   constexpr int MM = Lay::MM, NS = Lay::NS, TB = Lay::TB;
 #define BIDX(a, b) ((b) * MS + (a))
+  // shared-memory blocks: element index XOR-swizzled by the block index, so that threads touching the
+  // same element of consecutive blocks hit different banks (a 128-byte block stride would put them all
+  // in one bank)
+#define SW(pb, x) (HBS ? ((x) ^ ((pb) & 15)) : (x))
   extern __shared__ __align__(16) double sm[];
   const int N = P.T.N, Q = P.T.Q, QP = P.T.QP;
   const double* __restrict__ PhiT = P.T.PhiT;
@@ -254,7 +258,7 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
 #pragma unroll
             for (int a = 0; a < MS; ++a)
 #pragma unroll
-              for (int b = 0; b < MS; ++b) o[BIDX(a, b)] = acc[a <= b ? sym_idx<MS>(a, b) : sym_idx<MS>(b, a)];
+              for (int b = 0; b < MS; ++b) o[SW(p, BIDX(a, b))] = acc[a <= b ? sym_idx<MS>(a, b) : sym_idx<MS>(b, a)];
           }
         } else
         for (int p = t; p < NPl; p += NT) {
@@ -275,7 +279,7 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
 #pragma unroll
           for (int a = 0; a < MS; ++a)
 #pragma unroll
-            for (int b = 0; b < MS; ++b) o[BIDX(a, b)] = acc[a <= b ? sym_idx<MS>(a, b) : sym_idx<MS>(b, a)];
+            for (int b = 0; b < MS; ++b) o[SW(p, BIDX(a, b))] = acc[a <= b ? sym_idx<MS>(a, b) : sym_idx<MS>(b, a)];
         }
         for (int r = t; r < n; r += NT) dd[r] = -g[r];
         __syncthreads();
@@ -283,13 +287,14 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
         bool chol_ok = true;
         for (int K = 0; K < Nl; ++K) {
           if (t == 0) {
-            double* Bk = Hb + (size_t)(K * (K + 1) / 2 + K) * TB;
+            const int pk = K * (K + 1) / 2 + K;
+            double* Bk = Hb + (size_t)pk * TB;
             double L[MS][MS], li[MS][MS], inv[MS];
             bool ok = true;
 #pragma unroll
             for (int a = 0; a < MS; ++a)
 #pragma unroll
-              for (int b = 0; b < MS; ++b) L[a][b] = Bk[BIDX(a, b)];
+              for (int b = 0; b < MS; ++b) L[a][b] = Bk[SW(pk, BIDX(a, b))];
 #pragma unroll
             for (int c = 0; c < MS; ++c) {
               double sv = L[c][c];
@@ -323,8 +328,8 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
             for (int a = 0; a < MS; ++a)
 #pragma unroll
               for (int b = 0; b < MS; ++b) {
-                Bk[BIDX(a, b)] = (b <= a) ? L[a][b] : 0.0;
-                oi[BIDX(a, b)] = (b <= a) ? li[a][b] : 0.0;
+                Bk[SW(pk, BIDX(a, b))] = (b <= a) ? L[a][b] : 0.0;
+                oi[SW(K, BIDX(a, b))] = (b <= a) ? li[a][b] : 0.0;
               }
             double bk[MS];
 #pragma unroll
@@ -345,19 +350,20 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
           }
           const double* Li = Linv + (size_t)K * TB;
           for (int I = K + 1 + t; I < Nl; I += NT) {
-            double* Bik = Hb + (size_t)(I * (I + 1) / 2 + K) * TB;
+            const int pik = I * (I + 1) / 2 + K;
+            double* Bik = Hb + (size_t)pik * TB;
             double A_[MS][MS], X[MS][MS], yk[MS];
 #pragma unroll
             for (int a = 0; a < MS; ++a)
 #pragma unroll
-              for (int b = 0; b < MS; ++b) A_[a][b] = Bik[BIDX(a, b)];
+              for (int b = 0; b < MS; ++b) A_[a][b] = Bik[SW(pik, BIDX(a, b))];
 #pragma unroll
             for (int r = 0; r < MS; ++r)
 #pragma unroll
               for (int c = 0; c < MS; ++c) {
                 double v = 0.0;
 #pragma unroll
-                for (int x = 0; x <= c; ++x) v = fma(A_[r][x], Li[BIDX(c, x)], v);
+                for (int x = 0; x <= c; ++x) v = fma(A_[r][x], Li[SW(K, BIDX(c, x))], v);
                 X[r][c] = v;
               }
 #pragma unroll
@@ -367,7 +373,7 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
               double v = dd[I * MS + r];
 #pragma unroll
               for (int c = 0; c < MS; ++c) {
-                Bik[BIDX(r, c)] = X[r][c];
+                Bik[SW(pik, BIDX(r, c))] = X[r][c];
                 v = fma(-X[r][c], yk[c], v);
               }
               dd[I * MS + r] = v;
@@ -380,21 +386,22 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
             int a_, b_;
             blk_ij(e, a_, b_);
             const int I = K + 1 + a_, J = K + 1 + b_;
-            const double* Lik = Hb + (size_t)(I * (I + 1) / 2 + K) * TB;
-            const double* Ljk = Hb + (size_t)(J * (J + 1) / 2 + K) * TB;
-            double* Bij = Hb + (size_t)(I * (I + 1) / 2 + J) * TB;
+            const int pik = I * (I + 1) / 2 + K, pjk = J * (J + 1) / 2 + K, pij = I * (I + 1) / 2 + J;
+            const double* Lik = Hb + (size_t)pik * TB;
+            const double* Ljk = Hb + (size_t)pjk * TB;
+            double* Bij = Hb + (size_t)pij * TB;
             double acc[MS][MS];
 #pragma unroll
             for (int a = 0; a < MS; ++a)
 #pragma unroll
-              for (int b = 0; b < MS; ++b) acc[a][b] = Bij[BIDX(a, b)];
+              for (int b = 0; b < MS; ++b) acc[a][b] = Bij[SW(pij, BIDX(a, b))];
 #pragma unroll
             for (int x = 0; x < MS; ++x) {
               double ci[MS], cj[MS];
 #pragma unroll
               for (int a = 0; a < MS; ++a) {
-                ci[a] = Lik[BIDX(a, x)];
-                cj[a] = Ljk[BIDX(a, x)];
+                ci[a] = Lik[SW(pik, BIDX(a, x))];
+                cj[a] = Ljk[SW(pjk, BIDX(a, x))];
               }
 #pragma unroll
               for (int r = 0; r < MS; ++r)
@@ -404,7 +411,7 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
 #pragma unroll
             for (int a = 0; a < MS; ++a)
 #pragma unroll
-              for (int b = 0; b < MS; ++b) Bij[BIDX(a, b)] = acc[a][b];
+              for (int b = 0; b < MS; ++b) Bij[SW(pij, BIDX(a, b))] = acc[a][b];
           }
           __syncthreads();
         }
@@ -421,7 +428,7 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
             for (int c = 0; c < MS; ++c) {
               double v = 0.0;
 #pragma unroll
-              for (int x = c; x < MS; ++x) v = fma(Li[BIDX(x, c)], dd[K * MS + x], v);
+              for (int x = c; x < MS; ++x) v = fma(Li[SW(K, BIDX(x, c))], dd[K * MS + x], v);
               dk[c] = v;
             }
             __syncwarp();
@@ -432,10 +439,11 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
             }
             for (int e = lane; e < K * MS; e += 32) {
               const int J = e / MS, c = e - J * MS;
-              const double* Lkj = Hb + (size_t)(K * (K + 1) / 2 + J) * TB;
+              const int pkj = K * (K + 1) / 2 + J;
+              const double* Lkj = Hb + (size_t)pkj * TB;
               double v = dd[J * MS + c];
 #pragma unroll
-              for (int x = 0; x < MS; ++x) v = fma(-Lkj[BIDX(x, c)], dk[x], v);
+              for (int x = 0; x < MS; ++x) v = fma(-Lkj[SW(pkj, BIDX(x, c))], dk[x], v);
               dd[J * MS + c] = v;
             }
             __syncwarp();
@@ -536,4 +544,5 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
     }
   }
 #undef BIDX
+#undef SW
 }
