@@ -74,15 +74,17 @@ struct MmaLayout {
   //                      [T chunk q1 x NPR x CHW] at offset TO (SF only)
   // S may overlap the dead part of the node buffer chunk by chunk (see s_base)
   static __host__ __device__ int npp(int N) { return N * (N + 1) / 2; }
+  // row stride of S[ab][pair]: odd, so the gather's rows (different ab) fall into different banks
+  static __host__ __device__ int nps(int N) { return npp(N) | 1; }
   static __host__ __device__ int node(int Q) { return Q * (MS + MM); }
   static __host__ __device__ bool s_overlaps(int N, int Q, int SF) {
     if (SF == 0) return false;  // the direct sum reads J until the end
     for (int ch = 0; ch + 1 < NCH; ++ch)
-      if ((ch + 1) * CHW * npp(N) > (MS + (ch + 1) * CHW) * Q) return false;
+      if ((ch + 1) * CHW * nps(N) > (MS + (ch + 1) * CHW) * Q) return false;
     return true;
   }
   static __host__ __device__ int t_off(int N, int Q, int SF) {
-    const int s = s_overlaps(N, Q, SF) ? MM * npp(N) : 0;
+    const int s = s_overlaps(N, Q, SF) ? MM * nps(N) : 0;
     return ((node(Q) > s ? node(Q) : s) + 1) & ~1;
   }
   static __host__ __device__ int s_base(int N, int Q, int SF, int q1d) {
@@ -91,7 +93,7 @@ struct MmaLayout {
     return (t_off(N, Q, SF) + t + 1) & ~1;
   }
   static __host__ __device__ int region(int N, int Q, int SF, int q1d, int NB) {
-    int r = s_base(N, Q, SF, q1d) + MM * npp(N);
+    int r = s_base(N, Q, SF, q1d) + MM * nps(N);
     const int t = t_off(N, Q, SF) + ((SF > 0) ? q1d * (SF * (SF + 1) / 2) * CHW : 0);
     if (t > r) r = t;
     const int c = (2 * NB + 1) * 64;  // Cholesky: panel [NB][64], Linv fragment [64], diagonal [NB][64]
@@ -177,10 +179,13 @@ struct DualMma {
     f0 = (q & 1) ? u1 : u0;
     f1 = (q & 1) ? v1 : v0;
   }
-  // store a C-fragment block into operand (A-fragment) order: element (r, c) at (c/4)*32 + r*4 + c%4
+  // block storage in shared memory for fragment exchange: row-major, element (r, c) at r*8 + c.
+  // (An XOR swizzle that also removes the 2-way conflicts of the A/B-fragment loads measured 3 %
+  // slower: the extra index arithmetic costs more than the conflicts.)
+  __device__ static int bpos(int r, int c) { return r * 8 + c; }
   __device__ static void store_afrag(double* dst, double c0, double c1, int lane) {
     const int r = lane >> 2, q = lane & 3;
-    double2* p = reinterpret_cast<double2*>(dst + (q >> 1) * 32 + r * 4 + 2 * (q & 1));
+    double2* p = reinterpret_cast<double2*>(dst + bpos(r, 2 * q));
     *p = make_double2(c0, c1);
   }
 
@@ -296,18 +301,18 @@ struct DualMma {
     CPH(4);
     // Fragment orders (mma.m8n8k4.f64; lane l, r = l/4, q = l%4):
     //   C: (r, 2q + e), e = 0, 1          A: (r, q + 4kk)          B: (q + 4kk, r)
-    // Conversions go through shared memory (store in A order, reload), not shuffles.
+    // Conversions go through shared memory (store as bpos(r, c), reload), not shuffles.
     //   blk[s]  C-fragment of the trailing block A_IJ; after its panel step the B-fragment of L_IJ
-    //   pan[I]  L_IK of the current panel, A order;  linvf: Linv_K, A order
+    //   pan[I]  L_IK of the current panel;  linvf: Linv_K (both stored as bpos)
     //   dg[K]   C-fragment of A_KK; after the factorisation the B-fragment of Linv_K
     auto afrag_ld = [&](const double* src, double& f0, double& f1) {
-      f0 = src[lane];
-      f1 = src[32 + lane];
+      f0 = src[bpos(r, q)];
+      f1 = src[bpos(r, q + 4)];
     };
-    // B-fragment of a block stored in A order: element (row, c) sits at (c/4)*32 + row*4 + c%4
+    // B-fragment: element (q + 4kk, r) of the stored block
     auto bfrag_ld = [&](const double* src, double& f0, double& f1) {
-      f0 = src[(r >> 2) * 32 + q * 4 + (r & 3)];
-      f1 = src[(r >> 2) * 32 + (q + 4) * 4 + (r & 3)];
+      f0 = src[bpos(q, r)];
+      f1 = src[bpos(q + 4, r)];
     };
     // vector as an operand: column 0 of B or row 0 of A (lanes 0-3)
     auto vec_frag = [&](const double* v, double& f0, double& f1) {
@@ -522,7 +527,7 @@ __global__ void __launch_bounds__(IPM_MMA_THREADS) k_dual_mma(DualParams P) {
   const int wig = t >> 5, lane = t & 31;
   const int bar = 1 + grp;
   const int nmax = N * MS;
-  const int npp = Lay::npp(N);
+  const int npp = Lay::nps(N);  // S row stride
   double* base = sm + tabsz + (size_t)grp * Lay::per_group(N, Q, W, SF, q1, NB);
   double* lam = base;
   double* lt = lam + NV;
