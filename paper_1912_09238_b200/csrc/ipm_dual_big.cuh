@@ -63,9 +63,12 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
   double* T2 = Linv + (size_t)N * TB;               // [k1][pr2][pr3][ab] (p = 3)
   // Hessian blocks (row-major lower enumeration): in shared memory when they fit (config 5: 204 KB),
   // so the blocked Cholesky works on-chip; else in the L2-resident scratch slice
-  // (HBS: a compile-time choice, so the Cholesky's accesses are shared-memory instructions)
+  // HBS (compile time): the Hessian as 8 x 8 blocks (row-major, lower block triangle, 64 doubles each)
+  // in shared memory, factored with DMMA (as k_dual_mma, blocks in shared memory instead of
+  // registers); otherwise 4 x 4 blocks in the L2-resident scratch slice
   double* Hb = HBS ? sLL + ((P.T.q1d * P.T.npr + 1) & ~1) + 8 : T1;  // after ctl (8 doubles)
-  if (HBS) Linv = Hb + (size_t)(N * (N + 1) / 2) * TB;
+  const int NB8 = (N * MS + 7) / 8;
+  double* linvf = Hb + (size_t)(NB8 * (NB8 + 1) / 2) * 64;  // HBS: Linv_K row-major (panel operand)
 
   const DualLaunch& A = P.a;
   long long my_iters = 0, my_failed = 0;
@@ -116,21 +119,33 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
     return isfinite(v[0]) && isfinite(v[1]);
   };
   auto grad = [&](int Nl) -> double {
+    // two threads per output (halves of the node range, combined by a shuffle): a 1000-node dot
+    // product per output is a long latency chain
     const int n = Nl * MS;
     double part[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int r = t; r < n; r += NT) {
-      const int i = r / MS, a = r - i * MS;
-      const double* wp = WPhiT + (size_t)i * QP;
+    const int Qh = (Q + 1) / 2;
+    for (int base = 0; base < 2 * n; base += NT) {
+      const int idx = base + t, r = idx >> 1, half = idx & 1;
       double s0 = 0.0, s1 = 0.0;
-      int k = 0;
-      for (; k + 1 < Q; k += 2) {
-        s0 = fma(wp[k], nb[(size_t)k * NS + a], s0);
-        s1 = fma(wp[k + 1], nb[(size_t)(k + 1) * NS + a], s1);
+      if (idx < 2 * n) {
+        const int i = r / MS, a = r - i * MS;
+        const double* wp = WPhiT + (size_t)i * QP;
+        const int k0 = half * Qh, k1 = half ? Q : Qh;
+        int k = k0;
+        for (; k + 1 < k1; k += 2) {
+          s0 = fma(wp[k], nb[(size_t)k * NS + a], s0);
+          s1 = fma(wp[k + 1], nb[(size_t)(k + 1) * NS + a], s1);
+        }
+        if (k < k1) s0 = fma(wp[k], nb[(size_t)k * NS + a], s0);
       }
-      if (k < Q) s0 = fma(wp[k], nb[(size_t)k * NS + a], s0);
-      const double gr = (s0 + s1) - uh[r];
-      g[r] = gr;
-      part[a] = fma(gr, gr, part[a]);
+      double sum = s0 + s1;
+      sum += __shfl_xor_sync(FULL_MASK, sum, 1);
+      if (idx < 2 * n && half == 0) {
+        const int a = r % MS;
+        const double gr = sum - uh[r];
+        g[r] = gr;
+        part[a] = fma(gr, gr, part[a]);
+      }
     }
     bsum(part, MS);
     double crit = 0.0;
@@ -148,11 +163,127 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
     d = v[0];
     ad = v[1];
   };
+  // write the m x m block of basis pair (I >= J) of the Hessian (unique entries acc[ab])
+  auto hput = [&](int p, int I, int J, const double* acc) {
+#pragma unroll
+    for (int a = 0; a < MS; ++a)
+#pragma unroll
+      for (int b = 0; b < MS; ++b) {
+        const double v = acc[a <= b ? sym_idx<MS>(a, b) : sym_idx<MS>(b, a)];
+        if constexpr (HBS) {
+          const int R = I * MS + a, C = J * MS + b, bi = R >> 3, bj = C >> 3;
+          Hb[(size_t)(bi * (bi + 1) / 2 + bj) * 64 + (R & 7) * 8 + (C & 7)] = v;
+        } else {
+          Hb[(size_t)p * TB + BIDX(a, b)] = v;
+        }
+      }
+  };
   auto blk_ij = [](int p, int& I, int& J) {
     I = (int)((sqrtf(8.0f * p + 1.0f) - 1.0f) * 0.5f);
     while (I * (I + 1) / 2 > p) --I;
     while ((I + 1) * (I + 2) / 2 <= p) ++I;
     J = p - I * (I + 1) / 2;
+  };
+
+  // Cholesky of the 8 x 8-blocked Hessian in shared memory on the fp64 tensor path (HBS), forward
+  // solve folded in, then the back substitution; dd: in -g (padded), out: the Newton direction.
+  // Block (I, J) is row-major; after step J it holds L_IJ, the diagonal slot holds Linv_J.
+  //   fragments (mma.m8n8k4.f64, lane = 4r + q): A (r, q + 4kk), B (q + 4kk, r), C (r, 2q + e)
+  auto chol8 = [&](int n) -> bool {
+    constexpr int NWp = NT / 32;
+    const int NBl = (n + 7) >> 3, r = lane >> 2, q = lane & 3;
+    auto blk = [&](int I, int J) -> double* { return Hb + (size_t)(I * (I + 1) / 2 + J) * 64; };
+    if (t == 0) ctl[1] = 0;
+    for (int K = 0; K < NBl; ++K) {
+      if (wid == 0) {  // diagonal block: L_KK by quad shuffles, Linv_K, y_K = Linv_K b_K
+        double* D = blk(K, K);
+        double a0 = D[r * 8 + 2 * q], a1 = D[r * 8 + 2 * q + 1];
+        const bool ok = blk8_diag_factor(a0, a1, lane, min(8, n - 8 * K));
+        __syncwarp();
+        *reinterpret_cast<double2*>(linvf + r * 8 + 2 * q) = make_double2(a0, a1);
+        *reinterpret_cast<double2*>(D + r * 8 + 2 * q) = make_double2(a0, a1);
+        __syncwarp();
+        const double f0 = linvf[r * 8 + q], f1 = linvf[r * 8 + q + 4];
+        const double b0 = lane < 4 ? dd[K * 8 + lane] : 0.0, b1 = lane < 4 ? dd[K * 8 + 4 + lane] : 0.0;
+        double y0 = 0.0, y1 = 0.0;
+        dmma884(y0, y1, f0, b0);
+        dmma884(y0, y1, f1, b1);
+        __syncwarp();
+        if (q == 0) dd[K * 8 + r] = y0;
+        if (lane == 0 && !ok) ctl[1] = 1;
+      }
+      __syncthreads();
+      if (ctl[1]) return false;
+      {  // panel: L_IK = A_IK Linv_K^T, b_I -= L_IK y_K
+        const double lf0 = linvf[r * 8 + q], lf1 = linvf[r * 8 + q + 4];
+        const double yf0 = lane < 4 ? dd[K * 8 + lane] : 0.0, yf1 = lane < 4 ? dd[K * 8 + 4 + lane] : 0.0;
+        for (int I = K + 1 + wid; I < NBl; I += NWp) {
+          double* B = blk(I, K);
+          double f0 = B[r * 8 + q], f1 = B[r * 8 + q + 4];
+          double x0 = 0.0, x1 = 0.0;
+          dmma884(x0, x1, f0, lf0);
+          dmma884(x0, x1, f1, lf1);
+          __syncwarp();
+          *reinterpret_cast<double2*>(B + r * 8 + 2 * q) = make_double2(x0, x1);
+          __syncwarp();
+          f0 = B[r * 8 + q];
+          f1 = B[r * 8 + q + 4];
+          double v0 = 0.0, v1 = 0.0;
+          dmma884(v0, v1, f0, yf0);
+          dmma884(v0, v1, f1, yf1);
+          if (q == 0) dd[I * 8 + r] -= v0;
+        }
+      }
+      __syncthreads();
+      {  // trailing: A_IJ -= L_IK L_JK^T, K < J <= I
+        const int R = NBl - 1 - K, ntr = R * (R + 1) / 2;
+        for (int e = wid; e < ntr; e += NWp) {
+          int a_, b_;
+          blk_ij(e, a_, b_);
+          const int I = K + 1 + a_, J = K + 1 + b_;
+          const double* Lik = blk(I, K);
+          const double* Ljk = blk(J, K);
+          double* C = blk(I, J);
+          double2 c = *reinterpret_cast<const double2*>(C + r * 8 + 2 * q);
+          const double a0 = Lik[r * 8 + q], a1 = Lik[r * 8 + q + 4];
+          const double b0 = Ljk[r * 8 + q], b1 = Ljk[r * 8 + q + 4];
+          dmma884(c.x, c.y, dneg(a0), b0);
+          dmma884(c.x, c.y, dneg(a1), b1);
+          *reinterpret_cast<double2*>(C + r * 8 + 2 * q) = c;
+        }
+      }
+      __syncthreads();
+    }
+    // back substitution: d_K = Linv_K^T z_K, z_J -= L_KJ^T d_K (row-vector DMMAs)
+    for (int K = NBl - 1; K >= 0; --K) {
+      if (wid == 0) {
+        const double* D = blk(K, K);
+        const double z0 = lane < 4 ? dd[K * 8 + lane] : 0.0, z1 = lane < 4 ? dd[K * 8 + 4 + lane] : 0.0;
+        double v0 = 0.0, v1 = 0.0;
+        dmma884(v0, v1, z0, D[q * 8 + r]);
+        dmma884(v0, v1, z1, D[(q + 4) * 8 + r]);
+        __syncwarp();
+        if (lane < 4) {
+          dd[K * 8 + 2 * q] = v0;
+          dd[K * 8 + 2 * q + 1] = v1;
+        }
+      }
+      __syncthreads();
+      if (K == 0) break;
+      const double d0 = lane < 4 ? dd[K * 8 + lane] : 0.0, d1 = lane < 4 ? dd[K * 8 + 4 + lane] : 0.0;
+      for (int J = wid; J < K; J += NWp) {
+        const double* L = blk(K, J);
+        double v0 = 0.0, v1 = 0.0;
+        dmma884(v0, v1, d0, L[q * 8 + r]);
+        dmma884(v0, v1, d1, L[(q + 4) * 8 + r]);
+        if (lane < 4) {
+          dd[J * 8 + 2 * q] -= v0;
+          dd[J * 8 + 2 * q + 1] -= v1;
+        }
+      }
+      __syncthreads();
+    }
+    return true;
   };
 
   for (;;) {
@@ -254,11 +385,7 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
 #pragma unroll
               for (int z = 0; z < MM; ++z) acc[z] = fma(lv, tv[z], acc[z]);
             }
-            double* o = Hb + (size_t)p * TB;
-#pragma unroll
-            for (int a = 0; a < MS; ++a)
-#pragma unroll
-              for (int b = 0; b < MS; ++b) o[SW(p, BIDX(a, b))] = acc[a <= b ? sym_idx<MS>(a, b) : sym_idx<MS>(b, a)];
+            hput(p, I, J, acc);
           }
         } else
         for (int p = t; p < NPl; p += NT) {
@@ -275,16 +402,29 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
 #pragma unroll
             for (int z = 0; z < MM; ++z) acc[z] = fma(f, Jk[z], acc[z]);
           }
-          double* o = Hb + (size_t)p * TB;
-#pragma unroll
-          for (int a = 0; a < MS; ++a)
-#pragma unroll
-            for (int b = 0; b < MS; ++b) o[SW(p, BIDX(a, b))] = acc[a <= b ? sym_idx<MS>(a, b) : sym_idx<MS>(b, a)];
+          hput(p, I, J, acc);
         }
-        for (int r = t; r < n; r += NT) dd[r] = -g[r];
+        // identity padding of the last 8 x 8 block row beyond n (HBS), right-hand side -g
+        if constexpr (HBS) {
+          const int NBl = (n + 7) >> 3;
+          if (n < NBl * 8) {
+            const int I = NBl - 1;
+            for (int e = t; e < NBl * 64; e += NT) {
+              const int J = e >> 6, rr = (e >> 3) & 7, cc = e & 7;
+              const int R = 8 * I + rr, C = 8 * J + cc;
+              if (R >= n || C >= n) Hb[(size_t)(I * (I + 1) / 2 + J) * 64 + rr * 8 + cc] = (R == C) ? 1.0 : 0.0;
+            }
+          }
+          for (int r = t; r < NBl * 8; r += NT) dd[r] = (r < n) ? -g[r] : 0.0;
+        } else {
+          for (int r = t; r < n; r += NT) dd[r] = -g[r];
+        }
         __syncthreads();
-        // blocked right-looking Cholesky, blocks resident in the scratch slice; forward solve folded
         bool chol_ok = true;
+        if constexpr (HBS) {
+          chol_ok = chol8(n);
+        } else {
+        // blocked right-looking Cholesky, blocks resident in the scratch slice; forward solve folded
         for (int K = 0; K < Nl; ++K) {
           if (t == 0) {
             const int pk = K * (K + 1) / 2 + K;
@@ -415,10 +555,7 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
           }
           __syncthreads();
         }
-        if (!chol_ok) {
-          status = 2;
-          break;
-        }
+          if (chol_ok) {
         // back substitution L^T d = y (warp 0)
         if (wid == 0) {
           for (int K = Nl - 1; K >= 0; --K) {
@@ -448,6 +585,13 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
             }
             __syncwarp();
           }
+        }
+        __syncthreads();
+          }
+        }
+        if (!chol_ok) {
+          status = 2;
+          break;
         }
         __syncthreads();
         double slope, dummy;

@@ -64,6 +64,63 @@ __host__ __device__ constexpr int cmI(int r, int NB) {
   return J + r;
 }
 
+// 1/sqrt(x): hardware approximation + two Newton steps (rounding-level accuracy for the positive
+// normal pivots of an SPD matrix; shorter latency than the library rsqrt, which also handles
+// special operands, on the Cholesky's critical path)
+__device__ __forceinline__ double rsqrt_nr(double x) {
+#ifdef IPM_DIAG_LIBRSQRT
+  return rsqrt(x);
+#else
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  double e = fma(-h * y, y, 0.5);
+  y = fma(y, e, y);
+  e = fma(-h * y, y, 0.5);
+  return fma(y, e, y);
+#endif
+}
+
+// ---- 8x8 diagonal block: in C-fragment layout A (lower part used); out: Linv = L^{-1} -------
+// ncol: columns to factor (the rest of the block is identity padding beyond n)
+__device__ __forceinline__ bool blk8_diag_factor(double& a0, double& a1, int lane, int ncol = 8) {
+  const int r = lane >> 2, q = lane & 3;
+  double x0 = (r == 2 * q) ? 1.0 : 0.0, x1 = (r == 2 * q + 1) ? 1.0 : 0.0;
+  bool ok = true;
+  __syncwarp();  // the warp is converged here: lets the compiler drop divergent-shuffle fallbacks
+#ifdef IPM_DIAG_UNROLL
+#pragma unroll
+#else
+#pragma unroll 1  // smaller code beats the extra ILP (instruction-cache bound kernel)
+#endif
+  for (int c = 0; c < ncol; ++c) {
+    const int cq = c >> 1;
+    const double mine = (c & 1) ? a1 : a0;
+    const double d = __shfl_sync(FULL_MASK, mine, c * 4 + cq);
+    const double arc = __shfl_sync(FULL_MASK, mine, r * 4 + cq);
+    const double a0c = __shfl_sync(FULL_MASK, mine, (2 * q) * 4 + cq);
+    const double a1c = __shfl_sync(FULL_MASK, mine, (2 * q + 1) * 4 + cq);
+    if (!(d > 0.0) || !isfinite(d)) ok = false;
+    const double rs = rsqrt_nr(d);
+    const double lrc = arc * rs;
+    if (2 * q > c) a0 = fma(-lrc, a0c * rs, a0);
+    if (2 * q + 1 > c) a1 = fma(-lrc, a1c * rs, a1);
+    const double xs = (r == c) ? rs : 1.0;
+    x0 *= xs;
+    x1 *= xs;
+    const double xc0 = __shfl_sync(FULL_MASK, x0, c * 4 + q);
+    const double xc1 = __shfl_sync(FULL_MASK, x1, c * 4 + q);
+    if (r > c) {
+      x0 = fma(-lrc, xc0, x0);
+      x1 = fma(-lrc, xc1, x1);
+    }
+  }
+  a0 = x0;
+  a1 = x1;
+  return ok;
+}
+
+
 template <int MS>
 struct MmaLayout {
   static constexpr int MM = MS * (MS + 1) / 2;
@@ -114,60 +171,8 @@ struct DualMma {
   static constexpr int G = 32 * W;
   static constexpr int NBT = NB * (NB + 1) / 2;
   
-  // 1/sqrt(x): hardware approximation + two Newton steps (rounding-level accuracy for the positive
-  // normal pivots of an SPD matrix; shorter latency than the library rsqrt, which also handles
-  // special operands, on the Cholesky's critical path)
-  __device__ static double rsqrt_nr(double x) {
-#ifdef IPM_DIAG_LIBRSQRT
-    return rsqrt(x);
-#else
-    double y;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-    const double h = 0.5 * x;
-    double e = fma(-h * y, y, 0.5);
-    y = fma(y, e, y);
-    e = fma(-h * y, y, 0.5);
-    return fma(y, e, y);
-#endif
-  }
-
-  // ---- 8x8 diagonal block: in C-fragment layout A (lower part used); out: Linv = L^{-1} -------
-  // ncol: columns to factor (the rest of the block is identity padding beyond n)
   __device__ static bool diag_factor(double& a0, double& a1, int lane, int ncol = 8) {
-    const int r = lane >> 2, q = lane & 3;
-    double x0 = (r == 2 * q) ? 1.0 : 0.0, x1 = (r == 2 * q + 1) ? 1.0 : 0.0;
-    bool ok = true;
-    __syncwarp();  // the warp is converged here: lets the compiler drop divergent-shuffle fallbacks
-#ifdef IPM_DIAG_UNROLL
-#pragma unroll
-#else
-#pragma unroll 1  // smaller code beats the extra ILP (instruction-cache bound kernel)
-#endif
-    for (int c = 0; c < ncol; ++c) {
-      const int cq = c >> 1;
-      const double mine = (c & 1) ? a1 : a0;
-      const double d = __shfl_sync(FULL_MASK, mine, c * 4 + cq);
-      const double arc = __shfl_sync(FULL_MASK, mine, r * 4 + cq);
-      const double a0c = __shfl_sync(FULL_MASK, mine, (2 * q) * 4 + cq);
-      const double a1c = __shfl_sync(FULL_MASK, mine, (2 * q + 1) * 4 + cq);
-      if (!(d > 0.0) || !isfinite(d)) ok = false;
-      const double rs = rsqrt_nr(d);
-      const double lrc = arc * rs;
-      if (2 * q > c) a0 = fma(-lrc, a0c * rs, a0);
-      if (2 * q + 1 > c) a1 = fma(-lrc, a1c * rs, a1);
-      const double xs = (r == c) ? rs : 1.0;
-      x0 *= xs;
-      x1 *= xs;
-      const double xc0 = __shfl_sync(FULL_MASK, x0, c * 4 + q);
-      const double xc1 = __shfl_sync(FULL_MASK, x1, c * 4 + q);
-      if (r > c) {
-        x0 = fma(-lrc, xc0, x0);
-        x1 = fma(-lrc, xc1, x1);
-      }
-    }
-    a0 = x0;
-    a1 = x1;
-    return ok;
+    return blk8_diag_factor(a0, a1, lane, ncol);
   }
 
   // C-fragment -> A-fragment (lane l: row l/4, column l%4 + 4 kk)

@@ -1080,7 +1080,8 @@ int launch_dual(const KernelCtx& k, const DualLaunch& a) {
     if (k.big_scratch && k.closure == CL_EULER && k.m == 4) {
       constexpr int NT = 512;
       const size_t smem0 = ((size_t)5 * k.T.N * 4 + 8 * (NT / 32) + ((k.T.q1d * k.T.npr + 1) & ~1) + 8) * 8;
-      const size_t hbl = ((size_t)(k.T.N * (k.T.N + 1) / 2) * 16 + (size_t)k.T.N * 16) * 8;
+      const size_t nb8 = (size_t)(k.T.N * 4 + 7) / 8;
+      const size_t hbl = (nb8 * (nb8 + 1) / 2 * 64 + 64) * 8;  // 8 x 8 blocks + Linv operand
       const int hb_in_smem = (smem0 + hbl <= k.smem_optin) ? 1 : 0;
       const size_t smem = smem0 + (hb_in_smem ? hbl : 0);
       auto kern = hb_in_smem ? k_dual_big<CL_EULER, 4, NT, true> : k_dual_big<CL_EULER, 4, NT, false>;
