@@ -193,26 +193,42 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
     constexpr int NWp = NT / 32;
     const int NBl = (n + 7) >> 3, r = lane >> 2, q = lane & 3;
     auto blk = [&](int I, int J) -> double* { return Hb + (size_t)(I * (I + 1) / 2 + J) * 64; };
-    if (t == 0) ctl[1] = 0;
-    for (int K = 0; K < NBl; ++K) {
-      if (wid == 0) {  // diagonal block: L_KK by quad shuffles, Linv_K, y_K = Linv_K b_K
-        double* D = blk(K, K);
-        double a0 = D[r * 8 + 2 * q], a1 = D[r * 8 + 2 * q + 1];
-        const bool ok = blk8_diag_factor(a0, a1, lane, min(8, n - 8 * K));
-        __syncwarp();
-        *reinterpret_cast<double2*>(linvf + r * 8 + 2 * q) = make_double2(a0, a1);
-        *reinterpret_cast<double2*>(D + r * 8 + 2 * q) = make_double2(a0, a1);
-        __syncwarp();
-        const double f0 = linvf[r * 8 + q], f1 = linvf[r * 8 + q + 4];
-        const double b0 = lane < 4 ? dd[K * 8 + lane] : 0.0, b1 = lane < 4 ? dd[K * 8 + 4 + lane] : 0.0;
-        double y0 = 0.0, y1 = 0.0;
-        dmma884(y0, y1, f0, b0);
-        dmma884(y0, y1, f1, b1);
-        __syncwarp();
-        if (q == 0) dd[K * 8 + r] = y0;
-        if (lane == 0 && !ok) ctl[1] = 1;
+    // diagonal block K (warp 0): L_KK by quad shuffles, Linv_K (into linvf and the diagonal slot),
+    // y_K = Linv_K b_K
+    auto diag = [&](int K) {
+      double* D = blk(K, K);
+      double a0 = D[r * 8 + 2 * q], a1 = D[r * 8 + 2 * q + 1];
+      const bool ok = blk8_diag_factor(a0, a1, lane, min(8, n - 8 * K));
+      __syncwarp();
+      *reinterpret_cast<double2*>(linvf + r * 8 + 2 * q) = make_double2(a0, a1);
+      *reinterpret_cast<double2*>(D + r * 8 + 2 * q) = make_double2(a0, a1);
+      __syncwarp();
+      const double f0 = linvf[r * 8 + q], f1 = linvf[r * 8 + q + 4];
+      const double b0 = lane < 4 ? dd[K * 8 + lane] : 0.0, b1 = lane < 4 ? dd[K * 8 + 4 + lane] : 0.0;
+      double y0 = 0.0, y1 = 0.0;
+      dmma884(y0, y1, f0, b0);
+      dmma884(y0, y1, f1, b1);
+      __syncwarp();
+      if (q == 0) dd[K * 8 + r] = y0;
+      if (lane == 0 && !ok) ctl[1] = 1;
+    };
+    // A_IJ -= L_IK L_JK^T for the row I, columns J in [j0, j1]
+    auto row_update = [&](int K, int I, int j0, int j1) {
+      const double* Lik = blk(I, K);
+      const double a0 = dneg(Lik[r * 8 + q]), a1 = dneg(Lik[r * 8 + q + 4]);
+      for (int J = j0; J <= j1; ++J) {
+        const double* Ljk = blk(J, K);
+        double* C = blk(I, J);
+        double2 c = *reinterpret_cast<const double2*>(C + r * 8 + 2 * q);
+        dmma884(c.x, c.y, a0, Ljk[r * 8 + q]);
+        dmma884(c.x, c.y, a1, Ljk[r * 8 + q + 4]);
+        *reinterpret_cast<double2*>(C + r * 8 + 2 * q) = c;
       }
-      __syncthreads();
+    };
+    if (t == 0) ctl[1] = 0;
+    if (wid == 0) diag(0);
+    __syncthreads();
+    for (int K = 0; K < NBl; ++K) {
       if (ctl[1]) return false;
       {  // panel: L_IK = A_IK Linv_K^T, b_I -= L_IK y_K
         const double lf0 = linvf[r * 8 + q], lf1 = linvf[r * 8 + q + 4];
@@ -235,22 +251,16 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
         }
       }
       __syncthreads();
-      {  // trailing: A_IJ -= L_IK L_JK^T, K < J <= I
-        const int R = NBl - 1 - K, ntr = R * (R + 1) / 2;
-        for (int e = wid; e < ntr; e += NWp) {
-          int a_, b_;
-          blk_ij(e, a_, b_);
-          const int I = K + 1 + a_, J = K + 1 + b_;
-          const double* Lik = blk(I, K);
-          const double* Ljk = blk(J, K);
-          double* C = blk(I, J);
-          double2 c = *reinterpret_cast<const double2*>(C + r * 8 + 2 * q);
-          const double a0 = Lik[r * 8 + q], a1 = Lik[r * 8 + q + 4];
-          const double b0 = Ljk[r * 8 + q], b1 = Ljk[r * 8 + q + 4];
-          dmma884(c.x, c.y, dneg(a0), b0);
-          dmma884(c.x, c.y, dneg(a1), b1);
-          *reinterpret_cast<double2*>(C + r * 8 + 2 * q) = c;
+      // trailing update by rows (the row's L_IK operand is loaded once); warp 0 first updates and
+      // factors the next diagonal block (look-ahead), the other warps share the remaining rows
+      if (K + 1 < NBl) {
+        if (wid == 0) {
+          row_update(K, K + 1, K + 1, K + 1);
+          diag(K + 1);
         }
+        // rows I = K+2 .. NBl-1 (row K+1 is only the diagonal block), cyclic over warps 1..NWp-1
+        if (wid > 0)
+          for (int idx = wid; idx < NBl - 1 - K; idx += NWp - 1) row_update(K, K + 1 + idx, K + 1, K + 1 + idx);
       }
       __syncthreads();
     }
