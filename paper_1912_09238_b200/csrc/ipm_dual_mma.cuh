@@ -519,7 +519,10 @@ __global__ void __launch_bounds__(IPM_MMA_THREADS) k_dual_mma(DualParams P) {
   const int q1 = P.T.q1d;
   const int KS = P.T.KS, MTT = P.T.MT;
   double* sWF = sm + 2 * N * QP + ((SF > 0) ? ((q1 * NPR + 1) & ~1) : 0);  // [MT][KS][32] omega Phi^T fragments
-  const int tabsz = 2 * N * QP + ((SF > 0) ? ((q1 * NPR + 1) & ~1) : 0) + MTT * KS * 32;
+  // per pair p = i(i+1)/2 + j: the 1D pair indices (pr1, pr2) of the sum factorisation, packed
+  int* sPR = (int*)(sWF + MTT * KS * 32);
+  const int NPT = N * (N + 1) / 2;
+  const int tabsz = 2 * N * QP + ((SF > 0) ? ((q1 * NPR + 1) & ~1) : 0) + MTT * KS * 32 + ((NPT + 3) / 4) * 2;
   for (int x = threadIdx.x; x < N * QP; x += blockDim.x) {
     sPhiT[x] = P.T.PhiT[x];
     sWPhiT[x] = P.T.WPhiT[x];
@@ -527,6 +530,17 @@ __global__ void __launch_bounds__(IPM_MMA_THREADS) k_dual_mma(DualParams P) {
   if (SF > 0)
     for (int x = threadIdx.x; x < q1 * NPR; x += blockDim.x) sLL[x] = P.T.LL[x];
   for (int x = threadIdx.x; x < MTT * KS * 32; x += blockDim.x) sWF[x] = P.T.WPhiF[x];
+  if constexpr (SF > 0) {
+    for (int p = threadIdx.x; p < NPT; p += blockDim.x) {
+      int i = 0;
+      while ((i + 1) * (i + 2) / 2 <= p) ++i;
+      const int j = p - i * (i + 1) / 2;
+      int a1 = P.T.idx[i * 2], a2 = P.T.idx[i * 2 + 1], b1 = P.T.idx[j * 2], b2 = P.T.idx[j * 2 + 1];
+      if (a1 > b1) { const int x = a1; a1 = b1; b1 = x; }
+      if (a2 > b2) { const int x = a2; a2 = b2; b2 = x; }
+      sPR[p] = (a1 * SF - a1 * (a1 - 1) / 2 + (b1 - a1)) | ((a2 * SF - a2 * (a2 - 1) / 2 + (b2 - a2)) << 16);
+    }
+  }
   __syncthreads();
   const int grp = threadIdx.x / G, t = threadIdx.x - grp * G;
   const int wig = t >> 5, lane = t & 31;
@@ -607,15 +621,7 @@ __global__ void __launch_bounds__(IPM_MMA_THREADS) k_dual_mma(DualParams P) {
         // stage 2: S[ab0+c][pair] = sum_k1 LL[k1][pr1] T[k1][pr2][c]
 #pragma unroll 1
         for (int p = t; p < NPl; p += G) {
-          int i = (int)((sqrtf(8.0f * p + 1.0f) - 1.0f) * 0.5f);
-          if ((i + 1) * (i + 2) / 2 <= p) ++i;
-          if (i * (i + 1) / 2 > p) --i;
-          const int j = p - i * (i + 1) / 2;
-          int a1 = P.T.idx[i * 2], a2 = P.T.idx[i * 2 + 1], b1 = P.T.idx[j * 2], b2 = P.T.idx[j * 2 + 1];
-          if (a1 > b1) { const int x = a1; a1 = b1; b1 = x; }
-          if (a2 > b2) { const int x = a2; a2 = b2; b2 = x; }
-          const int pr1 = a1 * SF - a1 * (a1 - 1) / 2 + (b1 - a1);
-          const int pr2 = a2 * SF - a2 * (a2 - 1) / 2 + (b2 - a2);
+          const int prp = sPR[p], pr1 = prp & 0xffff, pr2 = prp >> 16;
           double acc[CHW];
 #pragma unroll
           for (int c = 0; c < CHW; ++c) acc[c] = 0.0;

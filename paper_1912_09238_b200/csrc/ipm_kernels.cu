@@ -984,7 +984,7 @@ static int dual_mma_impl(const KernelCtx& k, const DualLaunch& a) {
   constexpr int G = 32 * W;
   const int npr = SF * (SF + 1) / 2;
   const size_t tab = ((size_t)2 * k.T.N * k.T.QP + (SF > 0 ? ((k.T.q1d * npr + 1) & ~1) : 0) +
-                      (size_t)k.T.MT * k.T.KS * 32) * 8;
+                      (size_t)k.T.MT * k.T.KS * 32 + ((size_t)k.T.N * (k.T.N + 1) / 2 + 3) / 4 * 2) * 8;
   const size_t pg = (size_t)Lay::per_group(k.T.N, k.T.Q, W, SF, k.T.q1d, NB) * 8;
   if (tab + pg > k.smem_optin) return -1;
   int groups = (int)((k.smem_optin - tab) / pg);
