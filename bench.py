@@ -135,7 +135,31 @@ def workload(args):
     cfg = configs.get(args.config)
     if args.nx and cfg["mesh"]["kind"] == "cart2d":
         cfg["mesh"].update(nx=args.nx, ny=args.nx)
+    elif args.nx and cfg["mesh"]["kind"] == "1d":
+        cfg["mesh"].update(nx=args.nx)
     return cfg
+
+
+def mesh_arrays(cfg):
+    """triangle meshes (config 4) are generated from their seeded recipe (inputs/generators.py)"""
+    from inputs.generators import bump_channel_mesh
+
+    m = cfg["mesh"]
+    return bump_channel_mesh(m["nx_pts"], m["ny_pts"], m["seed"]) if m["kind"] == "tri" else None
+
+
+def stress_kind(cfg):
+    if cfg["closure"] != "euler":
+        return "burgers"
+    if cfg["mesh"]["kind"] == "tri":
+        return "bump"
+    return "euler1d" if cfg["m"] == 3 else "euler2d"
+
+
+def centres(cfg, ma):
+    from inputs.generators import cell_centres
+
+    return cell_centres(cfg["mesh"], *(ma[:2] if ma is not None else (None, None)))
 
 
 def run_reference(args):
@@ -148,13 +172,19 @@ def run_reference(args):
     if rank != 0:
         return None
     cfg = workload(args)
-    full_cells = cfg["mesh"]["nx"] * cfg["mesh"].get("ny", 1)
-    side = 128 if cfg["p"] <= 2 else 8
-    sample = configs.get(args.config, mesh=dict(nx=side, ny=side))
-    o = oracle.Oracle(sample)
-    base, z = stress_state("euler2d" if cfg["closure"] == "euler" else "burgers", cell_centres(sample["mesh"]),
-                           o.N, o.m, args.seed)
-    amp = STRESS_AMP["euler2d" if cfg["closure"] == "euler" else "burgers"]
+    kind = stress_kind(cfg)
+    if cfg["mesh"]["kind"] == "tri":
+        full_cells = len(mesh_arrays(cfg)[1])
+        sample = configs.parity_variant(args.config)
+        side = None
+    else:
+        full_cells = cfg["mesh"]["nx"] * cfg["mesh"].get("ny", 1)
+        side = (128 if cfg["p"] <= 2 else 8) if cfg["mesh"]["kind"] == "cart2d" else min(cfg["mesh"]["nx"], 4096)
+        sample = configs.get(args.config, mesh=dict(nx=side, ny=side))
+    ma = mesh_arrays(sample)
+    o = oracle.Oracle(sample, ma)
+    base, z = stress_state(kind, centres(sample, ma), o.N, o.m, args.seed, sample.get("gamma", 1.4))
+    amp = STRESS_AMP[kind]
     lam_star = o.stress_dual(base, z, amp)
     uhat = o.moments_from_dual_all(lam_star)
     lam = o.warm_start(uhat)
@@ -174,7 +204,7 @@ def run_reference(args):
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config, "cells_full": full_cells, "sample_cells": o.cells},
         "cpu_baseline": {"value": value, "unit": "cell-steps/s", "cores": cores, "kind": "oracle",
-                         "sample": f"{side}x{side} cells of the {args.config} stress state, {steps} steps "
+                         "sample": f"{o.cells} cells of the {args.config} stress state, {steps} steps "
                                    f"({iters} Newton iterations), OpenMP over cells"},
         "e2e": {"value": value, "unit": "cell-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -223,10 +253,16 @@ def run_ours(args):
     if world > 1 and cfg["mesh"]["kind"] == "cart2d":
         # weak scaling: every rank owns a block of the single-GPU size, halos exchanged over NVLink
         cfg["mesh"].update(nx=cfg["mesh"]["nx"] * px, ny=cfg["mesh"]["ny"] * py)
-    g = Context(cfg, rank=rank, nranks=world, px=px, py=py)
-    kind = "euler2d" if cfg["closure"] == "euler" else "burgers"
-    xy = cell_centres(cfg["mesh"]) if world == 1 else _local_centres(cfg["mesh"], g.cell_ids())
-    base, z = stress_state(kind, xy, g.N, g.m, args.seed + rank)
+    ma = mesh_arrays(cfg)
+    g = Context(cfg, ma, rank=rank, nranks=world, px=px, py=py)
+    kind = stress_kind(cfg)
+    if world == 1:
+        xy = centres(cfg, ma)
+    elif cfg["mesh"]["kind"] == "cart2d":
+        xy = _local_centres(cfg["mesh"], g.cell_ids())
+    else:
+        xy = centres(cfg, ma)[g.cell_ids()]
+    base, z = stress_state(kind, xy, g.N, g.m, args.seed + rank, cfg.get("gamma", 1.4))
     amp = STRESS_AMP[kind]
     dev = torch.device("cuda", local)
     lam_s = g.zeros()
@@ -249,21 +285,38 @@ def run_ours(args):
         g.ipm_step(uhat, lam, None, sync=False)
     barrier()
     # timed region: K consecutive steps (Algorithm 1), device-timed with CUDA events
+    # inputs smaller than L2 (configs 1, 2, small windows): every step is timed on its own after an
+    # L2 flush (a write of twice the L2 size), and the step times are summed
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    state_bytes = g.cells * (g.Q * g.m + 2 * g.N * g.m) * 8
+    flush = state_bytes < 2 * l2
+    fbuf = torch.empty(2 * l2 // 4, dtype=torch.int32, device=dev) if flush else None
     dual_ms, flux_ms, iters = [], [], 0
+    ms = 0.0
     with ClockSampler(local) as clk:
         barrier()
-        e0.record(stream)
-        for _ in range(args.steps):
+        if not flush:
+            e0.record(stream)
+        for k in range(args.steps):
+            if flush:
+                fbuf.fill_(k)
+                e0.record(stream)
             info = g.ipm_step(uhat, lam, None, sync=True)
+            if flush:
+                e1.record(stream)
+                e1.synchronize()
+                ms += e0.elapsed_time(e1)
             iters += info.newton_iters
             d, f = g.last_kernel_ms()
             dual_ms.append(d)
             flux_ms.append(f)
-        e1.record(stream)
+        if not flush:
+            e1.record(stream)
         barrier()
-    ms = e0.elapsed_time(e1)
+    if not flush:
+        ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -324,7 +377,8 @@ def run_ours(args):
             "config": {"workload": args.config, "cells_per_gpu": g.cells, "N": N, "m": m, "Q": Q,
                        "newton": cfg["newton"], "tau": cfg["tau"],
                        "state": "seeded dual-solve stress state (SURVEY §8d), steps continue Algorithm 1",
-                       "l2": "inputs larger than L2 (node states %.1f GB)" % (g.cells * Q * m * 8 / 1e9),
+                       "l2": ("L2 flushed before every timed step (step state %.1f MB < 2x L2)" % (state_bytes / 1e6))
+                       if flush else "inputs larger than L2 (node states %.1f GB)" % (g.cells * Q * m * 8 / 1e9),
                        "parallelism": f"domain decomposition {px}x{py}, NCCL halo exchange" if world > 1
                        else "single", "global_cells": g.cells * world},
             "newton_iters_per_cell_step": iters / (g.cells * args.steps),
