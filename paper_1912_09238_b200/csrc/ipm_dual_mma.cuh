@@ -807,8 +807,14 @@ if constexpr (W == 1) {
         } else if constexpr (W == 2) {
           chol_ok = (wig == 0) ? D::template chol_solve<0>(Sx, npp, dd, nb, ctl, n, NBl, lane, bar)
                                : D::template chol_solve<1>(Sx, npp, dd, nb, ctl, n, NBl, lane, bar);
+        } else if constexpr (W == 3) {
+          switch (wig) {
+            case 0: chol_ok = D::template chol_solve<0>(Sx, npp, dd, nb, ctl, n, NBl, lane, bar); break;
+            case 1: chol_ok = D::template chol_solve<1>(Sx, npp, dd, nb, ctl, n, NBl, lane, bar); break;
+            default: chol_ok = D::template chol_solve<2>(Sx, npp, dd, nb, ctl, n, NBl, lane, bar); break;
+          }
         } else {
-          static_assert(W == 4, "W in {1, 2, 4}");
+          static_assert(W == 4, "W in {1, 2, 3, 4}");
           switch (wig) {
             case 0: chol_ok = D::template chol_solve<0>(Sx, npp, dd, nb, ctl, n, NBl, lane, bar); break;
             case 1: chol_ok = D::template chol_solve<1>(Sx, npp, dd, nb, ctl, n, NBl, lane, bar); break;
