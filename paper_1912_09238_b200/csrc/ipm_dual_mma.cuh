@@ -599,23 +599,43 @@ __global__ void __launch_bounds__(IPM_MMA_THREADS) k_dual_mma(DualParams P) {
       for (int ch = 0; ch < NCH; ++ch) {
         const int ab0 = ch * CHW;
         const int nab = (MM - ab0) < CHW ? (MM - ab0) : CHW;
-        // stage 1: T[k1][pr2][c] = sum_k2 LL[k2][pr2] J_{ab0+c}(k1, k2)
+        // stage 1: T[k1][pr2][c] = sum_k2 LL[k2][pr2] J_{ab0+c}(k1, k2), on the fp64 tensor path:
+        // rows (k1, c), columns pr2, contraction over k2 (zero-padded to whole 8 x 8 x 4 tiles)
+        {
+          const int rows = q1 * nab, MTs = (rows + 7) >> 3, KSs = (q1 + 3) >> 2;
+          constexpr int NTs = (NPR + 7) / 8;
+          const int lr = lane >> 2, lq = lane & 3;
 #pragma unroll 1
-        for (int e = t; e < q1 * nab; e += G) {
-          const int k1 = e / nab, c = e - k1 * nab;
-          double at[NPR];
+          for (int mt = wig; mt < MTs; mt += W) {
+            const int row = 8 * mt + lr;  // A-fragment row of this lane
+            const bool rok = row < rows;
+            const int k1a = rok ? row / nab : 0, ca = rok ? row - k1a * nab : 0;
+            const double* jrow = nb + (MS + ab0 + ca) * Q + k1a * q1;
+            double acc[NTs][2];
 #pragma unroll
-          for (int pr = 0; pr < NPR; ++pr) at[pr] = 0.0;
-          const double* jrow = nb + (MS + ab0 + c) * Q + k1 * q1;
-#pragma unroll 2
-          for (int k2 = 0; k2 < q1; ++k2) {
-            const double jv = jrow[k2];
-            const double* ll = sLL + k2 * NPR;
+            for (int nt = 0; nt < NTs; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+#pragma unroll 1
+            for (int ks = 0; ks < KSs; ++ks) {
+              const int k2 = 4 * ks + lq;  // A column / B row of this lane
+              const double av = (rok && k2 < q1) ? jrow[k2] : 0.0;
 #pragma unroll
-            for (int pr = 0; pr < NPR; ++pr) at[pr] = fma(ll[pr], jv, at[pr]);
+              for (int nt = 0; nt < NTs; ++nt) {
+                const int pr = 8 * nt + lr;
+                const double bv = (k2 < q1 && pr < NPR) ? sLL[k2 * NPR + pr] : 0.0;
+                dmma884(acc[nt][0], acc[nt][1], av, bv);
+              }
+            }
+            // C-fragment (row 8mt + lr, columns 8nt + 2lq + e) -> T[k1][pr2][c]
+            if (rok) {
+#pragma unroll
+              for (int nt = 0; nt < NTs; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                  const int pr = 8 * nt + 2 * lq + e;
+                  if (pr < NPR) Tt[(k1a * NPR + pr) * CHW + ca] = acc[nt][e];
+                }
+            }
           }
-#pragma unroll
-          for (int pr = 0; pr < NPR; ++pr) Tt[(k1 * NPR + pr) * CHW + c] = at[pr];
         }
         gsync();
         // stage 2: S[ab0+c][pair] = sum_k1 LL[k1][pr1] T[k1][pr2][c]

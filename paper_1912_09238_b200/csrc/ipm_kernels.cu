@@ -989,6 +989,7 @@ static int dual_mma_impl(const KernelCtx& k, const DualLaunch& a) {
   if (tab + pg > k.smem_optin) return -1;
   int groups = (int)((k.smem_optin - tab) / pg);
   groups = std::min(groups, std::min(512 / G, 15));  // named barriers 1..15 (0 = __syncthreads)
+  if (const char* ge = std::getenv("IPM_MMA_GROUPS")) groups = std::max(1, std::min(groups, std::atoi(ge)));  // experiments
   const size_t smem = tab + groups * pg;
   auto kern = k_dual_mma<CL, MS, NB, W, SF>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
