@@ -1,6 +1,7 @@
 """Print the main stall reasons and counters of one ncu report (first kernel)."""
 import csv, subprocess, sys
-out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+out = (open(sys.argv[1]).read() if sys.argv[1].endswith(".csv") else
+       subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True, text=True).stdout)
 rows = list(csv.reader(out.splitlines()))
 h, v = rows[0], rows[2]
 d = dict(zip(h, v))

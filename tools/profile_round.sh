@@ -11,4 +11,14 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_du
   python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/${tag}_ncu_dual.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_flux_cart -s 1 -c 1 -o gpurun_out/${tag}_flux \
   python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/${tag}_ncu_flux.log 2>&1
+
+# keep gpurun_out small (<= 64 MiB merge limit): export the pages we read, drop large reports
+for rep in gpurun_out/${tag}_dual gpurun_out/${tag}_flux gpurun_out/${tag}_big; do
+  if [ -f $rep.ncu-rep ]; then
+    ncu -i $rep.ncu-rep --page raw --csv > $rep.raw.csv 2>/dev/null
+    ncu -i $rep.ncu-rep --page source --csv --print-source cuda,sass > $rep.source.csv 2>/dev/null
+    gzip -f $rep.source.csv
+    sz=$(stat -c %s $rep.ncu-rep); if [ $sz -gt 20000000 ]; then rm -f $rep.ncu-rep; fi
+  fi
+done
 echo done > gpurun_out/${tag}_done
