@@ -549,7 +549,10 @@ struct RusNode {
 };
 
 template <int FX, int MS, int MK>
-__global__ void __launch_bounds__(256) k_flux_cart(FluxParams P) {
+#ifndef IPM_FLUX_MINB
+#define IPM_FLUX_MINB 2  // measured: 3 blocks per SM (80 registers, spills) is 14 % slower
+#endif
+__global__ void __launch_bounds__(256, IPM_FLUX_MINB) k_flux_cart(FluxParams P) {
   constexpr int CPW = 8 / MS;              // cells per warp (DMMA columns = CPW * MS <= 8)
   constexpr int F = (MK == MK_CART) ? 4 : 2;
   constexpr int ND = F / 2;                // directions
