@@ -180,6 +180,8 @@ def run_reference(args):
     else:
         full_cells = cfg["mesh"]["nx"] * cfg["mesh"].get("ny", 1)
         side = (128 if cfg["p"] <= 2 else 8) if cfg["mesh"]["kind"] == "cart2d" else min(cfg["mesh"]["nx"], 4096)
+        if args.nx:
+            side = min(side, args.nx)
         sample = configs.get(args.config, mesh=dict(nx=side, ny=side))
     ma = mesh_arrays(sample)
     o = oracle.Oracle(sample, ma)
