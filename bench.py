@@ -360,12 +360,13 @@ def run_ours(args):
     flops_ex = iters / args.steps * flops_executed_per_iteration(N, m, Q, cfg["p"], cfg["q1d"], kname) + \
         g.cells * flops_initial(N, m, Q)
     achieved_ex = flops_ex / (dual_avg / 1e3) / 1e12
-    traffic = None
-    if os.path.exists(NCU_SUMMARY):
+    traffic = traffic_flux = None
+    if os.path.exists(NCU_SUMMARY) and not args.nx:  # measured at the bench configuration only
         try:
-            traffic = json.load(open(NCU_SUMMARY)).get(args.config, {}).get("dual_dram_bytes_per_launch")
+            ent = json.load(open(NCU_SUMMARY)).get(args.config, {})
+            traffic, traffic_flux = ent.get("dual_dram_bytes_per_launch"), ent.get("flux_dram_bytes_per_launch")
         except Exception:
-            traffic = None
+            traffic = traffic_flux = None
     flux_avg = float(np.mean(flux_ms))
     hbm = json.load(open(MEASURED))["hbm_gbs"] if os.path.exists(MEASURED) else 6650.0
     flux_gbs = g.cells * flux_bytes_per_cell(N, m, Q) / (flux_avg / 1e3) / 1e9
@@ -393,7 +394,8 @@ def run_ours(args):
                          "traffic": traffic, "dual_ms_avg": dual_avg,
                          "share_of_step": dual_avg / (ms / args.steps)},
             "roofline_flux": {"bound": "hbm", "kernel": "k_flux_cart" if cfg["mesh"]["kind"] != "tri" else "k_flux_warp", "achieved": flux_gbs, "peak": hbm,
-                              "unit": "GB/s", "frac": flux_gbs / hbm, "flux_ms_avg": flux_avg},
+                              "unit": "GB/s", "frac": flux_gbs / hbm, "traffic": traffic_flux,
+                              "bytes_per_launch": g.cells * flux_bytes_per_cell(N, m, Q), "flux_ms_avg": flux_avg},
             "e2e": e2e,
             "gpu_launches": (4 if world == 1 else 6) * args.steps,
             "clocks": clk.summary(),
