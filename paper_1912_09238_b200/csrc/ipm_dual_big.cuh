@@ -119,10 +119,51 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
     return isfinite(v[0]) && isfinite(v[1]);
   };
   auto grad = [&](int Nl) -> double {
-    // two threads per output (halves of the node range, combined by a shuffle): a 1000-node dot
-    // product per output is a long latency chain
     const int n = Nl * MS;
     double part[4] = {0.0, 0.0, 0.0, 0.0};
+    if (HBS && ((Nl + 7) >> 3) <= 8) {
+      // on the fp64 tensor path: C[i][a] = sum_k (omega phi_i)(xi_k) u_a(xi_k), A = omega Phi^T in
+      // fragment order (Tables::WPhiF, L2), B = the node buffer's u; the node range is split over
+      // the warps and the partial C tiles are summed through shared memory (the Hessian blocks of
+      // the previous iteration are dead here)
+      constexpr int NWp = NT / 32;
+      const int MTg = (Nl + 7) >> 3, KS = P.T.KS;
+      const int rr = lane >> 2, qq = lane & 3;
+      double acc[8][2];
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+      for (int ks = wid; ks < KS; ks += NWp) {
+        const int k = 4 * ks + qq;
+        const double bv = (rr < MS && k < Q) ? nb[(size_t)k * NS + rr] : 0.0;
+        const double* af = P.T.WPhiF + (size_t)ks * 32 + lane;
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt)
+          if (mt < MTg) dmma884(acc[mt][0], acc[mt][1], af[(size_t)mt * KS * 32], bv);
+      }
+      double* red_c = Hb;  // [NWp][8][64]
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt)
+        if (mt < MTg)
+          *reinterpret_cast<double2*>(red_c + ((size_t)wid * 8 + mt) * 64 + 2 * lane) =
+              make_double2(acc[mt][0], acc[mt][1]);
+      __syncthreads();
+      for (int r = t; r < n; r += NT) {
+        const int i = r / MS, a = r - i * MS, mt = i >> 3;
+        const int off = mt * 64 + ((i & 7) * 4 + (a >> 1)) * 2 + (a & 1);
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < NWp; ++w) sum += red_c[(size_t)w * 8 * 64 + off];
+        const double gr = sum - uh[r];
+        g[r] = gr;
+        part[a] = fma(gr, gr, part[a]);
+      }
+      bsum(part, MS);
+      double crit = 0.0;
+      for (int a = 0; a < MS; ++a) crit += sqrt(part[a]);
+      return crit;
+    }
+    // two threads per output (halves of the node range, combined by a shuffle): a 1000-node dot
+    // product per output is a long latency chain
     const int Qh = (Q + 1) / 2;
     for (int base = 0; base < 2 * n; base += NT) {
       const int idx = base + t, r = idx >> 1, half = idx & 1;
@@ -392,8 +433,17 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
             for (int k1 = 0; k1 < q1; ++k1) {
               const double lv = sLL[k1 * npr + pr[0]];
               const double* tv = T2 + (((size_t)k1 * npr + pr[1]) * npr + pr[2]) * MM;
+              if constexpr (MM % 2 == 0) {  // rows of MM doubles start 16-byte aligned: vector loads
 #pragma unroll
-              for (int z = 0; z < MM; ++z) acc[z] = fma(lv, tv[z], acc[z]);
+                for (int z = 0; z < MM; z += 2) {
+                  const double2 v2 = *reinterpret_cast<const double2*>(tv + z);
+                  acc[z] = fma(lv, v2.x, acc[z]);
+                  acc[z + 1] = fma(lv, v2.y, acc[z + 1]);
+                }
+              } else {
+#pragma unroll
+                for (int z = 0; z < MM; ++z) acc[z] = fma(lv, tv[z], acc[z]);
+              }
             }
             hput(p, I, J, acc);
           }
