@@ -378,6 +378,71 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
           // sum factorisation over the tensor rule, k = (k1 q1 + k2) q1 + k3, LL[k][(a,b)] =
           // (w_k/2) L_a L_b (x_k):  T1 = sum_k3 LL J,  T2 = sum_k2 LL T1,  H = sum_k1 LL T2
           const int SF = (int)((sqrtf(8.0f * npr + 1.0f) - 1.0f) * 0.5f + 0.5f);
+          if (npr <= 24 && q1 <= 12) {
+            // stages 1 and 2 on the fp64 tensor path: both contract a 1D node index with LL, so the
+            // A operand LL^T[pr][k] (pr < 24, k < 12: 3 x 3 fragments) stays in registers
+            constexpr int NWp = NT / 32;
+            const int rr = lane >> 2, qq = lane & 3;
+            double lla[3][3];
+#pragma unroll
+            for (int mt = 0; mt < 3; ++mt)
+#pragma unroll
+              for (int ks = 0; ks < 3; ++ks) {
+                const int pr = 8 * mt + rr, k = 4 * ks + qq;
+                lla[mt][ks] = (pr < npr && k < q1) ? sLL[k * npr + pr] : 0.0;
+              }
+            // stage 1: per (k1 k2): T1[k12][pr3][ab] = sum_k3 LL[k3][pr3] J_ab(k12 q1 + k3)
+            for (int u = wid; u < q1 * q1 * 2; u += NWp) {
+              const int k12 = u >> 1, nt = u & 1, ab = 8 * nt + rr;
+              double bfr[3];
+#pragma unroll
+              for (int ks = 0; ks < 3; ++ks) {
+                const int k3 = 4 * ks + qq;
+                bfr[ks] = (k3 < q1 && ab < MM) ? nb[((size_t)k12 * q1 + k3) * NS + MS + ab] : 0.0;
+              }
+#pragma unroll
+              for (int mt = 0; mt < 3; ++mt) {
+                double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < 3; ++ks) dmma884(c0, c1, lla[mt][ks], bfr[ks]);
+                const int pr3 = 8 * mt + rr, abo = 8 * nt + 2 * qq;
+                if (pr3 < npr) {
+                  double* o = T1 + ((size_t)k12 * npr + pr3) * MM + abo;
+                  if (abo + 1 < MM)
+                    *reinterpret_cast<double2*>(o) = make_double2(c0, c1);
+                  else if (abo < MM)
+                    o[0] = c0;
+                }
+              }
+            }
+            __syncthreads();
+            // stage 2: per k1: T2[k1][pr2][col] = sum_k2 LL[k2][pr2] T1[k1 q1 + k2][col], col = pr3 MM + ab
+            const int ncol = npr * MM, ntl = (ncol + 7) >> 3;
+            for (int u = wid; u < q1 * ntl; u += NWp) {
+              const int k1 = u / ntl, nt = u - k1 * ntl, col = 8 * nt + rr;
+              double bfr[3];
+#pragma unroll
+              for (int ks = 0; ks < 3; ++ks) {
+                const int k2 = 4 * ks + qq;
+                bfr[ks] = (k2 < q1 && col < ncol) ? T1[((size_t)k1 * q1 + k2) * ncol + col] : 0.0;
+              }
+#pragma unroll
+              for (int mt = 0; mt < 3; ++mt) {
+                double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < 3; ++ks) dmma884(c0, c1, lla[mt][ks], bfr[ks]);
+                const int pr2 = 8 * mt + rr, co = 8 * nt + 2 * qq;
+                if (pr2 < npr) {
+                  double* o = T2 + ((size_t)k1 * npr + pr2) * ncol + co;
+                  if (co + 1 < ncol)
+                    *reinterpret_cast<double2*>(o) = make_double2(c0, c1);
+                  else if (co < ncol)
+                    o[0] = c0;
+                }
+              }
+            }
+            __syncthreads();
+          } else {
           for (int e = t; e < q1 * q1 * MM; e += NT) {
             const int k12 = e / MM, ab = e - k12 * MM;
             double at[32];
@@ -413,6 +478,7 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
               if (x < npr) T2[(((size_t)k1 * npr + x) * npr + pr3) * MM + ab] = at[x];
           }
           __syncthreads();
+          }
           for (int p = t; p < NPl; p += NT) {
             int I, J;
             blk_ij(p, I, J);
