@@ -162,6 +162,16 @@ def centres(cfg, ma):
     return cell_centres(cfg["mesh"], *(ma[:2] if ma is not None else (None, None)))
 
 
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def run_reference(args):
     """The reference arm of this tier: the CPU oracle, as it stands, on a bounded sample."""
     import oracle
@@ -197,7 +207,7 @@ def run_reference(args):
         w, it, _, _, _ = o.step(uhat, lam)
         iters += int(it.sum())
     dt = time.perf_counter() - t0
-    cores = os.cpu_count()
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     value = o.cells * steps / dt
     line = {
         "impl": "reference", "metric": "IPM cell-steps/s (= cell dual-solves/s)", "value": value,
@@ -206,6 +216,7 @@ def run_reference(args):
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config, "cells_full": full_cells, "sample_cells": o.cells},
         "cpu_baseline": {"value": value, "unit": "cell-steps/s", "cores": cores, "kind": "oracle",
+                         "cpu": cpu_model(),
                          "sample": f"{o.cells} cells of the {args.config} stress state, {steps} steps "
                                    f"({iters} Newton iterations), OpenMP over cells"},
         "e2e": {"value": value, "unit": "cell-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -325,6 +336,15 @@ def run_ours(args):
     ms = float(t.item())
     cells_total = g.cells * world
     value = cells_total * args.steps / (ms / 1e3)
+    # Newton-iteration balance across ranks (the scaling risk is the imbalance)
+    imbalance, iters_all = None, iters
+    if world > 1:
+        it_t = torch.tensor([float(iters)], device=dev, dtype=torch.float64)
+        it_max = it_t.clone()
+        dist.all_reduce(it_t, op=dist.ReduceOp.SUM)
+        dist.all_reduce(it_max, op=dist.ReduceOp.MAX)
+        iters_all = float(it_t.item())
+        imbalance = float(it_max.item()) / max(1e-30, iters_all / world)
 
     # end-to-end through the C-ABI with host buffers: H2D of the step inputs (uhat, lambda) from
     # pinned memory, ipm_step, D2H of the step result (uhat, lambda), every step
@@ -384,8 +404,9 @@ def run_ours(args):
                        if flush else "inputs larger than L2 (node states %.1f GB)" % (g.cells * Q * m * 8 / 1e9),
                        "parallelism": f"domain decomposition {px}x{py}, NCCL halo exchange" if world > 1
                        else "single", "global_cells": g.cells * world},
-            "newton_iters_per_cell_step": iters / (g.cells * args.steps),
-            "cell_newton_iters_per_s": iters * world / (ms / 1e3),
+            "newton_iters_per_cell_step": iters_all / (cells_total * args.steps),
+            "cell_newton_iters_per_s": iters_all / (ms / 1e3),
+            "newton_imbalance_max_over_mean": imbalance,
             "roofline": {"bound": "alu", "kernel": kname, "achieved": achieved,
                          "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
                          "flops": "algorithmic (SURVEY §8d: direct unique-entry Hessian, Cholesky n^3/3)",
