@@ -232,6 +232,18 @@ def cpu_baseline(args, cfg):
     return ref["cpu_baseline"]
 
 
+def _allreduce(t, op):
+    """all-reduce of a device tensor (staged through the host on gloo, the one-GPU functional test)"""
+    import torch.distributed as dist
+
+    if dist.get_backend() == "gloo" and t.is_cuda:
+        h = t.cpu()
+        dist.all_reduce(h, op=op)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=op)
+
+
 def decompose(world):
     """px x py block decomposition of the 2D grid (py >= px; rows of cells are contiguous in y)."""
     py = 1
@@ -258,9 +270,16 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("IPM_DIST_BACKEND", "nccl") != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # NCCL over NVLink; IPM_DIST_BACKEND=gloo runs the multi-rank path on one GPU (functional test)
+        backend = os.environ.get("IPM_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     cfg = workload(args)
     px, py = decompose(world)
     if world > 1 and cfg["mesh"]["kind"] == "cart2d":
@@ -332,7 +351,7 @@ def run_ours(args):
         ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], device=dev, dtype=torch.float64)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        _allreduce(t, dist.ReduceOp.MAX)
     ms = float(t.item())
     cells_total = g.cells * world
     value = cells_total * args.steps / (ms / 1e3)
@@ -341,8 +360,8 @@ def run_ours(args):
     if world > 1:
         it_t = torch.tensor([float(iters)], device=dev, dtype=torch.float64)
         it_max = it_t.clone()
-        dist.all_reduce(it_t, op=dist.ReduceOp.SUM)
-        dist.all_reduce(it_max, op=dist.ReduceOp.MAX)
+        _allreduce(it_t, dist.ReduceOp.SUM)
+        _allreduce(it_max, dist.ReduceOp.MAX)
         iters_all = float(it_t.item())
         imbalance = float(it_max.item()) / max(1e-30, iters_all / world)
 
@@ -367,7 +386,7 @@ def run_ours(args):
         ms_e = e0.elapsed_time(e1)
         te = torch.tensor([ms_e], device=dev, dtype=torch.float64)
         if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            _allreduce(te, dist.ReduceOp.MAX)
         nbytes = (uhat.numel() + lam.numel()) * 8
         e2e = {"value": cells_total * args.steps / (float(te.item()) / 1e3), "unit": "cell-steps/s",
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes}
@@ -402,7 +421,7 @@ def run_ours(args):
                        "state": "seeded dual-solve stress state (SURVEY §8d), steps continue Algorithm 1",
                        "l2": ("L2 flushed before every timed step (step state %.1f MB < 2x L2)" % (state_bytes / 1e6))
                        if flush else "inputs larger than L2 (node states %.1f GB)" % (g.cells * Q * m * 8 / 1e9),
-                       "parallelism": f"domain decomposition {px}x{py}, NCCL halo exchange" if world > 1
+                       "parallelism": f"domain decomposition {px}x{py}, {os.environ.get('IPM_DIST_BACKEND', 'nccl').upper()} halo exchange" if world > 1
                        else "single", "global_cells": g.cells * world},
             "newton_iters_per_cell_step": iters_all / (cells_total * args.steps),
             "cell_newton_iters_per_s": iters_all / (ms / 1e3),

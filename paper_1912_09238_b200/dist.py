@@ -15,7 +15,18 @@ import torch
 import torch.distributed as dist
 
 
+def _staged(t: torch.Tensor, group) -> bool:
+    """gloo has no point-to-point for device tensors: stage through host memory (functional tests of
+    the multi-rank path on one GPU; the production backend is NCCL)"""
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
 def halo_exchange(sendbuf: torch.Tensor, recvbuf: torch.Tensor, layout: dict, group=None) -> None:
+    if _staged(sendbuf, group):
+        rh = recvbuf.cpu()
+        halo_exchange(sendbuf.cpu(), rh, layout, group)
+        recvbuf.copy_(rh)
+        return
     ops = []
     s0 = r0 = 0
     for peer, ns, nr in zip(layout["peers"], layout["send_count"], layout["recv_count"]):
@@ -31,15 +42,21 @@ def halo_exchange(sendbuf: torch.Tensor, recvbuf: torch.Tensor, layout: dict, gr
 
 
 def allreduce_max_(t: torch.Tensor, group=None) -> None:
+    if _staged(t, group):
+        h = t.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.MAX, group=group)
+        t.copy_(h)
+        return
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
 
 
 def reduce_info_(info, device, group=None) -> None:
     """Global step statistics from the local ones (ctypes ipm_step_info, in place)."""
+    dev = "cpu" if dist.get_backend(group) == "gloo" else device
     v = torch.tensor([info.residual, float(info.newton_iters), float(info.failed_cells)], dtype=torch.float64,
-                     device=device)
+                     device=dev)
     dist.all_reduce(v, op=dist.ReduceOp.SUM, group=group)
-    w = torch.tensor([info.worst_status], dtype=torch.int64, device=device)
+    w = torch.tensor([info.worst_status], dtype=torch.int64, device=dev)
     dist.all_reduce(w, op=dist.ReduceOp.MAX, group=group)
     info.residual = float(v[0])
     info.newton_iters = int(v[1])
