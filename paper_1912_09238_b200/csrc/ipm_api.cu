@@ -429,6 +429,23 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   k.mesh.inv_dy = inv_dy;
   k.mesh.ghost = d_ghost;
   for (int t = 0; t < 4; ++t) k.mesh.bc_kind[t] = C.bc_kind[t];
+  k.mesh.bx = k.mesh.by = 0;
+  if (C.mesh_kind == IPM_MESH_CART2D && cells > 0) {
+    // row-major block structure of the (local) cells, as the strip flux kernel walks it: row 0 is
+    // cells 0..bx-1 (east links), every owned neighbour is the index arithmetic says
+    int64_t bx = 1;
+    while (bx < cells && nbr[(bx - 1) * 4 + 1] == (int32_t)bx) ++bx;
+    bool ok = cells % bx == 0;
+    for (int64_t j = 0; ok && j < cells; ++j) {
+      const int64_t x = j % bx, y = j / bx, by = cells / bx;
+      ok = (x == 0 || nbr[j * 4 + 0] == (int32_t)(j - 1)) && (x == bx - 1 || nbr[j * 4 + 1] == (int32_t)(j + 1)) &&
+           (y == 0 || nbr[j * 4 + 2] == (int32_t)(j - bx)) && (y == by - 1 || nbr[j * 4 + 3] == (int32_t)(j + bx));
+    }
+    if (ok && cells < ((int64_t)1 << 31)) {
+      k.mesh.bx = (int)bx;
+      k.mesh.by = (int)(cells / bx);
+    }
+  }
   k.nw = ipm::Newton{C.tau, C.armijo_c, C.max_newton, C.max_halvings, C.newton_mode};
   k.ad.n_levels = C.n_levels;
   for (int l = 0; l < C.n_levels; ++l) k.ad.Nl[l] = binom_total(p, C.level_M[l]);

@@ -795,9 +795,9 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
       for (int k = t; k < Q; k += NT) {
         const double* u = nb + (size_t)k * NS;
         if (A.uq) {
-          double* o = A.uq + (cell * Q + k) * MS;
+          double* o = A.uq + cell * Q * MS + k;  // [cell][state][node]
 #pragma unroll
-          for (int a = 0; a < MS; ++a) o[a] = u[a];
+          for (int a = 0; a < MS; ++a) o[a * Q] = u[a];
         }
         if (A.want_rate) my_rate = fmax(my_rate, node_rate<CL, MS>(u, P.mesh, cell, P.cl.gamma));
       }

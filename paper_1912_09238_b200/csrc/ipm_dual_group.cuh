@@ -635,9 +635,9 @@ __global__ void __launch_bounds__(IPM_GROUP_THREADS) k_dual_group(DualParams P) 
       for (int k = t; k < Q; k += G) {
         const double* u = nb + k * NS;
         if (A.uq) {
-          double* o = A.uq + (cell * Q + k) * MS;
+          double* o = A.uq + cell * Q * MS + k;  // [cell][state][node]
 #pragma unroll
-          for (int a = 0; a < MS; ++a) o[a] = u[a];
+          for (int a = 0; a < MS; ++a) o[a * Q] = u[a];
         }
         if (A.want_rate) my_rate = fmax(my_rate, node_rate<CL, MS>(u, P.mesh, cell, P.cl.gamma));
       }

@@ -914,9 +914,9 @@ if constexpr (W == 1) {
 #pragma unroll
         for (int a = 0; a < MS; ++a) u[a] = nb[a * Q + k];
         if (A.uq) {
-          double* o = A.uq + (cell * Q + k) * MS;
+          double* o = A.uq + cell * Q * MS + k;  // [cell][state][node]
 #pragma unroll
-          for (int a = 0; a < MS; ++a) o[a] = u[a];
+          for (int a = 0; a < MS; ++a) o[a * Q] = u[a];
         }
         if (A.want_rate) my_rate = fmax(my_rate, node_rate<CL, MS>(u, P.mesh, cell, P.cl.gamma));
       }

@@ -45,6 +45,7 @@ struct Mesh {
   double inv_dx, inv_dy;   // 1D / cartesian
   const double* ghost;     // [4][Q][m] STATE boundary node states
   int bc_kind[4];
+  int bx, by;  // cartesian: the cells form a row-major bx x by block (verified from nbr on the host), else 0
 };
 
 struct Newton {

@@ -355,9 +355,9 @@ __global__ void __launch_bounds__(512) k_dual_warp(DualParams P) {
       for (int k = lane; k < Q; k += 32) {
         const double* u = nb + k * Lay::NS;
         if (A.uq) {
-          double* o = A.uq + (cell * Q + k) * MS;
+          double* o = A.uq + cell * Q * MS + k;  // [cell][state][node]
 #pragma unroll
-          for (int a = 0; a < MS; ++a) o[a] = u[a];
+          for (int a = 0; a < MS; ++a) o[a * Q] = u[a];
         }
         if (A.want_rate) cr = fmax(cr, node_rate<CL, MS>(u, P.mesh, cell, P.cl.gamma));
       }
@@ -419,10 +419,10 @@ __global__ void __launch_bounds__(256) k_flux_warp(FluxParams P) {
   for (int64_t cell = (int64_t)blockIdx.x * nw + warp; cell < P.mesh.cells; cell += total_warps) {
     for (int k = lane; k < Q; k += 32) {
       double uj[MS], r[MS], gneg[MS];
-      const double* src = A.uq + (cell * Q + k) * MS;
+      const double* src = A.uq + cell * Q * MS + k;
 #pragma unroll
       for (int a = 0; a < MS; ++a) {
-        uj[a] = src[a];
+        uj[a] = src[a * Q];
         r[a] = 0.0;
       }
       for (int f = 0; f < F; ++f) {
@@ -437,9 +437,9 @@ __global__ void __launch_bounds__(256) k_flux_warp(FluxParams P) {
           nv[1] = (f >> 1) == 1 ? 1.0 : 0.0;
         }
         if (nbc >= 0) {
-          const double* s2 = A.uq + ((int64_t)nbc * Q + k) * MS;
+          const double* s2 = A.uq + (int64_t)nbc * Q * MS + k;
 #pragma unroll
-          for (int a = 0; a < MS; ++a) un[a] = s2[a];
+          for (int a = 0; a < MS; ++a) un[a] = s2[a * Q];
         } else {
           const int tag = -1 - nbc;
           const int kind = P.mesh.bc_kind[tag];
@@ -580,10 +580,10 @@ __global__ void __launch_bounds__(256, IPM_FLUX_MINB) k_flux_cart(FluxParams P) 
       const int64_t cell = cell0 + c;
       if (cell >= cells) continue;
       double uj[MS], r[MS];
-      const double* src = A.uq + (cell * Q + k) * MS;
+      const double* src = A.uq + cell * Q * MS + k;
 #pragma unroll
       for (int a = 0; a < MS; ++a) {
-        uj[a] = src[a];
+        uj[a] = src[a * Q];
         r[a] = 0.0;
       }
       // all neighbour node states first: their loads are independent and overlap
@@ -592,9 +592,9 @@ __global__ void __launch_bounds__(256, IPM_FLUX_MINB) k_flux_cart(FluxParams P) 
       for (int f = 0; f < F; ++f) {
         const int nbc = P.mesh.nbr[cell * F + f];
         if (nbc >= 0) {
-          const double* s2 = A.uq + ((int64_t)nbc * Q + k) * MS;
+          const double* s2 = A.uq + (int64_t)nbc * Q * MS + k;
 #pragma unroll
-          for (int a = 0; a < MS; ++a) un[f][a] = s2[a];
+          for (int a = 0; a < MS; ++a) un[f][a] = s2[a * Q];
         } else {
           const int tag = -1 - nbc;
           const int kind = P.mesh.bc_kind[tag];
@@ -696,6 +696,8 @@ __global__ void __launch_bounds__(256, IPM_FLUX_MINB) k_flux_cart(FluxParams P) 
   my_res = warp_sum(my_res);
   if (lane == 0 && my_res != 0.0) atomicAdd(&P.sc->residual, my_res);
 }
+
+#include "ipm_flux_strip.cuh"
 
 // ------------------------------------------------------------------------------------------------
 // small kernels
@@ -828,9 +830,9 @@ __global__ void k_nodes(Tables T, Mesh mesh, ClParams cp, const double* __restri
     for (int k = lane; k < Q; k += 32) {
       const double* u = nb + k * Lay::NS;
       if (uq) {
-        double* o = uq + (cell * Q + k) * MS;
+        double* o = uq + cell * Q * MS + k;  // [cell][state][node]
 #pragma unroll
-        for (int a = 0; a < MS; ++a) o[a] = u[a];
+        for (int a = 0; a < MS; ++a) o[a * Q] = u[a];
       }
       if (want_rate) my_rate = fmax(my_rate, node_rate<CL, MS>(u, mesh, cell, cp.gamma));
     }
@@ -1151,10 +1153,40 @@ static int flux_cart_impl(const KernelCtx& k, const FluxLaunch& a) {
   return (int)cudaGetLastError();
 }
 
+#ifndef IPM_STRIP_TX
+#define IPM_STRIP_TX 8
+#endif
+// strip kernel (row-major cartesian block, Euler 2D Rusanov, Q = QC): -1 when not applicable
+template <int TX, int NT, int MINB, int QC>
+static int flux_strip_impl(const KernelCtx& k, const FluxLaunch& a) {
+  if (k.mesh.kind != MK_CART || k.m != 4 || k.flux != FX_RUSANOV || k.mesh.bx <= 0 || k.T.Q != QC) return -1;
+  const strip::Layout<TX, QC> lay(k.T.MT, k.T.N * 4);
+  const size_t smem = lay.total * 8;
+  if (smem > k.smem_optin) return -1;
+  auto kern = k_flux_strip<TX, NT, MINB, QC>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t rows = (int64_t)((k.mesh.bx + TX - 1) / TX) * k.mesh.by;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(rows, (int64_t)k.sm_count * per_sm));
+  FluxParams P{k.T, k.mesh, k.cl, k.ad, a, k.sc, 1};
+  kern<<<grid, NT, smem, S(k)>>>(P);
+  return (int)cudaGetLastError();
+}
+
 int launch_flux(const KernelCtx& k, const FluxLaunch& a) {
   if (k.mesh.cells == 0) return 0;
   const int key = (k.flux * 10 + k.m) * 10 + k.mesh.kind;
   const char* fk = std::getenv("IPM_FLUX_KERNEL");
+  if (!fk || std::string(fk) == "strip") {
+#if IPM_STRIP_TX == 4
+    const int rc = flux_strip_impl<4, 320, 2, 100>(k, a);
+#else
+    const int rc = flux_strip_impl<8, 512, 1, 100>(k, a);
+#endif
+    if (rc != -1) return rc;
+  }
   if (!(fk && std::string(fk) == "warp")) {
     int rc = -1;
     switch (key) {
