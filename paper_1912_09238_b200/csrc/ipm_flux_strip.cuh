@@ -3,20 +3,23 @@
 //
 // What it computes is k_flux_cart's a11 + projection (PAPER.md:130 difference form per direction,
 // PAPER.md:182-185 update forms), with every node's Rusanov ingredients formed ONCE and every face
-// flux formed once per node (y faces) or twice (x faces, by both cells) instead of five ingredient
-// evaluations and four faces per node:
-//   * a CTA owns a strip of TX cell columns and walks its rows y = ya..yb-1 (a contiguous share of
-//     all strip rows, so every CTA gets the same number of rows);
-//   * the node states of the TX cells of a row plus the two x-halo cells are copied into a 3-row
-//     shared-memory ring with cp.async two rows ahead (every cell's Q x m block is contiguous);
-//   * thread items (column j, node k), two per thread, fixed for the whole walk: the item carries the
-//     ingredients (1/rho, p, c) of its current row and the y-face flux g_{y-1/2} from the previous
-//     row, forms the next row's ingredients and g_{y+1/2}, publishes (F_x, s_x) of its current node
-//     for the x neighbours, and then r = (g_E - g_W)/dx + (g_N - g_S)/dy;
-//   * the projection Phi^T(omega o r) of the row's TX cells is a set of DMMAs with A = r^T (rows =
-//     (cell, state), K = nodes; written conflict-free by the items) and B = the WPhiF fragments.
-// Boundary states (ghost / slip wall / outflow copy) follow k_flux_cart exactly; x-halo boundary
-// states are materialised in the ring's halo column by the halo threads.
+// flux formed ONCE (k_flux_cart forms five ingredient sets and four faces per node):
+//   * a CTA owns a strip of TX = 8 cell columns and walks its rows y = ya..yb-1 (a contiguous share
+//     of all strip rows, so every CTA gets the same number of rows);
+//   * the node states of the row's 8 cells and its two x-halo cells are TMA bulk copies (one per
+//     cell: the node states are stored [cell][state][node]) into a 4-row shared-memory ring, three
+//     rows ahead, completing on an mbarrier;
+//   * compute warps: lane = (column c, node kk of a group of 4); each thread holds two node groups
+//     for the whole walk and carries, per item, the current node state, its ingredients (1/rho, p,
+//     c) and the y-face flux g_{y-1/2}; it forms the next row's ingredients and g_{y+1/2}, the east
+//     x face from its east neighbour's (u, F_x, s_x) by warp shuffles, the west one by a shuffle of
+//     that face (the strip's edge columns take the halo ingredients from shared memory), and then
+//     r = (g_E - g_W)/dx + (g_N - g_S)/dy;
+//   * halo warps form the x-halo ingredients of the next row (boundary states: ghost / slip wall /
+//     outflow copy, k_flux_cart's rules); the last NPW warps (one per SM sub-partition) project the
+//     previous row, Phi^T(omega o r), on DMMA with A = r^T (rows (cell, state), K = nodes) and
+//     B = the WPhiF fragments, and write the update;
+//   * one CTA barrier per row.
 
 #ifndef IPM_FLUX_STRIP_CUH
 #define IPM_FLUX_STRIP_CUH
@@ -81,17 +84,17 @@ template <int TX, int QC>
 struct Layout {
   static constexpr int NC = TX + 2;  // ring columns: west halo, TX owned, east halo
   static constexpr int CT = TX / 2;  // DMMA row tiles of r^T (8 rows = 2 cells x 4 states)
-  static constexpr int QM = QC * 4, KS = (QC + 3) / 4, KP = kp(KS), RB = CT * 8 * KP;
-  int MT, NM, RS;
-  size_t a, ring, row, xs, rb, idx, bar, total;  // offsets in doubles
-  // per ring row besides the node states: uhat_old of the TX cells [TX][NM]
-  __host__ __device__ Layout(int MT_, int NM_) : MT(MT_), NM(NM_), RS(TX * NM_) {
+  // ring column stride: 4 Q doubles + padding so that 4 columns x 4 nodes fall into distinct banks
+  static constexpr int QMP = 4 * QC + ((4 - (4 * QC) % 16) + 16) % 16;
+  static constexpr int KS = (QC + 3) / 4, KP = kp(KS), RB = CT * 8 * KP, HXS = 2 * 4 * QC;
+  int MT;
+  size_t a, ring, hx, rb, idx, bar, total;  // offsets in doubles
+  __host__ __device__ Layout(int MT_, int) : MT(MT_) {
     a = 0;
     ring = a + (size_t)MT * KS * 32;
-    row = ring + (size_t)4 * NC * QM;
-    xs = row + (size_t)5 * RS;
-    rb = xs + (((size_t)NC * 5 * QC + 1) & ~(size_t)1);
-    idx = rb + (size_t)RB;
+    hx = ring + (size_t)4 * NC * QMP;
+    rb = hx + (size_t)2 * HXS;
+    idx = rb + (size_t)2 * RB;
     bar = idx + (8 * NC + 1) / 2;
     total = bar + 4;
   }
@@ -130,9 +133,8 @@ __device__ __forceinline__ void ld4(const double* p, double* u) {
 }  // namespace strip
 
 #ifdef IPM_STRIP_PROF
-__device__ int g_strip_prof_done = 0;
 #define STRIP_STAMP(n) \
-  if (prof && lane == 0 && it >= 20 && it < 24) st[(it - 20) * 4 + (n)] = clock64();
+  if (blockIdx.x == 0 && lane == 0 && it >= 20 && it < 24) st[(it - 20) * 4 + (n)] = clock64();
 #else
 #define STRIP_STAMP(n)
 #endif
@@ -140,23 +142,19 @@ __device__ int g_strip_prof_done = 0;
 template <int TX, int NT, int MINB, int QC>
 __global__ void __launch_bounds__(NT, MINB) k_flux_strip(FluxParams P) {
   using L = strip::Layout<TX, QC>;
-  constexpr int NC = L::NC, CT = L::CT, QM = L::QM, KS = L::KS, KP = L::KP, RB = L::RB;
-  constexpr int Q = QC, OT = TX * QC / 2;  // owned-item threads (2 items each); [OT, OT+Q): x-halo items
-  constexpr int NW = NT / 32, PW0 = (OT + 31) / 32;  // warps [PW0, NW) hold no owned items
-#ifndef IPM_STRIP_NPW
-#define IPM_STRIP_NPW 4
-#endif
-  constexpr int NPW = IPM_STRIP_NPW;  // projection warps: the last NPW, one per SM sub-partition (DMMA pipe)
-  static_assert(OT + QC <= NT && PW0 - 1 <= NW - NPW && CT % NPW == 0, "strip kernel: not enough threads");
+  constexpr int NC = L::NC, CT = L::CT, QMP = L::QMP, KS = L::KS, KP = L::KP, RB = L::RB, HXS = L::HXS;
+  constexpr int Q = QC, G = (QC + 3) / 4;  // node groups of 4 (one per 4 lanes x 8 columns warp slot)
+  constexpr int CW = (G + 1) / 2;          // compute warps, two node groups each
+  constexpr int NW = NT / 32, HT0 = CW * 32, NTH = NT - HT0;  // halo threads [HT0, NT)
+  constexpr int NPW = 4;                                       // projection warps: the last NPW
+  static_assert(TX == 8 && NTH >= 32 && CW <= NW - 1 && CT % NPW == 0, "strip kernel geometry");
   extern __shared__ __align__(16) double sm[];
   const int N = P.T.N, MT = P.T.MT, nmax = N * 4;
   const L lay(MT, nmax);
-  const int RS = lay.RS;
   double* sA = sm + lay.a;
-  double* ring = sm + lay.ring;  // [4 rows][NC][4][Q] (node states are stored [cell][state][node])
-  double* rowd = sm + lay.row;   // [5 rows][TX][nmax] uhat_old
-  double* XS = sm + lay.xs;      // [NC][5][Q]: F_x, s_x of the current row
-  double* rbT = sm + lay.rb;     // [CT][8][KP]: r^T of the current row
+  double* ring = sm + lay.ring;  // [4 rows][NC][4][Q] (+pad): node states of the row's cells
+  double* HX = sm + lay.hx;      // [2 rows][2 sides][4][Q]: x fluxes at the strip's west / east faces
+  double* rbT = sm + lay.rb;     // [2 rows][CT][8][KP]: r^T
   int* sidx = reinterpret_cast<int*>(sm + lay.idx);  // [8 rows][NC] cell codes
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(sm + lay.bar);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -166,7 +164,7 @@ __global__ void __launch_bounds__(NT, MINB) k_flux_strip(FluxParams P) {
   }
   unsigned rows_done = 0;  // ring rows issued by this CTA before the current segment (mbarrier phases)
   for (int x = tid; x < MT * KS * 32; x += NT) sA[x] = P.T.WPhiF[x];
-  for (int x = tid; x < RB; x += NT) rbT[x] = 0.0;  // K padding (k >= Q) stays 0
+  for (int x = tid; x < 2 * RB; x += NT) rbT[x] = 0.0;  // K padding (k >= Q) stays 0
   __syncthreads();
 
   const int bx = P.mesh.bx, by = P.mesh.by;
@@ -180,20 +178,21 @@ __global__ void __launch_bounds__(NT, MINB) k_flux_strip(FluxParams P) {
   const bool cform = A.update_form == 1;
   double my_res = 0.0;
 
-  // fixed per-thread item offsets (ring row, XS, r^T)
-  int jj[2], ro[2], xo[2], bo[2];
+  // compute-warp items: column c, node k = 4 (2 warp + sl) + kk
+  const int c = lane >> 2;
+  int kq[2];  // node, clamped to a valid one for idle items (they only feed shuffles)
+  bool kv[2];
 #pragma unroll
   for (int sl = 0; sl < 2; ++sl) {
-    const int i = tid + sl * OT, j = i / Q, k = i - j * Q;
-    jj[sl] = tid < OT ? j : TX;
-    ro[sl] = (j + 1) * QM + k;
-    xo[sl] = (j + 1) * 5 * Q + k;
-    bo[sl] = (j >> 1) * 8 * KP + (j & 1) * 4 * KP + k;
+    const int k = 4 * (2 * warp + sl) + (lane & 3);
+    kv[sl] = warp < CW && k < Q;
+    kq[sl] = k < Q ? k : Q - 1;
   }
-  const int hk = tid - OT;  // halo node
+  // r^T rows of tile ct = c/2: (cell c&1, state a) -> row 4 (c&1) + ((a + ct) & 3), so that the 8
+  // columns' stores of one state fall into 4 distinct bank groups
+  const int bo = (c >> 1) * 8 * KP + (c & 1) * 4 * KP;
 #ifdef IPM_STRIP_PROF
   long long st[16];
-  const bool prof = blockIdx.x == 0 && g_strip_prof_done == 0;
   bool first_seg = true;
 #endif
 
@@ -220,95 +219,72 @@ __global__ void __launch_bounds__(NT, MINB) k_flux_strip(FluxParams P) {
       if (y < 0) return nbr[(int64_t)x * 4 + 2];
       return nbr[((int64_t)(by - 1) * bx + x) * 4 + 3];
     };
-    // one thread: TMA bulk copies of ring row it (node states of its cells, uhat_old of owned rows)
+    // one thread: TMA bulk copies of ring row it (node states of its cells)
     auto issue_row = [&](int it) {
       const int* code = sidx + (it & 7) * NC;
-      double* dst = ring + (it & 3) * NC * QM;
+      double* dst = ring + (it & 3) * NC * QMP;
       unsigned long long* bar = mbar + ((rows_done + it) & 3);
-      const int yr = ya - 1 + it;
-      const bool owned = yr >= ya && yr < yb;
-      unsigned bytes = owned ? (unsigned)(tw * nmax * 8) : 0u;
+      unsigned bytes = 0;
       for (int col = 0; col < NC; ++col)
-        if (code[col] >= 0) bytes += QM * 8;
-      strip::fence_proxy_async();  // generic writes into the ring (boundary states) before the async ones
+        if (code[col] >= 0) bytes += 4 * Q * 8;
       strip::mbar_expect_tx(bar, bytes);
       for (int col = 0; col < NC; ++col)
-        if (code[col] >= 0) strip::bulk_g2s(dst + col * QM, A.uq + (int64_t)code[col] * QM, QM * 8, bar);
-      if (owned)
-        strip::bulk_g2s(rowd + (it % 5) * RS, A.uhat_old + ((int64_t)yr * bx + x0) * nmax, (unsigned)(tw * nmax * 8),
-                        bar);
+        if (code[col] >= 0) strip::bulk_g2s(dst + col * QMP, A.uq + (int64_t)code[col] * 4 * Q, 4 * Q * 8, bar);
     };
     auto wait_row = [&](int it) {
       const unsigned gi = rows_done + it;
       strip::mbar_wait(mbar + (gi & 3), (gi >> 2) & 1);
     };
-    // projection C^T = r^T (omega Phi^T) on DMMA (two accumulator chains) and the update of ring row
-    // itp's cells (projection warps)
-    // projection warps: the last NPW warps; for MT == 2 each holds CT/NPW column tiles x both row tiles
-    // of C^T in registers, so every A fragment (r^T) and B fragment (omega Phi) is loaded once per k step
+    // projection of ring row itp: C^T = r^T (omega Phi^T) on DMMA, then the update of its cells
     auto project = [&](int itp) {
       const int y = ya - 1 + itp;
-      const double* rd = rowd + (itp % 5) * RS;
+      const double* rb = rbT + (itp & 1) * RB;
       const int rr = lane >> 2, q = lane & 3, pw = warp - (NW - NPW);
-      auto epilogue = [&](int mt, int ct, double c0, double c1) {
-        const int cl = ct * 2 + (rr >> 2), av = rr & 3;
-        if (cl >= tw) return;
+      for (int ct = pw; ct < CT; ct += NPW) {
+        const int av = (rr - ct) & 3;
+        const int cl = ct * 2 + (rr >> 2);
+        const bool cv_ = cl < tw;
         const int64_t cell = (int64_t)y * bx + x0 + cl;
-        const int Nnew = (P.ad.n_levels > 0 && A.level_new) ? P.ad.Nl[A.level_new[cell]] : N;
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int i = 8 * mt + 2 * q + e;
-          if (i >= N) continue;
-          const int64_t idx = cell * nmax + i * 4 + av;
-          const double old = rd[cl * nmax + i * 4 + av];
-          const double cv = e == 0 ? c0 : c1;
-          double out = 0.0;
-          if (i < Nnew) out = cform ? cv : old - dt * cv;
-          A.uhat_new[idx] = out;
-          if (i == 0 && av == 0) my_res += P.mesh.area[cell] * fabs(out - old);
-          if (A.lam && i >= Nnew) A.lam[idx] = 0.0;
-        }
-      };
-      if (MT == 2) {
-        constexpr int NCT = CT / NPW;
-        double acc[2][NCT][2];
-#pragma unroll
-        for (int m = 0; m < 2; ++m)
-#pragma unroll
-          for (int c = 0; c < NCT; ++c) acc[m][c][0] = acc[m][c][1] = 0.0;
-        const double* a = rbT + rr * KP + q;
-        const double* b = sA + lane;
-#pragma unroll 3
-        for (int ks = 0; ks < KS; ++ks) {
-          double bf[2], af[NCT];
-#pragma unroll
-          for (int m = 0; m < 2; ++m) bf[m] = b[(m * KS + ks) * 32];
-#pragma unroll
-          for (int c = 0; c < NCT; ++c) af[c] = a[(pw + c * NPW) * 8 * KP + ks * 4];
+        const double area = (cv_ && q == 0 && av == 0) ? P.mesh.area[cell] : 0.0;
+        const int Nnew = (cv_ && P.ad.n_levels > 0 && A.level_new) ? P.ad.Nl[A.level_new[cell]] : N;
+        for (int mt0 = 0; mt0 < MT; mt0 += 2) {
+          const bool two = mt0 + 1 < MT;
+          double old[2][2];
 #pragma unroll
           for (int m = 0; m < 2; ++m)
 #pragma unroll
-            for (int c = 0; c < NCT; ++c)
-              asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                           : "+d"(acc[m][c][0]), "+d"(acc[m][c][1])
-                           : "d"(af[c]), "d"(bf[m]));
-        }
-#pragma unroll
-        for (int m = 0; m < 2; ++m)
-#pragma unroll
-          for (int c = 0; c < NCT; ++c) epilogue(m, pw + c * NPW, acc[m][c][0], acc[m][c][1]);
-      } else {
-        for (int tile = pw; tile < MT * CT; tile += NPW) {
-          const int mt = tile / CT, ct = tile - mt * CT;
-          double c0 = 0.0, c1 = 0.0;
-          const double* a = rbT + ct * 8 * KP + rr * KP + q;
-          const double* b = sA + mt * KS * 32 + lane;
+            for (int e = 0; e < 2; ++e) {
+              const int i = 8 * (mt0 + m) + 2 * q + e;
+              old[m][e] = (cv_ && i < N) ? A.uhat_old[cell * nmax + i * 4 + av] : 0.0;
+            }
+          double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+          const double* a = rb + ct * 8 * KP + rr * KP + q;
+          const double* b = sA + mt0 * KS * 32 + lane;
 #pragma unroll 5
-          for (int ks = 0; ks < KS; ++ks)
+          for (int ks = 0; ks < KS; ++ks) {
+            const double af = a[ks * 4];
             asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                         : "+d"(c0), "+d"(c1)
-                         : "d"(a[ks * 4]), "d"(b[ks * 32]));
-          epilogue(mt, ct, c0, c1);
+                         : "+d"(acc[0][0]), "+d"(acc[0][1])
+                         : "d"(af), "d"(b[ks * 32]));
+            if (two)
+              asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                           : "+d"(acc[1][0]), "+d"(acc[1][1])
+                           : "d"(af), "d"(b[(KS + ks) * 32]));
+          }
+          if (!cv_) continue;
+#pragma unroll
+          for (int m = 0; m < 2; ++m)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int i = 8 * (mt0 + m) + 2 * q + e;
+              if (i >= N) continue;
+              const int64_t idx = cell * nmax + i * 4 + av;
+              double out = 0.0;
+              if (i < Nnew) out = cform ? acc[m][e] : old[m][e] - dt * acc[m][e];
+              A.uhat_new[idx] = out;
+              if (i == 0 && av == 0) my_res += area * fabs(out - old[m][e]);
+              if (A.lam && i >= Nnew) A.lam[idx] = 0.0;
+            }
         }
       }
     };
@@ -322,14 +298,17 @@ __global__ void __launch_bounds__(NT, MINB) k_flux_strip(FluxParams P) {
     if (tid == NT - 1)
       for (int it = 0; it < 3 && it < LR; ++it) issue_row(it);
 
-    // per-item carried state (two items per owned thread)
-    double cir[2], cp[2], cc_[2], gS[2][4];
-    const int hro = (tw + 1) * QM + hk, hxo = (tw + 1) * 5 * Q + hk;
+    // per-item carried state: node state, its ingredients, the south face flux
+    double cu[2][4], cir[2], cp[2], cc_[2], gS[2][4];
+    bool act[2];
+#pragma unroll
+    for (int sl = 0; sl < 2; ++sl) act[sl] = kv[sl] && c < tw;
+    const int ro0 = ((c < tw ? c : tw - 1) + 1) * QMP;  // idle columns read the last owned one
 
     for (int it = 0; it + 1 < LR; ++it) {
       if (it == 0) wait_row(0);
       wait_row(it + 1);
-      __syncthreads();  // rows <= it+1 in the ring; F2 of row it-1 done (r^T, XS free)
+      __syncthreads();  // rows <= it+1 in the ring; halo of row it in HX; r^T of row it-1 complete
       STRIP_STAMP(0)
       if (tid == NT - 1 && it + 3 < LR) issue_row(it + 3);
       if (tid < NC && it + 4 < LR) {
@@ -338,172 +317,134 @@ __global__ void __launch_bounds__(NT, MINB) k_flux_strip(FluxParams P) {
       }
       const int* codeC = sidx + (it & 7) * NC;
       const int* codeN = sidx + ((it + 1) & 7) * NC;
-      double* rC = ring + (it & 3) * NC * QM;
-      const double* rN = ring + ((it + 1) & 3) * NC * QM;
+      const double* rC = ring + (it & 3) * NC * QMP;
+      const double* rN = ring + ((it + 1) & 3) * NC * QMP;
       const bool own_row = it > 0;
       const bool general = it == 0 || it + 2 == LR;  // rows that may hold boundary states
 
-      // ---- phase 1: next-row ingredients, y face, x ingredients | x halo | projection of row it-1 ----
-      double nir[2], np[2], nc[2], gN[2][4];
-      if (tid < OT) {
+      if (warp < CW) {
+        const double* hxr = HX + (it & 1) * HXS;  // strip-edge x fluxes of the current row
+        double* rb = rbT + (it & 1) * RB;
+        double un[2][4];
         if (!general) {
 #pragma unroll
-          for (int sl = 0; sl < 2; ++sl) {
-            double cu[4], un[4];
-            strip::ld4<Q>(rC + ro[sl], cu);
-            strip::ld4<Q>(rN + ro[sl], un);
-            RusNode<4> ncur, nnx;
-            ncur.irho = cir[sl];
-            ncur.p = cp[sl];
-            ncur.c = cc_[sl];
-            nnx.init(un, gam);
-            nir[sl] = nnx.irho;
-            np[sl] = nnx.p;
-            nc[sl] = nnx.c;
-            double fc[4], fn[4], sc, sn, fx[4], sx;
-            ncur.flux(cu, 1, fc, sc);
-            nnx.flux(un, 1, fn, sn);
-            strip::face(fc, sc, cu, fn, sn, un, gN[sl]);
-            ncur.flux(cu, 0, fx, sx);
-            if (jj[sl] < tw) {
-              double* xs = XS + xo[sl];
-#pragma unroll
-              for (int a = 0; a < 4; ++a) xs[a * Q] = fx[a];
-              xs[4 * Q] = sx;
-            }
-          }
+          for (int sl = 0; sl < 2; ++sl) strip::ld4<Q>(rN + ro0 + kq[sl], un[sl]);
         } else {
 #pragma unroll
           for (int sl = 0; sl < 2; ++sl) {
-            if (jj[sl] >= tw) continue;
-            const int col = jj[sl] + 1, k = ro[sl] - col * QM;
-            double cu[4], un[4];
-            if (codeC[col] >= 0) {
-              strip::ld4<Q>(rC + ro[sl], cu);
-            } else {  // current row is the south boundary row
-              double ur[4];
-              strip::ld4<Q>(rN + ro[sl], ur);
-              strip::bstate(P, codeC[col], 2, k, ur, cu);
-            }
-            if (!own_row) {
+            const int k = kq[sl];
+            if (it == 0) {
+              if (act[sl]) {
+                if (codeC[c + 1] >= 0) {
+                  strip::ld4<Q>(rC + ro0 + k, cu[sl]);
+                } else {  // the current row is the south boundary row
+                  double ur[4];
+                  strip::ld4<Q>(rN + ro0 + k, ur);
+                  strip::bstate(P, codeC[c + 1], 2, k, ur, cu[sl]);
+                }
+              } else {
+#pragma unroll
+                for (int a = 0; a < 4; ++a) cu[sl][a] = a == 0 ? 1.0 : (a == 3 ? 2.5 : 0.0);
+              }
               RusNode<4> n0;
-              n0.init(cu, gam);
+              n0.init(cu[sl], gam);
               cir[sl] = n0.irho;
               cp[sl] = n0.p;
               cc_[sl] = n0.c;
             }
-            if (codeN[col] >= 0)
-              strip::ld4<Q>(rN + ro[sl], un);
+            if (act[sl] && codeN[c + 1] < 0)
+              strip::bstate(P, codeN[c + 1], 3, k, cu[sl], un[sl]);
             else
-              strip::bstate(P, codeN[col], 3, k, cu, un);
-            RusNode<4> ncur, nnx;
-            ncur.irho = cir[sl];
-            ncur.p = cp[sl];
-            ncur.c = cc_[sl];
-            nnx.init(un, gam);
-            nir[sl] = nnx.irho;
-            np[sl] = nnx.p;
-            nc[sl] = nnx.c;
-            double fc[4], fn[4], sc, sn;
-            ncur.flux(cu, 1, fc, sc);
-            nnx.flux(un, 1, fn, sn);
-            strip::face(fc, sc, cu, fn, sn, un, gN[sl]);
-            if (own_row) {
-              double fx[4], sx;
-              ncur.flux(cu, 0, fx, sx);
-              double* xs = XS + xo[sl];
-#pragma unroll
-              for (int a = 0; a < 4; ++a) xs[a * Q] = fx[a];
-              xs[4 * Q] = sx;
-            }
+              strip::ld4<Q>(rN + ro0 + k, un[sl]);
           }
         }
-      } else {
-        if (tid < OT + Q && own_row) {
-#pragma unroll
-          for (int side = 0; side < 2; ++side) {
-            const int col = side ? tw + 1 : 0;
-            double* up = rC + (side ? hro : hk);
-            double u[4];
-            if (codeC[col] >= 0) {
-              strip::ld4<Q>(up, u);
-            } else {
-              double ur[4];
-              strip::ld4<Q>(up + (side ? -QM : QM), ur);
-              strip::bstate(P, codeC[col], side, hk, ur, u);
-#pragma unroll
-              for (int a = 0; a < 4; ++a) up[a * Q] = u[a];
-            }
-            RusNode<4> h;
-            h.init(u, gam);
-            double fx[4], sx;
-            h.flux(u, 0, fx, sx);
-            double* xs = XS + (side ? hxo : hk);
-#pragma unroll
-            for (int a = 0; a < 4; ++a) xs[a * Q] = fx[a];
-            xs[4 * Q] = sx;
-          }
-        }
-      }
-#ifndef IPM_STRIP_NOPROJ
-      if (warp >= NW - NPW && it >= 2) project(it - 1);
-#endif
-      STRIP_STAMP(1)
-      __syncthreads();
-      STRIP_STAMP(2)
-
-      // ---- phase 2: x faces, the residual r and r^T (owned items) ------------------------------------
-      if (tid < OT) {
 #pragma unroll
         for (int sl = 0; sl < 2; ++sl) {
-#ifdef IPM_STRIP_NOF2
-          if (false) {
-#else
+          RusNode<4> ncur, nnx;
+          ncur.irho = cir[sl];
+          ncur.p = cp[sl];
+          ncur.c = cc_[sl];
+          nnx.init(un[sl], gam);
+          double fc[4], fn[4], sc, sn, gN[4];
+          ncur.flux(cu[sl], 1, fc, sc);
+          nnx.flux(un[sl], 1, fn, sn);
+          strip::face(fc, sc, cu[sl], fn, sn, un[sl], gN);
           if (own_row) {
-#endif
-            const double* pc = rC + ro[sl];
-            double cu[4], uw[4], ue[4], fw[4], fc[4], fe[4];
-            strip::ld4<Q>(pc, cu);
-            strip::ld4<Q>(pc - QM, uw);
-            strip::ld4<Q>(pc + QM, ue);
-            const double* xc = XS + xo[sl];
-            const double* xw = xc - 5 * Q;
-            const double* xe = xc + 5 * Q;
+            double fx[4], sx, ue[4], fe[4], gE[4], gW[4];
+            ncur.flux(cu[sl], 0, fx, sx);
+            // east face from column c+1's (u, F_x, s_x) by shuffle; the strip's edge faces come from
+            // the halo warps (shared memory)
 #pragma unroll
             for (int a = 0; a < 4; ++a) {
-              fw[a] = xw[a * Q];
-              fc[a] = xc[a * Q];
-              fe[a] = xe[a * Q];
+              ue[a] = __shfl_down_sync(0xffffffffu, cu[sl][a], 4);
+              fe[a] = __shfl_down_sync(0xffffffffu, fx[a], 4);
             }
-            double gw[4], ge[4], r[4];
-            strip::face(fw, xw[4 * Q], uw, fc, xc[4 * Q], cu, gw);
-            strip::face(fc, xc[4 * Q], cu, fe, xe[4 * Q], ue, ge);
+            const double se = __shfl_down_sync(0xffffffffu, sx, 4);
+            strip::face(fx, sx, cu[sl], fe, se, ue, gE);
+            if (c == tw - 1) {
 #pragma unroll
-            for (int a = 0; a < 4; ++a) {
-              r[a] = 0.0;
-              r[a] += (ge[a] - gw[a]) * cfx;
-              r[a] += (gN[sl][a] - gS[sl][a]) * cfy;
+              for (int a = 0; a < 4; ++a) gE[a] = hxr[(4 + a) * Q + kq[sl]];
             }
-            if (jj[sl] < tw) {
-              double* o = rbT + bo[sl];
 #pragma unroll
-              for (int a = 0; a < 4; ++a) o[a * KP] = cform ? cu[a] - dt * r[a] : r[a];
+            for (int a = 0; a < 4; ++a) gW[a] = __shfl_up_sync(0xffffffffu, gE[a], 4);
+            if (c == 0) {
+#pragma unroll
+              for (int a = 0; a < 4; ++a) gW[a] = hxr[a * Q + kq[sl]];
+            }
+            if (act[sl]) {
+              double* o = rb + bo + kq[sl];
+#pragma unroll
+              for (int a = 0; a < 4; ++a) {
+                double r = 0.0;
+                r += (gE[a] - gW[a]) * cfx;
+                r += (gN[a] - gS[sl][a]) * cfy;
+                o[((a + (c >> 1)) & 3) * KP] = cform ? cu[sl][a] - dt * r : r;
+              }
             }
           }
 #pragma unroll
-          for (int a = 0; a < 4; ++a) gS[sl][a] = gN[sl][a];
-          cir[sl] = nir[sl];
-          cp[sl] = np[sl];
-          cc_[sl] = nc[sl];
+          for (int a = 0; a < 4; ++a) {
+            gS[sl][a] = gN[a];
+            cu[sl][a] = un[sl][a];
+          }
+          cir[sl] = nnx.irho;
+          cp[sl] = nnx.p;
+          cc_[sl] = nnx.c;
+        }
+      } else if (it + 2 < LR) {
+        // x fluxes at the strip's west and east faces of the next row (an owned row)
+        double* hxn = HX + ((it + 1) & 1) * HXS;
+        for (int h = tid - HT0; h < 2 * Q; h += NTH) {
+          const int side = h >= Q, k = h - side * Q;
+          const int hcol = side ? tw + 1 : 0, icol = side ? tw : 1;  // halo / inner column
+          double ui[4], uh[4];
+          strip::ld4<Q>(rN + icol * QMP + k, ui);
+          if (codeN[hcol] >= 0)
+            strip::ld4<Q>(rN + hcol * QMP + k, uh);
+          else
+            strip::bstate(P, codeN[hcol], side, k, ui, uh);
+          RusNode<4> ni, nh;
+          ni.init(ui, gam);
+          nh.init(uh, gam);
+          double fi[4], fh[4], si, sh, gf[4];
+          ni.flux(ui, 0, fi, si);
+          nh.flux(uh, 0, fh, sh);
+          if (side)
+            strip::face(fi, si, ui, fh, sh, uh, gf);
+          else
+            strip::face(fh, sh, uh, fi, si, ui, gf);
+#pragma unroll
+          for (int a = 0; a < 4; ++a) hxn[(side * 4 + a) * Q + k] = gf[a];
         }
       }
-      STRIP_STAMP(3)
+      STRIP_STAMP(1)
+      if (warp >= NW - NPW && it >= 2) project(it - 1);
+      STRIP_STAMP(2)
     }
 #ifdef IPM_STRIP_PROF
-    if (prof && first_seg && lane == 0)
+    if (blockIdx.x == 0 && first_seg && lane == 0)
       for (int r = 0; r < 4; ++r)
-        printf("PROF warp %d row %d t0 %lld p1 %lld syncA %lld p2 %lld\n", warp, r, 0LL, st[r * 4 + 1] - st[r * 4],
-               st[r * 4 + 2] - st[r * 4], st[r * 4 + 3] - st[r * 4]);
+        printf("PROF warp %d row %d work %lld proj %lld\n", warp, r, st[r * 4 + 1] - st[r * 4], st[r * 4 + 2] - st[r * 4 + 1]);
     first_seg = false;
 #endif
     __syncthreads();

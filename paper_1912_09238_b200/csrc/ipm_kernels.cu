@@ -1153,9 +1153,6 @@ static int flux_cart_impl(const KernelCtx& k, const FluxLaunch& a) {
   return (int)cudaGetLastError();
 }
 
-#ifndef IPM_STRIP_TX
-#define IPM_STRIP_TX 8
-#endif
 // strip kernel (row-major cartesian block, Euler 2D Rusanov, Q = QC): -1 when not applicable
 template <int TX, int NT, int MINB, int QC>
 static int flux_strip_impl(const KernelCtx& k, const FluxLaunch& a) {
@@ -1180,11 +1177,7 @@ int launch_flux(const KernelCtx& k, const FluxLaunch& a) {
   const int key = (k.flux * 10 + k.m) * 10 + k.mesh.kind;
   const char* fk = std::getenv("IPM_FLUX_KERNEL");
   if (!fk || std::string(fk) == "strip") {
-#if IPM_STRIP_TX == 4
-    const int rc = flux_strip_impl<4, 320, 2, 100>(k, a);
-#else
     const int rc = flux_strip_impl<8, 512, 1, 100>(k, a);
-#endif
     if (rc != -1) return rc;
   }
   if (!(fk && std::string(fk) == "warp")) {
