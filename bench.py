@@ -433,7 +433,7 @@ def run_ours(args):
                                       "flops": "as executed: sum-factorised Hessian, 8-padded DMMA Cholesky"},
                          "traffic": traffic, "dual_ms_avg": dual_avg,
                          "share_of_step": dual_avg / (ms / args.steps)},
-            "roofline_flux": {"bound": "hbm", "kernel": "k_flux_cart" if cfg["mesh"]["kind"] != "tri" else "k_flux_warp", "achieved": flux_gbs, "peak": hbm,
+            "roofline_flux": {"bound": "hbm", "kernel": Context.last_flux_kernel(), "achieved": flux_gbs, "peak": hbm,
                               "unit": "GB/s", "frac": flux_gbs / hbm, "traffic": traffic_flux,
                               "bytes_per_launch": g.cells * flux_bytes_per_cell(N, m, Q), "flux_ms_avg": flux_avg},
             "e2e": e2e,

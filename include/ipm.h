@@ -232,6 +232,10 @@ IPM_API ipm_status ipm_enable_timing(ipm_ctx *c, int32_t on);
  * the string is static. */
 IPM_API const char *ipm_last_dual_kernel(void);
 
+/* Name of the flux kernel the last flux launch of this process used ("k_flux_strip", "k_flux_cart",
+ * "k_flux_warp"; "" before the first launch).  Host only, never fails; the string is static. */
+IPM_API const char *ipm_last_flux_kernel(void);
+
 /* Debug: per-phase clock64 cycle totals of the dual kernel (builds with -DIPM_PHASE_TIMERS;
  * zeros otherwise).  h_out[8]: 0 eval/grad/line search, 1 Hessian, 2 Cholesky, 3 back-substitution,
  * 4 final line search, 7 epilogue + cell fetch.  Synchronous; resets the counters. */

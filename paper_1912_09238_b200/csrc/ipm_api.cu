@@ -763,6 +763,7 @@ ipm_status ipm_last_kernel_ms(ipm_ctx* c, float* dual_ms, float* flux_ms) {
 }
 
 const char* ipm_last_dual_kernel(void) { return ipm::last_dual_kernel(); }
+const char* ipm_last_flux_kernel(void) { return ipm::last_flux_kernel(); }
 
 ipm_status ipm_debug_phase_cycles(uint64_t* h_out) {
   if (!h_out) return fail(IPM_ERR_ARG, "null argument");

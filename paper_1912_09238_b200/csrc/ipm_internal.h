@@ -116,6 +116,7 @@ size_t big_scratch_doubles(int N, int Q, int m, int q1d, int npr, int p);
 int debug_phase_cycles(unsigned long long* out);
 int launch_dual(const KernelCtx& k, const DualLaunch& a);
 const char* last_dual_kernel();
+const char* last_flux_kernel();
 int launch_dt(const KernelCtx& k, double t_end, double dt_fixed, double cfl);
 int launch_flux(const KernelCtx& k, const FluxLaunch& a);
 int launch_project_ic(const KernelCtx& k, const double* d_region /*[R][Q][m]*/, const double* d_split /*[Q][2]*/,

@@ -1172,13 +1172,19 @@ static int flux_strip_impl(const KernelCtx& k, const FluxLaunch& a) {
   return (int)cudaGetLastError();
 }
 
+static const char* g_last_flux = "";
+const char* last_flux_kernel() { return g_last_flux; }
+
 int launch_flux(const KernelCtx& k, const FluxLaunch& a) {
   if (k.mesh.cells == 0) return 0;
   const int key = (k.flux * 10 + k.m) * 10 + k.mesh.kind;
   const char* fk = std::getenv("IPM_FLUX_KERNEL");
   if (!fk || std::string(fk) == "strip") {
     const int rc = flux_strip_impl<8, 512, 1, 100>(k, a);
-    if (rc != -1) return rc;
+    if (rc != -1) {
+      g_last_flux = "k_flux_strip";
+      return rc;
+    }
   }
   if (!(fk && std::string(fk) == "warp")) {
     int rc = -1;
@@ -1189,8 +1195,12 @@ int launch_flux(const KernelCtx& k, const FluxLaunch& a) {
       case (FX_RUSANOV * 10 + 4) * 10 + MK_CART: rc = flux_cart_impl<FX_RUSANOV, 4, MK_CART>(k, a); break;
       case (FX_HLL * 10 + 4) * 10 + MK_CART: rc = flux_cart_impl<FX_HLL, 4, MK_CART>(k, a); break;
     }
-    if (rc != -1) return rc;
+    if (rc != -1) {
+      g_last_flux = "k_flux_cart";
+      return rc;
+    }
   }
+  g_last_flux = "k_flux_warp";
   switch (key) {
     case (FX_LF_GLOBAL * 10 + 1) * 10 + MK_1D: return flux_impl<FX_LF_GLOBAL, 1, MK_1D>(k, a);
     case (FX_HLL * 10 + 3) * 10 + MK_1D: return flux_impl<FX_HLL, 3, MK_1D>(k, a);

@@ -28,7 +28,7 @@ EXPORTS = [
     "ipm_init", "ipm_destroy", "ipm_status_string", "ipm_last_error", "ipm_sizes", "ipm_get_basis",
     "ipm_get_cell_ids", "ipm_dual_solve", "ipm_flux_update", "ipm_step", "ipm_project_ic", "ipm_warm_start",
     "ipm_moments_from_dual", "ipm_stress_dual", "ipm_get_levels", "ipm_set_levels", "ipm_last_cell_stats",
-    "ipm_get_time", "ipm_set_time", "ipm_last_kernel_ms", "ipm_enable_timing", "ipm_last_dual_kernel",
+    "ipm_get_time", "ipm_set_time", "ipm_last_kernel_ms", "ipm_enable_timing", "ipm_last_dual_kernel", "ipm_last_flux_kernel",
     "ipm_debug_phase_cycles", "ipm_step_dual", "ipm_step_flux", "ipm_halo_layout", "ipm_partition_query",
 ]
 
@@ -116,6 +116,7 @@ def lib():
             "ipm_last_kernel_ms": (st, [P, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
             "ipm_enable_timing": (st, [P, C.c_int32]),
             "ipm_last_dual_kernel": (C.c_char_p, []),
+            "ipm_last_flux_kernel": (C.c_char_p, []),
             "ipm_debug_phase_cycles": (st, [P]),
         }
         for name, (res, args) in sig.items():
@@ -368,6 +369,11 @@ class Context:
     def last_dual_kernel() -> str:
         """name of the dual kernel of the last launch (process-wide)"""
         return lib().ipm_last_dual_kernel().decode()
+
+    @staticmethod
+    def last_flux_kernel() -> str:
+        """name of the flux kernel of the last launch (process-wide)"""
+        return lib().ipm_last_flux_kernel().decode()
 
     def last_kernel_ms(self):
         a, b = C.c_float(), C.c_float()
