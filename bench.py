@@ -38,6 +38,7 @@ def parse():
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--nx", type=int, default=0, help="override grid size (cartesian nx = ny)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-chunks", type=int, default=16, help="ipm_step_host copy/solve ranges (e2e, N=1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=9238)
     return ap.parse_args()
@@ -376,11 +377,15 @@ def run_ours(args):
         barrier()
         e0.record(stream)
         for _ in range(args.steps):
-            uhat.copy_(h_u, non_blocking=True)
-            lam.copy_(h_l, non_blocking=True)
-            g.ipm_step(uhat, lam, None, sync=False)
-            h_u.copy_(uhat, non_blocking=True)
-            h_l.copy_(lam, non_blocking=True)
+            if world == 1:
+                # the C-ABI host-buffer step: copies in cell ranges overlapped with the dual solves
+                g.ipm_step_host(h_u, h_l, uhat, lam, None, nchunks=args.e2e_chunks)
+            else:
+                uhat.copy_(h_u, non_blocking=True)
+                lam.copy_(h_l, non_blocking=True)
+                g.ipm_step(uhat, lam, None, sync=False)
+                h_u.copy_(uhat, non_blocking=True)
+                h_l.copy_(lam, non_blocking=True)
         e1.record(stream)
         barrier()
         ms_e = e0.elapsed_time(e1)
@@ -389,7 +394,9 @@ def run_ours(args):
             _allreduce(te, dist.ReduceOp.MAX)
         nbytes = (uhat.numel() + lam.numel()) * 8
         e2e = {"value": cells_total * args.steps / (float(te.item()) / 1e3), "unit": "cell-steps/s",
-               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes}
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+               "path": f"ipm_step_host, {args.e2e_chunks} copy/solve cell ranges" if world == 1
+               else "cudaMemcpyAsync + ipm_step"}
 
     N, m, Q = g.N, g.m, g.Q
     dual_avg = float(np.mean(dual_ms))

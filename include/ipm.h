@@ -170,6 +170,21 @@ IPM_API ipm_status ipm_flux_update(ipm_ctx *c, const double *d_lambda, const dou
  * info == NULL: asynchronous.  info != NULL: synchronous; fills info. */
 IPM_API ipm_status ipm_step(ipm_ctx *c, double *d_uhat, double *d_lambda, double t_end, ipm_step_info *info);
 
+/* ipm_step with the state in HOST memory (the end-to-end path):
+ *   h_uhat, h_lambda  [cells][N][m] host, in/out; page-locked (cudaHostAlloc / torch pin_memory)
+ *                     for the copies to overlap, pageable memory works but serialises them
+ *   d_uhat, d_lambda  [cells][N][m] device work buffers (caller-owned, contents overwritten)
+ *   nchunks >= 1      the host->device copies are split into nchunks contiguous cell ranges on a
+ *                     copy stream; the dual solve of a range starts when its copy has landed, so
+ *                     the copies of later ranges overlap the solves of earlier ones; the duals of a
+ *                     range go back to the host right after its solve (no adaptive levels), the
+ *                     moments (and duals with adaptive levels) after the flux update.
+ * The result equals ipm_step on the same data bit for bit.  Synchronous: returns when h_uhat /
+ * h_lambda hold the result; info (nullable) as for ipm_step.  Single-rank contexts only
+ * (IPM_ERR_ARG otherwise). */
+IPM_API ipm_status ipm_step_host(ipm_ctx *c, double *h_uhat, double *h_lambda, double *d_uhat, double *d_lambda,
+                                 double t_end, int32_t nchunks, ipm_step_info *info);
+
 /* Helpers for inputs (not steps of the path):
  *   ipm_project_ic: uhat_j = <ubar_j(xi) phi>_Q with exact cell averages of a piecewise-constant IC
  *                   (Alg. 1 line 2); also resets t = 0 and levels to initial_level.

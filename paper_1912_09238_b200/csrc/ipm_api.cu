@@ -199,6 +199,8 @@ struct ipm_ctx {
   int32_t *d_level = nullptr, *d_level_new = nullptr, *d_iters = nullptr, *d_status = nullptr;
   ipm::StepScalars* d_sc = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaStream_t copy_stream = nullptr;  // ipm_step_host
+  std::vector<cudaEvent_t> hev;        // ipm_step_host: per-chunk copy / solve events
   bool timing = false;
   int initial_level = 0;
 };
@@ -223,6 +225,8 @@ void ipm_destroy(ipm_ctx* c) {
   if (!c) return;
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : c->hev) cudaEventDestroy(e);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   for (void* p : c->owned) cudaFree(p);
   delete c;
 }
@@ -613,6 +617,83 @@ ipm_status ipm_step(ipm_ctx* c, double* d_uhat, double* d_lambda, double t_end, 
     return fail(IPM_ERR_ARG, "distributed context: use ipm_step_dual / exchange / ipm_step_flux");
   if (ipm_status s = ipm_step_dual(c, d_uhat, d_lambda, nullptr, nullptr)) return s;
   return ipm_step_flux(c, d_uhat, d_lambda, nullptr, nullptr, t_end, info);
+}
+
+ipm_status ipm_step_host(ipm_ctx* c, double* h_uhat, double* h_lambda, double* d_uhat, double* d_lambda, double t_end,
+                         int32_t nchunks, ipm_step_info* info) {
+  if (!c || !h_uhat || !h_lambda || !d_uhat || !d_lambda) return fail(IPM_ERR_ARG, "null argument");
+  if (c->halo > 0 || !c->part.send_local.empty())
+    return fail(IPM_ERR_ARG, "ipm_step_host: single-rank contexts only");
+  if (nchunks < 1) return fail(IPM_ERR_ARG, "nchunks must be >= 1");
+  const int64_t cells = c->cells;
+  const int nch = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, std::max<int64_t>(cells, 1)));
+  if (!c->copy_stream) CUDA_OK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  while ((int)c->hev.size() < 2 * nch + 2) {
+    cudaEvent_t e;
+    CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->hev.push_back(e);
+  }
+  cudaStream_t ms = c->stream, cs = c->copy_stream;
+  const size_t row = (size_t)c->N * c->m;
+  const bool adaptive = c->cfg.n_levels > 0;
+  const ipm::KernelCtx& k = c->k;
+  auto lo = [&](int i) { return cells * i / nch; };
+  // the copy stream starts after everything queued on the ctx stream (the previous step)
+  CUDA_OK(cudaEventRecord(c->hev[2 * nch], ms));
+  CUDA_OK(cudaStreamWaitEvent(cs, c->hev[2 * nch], 0));
+  for (int i = 0; i < nch; ++i) {
+    const size_t r0 = (size_t)lo(i), nr = (size_t)(lo(i + 1) - lo(i));
+    CUDA_OK(cudaMemcpyAsync(d_uhat + r0 * row, h_uhat + r0 * row, nr * row * 8, cudaMemcpyHostToDevice, cs));
+    CUDA_OK(cudaMemcpyAsync(d_lambda + r0 * row, h_lambda + r0 * row, nr * row * 8, cudaMemcpyHostToDevice, cs));
+    CUDA_OK(cudaEventRecord(c->hev[i], cs));
+  }
+  if (int rc = ipm::launch_step_begin(k, c->ghost_rate)) return launch_rc(rc, "step_begin");
+  for (int i = 0; i < nch; ++i) {
+    const int64_t r0 = lo(i), nr = lo(i + 1) - lo(i);
+    CUDA_OK(cudaStreamWaitEvent(ms, c->hev[i], 0));
+    if (nr == 0) continue;
+    // dual solve of cells [r0, r0 + nr): a fresh work queue, pointers offset to the range
+    CUDA_OK(cudaMemsetAsync(&c->d_sc->work_counter, 0, sizeof(int), ms));
+    ipm::KernelCtx kc = k;
+    if (kc.mesh.rate_geo) kc.mesh.rate_geo += r0;
+    ipm::DualLaunch a{};
+    a.uhat = d_uhat + r0 * row;
+    a.lam = d_lambda + r0 * row;
+    a.iters = c->d_iters + r0;
+    a.status = c->d_status + r0;
+    a.crit = c->d_crit + r0;
+    a.uq = c->d_uq + (size_t)r0 * c->Q * c->m;
+    a.level = adaptive ? c->d_level + r0 : nullptr;
+    a.level_new = adaptive ? c->d_level_new + r0 : nullptr;
+    a.cells = nr;
+    a.mode = c->cfg.newton_mode;
+    a.want_rate = 1;
+    if (int rc = ipm::launch_dual(kc, a)) return launch_rc(rc, "dual_solve");
+    if (!adaptive) {  // final duals of the range go back while later ranges solve
+      CUDA_OK(cudaEventRecord(c->hev[nch + i], ms));
+      CUDA_OK(cudaStreamWaitEvent(cs, c->hev[nch + i], 0));
+      CUDA_OK(cudaMemcpyAsync(h_lambda + r0 * row, d_lambda + r0 * row, (size_t)nr * row * 8, cudaMemcpyDeviceToHost,
+                              cs));
+    }
+  }
+  if (ipm_status s = ipm_step_flux(c, d_uhat, d_lambda, nullptr, nullptr, t_end, nullptr)) return s;
+  CUDA_OK(cudaMemcpyAsync(h_uhat, d_uhat, (size_t)cells * row * 8, cudaMemcpyDeviceToHost, ms));
+  if (adaptive) CUDA_OK(cudaMemcpyAsync(h_lambda, d_lambda, (size_t)cells * row * 8, cudaMemcpyDeviceToHost, ms));
+  CUDA_OK(cudaEventRecord(c->hev[2 * nch + 1], cs));
+  CUDA_OK(cudaStreamWaitEvent(ms, c->hev[2 * nch + 1], 0));
+  ipm::StepScalars s;
+  CUDA_OK(cudaMemcpyAsync(&s, c->d_sc, sizeof(s), cudaMemcpyDeviceToHost, ms));
+  CUDA_OK(cudaStreamSynchronize(ms));
+  if (info) {
+    info->dt = s.dt;
+    info->t = s.t;
+    info->residual = s.residual;
+    info->newton_iters = (int64_t)s.newton_iters;
+    info->failed_cells = (int64_t)s.failed;
+    info->worst_status = s.worst;
+    if (s.failed) return fail(IPM_ERR_NUMERIC, "failed cells in step");
+  }
+  return IPM_OK;
 }
 
 ipm_status ipm_halo_layout(const ipm_ctx* c, int32_t* npeers, int64_t* nsend, int64_t* nrecv, int32_t* h_peers,

@@ -75,9 +75,13 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   const double h = 0.5 * x;
   double e = fma(-h * y, y, 0.5);
+#ifdef IPM_RSQRT_NR1  // one Newton step (~1e-13 relative): +1 % on config 3, not the default
+  return fma(y, e, y);
+#else
   y = fma(y, e, y);
   e = fma(-h * y, y, 0.5);
   return fma(y, e, y);
+#endif
 #endif
 }
 

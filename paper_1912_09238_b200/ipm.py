@@ -26,7 +26,7 @@ CELL_STATUS = {0: "ok", 1: "nonconvergence", 2: "illconditioned", 3: "linesearch
 
 EXPORTS = [
     "ipm_init", "ipm_destroy", "ipm_status_string", "ipm_last_error", "ipm_sizes", "ipm_get_basis",
-    "ipm_get_cell_ids", "ipm_dual_solve", "ipm_flux_update", "ipm_step", "ipm_project_ic", "ipm_warm_start",
+    "ipm_get_cell_ids", "ipm_dual_solve", "ipm_flux_update", "ipm_step", "ipm_step_host", "ipm_project_ic", "ipm_warm_start",
     "ipm_moments_from_dual", "ipm_stress_dual", "ipm_get_levels", "ipm_set_levels", "ipm_last_cell_stats",
     "ipm_get_time", "ipm_set_time", "ipm_last_kernel_ms", "ipm_enable_timing", "ipm_last_dual_kernel", "ipm_last_flux_kernel",
     "ipm_debug_phase_cycles", "ipm_step_dual", "ipm_step_flux", "ipm_halo_layout", "ipm_partition_query",
@@ -99,6 +99,7 @@ def lib():
             "ipm_dual_solve": (st, [P, D, D, C.c_int32, I, I, D]),
             "ipm_flux_update": (st, [P, D, D, D, C.c_double, D]),
             "ipm_step": (st, [P, D, D, C.c_double, C.POINTER(ipm_step_info)]),
+            "ipm_step_host": (st, [P, D, D, D, D, C.c_double, C.c_int32, C.POINTER(ipm_step_info)]),
             "ipm_project_ic": (st, [P, C.POINTER(ipm_ic), D]),
             "ipm_warm_start": (st, [P, D, D]),
             "ipm_moments_from_dual": (st, [P, D, D]),
@@ -313,6 +314,18 @@ class Context:
         if rc == 5:  # IPM_ERR_NUMERIC: report, caller decides
             return info
         check(rc, "ipm_step")
+        return info
+
+    def ipm_step_host(self, h_uhat, h_lam, d_uhat, d_lam, t_end=None, nchunks=4):
+        """One step with the state in (pinned) host tensors h_uhat / h_lam, d_uhat / d_lam device work
+        buffers; copies overlapped with the dual solves in nchunks cell ranges (synchronous)."""
+        info = ipm_step_info()
+        te = -1.0 if t_end is None else float(t_end)
+        rc = lib().ipm_step_host(self.h, _ptr(h_uhat), _ptr(h_lam), _ptr(d_uhat), _ptr(d_lam), te, int(nchunks),
+                                 C.byref(info))
+        if rc == 5:
+            return info
+        check(rc, "ipm_step_host")
         return info
 
     # --- helpers ----------------------------------------------------------------------------

@@ -115,3 +115,25 @@ def test_one_step_mode_matches_oracle(torch, dual_kernel, name):
     np.testing.assert_array_equal(to_np(st_g), st_o)
     scale = np.abs(lam_star).max(axis=(0, 1))
     assert (np.abs(to_np(lam_g) - lam0_o) / scale).max() < 1e-9
+
+
+@pytest.mark.parametrize("nchunks", [1, 3, 7])
+def test_step_host_matches_device_step(torch, nchunks):
+    """ipm_step_host (host buffers, copies overlapped with the dual solves of earlier cell ranges)
+    gives ipm_step's result bit for bit"""
+    from paper_1912_09238_b200 import Context
+
+    cfg = configs.get("cfg3", mesh=dict(nx=13, ny=11))
+    g = Context(cfg)
+    o = __import__("oracle").Oracle(cfg)
+    _, _, lam_s, u_g = _stress(torch, g, o, cfg, seed=3)
+    lam0 = g.zeros()
+    g.ipm_warm_start(u_g, lam0)
+    ref_u, ref_l = u_g.clone(), lam0.clone()
+    h_u, h_l = u_g.cpu().pin_memory(), lam0.cpu().pin_memory()
+    d_u, d_l = g.zeros(), g.zeros()
+    for _ in range(2):
+        ia = g.ipm_step(ref_u, ref_l)
+        ib = g.ipm_step_host(h_u, h_l, d_u, d_l, None, nchunks=nchunks)
+        assert ia.newton_iters == ib.newton_iters and ia.dt == ib.dt
+    assert torch.equal(h_u, ref_u.cpu()) and torch.equal(h_l, ref_l.cpu())
