@@ -122,6 +122,14 @@ typedef struct {
   int32_t rank, nranks, px, py;
   const void *reserved_ptr;  /* unused (the exchange is performed by the caller) */
   void *stream;              /* cudaStream_t */
+  /* refinement retardation (Algorithm 4; n_levels > 0): stage l caps every
+   * cell's level index at retard_level[l] until the steady residual of a step falls below
+   * retard_eps[l], then the next stage applies; past the last stage no cap.  n_retard = 0 -> off.
+   * Reading 31: Algorithm 4's max{DetermineRefinementLevel, l*_l} is read as the cap
+   * min{.} the text describes ("maximal refinement levels"). */
+  int32_t n_retard;
+  int32_t retard_level[8];
+  double retard_eps[8];
 } ipm_config;
 
 typedef struct {
@@ -246,6 +254,14 @@ IPM_API ipm_status ipm_enable_timing(ipm_ctx *c, int32_t on);
  * "k_dual_group", "k_dual_warp", "k_dual_big"; "" before the first launch).  Host only, never fails;
  * the string is static. */
 IPM_API const char *ipm_last_dual_kernel(void);
+
+/* Refinement retardation stage (Algorithm 4): ipm_retard_stage reads the current stage
+ * (synchronous; 0 when retardation is off).  Single-rank contexts advance the stage on the device
+ * after every step from the step's residual; distributed contexts (nranks > 1) do not — the caller
+ * passes the global residual of each step to ipm_retard_advance (the Python binding does after its
+ * residual all-reduce), which advances the stage when it lies below the stage's tolerance. */
+IPM_API ipm_status ipm_retard_stage(ipm_ctx *c, int32_t *stage);
+IPM_API ipm_status ipm_retard_advance(ipm_ctx *c, double global_residual);
 
 /* Name of the flux kernel the last flux launch of this process used ("k_flux_strip", "k_flux_cart",
  * "k_flux_warp"; "" before the first launch).  Host only, never fails; the string is static. */

@@ -36,6 +36,7 @@ struct orc_ctx {
   double *xc;     /* [cells][2] cell centre (1D/cart) */
   double *bc_u;   /* [4][Q][m] ghost states of STATE boundaries */
   int32_t *level; /* [cells] refinement level index (adaptivity) */
+  int retard_stage; /* refinement retardation stage (Alg. 4) */
   int n_levels;
   int Nl[8];      /* N at each level */
 };
@@ -852,6 +853,7 @@ void orc_warm_start(const orc_ctx *c, const double *uhat, double *lam) {
   }
 }
 
+int orc_retard_stage(const orc_ctx *c) { return c->retard_stage; }
 void orc_set_levels(orc_ctx *c, const int32_t *levels) { memcpy(c->level, levels, sizeof(int32_t) * c->cells); }
 void orc_get_levels(const orc_ctx *c, int32_t *levels) { memcpy(levels, c->level, sizeof(int32_t) * c->cells); }
 
@@ -1042,7 +1044,7 @@ double orc_indicator(const orc_ctx *c, int lvl, const double *h) {
 }
 
 /* One step of Algorithm 1 (FULL) / 2 (ONE_STEP) / 3-4 structure (levels), PAPER.md:196-217,
- * 252-269, 400-450 (without retardation). */
+ * 252-269, 400-450; refinement retardation (Alg. 4) when n_retard > 0. */
 int orc_step(orc_ctx *c, double *uhat, double *lam, double t_remaining, int32_t *iters,
              int32_t *status, double *dt_used, double *residual) {
   int N = c->N, m = c->m, Q = c->Q, cells = c->cells;
@@ -1066,6 +1068,9 @@ int orc_step(orc_ctx *c, double *uhat, double *lam, double t_remaining, int32_t 
       int nl = lvl;
       if (S < c->P.delta_dec && lvl > 0) nl = lvl - 1;
       else if (S > c->P.delta_inc && lvl < c->n_levels - 1) nl = lvl + 1;
+      /* Alg. 4 line 6: the current stage's maximal level l*_l (reading 31: a cap) */
+      if (c->P.n_retard > 0 && c->retard_stage < c->P.n_retard && nl > c->P.retard_level[c->retard_stage])
+        nl = c->P.retard_level[c->retard_stage];
       newlev[j] = nl;
     }
   }
@@ -1080,6 +1085,9 @@ int orc_step(orc_ctx *c, double *uhat, double *lam, double t_remaining, int32_t 
   double res = 0.0;
   for (int j = 0; j < cells; ++j) res += c->area[j] * fabs(unew[(size_t)j * N * m] - uhat[(size_t)j * N * m]);
   memcpy(uhat, unew, sizeof(double) * (size_t)cells * N * m);
+  /* Alg. 4 lines 12-14: next stage once the residual lies below the stage's tolerance */
+  if (c->P.n_retard > 0 && c->retard_stage < c->P.n_retard && res < c->P.retard_eps[c->retard_stage])
+    c->retard_stage += 1;
   /* lambda zero-padded (refine) or truncated (coarsen) to the new level */
   if (c->n_levels > 0) {
     for (int j = 0; j < cells; ++j) {

@@ -84,7 +84,12 @@ typedef struct {
   int32_t pad1;
   double delta_dec, delta_inc;
   int32_t n_threads;         /* OpenMP threads, 0 = default */
-  int32_t pad2;
+  /* refinement retardation (Alg. 4): stage l caps the level index at
+   * retard_level[l] until the steady residual falls below retard_eps[l]; past the last stage no cap.
+   * n_retard == 0 -> off (reading 31: Alg. 4's max{., l*} is a cap, min) */
+  int32_t n_retard;
+  int32_t retard_level[8];
+  double retard_eps[8];
 } orc_problem;
 
 typedef struct {
@@ -98,6 +103,7 @@ typedef struct {
 typedef struct orc_ctx orc_ctx;
 
 orc_ctx *orc_create(const orc_problem *P);
+int orc_retard_stage(const orc_ctx *c); /* refinement retardation stage (Alg. 4) */
 void orc_destroy(orc_ctx *c);
 /* sizes */
 int orc_N(const orc_ctx *c);

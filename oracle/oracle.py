@@ -57,7 +57,8 @@ class Problem(C.Structure):
         ("cfl", C.c_double),
         ("n_levels", C.c_int32), ("level_M", C.c_int32 * 8), ("pad1", C.c_int32),
         ("delta_dec", C.c_double), ("delta_inc", C.c_double),
-        ("n_threads", C.c_int32), ("pad2", C.c_int32),
+        ("n_threads", C.c_int32),
+        ("n_retard", C.c_int32), ("retard_level", C.c_int32 * 8), ("retard_eps", C.c_double * 8),
     ]
 
 
@@ -96,6 +97,7 @@ def lib():
             "orc_warm_start": (None, [P, D, D]),
             "orc_indicator": (C.c_double, [P, C.c_int, D]),
             "orc_set_levels": (None, [P, I]), "orc_get_levels": (None, [P, I]),
+            "orc_retard_stage": (C.c_int, [P]),
             "orc_dual_solve_all": (None, [P, D, D, I, I, D]),
             "orc_compute_dt": (C.c_double, [P, D, C.c_double]),
             "orc_cell_rates": (None, [P, D, D]),
@@ -190,6 +192,11 @@ class Oracle:
             P.level_M[k] = Mk
         P.delta_dec, P.delta_inc = cfg.get("delta_dec", 0.0), cfg.get("delta_inc", 0.0)
         P.n_threads = n_threads
+        # refinement retardation (Alg. 4): [(eps_l, level index cap l*_l), ...]
+        retard = cfg.get("retard") or []
+        P.n_retard = len(retard)
+        for k, (eps, lv) in enumerate(retard):
+            P.retard_eps[k], P.retard_level[k] = eps, lv
         self._P = P
         self.ctx = L.orc_create(C.byref(P))
         self.N, self.Q, self.cells, self.m = L.orc_N(self.ctx), L.orc_Q(self.ctx), L.orc_cells(self.ctx), cfg["m"]
@@ -317,6 +324,10 @@ class Oracle:
     def indicator(self, lvl, h):
         h = np.ascontiguousarray(h, np.float64)
         return lib().orc_indicator(self.ctx, lvl, _d(h))
+
+    def retard_stage(self) -> int:
+        """refinement retardation stage (Algorithm 4)"""
+        return lib().orc_retard_stage(self.ctx)
 
     def levels(self):
         lv = np.zeros(self.cells, dtype=np.int32)

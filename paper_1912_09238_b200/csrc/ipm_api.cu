@@ -246,6 +246,9 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   if (C.nranks > 1 && (C.rank < 0 || C.rank >= C.nranks)) return fail(IPM_ERR_ARG, "rank out of range");
   if (C.n_levels < 0 || C.n_levels > 8) return fail(IPM_ERR_ARG, "n_levels in [0, 8]");
   if (C.n_levels > 0 && C.level_M[C.n_levels - 1] != C.M) return fail(IPM_ERR_ARG, "level_M[last] must equal M");
+  if (C.n_retard < 0 || C.n_retard > 8) return fail(IPM_ERR_ARG, "n_retard must be in [0, 8]");
+  for (int l = 0; l < C.n_retard && C.n_levels > 0; ++l)
+    if (C.retard_level[l] < 0 || C.retard_level[l] >= C.n_levels) return fail(IPM_ERR_ARG, "retard_level out of range");
 
   ipm_ctx* c = new ipm_ctx();
   c->cfg = C;
@@ -455,6 +458,11 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   for (int l = 0; l < C.n_levels; ++l) k.ad.Nl[l] = binom_total(p, C.level_M[l]);
   k.ad.Nprev0 = C.n_levels > 0 ? (C.level_M[0] > 0 ? binom_total(p, C.level_M[0] - 1) : 0) : 0;
   k.ad.delta_dec = C.delta_dec;
+  k.ad.n_retard = C.n_levels > 0 ? C.n_retard : 0;
+  for (int l = 0; l < 8; ++l) {
+    k.ad.retard_level[l] = l < k.ad.n_retard ? C.retard_level[l] : 0;
+    k.ad.retard_eps[l] = l < k.ad.n_retard ? C.retard_eps[l] : 0.0;
+  }
   k.ad.delta_inc = C.delta_inc;
   k.cl = ipm::ClParams{C.gamma, C.u_minus, C.u_plus, C.gamma > 1.0 ? 1.0 / (C.gamma - 1.0) : 0.0};
   k.closure = C.closure;
@@ -596,6 +604,8 @@ ipm_status ipm_step_flux(ipm_ctx* c, double* d_uhat, double* d_lambda, const dou
   if (int rc = ipm::launch_flux(k, f)) return launch_rc(rc, "flux");
   if (c->timing) cudaEventRecord(c->ev[3], c->stream);
   if (c->cfg.n_levels > 0) std::swap(c->d_level, c->d_level_new);
+  if (c->cfg.nranks <= 1)  // distributed: the caller advances with the global residual
+    if (int rc = ipm::launch_retard(k)) return launch_rc(rc, "retard");
   if (info) {
     ipm::StepScalars s;
     CUDA_OK(cudaMemcpyAsync(&s, c->d_sc, sizeof(s), cudaMemcpyDeviceToHost, c->stream));
@@ -692,6 +702,30 @@ ipm_status ipm_step_host(ipm_ctx* c, double* h_uhat, double* h_lambda, double* d
     info->failed_cells = (int64_t)s.failed;
     info->worst_status = s.worst;
     if (s.failed) return fail(IPM_ERR_NUMERIC, "failed cells in step");
+  }
+  return IPM_OK;
+}
+
+ipm_status ipm_retard_stage(ipm_ctx* c, int32_t* stage) {
+  if (!c || !stage) return fail(IPM_ERR_ARG, "null argument");
+  int st = 0;
+  CUDA_OK(cudaMemcpyAsync(&st, &c->d_sc->stage, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(cudaStreamSynchronize(c->stream));
+  *stage = st;
+  return IPM_OK;
+}
+
+ipm_status ipm_retard_advance(ipm_ctx* c, double global_residual) {
+  if (!c) return fail(IPM_ERR_ARG, "null ctx");
+  const ipm::Adapt& ad = c->k.ad;
+  if (ad.n_retard <= 0) return IPM_OK;
+  int st = 0;
+  CUDA_OK(cudaMemcpyAsync(&st, &c->d_sc->stage, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(cudaStreamSynchronize(c->stream));
+  if (st < ad.n_retard && global_residual < ad.retard_eps[st]) {
+    ++st;
+    CUDA_OK(cudaMemcpyAsync(&c->d_sc->stage, &st, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(cudaStreamSynchronize(c->stream));
   }
   return IPM_OK;
 }

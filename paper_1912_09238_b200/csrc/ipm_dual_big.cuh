@@ -777,6 +777,7 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
         else if (S > P.ad.delta_inc && lvl < P.ad.n_levels - 1)
           nl = lvl + 1;
       }
+      nl = retard_cap(P.ad, P.sc, nl);  // Alg. 4: the stage's maximal level
       Nnew = P.ad.Nl[nl];
       if (t == 0) A.level_new[cell] = nl;
     }

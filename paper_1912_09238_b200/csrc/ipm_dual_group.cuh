@@ -617,6 +617,7 @@ __global__ void __launch_bounds__(IPM_GROUP_THREADS) k_dual_group(DualParams P) 
         else if (S > P.ad.delta_inc && lvl < P.ad.n_levels - 1)
           nl = lvl + 1;
       }
+      nl = retard_cap(P.ad, P.sc, nl);  // Alg. 4: the stage's maximal level
       Nnew = P.ad.Nl[nl];
       if (t == 0) A.level_new[cell] = nl;
     }

@@ -896,6 +896,7 @@ if constexpr (W == 1) {
         else if (Sv > P.ad.delta_inc && lvl < P.ad.n_levels - 1)
           nl = lvl + 1;
       }
+      nl = retard_cap(P.ad, P.sc, nl);  // Alg. 4: the stage's maximal level
       if (t == 0) A.level_new[cell] = nl;
     }
     {

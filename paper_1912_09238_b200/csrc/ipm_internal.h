@@ -59,6 +59,9 @@ struct Adapt {
   int Nl[8];
   int Nprev0;  // basis size of degree level_M[0]-1 (indicator band at the lowest level)
   double delta_dec, delta_inc;
+  int n_retard;  // refinement retardation (Alg. 4): 0 = off
+  int retard_level[8];
+  double retard_eps[8];
 };
 
 // Device scalars of one step (ctx-owned).
@@ -66,7 +69,8 @@ struct StepScalars {
   unsigned long long rate_bits;  // max over nodes of the CFL rate (as ordered bits of a double >= 0)
   double dt, t, residual;
   unsigned long long newton_iters, failed;
-  int worst, work_counter, work_counter2, pad;
+  int worst, work_counter, work_counter2;
+  int stage;  // refinement retardation stage (Alg. 4)
 };
 
 struct DualLaunch {
@@ -117,6 +121,7 @@ int debug_phase_cycles(unsigned long long* out);
 int launch_dual(const KernelCtx& k, const DualLaunch& a);
 const char* last_dual_kernel();
 const char* last_flux_kernel();
+int launch_retard(const KernelCtx& k);
 int launch_dt(const KernelCtx& k, double t_end, double dt_fixed, double cfl);
 int launch_flux(const KernelCtx& k, const FluxLaunch& a);
 int launch_project_ic(const KernelCtx& k, const double* d_region /*[R][Q][m]*/, const double* d_split /*[Q][2]*/,

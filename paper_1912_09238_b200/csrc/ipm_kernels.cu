@@ -207,6 +207,16 @@ __device__ __forceinline__ double node_rate(const double* u, const Mesh& M, int6
   }
 }
 
+// refinement retardation (Algorithm 4; reading 31): the current stage caps the
+// level index
+__device__ __forceinline__ int retard_cap(const Adapt& ad, const StepScalars* sc, int nl) {
+  if (ad.n_retard > 0) {
+    const int st = *(volatile const int*)&sc->stage;
+    if (st < ad.n_retard && nl > ad.retard_level[st]) nl = ad.retard_level[st];
+  }
+  return nl;
+}
+
 struct DualParams {
   Tables T;
   Mesh mesh;
@@ -340,6 +350,7 @@ __global__ void __launch_bounds__(512) k_dual_warp(DualParams P) {
         else if (S > P.ad.delta_inc && lvl < P.ad.n_levels - 1)
           nl = lvl + 1;
       }
+      nl = retard_cap(P.ad, P.sc, nl);  // Alg. 4: the stage's maximal level
       Nnew = P.ad.Nl[nl];
       if (lane == 0) A.level_new[cell] = nl;
     }
@@ -710,6 +721,11 @@ __global__ void k_step_begin(StepScalars* sc, double rate0) {
   sc->worst = 0;
   sc->work_counter = 0;
   sc->work_counter2 = 0;
+}
+
+// Algorithm 4 lines 12-14: next retardation stage once the step's residual is below its tolerance
+__global__ void k_retard(StepScalars* sc, Adapt ad) {
+  if (sc->stage < ad.n_retard && sc->residual < ad.retard_eps[sc->stage]) sc->stage += 1;
 }
 
 // dt = min(cfl / rate, t_end - t) (t_end <= 0: no cap), then t += dt
@@ -1169,6 +1185,12 @@ static int flux_strip_impl(const KernelCtx& k, const FluxLaunch& a) {
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(rows, (int64_t)k.sm_count * per_sm));
   FluxParams P{k.T, k.mesh, k.cl, k.ad, a, k.sc, 1};
   kern<<<grid, NT, smem, S(k)>>>(P);
+  return (int)cudaGetLastError();
+}
+
+int launch_retard(const KernelCtx& k) {
+  if (k.ad.n_retard <= 0) return 0;
+  k_retard<<<1, 1, 0, S(k)>>>(k.sc, k.ad);
   return (int)cudaGetLastError();
 }
 

@@ -28,7 +28,7 @@ EXPORTS = [
     "ipm_init", "ipm_destroy", "ipm_status_string", "ipm_last_error", "ipm_sizes", "ipm_get_basis",
     "ipm_get_cell_ids", "ipm_dual_solve", "ipm_flux_update", "ipm_step", "ipm_step_host", "ipm_project_ic", "ipm_warm_start",
     "ipm_moments_from_dual", "ipm_stress_dual", "ipm_get_levels", "ipm_set_levels", "ipm_last_cell_stats",
-    "ipm_get_time", "ipm_set_time", "ipm_last_kernel_ms", "ipm_enable_timing", "ipm_last_dual_kernel", "ipm_last_flux_kernel",
+    "ipm_get_time", "ipm_set_time", "ipm_last_kernel_ms", "ipm_enable_timing", "ipm_last_dual_kernel", "ipm_last_flux_kernel", "ipm_retard_stage", "ipm_retard_advance",
     "ipm_debug_phase_cycles", "ipm_step_dual", "ipm_step_flux", "ipm_halo_layout", "ipm_partition_query",
 ]
 
@@ -60,6 +60,7 @@ class ipm_config(C.Structure):
         ("delta_dec", C.c_double), ("delta_inc", C.c_double),
         ("rank", C.c_int32), ("nranks", C.c_int32), ("px", C.c_int32), ("py", C.c_int32),
         ("reserved_ptr", C.c_void_p), ("stream", C.c_void_p),
+        ("n_retard", C.c_int32), ("retard_level", C.c_int32 * 8), ("retard_eps", C.c_double * 8),
     ]
 
 
@@ -118,6 +119,8 @@ def lib():
             "ipm_enable_timing": (st, [P, C.c_int32]),
             "ipm_last_dual_kernel": (C.c_char_p, []),
             "ipm_last_flux_kernel": (C.c_char_p, []),
+            "ipm_retard_stage": (st, [P, C.POINTER(C.c_int32)]),
+            "ipm_retard_advance": (st, [P, C.c_double]),
             "ipm_debug_phase_cycles": (st, [P]),
         }
         for name, (res, args) in sig.items():
@@ -188,6 +191,10 @@ def make_config(cfg: dict, mesh_arrays=None, rank=0, nranks=1, px=1, py=1):
     for k, Mk in enumerate(levels):
         c.level_M[k] = Mk
     c.delta_dec, c.delta_inc = cfg.get("delta_dec", 0.0), cfg.get("delta_inc", 0.0)
+    retard = cfg.get("retard") or []  # refinement retardation (Alg. 4): [(eps_l, level index cap), ...]
+    c.n_retard = len(retard)
+    for k, (eps, lv) in enumerate(retard):
+        c.retard_eps[k], c.retard_level[k] = eps, lv
     c.rank, c.nranks, c.px, c.py = rank, nranks, px, py
     return c, keep
 
@@ -311,10 +318,18 @@ class Context:
             if sync and rc in (0, 5):
                 dist.reduce_info_(info, self.device, self.group)
                 rc = 5 if info.failed_cells else 0
+                if self.cfg.get("retard"):  # Alg. 4 stage from the global residual
+                    check(lib().ipm_retard_advance(self.h, info.residual), "ipm_retard_advance")
         if rc == 5:  # IPM_ERR_NUMERIC: report, caller decides
             return info
         check(rc, "ipm_step")
         return info
+
+    def retard_stage(self) -> int:
+        """current refinement retardation stage (Algorithm 4)"""
+        st = C.c_int32()
+        check(lib().ipm_retard_stage(self.h, C.byref(st)), "ipm_retard_stage")
+        return st.value
 
     def ipm_step_host(self, h_uhat, h_lam, d_uhat, d_lam, t_end=None, nchunks=4):
         """One step with the state in (pinned) host tensors h_uhat / h_lam, d_uhat / d_lam device work

@@ -122,6 +122,20 @@ def test_one_shot_adaptive_cfg4_parity(torch):
         assert abs(ro - rg) <= 1e-9 * max(ro, 1e-300)
 
 
+def test_refinement_retardation_cfg4_parity(torch):
+    """Algorithm 4: the stage caps and their residual-driven advance on the GPU
+    (device-side stage) against the oracle; the schedule moves the stage twice within the run"""
+    cfg = dict(configs.parity_variant("cfg4"), delta_inc=1e-9, delta_dec=0.0, initial_level=0,
+               retard=[(1.9e-4, 0), (1.8759e-4, 1)])
+    g, o, (u_o, l_o, io), (u_g, l_g, ig) = _run_both(cfg, n_steps=8)
+    assert o.retard_stage() == g.retard_stage() == 2
+    assert (o.levels() != to_np(g.levels())).mean() < 0.01
+    assert_moments_close(u_g, u_o, 1e-9, "cfg4 retardation")
+    for (_, ito, ro), (_, itg, rg) in zip(io["hist"], ig["hist"]):
+        assert np.abs(ito - itg).max() <= 1
+        assert abs(ro - rg) <= 1e-9 * max(ro, 1e-300)
+
+
 def test_one_shot_steady_fixed_point(torch):
     from paper_1912_09238_b200 import Context
 

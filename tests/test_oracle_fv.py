@@ -349,3 +349,49 @@ def test_triangle_mesh_geometry(oracle_mod):
     # total area = channel minus the piecewise-linear bump (circular segment 0.0672...)
     seg = 1.3 ** 2 * np.arccos(1.2 / 1.3) - 1.2 * np.sqrt(1.3 ** 2 - 1.2 ** 2)
     assert abs(area.sum() - (3.0 - seg)) < 2e-3
+
+
+# ------------------------------------------------------------------ refinement retardation (Alg. 4)
+def _retard_run(oracle_mod, cfg, steps):
+    mesh = bump_channel_mesh(cfg["mesh"]["nx_pts"], cfg["mesh"]["ny_pts"], cfg["mesh"]["seed"])
+    o = oracle_mod.Oracle(cfg, mesh)
+    u = o.project_ic()
+    lam = o.warm_start(u)
+    hist = []
+    for _ in range(steps):
+        w, _, _, _, res = o.step(u, lam)
+        assert w == 0
+        hist.append((res, o.levels().copy(), o.retard_stage()))
+    return o, u, lam, hist
+
+
+def test_retardation_capped_at_lowest_level_is_degree2_ipm(oracle_mod):
+    """while the stage's maximal level is the lowest one, the adaptive ladder
+    computes the fixed degree-2 IPM (tolerance 0: the stage never advances)"""
+    base = dict(configs.parity_variant("cfg4"), delta_inc=1e-9, delta_dec=0.0, initial_level=0)
+    _, ua, la, ha = _retard_run(oracle_mod, dict(base, retard=[(0.0, 0)]), 4)
+    _, ub, lb, _ = _retard_run(oracle_mod, dict(base, levels=[2], M=2), 4)
+    assert all(st == 0 and lv.max() == 0 for _, lv, st in ha)
+    np.testing.assert_array_equal(ua[:, :6], ub)
+    np.testing.assert_array_equal(la[:, :6], lb)
+    assert np.all(ua[:, 6:] == 0.0) and np.all(la[:, 6:] == 0.0)
+
+
+def test_retardation_stage_lifts_the_cap_when_the_residual_drops(oracle_mod):
+    """Alg. 4 lines 12-14: the stage advances after the first step whose residual is below its
+    tolerance; until then no cell exceeds the stage's level; a schedule whose caps are the top level
+    changes nothing"""
+    base = dict(configs.parity_variant("cfg4"), delta_inc=1e-9, delta_dec=0.0, initial_level=0)
+    _, u0, l0, h0 = _retard_run(oracle_mod, base, 4)
+    assert h0[0][1].max() == 1  # uncapped: the indicator refines at the first step
+    _, u1, l1, h1 = _retard_run(oracle_mod, dict(base, retard=[(1.9e-4, 0)]), 4)
+    stages = [st for _, _, st in h1]
+    first_below = next(i for i, (r, _, _) in enumerate(h1) if r < 1.9e-4)
+    assert stages == [0 if i < first_below else 1 for i in range(4)]
+    for i, (_, lv, _) in enumerate(h1):
+        if i <= first_below:
+            assert lv.max() == 0
+    assert h1[first_below + 1][1].max() == 1  # cap lifted: refinement resumes
+    _, u2, l2, h2 = _retard_run(oracle_mod, dict(base, retard=[(1e300, 3), (1e300, 3)]), 4)
+    np.testing.assert_array_equal(u2, u0)
+    np.testing.assert_array_equal(l2, l0)
