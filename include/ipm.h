@@ -206,6 +206,21 @@ typedef struct {
   ipm_state state[4];        /* STEP1D: left,right; QUAD2D: NE,NW,SW,SE; UNIFORM: [0] */
 } ipm_ic;
 IPM_API ipm_status ipm_project_ic(ipm_ctx *c, const ipm_ic *ic, double *d_uhat);
+
+/* Stochastic Collocation: the deterministic finite-volume
+ * scheme with the same numerical flux (ipm_config.flux) run at every quadrature node; all nodes
+ * advance together with one CFL step (the paper's coupled collocation code).
+ *   d_nodes  [cells][m][Q] node states (device, caller-owned)
+ *   ipm_sc_init     node states of the IC (the cell averages ipm_project_ic projects); sets t = 0
+ *   ipm_sc_step     d_out = d_in - dt r(d_in), dt = CFL / max node rate capped at t_end - t
+ *                   (t_end <= 0: no cap); d_in and d_out must not alias; info (nullable, makes the
+ *                   call synchronous): dt, t, residual = sum_j |Omega_j| |change of the mean of the
+ *                   first state|, newton_iters = 0
+ *   ipm_sc_moments  uhat_i = sum_k w_k u(xi_k) phi_i(xi_k), [cells][N][m]
+ * Single-rank contexts only (IPM_ERR_ARG otherwise). */
+IPM_API ipm_status ipm_sc_init(ipm_ctx *c, const ipm_ic *ic, double *d_nodes);
+IPM_API ipm_status ipm_sc_step(ipm_ctx *c, const double *d_in, double *d_out, double t_end, ipm_step_info *info);
+IPM_API ipm_status ipm_sc_moments(ipm_ctx *c, const double *d_nodes, double *d_uhat);
 IPM_API ipm_status ipm_warm_start(ipm_ctx *c, const double *d_uhat, double *d_lambda);
 IPM_API ipm_status ipm_moments_from_dual(ipm_ctx *c, const double *d_lambda, double *d_uhat);
 IPM_API ipm_status ipm_stress_dual(ipm_ctx *c, const double *d_base, const double *d_z, double rel, double abs_,

@@ -799,44 +799,53 @@ done:
 
 static double clamp01(double x) { return x < 0.0 ? 0.0 : (x > 1.0 ? 1.0 : x); }
 
+/* cell average of the piecewise-constant IC at node xi_k (exact fractions of the cell on each side
+ * of the split lines, reading 17) */
+static void ic_node_state(const orc_ctx *c, const orc_ic *ic, int j, int k, double *ub) {
+  const orc_problem *P = &c->P;
+  int m = c->m, p = P->p;
+  const double *xi = c->xi + k * p;
+  double us[4][4];
+  for (int a = 0; a < 4; ++a) ub[a] = 0.0;
+  if (ic->kind == ORC_IC_UNIFORM) {
+    spec_state(c, &ic->state[0], xi, ub);
+    return;
+  }
+  double xs = ic->xs0, ys = ic->ys0;
+  for (int d = 0; d < p && d < 3; ++d) {
+    xs += ic->xs1[d] * xi[d];
+    ys += ic->ys1[d] * xi[d];
+  }
+  int nreg = ic->kind == ORC_IC_STEP1D ? 2 : 4;
+  for (int r = 0; r < nreg; ++r) spec_state(c, &ic->state[r], xi, us[r]);
+  if (P->mesh_kind == ORC_MESH_1D) {
+    double dx = (P->x1 - P->x0) / P->nx;
+    double xl = P->x0 + j * dx;
+    double fl = clamp01((xs - xl) / dx); /* fraction of the cell left of x_s */
+    for (int a = 0; a < m; ++a) ub[a] = fl * us[0][a] + (1.0 - fl) * us[1][a];
+  } else {
+    int ix = j % P->nx, iy = j / P->nx;
+    double dx = (P->x1 - P->x0) / P->nx, dy = (P->y1 - P->y0) / P->ny;
+    double fx = clamp01((xs - (P->x0 + ix * dx)) / dx); /* fraction with x < x_s */
+    double fy = clamp01((ys - (P->y0 + iy * dy)) / dy); /* fraction with y < y_s */
+    for (int a = 0; a < m; ++a)
+      ub[a] = (1.0 - fx) * (1.0 - fy) * us[0][a] + fx * (1.0 - fy) * us[1][a] + fx * fy * us[2][a] +
+              (1.0 - fx) * fy * us[3][a];
+  }
+}
+
 /* u_j^0 = (1/|Omega_j|) int <u_IC phi>_Q dx with exact cell averages of the piecewise-constant IC
  * at every node (Alg. 1 line 2; reading 17). */
 void orc_project_ic(const orc_ctx *c, const orc_ic *ic, double *uhat) {
-  const orc_problem *P = &c->P;
-  int N = c->N, Q = c->Q, m = c->m, p = P->p;
+  int N = c->N, Q = c->Q, m = c->m;
 #pragma omp parallel for schedule(static)
   for (int j = 0; j < c->cells; ++j) {
     int Nl = cell_N(c, j);
     double *uj = uhat + (size_t)j * N * m;
     for (int r = 0; r < N * m; ++r) uj[r] = 0.0;
     for (int k = 0; k < Q; ++k) {
-      const double *xi = c->xi + k * p;
-      double ub[4] = {0, 0, 0, 0}, us[4][4];
-      if (ic->kind == ORC_IC_UNIFORM) {
-        spec_state(c, &ic->state[0], xi, ub);
-      } else {
-        double xs = ic->xs0, ys = ic->ys0;
-        for (int d = 0; d < p && d < 3; ++d) {
-          xs += ic->xs1[d] * xi[d];
-          ys += ic->ys1[d] * xi[d];
-        }
-        int nreg = ic->kind == ORC_IC_STEP1D ? 2 : 4;
-        for (int r = 0; r < nreg; ++r) spec_state(c, &ic->state[r], xi, us[r]);
-        if (P->mesh_kind == ORC_MESH_1D) {
-          double dx = (P->x1 - P->x0) / P->nx;
-          double xl = P->x0 + j * dx;
-          double fl = clamp01((xs - xl) / dx); /* fraction of the cell left of x_s */
-          for (int a = 0; a < m; ++a) ub[a] = fl * us[0][a] + (1.0 - fl) * us[1][a];
-        } else {
-          int ix = j % P->nx, iy = j / P->nx;
-          double dx = (P->x1 - P->x0) / P->nx, dy = (P->y1 - P->y0) / P->ny;
-          double fx = clamp01((xs - (P->x0 + ix * dx)) / dx); /* fraction with x < x_s */
-          double fy = clamp01((ys - (P->y0 + iy * dy)) / dy); /* fraction with y < y_s */
-          for (int a = 0; a < m; ++a)
-            ub[a] = (1.0 - fx) * (1.0 - fy) * us[0][a] + fx * (1.0 - fy) * us[1][a] + fx * fy * us[2][a] +
-                    (1.0 - fx) * fy * us[3][a];
-        }
-      }
+      double ub[4];
+      ic_node_state(c, ic, j, k, ub);
       for (int i = 0; i < Nl; ++i)
         for (int a = 0; a < m; ++a) uj[i * m + a] += c->omega[k] * ub[a] * c->Phi[k * N + i];
     }
@@ -958,10 +967,47 @@ double orc_compute_dt(const orc_ctx *c, const double *lam, double t_remaining) {
  *             tri:  sum_e |e|/|Omega_j| g(u_j, u_nb; n_e)                          (edge sum)
  *   CONSERVATIVE: uhat^{n+1} = uhat^n - dt <r phi^T>_Q^T                          (reading 13)
  *   PAPER_C:      uhat^{n+1} = <(u^{(j)} - dt r) phi_{l^{n+1}}^T>_Q^T */
+/* kinetic-flux residual r_{j,k} of node k of cell j from the node states U [cells][Q][m] (the
+ * formulas in the comment above) */
+static void node_residual(const orc_ctx *c, const double *U, int j, int k, double dx_over_dt, double *r) {
+  const orc_problem *P = &c->P;
+  int m = c->m, Q = c->Q, F = c->F;
+  const double *uj = U + ((size_t)j * Q + k) * m;
+  double nb_u[4][4];
+  for (int f = 0; f < F; ++f) {
+    int nb = c->nbr[j * F + f];
+    if (nb >= 0)
+      memcpy(nb_u[f], U + ((size_t)nb * Q + k) * m, sizeof(double) * m);
+    else
+      ghost_state(c, -1 - nb, k, uj, c->nrm + (j * F + f) * 2, nb_u[f]);
+  }
+  double gp[4], gm[4];
+  for (int a = 0; a < 4; ++a) r[a] = 0.0;
+  if (P->mesh_kind == ORC_MESH_1D) {
+    double n1[2] = {1.0, 0.0};
+    orc_flux_g(c, uj, nb_u[1], n1, dx_over_dt, gp);    /* g_{j+1/2} = g(u_j, u_{j+1}) */
+    orc_flux_g(c, nb_u[0], uj, n1, dx_over_dt, gm);    /* g_{j-1/2} = g(u_{j-1}, u_j) */
+    for (int a = 0; a < m; ++a) r[a] = (gp[a] - gm[a]) * c->coef[j * 2];
+  } else if (P->mesh_kind == ORC_MESH_CART2D) {
+    double nx[2] = {1.0, 0.0}, ny[2] = {0.0, 1.0};
+    orc_flux_g(c, uj, nb_u[1], nx, 0.0, gp);
+    orc_flux_g(c, nb_u[0], uj, nx, 0.0, gm);
+    for (int a = 0; a < m; ++a) r[a] = (gp[a] - gm[a]) * c->coef[j * 4 + 0];
+    orc_flux_g(c, uj, nb_u[3], ny, 0.0, gp);
+    orc_flux_g(c, nb_u[2], uj, ny, 0.0, gm);
+    for (int a = 0; a < m; ++a) r[a] += (gp[a] - gm[a]) * c->coef[j * 4 + 2];
+  } else {
+    for (int f = 0; f < F; ++f) {
+      orc_flux_g(c, uj, nb_u[f], c->nrm + (j * F + f) * 2, 0.0, gp);
+      for (int a = 0; a < m; ++a) r[a] += c->coef[j * F + f] * gp[a];
+    }
+  }
+}
+
 static void flux_update_states(const orc_ctx *c, const double *U, const int32_t *new_level,
                                const double *uhat_old, double *uhat_new, double dt) {
   const orc_problem *P = &c->P;
-  int N = c->N, m = c->m, Q = c->Q, F = c->F;
+  int N = c->N, m = c->m, Q = c->Q;
   double dx_over_dt = (P->mesh_kind == ORC_MESH_1D) ? ((P->x1 - P->x0) / P->nx) / dt : 0.0;
 #pragma omp parallel for schedule(static)
   for (int j = 0; j < c->cells; ++j) {
@@ -972,34 +1018,8 @@ static void flux_update_states(const orc_ctx *c, const double *U, const int32_t 
     for (int r = 0; r < N * m; ++r) acc[r] = 0.0;
     for (int k = 0; k < Q; ++k) {
       const double *uj = U + ((size_t)j * Q + k) * m;
-      double nb_u[4][4];
-      for (int f = 0; f < F; ++f) {
-        int nb = c->nbr[j * F + f];
-        if (nb >= 0)
-          memcpy(nb_u[f], U + ((size_t)nb * Q + k) * m, sizeof(double) * m);
-        else
-          ghost_state(c, -1 - nb, k, uj, c->nrm + (j * F + f) * 2, nb_u[f]);
-      }
-      double r[4] = {0, 0, 0, 0}, gp[4], gm[4];
-      if (P->mesh_kind == ORC_MESH_1D) {
-        double n1[2] = {1.0, 0.0};
-        orc_flux_g(c, uj, nb_u[1], n1, dx_over_dt, gp);    /* g_{j+1/2} = g(u_j, u_{j+1}) */
-        orc_flux_g(c, nb_u[0], uj, n1, dx_over_dt, gm);    /* g_{j-1/2} = g(u_{j-1}, u_j) */
-        for (int a = 0; a < m; ++a) r[a] = (gp[a] - gm[a]) * c->coef[j * 2];
-      } else if (P->mesh_kind == ORC_MESH_CART2D) {
-        double nx[2] = {1.0, 0.0}, ny[2] = {0.0, 1.0};
-        orc_flux_g(c, uj, nb_u[1], nx, 0.0, gp);
-        orc_flux_g(c, nb_u[0], uj, nx, 0.0, gm);
-        for (int a = 0; a < m; ++a) r[a] = (gp[a] - gm[a]) * c->coef[j * 4 + 0];
-        orc_flux_g(c, uj, nb_u[3], ny, 0.0, gp);
-        orc_flux_g(c, nb_u[2], uj, ny, 0.0, gm);
-        for (int a = 0; a < m; ++a) r[a] += (gp[a] - gm[a]) * c->coef[j * 4 + 2];
-      } else {
-        for (int f = 0; f < F; ++f) {
-          orc_flux_g(c, uj, nb_u[f], c->nrm + (j * F + f) * 2, 0.0, gp);
-          for (int a = 0; a < m; ++a) r[a] += c->coef[j * F + f] * gp[a];
-        }
-      }
+      double r[4];
+      node_residual(c, U, j, k, dx_over_dt, r);
       for (int i = 0; i < Nnew; ++i)
         for (int a = 0; a < m; ++a) {
           if (P->update_form == ORC_UPDATE_PAPER_C)
@@ -1100,4 +1120,56 @@ int orc_step(orc_ctx *c, double *uhat, double *lam, double t_remaining, int32_t 
   if (residual) *residual = res;
   free(U); free(unew); free(st); free(newlev);
   return worst;
+}
+
+
+/* ---- Stochastic Collocation (reading 32) -------------
+ * The deterministic finite-volume solver with the same numerical flux g runs at every quadrature
+ * point; the points advance together with one CFL step (the paper's coupled collocation code,
+ * PAPER.md:463), and the moments come from the quadrature rule uhat_i = sum_k w_k u(xi_k) phi_i(xi_k). */
+void orc_sc_init(const orc_ctx *c, const orc_ic *ic, double *U) {
+  int Q = c->Q, m = c->m;
+#pragma omp parallel for schedule(static)
+  for (int j = 0; j < c->cells; ++j)
+    for (int k = 0; k < Q; ++k) {
+      double ub[4];
+      ic_node_state(c, ic, j, k, ub);
+      for (int a = 0; a < m; ++a) U[((size_t)j * Q + k) * m + a] = ub[a];
+    }
+}
+
+/* one step: dt = CFL / max rate over all node (and ghost) states, u_k^{n+1} = u_k^n - dt r_k(u^n);
+ * residual = sum_j |Omega_j| |sum_k w_k (u_k^{n+1} - u_k^n)_0| (PAPER.md:238-241 on the mean) */
+double orc_sc_step(const orc_ctx *c, const double *U, double *Unew, double t_remaining, double *residual) {
+  const orc_problem *P = &c->P;
+  int Q = c->Q, m = c->m;
+  double dt = dt_from_states(c, U, t_remaining);
+  double dx_over_dt = (P->mesh_kind == ORC_MESH_1D) ? ((P->x1 - P->x0) / P->nx) / dt : 0.0;
+  double res = 0.0;
+#pragma omp parallel for schedule(static) reduction(+ : res)
+  for (int j = 0; j < c->cells; ++j) {
+    double dmean = 0.0;
+    for (int k = 0; k < Q; ++k) {
+      double r[4];
+      node_residual(c, U, j, k, dx_over_dt, r);
+      const double *uj = U + ((size_t)j * Q + k) * m;
+      double *un = Unew + ((size_t)j * Q + k) * m;
+      for (int a = 0; a < m; ++a) un[a] = uj[a] - dt * r[a];
+      dmean += c->omega[k] * (un[0] - uj[0]);
+    }
+    res += c->area[j] * fabs(dmean);
+  }
+  if (residual) *residual = res;
+  return dt;
+}
+
+void orc_sc_moments(const orc_ctx *c, const double *U, double *uhat) {
+  int N = c->N, Q = c->Q, m = c->m;
+  for (int j = 0; j < c->cells; ++j) {
+    double *uj = uhat + (size_t)j * N * m;
+    for (int r = 0; r < N * m; ++r) uj[r] = 0.0;
+    for (int k = 0; k < Q; ++k)
+      for (int i = 0; i < N; ++i)
+        for (int a = 0; a < m; ++a) uj[i * m + a] += c->omega[k] * U[((size_t)j * Q + k) * m + a] * c->Phi[k * N + i];
+  }
 }

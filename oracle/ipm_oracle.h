@@ -104,6 +104,10 @@ typedef struct orc_ctx orc_ctx;
 
 orc_ctx *orc_create(const orc_problem *P);
 int orc_retard_stage(const orc_ctx *c); /* refinement retardation stage (Alg. 4) */
+/* Stochastic Collocation: node states U [cells][Q][m] */
+void orc_sc_init(const orc_ctx *c, const orc_ic *ic, double *U);
+double orc_sc_step(const orc_ctx *c, const double *U, double *Unew, double t_remaining, double *residual);
+void orc_sc_moments(const orc_ctx *c, const double *U, double *uhat);
 void orc_destroy(orc_ctx *c);
 /* sizes */
 int orc_N(const orc_ctx *c);

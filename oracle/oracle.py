@@ -98,6 +98,9 @@ def lib():
             "orc_indicator": (C.c_double, [P, C.c_int, D]),
             "orc_set_levels": (None, [P, I]), "orc_get_levels": (None, [P, I]),
             "orc_retard_stage": (C.c_int, [P]),
+            "orc_sc_init": (None, [P, C.POINTER(ICSpec), D]),
+            "orc_sc_step": (C.c_double, [P, D, D, C.c_double, D]),
+            "orc_sc_moments": (None, [P, D, D]),
             "orc_dual_solve_all": (None, [P, D, D, I, I, D]),
             "orc_compute_dt": (C.c_double, [P, D, C.c_double]),
             "orc_cell_rates": (None, [P, D, D]),
@@ -297,6 +300,38 @@ class Oracle:
         return g
 
     # --- fields -------------------------------------------------------------
+    def _ic_spec(self, ic):
+        spec = ICSpec()
+        spec.kind = IC[ic["kind"]]
+        spec.xs0, spec.ys0 = ic.get("xs0", 0.0), ic.get("ys0", 0.0)
+        for d, v in enumerate(ic.get("xs1", ())):
+            spec.xs1[d] = v
+        for d, v in enumerate(ic.get("ys1", ())):
+            spec.ys1[d] = v
+        for r, s in enumerate(ic["states"]):
+            spec.state[r] = _spec(s)
+        return spec
+
+    # --- Stochastic Collocation (reading 32) -------------------
+    def sc_init(self, ic: dict | None = None):
+        """node states [cells][Q][m] of the IC (cell averages at every quadrature point)"""
+        spec = self._ic_spec(ic or self.cfg["ic"])
+        U = np.zeros((self.cells, self.Q, self.m))
+        lib().orc_sc_init(self.ctx, C.byref(spec), _d(U))
+        return U
+
+    def sc_step(self, U, t_remaining=np.inf):
+        """one coupled collocation step; returns (new states, dt, residual)"""
+        Un = np.zeros_like(U)
+        res = C.c_double()
+        dt = lib().orc_sc_step(self.ctx, _d(U), _d(Un), float(t_remaining), C.byref(res))
+        return Un, dt, res.value
+
+    def sc_moments(self, U):
+        u = self.zeros()
+        lib().orc_sc_moments(self.ctx, _d(U), _d(u))
+        return u
+
     def project_ic(self, ic: dict | None = None):
         ic = ic or self.cfg["ic"]
         spec = ICSpec()

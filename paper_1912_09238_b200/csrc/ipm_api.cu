@@ -770,8 +770,7 @@ ipm_status ipm_partition_query(const ipm_config* cfg, int64_t* cells, int64_t* n
   return IPM_OK;
 }
 
-ipm_status ipm_project_ic(ipm_ctx* c, const ipm_ic* ic, double* d_uhat) {
-  if (!c || !ic || !d_uhat) return fail(IPM_ERR_ARG, "null argument");
+static ipm_status project_ic_impl(ipm_ctx* c, const ipm_ic* ic, double* d_uhat, double* d_nodes) {
   const ipm_config& C = c->cfg;
   const int Q = c->Q, m = c->m, p = c->p;
   const int R = ic->kind == IPM_IC_UNIFORM ? 1 : (ic->kind == IPM_IC_STEP1D ? 2 : 4);
@@ -803,13 +802,52 @@ ipm_status ipm_project_ic(ipm_ctx* c, const ipm_ic* ic, double* d_uhat) {
   }
   const double dx = C.nx > 0 ? (C.x1 - C.x0) / C.nx : 0.0, dy = C.ny > 0 ? (C.y1 - C.y0) / C.ny : 0.0;
   int rc = ipm::launch_project_ic(c->k, d_reg, d_split, ic->kind, C.nx, C.x0, C.y0, dx, dy,
-                                  C.n_levels > 0 ? c->d_level : nullptr, c->d_gid, d_uhat);
+                                  C.n_levels > 0 ? c->d_level : nullptr, c->d_gid, d_uhat, d_nodes);
   ipm::StepScalars s{};
   cudaMemcpy(c->d_sc, &s, sizeof(s), cudaMemcpyHostToDevice);  // t = 0
   cudaStreamSynchronize(c->stream);
   cudaFree(d_reg);
   cudaFree(d_split);
   return launch_rc(rc, "project_ic");
+}
+
+ipm_status ipm_project_ic(ipm_ctx* c, const ipm_ic* ic, double* d_uhat) {
+  if (!c || !ic || !d_uhat) return fail(IPM_ERR_ARG, "null argument");
+  return project_ic_impl(c, ic, d_uhat, nullptr);
+}
+
+// ---- Stochastic Collocation (reading 32) -----------------------------------
+ipm_status ipm_sc_init(ipm_ctx* c, const ipm_ic* ic, double* d_nodes) {
+  if (!c || !ic || !d_nodes) return fail(IPM_ERR_ARG, "null argument");
+  if (c->halo > 0 || !c->part.send_local.empty()) return fail(IPM_ERR_ARG, "SC: single-rank contexts only");
+  return project_ic_impl(c, ic, nullptr, d_nodes);
+}
+
+ipm_status ipm_sc_step(ipm_ctx* c, const double* d_in, double* d_out, double t_end, ipm_step_info* info) {
+  if (!c || !d_in || !d_out || d_in == d_out) return fail(IPM_ERR_ARG, "null or aliased argument");
+  if (c->halo > 0 || !c->part.send_local.empty()) return fail(IPM_ERR_ARG, "SC: single-rank contexts only");
+  const ipm::KernelCtx& k = c->k;
+  if (int rc = ipm::launch_step_begin(k, c->ghost_rate)) return launch_rc(rc, "step_begin");
+  if (int rc = ipm::launch_sc_rate(k, d_in)) return launch_rc(rc, "sc_rate");
+  if (int rc = ipm::launch_dt(k, t_end, -1.0, c->cfg.cfl)) return launch_rc(rc, "dt");
+  if (int rc = ipm::launch_sc_update(k, d_in, d_out)) return launch_rc(rc, "sc_update");
+  if (info) {
+    ipm::StepScalars s;
+    CUDA_OK(cudaMemcpyAsync(&s, c->d_sc, sizeof(s), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+    info->dt = s.dt;
+    info->t = s.t;
+    info->residual = s.residual;
+    info->newton_iters = 0;
+    info->failed_cells = 0;
+    info->worst_status = 0;
+  }
+  return IPM_OK;
+}
+
+ipm_status ipm_sc_moments(ipm_ctx* c, const double* d_nodes, double* d_uhat) {
+  if (!c || !d_nodes || !d_uhat) return fail(IPM_ERR_ARG, "null argument");
+  return launch_rc(ipm::launch_sc_moments(c->k, d_nodes, d_uhat), "sc_moments");
 }
 
 ipm_status ipm_warm_start(ipm_ctx* c, const double* d_uhat, double* d_lambda) {

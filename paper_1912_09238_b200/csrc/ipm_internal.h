@@ -122,11 +122,14 @@ int launch_dual(const KernelCtx& k, const DualLaunch& a);
 const char* last_dual_kernel();
 const char* last_flux_kernel();
 int launch_retard(const KernelCtx& k);
+int launch_sc_rate(const KernelCtx& k, const double* Uin);
+int launch_sc_update(const KernelCtx& k, const double* Uin, double* Uout);
+int launch_sc_moments(const KernelCtx& k, const double* U, double* uhat);
 int launch_dt(const KernelCtx& k, double t_end, double dt_fixed, double cfl);
 int launch_flux(const KernelCtx& k, const FluxLaunch& a);
 int launch_project_ic(const KernelCtx& k, const double* d_region /*[R][Q][m]*/, const double* d_split /*[Q][2]*/,
                       int ic_kind, int nx, double x0, double y0, double dx, double dy, const int32_t* level,
-                      const int64_t* gid, double* uhat);
+                      const int64_t* gid, double* uhat, double* unodes = nullptr);
 // pack duals of the listed local cells into a contiguous send buffer [n][N][m]
 int launch_pack(const KernelCtx& k, const double* lam, const int32_t* idx, int64_t n, double* out);
 int launch_warm_start(const KernelCtx& k, const double* uhat, double* lam);

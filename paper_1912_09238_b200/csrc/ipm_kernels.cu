@@ -526,6 +526,114 @@ __global__ void __launch_bounds__(256) k_flux_warp(FluxParams P) {
 }
 
 // ------------------------------------------------------------------------------------------------
+// Stochastic Collocation (reading 32): the deterministic
+// finite-volume scheme with the same numerical flux at every quadrature node, all nodes advancing
+// with one CFL step. Node states [cells][m][Q] (the flux kernels' layout); warp per cell, lanes over
+// nodes; the residual is the change of the mean, sum_j |Omega_j| |sum_k w_k (u^{n+1} - u^n)_0|.
+// ------------------------------------------------------------------------------------------------
+template <int MS>
+__global__ void k_sc_rate(int64_t cells, int Q, Mesh mesh, double gamma, const double* __restrict__ U,
+                          StepScalars* sc) {
+  double my = 0.0;
+  const int64_t n = cells * Q;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t cell = t / Q;
+    const int k = (int)(t - cell * Q);
+    double u[MS];
+#pragma unroll
+    for (int a = 0; a < MS; ++a) u[a] = U[cell * Q * MS + a * Q + k];
+    my = fmax(my, node_rate<0, MS>(u, mesh, cell, gamma));
+  }
+  my = warp_max(my);
+  if ((threadIdx.x & 31) == 0 && my > 0.0) atomicMax(&sc->rate_bits, (unsigned long long)__double_as_longlong(my));
+}
+
+template <int FX, int MS, int MK>
+__global__ void __launch_bounds__(256) k_sc_update(FluxParams P, const double* __restrict__ Uin,
+                                                   double* __restrict__ Uout) {
+  const int Q = P.T.Q;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const double dt = P.sc->dt, gam = P.cl.gamma;
+  const int F = P.mesh.F;
+  double my_res = 0.0;
+  for (int64_t cell = (int64_t)blockIdx.x * nw + warp; cell < P.mesh.cells; cell += (int64_t)gridDim.x * nw) {
+    double dmean = 0.0;
+    for (int k = lane; k < Q; k += 32) {
+      double uj[MS], r[MS], gneg[MS];
+      const double* src = Uin + cell * Q * MS + k;
+#pragma unroll
+      for (int a = 0; a < MS; ++a) {
+        uj[a] = src[a * Q];
+        r[a] = 0.0;
+      }
+      for (int f = 0; f < F; ++f) {
+        const int nbc = P.mesh.nbr[cell * F + f];
+        double un[MS], nv[2];
+        if (MK == MK_TRI) {
+          nv[0] = P.mesh.nrm[(cell * F + f) * 2];
+          nv[1] = P.mesh.nrm[(cell * F + f) * 2 + 1];
+        } else {
+          nv[0] = (f >> 1) == 0 ? 1.0 : 0.0;
+          nv[1] = (f >> 1) == 1 ? 1.0 : 0.0;
+        }
+        if (nbc >= 0) {
+          const double* s2 = Uin + (int64_t)nbc * Q * MS + k;
+#pragma unroll
+          for (int a = 0; a < MS; ++a) un[a] = s2[a * Q];
+        } else {
+          const int tag = -1 - nbc;
+          const int kind = P.mesh.bc_kind[tag];
+          if (kind == 1) {
+            const double* gs = P.mesh.ghost + ((int64_t)tag * Q + k) * MS;
+#pragma unroll
+            for (int a = 0; a < MS; ++a) un[a] = gs[a];
+          } else if (kind == 2 && MS > 1) {  // slip wall: mirror the normal momentum
+            const double sgn = (MK == MK_TRI || (f & 1)) ? 1.0 : -1.0;
+            const double on[2] = {nv[0] * sgn, nv[1] * sgn};
+            double mn = 0.0;
+#pragma unroll
+            for (int d = 0; d < MS - 2; ++d) mn += uj[1 + d] * on[d];
+            un[0] = uj[0];
+#pragma unroll
+            for (int d = 0; d < MS - 2; ++d) un[1 + d] = uj[1 + d] - 2.0 * mn * on[d];
+            un[MS - 1] = uj[MS - 1];
+          } else {
+#pragma unroll
+            for (int a = 0; a < MS; ++a) un[a] = uj[a];
+          }
+        }
+        const double cf = P.mesh.coef[cell * F + f];
+        if (MK == MK_TRI) {
+          double gf[MS];
+          NumFlux<FX, MS>::g(uj, un, nv, gam, 0.0, gf);
+#pragma unroll
+          for (int a = 0; a < MS; ++a) r[a] = fma(cf, gf[a], r[a]);
+        } else if ((f & 1) == 0) {
+          NumFlux<FX, MS>::g(un, uj, nv, gam, 1.0 / (cf * dt), gneg);
+        } else {
+          double gpos[MS];
+          NumFlux<FX, MS>::g(uj, un, nv, gam, 1.0 / (cf * dt), gpos);
+#pragma unroll
+          for (int a = 0; a < MS; ++a) r[a] += (gpos[a] - gneg[a]) * cf;
+        }
+      }
+      double* dst = Uout + cell * Q * MS + k;
+      double u0n = 0.0;
+#pragma unroll
+      for (int a = 0; a < MS; ++a) {
+        const double v = uj[a] - dt * r[a];
+        dst[a * Q] = v;
+        if (a == 0) u0n = v;
+      }
+      dmean = fma(P.T.omega[k], u0n - uj[0], dmean);
+    }
+    dmean = warp_sum(dmean);
+    if (lane == 0) my_res += P.mesh.area[cell] * fabs(dmean);
+  }
+  if (lane == 0 && my_res != 0.0) atomicAdd(&P.sc->residual, my_res);
+}
+
+// ------------------------------------------------------------------------------------------------
 // flux kernel for 1D / cartesian meshes: CPW = 8/m cells per warp so that the projection
 // Phi^T(omega o r) of all of them is one set of DMMAs (columns = (cell, state) pairs):
 //   flux    lanes over (cell, node): the node's physical flux along each direction is formed once
@@ -748,7 +856,7 @@ template <int MS>
 __global__ void k_project_ic(Tables T, int64_t cells, const double* __restrict__ region,
                              const double* __restrict__ split, int kind, int nx, double x0, double y0, double dx,
                              double dy, const int32_t* __restrict__ level, const int64_t* __restrict__ gid, Adapt ad,
-                             double* __restrict__ uhat) {
+                             double* __restrict__ uhat, double* __restrict__ unodes) {
   extern __shared__ __align__(16) double sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int Q = T.Q, N = T.N;
@@ -780,8 +888,13 @@ __global__ void k_project_ic(Tables T, int64_t cells, const double* __restrict__
       }
 #pragma unroll
       for (int a = 0; a < MS; ++a) q[k * MS + a] = ub[a];
+      if (unodes) {  // Stochastic Collocation: the node states themselves, [cell][state][node]
+#pragma unroll
+        for (int a = 0; a < MS; ++a) unodes[cell * Q * MS + a * Q + k] = ub[a];
+      }
     }
     __syncwarp();
+    if (!uhat) continue;
     const int Nl = (ad.n_levels > 0 && level) ? ad.Nl[level[cell]] : N;
     for (int r = lane; r < N * MS; r += 32) {
       const int i = r / MS, a = r - i * MS;
@@ -1234,9 +1347,66 @@ int launch_flux(const KernelCtx& k, const FluxLaunch& a) {
   return -1;
 }
 
+template <int FX, int MS, int MK>
+static int sc_impl(const KernelCtx& k, const double* Uin, double* Uout) {
+  const int threads = 256;
+  const int64_t n = k.mesh.cells * k.T.Q;
+  const int rgrid = (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, (int64_t)k.sm_count * 8));
+  k_sc_rate<MS><<<rgrid, threads, 0, S(k)>>>(k.mesh.cells, k.T.Q, k.mesh, k.cl.gamma, Uin, k.sc);
+  return (int)cudaGetLastError();
+}
+template <int FX, int MS, int MK>
+static int sc_update_impl(const KernelCtx& k, const double* Uin, double* Uout) {
+  const int64_t want = (k.mesh.cells + 7) / 8;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)k.sm_count * 8));
+  FluxParams P{k.T, k.mesh, k.cl, k.ad, FluxLaunch{}, k.sc, 0};
+  k_sc_update<FX, MS, MK><<<grid, 256, 0, S(k)>>>(P, Uin, Uout);
+  return (int)cudaGetLastError();
+}
+#define IPM_SC_DISPATCH(FN)                                                                          \
+  switch ((k.flux * 10 + k.m) * 10 + k.mesh.kind) {                                                 \
+    case (FX_LF_GLOBAL * 10 + 1) * 10 + MK_1D: return FN<FX_LF_GLOBAL, 1, MK_1D>(k, Uin, Uout);     \
+    case (FX_HLL * 10 + 3) * 10 + MK_1D: return FN<FX_HLL, 3, MK_1D>(k, Uin, Uout);                 \
+    case (FX_RUSANOV * 10 + 3) * 10 + MK_1D: return FN<FX_RUSANOV, 3, MK_1D>(k, Uin, Uout);         \
+    case (FX_RUSANOV * 10 + 4) * 10 + MK_CART: return FN<FX_RUSANOV, 4, MK_CART>(k, Uin, Uout);     \
+    case (FX_HLL * 10 + 4) * 10 + MK_CART: return FN<FX_HLL, 4, MK_CART>(k, Uin, Uout);             \
+    case (FX_RUSANOV * 10 + 4) * 10 + MK_TRI: return FN<FX_RUSANOV, 4, MK_TRI>(k, Uin, Uout);       \
+  }                                                                                                  \
+  return -1;
+int launch_sc_rate(const KernelCtx& k, const double* Uin) {
+  double* Uout = nullptr;
+  IPM_SC_DISPATCH(sc_impl)
+}
+int launch_sc_update(const KernelCtx& k, const double* Uin, double* Uout) { IPM_SC_DISPATCH(sc_update_impl) }
+
+template <int MS>
+__global__ void k_sc_moments(Tables T, int64_t cells, const double* __restrict__ U, double* __restrict__ uhat) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int N = T.N, Q = T.Q;
+  for (int64_t cell = (int64_t)blockIdx.x * nw + warp; cell < cells; cell += (int64_t)gridDim.x * nw)
+    for (int r = lane; r < N * MS; r += 32) {
+      const int i = r / MS, a = r - i * MS;
+      double s = 0.0;
+      for (int k = 0; k < Q; ++k) s = fma(T.WPhiT[i * T.QP + k], U[cell * Q * MS + a * Q + k], s);
+      uhat[cell * N * MS + r] = s;
+    }
+}
+int launch_sc_moments(const KernelCtx& k, const double* U, double* uhat) {
+  const int64_t want = (k.mesh.cells + 7) / 8;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)k.sm_count * 8));
+  switch (k.m) {
+    case 1: k_sc_moments<1><<<grid, 256, 0, S(k)>>>(k.T, k.mesh.cells, U, uhat); break;
+    case 3: k_sc_moments<3><<<grid, 256, 0, S(k)>>>(k.T, k.mesh.cells, U, uhat); break;
+    case 4: k_sc_moments<4><<<grid, 256, 0, S(k)>>>(k.T, k.mesh.cells, U, uhat); break;
+    default: return -1;
+  }
+  return (int)cudaGetLastError();
+}
+
 template <int MS>
 static int ic_impl(const KernelCtx& k, const double* region, const double* split, int kind, int nx, double x0,
-                   double y0, double dx, double dy, const int32_t* level, const int64_t* gid, double* uhat) {
+                   double y0, double dx, double dy, const int32_t* level, const int64_t* gid, double* uhat,
+                   double* unodes) {
   const size_t pw = (size_t)(k.T.Q * MS + 1) * 8;
   const int warps = (int)std::min<size_t>(8, k.smem_optin / pw);
   if (warps < 1) return -1;
@@ -1246,16 +1416,17 @@ static int ic_impl(const KernelCtx& k, const double* region, const double* split
   const int64_t want = (k.mesh.cells + warps - 1) / warps;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)k.sm_count * 8));
   kern<<<grid, warps * 32, smem, S(k)>>>(k.T, k.mesh.cells, region, split, kind, nx, x0, y0, dx, dy, level, gid,
-                                         k.ad, uhat);
+                                         k.ad, uhat, unodes);
   return (int)cudaGetLastError();
 }
 
 int launch_project_ic(const KernelCtx& k, const double* region, const double* split, int kind, int nx, double x0,
-                      double y0, double dx, double dy, const int32_t* level, const int64_t* gid, double* uhat) {
+                      double y0, double dx, double dy, const int32_t* level, const int64_t* gid, double* uhat,
+                      double* unodes) {
   switch (k.m) {
-    case 1: return ic_impl<1>(k, region, split, kind, nx, x0, y0, dx, dy, level, gid, uhat);
-    case 3: return ic_impl<3>(k, region, split, kind, nx, x0, y0, dx, dy, level, gid, uhat);
-    case 4: return ic_impl<4>(k, region, split, kind, nx, x0, y0, dx, dy, level, gid, uhat);
+    case 1: return ic_impl<1>(k, region, split, kind, nx, x0, y0, dx, dy, level, gid, uhat, unodes);
+    case 3: return ic_impl<3>(k, region, split, kind, nx, x0, y0, dx, dy, level, gid, uhat, unodes);
+    case 4: return ic_impl<4>(k, region, split, kind, nx, x0, y0, dx, dy, level, gid, uhat, unodes);
   }
   return -1;
 }

@@ -26,7 +26,7 @@ CELL_STATUS = {0: "ok", 1: "nonconvergence", 2: "illconditioned", 3: "linesearch
 
 EXPORTS = [
     "ipm_init", "ipm_destroy", "ipm_status_string", "ipm_last_error", "ipm_sizes", "ipm_get_basis",
-    "ipm_get_cell_ids", "ipm_dual_solve", "ipm_flux_update", "ipm_step", "ipm_step_host", "ipm_project_ic", "ipm_warm_start",
+    "ipm_get_cell_ids", "ipm_dual_solve", "ipm_flux_update", "ipm_step", "ipm_step_host", "ipm_sc_init", "ipm_sc_step", "ipm_sc_moments", "ipm_project_ic", "ipm_warm_start",
     "ipm_moments_from_dual", "ipm_stress_dual", "ipm_get_levels", "ipm_set_levels", "ipm_last_cell_stats",
     "ipm_get_time", "ipm_set_time", "ipm_last_kernel_ms", "ipm_enable_timing", "ipm_last_dual_kernel", "ipm_last_flux_kernel", "ipm_retard_stage", "ipm_retard_advance",
     "ipm_debug_phase_cycles", "ipm_step_dual", "ipm_step_flux", "ipm_halo_layout", "ipm_partition_query",
@@ -102,6 +102,9 @@ def lib():
             "ipm_step": (st, [P, D, D, C.c_double, C.POINTER(ipm_step_info)]),
             "ipm_step_host": (st, [P, D, D, D, D, C.c_double, C.c_int32, C.POINTER(ipm_step_info)]),
             "ipm_project_ic": (st, [P, C.POINTER(ipm_ic), D]),
+            "ipm_sc_init": (st, [P, C.POINTER(ipm_ic), D]),
+            "ipm_sc_step": (st, [P, D, D, C.c_double, C.POINTER(ipm_step_info)]),
+            "ipm_sc_moments": (st, [P, D, D]),
             "ipm_warm_start": (st, [P, D, D]),
             "ipm_moments_from_dual": (st, [P, D, D]),
             "ipm_stress_dual": (st, [P, D, D, C.c_double, C.c_double, D]),
@@ -344,6 +347,37 @@ class Context:
         return info
 
     # --- helpers ----------------------------------------------------------------------------
+    def _ic(self, ic):
+        s = ipm_ic()
+        s.kind = IC[ic["kind"]]
+        s.initial_level = self.cfg.get("initial_level", 0)
+        s.xs0, s.ys0 = ic.get("xs0", 0.0), ic.get("ys0", 0.0)
+        for d, v in enumerate(ic.get("xs1", ())):
+            s.xs1[d] = v
+        for d, v in enumerate(ic.get("ys1", ())):
+            s.ys1[d] = v
+        for r, st in enumerate(ic["states"]):
+            s.state[r] = _state(st)
+        return s
+
+    # --- Stochastic Collocation (ipm.h ipm_sc_*) ----------------------------------------------
+    def sc_zeros(self):
+        """node-state buffer [cells][m][Q]"""
+        return self.torch.zeros((self.cells, self.m, self.Q), dtype=self.torch.float64, device=self.device)
+
+    def ipm_sc_init(self, nodes, ic: dict | None = None):
+        check(lib().ipm_sc_init(self.h, C.byref(self._ic(ic or self.cfg["ic"])), _ptr(nodes)), "ipm_sc_init")
+
+    def ipm_sc_step(self, nodes_in, nodes_out, t_end=None, sync=True):
+        info = ipm_step_info() if sync else None
+        te = -1.0 if t_end is None else float(t_end)
+        check(lib().ipm_sc_step(self.h, _ptr(nodes_in), _ptr(nodes_out), te, C.byref(info) if sync else None),
+              "ipm_sc_step")
+        return info
+
+    def ipm_sc_moments(self, nodes, uhat):
+        check(lib().ipm_sc_moments(self.h, _ptr(nodes), _ptr(uhat)), "ipm_sc_moments")
+
     def ipm_project_ic(self, uhat, ic: dict | None = None):
         ic = ic or self.cfg["ic"]
         s = ipm_ic()

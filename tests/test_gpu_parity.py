@@ -136,6 +136,28 @@ def test_refinement_retardation_cfg4_parity(torch):
         assert abs(ro - rg) <= 1e-9 * max(ro, 1e-300)
 
 
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4"])
+def test_stochastic_collocation_parity(torch, name):
+    """Stochastic Collocation (reading 32) through the C-ABI against the oracle:
+    node states of the IC, coupled CFL steps with the same numerical flux, quadrature moments"""
+    cfg = configs.parity_variant(name)
+    g, o, _ = ctx_and_oracle(cfg)
+    steps = 6
+    U = o.sc_init()
+    a, b = g.sc_zeros(), g.sc_zeros()
+    g.ipm_sc_init(a)
+    np.testing.assert_allclose(to_np(a).transpose(0, 2, 1), U, rtol=1e-15, atol=0)  # FMA contraction: 1 ulp
+    for _ in range(steps):
+        U, dt_o, res_o = o.sc_step(U)
+        info = g.ipm_sc_step(a, b)
+        a, b = b, a
+        assert abs(info.dt - dt_o) <= 1e-12 * dt_o
+        assert abs(info.residual - res_o) <= 1e-9 * max(res_o, 1e-300)
+    u_g = g.zeros()
+    g.ipm_sc_moments(a, u_g)
+    assert_moments_close(to_np(u_g), o.sc_moments(U), 1e-10, f"SC {name}")
+
+
 def test_one_shot_steady_fixed_point(torch):
     from paper_1912_09238_b200 import Context
 

@@ -395,3 +395,60 @@ def test_retardation_stage_lifts_the_cap_when_the_residual_drops(oracle_mod):
     _, u2, l2, h2 = _retard_run(oracle_mod, dict(base, retard=[(1e300, 3), (1e300, 3)]), 4)
     np.testing.assert_array_equal(u2, u0)
     np.testing.assert_array_equal(l2, l0)
+
+
+# ------------------------------------------------------------------ Stochastic Collocation (reading 32)
+def _sc_run(o, steps, t_end=None):
+    U = o.sc_init()
+    t, hist = 0.0, []
+    for _ in range(steps):
+        U, dt, res = o.sc_step(U, np.inf if t_end is None else t_end - t)
+        t += dt
+        hist.append((dt, res))
+    return U, hist
+
+
+def test_sc_initial_moments_are_the_ipm_projection(oracle_mod):
+    """SC's moments are the quadrature of the node solutions, so at t = 0 they are
+    the IPM initial projection (Alg. 1 line 2) of the same cell averages"""
+    for name in ("cfg1", "cfg3"):
+        o = oracle_mod.Oracle(configs.parity_variant(name))
+        np.testing.assert_array_equal(o.sc_moments(o.sc_init()), o.project_ic())
+
+
+def test_sc_single_node_is_degree0_stochastic_galerkin(oracle_mod):
+    """one quadrature node at xi = 0 (q1d = 1): SC is the deterministic scheme for the IC at xi = 0,
+    and so is the degree-0 IPM with the quadratic entropy (SG) on the same rule"""
+    base = dict(configs.parity_variant("cfg1"), closure="quadratic", M=0, q1d=1)
+    o = oracle_mod.Oracle(base)
+    U, hist = _sc_run(o, 6)
+    u_sg, _, info = o.run(n_steps=6, record=True)
+    np.testing.assert_allclose(o.sc_moments(U), u_sg, rtol=0, atol=1e-13)
+    for (dt_sc, _), (dt_sg, _, _) in zip(hist, info["hist"]):
+        assert abs(dt_sc - dt_sg) <= 1e-15 * dt_sg
+
+
+def test_sc_xi_independent_data_stay_deterministic(oracle_mod):
+    """an IC without xi dependence gives the same solution at every node: the higher moments stay
+    zero (orthogonality of phi_i, i > 0, to 1 under the quadrature)"""
+    cfg = configs.parity_variant("cfg2")
+    cfg["ic"] = dict(cfg["ic"])
+    cfg["ic"]["states"] = [{"prim": s["prim"]} for s in cfg["ic"]["states"]]
+    cfg["ic"]["xs1"] = ()  # the split position must not depend on xi either
+    o = oracle_mod.Oracle(cfg)
+    U, _ = _sc_run(o, 5)
+    assert np.abs(U - U[:, :1, :]).max() == 0.0
+    u = o.sc_moments(U)
+    assert np.abs(u[:, 1:, :]).max() < 1e-13 * np.abs(u[:, 0, :]).max()
+
+
+def test_sc_conserves_the_mean_on_periodic_meshes(oracle_mod):
+    cfg = configs.get("cfg3", mesh=dict(nx=9, ny=7, periodic=True))
+    o = oracle_mod.Oracle(cfg)
+    area = o.geometry()[3]
+    U0 = o.sc_init()
+    U, _ = _sc_run(o, 5)
+    m0, m1 = o.sc_moments(U0), o.sc_moments(U)
+    tot0 = (area[:, None] * m0[:, 0, :]).sum(axis=0)
+    tot1 = (area[:, None] * m1[:, 0, :]).sum(axis=0)
+    np.testing.assert_allclose(tot1, tot0, rtol=1e-13, atol=1e-14)
