@@ -130,6 +130,11 @@ typedef struct {
   int32_t n_retard;
   int32_t retard_level[8];
   double retard_eps[8];
+  /* quadrature (reading 33): 0 tensor Gauss-Legendre with q1d points per dimension
+   * (default), 1 tensor Clenshaw-Curtis with q1d points (q1d <= 33), 2 Smolyak sparse grid of nested
+   * Clenshaw-Curtis rules of level quad_level (p <= quad_level <= p + 5; negative weights: cells whose
+   * Hessian is then indefinite report IPM_CELL_ILLCONDITIONED).  Rules other than 0 need n = N m <= 88. */
+  int32_t quad_kind, quad_level;
 } ipm_config;
 
 typedef struct {

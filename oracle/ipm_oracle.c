@@ -59,6 +59,106 @@ static double phi_1d(int i, double x) {
   return sqrt(2.0 * i + 1.0) * P[i];
 }
 
+/* Clenshaw-Curtis rule: nodes -cos(pi j / (n-1)), weights by the classical cosine
+ * sum w_j = c_j/(n-1) (1 - sum_{k=1}^{(n-1)/2} b_k/(4k^2-1) cos(2 k theta_j)), c_j = 1 at the ends,
+ * 2 inside, b_k = 1 for k = (n-1)/2, else 2 (n odd); n = 1: the midpoint with weight 2. */
+void orc_clenshaw_curtis(int n, double *x, double *w) {
+  if (n == 1) {
+    x[0] = 0.0;
+    w[0] = 2.0;
+    return;
+  }
+  int Nn = n - 1;
+  for (int j = 0; j < n; ++j) {
+    double th = PI_ * j / Nn;
+    x[j] = -cos(th);
+    double s = 0.0;
+    for (int k = 1; k <= Nn / 2; ++k) {
+      double b = (2 * k == Nn) ? 1.0 : 2.0;
+      s += b / (4.0 * k * k - 1.0) * cos(2.0 * k * th);
+    }
+    double cj = (j == 0 || j == Nn) ? 1.0 : 2.0;
+    w[j] = cj / Nn * (1.0 - s);
+  }
+  if (n % 2 == 1) x[Nn / 2] = 0.0; /* exact midpoint */
+}
+
+/* Smolyak formula A(L, p) = sum_{L-p+1 <= |i| <= L} (-1)^{L-|i|} C(p-1, L-|i|) (U^{i_1} x ... x U^{i_p}),
+ * i_d >= 1, U^1 the midpoint rule, U^i Clenshaw-Curtis with 2^{i-1}+1 nodes (nested); coincident
+ * nodes merged by their index on the finest 1D grid (2^{L-1}+1 nodes). */
+static int binom_(int n, int k) {
+  if (k < 0 || k > n) return 0;
+  int r = 1;
+  for (int i = 1; i <= k; ++i) r = r * (n - k + i) / i;
+  return r;
+}
+int orc_smolyak_cc(int p, int L, double *xi, double *w) {
+  int F = L - p + 1;                 /* largest 1D level in the sum */
+  int nf = F >= 2 ? (1 << (F - 1)) + 1 : 1; /* finest 1D grid */
+  int ngrid = 1;
+  for (int d = 0; d < p; ++d) ngrid *= nf;
+  double *acc = (double *)calloc(ngrid, sizeof(double));
+  char *used = (char *)calloc(ngrid, 1);
+  int i[3] = {1, 1, 1};
+  for (;;) {
+    int s = 0;
+    for (int d = 0; d < p; ++d) s += i[d];
+    if (s >= L - p + 1 && s <= L) {
+      int coef = ((L - s) % 2 ? -1 : 1) * binom_(p - 1, L - s);
+      double xs[3][129], ws[3][129];
+      int ns[3], step[3];
+      for (int d = 0; d < p; ++d) {
+        ns[d] = i[d] == 1 ? 1 : (1 << (i[d] - 1)) + 1;
+        orc_clenshaw_curtis(ns[d], xs[d], ws[d]);
+        step[d] = ns[d] == 1 ? 0 : (nf - 1) / (ns[d] - 1);
+      }
+      int cnt = 1;
+      for (int d = 0; d < p; ++d) cnt *= ns[d];
+      for (int t = 0; t < cnt; ++t) {
+        int r = t, key = 0;
+        double wt = coef;
+        int jd[3];
+        for (int d = p - 1; d >= 0; --d) {
+          jd[d] = r % ns[d];
+          r /= ns[d];
+        }
+        for (int d = 0; d < p; ++d) {
+          int fi = ns[d] == 1 ? (nf - 1) / 2 : jd[d] * step[d];
+          key = key * nf + fi;
+          wt *= ws[d][jd[d]];
+        }
+        acc[key] += wt;
+        used[key] = 1;
+      }
+    }
+    int d = p - 1;
+    while (d >= 0) {
+      if (++i[d] <= L) break;
+      i[d] = 1;
+      --d;
+    }
+    if (d < 0) break;
+  }
+  double xf[129], wf[129];
+  orc_clenshaw_curtis(nf, xf, wf);
+  int Q = 0;
+  for (int key = 0; key < ngrid; ++key) {
+    if (!used[key]) continue;
+    if (xi) {
+      int r = key;
+      for (int d = p - 1; d >= 0; --d) {
+        xi[Q * p + d] = xf[r % nf];
+        r /= nf;
+      }
+      w[Q] = acc[key];
+    }
+    ++Q;
+  }
+  free(acc);
+  free(used);
+  return Q;
+}
+
 /* Gauss-Legendre nodes (ascending) and weights (sum 2): Newton on P_q. */
 void orc_gauss_legendre(int q, double *x, double *w) {
   double P[256];
@@ -519,7 +619,10 @@ orc_ctx *orc_create(const orc_problem *P) {
   int p = P->p;
   c->N = orc_num_basis(p, P->M);
   c->Q = 1;
-  for (int d = 0; d < p; ++d) c->Q *= P->q1d;
+  if (P->quad_kind == 2)
+    c->Q = orc_smolyak_cc(p, P->quad_level, NULL, NULL);
+  else
+    for (int d = 0; d < p; ++d) c->Q *= P->q1d;
   c->m = P->m;
   c->d = (P->mesh_kind == ORC_MESH_1D) ? 1 : 2;
   c->F = (P->mesh_kind == ORC_MESH_1D) ? 2 : (P->mesh_kind == ORC_MESH_CART2D ? 4 : 3);
@@ -527,20 +630,34 @@ orc_ctx *orc_create(const orc_problem *P) {
   int N = c->N, Q = c->Q;
   c->idx = (int32_t *)malloc(sizeof(int32_t) * N * p);
   orc_multi_indices(p, P->M, c->idx);
-  /* tensor Gauss-Legendre rule, last dimension fastest; omega_k = prod w_{k_d} / 2 (f_Xi = 2^-p) */
-  double x1[128], w1[128];
-  orc_gauss_legendre(P->q1d, x1, w1);
+  /* tensor rule (Gauss-Legendre or Clenshaw-Curtis), last dimension fastest, or the Smolyak sparse
+   * grid; omega_k = w_k 2^-p (f_Xi = 2^-p) */
+  double x1[129], w1[129];
+  if (P->quad_kind == 1)
+    orc_clenshaw_curtis(P->q1d, x1, w1);
+  else if (P->quad_kind == 0)
+    orc_gauss_legendre(P->q1d, x1, w1);
   c->xi = (double *)malloc(sizeof(double) * Q * p);
   c->omega = (double *)malloc(sizeof(double) * Q);
   c->Phi = (double *)malloc(sizeof(double) * Q * N);
+  double *wsg = NULL;
+  if (P->quad_kind == 2) {
+    wsg = (double *)malloc(sizeof(double) * Q);
+    orc_smolyak_cc(p, P->quad_level, c->xi, wsg);
+  }
   for (int k = 0; k < Q; ++k) {
-    int r = k;
     double om = 1.0;
-    for (int d = p - 1; d >= 0; --d) {
-      int kd = r % P->q1d;
-      r /= P->q1d;
-      c->xi[k * p + d] = x1[kd];
-      om *= w1[kd] / 2.0;
+    if (P->quad_kind == 2) {
+      for (int d = 0; d < p; ++d) om /= 2.0;
+      om *= wsg[k];
+    } else {
+      int r = k;
+      for (int d = p - 1; d >= 0; --d) {
+        int kd = r % P->q1d;
+        r /= P->q1d;
+        c->xi[k * p + d] = x1[kd];
+        om *= w1[kd] / 2.0;
+      }
     }
     c->omega[k] = om;
     for (int i = 0; i < N; ++i) {
@@ -549,6 +666,7 @@ orc_ctx *orc_create(const orc_problem *P) {
       c->Phi[k * N + i] = v;
     }
   }
+  free(wsg);
   build_geometry(c);
   c->bc_u = (double *)calloc((size_t)4 * Q * c->m, sizeof(double));
   for (int t = 0; t < 4; ++t)

@@ -90,6 +90,10 @@ typedef struct {
   int32_t n_retard;
   int32_t retard_level[8];
   double retard_eps[8];
+  /* quadrature (reading 33): 0 tensor Gauss-Legendre with q1d points per
+   * dimension, 1 tensor Clenshaw-Curtis with q1d points, 2 Smolyak sparse grid of nested
+   * Clenshaw-Curtis rules of level quad_level */
+  int32_t quad_kind, quad_level;
 } orc_problem;
 
 typedef struct {
@@ -117,6 +121,12 @@ int orc_cells(const orc_ctx *c);
 /* random space */
 void orc_gauss_legendre(int q, double *x, double *w);
 int orc_num_basis(int p, int M);
+/* Clenshaw-Curtis nodes x_j = -cos(pi j/(n-1)) (ascending) and weights (sum 2) */
+void orc_clenshaw_curtis(int n, double *x, double *w);
+/* Smolyak sparse grid of nested Clenshaw-Curtis rules (level L >= p, dimension p): number of points,
+ * and (when xi/w are non-NULL) points [Q][p] in lexicographic order of their finest-grid indices,
+ * weights summing to 2^p */
+int orc_smolyak_cc(int p, int L, double *xi, double *w);
 void orc_multi_indices(int p, int M, int32_t *idx);
 void orc_get_quadrature(const orc_ctx *c, double *xi, double *omega, double *Phi);
 void orc_get_geometry(const orc_ctx *c, int32_t *nbr, double *nrm, double *coef, double *area);

@@ -59,6 +59,7 @@ class Problem(C.Structure):
         ("delta_dec", C.c_double), ("delta_inc", C.c_double),
         ("n_threads", C.c_int32),
         ("n_retard", C.c_int32), ("retard_level", C.c_int32 * 8), ("retard_eps", C.c_double * 8),
+        ("quad_kind", C.c_int32), ("quad_level", C.c_int32),
     ]
 
 
@@ -80,7 +81,9 @@ def lib():
         sig = {
             "orc_create": (P, [C.POINTER(Problem)]), "orc_destroy": (None, [P]),
             "orc_N": (C.c_int, [P]), "orc_Q": (C.c_int, [P]), "orc_cells": (C.c_int, [P]),
-            "orc_gauss_legendre": (None, [C.c_int, D, D]), "orc_num_basis": (C.c_int, [C.c_int, C.c_int]),
+            "orc_gauss_legendre": (None, [C.c_int, D, D]),
+            "orc_clenshaw_curtis": (None, [C.c_int, D, D]),
+            "orc_smolyak_cc": (C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_void_p]), "orc_num_basis": (C.c_int, [C.c_int, C.c_int]),
             "orc_multi_indices": (None, [C.c_int, C.c_int, I]),
             "orc_get_quadrature": (None, [P, D, D, D]), "orc_get_geometry": (None, [P, I, D, D, D]),
             "orc_closure_u": (C.c_int, [P, D, D]), "orc_closure_du": (C.c_int, [P, D, D]),
@@ -150,6 +153,19 @@ def multi_indices(p: int, M: int) -> np.ndarray:
     return out
 
 
+def clenshaw_curtis(n: int):
+    x, w = np.zeros(n), np.zeros(n)
+    lib().orc_clenshaw_curtis(n, _d(x), _d(w))
+    return x, w
+
+
+def smolyak_cc(p: int, L: int):
+    Q = lib().orc_smolyak_cc(p, L, None, None)
+    xi, w = np.zeros((Q, p)), np.zeros(Q)
+    lib().orc_smolyak_cc(p, L, xi.ctypes.data, w.ctypes.data)
+    return xi, w
+
+
 def gauss_legendre(q: int):
     x, w = np.zeros(q), np.zeros(q)
     lib().orc_gauss_legendre(q, _d(x), _d(w))
@@ -195,6 +211,10 @@ class Oracle:
             P.level_M[k] = Mk
         P.delta_dec, P.delta_inc = cfg.get("delta_dec", 0.0), cfg.get("delta_inc", 0.0)
         P.n_threads = n_threads
+        # quadrature (reading 33): "gl" tensor Gauss-Legendre, "cc" tensor Clenshaw-Curtis (q1d points),
+        # "smolyak" sparse grid of nested Clenshaw-Curtis rules of level quad_level
+        P.quad_kind = {"gl": 0, "cc": 1, "smolyak": 2}[cfg.get("quad", "gl")]
+        P.quad_level = cfg.get("quad_level", 0)
         # refinement retardation (Alg. 4): [(eps_l, level index cap l*_l), ...]
         retard = cfg.get("retard") or []
         P.n_retard = len(retard)

@@ -8,6 +8,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
+#include <map>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -79,6 +81,101 @@ void gauss_legendre(int q, std::vector<double>& x, std::vector<double>& w) {
     w[q - k] = wk;
   }
   if (q % 2 == 1) x[q / 2] = 0.0;
+}
+
+// Clenshaw-Curtis rule with n points (reading 33): nodes -cos(pi j/(n-1)); weights
+// from the exactness conditions sum_j w_j P_k(x_j) = 2 delta_k0, k < n (Legendre moment fitting,
+// Gaussian elimination with partial pivoting); n = 1: the midpoint, weight 2.
+void clenshaw_curtis(int n, std::vector<double>& x, std::vector<double>& w) {
+  x.assign(n, 0.0);
+  w.assign(n, 0.0);
+  if (n == 1) {
+    w[0] = 2.0;
+    return;
+  }
+  for (int j = 0; j < n; ++j) x[j] = -std::cos(M_PI * j / (n - 1));
+  if (n % 2 == 1) x[(n - 1) / 2] = 0.0;
+  std::vector<long double> A((size_t)n * (n + 1));
+  for (int j = 0; j < n; ++j) {  // row k: P_k(x_j), Legendre (not normalised) by recurrence
+    long double p0 = 1.0L, p1 = x[j];
+    A[(size_t)0 * (n + 1) + j] = p0;
+    if (n > 1) A[(size_t)1 * (n + 1) + j] = p1;
+    for (int k = 2; k < n; ++k) {
+      const long double p2 = ((2.0L * k - 1.0L) * x[j] * p1 - (k - 1.0L) * p0) / k;
+      A[(size_t)k * (n + 1) + j] = p2;
+      p0 = p1;
+      p1 = p2;
+    }
+  }
+  for (int k = 0; k < n; ++k) A[(size_t)k * (n + 1) + n] = (k == 0) ? 2.0L : 0.0L;
+  for (int c = 0; c < n; ++c) {
+    int piv = c;
+    for (int r = c + 1; r < n; ++r)
+      if (std::fabs((double)A[(size_t)r * (n + 1) + c]) > std::fabs((double)A[(size_t)piv * (n + 1) + c])) piv = r;
+    for (int cc = 0; cc <= n; ++cc) std::swap(A[(size_t)c * (n + 1) + cc], A[(size_t)piv * (n + 1) + cc]);
+    for (int r = 0; r < n; ++r) {
+      if (r == c) continue;
+      const long double f = A[(size_t)r * (n + 1) + c] / A[(size_t)c * (n + 1) + c];
+      for (int cc = c; cc <= n; ++cc) A[(size_t)r * (n + 1) + cc] -= f * A[(size_t)c * (n + 1) + cc];
+    }
+  }
+  for (int j = 0; j < n; ++j) w[j] = (double)(A[(size_t)j * (n + 1) + n] / A[(size_t)j * (n + 1) + j]);
+}
+
+// Smolyak sparse grid of nested Clenshaw-Curtis rules (reading 33): the combination formula
+// sum over multi-levels i (i_d >= 1, L-p+1 <= |i| <= L) of (-1)^{L-|i|} C(p-1, L-|i|) times the tensor
+// rule of levels i (level 1: midpoint; level l > 1: 2^{l-1}+1 points); coincident points merged by
+// their index on the finest 1D grid, listed in lexicographic order of those indices.
+void smolyak_cc(int p, int L, std::vector<double>& xi, std::vector<double>& w) {
+  const int Fl = L - p + 1, nf = Fl >= 2 ? (1 << (Fl - 1)) + 1 : 1;
+  std::vector<double> xf, wf;
+  clenshaw_curtis(nf, xf, wf);
+  std::map<std::vector<int>, double> acc;
+  std::vector<int> lev(p, 1);
+  std::function<void(int, int)> rec = [&](int d, int used) {
+    if (d == p) {
+      if (used < L - p + 1 || used > L) return;
+      double coef = ((L - used) % 2) ? -1.0 : 1.0;
+      {
+        long long b = 1;  // C(p-1, L-used)
+        const int kk = L - used;
+        for (int t = 1; t <= kk; ++t) b = b * (p - 1 - kk + t) / t;
+        coef *= (double)b;
+      }
+      std::vector<std::vector<double>> ws(p);
+      std::vector<int> ns(p), stride(p);
+      for (int e = 0; e < p; ++e) {
+        ns[e] = lev[e] == 1 ? 1 : (1 << (lev[e] - 1)) + 1;
+        std::vector<double> xx;
+        clenshaw_curtis(ns[e], xx, ws[e]);
+        stride[e] = ns[e] == 1 ? 0 : (nf - 1) / (ns[e] - 1);
+      }
+      std::vector<int> j(p, 0), key(p);
+      for (;;) {
+        double wt = coef;
+        for (int e = 0; e < p; ++e) {
+          key[e] = ns[e] == 1 ? (nf - 1) / 2 : j[e] * stride[e];
+          wt *= ws[e][j[e]];
+        }
+        acc[key] += wt;
+        int e = p - 1;
+        while (e >= 0 && ++j[e] == ns[e]) j[e--] = 0;
+        if (e < 0) break;
+      }
+      return;
+    }
+    for (int l = 1; used + l <= L; ++l) {
+      lev[d] = l;
+      rec(d + 1, used + l);
+    }
+  };
+  rec(0, 0);
+  xi.clear();
+  w.clear();
+  for (const auto& kv : acc) {
+    for (int e = 0; e < p; ++e) xi.push_back(xf[kv.first[e]]);
+    w.push_back(kv.second);
+  }
 }
 
 double legendre_orthonormal(int n, double x) {
@@ -238,7 +335,13 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     return fail(IPM_ERR_CUDA, "no CUDA device (libipm has no CPU path)");
   const ipm_config& C = *cfg;
-  if (C.p < 1 || C.p > 3 || C.M < 0 || C.q1d < 1 || C.q1d > 64) return fail(IPM_ERR_ARG, "bad random space");
+  if (C.p < 1 || C.p > 3 || C.M < 0) return fail(IPM_ERR_ARG, "bad random space");
+  if (C.quad_kind < 0 || C.quad_kind > 2) return fail(IPM_ERR_ARG, "quad_kind must be 0 (GL), 1 (CC), 2 (Smolyak)");
+  if (C.quad_kind != 2 && (C.q1d < 1 || C.q1d > (C.quad_kind == 1 ? 33 : 64))) return fail(IPM_ERR_ARG, "bad q1d");
+  if (C.quad_kind == 2 && (C.quad_level < C.p || C.quad_level - C.p + 1 > 6))
+    return fail(IPM_ERR_ARG, "Smolyak level must satisfy p <= L <= p + 5");
+  if (C.quad_kind != 0 && binom_total(C.p, C.M) * C.m > 88)
+    return fail(IPM_ERR_ARG, "non-tensor-GL rules: n = N m <= 88 (the large-cell kernel is sum-factorised)");
   if (!(C.m == 1 || C.m == 3 || C.m == 4)) return fail(IPM_ERR_ARG, "m must be 1, 3 or 4");
   if (C.closure == IPM_CLOSURE_BARRIER && (C.m != 1 || !(C.u_plus > C.u_minus)))
     return fail(IPM_ERR_ARG, "barrier closure needs m = 1 and u+ > u-");
@@ -256,8 +359,15 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   c->p = C.p;
   c->m = C.m;
   c->N = binom_total(C.p, C.M);
-  c->Q = 1;
-  for (int d = 0; d < C.p; ++d) c->Q *= C.q1d;
+  // quadrature (reading 33): tensor Gauss-Legendre (default), tensor Clenshaw-Curtis, or Smolyak
+  std::vector<double> sg_xi, sg_w;
+  if (C.quad_kind == 2) {
+    smolyak_cc(C.p, C.quad_level, sg_xi, sg_w);
+    c->Q = (int)sg_w.size();
+  } else {
+    c->Q = 1;
+    for (int d = 0; d < C.p; ++d) c->Q *= C.q1d;
+  }
   c->QP = (c->Q % 2 == 0) ? c->Q + 1 : c->Q;
   const int N = c->N, Q = c->Q, QP = c->QP, p = c->p, m = c->m;
 
@@ -270,18 +380,29 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
     c->deg[i] = s;
   }
   std::vector<double> x1, w1;
-  gauss_legendre(C.q1d, x1, w1);
+  if (C.quad_kind == 1)
+    clenshaw_curtis(C.q1d, x1, w1);
+  else if (C.quad_kind == 0)
+    gauss_legendre(C.q1d, x1, w1);
   c->xi.resize((size_t)Q * p);
   c->omega.resize(Q);
   c->phi.resize((size_t)Q * N);
   for (int k = 0; k < Q; ++k) {
-    int r = k;
     double om = 1.0;
-    for (int d = p - 1; d >= 0; --d) {
-      const int kd = r % C.q1d;
-      r /= C.q1d;
-      c->xi[(size_t)k * p + d] = x1[kd];
-      om *= 0.5 * w1[kd];  // f_Xi = 2^{-p}
+    if (C.quad_kind == 2) {
+      for (int d = 0; d < p; ++d) {
+        c->xi[(size_t)k * p + d] = sg_xi[(size_t)k * p + d];
+        om *= 0.5;  // f_Xi = 2^{-p}
+      }
+      om *= sg_w[k];
+    } else {
+      int r = k;
+      for (int d = p - 1; d >= 0; --d) {
+        const int kd = r % C.q1d;
+        r /= C.q1d;
+        c->xi[(size_t)k * p + d] = x1[kd];
+        om *= 0.5 * w1[kd];  // f_Xi = 2^{-p}
+      }
     }
     c->omega[k] = om;
     for (int i = 0; i < N; ++i) {
@@ -291,9 +412,11 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
     }
   }
   // 1D pair table for the sum-factorised Hessian: LL[k][pr] = (w_k/2) L_a(x_k) L_b(x_k), a <= b <= M
-  const int npr = (C.M + 1) * (C.M + 2) / 2;
-  std::vector<double> LL((size_t)C.q1d * npr);
-  for (int k = 0; k < C.q1d; ++k) {
+  // (tensor Gauss-Legendre only: other rules use the direct Hessian sum, q1d = npr = 0 on the device)
+  const bool tensor_gl = C.quad_kind == 0;
+  const int npr = tensor_gl ? (C.M + 1) * (C.M + 2) / 2 : 0;
+  std::vector<double> LL((size_t)std::max(1, (tensor_gl ? C.q1d : 0) * npr), 0.0);
+  for (int k = 0; tensor_gl && k < C.q1d; ++k) {
     int pr = 0;
     for (int aa = 0; aa <= C.M; ++aa)
       for (int bb = aa; bb <= C.M; ++bb, ++pr)
@@ -423,7 +546,7 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
 
   ipm::KernelCtx& k = c->k;
-  k.T = ipm::Tables{d_PhiT, d_WPhiT, d_omega, d_deg, N, Q, QP, p, d_LL, d_idx, C.q1d, npr, d_WPhiF, MT, KS};
+  k.T = ipm::Tables{d_PhiT, d_WPhiT, d_omega, d_deg, N, Q, QP, p, d_LL, d_idx, tensor_gl ? C.q1d : 0, npr, d_WPhiF, MT, KS};
   k.mesh.kind = C.mesh_kind;
   k.mesh.F = F;
   k.mesh.cells = cells;

@@ -61,6 +61,7 @@ class ipm_config(C.Structure):
         ("rank", C.c_int32), ("nranks", C.c_int32), ("px", C.c_int32), ("py", C.c_int32),
         ("reserved_ptr", C.c_void_p), ("stream", C.c_void_p),
         ("n_retard", C.c_int32), ("retard_level", C.c_int32 * 8), ("retard_eps", C.c_double * 8),
+        ("quad_kind", C.c_int32), ("quad_level", C.c_int32),
     ]
 
 
@@ -194,6 +195,8 @@ def make_config(cfg: dict, mesh_arrays=None, rank=0, nranks=1, px=1, py=1):
     for k, Mk in enumerate(levels):
         c.level_M[k] = Mk
     c.delta_dec, c.delta_inc = cfg.get("delta_dec", 0.0), cfg.get("delta_inc", 0.0)
+    c.quad_kind = {"gl": 0, "cc": 1, "smolyak": 2}[cfg.get("quad", "gl")]  # quadrature (reading 33)
+    c.quad_level = cfg.get("quad_level", 0)
     retard = cfg.get("retard") or []  # refinement retardation (Alg. 4): [(eps_l, level index cap), ...]
     c.n_retard = len(retard)
     for k, (eps, lv) in enumerate(retard):

@@ -41,6 +41,58 @@ def test_basis_tables_match(torch, name):
     np.testing.assert_allclose(pg, po, rtol=1e-12, atol=1e-12)
 
 
+QUAD_VARIANTS = {"cc17_cfg1": ("cfg1", dict(quad="cc", q1d=17)), "cc9_cfg3": ("cfg3", dict(quad="cc", q1d=9)),
+                 "smolyak6_cfg3": ("cfg3", dict(quad="smolyak", quad_level=6)),
+                 "smolyak7_cfg3": ("cfg3", dict(quad="smolyak", quad_level=7))}
+
+
+@pytest.mark.parametrize("variant", list(QUAD_VARIANTS))
+def test_quadrature_variants_tables_match(torch, variant):
+    """reading 33: the device's Clenshaw-Curtis (moment-fitted weights) and Smolyak rules against the
+    oracle's (cosine-sum weights): the same points in the same order, weights and basis values"""
+    name, kw = QUAD_VARIANTS[variant]
+    cfg = dict(configs.parity_variant(name), **kw)
+    g, o, _ = ctx_and_oracle(cfg)
+    xg, wg, pg = g.basis()
+    xo, wo, po = o.quadrature()
+    np.testing.assert_allclose(xg, xo, atol=2e-15)
+    np.testing.assert_allclose(wg, wo, rtol=1e-12, atol=1e-15)
+    np.testing.assert_allclose(pg, po, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("variant", list(QUAD_VARIANTS))
+def test_quadrature_variants_dual_solve_parity(torch, variant):
+    """the dual solve under the chosen rule: per-cell statuses (Smolyak's negative weights make some
+    Hessians indefinite: IPM_CELL_ILLCONDITIONED, the failure mode of PAPER.md:753-773) and duals"""
+    name, kw = QUAD_VARIANTS[variant]
+    cfg = dict(configs.parity_variant(name), **kw)
+    g, o, ma = ctx_and_oracle(cfg)
+    base, z, amp = stress_inputs(cfg, seed=3, ma=ma)
+    lam_star = o.stress_dual(base, z, amp)
+    u_o = o.moments_from_dual_all(lam_star)
+    lam_o = o.warm_start(u_o)
+    it_o, st_o, _ = o.dual_solve_all(u_o, lam_o)
+    lam_s = g.zeros()
+    g.ipm_stress_dual(torch.tensor(base, device="cuda"), torch.tensor(z, device="cuda"), amp[0], amp[1], lam_s)
+    u_g = g.zeros()
+    g.ipm_moments_from_dual(lam_s, u_g)
+    lam_g = g.zeros()
+    g.ipm_warm_start(u_g, lam_g)
+    it_g = g.zeros(g.cells, dtype=torch.int32)
+    st_g = g.zeros(g.cells, dtype=torch.int32)
+    g.ipm_dual_solve(u_g, lam_g, "full", it_g, st_g)
+    torch.cuda.synchronize()
+    st_g = to_np(st_g)
+    assert (st_g == st_o).mean() >= 0.99  # a pivot at the rounding level may flip a cell
+    if variant.startswith("smolyak"):
+        assert (st_o == 2).any()
+    ok = (st_o == 0) & (st_g == 0)
+    assert np.abs(to_np(it_g)[ok] - it_o[ok]).max() <= 1
+    scale = np.abs(lam_star).max(axis=(0, 1))
+    err = (np.abs(to_np(lam_g)[ok] - lam_o[ok]) / scale).max()
+    assert err < 1e-9, err
+
+
 @pytest.fixture(params=["group", "mma"])
 def dual_kernel(request, monkeypatch):
     """both dual-solve kernels (IPM_DUAL_KERNEL is read at every launch)"""
