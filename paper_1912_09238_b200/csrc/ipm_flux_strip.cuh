@@ -196,12 +196,48 @@ __global__ void __launch_bounds__(NT, MINB) k_flux_strip(FluxParams P) {
   bool first_seg = true;
 #endif
 
-  for (int64_t g = R * blockIdx.x / gridDim.x; g < g1;) {
-    const int s = (int)(g / by);
-    const int ya = (int)(g - (int64_t)s * by);
-    const int64_t ybl = ya + (g1 - g);
-    const int yb = ybl < by ? (int)ybl : by;
-    g += yb - ya;
+  // Work split. With at least one CTA per strip (gridDim >= nstrips) the first nstrips CTAs walk rows
+  // [0, RA) of strip b side by side, so the x-halo cells one CTA reads were just read by its
+  // neighbour (L2 hits); the other CTAs share the rows [RA, by) of all strips, contiguous in
+  // strip-major order; RA = the rows per CTA of an even split.  Otherwise: contiguous strip-major
+  // shares of all strip rows.
+  const bool banded = (int64_t)gridDim.x >= nstrips && gridDim.x > 1;
+  const int64_t RA0 = (R + gridDim.x - 1) / gridDim.x;
+  const int RA = banded ? (int)(RA0 < by ? RA0 : by) : 0;
+  int64_t ga, gb;  // this CTA's range in its ordering
+  if (!banded) {
+    ga = R * blockIdx.x / gridDim.x;
+    gb = g1;
+  } else if ((int)blockIdx.x < nstrips) {
+    ga = 0;
+    gb = 0;  // band A handled below
+  } else {
+    const int64_t RB = (int64_t)nstrips * (by - RA), G2 = gridDim.x - nstrips, b2 = blockIdx.x - nstrips;
+    ga = RB * b2 / G2;
+    gb = RB * (b2 + 1) / G2;
+  }
+  const bool bandA = banded && (int)blockIdx.x < nstrips && RA > 0;
+  for (int64_t g = bandA ? -1 : ga; bandA ? g < 0 : g < gb;) {
+    int s, ya, yb;
+    if (bandA) {
+      s = blockIdx.x;
+      ya = 0;
+      yb = RA;
+      g = 0;
+    } else if (banded) {  // band B: rows RA..by-1 of every strip
+      const int hb = by - RA;
+      s = (int)(g / hb);
+      ya = RA + (int)(g - (int64_t)s * hb);
+      const int64_t ybl = ya + (gb - g);
+      yb = ybl < by ? (int)ybl : by;
+      g += yb - ya;
+    } else {
+      s = (int)(g / by);
+      ya = (int)(g - (int64_t)s * by);
+      const int64_t ybl = ya + (gb - g);
+      yb = ybl < by ? (int)ybl : by;
+      g += yb - ya;
+    }
     const int x0 = s * TX, tw = min(TX, bx - x0);
     const int LR = yb - ya + 2;  // ring rows ya-1 .. yb
 
