@@ -27,11 +27,14 @@ def _case(name):
     if name == "cart":
         return configs.parity_variant("cfg3"), None
     cfg = configs.parity_variant("cfg4")
+    if name == "tri_retard":  # refinement retardation: the stage advances from the global residual
+        cfg.update(delta_inc=1e-9, delta_dec=0.0, initial_level=0, retard=[(1.9e-4, 0), (1.8759e-4, 1)])
     m = cfg["mesh"]
     return cfg, bump_channel_mesh(m["nx_pts"], m["ny_pts"], m["seed"])
 
 
-@pytest.mark.parametrize("name,R,px,py", [("cart", 2, 2, 1), ("cart", 4, 2, 2), ("tri", 3, 0, 0)])
+@pytest.mark.parametrize("name,R,px,py", [("cart", 2, 2, 1), ("cart", 4, 2, 2), ("tri", 3, 0, 0),
+                                         ("tri_retard", 3, 0, 0)])
 def test_virtual_ranks_match_single_context(torch, name, R, px, py):
     from paper_1912_09238_b200 import Context
     from paper_1912_09238_b200.ipm import _ptr, check, ipm_step_info, lib
@@ -69,10 +72,15 @@ def test_virtual_ranks_match_single_context(torch, name, R, px, py):
         rate = torch.stack([g.rate for g in ctxs]).max()
         for g in ctxs:
             g.rate.copy_(rate.reshape(1))
+        res = 0.0
         for g, u, lam in zip(ctxs, us, lams):
             info = ipm_step_info()
             rc = L.ipm_step_flux(g.h, _ptr(u), _ptr(lam), _ptr(g.recvbuf), _ptr(g.rate), 1e9, C.byref(info))
             check(rc, "ipm_step_flux")
+            res += info.residual
+        if cfg.get("retard"):  # what the binding does after its residual all-reduce
+            for g in ctxs:
+                check(L.ipm_retard_advance(g.h, res), "ipm_retard_advance")
     seen = np.zeros(ref.cells, bool)
     ur = u_ref.cpu().numpy()
     for g, u in zip(ctxs, us):
@@ -81,3 +89,5 @@ def test_virtual_ranks_match_single_context(torch, name, R, px, py):
         seen[ids] = True
         np.testing.assert_array_equal(u.cpu().numpy(), ur[ids])
     assert seen.all()
+    if cfg.get("retard"):
+        assert ref.retard_stage() == 2 and all(g.retard_stage() == 2 for g in ctxs)
