@@ -74,11 +74,9 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND) : "memory");
 }
 
-// K stride of the r^T rows: >= KS*4 and = 4 mod 8 doubles so that the 8 rows x 4 k of an A fragment
-// fall into distinct banks
-__host__ __device__ constexpr int kp(int KS) { return (KS * 4) % 8 == 4 ? KS * 4 : KS * 4 + 4; }
-
 constexpr int UNUSED = -2147483647 - 1;
+
+__host__ __device__ constexpr int KS_(int QC) { return (QC + 3) / 4; }
 
 template <int TX, int QC>
 struct Layout {
@@ -86,7 +84,10 @@ struct Layout {
   static constexpr int CT = TX / 2;  // DMMA row tiles of r^T (8 rows = 2 cells x 4 states)
   // ring column stride: 4 Q doubles + padding so that 4 columns x 4 nodes fall into distinct banks
   static constexpr int QMP = 4 * QC + ((4 - (4 * QC) % 16) + 16) % 16;
-  static constexpr int KS = (QC + 3) / 4, KP = kp(KS), RB = CT * 8 * KP, HXS = 2 * 4 * QC;
+  // r^T row stride: room for the per-column k shift (4 (c & 3) doubles, bank spreading of the stores)
+  // and = 4 mod 16 (the A-fragment loads of 8 rows x 4 k fill 16 banks per half warp)
+  static constexpr int KP = ((KS_(QC) * 4 + 12 + 11) / 16) * 16 + 4;
+  static constexpr int KS = KS_(QC), RB = CT * 8 * KP, HXS = 2 * 4 * QC;
   int MT;
   size_t a, ring, hx, rb, idx, bar, total;  // offsets in doubles
   __host__ __device__ Layout(int MT_, int) : MT(MT_) {
@@ -188,9 +189,10 @@ __global__ void __launch_bounds__(NT, MINB) k_flux_strip(FluxParams P) {
     kv[sl] = warp < CW && k < Q;
     kq[sl] = k < Q ? k : Q - 1;
   }
-  // r^T rows of tile ct = c/2: (cell c&1, state a) -> row 4 (c&1) + ((a + ct) & 3), so that the 8
-  // columns' stores of one state fall into 4 distinct bank groups
-  const int bo = (c >> 1) * 8 * KP + (c & 1) * 4 * KP;
+  // r^T rows of tile ct = c/2: (cell c&1, state a) -> row 4 (c&1) + a; column c's node k is stored at
+  // k + 4 (c & 3), so that the 8 columns' stores of one state fall into 4 distinct bank groups (the
+  // projection's A-fragment loads add the same shift)
+  const int bo = (c >> 1) * 8 * KP + (c & 1) * 4 * KP + 4 * (c & 3);  // row block + k shift
 #ifdef IPM_STRIP_PROF
   long long st[16];
   bool first_seg = true;
@@ -277,7 +279,7 @@ __global__ void __launch_bounds__(NT, MINB) k_flux_strip(FluxParams P) {
       const double* rb = rbT + (itp & 1) * RB;
       const int rr = lane >> 2, q = lane & 3, pw = warp - (NW - NPW);
       for (int ct = pw; ct < CT; ct += NPW) {
-        const int av = (rr - ct) & 3;
+        const int av = rr & 3;
         const int cl = ct * 2 + (rr >> 2);
         const bool cv_ = cl < tw;
         const int64_t cell = (int64_t)y * bx + x0 + cl;
@@ -294,7 +296,7 @@ __global__ void __launch_bounds__(NT, MINB) k_flux_strip(FluxParams P) {
               old[m][e] = (cv_ && i < N) ? A.uhat_old[cell * nmax + i * 4 + av] : 0.0;
             }
           double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-          const double* a = rb + ct * 8 * KP + rr * KP + q;
+          const double* a = rb + ct * 8 * KP + rr * KP + q + 4 * ((2 * ct + (rr >> 2)) & 3);
           const double* b = sA + mt0 * KS * 32 + lane;
 #pragma unroll 5
           for (int ks = 0; ks < KS; ++ks) {
@@ -434,7 +436,7 @@ __global__ void __launch_bounds__(NT, MINB) k_flux_strip(FluxParams P) {
                 double r = 0.0;
                 r += (gE[a] - gW[a]) * cfx;
                 r += (gN[a] - gS[sl][a]) * cfy;
-                o[((a + (c >> 1)) & 3) * KP] = cform ? cu[sl][a] - dt * r : r;
+                o[a * KP] = cform ? cu[sl][a] - dt * r : r;
               }
             }
           }
