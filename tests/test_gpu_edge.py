@@ -137,3 +137,29 @@ def test_step_host_matches_device_step(torch, nchunks):
         ib = g.ipm_step_host(h_u, h_l, d_u, d_l, None, nchunks=nchunks)
         assert ia.newton_iters == ib.newton_iters and ia.dt == ib.dt
     assert torch.equal(h_u, ref_u.cpu()) and torch.equal(h_l, ref_l.cpu())
+
+
+def test_step_host_matches_device_step_adaptive(torch):
+    """the adaptive path of ipm_step_host (duals copied back after the flux, which truncates them to
+    the new levels) on config 4's One-Shot ladder"""
+    from paper_1912_09238_b200 import Context
+
+    from .gpu_common import mesh_arrays
+
+    cfg = dict(configs.parity_variant("cfg4"), delta_inc=1e-9, delta_dec=0.0, initial_level=0)
+    ma = mesh_arrays(cfg)
+    ga, gb = Context(cfg, ma), Context(cfg, ma)
+    u = ga.zeros()
+    ga.ipm_project_ic(u)
+    gb.ipm_project_ic(gb.zeros())  # levels / time of the second context
+    lam = ga.zeros()
+    ga.ipm_warm_start(u, lam)
+    ref_u, ref_l = u.clone(), lam.clone()
+    h_u, h_l = u.cpu().pin_memory(), lam.cpu().pin_memory()
+    d_u, d_l = gb.zeros(), gb.zeros()
+    for _ in range(3):
+        ia = ga.ipm_step(ref_u, ref_l)
+        ib = gb.ipm_step_host(h_u, h_l, d_u, d_l, None, nchunks=5)
+        assert ia.newton_iters == ib.newton_iters and ia.dt == ib.dt
+    assert torch.equal(h_u, ref_u.cpu()) and torch.equal(h_l, ref_l.cpu())
+    assert torch.equal(ga.levels(), gb.levels())

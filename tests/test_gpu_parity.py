@@ -188,11 +188,14 @@ def test_refinement_retardation_cfg4_parity(torch):
         assert abs(ro - rg) <= 1e-9 * max(ro, 1e-300)
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4"])
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg3_smolyak6"])
 def test_stochastic_collocation_parity(torch, name):
     """Stochastic Collocation (reading 32) through the C-ABI against the oracle:
     node states of the IC, coupled CFL steps with the same numerical flux, quadrature moments"""
-    cfg = configs.parity_variant(name)
+    if name == "cfg3_smolyak6":  # SC on a sparse grid (negative weights are harmless for SC)
+        cfg = dict(configs.parity_variant("cfg3"), quad="smolyak", quad_level=6)
+    else:
+        cfg = configs.parity_variant(name)
     g, o, _ = ctx_and_oracle(cfg)
     steps = 6
     U = o.sc_init()
