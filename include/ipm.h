@@ -218,7 +218,10 @@ IPM_API ipm_status ipm_project_ic(ipm_ctx *c, const ipm_ic *ic, double *d_uhat);
  *   d_nodes  [cells][m][Q] node states (device, caller-owned)
  *   ipm_sc_init     node states of the IC (the cell averages ipm_project_ic projects); sets t = 0
  *   ipm_sc_step     d_out = d_in - dt r(d_in), dt = CFL / max node rate capped at t_end - t
- *                   (t_end <= 0: no cap); d_in and d_out must not alias; info (nullable, makes the
+ *                   (t_end <= 0: no cap); d_in and d_out must not alias.  The step also records the
+ *                   CFL rate of d_out; the next call with d_in == that d_out reuses it instead of
+ *                   a rate pass, so the states must not be modified between such calls (any other
+ *                   d_in, or ipm_sc_init, recomputes it); info (nullable, makes the
  *                   call synchronous): dt, t, residual = sum_j |Omega_j| |change of the mean of the
  *                   first state|, newton_iters = 0
  *   ipm_sc_moments  uhat_i = sum_k w_k u(xi_k) phi_i(xi_k), [cells][N][m]

@@ -296,6 +296,7 @@ struct ipm_ctx {
   int32_t *d_level = nullptr, *d_level_new = nullptr, *d_iters = nullptr, *d_status = nullptr;
   ipm::StepScalars* d_sc = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  const double* sc_last_out = nullptr;  // ipm_sc_step: output whose CFL rate is cached on the device
   cudaStream_t copy_stream = nullptr;  // ipm_step_host
   std::vector<cudaEvent_t> hev;        // ipm_step_host: per-chunk copy / solve events
   bool timing = false;
@@ -943,6 +944,7 @@ ipm_status ipm_project_ic(ipm_ctx* c, const ipm_ic* ic, double* d_uhat) {
 ipm_status ipm_sc_init(ipm_ctx* c, const ipm_ic* ic, double* d_nodes) {
   if (!c || !ic || !d_nodes) return fail(IPM_ERR_ARG, "null argument");
   if (c->halo > 0 || !c->part.send_local.empty()) return fail(IPM_ERR_ARG, "SC: single-rank contexts only");
+  c->sc_last_out = nullptr;
   return project_ic_impl(c, ic, nullptr, d_nodes);
 }
 
@@ -950,10 +952,14 @@ ipm_status ipm_sc_step(ipm_ctx* c, const double* d_in, double* d_out, double t_e
   if (!c || !d_in || !d_out || d_in == d_out) return fail(IPM_ERR_ARG, "null or aliased argument");
   if (c->halo > 0 || !c->part.send_local.empty()) return fail(IPM_ERR_ARG, "SC: single-rank contexts only");
   const ipm::KernelCtx& k = c->k;
-  if (int rc = ipm::launch_step_begin(k, c->ghost_rate)) return launch_rc(rc, "step_begin");
-  if (int rc = ipm::launch_sc_rate(k, d_in)) return launch_rc(rc, "sc_rate");
+  // the CFL rate of d_in: cached by the previous step when d_in is its output, else a rate pass
+  const bool cached = d_in == c->sc_last_out;
+  if (int rc = ipm::launch_sc_begin(k, c->ghost_rate, cached ? 1 : 0)) return launch_rc(rc, "sc_begin");
+  if (!cached)
+    if (int rc = ipm::launch_sc_rate(k, d_in)) return launch_rc(rc, "sc_rate");
   if (int rc = ipm::launch_dt(k, t_end, -1.0, c->cfg.cfl)) return launch_rc(rc, "dt");
   if (int rc = ipm::launch_sc_update(k, d_in, d_out)) return launch_rc(rc, "sc_update");
+  c->sc_last_out = d_out;
   if (info) {
     ipm::StepScalars s;
     CUDA_OK(cudaMemcpyAsync(&s, c->d_sc, sizeof(s), cudaMemcpyDeviceToHost, c->stream));

@@ -71,6 +71,7 @@ struct StepScalars {
   unsigned long long newton_iters, failed;
   int worst, work_counter, work_counter2;
   int stage;  // refinement retardation stage (Alg. 4)
+  unsigned long long sc_rate_next;  // SC: CFL rate of the last ipm_sc_step output (ordered bits)
 };
 
 struct DualLaunch {
@@ -123,6 +124,7 @@ const char* last_dual_kernel();
 const char* last_flux_kernel();
 int launch_retard(const KernelCtx& k);
 int launch_sc_rate(const KernelCtx& k, const double* Uin);
+int launch_sc_begin(const KernelCtx& k, double rate0, int use_cached);
 int launch_sc_update(const KernelCtx& k, const double* Uin, double* Uout);
 int launch_sc_moments(const KernelCtx& k, const double* U, double* uhat);
 int launch_dt(const KernelCtx& k, double t_end, double dt_fixed, double cfl);

@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(256) k_sc_update(FluxParams P, const double* _
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const double dt = P.sc->dt, gam = P.cl.gamma;
   const int F = P.mesh.F;
-  double my_res = 0.0;
+  double my_res = 0.0, my_rate = 0.0;
   for (int64_t cell = (int64_t)blockIdx.x * nw + warp; cell < P.mesh.cells; cell += (int64_t)gridDim.x * nw) {
     double dmean = 0.0;
     for (int k = lane; k < Q; k += 32) {
@@ -626,11 +626,33 @@ __global__ void __launch_bounds__(256) k_sc_update(FluxParams P, const double* _
         if (a == 0) u0n = v;
       }
       dmean = fma(P.T.omega[k], u0n - uj[0], dmean);
+      {  // CFL rate of the new state, for the next step (ipm_sc_step reuses it when it gets this output)
+        double v[MS];
+#pragma unroll
+        for (int a = 0; a < MS; ++a) v[a] = dst[a * Q];
+        my_rate = fmax(my_rate, node_rate<0, MS>(v, P.mesh, cell, gam));
+      }
     }
     dmean = warp_sum(dmean);
     if (lane == 0) my_res += P.mesh.area[cell] * fabs(dmean);
   }
   if (lane == 0 && my_res != 0.0) atomicAdd(&P.sc->residual, my_res);
+  my_rate = warp_max(my_rate);
+  if (lane == 0 && my_rate > 0.0)
+    atomicMax(&P.sc->sc_rate_next, (unsigned long long)__double_as_longlong(my_rate));
+}
+
+// SC step begin: the rate starts at the ghost states' rate, maxed with the cached rate of the input
+// (the previous step's output) when the host knows it is valid
+__global__ void k_sc_begin(StepScalars* sc, double rate0, int use_cached) {
+  unsigned long long r = (unsigned long long)__double_as_longlong(rate0);
+  if (use_cached && sc->sc_rate_next > r) r = sc->sc_rate_next;
+  sc->rate_bits = r;
+  sc->sc_rate_next = 0ull;
+  sc->residual = 0.0;
+  sc->newton_iters = 0;
+  sc->failed = 0;
+  sc->worst = 0;
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -1035,6 +1057,11 @@ int debug_phase_cycles(unsigned long long* out) {
   for (int i = 0; i < 8; ++i) out[i] = 0;
   return 0;
 #endif
+}
+
+int launch_sc_begin(const KernelCtx& k, double rate0, int use_cached) {
+  k_sc_begin<<<1, 1, 0, S(k)>>>(k.sc, rate0, use_cached);
+  return (int)cudaGetLastError();
 }
 
 int launch_step_begin(const KernelCtx& k, double rate0) {
