@@ -89,7 +89,7 @@ struct Layout {
   static constexpr int KP = ((KS_(QC) * 4 + 12 + 11) / 16) * 16 + 4;
   static constexpr int KS = KS_(QC), RB = CT * 8 * KP, HXS = 2 * 4 * QC;
   int MT;
-  size_t a, ring, hx, rb, idx, bar, total;  // offsets in doubles
+  size_t a, ring, hx, rb, idx, bar, dm, total;  // offsets in doubles
   __host__ __device__ Layout(int MT_, int) : MT(MT_) {
     a = 0;
     ring = a + (size_t)MT * KS * 32;
@@ -97,7 +97,8 @@ struct Layout {
     rb = hx + (size_t)2 * HXS;
     idx = rb + (size_t)2 * RB;
     bar = idx + (8 * NC + 1) / 2;
-    total = bar + 4;
+    dm = bar + 4;  // SC mode: change of the mean per owned cell of the last two rows [2][TX]
+    total = dm + 2 * TX;
   }
 };
 
@@ -140,7 +141,10 @@ __device__ __forceinline__ void ld4(const double* p, double* u) {
 #define STRIP_STAMP(n)
 #endif
 
-template <int TX, int NT, int MINB, int QC>
+// SC = true: the Stochastic Collocation node update (reading 32) on the same walk: every node state
+// is advanced, u_k - dt r_k -> P.a.uhat_new [cells][m][Q], instead of projected; the change of each
+// cell's mean goes to the residual and the CFL rate of the new states to sc_rate_next.
+template <int TX, int NT, int MINB, int QC, bool SC = false>
 __global__ void __launch_bounds__(NT, MINB) k_flux_strip(FluxParams P) {
   using L = strip::Layout<TX, QC>;
   constexpr int NC = L::NC, CT = L::CT, QMP = L::QMP, KS = L::KS, KP = L::KP, RB = L::RB, HXS = L::HXS;
@@ -158,6 +162,8 @@ __global__ void __launch_bounds__(NT, MINB) k_flux_strip(FluxParams P) {
   double* rbT = sm + lay.rb;     // [2 rows][CT][8][KP]: r^T
   int* sidx = reinterpret_cast<int*>(sm + lay.idx);  // [8 rows][NC] cell codes
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(sm + lay.bar);
+  double* dmean = sm + lay.dm;  // SC
+  double my_rate = 0.0;         // SC
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int b = 0; b < 4; ++b) strip::mbar_init(mbar + b, 1);
@@ -166,6 +172,7 @@ __global__ void __launch_bounds__(NT, MINB) k_flux_strip(FluxParams P) {
   unsigned rows_done = 0;  // ring rows issued by this CTA before the current segment (mbarrier phases)
   for (int x = tid; x < MT * KS * 32; x += NT) sA[x] = P.T.WPhiF[x];
   for (int x = tid; x < 2 * RB; x += NT) rbT[x] = 0.0;  // K padding (k >= Q) stays 0
+  if (tid < 2 * TX) dmean[tid] = 0.0;
   __syncthreads();
 
   const int bx = P.mesh.bx, by = P.mesh.by;
@@ -327,6 +334,15 @@ __global__ void __launch_bounds__(NT, MINB) k_flux_strip(FluxParams P) {
       }
     };
 
+    // SC: residual contribution of ring row itp, sum |Omega_j| |change of the mean|, then clear
+    auto sc_residual = [&](int itp) {
+      if (lane < tw) {
+        double* d = dmean + (itp & 1) * TX + lane;
+        my_res += P.mesh.area[(int64_t)(ya - 1 + itp) * bx + x0 + lane] * fabs(*d);
+        *d = 0.0;
+      }
+    };
+
     int pend = 0;  // codes are loaded one iteration before they are stored (nbr latency off the barrier path)
     if (tid < NC) {
       for (int it = 0; it < 4 && it < LR; ++it) sidx[it * NC + tid] = row_code(it, tid);
@@ -430,13 +446,29 @@ __global__ void __launch_bounds__(NT, MINB) k_flux_strip(FluxParams P) {
               for (int a = 0; a < 4; ++a) gW[a] = hxr[a * Q + kq[sl]];
             }
             if (act[sl]) {
-              double* o = rb + bo + kq[sl];
+              if constexpr (SC) {
+                const int64_t cell = (int64_t)(ya - 1 + it) * bx + x0 + c;
+                double* o = A.uhat_new + cell * 4 * Q + kq[sl];
+                double v[4];
 #pragma unroll
-              for (int a = 0; a < 4; ++a) {
-                double r = 0.0;
-                r += (gE[a] - gW[a]) * cfx;
-                r += (gN[a] - gS[sl][a]) * cfy;
-                o[a * KP] = cform ? cu[sl][a] - dt * r : r;
+                for (int a = 0; a < 4; ++a) {
+                  double r = 0.0;
+                  r += (gE[a] - gW[a]) * cfx;
+                  r += (gN[a] - gS[sl][a]) * cfy;
+                  v[a] = cu[sl][a] - dt * r;
+                  o[a * Q] = v[a];
+                }
+                atomicAdd(dmean + (it & 1) * TX + c, P.T.omega[kq[sl]] * (v[0] - cu[sl][0]));
+                my_rate = fmax(my_rate, node_rate<0, 4>(v, P.mesh, cell, gam));
+              } else {
+                double* o = rb + bo + kq[sl];
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                  double r = 0.0;
+                  r += (gE[a] - gW[a]) * cfx;
+                  r += (gN[a] - gS[sl][a]) * cfy;
+                  o[a * KP] = cform ? cu[sl][a] - dt * r : r;
+                }
               }
             }
           }
@@ -476,7 +508,11 @@ __global__ void __launch_bounds__(NT, MINB) k_flux_strip(FluxParams P) {
         }
       }
       STRIP_STAMP(1)
-      if (warp >= NW - NPW && it >= 2) project(it - 1);
+      if constexpr (SC) {
+        if (warp == NW - 1 && it >= 2) sc_residual(it - 1);
+      } else {
+        if (warp >= NW - NPW && it >= 2) project(it - 1);
+      }
       STRIP_STAMP(2)
     }
 #ifdef IPM_STRIP_PROF
@@ -486,12 +522,21 @@ __global__ void __launch_bounds__(NT, MINB) k_flux_strip(FluxParams P) {
     first_seg = false;
 #endif
     __syncthreads();
-    if (warp >= NW - NPW) project(LR - 2);
+    if constexpr (SC) {
+      if (warp == NW - 1) sc_residual(LR - 2);
+    } else {
+      if (warp >= NW - NPW) project(LR - 2);
+    }
     rows_done += LR;
     __syncthreads();
   }
   my_res = warp_sum(my_res);
   if (lane == 0 && my_res != 0.0) atomicAdd(&P.sc->residual, my_res);
+  if constexpr (SC) {
+    my_rate = warp_max(my_rate);
+    if (lane == 0 && my_rate > 0.0)
+      atomicMax(&P.sc->sc_rate_next, (unsigned long long)__double_as_longlong(my_rate));
+  }
 }
 
 #endif

@@ -1310,13 +1310,13 @@ static int flux_cart_impl(const KernelCtx& k, const FluxLaunch& a) {
 }
 
 // strip kernel (row-major cartesian block, Euler 2D Rusanov, Q = QC): -1 when not applicable
-template <int TX, int NT, int MINB, int QC>
+template <int TX, int NT, int MINB, int QC, bool SC = false>
 static int flux_strip_impl(const KernelCtx& k, const FluxLaunch& a) {
   if (k.mesh.kind != MK_CART || k.m != 4 || k.flux != FX_RUSANOV || k.mesh.bx <= 0 || k.T.Q != QC) return -1;
   const strip::Layout<TX, QC> lay(k.T.MT, k.T.N * 4);
   const size_t smem = lay.total * 8;
   if (smem > k.smem_optin) return -1;
-  auto kern = k_flux_strip<TX, NT, MINB, QC>;
+  auto kern = k_flux_strip<TX, NT, MINB, QC, SC>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
@@ -1404,7 +1404,17 @@ int launch_sc_rate(const KernelCtx& k, const double* Uin) {
   double* Uout = nullptr;
   IPM_SC_DISPATCH(sc_impl)
 }
-int launch_sc_update(const KernelCtx& k, const double* Uin, double* Uout) { IPM_SC_DISPATCH(sc_update_impl) }
+int launch_sc_update(const KernelCtx& k, const double* Uin, double* Uout) {
+  const char* fk = std::getenv("IPM_FLUX_KERNEL");
+  if (!fk || std::string(fk) == "strip") {  // the strip walk (cartesian blocks, Euler Rusanov, Q = 100)
+    FluxLaunch a{};
+    a.uq = Uin;
+    a.uhat_new = Uout;
+    const int rc = flux_strip_impl<8, 512, 1, 100, true>(k, a);
+    if (rc != -1) return rc;
+  }
+  IPM_SC_DISPATCH(sc_update_impl)
+}
 
 template <int MS>
 __global__ void k_sc_moments(Tables T, int64_t cells, const double* __restrict__ U, double* __restrict__ uhat) {
