@@ -23,6 +23,8 @@ CASES = {
     "periodic_16x5": dict(mesh=dict(nx=16, ny=5, periodic=True)),
     "ghost_slip_9x11": dict(mesh=dict(nx=9, ny=11), bc=[("slip", None), ("state", FS), ("state", FS), ("slip", None)]),
     "cform_24x17": dict(mesh=dict(nx=24, ny=17), update="paper_c"),
+    # more strips (151) than CTAs (148 SMs): the contiguous (non-banded) work split of k_flux_strip
+    "wide_1201x3": dict(mesh=dict(nx=1201, ny=3)),
 }
 
 
