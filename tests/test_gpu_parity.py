@@ -188,12 +188,14 @@ def test_refinement_retardation_cfg4_parity(torch):
         assert abs(ro - rg) <= 1e-9 * max(ro, 1e-300)
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg3_smolyak6"])
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg3_smolyak6", "cfg3_wide"])
 def test_stochastic_collocation_parity(torch, name):
     """Stochastic Collocation (reading 32) through the C-ABI against the oracle:
     node states of the IC, coupled CFL steps with the same numerical flux, quadrature moments"""
     if name == "cfg3_smolyak6":  # SC on a sparse grid (negative weights are harmless for SC)
         cfg = dict(configs.parity_variant("cfg3"), quad="smolyak", quad_level=6)
+    elif name == "cfg3_wide":  # more strips than CTAs: the strip walk's contiguous work split
+        cfg = configs.get("cfg3", mesh=dict(nx=1201, ny=3))
     else:
         cfg = configs.parity_variant(name)
     g, o, _ = ctx_and_oracle(cfg)
