@@ -27,6 +27,7 @@
  */
 #ifndef IPM_H
 #define IPM_H
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -277,6 +278,10 @@ IPM_API ipm_status ipm_enable_timing(ipm_ctx *c, int32_t on);
  * "k_dual_group", "k_dual_warp", "k_dual_big"; "" before the first launch).  Host only, never fails;
  * the string is static. */
 IPM_API const char *ipm_last_dual_kernel(void);
+
+/* sizeof(ipm_config), sizeof(ipm_ic), sizeof(ipm_step_info) as compiled into the library (host only;
+ * bindings check their struct mirrors against them) */
+IPM_API size_t ipm_struct_size(int32_t which /* 0 config, 1 ic, 2 step_info */);
 
 /* Refinement retardation stage (Algorithm 4): ipm_retard_stage reads the current stage
  * (synchronous; 0 when retardation is off).  Single-rank contexts advance the stage on the device

@@ -981,6 +981,7 @@ void orc_warm_start(const orc_ctx *c, const double *uhat, double *lam) {
 }
 
 int orc_retard_stage(const orc_ctx *c) { return c->retard_stage; }
+size_t orc_problem_size(void) { return sizeof(orc_problem); }
 void orc_set_levels(orc_ctx *c, const int32_t *levels) { memcpy(c->level, levels, sizeof(int32_t) * c->cells); }
 void orc_get_levels(const orc_ctx *c, int32_t *levels) { memcpy(levels, c->level, sizeof(int32_t) * c->cells); }
 

@@ -17,6 +17,7 @@
  */
 #ifndef IPM_ORACLE_H
 #define IPM_ORACLE_H
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -107,6 +108,7 @@ typedef struct {
 typedef struct orc_ctx orc_ctx;
 
 orc_ctx *orc_create(const orc_problem *P);
+size_t orc_problem_size(void); /* sizeof(orc_problem) (binding check) */
 int orc_retard_stage(const orc_ctx *c); /* refinement retardation stage (Alg. 4) */
 /* Stochastic Collocation: node states U [cells][Q][m] */
 void orc_sc_init(const orc_ctx *c, const orc_ic *ic, double *U);

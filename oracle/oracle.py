@@ -101,6 +101,7 @@ def lib():
             "orc_indicator": (C.c_double, [P, C.c_int, D]),
             "orc_set_levels": (None, [P, I]), "orc_get_levels": (None, [P, I]),
             "orc_retard_stage": (C.c_int, [P]),
+            "orc_problem_size": (C.c_size_t, []),
             "orc_sc_init": (None, [P, C.POINTER(ICSpec), D]),
             "orc_sc_step": (C.c_double, [P, D, D, C.c_double, D]),
             "orc_sc_moments": (None, [P, D, D]),

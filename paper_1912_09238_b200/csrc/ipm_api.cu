@@ -1045,6 +1045,9 @@ ipm_status ipm_last_kernel_ms(ipm_ctx* c, float* dual_ms, float* flux_ms) {
 }
 
 const char* ipm_last_dual_kernel(void) { return ipm::last_dual_kernel(); }
+size_t ipm_struct_size(int32_t which) {
+  return which == 0 ? sizeof(ipm_config) : which == 1 ? sizeof(ipm_ic) : which == 2 ? sizeof(ipm_step_info) : 0;
+}
 const char* ipm_last_flux_kernel(void) { return ipm::last_flux_kernel(); }
 
 ipm_status ipm_debug_phase_cycles(uint64_t* h_out) {

@@ -28,7 +28,7 @@ EXPORTS = [
     "ipm_init", "ipm_destroy", "ipm_status_string", "ipm_last_error", "ipm_sizes", "ipm_get_basis",
     "ipm_get_cell_ids", "ipm_dual_solve", "ipm_flux_update", "ipm_step", "ipm_step_host", "ipm_sc_init", "ipm_sc_step", "ipm_sc_moments", "ipm_project_ic", "ipm_warm_start",
     "ipm_moments_from_dual", "ipm_stress_dual", "ipm_get_levels", "ipm_set_levels", "ipm_last_cell_stats",
-    "ipm_get_time", "ipm_set_time", "ipm_last_kernel_ms", "ipm_enable_timing", "ipm_last_dual_kernel", "ipm_last_flux_kernel", "ipm_retard_stage", "ipm_retard_advance",
+    "ipm_get_time", "ipm_set_time", "ipm_last_kernel_ms", "ipm_enable_timing", "ipm_last_dual_kernel", "ipm_last_flux_kernel", "ipm_struct_size", "ipm_retard_stage", "ipm_retard_advance",
     "ipm_debug_phase_cycles", "ipm_step_dual", "ipm_step_flux", "ipm_halo_layout", "ipm_partition_query",
 ]
 
@@ -123,6 +123,7 @@ def lib():
             "ipm_enable_timing": (st, [P, C.c_int32]),
             "ipm_last_dual_kernel": (C.c_char_p, []),
             "ipm_last_flux_kernel": (C.c_char_p, []),
+            "ipm_struct_size": (C.c_size_t, [C.c_int32]),
             "ipm_retard_stage": (st, [P, C.POINTER(C.c_int32)]),
             "ipm_retard_advance": (st, [P, C.c_double]),
             "ipm_debug_phase_cycles": (st, [P]),

@@ -52,6 +52,8 @@ int main(void) {{
   O(ipm_config, bc_state); O(ipm_config, tau); O(ipm_config, cfl); O(ipm_config, n_levels);
   O(ipm_config, delta_dec); O(ipm_config, rank); O(ipm_config, reserved_ptr); O(ipm_config, stream);
   O(ipm_ic, xs0); O(ipm_ic, state); O(ipm_step_info, newton_iters); O(ipm_step_info, worst_status);
+  O(ipm_config, n_retard); O(ipm_config, retard_level); O(ipm_config, retard_eps); O(ipm_config, quad_kind);
+  O(ipm_config, quad_level);
   return 0;
 }}
 """)
@@ -66,6 +68,17 @@ int main(void) {{
         if "." in key:
             struct, field = key.split(".")
             assert getattr(getattr(ipm, struct), field).offset == int(val), key
+    # and as compiled into the library (nvcc / host compiler of the .so)
+    L = ipm.lib()
+    assert L.ipm_struct_size(0) == C.sizeof(ipm.ipm_config)
+    assert L.ipm_struct_size(1) == C.sizeof(ipm.ipm_ic)
+    assert L.ipm_struct_size(2) == C.sizeof(ipm.ipm_step_info)
+
+
+def test_oracle_problem_layout_matches_c():
+    import oracle.oracle as orc
+
+    assert orc.lib().orc_problem_size() == C.sizeof(orc.Problem)
 
 
 def test_no_cpu_fallback(ipm):
