@@ -149,7 +149,11 @@ __global__ void __launch_bounds__(NT, MINB) k_flux_strip(FluxParams P) {
   using L = strip::Layout<TX, QC>;
   constexpr int NC = L::NC, CT = L::CT, QMP = L::QMP, KS = L::KS, KP = L::KP, RB = L::RB, HXS = L::HXS;
   constexpr int Q = QC, G = (QC + 3) / 4;  // node groups of 4 (one per 4 lanes x 8 columns warp slot)
-  constexpr int CW = (G + 1) / 2;          // compute warps, two node groups each
+#ifndef IPM_STRIP_SLOTS
+#define IPM_STRIP_SLOTS 2
+#endif
+  constexpr int SL = IPM_STRIP_SLOTS;      // node groups per compute thread
+  constexpr int CW = (G + SL - 1) / SL;    // compute warps
   constexpr int NW = NT / 32, HT0 = CW * 32, NTH = NT - HT0;  // halo threads [HT0, NT)
   constexpr int NPW = 4;                                       // projection warps: the last NPW
   static_assert(TX == 8 && NTH >= 32 && CW <= NW - 1 && CT % NPW == 0, "strip kernel geometry");
@@ -188,11 +192,11 @@ __global__ void __launch_bounds__(NT, MINB) k_flux_strip(FluxParams P) {
 
   // compute-warp items: column c, node k = 4 (2 warp + sl) + kk
   const int c = lane >> 2;
-  int kq[2];  // node, clamped to a valid one for idle items (they only feed shuffles)
-  bool kv[2];
+  int kq[SL];  // node, clamped to a valid one for idle items (they only feed shuffles)
+  bool kv[SL];
 #pragma unroll
-  for (int sl = 0; sl < 2; ++sl) {
-    const int k = 4 * (2 * warp + sl) + (lane & 3);
+  for (int sl = 0; sl < SL; ++sl) {
+    const int k = 4 * (SL * warp + sl) + (lane & 3);
     kv[sl] = warp < CW && k < Q;
     kq[sl] = k < Q ? k : Q - 1;
   }
@@ -353,10 +357,10 @@ __global__ void __launch_bounds__(NT, MINB) k_flux_strip(FluxParams P) {
       for (int it = 0; it < 3 && it < LR; ++it) issue_row(it);
 
     // per-item carried state: node state, its ingredients, the south face flux
-    double cu[2][4], cir[2], cp[2], cc_[2], gS[2][4];
-    bool act[2];
+    double cu[SL][4], cir[SL], cp[SL], cc_[SL], gS[SL][4];
+    bool act[SL];
 #pragma unroll
-    for (int sl = 0; sl < 2; ++sl) act[sl] = kv[sl] && c < tw;
+    for (int sl = 0; sl < SL; ++sl) act[sl] = kv[sl] && c < tw;
     const int ro0 = ((c < tw ? c : tw - 1) + 1) * QMP;  // idle columns read the last owned one
 
     for (int it = 0; it + 1 < LR; ++it) {
@@ -379,13 +383,13 @@ __global__ void __launch_bounds__(NT, MINB) k_flux_strip(FluxParams P) {
       if (warp < CW) {
         const double* hxr = HX + (it & 1) * HXS;  // strip-edge x fluxes of the current row
         double* rb = rbT + (it & 1) * RB;
-        double un[2][4];
+        double un[SL][4];
         if (!general) {
 #pragma unroll
-          for (int sl = 0; sl < 2; ++sl) strip::ld4<Q>(rN + ro0 + kq[sl], un[sl]);
+          for (int sl = 0; sl < SL; ++sl) strip::ld4<Q>(rN + ro0 + kq[sl], un[sl]);
         } else {
 #pragma unroll
-          for (int sl = 0; sl < 2; ++sl) {
+          for (int sl = 0; sl < SL; ++sl) {
             const int k = kq[sl];
             if (it == 0) {
               if (act[sl]) {
@@ -413,7 +417,7 @@ __global__ void __launch_bounds__(NT, MINB) k_flux_strip(FluxParams P) {
           }
         }
 #pragma unroll
-        for (int sl = 0; sl < 2; ++sl) {
+        for (int sl = 0; sl < SL; ++sl) {
           RusNode<4> ncur, nnx;
           ncur.irho = cir[sl];
           ncur.p = cp[sl];

@@ -1342,7 +1342,10 @@ int launch_flux(const KernelCtx& k, const FluxLaunch& a) {
   const int key = (k.flux * 10 + k.m) * 10 + k.mesh.kind;
   const char* fk = std::getenv("IPM_FLUX_KERNEL");
   if (!fk || std::string(fk) == "strip") {
-    const int rc = flux_strip_impl<8, 512, 1, 100>(k, a);
+#ifndef IPM_STRIP_NT
+#define IPM_STRIP_NT 512
+#endif
+    const int rc = flux_strip_impl<8, IPM_STRIP_NT, 1, 100>(k, a);
     if (rc != -1) {
       g_last_flux = "k_flux_strip";
       return rc;
@@ -1410,7 +1413,7 @@ int launch_sc_update(const KernelCtx& k, const double* Uin, double* Uout) {
     FluxLaunch a{};
     a.uq = Uin;
     a.uhat_new = Uout;
-    const int rc = flux_strip_impl<8, 512, 1, 100, true>(k, a);
+    const int rc = flux_strip_impl<8, IPM_STRIP_NT, 1, 100, true>(k, a);
     if (rc != -1) return rc;
   }
   IPM_SC_DISPATCH(sc_update_impl)
