@@ -13,7 +13,9 @@ import subprocess
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB = os.path.join(HERE, "libipm_oracle.so")
+# ORACLE_LIB: a prebuilt oracle library instead of the in-tree one (tests/test_oracle_mutants.py
+# points it at deliberately mutated builds to show that the pins catch those mistakes)
+LIB = os.environ.get("ORACLE_LIB") or os.path.join(HERE, "libipm_oracle.so")
 SRC = os.path.join(HERE, "ipm_oracle.c")
 HDR = os.path.join(HERE, "ipm_oracle.h")
 
@@ -29,6 +31,8 @@ STATUS = {0: "ok", 1: "nonconvergence", 2: "illconditioned", 3: "linesearch", 4:
 
 def build(force: bool = False) -> str:
     """Compile the oracle with gcc (plain -O2, OpenMP over cells)."""
+    if os.environ.get("ORACLE_LIB"):
+        return LIB
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(SRC), os.path.getmtime(HDR)):
         tmp = LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-Wall", "-o", tmp, SRC, "-lm"])
