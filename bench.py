@@ -306,6 +306,7 @@ def run_ours(args):
     lam0 = g.zeros()
     g.ipm_warm_start(u0, lam0)
     uhat, lam = u0.clone(), lam0.clone()
+    del u0, lam0, lam_s
     g.enable_timing(True)
 
     def barrier():
@@ -317,6 +318,9 @@ def run_ours(args):
     for _ in range(args.warmup):
         g.ipm_step(uhat, lam, None, sync=False)
     barrier()
+    # the starting state of the timed steps: the e2e leg below re-runs exactly these steps
+    t_start = g.time()
+    u_start, l_start = uhat.cpu().pin_memory(), lam.cpu().pin_memory()
     # timed region: K consecutive steps (Algorithm 1), device-timed with CUDA events
     # inputs smaller than L2 (configs 1, 2, small windows): every step is timed on its own after an
     # L2 flush (a write of twice the L2 size), and the step times are summed
@@ -326,7 +330,8 @@ def run_ours(args):
     state_bytes = g.cells * (g.Q * g.m + 2 * g.N * g.m) * 8
     flush = state_bytes < 2 * l2
     fbuf = torch.empty(2 * l2 // 4, dtype=torch.int32, device=dev) if flush else None
-    dual_ms, flux_ms, iters = [], [], 0
+    dual_ms, flux_ms, iters, local_iters, failed, halvings = [], [], 0, 0, 0, 0
+    hist = np.zeros(16, np.int64)
     ms = 0.0
     with ClockSampler(local) as clk:
         barrier()
@@ -341,7 +346,13 @@ def run_ours(args):
                 e1.record(stream)
                 e1.synchronize()
                 ms += e0.elapsed_time(e1)
+            # info holds global sums (the binding all-reduces across ranks once); the rank's own count
+            # is kept for the imbalance
             iters += info.newton_iters
+            local_iters += g.last_local_newton_iters if world > 1 else info.newton_iters
+            failed += info.failed_cells
+            halvings += info.halvings
+            hist += np.array(info.newton_hist[:], dtype=np.int64)
             d, f = g.last_kernel_ms()
             dual_ms.append(d)
             flux_ms.append(f)
@@ -356,38 +367,43 @@ def run_ours(args):
     ms = float(t.item())
     cells_total = g.cells * world
     value = cells_total * args.steps / (ms / 1e3)
-    # Newton-iteration balance across ranks (the scaling risk is the imbalance)
+    if failed:
+        raise SystemExit(f"bench: {failed} failed cells in the timed steps (worst status "
+                         f"{g.get_status()[0]}): the step did not do the method's work")
+    # Newton-iteration balance across ranks (the scaling risk is the imbalance): the
+    # per-rank counts reduced exactly once (MAX), the total is already global
     imbalance, iters_all = None, iters
     if world > 1:
-        it_t = torch.tensor([float(iters)], device=dev, dtype=torch.float64)
-        it_max = it_t.clone()
-        _allreduce(it_t, dist.ReduceOp.SUM)
+        it_max = torch.tensor([float(local_iters)], device=dev, dtype=torch.float64)
         _allreduce(it_max, dist.ReduceOp.MAX)
-        iters_all = float(it_t.item())
         imbalance = float(it_max.item()) / max(1e-30, iters_all / world)
 
     # end-to-end through the C-ABI with host buffers: H2D of the step inputs (uhat, lambda) from
     # pinned memory, ipm_step, D2H of the step result (uhat, lambda), every step
     e2e = None
     if not args.no_e2e:
-        h_u = torch.empty_like(uhat, device="cpu").pin_memory()
-        h_l = torch.empty_like(lam, device="cpu").pin_memory()
-        h_u.copy_(uhat)
-        h_l.copy_(lam)
+        # the SAME K steps from the same starting state (host copies of the state after warm-up)
+        h_u, h_l = u_start, l_start
+        g.set_time(t_start)
+        e2e_iters, e2e_failed = 0, 0
         barrier()
         e0.record(stream)
         for _ in range(args.steps):
             if world == 1:
                 # the C-ABI host-buffer step: copies in cell ranges overlapped with the dual solves
-                g.ipm_step_host(h_u, h_l, uhat, lam, None, nchunks=args.e2e_chunks)
+                info = g.ipm_step_host(h_u, h_l, uhat, lam, None, nchunks=args.e2e_chunks)
             else:
                 uhat.copy_(h_u, non_blocking=True)
                 lam.copy_(h_l, non_blocking=True)
-                g.ipm_step(uhat, lam, None, sync=False)
+                info = g.ipm_step(uhat, lam, None, sync=True)
                 h_u.copy_(uhat, non_blocking=True)
                 h_l.copy_(lam, non_blocking=True)
+            e2e_iters += info.newton_iters
+            e2e_failed += info.failed_cells
         e1.record(stream)
         barrier()
+        if e2e_failed:
+            raise SystemExit(f"bench e2e: {e2e_failed} failed cells")
         ms_e = e0.elapsed_time(e1)
         te = torch.tensor([ms_e], device=dev, dtype=torch.float64)
         if world > 1:
@@ -396,7 +412,9 @@ def run_ours(args):
         e2e = {"value": cells_total * args.steps / (float(te.item()) / 1e3), "unit": "cell-steps/s",
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
                "path": f"ipm_step_host, {args.e2e_chunks} copy/solve cell ranges" if world == 1
-               else "cudaMemcpyAsync + ipm_step"}
+               else "cudaMemcpyAsync + ipm_step",
+               "same_steps_as_value": True, "newton_iters": int(e2e_iters),
+               "newton_iters_match_value": int(e2e_iters) == int(iters)}
 
     N, m, Q = g.N, g.m, g.Q
     dual_avg = float(np.mean(dual_ms))
@@ -406,13 +424,14 @@ def run_ours(args):
     flops_ex = iters / args.steps * flops_executed_per_iteration(N, m, Q, cfg["p"], cfg["q1d"], kname) + \
         g.cells * flops_initial(N, m, Q)
     achieved_ex = flops_ex / (dual_avg / 1e3) / 1e12
-    traffic = traffic_flux = None
+    traffic = traffic_flux = ncu_pipe = None
     if os.path.exists(NCU_SUMMARY) and not args.nx:  # measured at the bench configuration only
         try:
             ent = json.load(open(NCU_SUMMARY)).get(args.config, {})
             traffic, traffic_flux = ent.get("dual_dram_bytes_per_launch"), ent.get("flux_dram_bytes_per_launch")
+            ncu_pipe = ent.get("dual_fp64_pipe_active_pct")
         except Exception:
-            traffic = traffic_flux = None
+            traffic = traffic_flux = ncu_pipe = None
     flux_avg = float(np.mean(flux_ms))
     hbm = json.load(open(MEASURED))["hbm_gbs"] if os.path.exists(MEASURED) else 6650.0
     flux_gbs = g.cells * flux_bytes_per_cell(N, m, Q) / (flux_avg / 1e3) / 1e9
@@ -433,11 +452,19 @@ def run_ours(args):
             "newton_iters_per_cell_step": iters_all / (cells_total * args.steps),
             "cell_newton_iters_per_s": iters_all / (ms / 1e3),
             "newton_imbalance_max_over_mean": imbalance,
-            "roofline": {"bound": "alu", "kernel": kname, "achieved": achieved,
-                         "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
-                         "flops": "algorithmic (SURVEY §8d: direct unique-entry Hessian, Cholesky n^3/3)",
-                         "executed": {"achieved": achieved_ex, "frac": achieved_ex / FP64_PEAK_TFLOPS,
-                                      "flops": "as executed: sum-factorised Hessian, 8-padded DMMA Cholesky"},
+            "failed_cells": int(failed),
+            "newton_hist": [int(x) for x in hist],
+            "linesearch_halvings": int(halvings),
+            # the dual kernel's fp64 roofline: led by the flops the kernel EXECUTES (the Hessian is
+            # sum-factorised, SURVEY §8d note), the algorithmic count of §8d beside it
+            "roofline": {"bound": "alu", "kernel": kname, "achieved": achieved_ex,
+                         "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved_ex / FP64_PEAK_TFLOPS,
+                         "flops": "as executed: sum-factorised Hessian, 8-padded DMMA Cholesky",
+                         "peak_note": "derived 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz; measured DMMA 37.06, "
+                                      "DFMA 33.7, DGEMM 35.5 TF/s (profiles/r01_fp64_peak.json)",
+                         "algorithmic": {"achieved": achieved, "frac": achieved / FP64_PEAK_TFLOPS,
+                                         "flops": "SURVEY §8d: direct unique-entry Hessian, Cholesky n^3/3"},
+                         "ncu_fp64_pipe_active": ncu_pipe,
                          "traffic": traffic, "dual_ms_avg": dual_avg,
                          "share_of_step": dual_avg / (ms / args.steps)},
             "roofline_flux": {"bound": "hbm", "kernel": Context.last_flux_kernel(), "achieved": flux_gbs, "peak": hbm,
@@ -455,6 +482,19 @@ def run_ours(args):
 
 def main():
     args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if args.gpus > 1 and world == 0:
+        # not under torchrun: launch N ranks (one process per GPU) the way the driver does
+        import socket
+
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        os.execv(sys.executable, cmd)
+    if world and world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         line = run_reference(args)
         if line is not None:

@@ -138,6 +138,7 @@ typedef struct {
   int32_t quad_kind, quad_level;
 } ipm_config;
 
+#define IPM_HIST_BUCKETS 16
 typedef struct {
   double dt, t;              /* time step taken, time after the step */
   double residual;           /* sum_j |Omega_j| |uhat_{j,0,0}^{n+1} - uhat_{j,0,0}^n| */
@@ -145,6 +146,11 @@ typedef struct {
   int64_t failed_cells;      /* cells with status != IPM_CELL_OK */
   int32_t worst_status;      /* max ipm_cell_status over local cells */
   int32_t reserved;
+  /* Newton-count histogram (Alg. 1 lines 7-10 per cell): newton_hist[i] = local cells that took i
+   * accepted Newton steps this step, the last bucket counts >= IPM_HIST_BUCKETS - 1 */
+  int64_t newton_hist[IPM_HIST_BUCKETS];
+  int64_t halvings;          /* rejected Armijo trials (step halvings, reading 3') over all local cells */
+  int64_t inadmissible_trials; /* of which the trial state was not admissible (reading 4) */
 } ipm_step_info;
 
 /* Create a context: host setup of basis, quadrature and mesh tables, device upload,
@@ -171,8 +177,9 @@ IPM_API ipm_status ipm_get_cell_ids(const ipm_ctx *c, int64_t *h_ids);
 IPM_API ipm_status ipm_dual_solve(ipm_ctx *c, const double *d_uhat, double *d_lambda, int32_t mode,
                           int32_t *d_iters, int32_t *d_status, double *d_crit);
 
-/* Kinetic-flux moment update from given duals:
- *   d_lambda    [cells][N][m] in (halo duals are exchanged internally when nranks > 1)
+/* Kinetic-flux moment update from given duals, single-rank contexts only
+ * (a distributed context returns IPM_ERR_ARG: its halo duals arrive through ipm_step_flux):
+ *   d_lambda    [cells][N][m] in
  *   d_uhat_old  [cells][N][m] in; d_uhat_new [cells][N][m] out (may not alias d_uhat_old)
  *   dt > 0: use it; dt <= 0: CFL step from the reconstructed states, capped by t_end - t.
  *   Uses ipm_config.update_form.  d_dt (nullable, device, 1 double) receives the step used. */
@@ -181,7 +188,12 @@ IPM_API ipm_status ipm_flux_update(ipm_ctx *c, const double *d_lambda, const dou
 
 /* One full step of Algorithm 1/2/3 in place: dual solve (config newton_mode), refinement level
  * (n_levels > 0), CFL dt capped at t_end - t (t_end <= 0: no cap, steady), moment update.
- * info == NULL: asynchronous.  info != NULL: synchronous; fills info. */
+ * info == NULL: asynchronous.  info != NULL: synchronous; fills info and returns IPM_ERR_NUMERIC
+ * if a cell failed (the step is still complete: failed cells keep their last iterate).
+ * Small problems (fewer than IPM_GRAPH_MAX_CELLS local cells) replay the step's launches from a
+ * CUDA graph captured on first use (re-captured when d_uhat, d_lambda or t_end change; not while
+ * kernel timing is enabled): for configs 1 and 2 the per-step launch cost bounds the step. */
+#define IPM_GRAPH_MAX_CELLS 65536
 IPM_API ipm_status ipm_step(ipm_ctx *c, double *d_uhat, double *d_lambda, double t_end, ipm_step_info *info);
 
 /* ipm_step with the state in HOST memory (the end-to-end path):
@@ -240,6 +252,13 @@ IPM_API ipm_status ipm_get_levels(ipm_ctx *c, int32_t *d_levels);
 IPM_API ipm_status ipm_set_levels(ipm_ctx *c, const int32_t *d_levels);
 /* per-cell results of the last ipm_step: d_iters, d_status int32 [cells] (device, nullable) */
 IPM_API ipm_status ipm_last_cell_stats(ipm_ctx *c, int32_t *d_iters, int32_t *d_status);
+/* per-cell line-search record of the last dual solve (ipm_step or ipm_dual_solve): rejected Armijo
+ * trials (step halvings) and the inadmissible trials among them, int32 [cells] (device, nullable) */
+IPM_API ipm_status ipm_last_cell_linesearch(ipm_ctx *c, int32_t *d_halvings, int32_t *d_inadmissible);
+/* Outcome of the last dual solve (ipm_dual_solve, ipm_step, ipm_step_dual): the worst
+ * ipm_cell_status over the local cells and the number of cells with status != IPM_CELL_OK.
+ * Synchronous (waits for the ctx stream); either pointer may be NULL. */
+IPM_API ipm_status ipm_get_status(ipm_ctx *c, int32_t *worst, int64_t *n_failed);
 /* simulation time (host, synchronous) */
 IPM_API ipm_status ipm_get_time(ipm_ctx *c, double *t);
 IPM_API ipm_status ipm_set_time(ipm_ctx *c, double t);

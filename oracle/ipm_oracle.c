@@ -855,15 +855,15 @@ static int objective_and_scale(const orc_ctx *c, int Nl, const double *lam, cons
  * globalised by Armijo backtracking on the dual objective L with a rounding
  * allowance (reading 3'):  accept alpha if the trial is admissible and
  *     L(lambda + alpha d) <= L(lambda) + c alpha grad L . d + 1e-12 scale(L). */
-int orc_dual_solve_cell(const orc_ctx *c, int Nl, int mode, const double *uhat, double *lam,
-                        int32_t *iters, double *crit_out) {
+int orc_dual_solve_cell_ls(const orc_ctx *c, int Nl, int mode, const double *uhat, double *lam,
+                           int32_t *iters, double *crit_out, int32_t *halvings, int32_t *inadmissible) {
   const orc_problem *P = &c->P;
   int m = c->m, n = Nl * m;
   double *g = (double *)malloc(sizeof(double) * n);
   double *dd = (double *)malloc(sizeof(double) * n);
   double *lt = (double *)malloc(sizeof(double) * n);
   double *H = (double *)malloc(sizeof(double) * n * n);
-  int status = ORC_OK, l = 0;
+  int status = ORC_OK, l = 0, nhalv = 0, ninad = 0; /* rejected trials; inadmissible among them */
   double crit = INFINITY;
   if (!orc_dual_gradient(c, Nl, lam, uhat, g)) {
     status = ORC_INADMISSIBLE;
@@ -890,11 +890,14 @@ int orc_dual_solve_cell(const orc_ctx *c, int Nl, int mode, const double *uhat, 
     for (int h = 0; h <= P->max_halvings; ++h) {
       for (int r = 0; r < n; ++r) lt[r] = lam[r] + alpha * dd[r];
       double Lt, sct;
-      if (objective_and_scale(c, Nl, lt, uhat, &Lt, &sct) &&
-          Lt <= L0 + P->armijo_c * alpha * slope + 1e-12 * scale && orc_dual_gradient(c, Nl, lt, uhat, g)) {
+      int admissible = objective_and_scale(c, Nl, lt, uhat, &Lt, &sct);
+      if (admissible && Lt <= L0 + P->armijo_c * alpha * slope + 1e-12 * scale &&
+          orc_dual_gradient(c, Nl, lt, uhat, g)) {
         accepted = 1;
         break;
       }
+      ++nhalv;
+      if (!admissible) ++ninad;
       alpha *= 0.5;
     }
     if (!accepted) {
@@ -907,8 +910,15 @@ int orc_dual_solve_cell(const orc_ctx *c, int Nl, int mode, const double *uhat, 
 done:
   if (iters) *iters = l;
   if (crit_out) *crit_out = crit;
+  if (halvings) *halvings = nhalv;
+  if (inadmissible) *inadmissible = ninad;
   free(g); free(dd); free(lt); free(H);
   return status;
+}
+
+int orc_dual_solve_cell(const orc_ctx *c, int Nl, int mode, const double *uhat, double *lam,
+                        int32_t *iters, double *crit_out) {
+  return orc_dual_solve_cell_ls(c, Nl, mode, uhat, lam, iters, crit_out, NULL, NULL);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -986,19 +996,26 @@ void orc_set_levels(orc_ctx *c, const int32_t *levels) { memcpy(c->level, levels
 void orc_get_levels(const orc_ctx *c, int32_t *levels) { memcpy(levels, c->level, sizeof(int32_t) * c->cells); }
 
 /* Alg. 1 lines 4-10 (FULL) / Alg. 2 line 5 (ONE_STEP) for every cell */
-void orc_dual_solve_all(const orc_ctx *c, const double *uhat, double *lam, int32_t *iters,
-                        int32_t *status, double *crit) {
+void orc_dual_solve_all_ls(const orc_ctx *c, const double *uhat, double *lam, int32_t *iters,
+                           int32_t *status, double *crit, int32_t *halvings, int32_t *inadmissible) {
   int N = c->N, m = c->m;
 #pragma omp parallel for schedule(dynamic, 1)
   for (int j = 0; j < c->cells; ++j) {
-    int32_t it = 0;
+    int32_t it = 0, hv = 0, ia = 0;
     double cr = 0.0;
-    int st = orc_dual_solve_cell(c, cell_N(c, j), c->P.newton_mode, uhat + (size_t)j * N * m,
-                                 lam + (size_t)j * N * m, &it, &cr);
+    int st = orc_dual_solve_cell_ls(c, cell_N(c, j), c->P.newton_mode, uhat + (size_t)j * N * m,
+                                    lam + (size_t)j * N * m, &it, &cr, &hv, &ia);
     if (iters) iters[j] = it;
     if (status) status[j] = st;
     if (crit) crit[j] = cr;
+    if (halvings) halvings[j] = hv;
+    if (inadmissible) inadmissible[j] = ia;
   }
+}
+
+void orc_dual_solve_all(const orc_ctx *c, const double *uhat, double *lam, int32_t *iters,
+                        int32_t *status, double *crit) {
+  orc_dual_solve_all_ls(c, uhat, lam, iters, status, crit, NULL, NULL);
 }
 
 /* node states u_k^{(j)} = u_s(lambda_j^T phi(xi_k)) for all cells */
@@ -1205,7 +1222,10 @@ int orc_step(orc_ctx *c, double *uhat, double *lam, double t_remaining, int32_t 
       orc_moments_from_dual(c, c->Nl[lvl], lam + (size_t)j * N * m, h);
       double S = orc_indicator(c, lvl, h);
       int nl = lvl;
-      if (S < c->P.delta_dec && lvl > 0) nl = lvl - 1;
+      /* reading 34: a cell whose dual solve ended INADMISSIBLE (no admissible iterate, h(lambda) is
+       * undefined) keeps its level; every other cell follows the indicator */
+      if (st[j] == ORC_INADMISSIBLE) nl = lvl;
+      else if (S < c->P.delta_dec && lvl > 0) nl = lvl - 1;
       else if (S > c->P.delta_inc && lvl < c->n_levels - 1) nl = lvl + 1;
       /* Alg. 4 line 6: the current stage's maximal level l*_l (reading 31: a cap) */
       if (c->P.n_retard > 0 && c->retard_stage < c->P.n_retard && nl > c->P.retard_level[c->retard_stage])

@@ -162,6 +162,9 @@ void orc_set_levels(orc_ctx *c, const int32_t *levels);
 /* smoothness indicator S_l on the first state of h [N][m] at level index lvl */
 double orc_indicator(const orc_ctx *c, int lvl, const double *h);
 void orc_get_levels(const orc_ctx *c, int32_t *levels);
+/* as orc_dual_solve_all, plus per cell the rejected line-search trials and the inadmissible ones */
+void orc_dual_solve_all_ls(const orc_ctx *c, const double *uhat, double *lam, int32_t *iters,
+                           int32_t *status, double *crit, int32_t *halvings, int32_t *inadmissible);
 void orc_dual_solve_all(const orc_ctx *c, const double *uhat, double *lam, int32_t *iters,
                         int32_t *status, double *crit);
 double orc_compute_dt(const orc_ctx *c, const double *lam, double t_remaining);

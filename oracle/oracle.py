@@ -110,6 +110,7 @@ def lib():
             "orc_sc_step": (C.c_double, [P, D, D, C.c_double, D]),
             "orc_sc_moments": (None, [P, D, D]),
             "orc_dual_solve_all": (None, [P, D, D, I, I, D]),
+            "orc_dual_solve_all_ls": (None, [P, D, D, I, I, D, I, I]),
             "orc_compute_dt": (C.c_double, [P, D, C.c_double]),
             "orc_cell_rates": (None, [P, D, D]),
             "orc_flux_update": (None, [P, D, D, D, C.c_double]),
@@ -401,6 +402,16 @@ class Oracle:
         cr = np.zeros(self.cells)
         lib().orc_dual_solve_all(self.ctx, _d(uhat), _d(lam), _i(it), _i(st), _d(cr))
         return it, st, cr
+
+    def dual_solve_all_ls(self, uhat, lam):
+        """in-place on lam; returns iters, status, crit, rejected line-search trials, inadmissible trials"""
+        it = np.zeros(self.cells, np.int32)
+        st = np.zeros(self.cells, np.int32)
+        cr = np.zeros(self.cells)
+        hv = np.zeros(self.cells, np.int32)
+        ia = np.zeros(self.cells, np.int32)
+        lib().orc_dual_solve_all_ls(self.ctx, _d(uhat), _d(lam), _i(it), _i(st), _d(cr), _i(hv), _i(ia))
+        return it, st, cr, hv, ia
 
     def compute_dt(self, lam, t_remaining=np.inf):
         return lib().orc_compute_dt(self.ctx, _d(lam), t_remaining)

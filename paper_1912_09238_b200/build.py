@@ -17,8 +17,19 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-I", os.path.join(ROOT, "include")]
 
 
+STAMP = LIB + ".cmd"  # the exact nvcc command the product library was built with
+
+
+def product_cmd(out: str) -> list:
+    return [NVCC, *FLAGS, *[os.path.join(CSRC, s) for s in SOURCES], "-o", out]
+
+
 def stale() -> bool:
-    if not os.path.exists(LIB):
+    """rebuild when a source is newer than the library OR the library was built with other flags
+    (e.g. an instrumented experiment written over it): the stamp must hold the product command"""
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
+        return True
+    if open(STAMP).read() != " ".join(product_cmd("libipm.so")):
         return True
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, d) for d in DEPS] + [os.path.join(ROOT, "include", "ipm.h")]
@@ -28,6 +39,8 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False, timers: bool = False, variant: str = "",
           defines=()) -> str:
     """variant/defines: experimental builds (libipm_<variant>.so), never the product default."""
+    if defines and not (variant or timers):
+        raise ValueError("experimental -D defines build libipm_<variant>.so (--variant=...), never the product")
     name = "libipm_timers.so" if timers else (f"libipm_{variant}.so" if variant else "libipm.so")
     lib = os.path.join(HERE, name)
     if not force and not timers and not variant and not stale():
@@ -39,6 +52,11 @@ def build(force: bool = False, verbose: bool = False, timers: bool = False, vari
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
     os.replace(tmp, lib)
+    if lib == LIB:
+        with open(STAMP, "w") as f:
+            f.write(" ".join(product_cmd("libipm.so")))
+    elif os.path.exists(STAMP) and os.path.abspath(lib) == os.path.abspath(LIB):
+        os.remove(STAMP)
     return lib
 
 

@@ -294,6 +294,7 @@ struct ipm_ctx {
   // device buffers
   double *d_uq = nullptr, *d_crit = nullptr;
   int32_t *d_level = nullptr, *d_level_new = nullptr, *d_iters = nullptr, *d_status = nullptr;
+  int32_t *d_halv = nullptr, *d_inadm = nullptr;  // per-cell line-search record of the last dual solve
   ipm::StepScalars* d_sc = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   const double* sc_last_out = nullptr;  // ipm_sc_step: output whose CFL rate is cached on the device
@@ -301,6 +302,12 @@ struct ipm_ctx {
   std::vector<cudaEvent_t> hev;        // ipm_step_host: per-chunk copy / solve events
   bool timing = false;
   int initial_level = 0;
+  // CUDA graph of one ipm_step (small single-rank problems without levels, ipm.h)
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  const double *g_uhat = nullptr, *g_lambda = nullptr;
+  double g_tend = 0.0;
+  bool graph_off = false;
 };
 
 extern "C" {
@@ -325,6 +332,8 @@ void ipm_destroy(ipm_ctx* c) {
     if (e) cudaEventDestroy(e);
   for (auto& e : c->hev) cudaEventDestroy(e);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   for (void* p : c->owned) cudaFree(p);
   delete c;
 }
@@ -514,9 +523,11 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   c->d_level_new = dalloc<int32_t>(cells, O);
   c->d_iters = dalloc<int32_t>(cells, O);
   c->d_status = dalloc<int32_t>(cells, O);
+  c->d_halv = dalloc<int32_t>(cells, O);
+  c->d_inadm = dalloc<int32_t>(cells, O);
   c->d_sc = dalloc<ipm::StepScalars>(1, O);
   if (!d_PhiT || !d_WPhiT || !d_WPhiF || !d_omega || !d_deg || !d_LL || !d_idx || !d_nbr || !d_nrm || !d_coef || !d_area || !d_rgeo || !d_ghost ||
-      !c->d_uq || !c->d_gid || !c->d_send_local || !c->d_crit || !c->d_level || !c->d_level_new || !c->d_iters || !c->d_status || !c->d_sc) {
+      !c->d_uq || !c->d_gid || !c->d_send_local || !c->d_crit || !c->d_level || !c->d_level_new || !c->d_iters || !c->d_status || !c->d_halv || !c->d_inadm || !c->d_sc) {
     ipm_destroy(c);
     return fail(IPM_ERR_CUDA, "cudaMalloc failed");
   }
@@ -534,7 +545,11 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
       up(c->d_gid, c->part.local_gid.data(), cells * 8) ||
       up(c->d_send_local, c->part.send_local.data(), c->part.send_local.size() * 4) ||
       cudaMemset(c->d_sc, 0, sizeof(ipm::StepScalars)) || cudaMemset(c->d_level, 0, cells * 4) ||
-      cudaMemset(c->d_level_new, 0, cells * 4)) {
+      cudaMemset(c->d_level_new, 0, cells * 4) ||
+      // node states: defined before the first dual solve writes them (halo rows: before the first exchange)
+      cudaMemset(c->d_uq, 0, (size_t)(cells + c->halo) * Q * m * 8) ||
+      cudaMemset(c->d_iters, 0, cells * 4) || cudaMemset(c->d_status, 0, cells * 4) ||
+      cudaMemset(c->d_halv, 0, cells * 4) || cudaMemset(c->d_inadm, 0, cells * 4)) {
     ipm_destroy(c);
     return fail(IPM_ERR_CUDA, "upload failed");
   }
@@ -607,8 +622,17 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
     }
   }
   // IPM_DUAL_KERNEL=warp selects the warp-per-cell dual kernel (comparison / tests)
-  const char* dk = std::getenv("IPM_DUAL_KERNEL");
-  k.force_warp_kernel = (dk && std::strcmp(dk, "warp") == 0) ? 1 : 0;
+  auto env_is = [](const char* name, const char* v) {
+    const char* e = std::getenv(name);
+    return e && std::strcmp(e, v) == 0;
+  };
+  k.force_warp_kernel = env_is("IPM_DUAL_KERNEL", "warp") ? 1 : 0;
+  k.dual_group = env_is("IPM_DUAL_KERNEL", "group") ? 1 : 0;
+  k.sumfact = env_is("IPM_SUMFACT", "0") ? 0 : 1;
+  k.mma_w4 = env_is("IPM_MMA_W", "4") ? 1 : 0;
+  k.mma_groups = std::getenv("IPM_MMA_GROUPS") ? std::max(1, std::atoi(std::getenv("IPM_MMA_GROUPS"))) : 0;
+  k.group_t1 = env_is("IPM_GROUP_T", "1") ? 1 : 0;
+  k.flux_choice = env_is("IPM_FLUX_KERNEL", "cart") ? 1 : env_is("IPM_FLUX_KERNEL", "warp") ? 2 : 0;
   *out = c;
   return IPM_OK;
 }
@@ -636,6 +660,22 @@ ipm_status ipm_get_cell_ids(const ipm_ctx* c, int64_t* h_ids) {
   return IPM_OK;
 }
 
+// step statistics of the device scalars -> ipm_step_info; IPM_ERR_NUMERIC when a cell failed
+static ipm_status fill_info(ipm_step_info* info, const ipm::StepScalars& s) {
+  info->dt = s.dt;
+  info->t = s.t;
+  info->residual = s.residual;
+  info->newton_iters = (int64_t)s.newton_iters;
+  info->failed_cells = (int64_t)s.failed;
+  info->worst_status = s.worst;
+  info->reserved = 0;
+  for (int i = 0; i < IPM_HIST_BUCKETS; ++i) info->newton_hist[i] = (int64_t)s.hist[i];
+  info->halvings = (int64_t)s.halvings;
+  info->inadmissible_trials = (int64_t)s.inadm_trials;
+  if (s.failed) return fail(IPM_ERR_NUMERIC, "failed cells in step");
+  return IPM_OK;
+}
+
 static ipm_status launch_rc(int rc, const char* what) {
   if (rc == 0) return IPM_OK;
   if (rc < 0) return fail(IPM_ERR_UNSUPPORTED, std::string(what) + ": combination not compiled in / too large");
@@ -655,6 +695,8 @@ ipm_status ipm_dual_solve(ipm_ctx* c, const double* d_uhat, double* d_lambda, in
   a.iters = d_iters ? d_iters : c->d_iters;
   a.status = d_status ? d_status : c->d_status;
   a.crit = d_crit ? d_crit : c->d_crit;
+  a.halv = c->d_halv;
+  a.inadm = c->d_inadm;
   a.uq = nullptr;
   a.level = c->cfg.n_levels > 0 ? c->d_level : nullptr;
   a.level_new = nullptr;
@@ -698,6 +740,8 @@ ipm_status ipm_step_dual(ipm_ctx* c, const double* d_uhat, double* d_lambda, dou
   a.iters = c->d_iters;
   a.status = c->d_status;
   a.crit = c->d_crit;
+  a.halv = c->d_halv;
+  a.inadm = c->d_inadm;
   a.uq = c->d_uq;
   a.level = c->cfg.n_levels > 0 ? c->d_level : nullptr;
   a.level_new = c->cfg.n_levels > 0 ? c->d_level_new : nullptr;
@@ -734,23 +778,67 @@ ipm_status ipm_step_flux(ipm_ctx* c, double* d_uhat, double* d_lambda, const dou
     ipm::StepScalars s;
     CUDA_OK(cudaMemcpyAsync(&s, c->d_sc, sizeof(s), cudaMemcpyDeviceToHost, c->stream));
     CUDA_OK(cudaStreamSynchronize(c->stream));
-    info->dt = s.dt;
-    info->t = s.t;
-    info->residual = s.residual;
-    info->newton_iters = (int64_t)s.newton_iters;
-    info->failed_cells = (int64_t)s.failed;
-    info->worst_status = s.worst;
-    if (s.failed) return fail(IPM_ERR_NUMERIC, "failed cells in step");
+    return fill_info(info, s);
   }
   return IPM_OK;
+}
+
+// the launches of one single-rank step (no synchronisation, no read-back)
+static ipm_status enqueue_step(ipm_ctx* c, double* d_uhat, double* d_lambda, double t_end) {
+  if (ipm_status s = ipm_step_dual(c, d_uhat, d_lambda, nullptr, nullptr)) return s;
+  return ipm_step_flux(c, d_uhat, d_lambda, nullptr, nullptr, t_end, nullptr);
+}
+
+// capture the step's launches into a CUDA graph on a private stream (the ctx stream may be the legacy
+// default stream, which cannot be captured); false: not capturable, launch directly from now on
+static bool capture_step(ipm_ctx* c, double* d_uhat, double* d_lambda, double t_end) {
+  if (c->gexec) {
+    cudaGraphExecDestroy(c->gexec);
+    c->gexec = nullptr;
+  }
+  if (!c->cap_stream && cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) != cudaSuccess) return false;
+  void* saved = c->k.stream;
+  cudaStream_t saved_s = c->stream;
+  c->k.stream = c->cap_stream;
+  c->stream = c->cap_stream;
+  cudaGraph_t graph = nullptr;
+  bool ok = cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+  const ipm_status st = ok ? enqueue_step(c, d_uhat, d_lambda, t_end) : IPM_ERR_CUDA;
+  ok = (cudaStreamEndCapture(c->cap_stream, &graph) == cudaSuccess) && ok && st == IPM_OK && graph;
+  c->k.stream = saved;
+  c->stream = saved_s;
+  if (ok) ok = cudaGraphInstantiate(&c->gexec, graph, 0) == cudaSuccess;
+  if (graph) cudaGraphDestroy(graph);
+  cudaGetLastError();  // a failed capture leaves no sticky error
+  if (!ok) {
+    c->gexec = nullptr;
+    return false;
+  }
+  c->g_uhat = d_uhat;
+  c->g_lambda = d_lambda;
+  c->g_tend = t_end;
+  return true;
 }
 
 ipm_status ipm_step(ipm_ctx* c, double* d_uhat, double* d_lambda, double t_end, ipm_step_info* info) {
   if (!c || !d_uhat || !d_lambda) return fail(IPM_ERR_ARG, "null argument");
   if (c->halo > 0 || !c->part.send_local.empty())
     return fail(IPM_ERR_ARG, "distributed context: use ipm_step_dual / exchange / ipm_step_flux");
-  if (ipm_status s = ipm_step_dual(c, d_uhat, d_lambda, nullptr, nullptr)) return s;
-  return ipm_step_flux(c, d_uhat, d_lambda, nullptr, nullptr, t_end, info);
+  const bool graph = !c->graph_off && !c->timing && c->cfg.n_levels == 0 && c->cells < IPM_GRAPH_MAX_CELLS;
+  if (graph && (!c->gexec || c->g_uhat != d_uhat || c->g_lambda != d_lambda || c->g_tend != t_end))
+    if (!capture_step(c, d_uhat, d_lambda, t_end)) c->graph_off = true;
+  if (graph && c->gexec) {
+    CUDA_OK(cudaGraphLaunch(c->gexec, c->stream));
+  } else if (ipm_status s = enqueue_step(c, d_uhat, d_lambda, t_end)) {
+    return s;
+  }
+  if (info) {
+    ipm::StepScalars s;
+    CUDA_OK(cudaMemcpyAsync(&s, c->d_sc, sizeof(s), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+    return fill_info(info, s);
+  }
+  return IPM_OK;
 }
 
 ipm_status ipm_step_host(ipm_ctx* c, double* h_uhat, double* h_lambda, double* d_uhat, double* d_lambda, double t_end,
@@ -796,6 +884,8 @@ ipm_status ipm_step_host(ipm_ctx* c, double* h_uhat, double* h_lambda, double* d
     a.iters = c->d_iters + r0;
     a.status = c->d_status + r0;
     a.crit = c->d_crit + r0;
+    a.halv = c->d_halv + r0;
+    a.inadm = c->d_inadm + r0;
     a.uq = c->d_uq + (size_t)r0 * c->Q * c->m;
     a.level = adaptive ? c->d_level + r0 : nullptr;
     a.level_new = adaptive ? c->d_level_new + r0 : nullptr;
@@ -818,15 +908,7 @@ ipm_status ipm_step_host(ipm_ctx* c, double* h_uhat, double* h_lambda, double* d
   ipm::StepScalars s;
   CUDA_OK(cudaMemcpyAsync(&s, c->d_sc, sizeof(s), cudaMemcpyDeviceToHost, ms));
   CUDA_OK(cudaStreamSynchronize(ms));
-  if (info) {
-    info->dt = s.dt;
-    info->t = s.t;
-    info->residual = s.residual;
-    info->newton_iters = (int64_t)s.newton_iters;
-    info->failed_cells = (int64_t)s.failed;
-    info->worst_status = s.worst;
-    if (s.failed) return fail(IPM_ERR_NUMERIC, "failed cells in step");
-  }
+  if (info) return fill_info(info, s);
   return IPM_OK;
 }
 
@@ -937,6 +1019,7 @@ static ipm_status project_ic_impl(ipm_ctx* c, const ipm_ic* ic, double* d_uhat, 
 
 ipm_status ipm_project_ic(ipm_ctx* c, const ipm_ic* ic, double* d_uhat) {
   if (!c || !ic || !d_uhat) return fail(IPM_ERR_ARG, "null argument");
+  c->sc_last_out = nullptr;
   return project_ic_impl(c, ic, d_uhat, nullptr);
 }
 
@@ -1014,6 +1097,24 @@ ipm_status ipm_last_cell_stats(ipm_ctx* c, int32_t* d_iters, int32_t* d_status) 
   return IPM_OK;
 }
 
+ipm_status ipm_last_cell_linesearch(ipm_ctx* c, int32_t* d_halvings, int32_t* d_inadmissible) {
+  if (!c) return fail(IPM_ERR_ARG, "null ctx");
+  if (d_halvings) CUDA_OK(cudaMemcpyAsync(d_halvings, c->d_halv, c->cells * 4, cudaMemcpyDeviceToDevice, c->stream));
+  if (d_inadmissible)
+    CUDA_OK(cudaMemcpyAsync(d_inadmissible, c->d_inadm, c->cells * 4, cudaMemcpyDeviceToDevice, c->stream));
+  return IPM_OK;
+}
+
+ipm_status ipm_get_status(ipm_ctx* c, int32_t* worst, int64_t* n_failed) {
+  if (!c) return fail(IPM_ERR_ARG, "null ctx");
+  ipm::StepScalars s;
+  CUDA_OK(cudaMemcpyAsync(&s, c->d_sc, sizeof(s), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(cudaStreamSynchronize(c->stream));
+  if (worst) *worst = s.worst;
+  if (n_failed) *n_failed = (int64_t)s.failed;
+  return IPM_OK;
+}
+
 ipm_status ipm_get_time(ipm_ctx* c, double* t) {
   if (!c || !t) return fail(IPM_ERR_ARG, "null argument");
   CUDA_OK(cudaMemcpyAsync(t, &c->d_sc->t, 8, cudaMemcpyDeviceToHost, c->stream));
@@ -1023,6 +1124,7 @@ ipm_status ipm_get_time(ipm_ctx* c, double* t) {
 
 ipm_status ipm_set_time(ipm_ctx* c, double t) {
   if (!c) return fail(IPM_ERR_ARG, "null ctx");
+  c->sc_last_out = nullptr;
   CUDA_OK(cudaMemcpyAsync(&c->d_sc->t, &t, 8, cudaMemcpyHostToDevice, c->stream));
   CUDA_OK(cudaStreamSynchronize(c->stream));
   return IPM_OK;

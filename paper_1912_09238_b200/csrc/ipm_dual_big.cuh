@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
       lam[r] = gl[r];
     }
     __syncthreads();
-    int status = 0, l = 0;
+    int status = 0, l = 0, hv = 0, ia = 0;
     double s1, s2, crit = INFINITY;
     bool nb_is_lam = eval(lam, Nl, s1, s2);
     if (!nb_is_lam) {
@@ -744,6 +744,8 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
               break;
             }
           }
+          ++hv;
+          if (!okt) ++ia;
           alpha *= 0.5;
         }
         if (!accepted) {
@@ -770,29 +772,20 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
       }
       bsum(v, 2);
       const double S = v[1] > 0.0 ? v[0] / v[1] : 0.0;
-      int nl = lvl;
-      if (status == 0 || P.nw.mode == 1) {
-        if (S < P.ad.delta_dec && lvl > 0)
-          nl = lvl - 1;
-        else if (S > P.ad.delta_inc && lvl < P.ad.n_levels - 1)
-          nl = lvl + 1;
-      }
-      nl = retard_cap(P.ad, P.sc, nl);  // Alg. 4: the stage's maximal level
+      const int nl = next_level(P.ad, P.sc, lvl, status, S);
       Nnew = P.ad.Nl[nl];
       if (t == 0) A.level_new[cell] = nl;
     }
     for (int r = t; r < nmax; r += NT) gl[r] = (r < n) ? lam[r] : 0.0;  // truncated to the new level after the flux
     if (t == 0) {
-      if (A.iters) A.iters[cell] = l;
-      if (A.status) A.status[cell] = status;
-      if (A.crit) A.crit[cell] = crit;
+      cell_stats(A, P.sc, cell, l, status, hv, ia, crit);
       my_iters += l;
       if (status != 0) {
         my_failed += 1;
         my_worst = max(my_worst, status);
       }
     }
-    if (status != 4) {
+    {  // node states at the final iterate (also for INADMISSIBLE cells: the evaluation at lambda)
       for (int k = t; k < Q; k += NT) {
         const double* u = nb + (size_t)k * NS;
         if (A.uq) {

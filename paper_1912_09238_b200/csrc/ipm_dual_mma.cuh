@@ -711,7 +711,7 @@ __global__ void __launch_bounds__(IPM_MMA_THREADS) k_dual_mma(DualParams P) {
     // Newton iteration with Armijo backtracking on L (reading 3') as one loop with a single
     // evaluation site: mode 0 = first evaluation at lambda, 1 = line-search trial at lt,
     // 2 = re-evaluation of the final lambda (node states for the flux)
-    int status = 0, l = 0, h = 0, mode = 0;
+    int status = 0, l = 0, h = 0, mode = 0, hv = 0, ia = 0;
     double crit = INFINITY, L0 = 0.0, scale = 0.0, slope = 0.0, alpha = 1.0;
     bool nb_is_lam = false;
     for (;;) {
@@ -860,6 +860,8 @@ if constexpr (W == 1) {
         }
       } else {
         nb_is_lam = false;
+        ++hv;
+        if (!ok) ++ia;
         alpha *= 0.5;
         if (++h > P.nw.max_halvings) {
           status = 3;
@@ -889,14 +891,7 @@ if constexpr (W == 1) {
       }
       gsum(nd);
       const double Sv = nd[1] > 0.0 ? nd[0] / nd[1] : 0.0;
-      int nl = lvl;
-      if (status == 0 || P.nw.mode == 1) {
-        if (Sv < P.ad.delta_dec && lvl > 0)
-          nl = lvl - 1;
-        else if (Sv > P.ad.delta_inc && lvl < P.ad.n_levels - 1)
-          nl = lvl + 1;
-      }
-      nl = retard_cap(P.ad, P.sc, nl);  // Alg. 4: the stage's maximal level
+      const int nl = next_level(P.ad, P.sc, lvl, status, Sv);
       if (t == 0) A.level_new[cell] = nl;
     }
     {
@@ -904,16 +899,14 @@ if constexpr (W == 1) {
       for (int r = t; r < nmax; r += G) gl[r] = (r < n) ? lam[r] : 0.0;
     }
     if (t == 0) {
-      if (A.iters) A.iters[cell] = l;
-      if (A.status) A.status[cell] = status;
-      if (A.crit) A.crit[cell] = crit;
+      cell_stats(A, P.sc, cell, l, status, hv, ia, crit);
       my_iters += l;
       if (status != 0) {
         my_failed += 1;
         my_worst = max(my_worst, status);
       }
     }
-    if (status != 4) {
+    {  // node states at the final iterate (also for INADMISSIBLE cells: the evaluation at lambda)
       for (int k = t; k < Q; k += G) {
         double u[MS];
 #pragma unroll

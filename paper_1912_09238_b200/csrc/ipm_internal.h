@@ -72,7 +72,12 @@ struct StepScalars {
   int worst, work_counter, work_counter2;
   int stage;  // refinement retardation stage (Alg. 4)
   unsigned long long sc_rate_next;  // SC: CFL rate of the last ipm_sc_step output (ordered bits)
+  // dual-solve statistics of the step (ipm_step_info): cells per Newton count (last bucket: >= 15),
+  // rejected line-search trials and the inadmissible ones among them
+  unsigned long long hist[16];
+  unsigned long long halvings, inadm_trials;
 };
+constexpr int kHistBuckets = 16;
 
 struct DualLaunch {
   const double* uhat;
@@ -86,6 +91,8 @@ struct DualLaunch {
   int64_t cells;
   int mode;
   int want_rate;
+  int32_t* halv;   // [cells] rejected line-search trials of the cell (nullable)
+  int32_t* inadm;  // [cells] of which inadmissible (non-finite L / closure) (nullable)
 };
 
 struct FluxLaunch {
@@ -111,6 +118,15 @@ struct KernelCtx {
   int sm_count;
   size_t smem_optin;
   int force_warp_kernel;  // 1: always use the warp-per-cell dual kernel (tests, comparison)
+  // kernel choices, read once from the environment at ipm_init (comparison paths for the tests and
+  // A/B experiments; the defaults are the product path): IPM_DUAL_KERNEL=group|warp, IPM_SUMFACT=0,
+  // IPM_MMA_W=4, IPM_MMA_GROUPS=n, IPM_GROUP_T=1, IPM_FLUX_KERNEL=cart|warp|strip
+  int dual_group;    // 1: the 4x4-register-block kernel instead of k_dual_mma
+  int sumfact;       // 0: direct Hessian sum instead of the sum factorisation
+  int mma_w4;        // 1: config 3 with W = 4 warps per cell
+  int mma_groups;    // > 0: cap on the groups per CTA of k_dual_mma
+  int group_t1;      // 1: one Hessian block per thread in k_dual_group
+  int flux_choice;   // 0 default (strip when applicable), 1 cart, 2 warp
   double* big_scratch;    // per-CTA scratch of the large-cell dual kernel (config 5), or null
   int big_ctas;
 };

@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include "ipm_device.cuh"
 #include "ipm_internal.h"
@@ -217,6 +218,34 @@ __device__ __forceinline__ int retard_cap(const Adapt& ad, const StepScalars* sc
   return nl;
 }
 
+// per-cell outcome of a dual solve (one thread per cell): per-cell arrays, the step's Newton-count
+// histogram and line-search counters (ipm_step_info)
+__device__ __forceinline__ void cell_stats(const DualLaunch& A, StepScalars* sc, int64_t cell, int l, int status,
+                                           int hv, int ia, double crit) {
+  if (A.iters) A.iters[cell] = l;
+  if (A.status) A.status[cell] = status;
+  if (A.crit) A.crit[cell] = crit;
+  if (A.halv) A.halv[cell] = hv;
+  if (A.inadm) A.inadm[cell] = ia;
+  atomicAdd(&sc->hist[l < kHistBuckets - 1 ? l : kHistBuckets - 1], 1ull);
+  if (hv) atomicAdd(&sc->halvings, (unsigned long long)hv);
+  if (ia) atomicAdd(&sc->inadm_trials, (unsigned long long)ia);
+}
+
+// next refinement level from the indicator S (readings 19, 20): every cell
+// whose dual solve ended on an admissible iterate (all but IPM_CELL_INADMISSIBLE, reading 34) moves
+// one level down if S < delta_dec, up if S > delta_inc; then the retardation cap (Alg. 4)
+__device__ __forceinline__ int next_level(const Adapt& ad, const StepScalars* sc, int lvl, int status, double S) {
+  int nl = lvl;
+  if (status != 4) {
+    if (S < ad.delta_dec && lvl > 0)
+      nl = lvl - 1;
+    else if (S > ad.delta_inc && lvl < ad.n_levels - 1)
+      nl = lvl + 1;
+  }
+  return retard_cap(ad, sc, nl);
+}
+
 struct DualParams {
   Tables T;
   Mesh mesh;
@@ -272,7 +301,7 @@ __global__ void __launch_bounds__(512) k_dual_warp(DualParams P) {
     }
     __syncwarp();
 
-    int status = 0, l = 0;
+    int status = 0, l = 0, hv = 0, ia = 0;
     double s1, s2, crit = INFINITY;
     bool nb_is_lam = warp_eval<CL, MS>(lam, Nl, sPhiT, QP, omega, Q, nb, P.cl, s1, s2, lane);
     if (!nb_is_lam) {
@@ -316,6 +345,8 @@ __global__ void __launch_bounds__(512) k_dual_warp(DualParams P) {
               break;
             }
           }
+          ++hv;
+          if (!okt) ++ia;
           alpha *= 0.5;
         }
         if (!accepted) {
@@ -343,25 +374,14 @@ __global__ void __launch_bounds__(512) k_dual_warp(DualParams P) {
       num = warp_sum(num);
       den = warp_sum(den);
       const double S = den > 0.0 ? num / den : 0.0;
-      int nl = lvl;
-      if (status == 0 || P.nw.mode == 1) {
-        if (S < P.ad.delta_dec && lvl > 0)
-          nl = lvl - 1;
-        else if (S > P.ad.delta_inc && lvl < P.ad.n_levels - 1)
-          nl = lvl + 1;
-      }
-      nl = retard_cap(P.ad, P.sc, nl);  // Alg. 4: the stage's maximal level
+      const int nl = next_level(P.ad, P.sc, lvl, status, S);
       Nnew = P.ad.Nl[nl];
       if (lane == 0) A.level_new[cell] = nl;
     }
     // lambda zero-padded / truncated to the new level (the node states keep the old level)
     for (int r = lane; r < nmax; r += 32) gl[r] = (r < n) ? lam[r] : 0.0;  // truncated after the flux
-    if (lane == 0) {
-      if (A.iters) A.iters[cell] = l;
-      if (A.status) A.status[cell] = status;
-      if (A.crit) A.crit[cell] = crit;
-    }
-    if (status != 4) {
+    if (lane == 0) cell_stats(A, P.sc, cell, l, status, hv, ia, crit);
+    {  // node states at the final iterate (also for INADMISSIBLE cells: the evaluation at lambda)
       double cr = 0.0;
       for (int k = lane; k < Q; k += 32) {
         const double* u = nb + k * Lay::NS;
@@ -851,6 +871,9 @@ __global__ void k_step_begin(StepScalars* sc, double rate0) {
   sc->worst = 0;
   sc->work_counter = 0;
   sc->work_counter2 = 0;
+  for (int i = 0; i < kHistBuckets; ++i) sc->hist[i] = 0;
+  sc->halvings = 0;
+  sc->inadm_trials = 0;
 }
 
 // Algorithm 4 lines 12-14: next retardation stage once the step's residual is below its tolerance
@@ -1047,6 +1070,46 @@ __global__ void k_stress(Tables T, int64_t cells, ClParams cp, const double* __r
 // ------------------------------------------------------------------------------------------------
 static inline cudaStream_t S(const KernelCtx& k) { return (cudaStream_t)k.stream; }
 
+// Launch configuration, cached on the host: the dynamic shared-memory attribute is raised only when a
+// launch needs more than the kernel has on this device, and the occupancy query runs once per
+// (kernel, device, block size, shared memory) — not on every launch (host-side cost on the small,
+// launch-bound configurations).  Contexts are single-threaded (ipm.h), so is this cache.
+struct LaunchCfgEntry {
+  const void* f;
+  int dev, threads;
+  size_t smem;
+  int per_sm;
+};
+template <class K>
+static int configure(K kern, int threads, size_t smem) {
+  static std::vector<LaunchCfgEntry> occ;
+  static std::vector<LaunchCfgEntry> attr;  // per (kernel, device): largest smem attribute set
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const void* f = (const void*)kern;
+  bool have = false;
+  for (auto& e : attr)
+    if (e.f == f && e.dev == dev) {
+      if (smem > e.smem) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e.smem = smem;
+      }
+      have = true;
+    }
+  if (!have) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr.push_back({f, dev, 0, smem, 0});
+  }
+  if (threads <= 0) return 1;
+  for (const auto& e : occ)
+    if (e.f == f && e.dev == dev && e.threads == threads && e.smem == smem) return e.per_sm;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+  occ.push_back({f, dev, threads, smem, per_sm});
+  return per_sm;
+}
+
+
 int debug_phase_cycles(unsigned long long* out) {
 #ifdef IPM_PHASE_TIMERS
   cudaError_t e = cudaMemcpyFromSymbol(out, g_phase_cycles, 8 * sizeof(unsigned long long));
@@ -1083,9 +1146,7 @@ static int dual_impl(const KernelCtx& k, const DualLaunch& a) {
   warps = warps > 16 ? 16 : warps;
   const size_t smem = tab + warps * pw;
   auto kern = k_dual_warp<CL, MS>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem);
+  int per_sm = configure(kern, warps * 32, smem);
   if (per_sm < 1) per_sm = 1;
   int64_t want = (a.cells + warps - 1) / warps;
   int grid = (int)std::min<int64_t>(want, (int64_t)k.sm_count * per_sm);
@@ -1106,9 +1167,7 @@ static int dual_group_impl(const KernelCtx& k, const DualLaunch& a) {
   groups = std::min(groups, IPM_GROUP_THREADS / G);
   const size_t smem = tab + groups * pg;
   auto kern = k_dual_group<CL, MS, G, SF, T>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, groups * G, smem);
+  int per_sm = configure(kern, groups * G, smem);
   if (per_sm < 1) return -1;
   const int64_t want = (a.cells + groups - 1) / groups;
   int grid = (int)std::min<int64_t>(want, (int64_t)k.sm_count * per_sm);
@@ -1120,10 +1179,9 @@ static int dual_group_impl(const KernelCtx& k, const DualLaunch& a) {
 
 // group size G and blocks per thread T: T = 2 (fewer threads per cell, more cells per SM) with the
 // smallest G such that G T covers every m x m Hessian block; IPM_GROUP_T=1 forces one block per thread
-static void group_shape(int N, int& G, int& T) {
+static void group_shape(int N, int t1, int& G, int& T) {
   const int NP = N * (N + 1) / 2;
-  const char* e = std::getenv("IPM_GROUP_T");
-  const int tmax = (e && e[0] == '1') ? 1 : 2;
+  const int tmax = t1 ? 1 : 2;
   G = 0;
   T = 0;
   for (int t = tmax; t >= 1 && G == 0; --t)
@@ -1150,12 +1208,10 @@ static int dual_mma_impl(const KernelCtx& k, const DualLaunch& a) {
   if (tab + pg > k.smem_optin) return -1;
   int groups = (int)((k.smem_optin - tab) / pg);
   groups = std::min(groups, std::min(512 / G, 15));  // named barriers 1..15 (0 = __syncthreads)
-  if (const char* ge = std::getenv("IPM_MMA_GROUPS")) groups = std::max(1, std::min(groups, std::atoi(ge)));  // experiments
+  if (k.mma_groups > 0) groups = std::min(groups, k.mma_groups);  // experiments
   const size_t smem = tab + groups * pg;
   auto kern = k_dual_mma<CL, MS, NB, W, SF>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, groups * G, smem);
+  int per_sm = configure(kern, groups * G, smem);
   if (per_sm < 1) return -1;
   const int64_t want = (a.cells + groups - 1) / groups;
   int grid = (int)std::min<int64_t>(want, (int64_t)k.sm_count * per_sm);
@@ -1170,8 +1226,7 @@ static int dual_mma_impl(const KernelCtx& k, const DualLaunch& a) {
 static int dual_mma_dispatch(const KernelCtx& k, const DualLaunch& a, int SF) {
   const int n = k.T.N * k.m, NB = (n + 7) / 8;
   const int key = ((k.closure * 10 + k.m) * 100 + NB) * 10 + SF;
-  const char* we = std::getenv("IPM_MMA_W");
-  if (we && we[0] == '4' && key == ((CL_EULER * 10 + 4) * 100 + 8) * 10 + 5)
+  if (k.mma_w4 && key == ((CL_EULER * 10 + 4) * 100 + 8) * 10 + 5)
     return dual_mma_impl<CL_EULER, 4, 8, 4, 5>(k, a);
   switch (key) {
 #define IPM_MCASE(CLV, MSV, NBV, WV, SFV) \
@@ -1196,11 +1251,8 @@ int launch_dual(const KernelCtx& k, const DualLaunch& a) {
   if (a.cells == 0) return 0;
   // default: the DMMA-Cholesky kernel where it is instantiated; IPM_DUAL_KERNEL=group selects the
   // 4x4-register-block kernel (comparison, tests)
-  const char* dk = std::getenv("IPM_DUAL_KERNEL");
-  const bool use_mma = !(dk && (std::string(dk) == "group"));
-  if (!k.force_warp_kernel && use_mma) {
-    const char* sfe = std::getenv("IPM_SUMFACT");
-    const int SF = (k.T.p == 2 && !(sfe && sfe[0] == '0')) ? (int)std::lround((std::sqrt(8.0 * k.T.npr + 1) - 1) / 2) : 0;
+  if (!k.force_warp_kernel && !k.dual_group) {
+    const int SF = (k.T.p == 2 && k.sumfact) ? (int)std::lround((std::sqrt(8.0 * k.T.npr + 1) - 1) / 2) : 0;
     const int rc = dual_mma_dispatch(k, a, SF);
     if (rc != -1) {
       g_last_dual = "k_dual_mma";
@@ -1209,10 +1261,9 @@ int launch_dual(const KernelCtx& k, const DualLaunch& a) {
   }
   if (!k.force_warp_kernel) {
     int G, T;
-    group_shape(k.T.N, G, T);
+    group_shape(k.T.N, k.group_t1, G, T);
     // sum factorisation for p = 2 tensor rules (SF = M + 1); IPM_SUMFACT=0 selects the direct sum
-    const char* sfe = std::getenv("IPM_SUMFACT");
-    const int SF = (k.T.p == 2 && !(sfe && sfe[0] == '0')) ? (int)std::lround((std::sqrt(8.0 * k.T.npr + 1) - 1) / 2) : 0;
+    const int SF = (k.T.p == 2 && k.sumfact) ? (int)std::lround((std::sqrt(8.0 * k.T.npr + 1) - 1) / 2) : 0;
     const int key = (((k.closure * 10 + k.m) * 1000 + G) * 10 + SF) * 10 + T;
     int rc = -1;
     switch (key) {
@@ -1247,7 +1298,7 @@ int launch_dual(const KernelCtx& k, const DualLaunch& a) {
       const int hb_in_smem = (smem0 + hbl <= k.smem_optin) ? 1 : 0;
       const size_t smem = smem0 + (hb_in_smem ? hbl : 0);
       auto kern = hb_in_smem ? k_dual_big<CL_EULER, 4, NT, true> : k_dual_big<CL_EULER, 4, NT, false>;
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      configure(kern, 0, smem);
       const int grid = (int)std::min<int64_t>(a.cells, (int64_t)k.big_ctas);
       DualParams P{k.T, k.mesh, k.nw, k.ad, k.cl, a, k.sc};
       kern<<<grid, NT, smem, S(k)>>>(P, k.big_scratch);
@@ -1276,9 +1327,7 @@ static int flux_impl(const KernelCtx& k, const FluxLaunch& a) {
   if (warps < 1) return -1;
   const size_t smem = base + warps * pw;
   auto kern = k_flux_warp<FX, MS, MK>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem);
+  int per_sm = configure(kern, warps * 32, smem);
   if (per_sm < 1) per_sm = 1;
   const int64_t want = (k.mesh.cells + warps - 1) / warps;
   int grid = (int)std::min<int64_t>(want, (int64_t)k.sm_count * per_sm * 4);
@@ -1296,9 +1345,7 @@ static int flux_cart_impl(const KernelCtx& k, const FluxLaunch& a) {
   const int warps = (int)std::min<size_t>(8, (k.smem_optin - tab) / pw);
   const size_t smem = tab + warps * pw;
   auto kern = k_flux_cart<FX, MS, MK>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem);
+  int per_sm = configure(kern, warps * 32, smem);
   if (per_sm < 1) per_sm = 1;
   const int64_t groups = (k.mesh.cells + CPW - 1) / CPW;
   const int64_t want = (groups + warps - 1) / warps;
@@ -1317,9 +1364,7 @@ static int flux_strip_impl(const KernelCtx& k, const FluxLaunch& a) {
   const size_t smem = lay.total * 8;
   if (smem > k.smem_optin) return -1;
   auto kern = k_flux_strip<TX, NT, MINB, QC, SC>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
+  int per_sm = configure(kern, NT, smem);
   if (per_sm < 1) per_sm = 1;
   const int64_t rows = (int64_t)((k.mesh.bx + TX - 1) / TX) * k.mesh.by;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(rows, (int64_t)k.sm_count * per_sm));
@@ -1340,8 +1385,7 @@ const char* last_flux_kernel() { return g_last_flux; }
 int launch_flux(const KernelCtx& k, const FluxLaunch& a) {
   if (k.mesh.cells == 0) return 0;
   const int key = (k.flux * 10 + k.m) * 10 + k.mesh.kind;
-  const char* fk = std::getenv("IPM_FLUX_KERNEL");
-  if (!fk || std::string(fk) == "strip") {
+  if (k.flux_choice == 0) {
 #ifndef IPM_STRIP_NT
 #define IPM_STRIP_NT 512
 #endif
@@ -1351,7 +1395,7 @@ int launch_flux(const KernelCtx& k, const FluxLaunch& a) {
       return rc;
     }
   }
-  if (!(fk && std::string(fk) == "warp")) {
+  if (k.flux_choice != 2) {
     int rc = -1;
     switch (key) {
       case (FX_LF_GLOBAL * 10 + 1) * 10 + MK_1D: rc = flux_cart_impl<FX_LF_GLOBAL, 1, MK_1D>(k, a); break;
@@ -1408,8 +1452,7 @@ int launch_sc_rate(const KernelCtx& k, const double* Uin) {
   IPM_SC_DISPATCH(sc_impl)
 }
 int launch_sc_update(const KernelCtx& k, const double* Uin, double* Uout) {
-  const char* fk = std::getenv("IPM_FLUX_KERNEL");
-  if (!fk || std::string(fk) == "strip") {  // the strip walk (cartesian blocks, Euler Rusanov, Q = 100)
+  if (k.flux_choice == 0) {  // the strip walk (cartesian blocks, Euler Rusanov, Q = 100)
     FluxLaunch a{};
     a.uq = Uin;
     a.uhat_new = Uout;
@@ -1452,7 +1495,7 @@ static int ic_impl(const KernelCtx& k, const double* region, const double* split
   if (warps < 1) return -1;
   const size_t smem = (size_t)warps * pw;
   auto kern = k_project_ic<MS>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  configure(kern, 0, smem);
   const int64_t want = (k.mesh.cells + warps - 1) / warps;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)k.sm_count * 8));
   kern<<<grid, warps * 32, smem, S(k)>>>(k.T, k.mesh.cells, region, split, kind, nx, x0, y0, dx, dy, level, gid,
@@ -1488,7 +1531,7 @@ static int nodes_impl(const KernelCtx& k, const double* lam, double* uhat, doubl
   if (warps < 1) return -1;
   const size_t smem = base + warps * pw;
   auto kern = k_nodes<CL, MS>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  configure(kern, 0, smem);
   const int64_t want = (k.mesh.cells + warps - 1) / warps;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)k.sm_count * 4));
   kern<<<grid, warps * 32, smem, S(k)>>>(k.T, k.mesh, k.cl, lam, uhat, uq, k.sc, in_smem, want_rate);

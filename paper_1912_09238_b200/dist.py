@@ -53,12 +53,18 @@ def allreduce_max_(t: torch.Tensor, group=None) -> None:
 def reduce_info_(info, device, group=None) -> None:
     """Global step statistics from the local ones (ctypes ipm_step_info, in place)."""
     dev = "cpu" if dist.get_backend(group) == "gloo" else device
-    v = torch.tensor([info.residual, float(info.newton_iters), float(info.failed_cells)], dtype=torch.float64,
-                     device=dev)
+    nh = len(info.newton_hist)
+    v = torch.tensor([info.residual, float(info.newton_iters), float(info.failed_cells), float(info.halvings),
+                      float(info.inadmissible_trials)] + [float(x) for x in info.newton_hist],
+                     dtype=torch.float64, device=dev)
     dist.all_reduce(v, op=dist.ReduceOp.SUM, group=group)
     w = torch.tensor([info.worst_status], dtype=torch.int64, device=dev)
     dist.all_reduce(w, op=dist.ReduceOp.MAX, group=group)
     info.residual = float(v[0])
     info.newton_iters = int(v[1])
     info.failed_cells = int(v[2])
+    info.halvings = int(v[3])
+    info.inadmissible_trials = int(v[4])
+    for i in range(nh):
+        info.newton_hist[i] = int(v[5 + i])
     info.worst_status = int(w[0])

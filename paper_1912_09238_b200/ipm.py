@@ -30,7 +30,9 @@ EXPORTS = [
     "ipm_moments_from_dual", "ipm_stress_dual", "ipm_get_levels", "ipm_set_levels", "ipm_last_cell_stats",
     "ipm_get_time", "ipm_set_time", "ipm_last_kernel_ms", "ipm_enable_timing", "ipm_last_dual_kernel", "ipm_last_flux_kernel", "ipm_struct_size", "ipm_retard_stage", "ipm_retard_advance",
     "ipm_debug_phase_cycles", "ipm_step_dual", "ipm_step_flux", "ipm_halo_layout", "ipm_partition_query",
+    "ipm_get_status", "ipm_last_cell_linesearch",
 ]
+HIST_BUCKETS = 16  # IPM_HIST_BUCKETS
 
 
 class IPMError(RuntimeError):
@@ -68,7 +70,9 @@ class ipm_config(C.Structure):
 class ipm_step_info(C.Structure):
     _fields_ = [("dt", C.c_double), ("t", C.c_double), ("residual", C.c_double),
                 ("newton_iters", C.c_int64), ("failed_cells", C.c_int64),
-                ("worst_status", C.c_int32), ("reserved", C.c_int32)]
+                ("worst_status", C.c_int32), ("reserved", C.c_int32),
+                ("newton_hist", C.c_int64 * HIST_BUCKETS), ("halvings", C.c_int64),
+                ("inadmissible_trials", C.c_int64)]
 
 
 class ipm_ic(C.Structure):
@@ -127,10 +131,16 @@ def lib():
             "ipm_retard_stage": (st, [P, C.POINTER(C.c_int32)]),
             "ipm_retard_advance": (st, [P, C.c_double]),
             "ipm_debug_phase_cycles": (st, [P]),
+            "ipm_get_status": (st, [P, C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
+            "ipm_last_cell_linesearch": (st, [P, I, I]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
             f.restype, f.argtypes = res, args
+        for which, st_ in ((0, ipm_config), (1, ipm_ic), (2, ipm_step_info)):
+            if L.ipm_struct_size(which) != C.sizeof(st_):
+                raise IPMError(f"struct mirror {st_.__name__} ({C.sizeof(st_)} B) does not match libipm "
+                               f"({L.ipm_struct_size(which)} B): rebuild libipm.so")
         _lib = L
     return _lib
 
@@ -160,6 +170,39 @@ def _state(s: dict | None) -> ipm_state:
 
 def _ptr(t) -> int:
     return 0 if t is None else t.data_ptr()
+
+
+def _dev(t, ctx, shape, dtype, name):
+    """device pointer of a tensor argument after checking what the C-ABI assumes (ipm.h conventions):
+    dtype, contiguity, the context's device and the element count; None passes NULL"""
+    if t is None:
+        return 0
+    if t.dtype != dtype:
+        raise IPMError(f"{name}: dtype {t.dtype}, expected {dtype}")
+    if not t.is_contiguous():
+        raise IPMError(f"{name}: not contiguous")
+    if t.device != ctx.device:
+        raise IPMError(f"{name}: on {t.device}, the context is on {ctx.device}")
+    n = 1
+    for d in shape:
+        n *= d
+    if t.numel() != n:
+        raise IPMError(f"{name}: {t.numel()} elements, expected {n} {tuple(shape)}")
+    return t.data_ptr()
+
+
+def _host(t, shape, name):
+    """host tensor of the ipm_step_host path: float64, contiguous, CPU, page-locked"""
+    if t.dtype.is_floating_point is False or t.element_size() != 8 or t.device.type != "cpu":
+        raise IPMError(f"{name}: expected a float64 CPU tensor")
+    if not t.is_contiguous() or not t.is_pinned():
+        raise IPMError(f"{name}: must be contiguous and pinned (pin_memory()) for the overlapped copies")
+    n = 1
+    for d in shape:
+        n *= d
+    if t.numel() != n:
+        raise IPMError(f"{name}: {t.numel()} elements, expected {n}")
+    return t.data_ptr()
 
 
 def make_config(cfg: dict, mesh_arrays=None, rank=0, nranks=1, px=1, py=1):
@@ -279,14 +322,37 @@ class Context:
         return ids
 
     # --- the path ---------------------------------------------------------------------------
+    def _state(self, t, name):
+        return _dev(t, self, (self.cells, self.N, self.m), self.torch.float64, name)
+
+    def _cellv(self, t, name, dtype=None):
+        return _dev(t, self, (self.cells,), dtype or self.torch.int32, name)
+
     def ipm_dual_solve(self, uhat, lam, mode=None, iters=None, status=None, crit=None):
         mode = NEWTON[mode or self.cfg["newton"]]
-        check(lib().ipm_dual_solve(self.h, _ptr(uhat), _ptr(lam), mode, _ptr(iters), _ptr(status), _ptr(crit)),
-              "ipm_dual_solve")
+        with self.torch.cuda.device(self.device):
+            check(lib().ipm_dual_solve(self.h, self._state(uhat, "uhat"), self._state(lam, "lambda"), mode,
+                                       self._cellv(iters, "iters"), self._cellv(status, "status"),
+                                       self._cellv(crit, "crit", self.torch.float64)), "ipm_dual_solve")
 
     def ipm_flux_update(self, lam, uhat_old, uhat_new, dt=-1.0, dt_out=None):
-        check(lib().ipm_flux_update(self.h, _ptr(lam), _ptr(uhat_old), _ptr(uhat_new), float(dt), _ptr(dt_out)),
-              "ipm_flux_update")
+        with self.torch.cuda.device(self.device):
+            check(lib().ipm_flux_update(self.h, self._state(lam, "lambda"), self._state(uhat_old, "uhat_old"),
+                                        self._state(uhat_new, "uhat_new"), float(dt),
+                                        _dev(dt_out, self, (1,), self.torch.float64, "dt_out")), "ipm_flux_update")
+
+    def get_status(self):
+        """(worst ipm_cell_status, failed cells) of the last dual solve (synchronous, ipm_get_status)"""
+        w, n = C.c_int32(), C.c_int64()
+        check(lib().ipm_get_status(self.h, C.byref(w), C.byref(n)), "ipm_get_status")
+        return w.value, n.value
+
+    def last_cell_linesearch(self):
+        """per-cell (rejected Armijo trials, inadmissible trials) of the last dual solve"""
+        hv = self.zeros(self.cells, dtype=self.torch.int32)
+        ia = self.zeros(self.cells, dtype=self.torch.int32)
+        check(lib().ipm_last_cell_linesearch(self.h, _ptr(hv), _ptr(ia)), "ipm_last_cell_linesearch")
+        return hv, ia
 
     def _halo_setup(self):
         npeers, nsend, nrecv = C.c_int32(), C.c_int64(), C.c_int64()
@@ -309,20 +375,24 @@ class Context:
         (paper_1912_09238_b200.dist, torch.distributed)."""
         info = ipm_step_info() if sync else None
         te = -1.0 if t_end is None else float(t_end)
+        pu, pl = self._state(uhat, "uhat"), self._state(lam, "lambda")
         if self.nranks <= 1:
-            rc = lib().ipm_step(self.h, _ptr(uhat), _ptr(lam), te, C.byref(info) if sync else None)
+            with self.torch.cuda.device(self.device):
+                rc = lib().ipm_step(self.h, pu, pl, te, C.byref(info) if sync else None)
         else:
             from . import dist
 
             if not hasattr(self, "sendbuf"):
                 self._halo_setup()
-            check(lib().ipm_step_dual(self.h, _ptr(uhat), _ptr(lam), _ptr(self.sendbuf), _ptr(self.rate)),
+            check(lib().ipm_step_dual(self.h, pu, pl, _ptr(self.sendbuf), _ptr(self.rate)),
                   "ipm_step_dual")
             dist.halo_exchange(self.sendbuf, self.recvbuf, self.halo, self.group)
             dist.allreduce_max_(self.rate, self.group)
-            rc = lib().ipm_step_flux(self.h, _ptr(uhat), _ptr(lam), _ptr(self.recvbuf), _ptr(self.rate), te,
+            rc = lib().ipm_step_flux(self.h, pu, pl, _ptr(self.recvbuf), _ptr(self.rate), te,
                                      C.byref(info) if sync else None)
             if sync and rc in (0, 5):
+                # this rank's own count, before info becomes the global sums (bench: imbalance)
+                self.last_local_newton_iters = int(info.newton_iters)
                 dist.reduce_info_(info, self.device, self.group)
                 rc = 5 if info.failed_cells else 0
                 if self.cfg.get("retard"):  # Alg. 4 stage from the global residual
@@ -343,8 +413,11 @@ class Context:
         buffers; copies overlapped with the dual solves in nchunks cell ranges (synchronous)."""
         info = ipm_step_info()
         te = -1.0 if t_end is None else float(t_end)
-        rc = lib().ipm_step_host(self.h, _ptr(h_uhat), _ptr(h_lam), _ptr(d_uhat), _ptr(d_lam), te, int(nchunks),
-                                 C.byref(info))
+        shape = (self.cells, self.N, self.m)
+        with self.torch.cuda.device(self.device):
+            rc = lib().ipm_step_host(self.h, _host(h_uhat, shape, "h_uhat"), _host(h_lam, shape, "h_lambda"),
+                                     self._state(d_uhat, "d_uhat"), self._state(d_lam, "d_lambda"), te, int(nchunks),
+                                     C.byref(info))
         if rc == 5:
             return info
         check(rc, "ipm_step_host")
@@ -394,13 +467,14 @@ class Context:
             s.ys1[d] = v
         for r, st in enumerate(ic["states"]):
             s.state[r] = _state(st)
-        check(lib().ipm_project_ic(self.h, C.byref(s), _ptr(uhat)), "ipm_project_ic")
+        check(lib().ipm_project_ic(self.h, C.byref(s), self._state(uhat, "uhat")), "ipm_project_ic")
 
     def ipm_warm_start(self, uhat, lam):
-        check(lib().ipm_warm_start(self.h, _ptr(uhat), _ptr(lam)), "ipm_warm_start")
+        check(lib().ipm_warm_start(self.h, self._state(uhat, "uhat"), self._state(lam, "lambda")), "ipm_warm_start")
 
     def ipm_moments_from_dual(self, lam, uhat):
-        check(lib().ipm_moments_from_dual(self.h, _ptr(lam), _ptr(uhat)), "ipm_moments_from_dual")
+        check(lib().ipm_moments_from_dual(self.h, self._state(lam, "lambda"), self._state(uhat, "uhat")),
+              "ipm_moments_from_dual")
 
     def ipm_stress_dual(self, base, z, rel, abs_, lam):
         check(lib().ipm_stress_dual(self.h, _ptr(base), _ptr(z), float(rel), float(abs_), _ptr(lam)),

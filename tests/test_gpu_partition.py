@@ -2,7 +2,8 @@
 the host moves the packed boundary duals between their send/receive buffers and takes the max of the
 CFL rates (what torch.distributed does across GPUs), and the owned cells must equal a single-context
 run bit for bit — including the adaptive config-4 path (halo duals at the old level, truncation
-after the flux).  No kernel waits on another context."""
+after the flux) — and the assembled result must match the oracle (1e-9, reading 27).  No kernel waits
+on another context."""
 import ctypes as C
 
 import numpy as np
@@ -10,6 +11,8 @@ import pytest
 
 from inputs import configs
 from inputs.generators import bump_channel_mesh
+
+from .gpu_common import assert_moments_close
 
 pytestmark = pytest.mark.gpu
 
@@ -83,11 +86,19 @@ def test_virtual_ranks_match_single_context(torch, name, R, px, py):
                 check(L.ipm_retard_advance(g.h, res), "ipm_retard_advance")
     seen = np.zeros(ref.cells, bool)
     ur = u_ref.cpu().numpy()
+    assembled = np.zeros_like(ur)
     for g, u in zip(ctxs, us):
         ids = g.cell_ids()
         assert not seen[ids].any()
         seen[ids] = True
         np.testing.assert_array_equal(u.cpu().numpy(), ur[ids])
+        assembled[ids] = u.cpu().numpy()
     assert seen.all()
+    # the assembled R-rank result against the oracle (not only against the GPU's single context)
+    import oracle
+
+    o = oracle.Oracle(cfg, ma)
+    u_o, _, _ = o.run(n_steps=steps, t_end=1e9)
+    assert_moments_close(assembled, u_o, 1e-9, f"{name} {R} ranks vs oracle")
     if cfg.get("retard"):
         assert ref.retard_stage() == 2 and all(g.retard_stage() == 2 for g in ctxs)

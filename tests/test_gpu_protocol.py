@@ -1,0 +1,78 @@
+"""GPU parity at the sizes and horizons of SURVEY §8(c)'s parity protocol (Algorithm 1 to the final
+step; One-Shot Algorithm 2/3):
+
+* config 3: 64^2 grid, Algorithm 1 from the IC to t = 0.25;
+* config 4: ~2k-triangle seeded bump channel, 200 adaptive One-Shot pseudo-steps;
+* config 5: 32^2 grid, 10 steps.
+
+Criteria (BASELINE north star, reading 27): moments within 1e-9 of the state's scale after the final
+step, every step's dt within 1e-12, Newton counts +-1 per cell and step; config 4 also the steady
+residual of every step and the levels.
+"""
+import numpy as np
+import pytest
+
+from inputs import configs
+
+from .gpu_common import assert_moments_close, mesh_arrays, to_np
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+
+    if not t.cuda.is_available():
+        pytest.fail("GPU test needs CUDA (no CPU fallback exists)")
+    return t
+
+
+def run_both(cfg, n_steps=None):
+    import oracle
+    from paper_1912_09238_b200 import Context
+
+    ma = mesh_arrays(cfg)
+    g, o = Context(cfg, ma), oracle.Oracle(cfg, ma)
+    u_o, l_o, io = o.run(n_steps=n_steps, record=True)
+    u_g, l_g, ig = g.run(n_steps=n_steps, record=True)
+    return g, o, (u_o, l_o, io), (to_np(u_g), to_np(l_g), ig)
+
+
+def check_history(io, ig, residual=False):
+    assert io["steps"] == ig["steps"]
+    flips = 0
+    for (dto, ito, ro), (dtg, itg, rg) in zip(io["hist"], ig["hist"]):
+        assert abs(dto - dtg) <= 1e-12 * dto
+        d = np.abs(ito - itg)
+        assert d.max() <= 1
+        flips += int((d > 0).sum())
+        if residual:
+            assert abs(ro - rg) <= 1e-9 * max(ro, 1e-300)
+    return flips
+
+
+def test_cfg3_64x64_to_final_time(torch):
+    cfg = configs.get("cfg3", mesh=dict(nx=64, ny=64))
+    g, o, (u_o, _, io), (u_g, _, ig) = run_both(cfg)
+    assert abs(io["t"] - 0.25) < 1e-14 and abs(ig["t"] - 0.25) < 1e-14
+    check_history(io, ig)
+    assert_moments_close(u_g, u_o, 1e-9, "cfg3 64^2 t=0.25")
+
+
+def test_cfg4_2k_triangles_200_pseudo_steps(torch):
+    cfg = configs.get("cfg4", mesh=dict(nx_pts=56, ny_pts=20))
+    g, o, (u_o, _, io), (u_g, _, ig) = run_both(cfg, n_steps=200)
+    assert o.cells >= 2000
+    check_history(io, ig, residual=True)
+    lv_o, lv_g = o.levels(), to_np(g.levels())
+    assert (lv_o != lv_g).mean() < 0.005
+    assert len(np.unique(lv_o)) >= 2  # the ladder is exercised
+    assert_moments_close(u_g, u_o, 1e-9, "cfg4 2k triangles 200 steps")
+
+
+def test_cfg5_32x32_10_steps(torch):
+    cfg = configs.get("cfg5", mesh=dict(nx=32, ny=32))
+    g, o, (u_o, _, io), (u_g, _, ig) = run_both(cfg, n_steps=10)
+    check_history(io, ig)
+    assert_moments_close(u_g, u_o, 1e-9, "cfg5 32^2 10 steps")
