@@ -38,7 +38,7 @@ def test_our_arm_contract():
               "vs_baseline", "dtype", "data", "config", "roofline", "roofline_flux", "e2e", "gpu_launches", "clocks"):
         assert k in d, k
     r = d["roofline"]
-    assert r["kernel"] in ("k_dual_mma", "k_dual_group") and 0 < r["frac"] < 1 and 0 < r["executed"]["frac"] < 1
+    assert r["kernel"] in ("k_dual_mma", "k_dual_group") and 0 < r["frac"] < 1 and 0 < r["algorithmic"]["frac"] < 1
     assert r["bound"] == "alu" and r["unit"] == "TFLOP/s"
     assert d["roofline_flux"]["bound"] == "hbm" and 0 < d["roofline_flux"]["frac"] < 1
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
