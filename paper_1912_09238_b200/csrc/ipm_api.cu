@@ -630,9 +630,47 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   k.dual_group = env_is("IPM_DUAL_KERNEL", "group") ? 1 : 0;
   k.sumfact = env_is("IPM_SUMFACT", "0") ? 0 : 1;
   k.mma_w4 = env_is("IPM_MMA_W", "4") ? 1 : 0;
+  k.mma_generic = env_is("IPM_MMA_SHAPE", "generic") ? 1 : 0;
   k.mma_groups = std::getenv("IPM_MMA_GROUPS") ? std::max(1, std::atoi(std::getenv("IPM_MMA_GROUPS"))) : 0;
   k.group_t1 = env_is("IPM_GROUP_T", "1") ? 1 : 0;
   k.flux_choice = env_is("IPM_FLUX_KERNEL", "cart") ? 1 : env_is("IPM_FLUX_KERNEL", "warp") ? 2 : 0;
+  // adaptive degree bucketed into uniform-degree launches (north star (c)): Euler 2D, tensor
+  // Gauss-Legendre sum factorisation, every level's (n = N_l m, degree) among the k_dual_mma shapes
+  // (n <= 24 / 40 / 64 / 88 with degrees 2 / 3 / 4 / 5); IPM_BUCKET=0 keeps the single N_max launch
+  k.bucket = 0;
+  if (C.n_levels > 0 && C.closure == IPM_CLOSURE_EULER && m == 4 && p == 2 && tensor_gl && !env_is("IPM_BUCKET", "0")) {
+    bool ok = true;
+    for (int l = 0; l < C.n_levels; ++l) ok = ok && C.level_M[l] >= 2 && C.level_M[l] <= 5;
+    if (ok) {
+      k.lists = dalloc<int32_t>((size_t)C.n_levels * std::max<int64_t>(cells, 1), c->owned);
+      if (!k.lists) {
+        ipm_destroy(c);
+        return fail(IPM_ERR_CUDA, "cudaMalloc (level lists) failed");
+      }
+      for (int l = 0; l < C.n_levels; ++l) {
+        const int Ml = C.level_M[l], nprl = (Ml + 1) * (Ml + 2) / 2;
+        std::vector<double> LLl((size_t)C.q1d * nprl);
+        for (int kq = 0; kq < C.q1d; ++kq) {
+          int pr = 0;
+          for (int aa = 0; aa <= Ml; ++aa)
+            for (int bb = aa; bb <= Ml; ++bb, ++pr)
+              LLl[(size_t)kq * nprl + pr] = 0.5 * w1[kq] * legendre_orthonormal(aa, x1[kq]) * legendre_orthonormal(bb, x1[kq]);
+        }
+        double* d_LLl = dalloc<double>(LLl.size(), c->owned);
+        if (!d_LLl || cudaMemcpy(d_LLl, LLl.data(), LLl.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
+          ipm_destroy(c);
+          return fail(IPM_ERR_CUDA, "level tables upload failed");
+        }
+        ipm::Tables t = k.T;
+        t.N = binom_total(p, Ml);
+        t.MT = (t.N + 7) / 8;
+        t.LL = d_LLl;
+        t.npr = nprl;
+        k.Tl[l] = t;
+      }
+      k.bucket = 1;
+    }
+  }
   *out = c;
   return IPM_OK;
 }

@@ -76,6 +76,8 @@ struct StepScalars {
   // rejected line-search trials and the inadmissible ones among them
   unsigned long long hist[16];
   unsigned long long halvings, inadm_trials;
+  // adaptive degree in uniform-degree buckets: cells per level, and a work queue per level's launch
+  int lvl_count[8], lvl_queue[8];
 };
 constexpr int kHistBuckets = 16;
 
@@ -93,6 +95,12 @@ struct DualLaunch {
   int want_rate;
   int32_t* halv;   // [cells] rejected line-search trials of the cell (nullable)
   int32_t* inadm;  // [cells] of which inadmissible (non-finite L / closure) (nullable)
+  // bucketed launches (k_dual_mma): the cells are list[0 .. *ncells_dev) (device count), the queue a
+  // per-launch counter, row the [cells][row] stride of uhat / lambda (0: N m of the tables)
+  const int32_t* list;
+  const int32_t* ncells_dev;
+  int* queue;
+  int row;
 };
 
 struct FluxLaunch {
@@ -124,11 +132,17 @@ struct KernelCtx {
   int dual_group;    // 1: the 4x4-register-block kernel instead of k_dual_mma
   int sumfact;       // 0: direct Hessian sum instead of the sum factorisation
   int mma_w4;        // 1: config 3 with W = 4 warps per cell
+  int mma_generic;   // 1: the run-time-shape k_dual_mma instance even where a fixed-shape one exists
   int mma_groups;    // > 0: cap on the groups per CTA of k_dual_mma
   int group_t1;      // 1: one Hessian block per thread in k_dual_group
   int flux_choice;   // 0 default (strip when applicable), 1 cart, 2 warp
   double* big_scratch;    // per-CTA scratch of the large-cell dual kernel (config 5), or null
   int big_ctas;
+  // adaptive degree bucketed into uniform-degree launches (north star (c); Alg. 3): per-level
+  // tables (N_l, its 1D pair table, tile counts; Phi / omega Phi shared by prefix) and cell lists
+  int bucket;             // 1: one k_dual_mma launch per level over that level's cells
+  Tables Tl[8];
+  int32_t* lists;         // [n_levels][cells]
 };
 
 // launchers (ipm_kernels.cu); return 0 on success, else a cudaError_t / -1 unsupported

@@ -1197,7 +1197,7 @@ size_t big_scratch_doubles(int N, int Q, int m, int q1d, int npr, int p) {
   return m == 4 ? BigLayout<4>::scratch(N, Q, q1d, npr, p) : 0;
 }
 
-template <int CL, int MS, int NB, int W, int SF>
+template <int CL, int MS, int NB, int W, int SF, int QC = 0, int NC = 0, int Q1C = 0>
 static int dual_mma_impl(const KernelCtx& k, const DualLaunch& a) {
   using Lay = MmaLayout<MS>;
   constexpr int G = 32 * W;
@@ -1210,7 +1210,7 @@ static int dual_mma_impl(const KernelCtx& k, const DualLaunch& a) {
   groups = std::min(groups, std::min(512 / G, 15));  // named barriers 1..15 (0 = __syncthreads)
   if (k.mma_groups > 0) groups = std::min(groups, k.mma_groups);  // experiments
   const size_t smem = tab + groups * pg;
-  auto kern = k_dual_mma<CL, MS, NB, W, SF>;
+  auto kern = k_dual_mma<CL, MS, NB, W, SF, QC, NC, Q1C>;
   int per_sm = configure(kern, groups * G, smem);
   if (per_sm < 1) return -1;
   const int64_t want = (a.cells + groups - 1) / groups;
@@ -1223,11 +1223,26 @@ static int dual_mma_impl(const KernelCtx& k, const DualLaunch& a) {
 
 // DMMA-Cholesky kernel: 8x8 blocks of the padded n x n Hessian, W warps per cell so that the
 // register blocks fit (<= 18 blocks per warp)
-static int dual_mma_dispatch(const KernelCtx& k, const DualLaunch& a, int SF) {
+int dual_mma_dispatch(const KernelCtx& k, const DualLaunch& a, int SF) {
   const int n = k.T.N * k.m, NB = (n + 7) / 8;
   const int key = ((k.closure * 10 + k.m) * 100 + NB) * 10 + SF;
   if (k.mma_w4 && key == ((CL_EULER * 10 + 4) * 100 + 8) * 10 + 5)
     return dual_mma_impl<CL_EULER, 4, 8, 4, 5>(k, a);
+  // the BASELINE configurations' shapes: compile-time-shape instances (Q, N, q1d constants)
+  if (!k.mma_generic && (k.ad.n_levels == 0 || a.list)) {  // uniform N over the launch
+    const int q1 = SF > 0 ? k.T.q1d : 0;
+#define IPM_FCASE(CLV, MSV, NBV, WV, SFV, QV, NV, Q1V)                                                 \
+  if (key == ((CLV * 10 + MSV) * 100 + NBV) * 10 + SFV && k.T.Q == QV && k.T.N == NV && q1 == Q1V) \
+    return dual_mma_impl<CLV, MSV, NBV, WV, SFV, QV, NV, Q1V>(k, a);
+    IPM_FCASE(CL_BARRIER, 1, 1, 1, 0, 20, 6, 0)   // config 1
+    IPM_FCASE(CL_EULER, 3, 4, 1, 0, 30, 10, 0)    // config 2
+    IPM_FCASE(CL_EULER, 4, 8, 2, 5, 100, 15, 10)  // config 3
+    IPM_FCASE(CL_EULER, 4, 11, 4, 6, 144, 21, 12) // config 4 (degree 5)
+    IPM_FCASE(CL_EULER, 4, 3, 1, 3, 144, 6, 12)   // config 4 degree-2 bucket
+    IPM_FCASE(CL_EULER, 4, 5, 1, 4, 144, 10, 12)  // config 4 degree-3 bucket
+    IPM_FCASE(CL_EULER, 4, 8, 2, 5, 144, 15, 12)  // config 4 degree-4 bucket
+#undef IPM_FCASE
+  }
   switch (key) {
 #define IPM_MCASE(CLV, MSV, NBV, WV, SFV) \
   case ((CLV * 10 + MSV) * 100 + NBV) * 10 + SFV: return dual_mma_impl<CLV, MSV, NBV, WV, SFV>(k, a);
@@ -1247,8 +1262,54 @@ static int dual_mma_dispatch(const KernelCtx& k, const DualLaunch& a, int SF) {
 static const char* g_last_dual = "";
 const char* last_dual_kernel() { return g_last_dual; }
 
+// cells -> per-level lists (warp-aggregated atomics; the order inside a list is irrelevant: every
+// cell's solve is independent of the others)
+__global__ void k_bucket(const int32_t* __restrict__ level, int64_t cells, int32_t* __restrict__ lists,
+                         StepScalars* sc) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x; j0 < cells; j0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = j0 + threadIdx.x;
+    const bool live = j < cells;
+    const int l = live ? level[j] : -1;
+    const unsigned peers = __match_any_sync(FULL_MASK, l);
+    const int leader = __ffs(peers) - 1;
+    int base = 0;
+    if (live && lane == leader) base = atomicAdd(&sc->lvl_count[l], __popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    if (live) lists[(int64_t)l * cells + base + __popc(peers & ((1u << lane) - 1))] = (int32_t)j;
+  }
+}
+
+int dual_mma_dispatch(const KernelCtx& k, const DualLaunch& a, int SF);
+
+// adaptive degree in uniform-degree buckets (north star (c); Alg. 3): one k_dual_mma launch per
+// level with that level's basis size N_l (its own register-block shape and warps per cell) over the
+// level's cells, instead of one launch at N_max looping over each cell's level
+static int launch_dual_bucketed(const KernelCtx& k, const DualLaunch& a) {
+  const int L = k.ad.n_levels;
+  cudaMemsetAsync(&k.sc->lvl_count[0], 0, sizeof(int) * 16, S(k));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((a.cells + 255) / 256, (int64_t)k.sm_count * 8));
+  k_bucket<<<grid, 256, 0, S(k)>>>(a.level, a.cells, k.lists, k.sc);
+  for (int l = 0; l < L; ++l) {
+    KernelCtx kl = k;
+    kl.T = k.Tl[l];
+    kl.bucket = 0;
+    DualLaunch al = a;
+    al.list = k.lists + (int64_t)l * a.cells;
+    al.ncells_dev = &k.sc->lvl_count[l];
+    al.queue = &k.sc->lvl_queue[l];
+    al.row = k.T.N * k.m;
+    const int SF = (k.T.p == 2 && k.sumfact) ? (int)std::lround((std::sqrt(8.0 * kl.T.npr + 1) - 1) / 2) : 0;
+    const int rc = dual_mma_dispatch(kl, al, SF);
+    if (rc) return rc;
+  }
+  g_last_dual = "k_dual_mma";
+  return (int)cudaGetLastError();
+}
+
 int launch_dual(const KernelCtx& k, const DualLaunch& a) {
   if (a.cells == 0) return 0;
+  if (k.bucket && a.level && !a.list && !k.force_warp_kernel && !k.dual_group) return launch_dual_bucketed(k, a);
   // default: the DMMA-Cholesky kernel where it is instantiated; IPM_DUAL_KERNEL=group selects the
   // 4x4-register-block kernel (comparison, tests)
   if (!k.force_warp_kernel && !k.dual_group) {

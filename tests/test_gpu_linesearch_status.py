@@ -175,3 +175,25 @@ def test_step_host_256_64_chunks_is_bit_identical(torch):
         assert info.failed_cells == 0
     np.testing.assert_array_equal(h_u.numpy(), to_np(u1))
     np.testing.assert_array_equal(h_l.numpy(), to_np(l1))
+
+
+@pytest.mark.parametrize("thresholds", [None, (1e-8, 1e-7)])
+def test_bucketed_levels_match_single_launch_and_oracle(torch, thresholds):
+    """Adaptive degree (north star (c), Alg. 3): the per-level launches over uniform-degree buckets
+    (default) against the single N_max launch (IPM_BUCKET=0) and the oracle, 30 One-Shot steps of the
+    config-4 parity mesh; with the lower thresholds cells move between levels during the run"""
+    cfg = configs.parity_variant("cfg4")
+    if thresholds:
+        cfg["delta_dec"], cfg["delta_inc"] = thresholds
+    out = []
+    for env in (None, {"IPM_BUCKET": "0"}):
+        g, o, _ = make(cfg, env)
+        u, lam, info = g.run(n_steps=30)
+        out.append((to_np(u), to_np(g.levels())))
+    u_o, _, _ = o.run(n_steps=30)
+    np.testing.assert_array_equal(out[0][1], out[1][1])
+    np.testing.assert_allclose(out[0][0], out[1][0], rtol=0, atol=1e-12 * np.abs(out[1][0]).max())
+    from .gpu_common import assert_moments_close
+
+    assert_moments_close(out[0][0], u_o, 1e-9, "bucketed cfg4")
+    assert (o.levels() != out[0][1]).mean() < 0.01
