@@ -39,8 +39,12 @@ def parse():
     ap.add_argument("--nx", type=int, default=0, help="override grid size (cartesian nx = ny)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=64, help="ipm_step_host copy/solve ranges (e2e, N=1)")
+    ap.add_argument("--e2e-max-gb", type=float, default=16.0, help="largest state (uhat + lambda) the e2e leg pins")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=9238)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = every rank a block of the configured grid; strong = the configured grid "
+                         "split into N blocks (fixed total work)")
     return ap.parse_args()
 
 
@@ -283,7 +287,7 @@ def run_ours(args):
             dist.init_process_group(backend)
     cfg = workload(args)
     px, py = decompose(world)
-    if world > 1 and cfg["mesh"]["kind"] == "cart2d":
+    if world > 1 and cfg["mesh"]["kind"] == "cart2d" and args.scaling == "weak":
         # weak scaling: every rank owns a block of the single-GPU size, halos exchanged over NVLink
         cfg["mesh"].update(nx=cfg["mesh"]["nx"] * px, ny=cfg["mesh"]["ny"] * py)
     ma = mesh_arrays(cfg)
@@ -298,15 +302,17 @@ def run_ours(args):
     base, z = stress_state(kind, xy, g.N, g.m, args.seed + rank, cfg.get("gamma", 1.4))
     amp = STRESS_AMP[kind]
     dev = torch.device("cuda", local)
-    lam_s = g.zeros()
-    g.ipm_stress_dual(torch.from_numpy(base).to(dev), torch.from_numpy(z).to(dev), amp[0], amp[1], lam_s)
+    # two state arrays only (config 5 at 4096^2: 30 GB each): lambda* -> uhat = h(lambda*) -> warm start
+    lam = g.zeros()
+    d_base, d_z = torch.from_numpy(base).to(dev), torch.from_numpy(z).to(dev)
     del base, z
-    u0 = g.zeros()
-    g.ipm_moments_from_dual(lam_s, u0)
-    lam0 = g.zeros()
-    g.ipm_warm_start(u0, lam0)
-    uhat, lam = u0.clone(), lam0.clone()
-    del u0, lam0, lam_s
+    g.ipm_stress_dual(d_base, d_z, amp[0], amp[1], lam)
+    del d_base, d_z
+    uhat = g.zeros()
+    g.ipm_moments_from_dual(lam, uhat)
+    g.ipm_warm_start(uhat, lam)
+    torch.cuda.synchronize()
+    state_gb = 2 * uhat.numel() * 8 / 1e9
     g.enable_timing(True)
 
     def barrier():
@@ -320,7 +326,9 @@ def run_ours(args):
     barrier()
     # the starting state of the timed steps: the e2e leg below re-runs exactly these steps
     t_start = g.time()
-    u_start, l_start = uhat.cpu().pin_memory(), lam.cpu().pin_memory()
+    do_e2e = not args.no_e2e and state_gb <= args.e2e_max_gb
+    if do_e2e:
+        u_start, l_start = uhat.cpu().pin_memory(), lam.cpu().pin_memory()
     # timed region: K consecutive steps (Algorithm 1), device-timed with CUDA events
     # inputs smaller than L2 (configs 1, 2, small windows): every step is timed on its own after an
     # L2 flush (a write of twice the L2 size), and the step times are summed
@@ -380,8 +388,9 @@ def run_ours(args):
 
     # end-to-end through the C-ABI with host buffers: H2D of the step inputs (uhat, lambda) from
     # pinned memory, ipm_step, D2H of the step result (uhat, lambda), every step
-    e2e = None
-    if not args.no_e2e:
+    e2e = None if do_e2e or args.no_e2e else {
+        "value": None, "skipped": f"state {state_gb:.0f} GB exceeds --e2e-max-gb {args.e2e_max_gb} of pinned host memory"}
+    if do_e2e:
         # the SAME K steps from the same starting state (host copies of the state after warm-up)
         h_u, h_l = u_start, l_start
         g.set_time(t_start)
@@ -440,7 +449,7 @@ def run_ours(args):
         line = {
             "metric": "IPM cell-steps/s (= cell dual-solves/s)", "value": value, "unit": "cell-steps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": args.config, "cells_per_gpu": g.cells, "N": N, "m": m, "Q": Q,
                        "newton": cfg["newton"], "tau": cfg["tau"],
@@ -448,7 +457,8 @@ def run_ours(args):
                        "l2": ("L2 flushed before every timed step (step state %.1f MB < 2x L2)" % (state_bytes / 1e6))
                        if flush else "inputs larger than L2 (node states %.1f GB)" % (g.cells * Q * m * 8 / 1e9),
                        "parallelism": f"domain decomposition {px}x{py}, {os.environ.get('IPM_DIST_BACKEND', 'nccl').upper()} halo exchange" if world > 1
-                       else "single", "global_cells": g.cells * world},
+                       else "single", "global_cells": g.cells * world,
+                       "node_state_bands": g.node_band_rows()},
             "newton_iters_per_cell_step": iters_all / (cells_total * args.steps),
             "cell_newton_iters_per_s": iters_all / (ms / 1e3),
             "newton_imbalance_max_over_mean": imbalance,

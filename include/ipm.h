@@ -162,6 +162,12 @@ IPM_API const char *ipm_last_error(void);
 
 /* sizes of the local problem: cells (owned), N, Q, m */
 IPM_API ipm_status ipm_sizes(const ipm_ctx *c, int64_t *cells, int32_t *N, int32_t *Q, int32_t *m);
+/* Node-state storage chosen by ipm_init (host only): *rows = 0 when the context keeps the node states
+ * u_s(lambda^T phi(xi_k)) of all cells ([cells + halo][m][Q], written by the dual solve for the flux),
+ * else the rows per band of the banded mode (row-major cartesian blocks without levels whose whole
+ * buffer would exceed IPM_NODE_BUDGET_GB, default 24 GB, or IPM_BAND_ROWS set): the flux then
+ * recomputes each band's node states from lambda (PAPER.md:455-462 needs them only face by face). */
+IPM_API ipm_status ipm_node_band_rows(const ipm_ctx *c, int64_t *rows);
 /* host copies of the basis tables: h_xi [Q][p], h_omega [Q], h_phi [Q][N] (any may be NULL) */
 IPM_API ipm_status ipm_get_basis(const ipm_ctx *c, double *h_xi, double *h_omega, double *h_phi);
 /* host copy of the owned cells' global ids [cells] (int64) */

@@ -308,6 +308,11 @@ struct ipm_ctx {
   const double *g_uhat = nullptr, *g_lambda = nullptr;
   double g_tend = 0.0;
   bool graph_off = false;
+  // banded node states (meshes whose [cells + halo][m][Q] buffer would not fit: config 5 at 4096^2
+  // is 537 GB): d_uq holds band_rows + 2 rows of a row-major cartesian block, d_uq_halo the halo cells;
+  // the dual kernel then writes no node states, the flux recomputes each band's from lambda
+  int64_t band_rows = 0;
+  double* d_uq_halo = nullptr;
 };
 
 extern "C" {
@@ -515,7 +520,6 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   double* d_area = dalloc<double>(area.size(), O);
   double* d_rgeo = dalloc<double>(rgeo.size(), O);
   double* d_ghost = dalloc<double>(ghost.size(), O);
-  c->d_uq = dalloc<double>((size_t)(cells + c->halo) * Q * m, O);
   c->d_gid = dalloc<int64_t>(cells, O);
   c->d_send_local = dalloc<int32_t>(c->part.send_local.size(), O);
   c->d_crit = dalloc<double>(cells, O);
@@ -527,7 +531,7 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   c->d_inadm = dalloc<int32_t>(cells, O);
   c->d_sc = dalloc<ipm::StepScalars>(1, O);
   if (!d_PhiT || !d_WPhiT || !d_WPhiF || !d_omega || !d_deg || !d_LL || !d_idx || !d_nbr || !d_nrm || !d_coef || !d_area || !d_rgeo || !d_ghost ||
-      !c->d_uq || !c->d_gid || !c->d_send_local || !c->d_crit || !c->d_level || !c->d_level_new || !c->d_iters || !c->d_status || !c->d_halv || !c->d_inadm || !c->d_sc) {
+      !c->d_gid || !c->d_send_local || !c->d_crit || !c->d_level || !c->d_level_new || !c->d_iters || !c->d_status || !c->d_halv || !c->d_inadm || !c->d_sc) {
     ipm_destroy(c);
     return fail(IPM_ERR_CUDA, "cudaMalloc failed");
   }
@@ -546,8 +550,6 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
       up(c->d_send_local, c->part.send_local.data(), c->part.send_local.size() * 4) ||
       cudaMemset(c->d_sc, 0, sizeof(ipm::StepScalars)) || cudaMemset(c->d_level, 0, cells * 4) ||
       cudaMemset(c->d_level_new, 0, cells * 4) ||
-      // node states: defined before the first dual solve writes them (halo rows: before the first exchange)
-      cudaMemset(c->d_uq, 0, (size_t)(cells + c->halo) * Q * m * 8) ||
       cudaMemset(c->d_iters, 0, cells * 4) || cudaMemset(c->d_status, 0, cells * 4) ||
       cudaMemset(c->d_halv, 0, cells * 4) || cudaMemset(c->d_inadm, 0, cells * 4)) {
     ipm_destroy(c);
@@ -590,6 +592,32 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
     if (ok && cells < ((int64_t)1 << 31)) {
       k.mesh.bx = (int)bx;
       k.mesh.by = (int)(cells / bx);
+    }
+  }
+  // node-state buffer: whole mesh, or bands of rows (IPM_BAND_ROWS forces bands of that many rows, e.g.
+  // for parity tests; otherwise bands when the whole buffer would exceed IPM_NODE_BUDGET_GB, default 24)
+  {
+    const size_t per_cell = (size_t)Q * m * 8;
+    const double budget = (std::getenv("IPM_NODE_BUDGET_GB") ? std::atof(std::getenv("IPM_NODE_BUDGET_GB")) : 24.0) * 1e9;
+    const int64_t forced = std::getenv("IPM_BAND_ROWS") ? std::atoll(std::getenv("IPM_BAND_ROWS")) : 0;
+    const bool can_band = k.mesh.bx > 0 && C.n_levels == 0;
+    if (can_band && (forced > 0 || (double)(cells + c->halo) * per_cell > budget)) {
+      const int64_t rows = forced > 0 ? forced : std::max<int64_t>(1, (int64_t)(budget / ((double)k.mesh.bx * per_cell)) - 2);
+      c->band_rows = std::min<int64_t>(rows, k.mesh.by);
+      c->d_uq = dalloc<double>((size_t)(c->band_rows + 2) * k.mesh.bx * Q * m, O);
+      c->d_uq_halo = dalloc<double>((size_t)std::max<int64_t>(c->halo, 1) * Q * m, O);
+      if (!c->d_uq || !c->d_uq_halo || cudaMemset(c->d_uq, 0, (size_t)(c->band_rows + 2) * k.mesh.bx * per_cell) ||
+          cudaMemset(c->d_uq_halo, 0, (size_t)std::max<int64_t>(c->halo, 1) * per_cell)) {
+        ipm_destroy(c);
+        return fail(IPM_ERR_CUDA, "cudaMalloc (node-state bands) failed");
+      }
+    } else {
+      c->d_uq = dalloc<double>((size_t)(cells + c->halo) * Q * m, O);
+      // defined before the first dual solve writes them (halo rows: before the first exchange)
+      if (!c->d_uq || cudaMemset(c->d_uq, 0, (size_t)(cells + c->halo) * per_cell)) {
+        ipm_destroy(c);
+        return fail(IPM_ERR_CUDA, "cudaMalloc (node states) failed");
+      }
     }
   }
   k.nw = ipm::Newton{C.tau, C.armijo_c, C.max_newton, C.max_halvings, C.newton_mode};
@@ -684,6 +712,12 @@ ipm_status ipm_sizes(const ipm_ctx* c, int64_t* cells, int32_t* N, int32_t* Q, i
   return IPM_OK;
 }
 
+ipm_status ipm_node_band_rows(const ipm_ctx* c, int64_t* rows) {
+  if (!c || !rows) return fail(IPM_ERR_ARG, "null argument");
+  *rows = c->band_rows;
+  return IPM_OK;
+}
+
 ipm_status ipm_get_basis(const ipm_ctx* c, double* h_xi, double* h_omega, double* h_phi) {
   if (!c) return fail(IPM_ERR_ARG, "null ctx");
   if (h_xi) std::memcpy(h_xi, c->xi.data(), c->xi.size() * 8);
@@ -749,7 +783,31 @@ static int halo_nodes(ipm_ctx* c, const double* d_recv) {
   if (c->halo == 0) return 0;
   ipm::KernelCtx kh = c->k;
   kh.mesh.cells = c->halo;
-  return ipm::launch_nodes(kh, d_recv, nullptr, c->d_uq + (size_t)c->cells * c->Q * c->m, 0);
+  double* dst = c->band_rows ? c->d_uq_halo : c->d_uq + (size_t)c->cells * c->Q * c->m;
+  return ipm::launch_nodes(kh, d_recv, nullptr, dst, 0);
+}
+
+// the flux update over bands of rows (banded node states): per band, the node states of its rows and
+// the rows above and below from lambda (k_nodes), then the flux of the band's cells
+static int band_flux(ipm_ctx* c, const double* d_lambda, ipm::FluxLaunch f) {
+  const ipm::KernelCtx& k = c->k;
+  const int64_t bx = k.mesh.bx, by = k.mesh.by, R = c->band_rows, row = (int64_t)c->N * c->m;
+  for (int64_t r0 = 0; r0 < by; r0 += R) {
+    const int64_t r1 = std::min(by, r0 + R), n0 = std::max<int64_t>(0, r0 - 1), n1 = std::min(by, r1 + 1);
+    ipm::KernelCtx kn = k;
+    kn.mesh.cells = (n1 - n0) * bx;
+    if (int rc = ipm::launch_nodes(kn, d_lambda + n0 * bx * row, nullptr, c->d_uq, 0)) return rc;
+    ipm::KernelCtx kf = k;
+    kf.mesh.cells = r1 * bx;
+    ipm::FluxLaunch fb = f;
+    fb.uq = c->d_uq;
+    fb.cell0 = r0 * bx;
+    fb.uq_base = n0 * bx;
+    fb.n_owned = c->cells;
+    fb.uq_halo = c->d_uq_halo;
+    if (int rc = ipm::launch_flux(kf, fb)) return rc;
+  }
+  return 0;
 }
 
 ipm_status ipm_flux_update(ipm_ctx* c, const double* d_lambda, const double* d_uhat_old, double* d_uhat_new,
@@ -758,10 +816,18 @@ ipm_status ipm_flux_update(ipm_ctx* c, const double* d_lambda, const double* d_u
   if (c->halo > 0) return fail(IPM_ERR_ARG, "ipm_flux_update needs halo duals: use ipm_step_dual/ipm_step_flux");
   const ipm::KernelCtx& k = c->k;
   if (int rc = ipm::launch_step_begin(k, c->ghost_rate)) return launch_rc(rc, "step_begin");
-  if (int rc = ipm::launch_nodes(k, d_lambda, nullptr, c->d_uq, 1)) return launch_rc(rc, "nodes");
+  if (c->band_rows) {  // the CFL rate of every cell first (no node states kept), then band by band
+    if (int rc = ipm::launch_nodes(k, d_lambda, nullptr, nullptr, 1)) return launch_rc(rc, "nodes");
+  } else if (int rc = ipm::launch_nodes(k, d_lambda, nullptr, c->d_uq, 1)) {
+    return launch_rc(rc, "nodes");
+  }
   if (int rc = ipm::launch_dt(k, -1.0, dt, c->cfg.cfl)) return launch_rc(rc, "dt");
   ipm::FluxLaunch f{c->d_uq, d_uhat_old, d_uhat_new, nullptr, nullptr, c->cfg.update_form, c->cfg.cfl};
-  if (int rc = ipm::launch_flux(k, f)) return launch_rc(rc, "flux");
+  if (c->band_rows) {
+    if (int rc = band_flux(c, d_lambda, f)) return launch_rc(rc, "flux (bands)");
+  } else if (int rc = ipm::launch_flux(k, f)) {
+    return launch_rc(rc, "flux");
+  }
   if (d_dt) CUDA_OK(cudaMemcpyAsync(d_dt, &c->d_sc->dt, 8, cudaMemcpyDeviceToDevice, c->stream));
   return IPM_OK;
 }
@@ -780,7 +846,7 @@ ipm_status ipm_step_dual(ipm_ctx* c, const double* d_uhat, double* d_lambda, dou
   a.crit = c->d_crit;
   a.halv = c->d_halv;
   a.inadm = c->d_inadm;
-  a.uq = c->d_uq;
+  a.uq = c->band_rows ? nullptr : c->d_uq;  // banded: the flux recomputes the node states
   a.level = c->cfg.n_levels > 0 ? c->d_level : nullptr;
   a.level_new = c->cfg.n_levels > 0 ? c->d_level_new : nullptr;
   a.cells = c->cells;
@@ -807,7 +873,11 @@ ipm_status ipm_step_flux(ipm_ctx* c, double* d_uhat, double* d_lambda, const dou
   const int32_t* lvl_new = c->cfg.n_levels > 0 ? c->d_level_new : nullptr;
   ipm::FluxLaunch f{c->d_uq, d_uhat, d_uhat, lvl_new, d_lambda, c->cfg.update_form, c->cfg.cfl};
   if (c->timing) cudaEventRecord(c->ev[2], c->stream);
-  if (int rc = ipm::launch_flux(k, f)) return launch_rc(rc, "flux");
+  if (c->band_rows) {
+    if (int rc = band_flux(c, d_lambda, f)) return launch_rc(rc, "flux (bands)");
+  } else if (int rc = ipm::launch_flux(k, f)) {
+    return launch_rc(rc, "flux");
+  }
   if (c->timing) cudaEventRecord(c->ev[3], c->stream);
   if (c->cfg.n_levels > 0) std::swap(c->d_level, c->d_level_new);
   if (c->cfg.nranks <= 1)  // distributed: the caller advances with the global residual
@@ -924,7 +994,7 @@ ipm_status ipm_step_host(ipm_ctx* c, double* h_uhat, double* h_lambda, double* d
     a.crit = c->d_crit + r0;
     a.halv = c->d_halv + r0;
     a.inadm = c->d_inadm + r0;
-    a.uq = c->d_uq + (size_t)r0 * c->Q * c->m;
+    a.uq = c->band_rows ? nullptr : c->d_uq + (size_t)r0 * c->Q * c->m;
     a.level = adaptive ? c->d_level + r0 : nullptr;
     a.level_new = adaptive ? c->d_level_new + r0 : nullptr;
     a.cells = nr;

@@ -111,6 +111,11 @@ struct FluxLaunch {
   double* lam;               // nullable: duals truncated to the new level after the update
   int update_form;
   double cfl;
+  // banded node states (k_flux_warp; zero = the whole-mesh buffer): the cells [cell0, mesh.cells)
+  // are updated; the node states of owned cell c live at uq + (c - uq_base) Q m, those of halo cell
+  // c >= n_owned at uq_halo + (c - n_owned) Q m
+  int64_t cell0, uq_base, n_owned;
+  const double* uq_halo;
 };
 
 // Everything a launcher needs.

@@ -202,8 +202,15 @@ __device__ __forceinline__ double node_rate(const double* u, const Mesh& M, int6
     return fabs(u[0]) * M.inv_dx;
   } else {
     if (M.kind == MK_1D) return Euler<MS>::speed_dir(u, 0, gamma) * M.inv_dx;
-    if (M.kind == MK_CART)
-      return Euler<MS>::speed_dir(u, 0, gamma) * M.inv_dx + Euler<MS>::speed_dir(u, 1, gamma) * M.inv_dy;
+    if (M.kind == MK_CART) {  // (|v_x| + c)/dx + (|v_y| + c)/dy with 1/rho, p and c formed once
+      const double irho = 1.0 / u[0];
+      double m2 = 0.0;
+#pragma unroll
+      for (int k = 0; k < MS - 2; ++k) m2 = fma(u[1 + k], u[1 + k], m2);
+      const double p = (gamma - 1.0) * (u[MS - 1] - 0.5 * m2 * irho);
+      const double c = sqrt(gamma * p * irho);
+      return (fabs(u[1] * irho) + c) * M.inv_dx + (fabs(u[2] * irho) + c) * M.inv_dy;
+    }
     return Euler<MS>::speed_norm(u, gamma) * M.rate_geo[cell];
   }
 }
@@ -447,10 +454,15 @@ __global__ void __launch_bounds__(256) k_flux_warp(FluxParams P) {
   const FluxLaunch& A = P.a;
   double my_res = 0.0;
   const int64_t total_warps = (int64_t)gridDim.x * nw;
-  for (int64_t cell = (int64_t)blockIdx.x * nw + warp; cell < P.mesh.cells; cell += total_warps) {
+  // node states of cell c: whole-mesh buffer, or a band of owned cells plus a halo buffer
+  auto nodes_of = [&](int64_t c) -> const double* {
+    if (A.uq_halo && c >= A.n_owned) return A.uq_halo + (c - A.n_owned) * Q * MS;
+    return A.uq + (c - A.uq_base) * Q * MS;
+  };
+  for (int64_t cell = A.cell0 + (int64_t)blockIdx.x * nw + warp; cell < P.mesh.cells; cell += total_warps) {
     for (int k = lane; k < Q; k += 32) {
       double uj[MS], r[MS], gneg[MS];
-      const double* src = A.uq + cell * Q * MS + k;
+      const double* src = nodes_of(cell) + k;
 #pragma unroll
       for (int a = 0; a < MS; ++a) {
         uj[a] = src[a * Q];
@@ -468,7 +480,7 @@ __global__ void __launch_bounds__(256) k_flux_warp(FluxParams P) {
           nv[1] = (f >> 1) == 1 ? 1.0 : 0.0;
         }
         if (nbc >= 0) {
-          const double* s2 = A.uq + (int64_t)nbc * Q * MS + k;
+          const double* s2 = nodes_of(nbc) + k;
 #pragma unroll
           for (int a = 0; a < MS; ++a) un[a] = s2[a * Q];
         } else {
@@ -1390,7 +1402,7 @@ static int flux_impl(const KernelCtx& k, const FluxLaunch& a) {
   auto kern = k_flux_warp<FX, MS, MK>;
   int per_sm = configure(kern, warps * 32, smem);
   if (per_sm < 1) per_sm = 1;
-  const int64_t want = (k.mesh.cells + warps - 1) / warps;
+  const int64_t want = (k.mesh.cells - a.cell0 + warps - 1) / warps;
   int grid = (int)std::min<int64_t>(want, (int64_t)k.sm_count * per_sm * 4);
   if (grid < 1) grid = 1;
   FluxParams P{k.T, k.mesh, k.cl, k.ad, a, k.sc, in_smem};
@@ -1444,9 +1456,10 @@ static const char* g_last_flux = "";
 const char* last_flux_kernel() { return g_last_flux; }
 
 int launch_flux(const KernelCtx& k, const FluxLaunch& a) {
-  if (k.mesh.cells == 0) return 0;
+  if (k.mesh.cells <= a.cell0) return 0;
   const int key = (k.flux * 10 + k.m) * 10 + k.mesh.kind;
-  if (k.flux_choice == 0) {
+  const bool banded = a.uq_halo != nullptr;  // banded node states: the cell-range kernel only
+  if (k.flux_choice == 0 && !banded) {
 #ifndef IPM_STRIP_NT
 #define IPM_STRIP_NT 512
 #endif
@@ -1456,7 +1469,7 @@ int launch_flux(const KernelCtx& k, const FluxLaunch& a) {
       return rc;
     }
   }
-  if (k.flux_choice != 2) {
+  if (k.flux_choice != 2 && !banded) {
     int rc = -1;
     switch (key) {
       case (FX_LF_GLOBAL * 10 + 1) * 10 + MK_1D: rc = flux_cart_impl<FX_LF_GLOBAL, 1, MK_1D>(k, a); break;

@@ -30,7 +30,7 @@ EXPORTS = [
     "ipm_moments_from_dual", "ipm_stress_dual", "ipm_get_levels", "ipm_set_levels", "ipm_last_cell_stats",
     "ipm_get_time", "ipm_set_time", "ipm_last_kernel_ms", "ipm_enable_timing", "ipm_last_dual_kernel", "ipm_last_flux_kernel", "ipm_struct_size", "ipm_retard_stage", "ipm_retard_advance",
     "ipm_debug_phase_cycles", "ipm_step_dual", "ipm_step_flux", "ipm_halo_layout", "ipm_partition_query",
-    "ipm_get_status", "ipm_last_cell_linesearch",
+    "ipm_get_status", "ipm_last_cell_linesearch", "ipm_node_band_rows",
 ]
 HIST_BUCKETS = 16  # IPM_HIST_BUCKETS
 
@@ -133,6 +133,7 @@ def lib():
             "ipm_debug_phase_cycles": (st, [P]),
             "ipm_get_status": (st, [P, C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
             "ipm_last_cell_linesearch": (st, [P, I, I]),
+            "ipm_node_band_rows": (st, [P, C.POINTER(C.c_int64)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -340,6 +341,12 @@ class Context:
             check(lib().ipm_flux_update(self.h, self._state(lam, "lambda"), self._state(uhat_old, "uhat_old"),
                                         self._state(uhat_new, "uhat_new"), float(dt),
                                         _dev(dt_out, self, (1,), self.torch.float64, "dt_out")), "ipm_flux_update")
+
+    def node_band_rows(self) -> int:
+        """0: whole node-state buffer; else rows per band of the banded node states"""
+        r = C.c_int64()
+        check(lib().ipm_node_band_rows(self.h, C.byref(r)), "ipm_node_band_rows")
+        return r.value
 
     def get_status(self):
         """(worst ipm_cell_status, failed cells) of the last dual solve (synchronous, ipm_get_status)"""
