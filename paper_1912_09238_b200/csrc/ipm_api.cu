@@ -659,6 +659,7 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   k.sumfact = env_is("IPM_SUMFACT", "0") ? 0 : 1;
   k.mma_w4 = env_is("IPM_MMA_W", "4") ? 1 : 0;
   k.mma_generic = env_is("IPM_MMA_SHAPE", "generic") ? 1 : 0;
+  c->graph_off = env_is("IPM_GRAPH", "0");  // comparison: launch small steps kernel by kernel
   k.mma_groups = std::getenv("IPM_MMA_GROUPS") ? std::max(1, std::atoi(std::getenv("IPM_MMA_GROUPS"))) : 0;
   k.group_t1 = env_is("IPM_GROUP_T", "1") ? 1 : 0;
   k.flux_choice = env_is("IPM_FLUX_KERNEL", "cart") ? 1 : env_is("IPM_FLUX_KERNEL", "warp") ? 2 : 0;

@@ -107,7 +107,7 @@ __device__ __forceinline__ void face(const double* fl, double sl, const double* 
                                      const double* ur, double* g) {
   const double amax = fmax(sl, sr);
 #pragma unroll
-  for (int a = 0; a < 4; ++a) g[a] = 0.5 * (fl[a] + fr[a]) - 0.5 * amax * (ur[a] - ul[a]);
+  for (int a = 0; a < 4; ++a) g[a] = 0.5 * fma(-amax, ur[a] - ul[a], fl[a] + fr[a]);
 }
 
 // boundary node state for a face whose neighbour code is a boundary tag (k_flux_cart's rules)

@@ -203,12 +203,12 @@ __device__ __forceinline__ double node_rate(const double* u, const Mesh& M, int6
   } else {
     if (M.kind == MK_1D) return Euler<MS>::speed_dir(u, 0, gamma) * M.inv_dx;
     if (M.kind == MK_CART) {  // (|v_x| + c)/dx + (|v_y| + c)/dy with 1/rho, p and c formed once
-      const double irho = 1.0 / u[0];
+      const double irho = rcp_nr(u[0]);
       double m2 = 0.0;
 #pragma unroll
       for (int k = 0; k < MS - 2; ++k) m2 = fma(u[1 + k], u[1 + k], m2);
       const double p = (gamma - 1.0) * (u[MS - 1] - 0.5 * m2 * irho);
-      const double c = sqrt(gamma * p * irho);
+      const double c = sqrt_nr(gamma * p * irho);
       return (fabs(u[1] * irho) + c) * M.inv_dx + (fabs(u[2] * irho) + c) * M.inv_dy;
     }
     return Euler<MS>::speed_norm(u, gamma) * M.rate_geo[cell];
@@ -703,12 +703,12 @@ struct RusNode {
   static constexpr int D = MS - 2;
   double irho, p, c;
   __device__ void init(const double* u, double gamma) {
-    irho = 1.0 / u[0];
+    irho = rcp_nr(u[0]);
     double m2 = 0.0;
 #pragma unroll
     for (int k = 0; k < D; ++k) m2 = fma(u[1 + k], u[1 + k], m2);
     p = (gamma - 1.0) * (u[MS - 1] - 0.5 * m2 * irho);
-    c = sqrt(gamma * p * irho);
+    c = sqrt_nr(gamma * p * irho);
   }
   // F_dir(u) and |v_dir| + c
   __device__ void flux(const double* u, int dir, double* f, double& s) const {
