@@ -39,6 +39,10 @@ struct orc_ctx {
   int retard_stage; /* refinement retardation stage (Alg. 4) */
   int n_levels;
   int Nl[8];      /* N at each level */
+  /* L-BFGS history (hessian_kind 1, reading 35): per cell lbfgs_m pairs, newest first */
+  double *lb_S, *lb_Y; /* [cells][lbfgs_m][N m] */
+  int32_t *lb_cnt;     /* [cells] stored pairs */
+  int32_t *lb_n;       /* [cells] unknowns n the pairs belong to (a level change clears them) */
 };
 
 /* ------------------------------------------------------------------------ */
@@ -679,6 +683,13 @@ orc_ctx *orc_create(const orc_problem *P) {
   } else {
     c->Nl[0] = N;
   }
+  if (P->hessian_kind == 1) {
+    size_t per = (size_t)P->lbfgs_m * N * c->m;
+    c->lb_S = (double *)calloc((size_t)c->cells * per, sizeof(double));
+    c->lb_Y = (double *)calloc((size_t)c->cells * per, sizeof(double));
+    c->lb_cnt = (int32_t *)calloc(c->cells, sizeof(int32_t));
+    c->lb_n = (int32_t *)calloc(c->cells, sizeof(int32_t));
+  }
 #ifdef _OPENMP
   if (P->n_threads > 0) omp_set_num_threads(P->n_threads);
 #endif
@@ -688,6 +699,7 @@ orc_ctx *orc_create(const orc_problem *P) {
 void orc_destroy(orc_ctx *c) {
   if (!c) return;
   free(c->idx); free(c->xi); free(c->omega); free(c->Phi);
+  free(c->lb_S); free(c->lb_Y); free(c->lb_cnt); free(c->lb_n);
   free(c->nbr); free(c->nrm); free(c->coef); free(c->area); free(c->perim); free(c->xc);
   free(c->bc_u); free(c->level);
   free(c);
@@ -850,21 +862,132 @@ static int objective_and_scale(const orc_ctx *c, int Nl, const double *lam, cons
   return isfinite(s);
 }
 
+/* ---- L-BFGS direction (reading 35) -----------------------------
+ * PAPER.md:843 proposes BFGS Hessian approximations built "from previously computed gradients", with
+ * gradients "from a certain number of old time steps ... saved in every spatial cell".  Here: the
+ * limited-memory BFGS inverse-Hessian approximation of Nocedal & Wright (the paper's reference
+ * [nocedal2006numerical]; two-loop recursion, Alg. 7.4) over the cell's most recent pairs
+ * s = lambda^{(l+1)} - lambda^{(l)}, y = grad L(lambda^{(l+1)}) - grad L(lambda^{(l)}), with the initial
+ * matrix H0 = I_N (x) Jbar^{-1}, Jbar = <grad u_s(lambda^T phi)>_Q (m x m): the exact inverse Hessian
+ * when lambda^T phi does not depend on xi, because <phi phi^T>_Q = I. */
+int orc_lbfgs_jbar(const orc_ctx *c, int Nl, const double *lam, double *Jbar) {
+  int m = c->m;
+  double Lk[4], J[16];
+  for (int r = 0; r < m * m; ++r) Jbar[r] = 0.0;
+  for (int k = 0; k < c->Q; ++k) {
+    reconstruct(c, Nl, lam, k, Lk);
+    if (!orc_closure_du(c, Lk, J)) return 0;
+    for (int r = 0; r < m * m; ++r) Jbar[r] += c->omega[k] * J[r];
+  }
+  return 1;
+}
+
+int orc_lbfgs_direction(const orc_ctx *c, int Nl, const double *lam, const double *g, const double *S,
+                        const double *Y, int cnt, double *d) {
+  int m = c->m, n = Nl * m;
+  double *q = (double *)malloc(sizeof(double) * n);
+  double al[64], Jb[16];
+  for (int r = 0; r < n; ++r) q[r] = g[r];
+  /* first loop, newest pair first: alpha_i = rho_i s_i^T q, q -= alpha_i y_i */
+  for (int i = 0; i < cnt; ++i) {
+    const double *si = S + (size_t)i * n, *yi = Y + (size_t)i * n;
+    double sy = 0.0, sq = 0.0;
+    for (int r = 0; r < n; ++r) {
+      sy += si[r] * yi[r];
+      sq += si[r] * q[r];
+    }
+    al[i] = sq / sy;
+    for (int r = 0; r < n; ++r) q[r] -= al[i] * yi[r];
+  }
+  /* r = H0 q: solve Jbar r_i = q_i for every moment i (m x m Cholesky) */
+  int ok = orc_lbfgs_jbar(c, Nl, lam, Jb);
+  if (ok) {
+    double L[16] = {0};
+    for (int j = 0; j < m && ok; ++j) {
+      double t = Jb[j * m + j];
+      for (int k = 0; k < j; ++k) t -= L[j * m + k] * L[j * m + k];
+      if (!(t > 0.0) || !isfinite(t)) { ok = 0; break; }
+      L[j * m + j] = sqrt(t);
+      for (int i = j + 1; i < m; ++i) {
+        double v = Jb[i * m + j];
+        for (int k = 0; k < j; ++k) v -= L[i * m + k] * L[j * m + k];
+        L[i * m + j] = v / L[j * m + j];
+      }
+    }
+    for (int i = 0; i < Nl && ok; ++i) {
+      double *qi = q + i * m, y[4];
+      for (int a = 0; a < m; ++a) {
+        double v = qi[a];
+        for (int k = 0; k < a; ++k) v -= L[a * m + k] * y[k];
+        y[a] = v / L[a * m + a];
+      }
+      for (int a = m - 1; a >= 0; --a) {
+        double v = y[a];
+        for (int k = a + 1; k < m; ++k) v -= L[k * m + a] * qi[k];
+        qi[a] = v / L[a * m + a];
+      }
+    }
+  }
+  /* second loop, oldest pair first: beta = rho_i y_i^T r, r += s_i (alpha_i - beta) */
+  for (int i = cnt - 1; i >= 0 && ok; --i) {
+    const double *si = S + (size_t)i * n, *yi = Y + (size_t)i * n;
+    double sy = 0.0, yr = 0.0;
+    for (int r = 0; r < n; ++r) {
+      sy += si[r] * yi[r];
+      yr += yi[r] * q[r];
+    }
+    double be = yr / sy;
+    for (int r = 0; r < n; ++r) q[r] += si[r] * (al[i] - be);
+  }
+  for (int r = 0; r < n; ++r) d[r] = -q[r];
+  free(q);
+  return ok;
+}
+
+/* the pair (s, y) enters the history if s^T y > 1e-10 |s| |y| (curvature condition with a rounding
+ * margin; s^T y > 0 holds for every s != 0 in exact arithmetic because L is strictly convex); the
+ * oldest pair drops out when lbfgs_m pairs are stored */
+static void lbfgs_push(int mh, int n, double *S, double *Y, int32_t *cnt, const double *s, const double *y) {
+  double sy = 0.0, ss = 0.0, yy = 0.0;
+  for (int r = 0; r < n; ++r) {
+    sy += s[r] * y[r];
+    ss += s[r] * s[r];
+    yy += y[r] * y[r];
+  }
+  if (!(sy > 1e-10 * sqrt(ss * yy))) return;
+  int keep = *cnt < mh ? *cnt : mh - 1;
+  for (int i = keep; i > 0; --i) {
+    memcpy(S + (size_t)i * n, S + (size_t)(i - 1) * n, sizeof(double) * n);
+    memcpy(Y + (size_t)i * n, Y + (size_t)(i - 1) * n, sizeof(double) * n);
+  }
+  memcpy(S, s, sizeof(double) * n);
+  memcpy(Y, y, sizeof(double) * n);
+  *cnt = keep + 1;
+}
+
 /* Newton iteration lambda^{(l+1)} = d(lambda^{(l)}; uhat) until the stopping
  * criterion holds (FULL, Alg. 1 lines 7-10) or once (ONE_STEP, Alg. 2 line 5),
  * globalised by Armijo backtracking on the dual objective L with a rounding
  * allowance (reading 3'):  accept alpha if the trial is admissible and
- *     L(lambda + alpha d) <= L(lambda) + c alpha grad L . d + 1e-12 scale(L). */
-int orc_dual_solve_cell_ls(const orc_ctx *c, int Nl, int mode, const double *uhat, double *lam,
-                           int32_t *iters, double *crit_out, int32_t *halvings, int32_t *inadmissible) {
+ *     L(lambda + alpha d) <= L(lambda) + c alpha grad L . d + 1e-12 scale(L).
+ * With lb_S != NULL the direction is the L-BFGS one over the cell's history (reading 35) instead of
+ * the exact Newton direction -H^{-1} g; everything else is the same iteration. */
+static int dual_solve_cell_impl(const orc_ctx *c, int Nl, int mode, const double *uhat, double *lam,
+                                int32_t *iters, double *crit_out, int32_t *halvings, int32_t *inadmissible,
+                                double *lb_S, double *lb_Y, int32_t *lb_cnt, int32_t *lb_n) {
   const orc_problem *P = &c->P;
   int m = c->m, n = Nl * m;
   double *g = (double *)malloc(sizeof(double) * n);
+  double *g0 = (double *)malloc(sizeof(double) * n);
   double *dd = (double *)malloc(sizeof(double) * n);
   double *lt = (double *)malloc(sizeof(double) * n);
-  double *H = (double *)malloc(sizeof(double) * n * n);
+  double *H = lb_S ? NULL : (double *)malloc(sizeof(double) * n * n);
   int status = ORC_OK, l = 0, nhalv = 0, ninad = 0; /* rejected trials; inadmissible among them */
   double crit = INFINITY;
+  if (lb_S && *lb_n != n) { /* history of another basis size (level change): start afresh */
+    *lb_cnt = 0;
+    *lb_n = n;
+  }
   if (!orc_dual_gradient(c, Nl, lam, uhat, g)) {
     status = ORC_INADMISSIBLE;
     goto done;
@@ -877,14 +1000,29 @@ int orc_dual_solve_cell_ls(const orc_ctx *c, int Nl, int mode, const double *uha
       status = ORC_NONCONVERGENCE;
       break;
     }
-    if (!orc_dual_hessian(c, Nl, lam, H) || !cholesky_solve(H, n, g, dd)) {
-      status = ORC_ILLCONDITIONED;
-      break;
+    double slope = 0.0;
+    if (lb_S) {
+      if (!orc_lbfgs_direction(c, Nl, lam, g, lb_S, lb_Y, *lb_cnt, dd)) {
+        status = ORC_ILLCONDITIONED;
+        break;
+      }
+      for (int r = 0; r < n; ++r) slope += g[r] * dd[r];
+      if (!(slope < 0.0) && *lb_cnt > 0) { /* not a descent direction (rounding): drop the history */
+        *lb_cnt = 0;
+        orc_lbfgs_direction(c, Nl, lam, g, lb_S, lb_Y, 0, dd);
+        slope = 0.0;
+        for (int r = 0; r < n; ++r) slope += g[r] * dd[r];
+      }
+    } else {
+      if (!orc_dual_hessian(c, Nl, lam, H) || !cholesky_solve(H, n, g, dd)) {
+        status = ORC_ILLCONDITIONED;
+        break;
+      }
+      for (int r = 0; r < n; ++r) slope += g[r] * dd[r];
     }
     double L0, scale;
     objective_and_scale(c, Nl, lam, uhat, &L0, &scale);
-    double slope = 0.0;
-    for (int r = 0; r < n; ++r) slope += g[r] * dd[r];
+    memcpy(g0, g, sizeof(double) * n);
     double alpha = 1.0;
     int accepted = 0;
     for (int h = 0; h <= P->max_halvings; ++h) {
@@ -901,8 +1039,16 @@ int orc_dual_solve_cell_ls(const orc_ctx *c, int Nl, int mode, const double *uha
       alpha *= 0.5;
     }
     if (!accepted) {
+      memcpy(g, g0, sizeof(double) * n);
       status = ORC_LINESEARCH;
       break;
+    }
+    if (lb_S) { /* pair s = lt - lam, y = g - g0 */
+      for (int r = 0; r < n; ++r) {
+        dd[r] = lt[r] - lam[r];
+        g0[r] = g[r] - g0[r];
+      }
+      lbfgs_push(P->lbfgs_m, n, lb_S, lb_Y, lb_cnt, dd, g0);
     }
     memcpy(lam, lt, sizeof(double) * n);
     ++l;
@@ -912,8 +1058,29 @@ done:
   if (crit_out) *crit_out = crit;
   if (halvings) *halvings = nhalv;
   if (inadmissible) *inadmissible = ninad;
-  free(g); free(dd); free(lt); free(H);
+  free(g); free(g0); free(dd); free(lt); free(H);
   return status;
+}
+
+int orc_dual_solve_cell_ls(const orc_ctx *c, int Nl, int mode, const double *uhat, double *lam,
+                           int32_t *iters, double *crit_out, int32_t *halvings, int32_t *inadmissible) {
+  return dual_solve_cell_impl(c, Nl, mode, uhat, lam, iters, crit_out, halvings, inadmissible, NULL, NULL, NULL,
+                              NULL);
+}
+
+int orc_lbfgs_history(const orc_ctx *c, int j, double *S, double *Y) {
+  if (!c->lb_S) return 0;
+  size_t per = (size_t)c->P.lbfgs_m * c->N * c->m;
+  int cnt = c->lb_cnt[j], n = c->lb_n[j];
+  for (int i = 0; i < cnt; ++i) {
+    if (S) memcpy(S + (size_t)i * c->N * c->m, c->lb_S + j * per + (size_t)i * n, sizeof(double) * n);
+    if (Y) memcpy(Y + (size_t)i * c->N * c->m, c->lb_Y + j * per + (size_t)i * n, sizeof(double) * n);
+  }
+  return cnt;
+}
+
+void orc_lbfgs_reset(orc_ctx *c) {
+  if (c->lb_cnt) memset(c->lb_cnt, 0, sizeof(int32_t) * c->cells);
 }
 
 int orc_dual_solve_cell(const orc_ctx *c, int Nl, int mode, const double *uhat, double *lam,
@@ -1003,8 +1170,16 @@ void orc_dual_solve_all_ls(const orc_ctx *c, const double *uhat, double *lam, in
   for (int j = 0; j < c->cells; ++j) {
     int32_t it = 0, hv = 0, ia = 0;
     double cr = 0.0;
-    int st = orc_dual_solve_cell_ls(c, cell_N(c, j), c->P.newton_mode, uhat + (size_t)j * N * m,
-                                    lam + (size_t)j * N * m, &it, &cr, &hv, &ia);
+    int st;
+    if (c->lb_S) { /* L-BFGS with the cell's history (reading 35) */
+      size_t per = (size_t)c->P.lbfgs_m * N * m;
+      st = dual_solve_cell_impl(c, cell_N(c, j), c->P.newton_mode, uhat + (size_t)j * N * m, lam + (size_t)j * N * m,
+                                &it, &cr, &hv, &ia, ((orc_ctx *)c)->lb_S + j * per, ((orc_ctx *)c)->lb_Y + j * per,
+                                ((orc_ctx *)c)->lb_cnt + j, ((orc_ctx *)c)->lb_n + j);
+    } else {
+      st = orc_dual_solve_cell_ls(c, cell_N(c, j), c->P.newton_mode, uhat + (size_t)j * N * m,
+                                  lam + (size_t)j * N * m, &it, &cr, &hv, &ia);
+    }
     if (iters) iters[j] = it;
     if (status) status[j] = st;
     if (crit) crit[j] = cr;

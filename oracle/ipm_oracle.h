@@ -95,6 +95,10 @@ typedef struct {
    * dimension, 1 tensor Clenshaw-Curtis with q1d points, 2 Smolyak sparse grid of nested
    * Clenshaw-Curtis rules of level quad_level */
   int32_t quad_kind, quad_level;
+  /* dual-solve direction (reading 35): 0 exact Newton (the
+   * Hessian of PAPER.md:169), 1 limited-memory BFGS with the lbfgs_m most recent (s, y) pairs of
+   * every cell kept across (pseudo-)time steps and the initial matrix I (x) Jbar^{-1} */
+  int32_t hessian_kind, lbfgs_m;
 } orc_problem;
 
 typedef struct {
@@ -150,6 +154,15 @@ int orc_dual_solve_cell(const orc_ctx *c, int Nl, int mode, const double *uhat, 
                         int32_t *iters, double *crit);
 /* h(lambda) = <u_s(lambda^T phi) phi^T>_Q^T */
 int orc_moments_from_dual(const orc_ctx *c, int Nl, const double *lam, double *uhat);
+/* L-BFGS (reading 35): direction d = -H g of the two-loop recursion over cnt pairs (S, Y: [cnt][n],
+ * newest first) with H0 = I (x) Jbar(lam)^{-1}; returns 0 if Jbar is not SPD or lam inadmissible */
+int orc_lbfgs_direction(const orc_ctx *c, int Nl, const double *lam, const double *g, const double *S,
+                        const double *Y, int cnt, double *d);
+/* Jbar(lam) = sum_k omega_k grad u_s(lam^T phi(xi_k))  [m][m] */
+int orc_lbfgs_jbar(const orc_ctx *c, int Nl, const double *lam, double *Jbar);
+/* history of cell j: pairs (newest first) into S, Y [lbfgs_m][N m] (nullable); returns the count */
+int orc_lbfgs_history(const orc_ctx *c, int j, double *S, double *Y);
+void orc_lbfgs_reset(orc_ctx *c);
 
 /* two-point flux at one node; dx_over_dt for global LF */
 void orc_flux_g(const orc_ctx *c, const double *ul, const double *ur, const double *n,

@@ -64,6 +64,7 @@ class Problem(C.Structure):
         ("n_threads", C.c_int32),
         ("n_retard", C.c_int32), ("retard_level", C.c_int32 * 8), ("retard_eps", C.c_double * 8),
         ("quad_kind", C.c_int32), ("quad_level", C.c_int32),
+        ("hessian_kind", C.c_int32), ("lbfgs_m", C.c_int32),
     ]
 
 
@@ -106,6 +107,10 @@ def lib():
             "orc_set_levels": (None, [P, I]), "orc_get_levels": (None, [P, I]),
             "orc_retard_stage": (C.c_int, [P]),
             "orc_problem_size": (C.c_size_t, []),
+            "orc_lbfgs_direction": (C.c_int, [P, C.c_int, D, D, D, D, C.c_int, D]),
+            "orc_lbfgs_jbar": (C.c_int, [P, C.c_int, D, D]),
+            "orc_lbfgs_history": (C.c_int, [P, C.c_int, C.c_void_p, C.c_void_p]),
+            "orc_lbfgs_reset": (None, [P]),
             "orc_sc_init": (None, [P, C.POINTER(ICSpec), D]),
             "orc_sc_step": (C.c_double, [P, D, D, C.c_double, D]),
             "orc_sc_moments": (None, [P, D, D]),
@@ -221,6 +226,9 @@ class Oracle:
         # "smolyak" sparse grid of nested Clenshaw-Curtis rules of level quad_level
         P.quad_kind = {"gl": 0, "cc": 1, "smolyak": 2}[cfg.get("quad", "gl")]
         P.quad_level = cfg.get("quad_level", 0)
+        # dual-solve direction (reading 35): "newton" exact Hessian, "lbfgs" limited-memory BFGS
+        P.hessian_kind = {"newton": 0, "lbfgs": 1}[cfg.get("hessian", "newton")]
+        P.lbfgs_m = cfg.get("lbfgs_m", 8)
         # refinement retardation (Alg. 4): [(eps_l, level index cap l*_l), ...]
         retard = cfg.get("retard") or []
         P.n_retard = len(retard)
@@ -310,6 +318,33 @@ class Oracle:
         it, crit = C.c_int32(), C.c_double()
         st = lib().orc_dual_solve_cell(self.ctx, Nl, NEWTON[mode], _d(uhat), _d(lam), C.byref(it), C.byref(crit))
         return lam, int(it.value), float(crit.value), int(st)
+
+    # --- L-BFGS dual solve (reading 35, NEXT-4) ---------------------------
+    def lbfgs_jbar(self, lam, Nl=None):
+        Nl = Nl or self.N
+        J = np.zeros((self.m, self.m))
+        ok = lib().orc_lbfgs_jbar(self.ctx, Nl, _d(np.ascontiguousarray(lam, np.float64)), _d(J))
+        return J, bool(ok)
+
+    def lbfgs_direction(self, lam, g, S, Y, Nl=None):
+        """two-loop direction -H g over the pairs S, Y [cnt][n] (newest first)"""
+        Nl = Nl or self.N
+        n = Nl * self.m
+        S = np.ascontiguousarray(S, np.float64).reshape(-1, n)
+        Y = np.ascontiguousarray(Y, np.float64).reshape(-1, n)
+        d = np.zeros(n)
+        ok = lib().orc_lbfgs_direction(self.ctx, Nl, _d(np.ascontiguousarray(lam, np.float64)),
+                                       _d(np.ascontiguousarray(g, np.float64)), _d(S), _d(Y), S.shape[0], _d(d))
+        return d, bool(ok)
+
+    def lbfgs_history(self, j):
+        mh, n = self._P.lbfgs_m, self.N * self.m
+        S, Y = np.zeros((mh, n)), np.zeros((mh, n))
+        cnt = lib().orc_lbfgs_history(self.ctx, j, S.ctypes.data, Y.ctypes.data)
+        return S[:cnt], Y[:cnt]
+
+    def lbfgs_reset(self):
+        lib().orc_lbfgs_reset(self.ctx)
 
     def moments_from_dual(self, lam, Nl=None):
         Nl = Nl or self.N

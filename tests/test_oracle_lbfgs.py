@@ -1,0 +1,184 @@
+"""Oracle pins: the quasi-Newton (L-BFGS) dual solve (reading 35).
+
+What fixes it, independently of the oracle's own code:
+  * the two-loop direction equals the explicit BFGS inverse-Hessian recursion written as matrices
+    (Nocedal & Wright eq. 6.17: H+ = (I - rho s y^T) H (I - rho y s^T) + rho s s^T, applied oldest to
+    newest to H0) — a different computation of the same definition;
+  * the secant equation H_l y_newest = s_newest;
+  * H0 = I (x) Jbar^{-1} with Jbar the top-left m x m block of the exact Hessian (phi_0 = 1), and
+    H0^{-1} equals the whole exact Hessian for xi-independent duals (Gram = I);
+  * quadratic entropy: Jbar = I = H, so one step gives lambda = uhat (stochastic Galerkin);
+  * L is strictly convex, so the L-BFGS solve reaches the Newton solve's unique minimiser;
+  * the history persists across calls (gradients of old time steps kept per cell).
+"""
+import numpy as np
+import pytest
+
+from inputs import configs
+from inputs.generators import STRESS_AMP, cell_centres, stress_state
+
+
+def _cfg3(oracle_mod, hessian="lbfgs", nx=4, ny=3):
+    cfg = configs.get("cfg3", mesh=dict(nx=nx, ny=ny), hessian=hessian)
+    return oracle_mod.Oracle(cfg), cfg
+
+
+def _stress(o, cfg, seed=1):
+    base, z = stress_state("euler2d", cell_centres(cfg["mesh"]), o.N, o.m, seed=seed)
+    return o.stress_dual(base, z, STRESS_AMP["euler2d"])
+
+
+def _bfgs_matrix(H0, S, Y):
+    """explicit BFGS inverse update (N&W eq. 6.17), pairs given newest first, applied oldest first"""
+    H = H0.copy()
+    n = H.shape[0]
+    for s, y in zip(S[::-1], Y[::-1]):
+        rho = 1.0 / (y @ s)
+        V = np.eye(n) - rho * np.outer(y, s)
+        H = V.T @ H @ V + rho * np.outer(s, s)
+    return H
+
+
+def _pairs(o, lam, rng, cnt):
+    """pairs with s^T y > 0: y = H(lam + t s) s-like secant pairs from the exact Hessian"""
+    H, ok = o.dual_hessian(lam)
+    assert ok
+    n = H.shape[0]
+    S = rng.standard_normal((cnt, n)) * 1e-2
+    Y = np.stack([H @ s + 1e-3 * np.abs(rng.standard_normal()) * s for s in S])
+    return S, Y, H
+
+
+def test_jbar_is_the_hessian_corner_block(oracle_mod):
+    o, cfg = _cfg3(oracle_mod)
+    lam = _stress(o, cfg)[0]
+    J, ok = o.lbfgs_jbar(lam)
+    H, _ = o.dual_hessian(lam)
+    assert ok
+    np.testing.assert_allclose(J, H[: o.m, : o.m], rtol=1e-13, atol=1e-15)
+    # xi-independent duals: the exact Hessian is I_N (x) Jbar (Gram = I), i.e. H0 is exact
+    lam0 = np.zeros_like(lam)
+    lam0[0] = lam[0]
+    J0, _ = o.lbfgs_jbar(lam0)
+    H0, _ = o.dual_hessian(lam0)
+    np.testing.assert_allclose(H0, np.kron(np.eye(o.N), J0), rtol=1e-12, atol=1e-12 * np.abs(J0).max())
+
+
+@pytest.mark.parametrize("cnt", [0, 1, 3, 8])
+def test_two_loop_equals_bfgs_matrix_recursion(oracle_mod, cnt):
+    o, cfg = _cfg3(oracle_mod)
+    rng = np.random.default_rng(cnt)
+    lam = _stress(o, cfg)[0]
+    S, Y, H = _pairs(o, lam, rng, cnt) if cnt else (np.zeros((0, o.N * o.m)), np.zeros((0, o.N * o.m)), None)
+    Hx, _ = o.dual_hessian(lam)
+    H0 = np.kron(np.eye(o.N), np.linalg.inv(Hx[: o.m, : o.m]))
+    g = rng.standard_normal(o.N * o.m)
+    d, ok = o.lbfgs_direction(lam, g, S, Y)
+    assert ok
+    ref = -_bfgs_matrix(H0, S, Y) @ g
+    np.testing.assert_allclose(d, ref, rtol=1e-9, atol=1e-9 * np.abs(ref).max())
+
+
+def test_secant_equation(oracle_mod):
+    o, cfg = _cfg3(oracle_mod)
+    rng = np.random.default_rng(7)
+    lam = _stress(o, cfg)[0]
+    S, Y, _ = _pairs(o, lam, rng, 5)
+    d, ok = o.lbfgs_direction(lam, Y[0], S, Y)  # d = -H y_newest = -s_newest
+    assert ok
+    np.testing.assert_allclose(d, -S[0], rtol=1e-9, atol=1e-9 * np.abs(S[0]).max())
+
+
+def test_quadratic_entropy_one_step_is_stochastic_galerkin(oracle_mod):
+    # s = u^2/2: Jbar = I = H, so the first L-BFGS direction is the Newton step and lambda = uhat
+    cfg = configs.get("cfg1", mesh=dict(nx=6), closure="quadratic", flux="lf_global", hessian="lbfgs")
+    o = oracle_mod.Oracle(cfg)
+    rng = np.random.default_rng(0)
+    uhat = rng.standard_normal((o.cells, o.N, 1))
+    lam = np.zeros_like(uhat)
+    it, st, crit = o.dual_solve_all(uhat, lam)
+    assert (st == 0).all() and (it == 1).all() and (crit < 1e-10).all()
+    np.testing.assert_allclose(lam, uhat, atol=1e-13)
+
+
+def test_xi_constant_cell_needs_no_iteration(oracle_mod):
+    o, cfg = _cfg3(oracle_mod)
+    lam = _stress(o, cfg)
+    lam[:, 1:] = 0.0
+    uhat = o.moments_from_dual_all(lam)
+    lam0 = o.warm_start(uhat)
+    it, st, crit = o.dual_solve_all(uhat, lam0)
+    assert (st == 0).all() and (it == 0).all()
+
+
+def test_lbfgs_reaches_the_newton_minimiser(oracle_mod):
+    # L is strictly convex: both iterations stop at ||grad L|| < tau near the same unique minimiser
+    o, cfg = _cfg3(oracle_mod)
+    on, _ = _cfg3(oracle_mod, "newton")
+    lam_s = _stress(o, cfg)
+    uhat = o.moments_from_dual_all(lam_s)
+    l_b, l_n = o.warm_start(uhat), on.warm_start(uhat)
+    it_b, st_b, cr_b = o.dual_solve_all(uhat, l_b)
+    it_n, st_n, cr_n = on.dual_solve_all(uhat, l_n)
+    assert (st_b == 0).all() and (st_n == 0).all() and (cr_b < 1e-10).all()
+    scale = np.abs(lam_s).max(axis=(0, 1))
+    assert (np.abs(l_b - lam_s).max(axis=(0, 1)) / scale).max() < 1e-8
+    assert (np.abs(l_b - l_n).max(axis=(0, 1)) / scale).max() < 1e-8
+    # more, cheaper iterations than Newton, far from the iteration cap
+    assert it_b.mean() > it_n.mean() and it_b.max() < 60
+
+
+def test_history_persists_and_resets(oracle_mod):
+    o, cfg = _cfg3(oracle_mod)
+    lam_s = _stress(o, cfg)
+    uhat = o.moments_from_dual_all(lam_s)
+    lam = o.warm_start(uhat)
+    lam_prev = lam.copy()
+    it, st, _ = o.dual_solve_all(uhat, lam)
+    n = o.N * o.m
+    for j in range(o.cells):
+        S, Y = o.lbfgs_history(j)
+        assert len(S) == min(8, it[j])  # every accepted step of these solves passes the curvature test
+        assert (np.einsum("ij,ij->i", S[:, :n], Y[:, :n]) > 0).all()
+        # the newest pair is the last accepted step
+        assert np.abs(S[0]).max() > 0
+    # pairs telescope: with fewer than 8 steps their sum is lambda_final - lambda_start
+    j = int(np.argmin(it))
+    if it[j] <= 8:
+        S, _ = o.lbfgs_history(j)
+        np.testing.assert_allclose(S.sum(axis=0), (lam[j] - lam_prev[j]).ravel(), atol=1e-12)
+    # a second solve of the converged problem takes no step and keeps the history
+    it2, st2, _ = o.dual_solve_all(uhat, lam)
+    assert (it2 == 0).all() and len(o.lbfgs_history(0)[0]) == min(8, it[0])
+    o.lbfgs_reset()
+    assert len(o.lbfgs_history(0)[0]) == 0
+
+
+def test_history_speeds_up_the_next_time_step(oracle_mod):
+    # curvature pairs of old time steps reduce the work of the next dual solves
+    o, cfg = _cfg3(oracle_mod)
+    lam_s = _stress(o, cfg)
+    u = o.moments_from_dual_all(lam_s)
+    lam = o.warm_start(u)
+    its = []
+    for _ in range(3):
+        w, it, st, dt, res = o.step(u, lam)
+        assert w == 0
+        its.append(it.mean())
+    u2, lam2 = u.copy(), lam.copy()
+    w, it_warm, _, _, _ = o.step(u, lam)
+    o.lbfgs_reset()
+    w, it_cold, _, _, _ = o.step(u2, lam2)
+    assert it_warm.mean() < it_cold.mean()
+    np.testing.assert_allclose(u, u2, rtol=0, atol=1e-9 * np.abs(u2[:, 0]).max())
+
+
+def test_lbfgs_run_matches_newton_run(oracle_mod):
+    # config 1 to t = 0.02: both dual iterations converge to tau, the moment trajectories agree
+    cb = configs.get("cfg1", hessian="lbfgs")
+    cn = configs.get("cfg1")
+    ob, on = oracle_mod.Oracle(cb), oracle_mod.Oracle(cn)
+    ub, _, ib = ob.run(t_end=0.02, record=True)
+    un, _, inn = on.run(t_end=0.02, record=True)
+    assert ib["steps"] == inn["steps"]
+    np.testing.assert_allclose(ub, un, rtol=0, atol=1e-8 * np.abs(un[:, 0]).max())
