@@ -43,7 +43,33 @@ struct orc_ctx {
   double *lb_S, *lb_Y; /* [cells][lbfgs_m][N m] */
   int32_t *lb_cnt;     /* [cells] stored pairs */
   int32_t *lb_n;       /* [cells] unknowns n the pairs belong to (a level change clears them) */
+  /* per-level nested rules (reading 36): level l uses the nodes lkf[l][0..lQ[l]) of the finest rule
+   * (c->xi, c->Phi) with its own weights lw[l] */
+  int lq_on;
+  int lQ[8];
+  int32_t *lkf[8];
+  double *lw[8];
 };
+
+/* the quadrature rule of a cell with basis size Nl: node q is node kf[q] of the finest rule (c->xi,
+ * c->Phi), weight w[q] (H_l, grad at level l use Q_l) */
+typedef struct {
+  int Q;
+  const int32_t *kf;
+  const double *w;
+} orc_rule;
+static orc_rule rule_of(const orc_ctx *c, int Nl) {
+  orc_rule R = {c->Q, NULL, c->omega};
+  if (c->lq_on)
+    for (int l = 0; l < c->n_levels; ++l)
+      if (c->Nl[l] == Nl) {
+        R.Q = c->lQ[l];
+        R.kf = c->lkf[l];
+        R.w = c->lw[l];
+      }
+  return R;
+}
+#define RK(R, q) ((R).kf ? (R).kf[q] : (q))
 
 /* ------------------------------------------------------------------------ */
 /* Random space: Legendre polynomials, Gauss-Legendre rule, total-degree basis */
@@ -683,6 +709,44 @@ orc_ctx *orc_create(const orc_problem *P) {
   } else {
     c->Nl[0] = N;
   }
+  /* per-level nested Clenshaw-Curtis rules (reading 36): level l's 1D points are every
+   * (n_f - 1)/(n_l - 1)-th point of the finest rule (n = 2^k + 1 nest), tensor index last dimension
+   * fastest, weights prod_d w_l[j_d] / 2 */
+  if (c->n_levels > 0 && P->level_q1d[0] > 0) {
+    int nf = P->level_q1d[c->n_levels - 1];
+    int okq = (P->quad_kind == 1 && P->q1d == nf);
+    for (int l = 0; l < c->n_levels && okq; ++l) {
+      int nl = P->level_q1d[l];
+      okq = nl >= 2 && nl <= nf && (nf - 1) % (nl - 1) == 0 && (l == 0 || nl >= P->level_q1d[l - 1]);
+    }
+    if (!okq) {
+      orc_destroy(c);
+      return NULL;
+    }
+    c->lq_on = 1;
+    for (int l = 0; l < c->n_levels; ++l) {
+      int nl = P->level_q1d[l], stride = (nf - 1) / (nl - 1), Ql = 1;
+      double xl[129], wl[129];
+      orc_clenshaw_curtis(nl, xl, wl);
+      for (int d = 0; d < p; ++d) Ql *= nl;
+      c->lQ[l] = Ql;
+      c->lkf[l] = (int32_t *)malloc(sizeof(int32_t) * Ql);
+      c->lw[l] = (double *)malloc(sizeof(double) * Ql);
+      for (int q = 0; q < Ql; ++q) {
+        int r = q, kf = 0, scale = 1;
+        double w = 1.0;
+        for (int d = p - 1; d >= 0; --d) {
+          int jd = r % nl;
+          r /= nl;
+          kf += jd * stride * scale;
+          scale *= nf;
+          w *= wl[jd] / 2.0;
+        }
+        c->lkf[l][q] = kf;
+        c->lw[l][q] = w;
+      }
+    }
+  }
   if (P->hessian_kind == 1) {
     size_t per = (size_t)P->lbfgs_m * N * c->m;
     c->lb_S = (double *)calloc((size_t)c->cells * per, sizeof(double));
@@ -700,6 +764,10 @@ void orc_destroy(orc_ctx *c) {
   if (!c) return;
   free(c->idx); free(c->xi); free(c->omega); free(c->Phi);
   free(c->lb_S); free(c->lb_Y); free(c->lb_cnt); free(c->lb_n);
+  for (int l = 0; l < 8; ++l) {
+    free(c->lkf[l]);
+    free(c->lw[l]);
+  }
   free(c->nbr); free(c->nrm); free(c->coef); free(c->area); free(c->perim); free(c->xc);
   free(c->bc_u); free(c->level);
   free(c);
@@ -743,9 +811,10 @@ static void reconstruct(const orc_ctx *c, int Nl, const double *lam, int k, doub
 int orc_dual_objective(const orc_ctx *c, int Nl, const double *lam, const double *uhat, double *L) {
   int m = c->m;
   double Lk[4], s = 0.0;
-  for (int k = 0; k < c->Q; ++k) {
-    reconstruct(c, Nl, lam, k, Lk);
-    s += c->omega[k] * orc_closure_sstar(c, Lk);
+  orc_rule R = rule_of(c, Nl);
+  for (int q = 0; q < R.Q; ++q) {
+    reconstruct(c, Nl, lam, RK(R, q), Lk);
+    s += R.w[q] * orc_closure_sstar(c, Lk);
   }
   for (int i = 0; i < Nl; ++i)
     for (int a = 0; a < m; ++a) s -= lam[i * m + a] * uhat[i * m + a];
@@ -759,11 +828,13 @@ int orc_dual_gradient(const orc_ctx *c, int Nl, const double *lam, const double 
   double Lk[4], uk[4];
   for (int i = 0; i < Nl; ++i)
     for (int a = 0; a < m; ++a) g[i * m + a] = 0.0;
-  for (int k = 0; k < c->Q; ++k) {
+  orc_rule R = rule_of(c, Nl);
+  for (int q = 0; q < R.Q; ++q) {
+    int k = RK(R, q);
     reconstruct(c, Nl, lam, k, Lk);
     if (!orc_closure_u(c, Lk, uk)) return 0;
     for (int i = 0; i < Nl; ++i)
-      for (int a = 0; a < m; ++a) g[i * m + a] += c->omega[k] * uk[a] * c->Phi[k * N + i];
+      for (int a = 0; a < m; ++a) g[i * m + a] += R.w[q] * uk[a] * c->Phi[k * N + i];
   }
   int ok = 1;
   for (int i = 0; i < Nl; ++i)
@@ -788,14 +859,16 @@ int orc_dual_hessian(const orc_ctx *c, int Nl, const double *lam, double *H) {
   int m = c->m, N = c->N, n = Nl * m;
   double Lk[4], J[16];
   for (int r = 0; r < n * n; ++r) H[r] = 0.0;
-  for (int k = 0; k < c->Q; ++k) {
+  orc_rule R = rule_of(c, Nl);
+  for (int q = 0; q < R.Q; ++q) {
+    int k = RK(R, q);
     reconstruct(c, Nl, lam, k, Lk);
     if (!orc_closure_du(c, Lk, J)) return 0;
     for (int i = 0; i < Nl; ++i)
       for (int a = 0; a < m; ++a)
         for (int j = 0; j < Nl; ++j)
           for (int b = 0; b < m; ++b)
-            H[(i * m + a) * n + (j * m + b)] += c->omega[k] * J[a * m + b] * c->Phi[k * N + i] * c->Phi[k * N + j];
+            H[(i * m + a) * n + (j * m + b)] += R.w[q] * J[a * m + b] * c->Phi[k * N + i] * c->Phi[k * N + j];
   }
   return 1;
 }
@@ -846,11 +919,12 @@ static int objective_and_scale(const orc_ctx *c, int Nl, const double *lam, cons
                                double *L, double *scale) {
   int m = c->m;
   double Lk[4], s = 0.0, sc = 0.0;
-  for (int k = 0; k < c->Q; ++k) {
-    reconstruct(c, Nl, lam, k, Lk);
+  orc_rule R = rule_of(c, Nl);
+  for (int q = 0; q < R.Q; ++q) {
+    reconstruct(c, Nl, lam, RK(R, q), Lk);
     double sk = orc_closure_sstar(c, Lk);
-    s += c->omega[k] * sk;
-    sc += c->omega[k] * fabs(sk);
+    s += R.w[q] * sk;
+    sc += R.w[q] * fabs(sk);
   }
   for (int i = 0; i < Nl; ++i)
     for (int a = 0; a < m; ++a) {
@@ -874,10 +948,11 @@ int orc_lbfgs_jbar(const orc_ctx *c, int Nl, const double *lam, double *Jbar) {
   int m = c->m;
   double Lk[4], J[16];
   for (int r = 0; r < m * m; ++r) Jbar[r] = 0.0;
-  for (int k = 0; k < c->Q; ++k) {
-    reconstruct(c, Nl, lam, k, Lk);
+  orc_rule R = rule_of(c, Nl);
+  for (int q = 0; q < R.Q; ++q) {
+    reconstruct(c, Nl, lam, RK(R, q), Lk);
     if (!orc_closure_du(c, Lk, J)) return 0;
-    for (int r = 0; r < m * m; ++r) Jbar[r] += c->omega[k] * J[r];
+    for (int r = 0; r < m * m; ++r) Jbar[r] += R.w[q] * J[r];
   }
   return 1;
 }
@@ -1079,6 +1154,19 @@ int orc_lbfgs_history(const orc_ctx *c, int j, double *S, double *Y) {
   return cnt;
 }
 
+int orc_level_rule(const orc_ctx *c, int l, int32_t *kf, double *w) {
+  if (!c->lq_on || l < 0 || l >= c->n_levels) {
+    for (int k = 0; k < c->Q; ++k) {
+      if (kf) kf[k] = k;
+      if (w) w[k] = c->omega[k];
+    }
+    return c->Q;
+  }
+  if (kf) memcpy(kf, c->lkf[l], sizeof(int32_t) * c->lQ[l]);
+  if (w) memcpy(w, c->lw[l], sizeof(double) * c->lQ[l]);
+  return c->lQ[l];
+}
+
 void orc_lbfgs_reset(orc_ctx *c) {
   if (c->lb_cnt) memset(c->lb_cnt, 0, sizeof(int32_t) * c->cells);
 }
@@ -1132,17 +1220,19 @@ static void ic_node_state(const orc_ctx *c, const orc_ic *ic, int j, int k, doub
 /* u_j^0 = (1/|Omega_j|) int <u_IC phi>_Q dx with exact cell averages of the piecewise-constant IC
  * at every node (Alg. 1 line 2; reading 17). */
 void orc_project_ic(const orc_ctx *c, const orc_ic *ic, double *uhat) {
-  int N = c->N, Q = c->Q, m = c->m;
+  int N = c->N, m = c->m;
 #pragma omp parallel for schedule(static)
   for (int j = 0; j < c->cells; ++j) {
     int Nl = cell_N(c, j);
+    orc_rule R = rule_of(c, Nl); /* Alg. 3 line 3: <u_IC phi_l>_{Q_l} at the initial level */
     double *uj = uhat + (size_t)j * N * m;
     for (int r = 0; r < N * m; ++r) uj[r] = 0.0;
-    for (int k = 0; k < Q; ++k) {
+    for (int q = 0; q < R.Q; ++q) {
+      int k = RK(R, q);
       double ub[4];
       ic_node_state(c, ic, j, k, ub);
       for (int i = 0; i < Nl; ++i)
-        for (int a = 0; a < m; ++a) uj[i * m + a] += c->omega[k] * ub[a] * c->Phi[k * N + i];
+        for (int a = 0; a < m; ++a) uj[i * m + a] += R.w[q] * ub[a] * c->Phi[k * N + i];
     }
   }
 }
@@ -1209,41 +1299,50 @@ static int node_states(const orc_ctx *c, const double *lam, double *U) {
 
 /* CFL rate of cell j: largest wave speed over its nodes and the ghost states of its boundary faces,
  * times the mesh factor (reading 15). */
+static double state_rate(const orc_ctx *c, const double *u, int j) {
+  const orc_problem *P = &c->P;
+  if (P->mesh_kind == ORC_MESH_1D) {
+    double n1[2] = {1.0, 0.0};
+    return wave_speed(c, u, n1) * c->coef[j * 2];
+  }
+  if (P->mesh_kind == ORC_MESH_CART2D) {
+    double nx[2] = {1.0, 0.0}, ny[2] = {0.0, 1.0};
+    return wave_speed(c, u, nx) * c->coef[j * 4 + 0] + wave_speed(c, u, ny) * c->coef[j * 4 + 2];
+  }
+  return speed_norm(c, u) * c->perim[j] / c->area[j];
+}
+
+/* CFL rate of cell j: largest wave speed over its nodes (those of its current level's rule, reading
+ * 36) and the ghost states of its boundary faces, times the mesh factor (reading 15); with per-level
+ * rules prescribed (STATE) ghost states enter at every node of the finest rule. */
 static double cell_rate(const orc_ctx *c, const double *U, int j) {
   const orc_problem *P = &c->P;
   int Q = c->Q, m = c->m, F = c->F;
   double rate = 0.0;
-  for (int k = 0; k < Q; ++k) {
+  orc_rule R = rule_of(c, cell_N(c, j));
+  for (int q = 0; q < R.Q; ++q) {
+    int k = RK(R, q);
     const double *u = U + ((size_t)j * Q + k) * m;
-    double r;
-    if (P->mesh_kind == ORC_MESH_1D) {
-      double n1[2] = {1.0, 0.0};
-      r = wave_speed(c, u, n1) * c->coef[j * 2];
-    } else if (P->mesh_kind == ORC_MESH_CART2D) {
-      double nx[2] = {1.0, 0.0}, ny[2] = {0.0, 1.0};
-      r = wave_speed(c, u, nx) * c->coef[j * 4 + 0] + wave_speed(c, u, ny) * c->coef[j * 4 + 2];
-    } else {
-      r = speed_norm(c, u) * c->perim[j] / c->area[j];
-    }
+    double r = state_rate(c, u, j);
     if (r > rate) rate = r;
     for (int f = 0; f < F; ++f) {
       int nb = c->nbr[j * F + f];
       if (nb >= 0) continue;
       double ug[4];
       ghost_state(c, -1 - nb, k, u, c->nrm + (j * F + f) * 2, ug);
-      double rg;
-      if (P->mesh_kind == ORC_MESH_1D) {
-        double n1[2] = {1.0, 0.0};
-        rg = wave_speed(c, ug, n1) * c->coef[j * 2];
-      } else if (P->mesh_kind == ORC_MESH_CART2D) {
-        double nx[2] = {1.0, 0.0}, ny[2] = {0.0, 1.0};
-        rg = wave_speed(c, ug, nx) * c->coef[j * 4 + 0] + wave_speed(c, ug, ny) * c->coef[j * 4 + 2];
-      } else {
-        rg = speed_norm(c, ug) * c->perim[j] / c->area[j];
-      }
+      double rg = state_rate(c, ug, j);
       if (rg > rate) rate = rg;
     }
   }
+  if (c->lq_on)
+    for (int f = 0; f < F; ++f) {
+      int nb = c->nbr[j * F + f];
+      if (nb >= 0 || P->bc_kind[-1 - nb] != ORC_BC_STATE) continue;
+      for (int k = 0; k < Q; ++k) {
+        double rg = state_rate(c, c->bc_u + ((size_t)(-1 - nb) * Q + k) * m, j);
+        if (rg > rate) rate = rg;
+      }
+    }
   return rate;
 }
 
@@ -1327,16 +1426,22 @@ static void flux_update_states(const orc_ctx *c, const double *U, const int32_t 
     const double *uo = uhat_old + (size_t)j * N * m;
     double acc[224 * 4];
     for (int r = 0; r < N * m; ++r) acc[r] = 0.0;
-    for (int k = 0; k < Q; ++k) {
+    /* eq. (adaptiveFVUpdate): the update at level l^{n+1} integrates with Q_{l^{n+1}};
+     * the stencil's states at those nodes come from their duals at the old levels (U holds every cell
+     * at every node of the finest rule: the neighbours "evaluated at the finer quadrature level",
+     * PAPER.md:398) */
+    orc_rule R = rule_of(c, Nnew);
+    for (int q = 0; q < R.Q; ++q) {
+      int k = RK(R, q);
       const double *uj = U + ((size_t)j * Q + k) * m;
       double r[4];
       node_residual(c, U, j, k, dx_over_dt, r);
       for (int i = 0; i < Nnew; ++i)
         for (int a = 0; a < m; ++a) {
           if (P->update_form == ORC_UPDATE_PAPER_C)
-            acc[i * m + a] += c->omega[k] * (uj[a] - dt * r[a]) * c->Phi[k * N + i];
+            acc[i * m + a] += R.w[q] * (uj[a] - dt * r[a]) * c->Phi[k * N + i];
           else
-            acc[i * m + a] += c->omega[k] * r[a] * c->Phi[k * N + i];
+            acc[i * m + a] += R.w[q] * r[a] * c->Phi[k * N + i];
         }
     }
     for (int i = 0; i < N; ++i)

@@ -99,6 +99,10 @@ typedef struct {
    * Hessian of PAPER.md:169), 1 limited-memory BFGS with the lbfgs_m most recent (s, y) pairs of
    * every cell kept across (pseudo-)time steps and the initial matrix I (x) Jbar^{-1} */
   int32_t hessian_kind, lbfgs_m;
+  /* per-level nested quadrature (reading 36): level_q1d[l] > 0
+   * gives level l its own tensor Clenshaw-Curtis rule of level_q1d[l] = 2^k + 1 points per dimension,
+   * nested in the finest one (quad_kind 1, q1d = level_q1d[n_levels-1]); 0 = one rule for all levels */
+  int32_t level_q1d[8];
 } orc_problem;
 
 typedef struct {
@@ -163,6 +167,9 @@ int orc_lbfgs_jbar(const orc_ctx *c, int Nl, const double *lam, double *Jbar);
 /* history of cell j: pairs (newest first) into S, Y [lbfgs_m][N m] (nullable); returns the count */
 int orc_lbfgs_history(const orc_ctx *c, int j, double *S, double *Y);
 void orc_lbfgs_reset(orc_ctx *c);
+/* per-level nested rule of level l (reading 36): its node indices into the finest rule kf [Q_l] and
+ * weights w [Q_l] (nullable); returns Q_l (the whole rule when per-level rules are off) */
+int orc_level_rule(const orc_ctx *c, int l, int32_t *kf, double *w);
 
 /* two-point flux at one node; dx_over_dt for global LF */
 void orc_flux_g(const orc_ctx *c, const double *ul, const double *ur, const double *n,

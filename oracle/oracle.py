@@ -65,6 +65,7 @@ class Problem(C.Structure):
         ("n_retard", C.c_int32), ("retard_level", C.c_int32 * 8), ("retard_eps", C.c_double * 8),
         ("quad_kind", C.c_int32), ("quad_level", C.c_int32),
         ("hessian_kind", C.c_int32), ("lbfgs_m", C.c_int32),
+        ("level_q1d", C.c_int32 * 8),
     ]
 
 
@@ -111,6 +112,7 @@ def lib():
             "orc_lbfgs_jbar": (C.c_int, [P, C.c_int, D, D]),
             "orc_lbfgs_history": (C.c_int, [P, C.c_int, C.c_void_p, C.c_void_p]),
             "orc_lbfgs_reset": (None, [P]),
+            "orc_level_rule": (C.c_int, [P, C.c_int, C.c_void_p, C.c_void_p]),
             "orc_sc_init": (None, [P, C.POINTER(ICSpec), D]),
             "orc_sc_step": (C.c_double, [P, D, D, C.c_double, D]),
             "orc_sc_moments": (None, [P, D, D]),
@@ -229,6 +231,9 @@ class Oracle:
         # dual-solve direction (reading 35): "newton" exact Hessian, "lbfgs" limited-memory BFGS
         P.hessian_kind = {"newton": 0, "lbfgs": 1}[cfg.get("hessian", "newton")]
         P.lbfgs_m = cfg.get("lbfgs_m", 8)
+        # per-level nested Clenshaw-Curtis rules (reading 36): points per dimension of every level
+        for k, q in enumerate(cfg.get("level_q1d") or []):
+            P.level_q1d[k] = q
         # refinement retardation (Alg. 4): [(eps_l, level index cap l*_l), ...]
         retard = cfg.get("retard") or []
         P.n_retard = len(retard)
@@ -236,6 +241,8 @@ class Oracle:
             P.retard_eps[k], P.retard_level[k] = eps, lv
         self._P = P
         self.ctx = L.orc_create(C.byref(P))
+        if not self.ctx:
+            raise ValueError("orc_create rejected the problem (per-level rules need nested tensor CC)")
         self.N, self.Q, self.cells, self.m = L.orc_N(self.ctx), L.orc_Q(self.ctx), L.orc_cells(self.ctx), cfg["m"]
         self.p = cfg["p"]
         if levels:
@@ -342,6 +349,13 @@ class Oracle:
         S, Y = np.zeros((mh, n)), np.zeros((mh, n))
         cnt = lib().orc_lbfgs_history(self.ctx, j, S.ctypes.data, Y.ctypes.data)
         return S[:cnt], Y[:cnt]
+
+    def level_rule(self, lvl):
+        """(finest-rule node indices, weights) of level lvl's nested rule (reading 36)"""
+        Ql = lib().orc_level_rule(self.ctx, lvl, None, None)
+        kf, w = np.zeros(Ql, np.int32), np.zeros(Ql)
+        lib().orc_level_rule(self.ctx, lvl, kf.ctypes.data, w.ctypes.data)
+        return kf, w
 
     def lbfgs_reset(self):
         lib().orc_lbfgs_reset(self.ctx)

@@ -38,7 +38,7 @@ MUTANTS = {
         "ug[1 + q] = uin[1 + q] - 2.0 * mn * n[q];", "ug[1 + q] = uin[1 + q] - mn * n[q];",
         ["test_slip_wall_closed_form_single_triangle", "test_triangle_step_is_numpy_fv"]),
     "triangle_cfl_without_perimeter": (
-        "r = speed_norm(c, u) * c->perim[j] / c->area[j];", "r = speed_norm(c, u) / c->area[j];",
+        "return speed_norm(c, u) * c->perim[j] / c->area[j];", "return speed_norm(c, u) / c->area[j];",
         ["test_triangle_step_is_numpy_fv"]),  # (single triangle: its wall ghosts carry the same rate)
     "freestream_mach_on_wrong_xi": (
         "double Ma = s->q0[2] + s->q0[3] * xi[s->dim_a];", "double Ma = s->q0[2] + s->q0[3] * xi[s->dim_b];",
