@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--e2e-max-gb", type=float, default=16.0, help="largest state (uhat + lambda) the e2e leg pins")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=9238)
+    ap.add_argument("--hessian", default="newton", choices=["newton", "lbfgs"],
+                    help="dual-solve direction: exact Newton (the paper's method, default) or L-BFGS "
+                         "(reading 35, SURVEY 8(f) NEXT-4)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N > 1: weak = every rank a block of the configured grid; strong = the configured grid "
                          "split into N blocks (fixed total work)")
@@ -78,6 +81,15 @@ def flops_executed_per_iteration(N, m, Q, p, q1, kernel):
     hess = sf if sf is not None else 2 * Q * (N * (N + 1) // 2) * MM
     nc = 8 * ((n + 7) // 8) if kernel == "k_dual_mma" else n
     return 4 * Q * N * m + hess + nc ** 3 / 3 + 2 * nc * nc
+
+
+def flops_lbfgs_per_iteration(N, m, Q, mh=8):
+    """fp64 flops of one L-BFGS iteration of one cell (reading 35): reconstruction 2QNm, gradient 2QNm,
+    Jbar = sum_k omega_k J_k 2Q m(m+1)/2, two-loop recursion over mh pairs (two dot products and two
+    axpys of length n each: 8 n mh), H0 = I (x) Jbar^{-1} by two m x m triangular solves per moment
+    (2 N m^2).  Executed = algorithmic (no sum factorisation, the DMMA gradient pads N to 8)."""
+    n = N * m
+    return 4 * Q * N * m + 2 * Q * (m * (m + 1) // 2) + 8 * n * mh + 2 * N * m * m
 
 
 def flops_initial(N, m, Q):
@@ -138,6 +150,7 @@ def workload(args):
     from inputs import configs
 
     cfg = configs.get(args.config)
+    cfg["hessian"] = args.hessian
     if args.nx and cfg["mesh"]["kind"] == "cart2d":
         cfg["mesh"].update(nx=args.nx, ny=args.nx)
     elif args.nx and cfg["mesh"]["kind"] == "1d":
@@ -190,14 +203,14 @@ def run_reference(args):
     kind = stress_kind(cfg)
     if cfg["mesh"]["kind"] == "tri":
         full_cells = len(mesh_arrays(cfg)[1])
-        sample = configs.parity_variant(args.config)
+        sample = dict(configs.parity_variant(args.config), hessian=args.hessian)
         side = None
     else:
         full_cells = cfg["mesh"]["nx"] * cfg["mesh"].get("ny", 1)
         side = (128 if cfg["p"] <= 2 else 8) if cfg["mesh"]["kind"] == "cart2d" else min(cfg["mesh"]["nx"], 4096)
         if args.nx:
             side = min(side, args.nx)
-        sample = configs.get(args.config, mesh=dict(nx=side, ny=side))
+        sample = configs.get(args.config, mesh=dict(nx=side, ny=side), hessian=args.hessian)
     ma = mesh_arrays(sample)
     o = oracle.Oracle(sample, ma)
     base, z = stress_state(kind, centres(sample, ma), o.N, o.m, args.seed, sample.get("gamma", 1.4))
@@ -441,14 +454,17 @@ def run_ours(args):
 
     N, m, Q = g.N, g.m, g.Q
     dual_avg = float(np.mean(dual_ms))
-    flops = iters / args.steps * flops_per_iteration(N, m, Q) + g.cells * flops_initial(N, m, Q)
-    achieved = flops / (dual_avg / 1e3) / 1e12
     kname = Context.last_dual_kernel()
-    flops_ex = iters / args.steps * flops_executed_per_iteration(N, m, Q, cfg["p"], cfg["q1d"], kname) + \
-        g.cells * flops_initial(N, m, Q)
+    if args.hessian == "lbfgs":
+        flops = flops_ex = iters / args.steps * flops_lbfgs_per_iteration(N, m, Q) + g.cells * flops_initial(N, m, Q)
+    else:
+        flops = iters / args.steps * flops_per_iteration(N, m, Q) + g.cells * flops_initial(N, m, Q)
+        flops_ex = iters / args.steps * flops_executed_per_iteration(N, m, Q, cfg["p"], cfg["q1d"], kname) + \
+            g.cells * flops_initial(N, m, Q)
+    achieved = flops / (dual_avg / 1e3) / 1e12
     achieved_ex = flops_ex / (dual_avg / 1e3) / 1e12
     traffic = traffic_flux = ncu_pipe = None
-    if os.path.exists(NCU_SUMMARY) and not args.nx:  # measured at the bench configuration only
+    if os.path.exists(NCU_SUMMARY) and not args.nx and args.hessian == "newton":  # the bench configuration only
         try:
             ent = json.load(open(NCU_SUMMARY)).get(args.config, {})
             traffic, traffic_flux = ent.get("dual_dram_bytes_per_launch"), ent.get("flux_dram_bytes_per_launch")
@@ -466,7 +482,7 @@ def run_ours(args):
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": args.config, "cells_per_gpu": g.cells, "N": N, "m": m, "Q": Q,
-                       "newton": cfg["newton"], "tau": cfg["tau"],
+                       "newton": cfg["newton"], "tau": cfg["tau"], "hessian": args.hessian,
                        "state": "seeded dual-solve stress state (SURVEY §8d), steps continue Algorithm 1",
                        "l2": ("L2 flushed before every timed step (step state %.1f MB < 2x L2)" % (state_bytes / 1e6))
                        if flush else "inputs larger than L2 (node states %.1f GB)" % (g.cells * Q * m * 8 / 1e9),
@@ -484,7 +500,9 @@ def run_ours(args):
             # sum-factorised, SURVEY §8d note), the algorithmic count of §8d beside it
             "roofline": {"bound": "alu", "kernel": kname, "achieved": achieved_ex,
                          "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved_ex / FP64_PEAK_TFLOPS,
-                         "flops": "as executed: sum-factorised Hessian, 8-padded DMMA Cholesky",
+                         "flops": ("L-BFGS iteration (reading 35): node pass, gradient, Jbar, two-loop recursion"
+                                   if args.hessian == "lbfgs" else
+                                   "as executed: sum-factorised Hessian, 8-padded DMMA Cholesky"),
                          "peak_note": "derived 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz; measured DMMA 37.06, "
                                       "DFMA 33.7, DGEMM 35.5 TF/s (profiles/r01_fp64_peak.json)",
                          "algorithmic": {"achieved": achieved, "frac": achieved / FP64_PEAK_TFLOPS,

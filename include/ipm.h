@@ -136,6 +136,28 @@ typedef struct {
    * Clenshaw-Curtis rules of level quad_level (p <= quad_level <= p + 5; negative weights: cells whose
    * Hessian is then indefinite report IPM_CELL_ILLCONDITIONED).  Rules other than 0 need n = N m <= 88. */
   int32_t quad_kind, quad_level;
+  /* dual-solve direction (reading 35, "Hessian
+   * approximations ... BFGS ... construct the Hessian from previously computed gradients"):
+   *   0 exact Newton: H(lambda) of PAPER.md:169, Cholesky (default);
+   *   1 limited-memory BFGS: d = -H_l g by the two-loop recursion over the cell's last lbfgs_m pairs
+   *     (s, y) of accepted iterates, kept in the context across (pseudo-)time steps (a cell whose basis
+   *     size changed starts without pairs), initial matrix I_N (x) Jbar^{-1}, Jbar = sum_k omega_k
+   *     grad u_s(Lambda_k); the pairs occupy 2 lbfgs_m N m doubles per cell of device memory.
+   *     Supported: lbfgs_m = 8 (0 selects 8), n = N m <= 96.  Same line search, stopping test, counts
+   *     (accepted steps) and statuses as Newton, with at most 4 max_newton steps (superlinear, not
+   *     quadratic convergence); IPM_CELL_ILLCONDITIONED = Jbar not positive definite. */
+  int32_t hessian_kind, lbfgs_m;
+  /* per-level nested quadrature (reading 36; PAPER.md:385-398 and 625,
+   * "Order 2 uses 5 quadrature points, orders 3 to 6 use 9"): level_q1d[0] > 0 gives adaptive level l
+   * (n_levels > 0) its own tensor Clenshaw-Curtis rule of level_q1d[l] points per dimension, nested in
+   * the context's rule (quad_kind 1, q1d = level_q1d[n_levels-1]; level_q1d ascending with
+   * (q1d - 1) % (level_q1d[l] - 1) == 0).  The dual solve of a cell at level l and the moment update
+   * to level l integrate with rule l; the states of the stencil at its nodes come from each cell's
+   * duals at its own level (a node pass evaluates every cell at every node of the finest rule).  The
+   * IC projection uses the initial level's rule; the CFL rate takes the cells at their own rule's
+   * nodes and prescribed (STATE) boundary states at every node of the finest rule.  Needs the bucketed
+   * dual launches (Euler 2D, p = 2, degrees 2-5; IPM_ERR_UNSUPPORTED otherwise).  0 = one rule. */
+  int32_t level_q1d[8];
 } ipm_config;
 
 #define IPM_HIST_BUCKETS 16
@@ -252,6 +274,14 @@ IPM_API ipm_status ipm_warm_start(ipm_ctx *c, const double *d_uhat, double *d_la
 IPM_API ipm_status ipm_moments_from_dual(ipm_ctx *c, const double *d_lambda, double *d_uhat);
 IPM_API ipm_status ipm_stress_dual(ipm_ctx *c, const double *d_base, const double *d_z, double rel, double abs_,
                            double *d_lambda);
+
+/* L-BFGS (hessian_kind 1): forget every cell's pairs (the next solves start from Jbar^{-1} alone);
+ * asynchronous on the ctx stream.  IPM_ERR_ARG for a Newton context. */
+IPM_API ipm_status ipm_lbfgs_reset(ipm_ctx *c);
+/* L-BFGS history of the owned cells (device, caller-owned, nullable): d_S, d_Y [cells][lbfgs_m][N m]
+ * pairs newest first (entries beyond the count / the cell's basis size unspecified), d_count int32
+ * [cells].  Asynchronous on the ctx stream.  IPM_ERR_ARG for a Newton context. */
+IPM_API ipm_status ipm_lbfgs_history(ipm_ctx *c, double *d_S, double *d_Y, int32_t *d_count);
 
 /* levels (adaptivity): device int32 [cells]; get/set copy from/to the context */
 IPM_API ipm_status ipm_get_levels(ipm_ctx *c, int32_t *d_levels);

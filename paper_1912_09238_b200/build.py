@@ -10,7 +10,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libipm.so")
 SOURCES = ["ipm_kernels.cu", "ipm_api.cu", "ipm_mesh.cpp"]
-DEPS = SOURCES + ["ipm_device.cuh", "ipm_internal.h", "ipm_dual_group.cuh", "ipm_dual_mma.cuh", "ipm_dual_big.cuh", "ipm_flux_strip.cuh", "ipm_host.h"]
+DEPS = SOURCES + ["ipm_device.cuh", "ipm_internal.h", "ipm_dual_group.cuh", "ipm_dual_mma.cuh", "ipm_dual_big.cuh", "ipm_dual_lbfgs.cuh", "ipm_flux_strip.cuh", "ipm_host.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-shared",

@@ -313,7 +313,24 @@ struct ipm_ctx {
   // the dual kernel then writes no node states, the flux recomputes each band's from lambda
   int64_t band_rows = 0;
   double* d_uq_halo = nullptr;
+  // L-BFGS history (hessian_kind 1, reading 35): pairs newest first, 1/(s^T y), counts, basis sizes
+  double *d_lbS = nullptr, *d_lbY = nullptr, *d_lbR = nullptr;
+  int32_t *d_lbC = nullptr, *d_lbN = nullptr;
+  // per-level nested rules (reading 36): each level's tables on its own nodes (no sum factorisation
+  // tables; the bucketed launches add them)
+  ipm::Tables lq_tables[8] = {};
 };
+
+// the L-BFGS history of cells [r0, ...) for a dual launch (nothing for Newton contexts)
+static void lb_attach(const ipm_ctx* c, ipm::DualLaunch& a, int64_t r0) {
+  if (c->k.hessian_kind != 1) return;
+  const int64_t row = (int64_t)c->N * c->m, mh = c->k.lbfgs_m;
+  a.lb_S = c->d_lbS + r0 * mh * row;
+  a.lb_Y = c->d_lbY + r0 * mh * row;
+  a.lb_rho = c->d_lbR + r0 * mh;
+  a.lb_cnt = c->d_lbC + r0;
+  a.lb_n = c->d_lbN + r0;
+}
 
 extern "C" {
 
@@ -365,6 +382,18 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   if (C.n_levels < 0 || C.n_levels > 8) return fail(IPM_ERR_ARG, "n_levels in [0, 8]");
   if (C.n_levels > 0 && C.level_M[C.n_levels - 1] != C.M) return fail(IPM_ERR_ARG, "level_M[last] must equal M");
   if (C.n_retard < 0 || C.n_retard > 8) return fail(IPM_ERR_ARG, "n_retard must be in [0, 8]");
+  // per-level nested rules (reading 36): a nested ladder of tensor Clenshaw-Curtis rules, the finest
+  // being the context's rule
+  const bool level_rules = C.n_levels > 0 && C.level_q1d[0] > 0;
+  if (level_rules) {
+    const int nf = C.level_q1d[C.n_levels - 1];
+    if (C.quad_kind != 1 || C.q1d != nf) return fail(IPM_ERR_ARG, "per-level rules: quad_kind 1 (CC) with q1d = level_q1d[last]");
+    for (int l = 0; l < C.n_levels; ++l) {
+      const int nl = C.level_q1d[l];
+      if (nl < 2 || nl > nf || (nf - 1) % (nl - 1) != 0 || (l > 0 && nl < C.level_q1d[l - 1]))
+        return fail(IPM_ERR_ARG, "per-level rules must nest: level_q1d ascending, (q1d_f - 1) % (q1d_l - 1) == 0");
+    }
+  }
   for (int l = 0; l < C.n_retard && C.n_levels > 0; ++l)
     if (C.retard_level[l] < 0 || C.retard_level[l] >= C.n_levels) return fail(IPM_ERR_ARG, "retard_level out of range");
 
@@ -663,11 +692,77 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   k.mma_groups = std::getenv("IPM_MMA_GROUPS") ? std::max(1, std::atoi(std::getenv("IPM_MMA_GROUPS"))) : 0;
   k.group_t1 = env_is("IPM_GROUP_T", "1") ? 1 : 0;
   k.flux_choice = env_is("IPM_FLUX_KERNEL", "cart") ? 1 : env_is("IPM_FLUX_KERNEL", "warp") ? 2 : 0;
+  // per-level nested rules (reading 36): every level's own tables (Phi^T, omega Phi^T, the A-fragment
+  // copy, omega) on its Q_l nodes, and the node indices into the finest rule for the flux
+  if (level_rules) {
+    const int nf = C.level_q1d[C.n_levels - 1];
+    k.ad.lq.on = 1;
+    for (int l = 0; l < C.n_levels; ++l) {
+      const int nl = C.level_q1d[l], stride = (nf - 1) / (nl - 1), Nl = binom_total(p, C.level_M[l]);
+      std::vector<double> xl, wl;
+      clenshaw_curtis(nl, xl, wl);
+      int Ql = 1;
+      for (int d = 0; d < p; ++d) Ql *= nl;
+      const int QPl = (Ql % 2 == 0) ? Ql + 1 : Ql, MTl = (Nl + 7) / 8, KSl = (Ql + 3) / 4;
+      std::vector<int32_t> kf(Ql);
+      std::vector<double> om(Ql), PT((size_t)Nl * QPl, 0.0), WT((size_t)Nl * QPl, 0.0), WF((size_t)MTl * KSl * 32, 0.0);
+      for (int q = 0; q < Ql; ++q) {
+        int r = q, kk = 0, sc = 1;
+        double w = 1.0;
+        for (int d = p - 1; d >= 0; --d) {
+          const int jd = r % nl;
+          r /= nl;
+          kk += jd * stride * sc;
+          sc *= nf;
+          w *= 0.5 * wl[jd];
+        }
+        kf[q] = kk;
+        om[q] = w;
+        for (int i = 0; i < Nl; ++i) {
+          PT[(size_t)i * QPl + q] = c->phi[(size_t)kk * N + i];  // the finest rule's basis values at the node
+          WT[(size_t)i * QPl + q] = w * c->phi[(size_t)kk * N + i];
+        }
+      }
+      for (int mt = 0; mt < MTl; ++mt)
+        for (int ks = 0; ks < KSl; ++ks)
+          for (int ln = 0; ln < 32; ++ln) {
+            const int i = 8 * mt + ln / 4, q = 4 * ks + ln % 4;
+            if (i < Nl && q < Ql) WF[((size_t)mt * KSl + ks) * 32 + ln] = WT[(size_t)i * QPl + q];
+          }
+      int32_t* d_kf = dalloc<int32_t>(Ql, O);
+      double *d_om = dalloc<double>(Ql, O), *d_PT = dalloc<double>(PT.size(), O), *d_WT = dalloc<double>(WT.size(), O),
+             *d_WF = dalloc<double>(WF.size(), O);
+      if (!d_kf || !d_om || !d_PT || !d_WT || !d_WF || up(d_kf, kf.data(), Ql * 4) || up(d_om, om.data(), Ql * 8) ||
+          up(d_PT, PT.data(), PT.size() * 8) || up(d_WT, WT.data(), WT.size() * 8) || up(d_WF, WF.data(), WF.size() * 8)) {
+        ipm_destroy(c);
+        return fail(IPM_ERR_CUDA, "per-level rule tables upload failed");
+      }
+      k.ad.lq.Q[l] = Ql;
+      k.ad.lq.QP[l] = QPl;
+      k.ad.lq.kf[l] = d_kf;
+      k.ad.lq.wphit[l] = d_WT;
+      ipm::Tables t = k.T;
+      t.PhiT = d_PT;
+      t.WPhiT = d_WT;
+      t.omega = d_om;
+      t.N = Nl;
+      t.Q = Ql;
+      t.QP = QPl;
+      t.WPhiF = d_WF;
+      t.MT = MTl;
+      t.KS = KSl;
+      t.LL = nullptr;
+      t.q1d = 0;
+      t.npr = 0;
+      c->lq_tables[l] = t;
+    }
+  }
   // adaptive degree bucketed into uniform-degree launches (north star (c)): Euler 2D, tensor
   // Gauss-Legendre sum factorisation, every level's (n = N_l m, degree) among the k_dual_mma shapes
   // (n <= 24 / 40 / 64 / 88 with degrees 2 / 3 / 4 / 5); IPM_BUCKET=0 keeps the single N_max launch
   k.bucket = 0;
-  if (C.n_levels > 0 && C.closure == IPM_CLOSURE_EULER && m == 4 && p == 2 && tensor_gl && !env_is("IPM_BUCKET", "0")) {
+  if (C.n_levels > 0 && C.closure == IPM_CLOSURE_EULER && m == 4 && p == 2 && (tensor_gl || level_rules) &&
+      !env_is("IPM_BUCKET", "0")) {
     bool ok = true;
     for (int l = 0; l < C.n_levels; ++l) ok = ok && C.level_M[l] >= 2 && C.level_M[l] <= 5;
     if (ok) {
@@ -678,29 +773,78 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
       }
       for (int l = 0; l < C.n_levels; ++l) {
         const int Ml = C.level_M[l], nprl = (Ml + 1) * (Ml + 2) / 2;
-        std::vector<double> LLl((size_t)C.q1d * nprl);
-        for (int kq = 0; kq < C.q1d; ++kq) {
+        // the level's 1D rule: the context's, or its own nested Clenshaw-Curtis rule (reading 36)
+        std::vector<double> xl = x1, wl = w1;
+        if (level_rules) clenshaw_curtis(C.level_q1d[l], xl, wl);
+        const int q1l = (int)xl.size();
+        std::vector<double> LLl((size_t)q1l * nprl);
+        for (int kq = 0; kq < q1l; ++kq) {
           int pr = 0;
           for (int aa = 0; aa <= Ml; ++aa)
             for (int bb = aa; bb <= Ml; ++bb, ++pr)
-              LLl[(size_t)kq * nprl + pr] = 0.5 * w1[kq] * legendre_orthonormal(aa, x1[kq]) * legendre_orthonormal(bb, x1[kq]);
+              LLl[(size_t)kq * nprl + pr] = 0.5 * wl[kq] * legendre_orthonormal(aa, xl[kq]) * legendre_orthonormal(bb, xl[kq]);
         }
         double* d_LLl = dalloc<double>(LLl.size(), c->owned);
         if (!d_LLl || cudaMemcpy(d_LLl, LLl.data(), LLl.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
           ipm_destroy(c);
           return fail(IPM_ERR_CUDA, "level tables upload failed");
         }
-        ipm::Tables t = k.T;
+        ipm::Tables t = level_rules ? c->lq_tables[l] : k.T;
         t.N = binom_total(p, Ml);
         t.MT = (t.N + 7) / 8;
         t.LL = d_LLl;
         t.npr = nprl;
+        t.q1d = q1l;
         k.Tl[l] = t;
       }
       k.bucket = 1;
     }
   }
+  if (level_rules && !k.bucket) {
+    ipm_destroy(c);
+    return fail(IPM_ERR_UNSUPPORTED, "per-level rules need the bucketed dual launches (Euler 2D, p = 2, degrees 2-5)");
+  }
+  // quasi-Newton dual solve (reading 35): per-cell pair history in device memory
+  k.hessian_kind = C.hessian_kind;
+  k.lbfgs_m = C.lbfgs_m > 0 ? C.lbfgs_m : 8;
+  if (C.hessian_kind == 1) {
+    if (k.lbfgs_m != 8 || N * m > 96) {
+      ipm_destroy(c);
+      return fail(IPM_ERR_UNSUPPORTED, "L-BFGS dual solve: lbfgs_m must be 8 and N m <= 96");
+    }
+    const size_t row = (size_t)N * m, mh = (size_t)k.lbfgs_m, nc = (size_t)std::max<int64_t>(cells, 1);
+    c->d_lbS = dalloc<double>(nc * mh * row, c->owned);
+    c->d_lbY = dalloc<double>(nc * mh * row, c->owned);
+    c->d_lbR = dalloc<double>(nc * mh, c->owned);
+    c->d_lbC = dalloc<int32_t>(nc, c->owned);
+    c->d_lbN = dalloc<int32_t>(nc, c->owned);
+    if (!c->d_lbS || !c->d_lbY || !c->d_lbR || !c->d_lbC || !c->d_lbN ||
+        cudaMemset(c->d_lbC, 0, nc * 4) != cudaSuccess || cudaMemset(c->d_lbN, 0, nc * 4) != cudaSuccess) {
+      ipm_destroy(c);
+      return fail(IPM_ERR_CUDA, "cudaMalloc (L-BFGS history) failed");
+    }
+  } else if (C.hessian_kind != 0) {
+    ipm_destroy(c);
+    return fail(IPM_ERR_ARG, "hessian_kind must be 0 (Newton) or 1 (L-BFGS)");
+  }
   *out = c;
+  return IPM_OK;
+}
+
+ipm_status ipm_lbfgs_reset(ipm_ctx* c) {
+  if (!c) return fail(IPM_ERR_ARG, "null ctx");
+  if (c->k.hessian_kind != 1) return fail(IPM_ERR_ARG, "not an L-BFGS context");
+  CUDA_OK(cudaMemsetAsync(c->d_lbC, 0, (size_t)std::max<int64_t>(c->cells, 1) * 4, c->stream));
+  return IPM_OK;
+}
+
+ipm_status ipm_lbfgs_history(ipm_ctx* c, double* d_S, double* d_Y, int32_t* d_count) {
+  if (!c) return fail(IPM_ERR_ARG, "null ctx");
+  if (c->k.hessian_kind != 1) return fail(IPM_ERR_ARG, "not an L-BFGS context");
+  const size_t nc = (size_t)c->cells, per = (size_t)c->k.lbfgs_m * c->N * c->m;
+  if (d_S) CUDA_OK(cudaMemcpyAsync(d_S, c->d_lbS, nc * per * 8, cudaMemcpyDeviceToDevice, c->stream));
+  if (d_Y) CUDA_OK(cudaMemcpyAsync(d_Y, c->d_lbY, nc * per * 8, cudaMemcpyDeviceToDevice, c->stream));
+  if (d_count) CUDA_OK(cudaMemcpyAsync(d_count, c->d_lbC, nc * 4, cudaMemcpyDeviceToDevice, c->stream));
   return IPM_OK;
 }
 
@@ -776,6 +920,7 @@ ipm_status ipm_dual_solve(ipm_ctx* c, const double* d_uhat, double* d_lambda, in
   a.cells = c->cells;
   a.mode = mode;
   a.want_rate = 0;
+  lb_attach(c, a, 0);
   return launch_rc(ipm::launch_dual(k, a), "dual_solve");
 }
 
@@ -847,12 +992,14 @@ ipm_status ipm_step_dual(ipm_ctx* c, const double* d_uhat, double* d_lambda, dou
   a.crit = c->d_crit;
   a.halv = c->d_halv;
   a.inadm = c->d_inadm;
-  a.uq = c->band_rows ? nullptr : c->d_uq;  // banded: the flux recomputes the node states
+  // banded: the flux recomputes the node states; per-level rules: a node pass on the finest rule
+  a.uq = (c->band_rows || c->k.ad.lq.on) ? nullptr : c->d_uq;
   a.level = c->cfg.n_levels > 0 ? c->d_level : nullptr;
   a.level_new = c->cfg.n_levels > 0 ? c->d_level_new : nullptr;
   a.cells = c->cells;
   a.mode = c->cfg.newton_mode;
   a.want_rate = 1;
+  lb_attach(c, a, 0);
   if (c->timing) cudaEventRecord(c->ev[0], c->stream);
   if (int rc = ipm::launch_dual(k, a)) return launch_rc(rc, "dual_solve");
   if (c->timing) cudaEventRecord(c->ev[1], c->stream);
@@ -874,6 +1021,10 @@ ipm_status ipm_step_flux(ipm_ctx* c, double* d_uhat, double* d_lambda, const dou
   const int32_t* lvl_new = c->cfg.n_levels > 0 ? c->d_level_new : nullptr;
   ipm::FluxLaunch f{c->d_uq, d_uhat, d_uhat, lvl_new, d_lambda, c->cfg.update_form, c->cfg.cfl};
   if (c->timing) cudaEventRecord(c->ev[2], c->stream);
+  // per-level nested rules (reading 36): every owned cell's states at every node of the finest rule
+  // from its duals at its old level (the flux of a cell at level l reads the nodes of Q_l)
+  if (k.ad.lq.on)
+    if (int rc = ipm::launch_nodes(k, d_lambda, nullptr, c->d_uq, 0)) return launch_rc(rc, "nodes (level rules)");
   if (c->band_rows) {
     if (int rc = band_flux(c, d_lambda, f)) return launch_rc(rc, "flux (bands)");
   } else if (int rc = ipm::launch_flux(k, f)) {
@@ -995,12 +1146,13 @@ ipm_status ipm_step_host(ipm_ctx* c, double* h_uhat, double* h_lambda, double* d
     a.crit = c->d_crit + r0;
     a.halv = c->d_halv + r0;
     a.inadm = c->d_inadm + r0;
-    a.uq = c->band_rows ? nullptr : c->d_uq + (size_t)r0 * c->Q * c->m;
+    a.uq = (c->band_rows || c->k.ad.lq.on) ? nullptr : c->d_uq + (size_t)r0 * c->Q * c->m;
     a.level = adaptive ? c->d_level + r0 : nullptr;
     a.level_new = adaptive ? c->d_level_new + r0 : nullptr;
     a.cells = nr;
     a.mode = c->cfg.newton_mode;
     a.want_rate = 1;
+    lb_attach(c, a, r0);
     if (int rc = ipm::launch_dual(kc, a)) return launch_rc(rc, "dual_solve");
     if (!adaptive) {  // final duals of the range go back while later ranges solve
       CUDA_OK(cudaEventRecord(c->hev[nch + i], ms));

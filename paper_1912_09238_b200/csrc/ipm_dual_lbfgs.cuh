@@ -1,0 +1,452 @@
+// ipm_dual_lbfgs.cuh — quasi-Newton (limited-memory BFGS) dual solve, one warp per cell (sm_100a, fp64).
+//
+// SURVEY 8(f) NEXT-4; reading 35.  PAPER.md:843 proposes to replace the exact dual Hessian
+// by BFGS approximations "which construct the Hessian from previously computed gradients", the
+// gradients of old time steps kept in every spatial cell.  Per cell, the direction is
+//   d = -H_l g,  H_l = the L-BFGS inverse-Hessian approximation (two-loop recursion) over the cell's
+//                      last MH pairs s = lambda^{(l+1)} - lambda^{(l)}, y = g^{(l+1)} - g^{(l)},
+//                      kept across (pseudo-)time steps in HBM,
+//   initial matrix H0 = I_N (x) Jbar^{-1},  Jbar = sum_k omega_k grad u_s(Lambda_k)  (m x m),
+// the exact inverse Hessian of a xi-independent state because <phi phi^T>_Q = I.
+// Everything else is the Newton iteration of k_dual_mma: node pass, gradient on DMMA, Armijo on L
+// with the rounding allowance (reading 3'), stopping test, epilogue.  Per iteration
+// there is no Hessian and no Cholesky: the node pass, one DMMA gradient and 2 cnt dot products.
+//
+// Layout: one warp per cell (no group barriers), lanes own unknowns r = lane + 32 e (e < NR) for the
+// vector work and the pairs, which live in REGISTERS (S, Y: MH x NR per lane, newest first; shifted
+// on insertion so every index is a compile-time constant); lambda, trial, uhat, g, the direction and
+// the node buffer u[a][k] live in the warp's shared-memory slice (the node pass reads lambda by
+// broadcast).  Tables as k_dual_mma: Phi^T [N][QP], omega Phi^T in A-fragment order.
+#pragma once
+// (included inside namespace ipm by ipm_kernels.cu, after ipm_dual_mma.cuh)
+
+template <int MS>
+struct LbfgsLayout {
+  // per warp: lam, lt, uh, g, q (direction / two-loop vector)  [5][NV]  + node buffer u [MS][Q]
+  static __host__ __device__ int per_warp(int NV, int Q) { return ((5 * NV + MS * Q) + 1) & ~1; }
+};
+
+#ifndef IPM_LBFGS_THREADS
+#define IPM_LBFGS_THREADS 384
+#endif
+template <int CL, int MS, int NR, int MH>
+__global__ void __launch_bounds__(IPM_LBFGS_THREADS, 1) k_dual_lbfgs(DualParams P) {
+  extern __shared__ __align__(16) double sm[];
+  constexpr int MM = MS * (MS + 1) / 2;
+  constexpr int NV = 32 * NR;
+  const int N = P.T.N, Q = P.T.Q, QP = P.T.QP, KS = P.T.KS;
+  double* sPhiT = sm;
+  double* sWF = sm + N * QP;  // [MT][KS][32]
+  const int MTT = P.T.MT;
+  const int tabsz = (N * QP + MTT * KS * 32 + 1) & ~1;
+  for (int x = threadIdx.x; x < N * QP; x += blockDim.x) sPhiT[x] = P.T.PhiT[x];
+  for (int x = threadIdx.x; x < MTT * KS * 32; x += blockDim.x) sWF[x] = P.T.WPhiF[x];
+  __syncthreads();
+  const int wig = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* base = sm + tabsz + (size_t)wig * LbfgsLayout<MS>::per_warp(NV, Q);
+  double* lam = base;
+  double* lt = lam + NV;
+  double* uh = lt + NV;
+  double* g = uh + NV;
+  double* qv = g + NV;
+  double* nb = qv + NV;  // u[a][k] at nb[a Q + k]
+
+  const double* __restrict__ omega = P.T.omega;
+  const DualLaunch& A = P.a;
+  const int nmax = A.row ? A.row : N * MS;
+  const int64_t ncells = A.ncells_dev ? (int64_t)*A.ncells_dev : A.cells;
+  int* const queue = A.queue ? A.queue : &P.sc->work_counter;
+  long long my_iters = 0, my_failed = 0;
+  int my_worst = 0;
+  double my_rate = 0.0;
+
+  for (;;) {
+    int ci = 0;
+    if (lane == 0) ci = atomicAdd(queue, 1);
+    ci = __shfl_sync(FULL_MASK, ci, 0);
+    if (ci >= ncells) break;
+    const int64_t cell = A.list ? (int64_t)A.list[ci] : (int64_t)ci;
+    const int lvl = A.level ? A.level[cell] : 0;
+    const int Nl = (P.ad.n_levels > 0 && !A.list) ? P.ad.Nl[lvl] : N;
+    const int n = Nl * MS;
+    // ---- load the cell: uhat, lambda, the L-BFGS history (pairs of another size are dropped) ----
+    {
+      const double* gu = A.uhat + cell * nmax;
+      const double* gl = A.lam + cell * nmax;
+      for (int r = lane; r < NV; r += 32) {
+        uh[r] = r < n ? gu[r] : 0.0;
+        lam[r] = r < n ? gl[r] : 0.0;
+      }
+    }
+    int cnt = A.lb_cnt[cell];
+    if (A.lb_n[cell] != n) cnt = 0;
+    double S[MH][NR], Y[MH][NR], rho[MH];
+    {
+      const double* gS = A.lb_S + cell * (int64_t)MH * nmax;
+      const double* gY = A.lb_Y + cell * (int64_t)MH * nmax;
+#pragma unroll
+      for (int i = 0; i < MH; ++i) {
+        rho[i] = (i < cnt) ? A.lb_rho[cell * MH + i] : 0.0;
+#pragma unroll
+        for (int e = 0; e < NR; ++e) {
+          const int r = lane + 32 * e;
+          const bool v = i < cnt && r < n;
+          S[i][e] = v ? gS[(int64_t)i * nmax + r] : 0.0;
+          Y[i][e] = v ? gY[(int64_t)i * nmax + r] : 0.0;
+        }
+      }
+    }
+    __syncwarp();
+
+    int status = 0, l = 0, h = 0, mode = 0, hv = 0, ia = 0;
+    double crit = INFINITY, L0 = 0.0, scale = 0.0, slope = 0.0, alpha = 1.0;
+    bool nb_is_lam = false;
+    double gold[NR], dreg[NR];
+#pragma unroll
+    for (int e = 0; e < NR; ++e) gold[e] = dreg[e] = 0.0;
+    for (;;) {
+      const double* x = (mode == 1) ? lt : lam;
+      // ---- a2: Lambda = Phi x, u = u_s(Lambda), s_*, and the lane's part of sum_k omega_k J_k -------
+      double sv0 = 0.0, sv1 = 0.0, jac[MM];
+#pragma unroll
+      for (int z = 0; z < MM; ++z) jac[z] = 0.0;
+      bool bad = false;
+      for (int k = lane; k < Q; k += 32) {
+        double Lam[MS];
+#pragma unroll
+        for (int a = 0; a < MS; ++a) Lam[a] = 0.0;
+#pragma unroll 4
+        for (int i = 0; i < Nl; ++i) {
+          const double ph = sPhiT[i * QP + k];
+#pragma unroll
+          for (int a = 0; a < MS; ++a) Lam[a] = fma(x[i * MS + a], ph, Lam[a]);
+        }
+        double u[MS], J[MM], ss;
+        if (!Closure<CL, MS>::eval(Lam, u, J, ss, P.cl)) bad = true;
+#pragma unroll
+        for (int a = 0; a < MS; ++a) nb[a * Q + k] = u[a];
+        const double w = omega[k];
+#pragma unroll
+        for (int z = 0; z < MM; ++z) jac[z] = fma(w, J[z], jac[z]);
+        sv0 = fma(w, ss, sv0);
+        sv1 = fma(w, fabs(ss), sv1);
+      }
+      if (bad) sv1 = INFINITY;
+      double dv0 = 0.0, dv1 = 0.0;
+#pragma unroll
+      for (int e = 0; e < NR; ++e) {
+        const int r = lane + 32 * e;
+        const double v = x[r] * uh[r];  // zero beyond n
+        dv0 += v;
+        dv1 += fabs(v);
+      }
+      sv0 = warp_sum(sv0);
+      sv1 = warp_sum(sv1);
+      dv0 = warp_sum(dv0);
+      dv1 = warp_sum(dv1);
+      __syncwarp();  // node buffer complete
+      if (mode == 2) {
+        nb_is_lam = true;
+        break;
+      }
+      const bool ok = isfinite(sv0) && isfinite(sv1);
+      const double Lt = sv0 - dv0;
+      bool accept;
+      if (mode == 0) {
+        if (!ok) {
+          status = 4;
+          break;
+        }
+        accept = true;
+      } else {
+        accept = ok && (Lt <= L0 + P.nw.armijo_c * alpha * slope + 1e-12 * scale);
+      }
+      bool finish = false;
+      if (accept) {
+        // ---- a3: gradient g = Phi^T (omega o u) - uhat on DMMA (A = omega Phi^T fragments) ----------
+        double part[MS];
+#pragma unroll
+        for (int a = 0; a < MS; ++a) part[a] = 0.0;
+        {
+          const int MTl = (Nl + 7) >> 3, bn = lane >> 2, bk = lane & 3;
+          const bool bval = bn < MS;
+          const double* bsrc = nb + (bval ? bn : 0) * Q + bk;
+#pragma unroll 1
+          for (int mt = 0; mt < MTl; ++mt) {
+            double c0 = 0.0, c1 = 0.0;
+            const double* asrc = sWF + mt * KS * 32 + lane;
+#pragma unroll 5
+            for (int ks = 0; ks < KS; ++ks) {
+              const double bv = (bval && 4 * ks + bk < Q) ? bsrc[4 * ks] : 0.0;
+              dmma884(c0, c1, asrc[ks * 32], bv);
+            }
+            const int i = 8 * mt + (lane >> 2);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int a = 2 * (lane & 3) + e;
+              if (a < MS && i < Nl) {
+                const int rr = i * MS + a;
+                const double gr = (e == 0 ? c0 : c1) - uh[rr];
+                g[rr] = gr;
+#pragma unroll
+                for (int b = 0; b < MS; ++b)
+                  if (b == a) part[b] = fma(gr, gr, part[b]);
+              }
+            }
+          }
+        }
+        __syncwarp();
+        double gr_[NR];
+#pragma unroll
+        for (int e = 0; e < NR; ++e) {
+          const int r = lane + 32 * e;
+          gr_[e] = r < n ? g[r] : 0.0;
+        }
+        if (mode == 1) {
+          // accepted trial: pair s = lt - lam, y = g_new - g_old (reading 35), then lam = lt
+          double sy = 0.0, ss2 = 0.0, yy = 0.0, sn[NR], yn[NR];
+#pragma unroll
+          for (int e = 0; e < NR; ++e) {
+            const int r = lane + 32 * e;
+            sn[e] = lt[r] - lam[r];
+            yn[e] = gr_[e] - gold[e];
+            sy = fma(sn[e], yn[e], sy);
+            ss2 = fma(sn[e], sn[e], ss2);
+            yy = fma(yn[e], yn[e], yy);
+          }
+          sy = warp_sum(sy);
+          ss2 = warp_sum(ss2);
+          yy = warp_sum(yy);
+          if (sy > 1e-10 * sqrt(ss2 * yy)) {  // curvature condition with a rounding margin
+#pragma unroll
+            for (int i = MH - 1; i > 0; --i) {
+              rho[i] = rho[i - 1];
+#pragma unroll
+              for (int e = 0; e < NR; ++e) {
+                S[i][e] = S[i - 1][e];
+                Y[i][e] = Y[i - 1][e];
+              }
+            }
+            rho[0] = 1.0 / sy;
+#pragma unroll
+            for (int e = 0; e < NR; ++e) {
+              S[0][e] = sn[e];
+              Y[0][e] = yn[e];
+            }
+            cnt = cnt < MH ? cnt + 1 : MH;
+          }
+#pragma unroll
+          for (int e = 0; e < NR; ++e) {
+            const int r = lane + 32 * e;
+            lam[r] = lt[r];
+          }
+          ++l;
+        }
+#pragma unroll
+        for (int e = 0; e < NR; ++e) gold[e] = gr_[e];
+#pragma unroll
+        for (int a = 0; a < MS; ++a) part[a] = warp_sum(part[a]);
+        crit = 0.0;
+#pragma unroll
+        for (int a = 0; a < MS; ++a) crit += sqrt(part[a]);
+        nb_is_lam = true;
+        L0 = Lt;
+        scale = sv1 + dv1;
+        // ---- a7: stopping tests ---------------------------------------------------------------------
+        if (crit < P.nw.tau || (P.nw.mode == 1 && l == 1)) break;
+        if (l == 4 * P.nw.max_newton) {  // reading 35: 4 max_newton quasi-Newton steps
+          status = 1;
+          break;
+        }
+        // ---- L-BFGS direction (two-loop recursion, H0 = I (x) Jbar^{-1}) ------------------------------
+        double Jb[MM];
+#pragma unroll
+        for (int z = 0; z < MM; ++z) Jb[z] = warp_sum(jac[z]);
+        // Cholesky of Jbar (m x m, every lane redundantly): Lc packed lower by rows
+        double Lc[MS][MS];
+        bool spd = true;
+#pragma unroll
+        for (int j = 0; j < MS; ++j) {
+          double t = Jb[sym_idx<MS>(j, j)];
+#pragma unroll
+          for (int k = 0; k < j; ++k) t = fma(-Lc[j][k], Lc[j][k], t);
+          if (!(t > 0.0) || !isfinite(t)) spd = false;
+          Lc[j][j] = sqrt(t);
+          const double inv = 1.0 / Lc[j][j];
+#pragma unroll
+          for (int i = j + 1; i < MS; ++i) {
+            double v = Jb[sym_idx<MS>(j, i)];
+#pragma unroll
+            for (int k = 0; k < j; ++k) v = fma(-Lc[i][k], Lc[j][k], v);
+            Lc[i][j] = v * inv;
+          }
+        }
+        if (!spd) {
+          status = 2;
+          finish = true;
+        } else {
+          for (int pass = 0; pass < 2; ++pass) {
+            // first loop, newest pair first
+            double q[NR], al[MH];
+#pragma unroll
+            for (int e = 0; e < NR; ++e) q[e] = gr_[e];
+#pragma unroll
+            for (int i = 0; i < MH; ++i) {
+              al[i] = 0.0;
+              if (i < cnt) {
+                double t = 0.0;
+#pragma unroll
+                for (int e = 0; e < NR; ++e) t = fma(S[i][e], q[e], t);
+                al[i] = rho[i] * warp_sum(t);
+#pragma unroll
+                for (int e = 0; e < NR; ++e) q[e] = fma(-al[i], Y[i][e], q[e]);
+              }
+            }
+            // r = H0 q: Jbar r_i = q_i per moment i (the m states of moment i through shared memory)
+#pragma unroll
+            for (int e = 0; e < NR; ++e) qv[lane + 32 * e] = q[e];
+            __syncwarp();
+#pragma unroll
+            for (int e = 0; e < NR; ++e) {
+              const int r = lane + 32 * e;
+              const int rc = r < n ? r : 0;  // (lanes beyond n: a valid moment, result discarded)
+              const int i = rc / MS, a = rc - i * MS;
+              double y[MS], z[MS];
+#pragma unroll
+              for (int b = 0; b < MS; ++b) {
+                double v = qv[i * MS + b];
+#pragma unroll
+                for (int k = 0; k < b; ++k) v = fma(-Lc[b][k], y[k], v);
+                y[b] = v / Lc[b][b];
+              }
+#pragma unroll
+              for (int b = MS - 1; b >= 0; --b) {
+                double v = y[b];
+#pragma unroll
+                for (int k = b + 1; k < MS; ++k) v = fma(-Lc[k][b], z[k], v);
+                z[b] = v / Lc[b][b];
+              }
+              double rv = 0.0;
+#pragma unroll
+              for (int b = 0; b < MS; ++b)
+                if (b == a) rv = z[b];
+              q[e] = (r < n) ? rv : 0.0;
+            }
+            __syncwarp();
+            // second loop, oldest pair first
+#pragma unroll
+            for (int i = MH - 1; i >= 0; --i) {
+              if (i < cnt) {
+                double t = 0.0;
+#pragma unroll
+                for (int e = 0; e < NR; ++e) t = fma(Y[i][e], q[e], t);
+                const double be = rho[i] * warp_sum(t);
+#pragma unroll
+                for (int e = 0; e < NR; ++e) q[e] = fma(S[i][e], al[i] - be, q[e]);
+              }
+            }
+            double sl = 0.0;
+#pragma unroll
+            for (int e = 0; e < NR; ++e) {
+              dreg[e] = -q[e];
+              sl = fma(gr_[e], dreg[e], sl);
+            }
+            slope = warp_sum(sl);
+            if (slope < 0.0 || cnt == 0) break;
+            cnt = 0;  // not a descent direction (rounding): drop the history, H0 alone
+          }
+          alpha = 1.0;
+          h = 0;
+        }
+      } else {
+        nb_is_lam = false;
+        ++hv;
+        if (!ok) ++ia;
+        alpha *= 0.5;
+        if (++h > P.nw.max_halvings) {
+          status = 3;
+          finish = true;
+        }
+      }
+      if (finish) {
+        if (nb_is_lam) break;
+        mode = 2;  // re-evaluate the last accepted iterate
+      } else {
+#pragma unroll
+        for (int e = 0; e < NR; ++e) {
+          const int r = lane + 32 * e;
+          lt[r] = (r < n) ? lam[r] + alpha * dreg[e] : 0.0;
+        }
+        mode = 1;
+      }
+      __syncwarp();
+    }
+    __syncwarp();
+    // ---- epilogue: level (adaptive), lambda, history, statistics, node states, CFL rate ------------
+    if (P.ad.n_levels > 0 && A.level_new) {
+      const int Nprev = lvl > 0 ? P.ad.Nl[lvl - 1] : P.ad.Nprev0;
+      double nd0 = 0.0, nd1 = 0.0;
+      for (int i = lane; i < Nl; i += 32) {
+        const double hv_ = g[i * MS] + uh[i * MS];
+        nd1 = fma(hv_, hv_, nd1);
+        if (i >= Nprev) nd0 = fma(hv_, hv_, nd0);
+      }
+      nd0 = warp_sum(nd0);
+      nd1 = warp_sum(nd1);
+      const double Sv = nd1 > 0.0 ? nd0 / nd1 : 0.0;
+      const int nl = next_level(P.ad, P.sc, lvl, status, Sv);
+      if (lane == 0) A.level_new[cell] = nl;
+    }
+    {
+      double* gl = A.lam + cell * nmax;
+      for (int r = lane; r < nmax; r += 32) gl[r] = (r < n) ? lam[r] : 0.0;
+      double* gS = A.lb_S + cell * (int64_t)MH * nmax;
+      double* gY = A.lb_Y + cell * (int64_t)MH * nmax;
+#pragma unroll
+      for (int i = 0; i < MH; ++i) {
+        if (i < cnt) {
+#pragma unroll
+          for (int e = 0; e < NR; ++e) {
+            const int r = lane + 32 * e;
+            if (r < n) {
+              gS[(int64_t)i * nmax + r] = S[i][e];
+              gY[(int64_t)i * nmax + r] = Y[i][e];
+            }
+          }
+          if (lane == 0) A.lb_rho[cell * MH + i] = rho[i];
+        }
+      }
+      if (lane == 0) {
+        A.lb_cnt[cell] = cnt;
+        A.lb_n[cell] = n;
+      }
+    }
+    if (lane == 0) {
+      cell_stats(A, P.sc, cell, l, status, hv, ia, crit);
+      my_iters += l;
+      if (status != 0) {
+        my_failed += 1;
+        my_worst = max(my_worst, status);
+      }
+    }
+    for (int k = lane; k < Q; k += 32) {  // node states at the final iterate (variant B)
+      double u[MS];
+#pragma unroll
+      for (int a = 0; a < MS; ++a) u[a] = nb[a * Q + k];
+      if (A.uq) {
+        double* o = A.uq + cell * Q * MS + k;  // [cell][state][node]
+#pragma unroll
+        for (int a = 0; a < MS; ++a) o[a * Q] = u[a];
+      }
+      if (A.want_rate) my_rate = fmax(my_rate, node_rate<CL, MS>(u, P.mesh, cell, P.cl.gamma));
+    }
+    __syncwarp();
+  }
+  my_rate = warp_max(my_rate);
+  if (lane == 0) {
+    if (A.want_rate) atomicMax(&P.sc->rate_bits, (unsigned long long)__double_as_longlong(my_rate));
+    if (my_iters) atomicAdd(&P.sc->newton_iters, (unsigned long long)my_iters);
+    if (my_failed) atomicAdd(&P.sc->failed, (unsigned long long)my_failed);
+    if (my_worst) atomicMax(&P.sc->worst, my_worst);
+  }
+}

@@ -54,7 +54,17 @@ struct Newton {
   int mode;
 };
 
+// per-level nested quadrature (reading 36): level l integrates with its own
+// tensor Clenshaw-Curtis rule, node q of which is node kf[l][q] of the finest rule (Tables T)
+struct LevelRules {
+  int on;
+  int Q[8], QP[8];
+  const int32_t* kf[8];    // [Q_l]
+  const double* wphit[8];  // [N_l][QP_l]  omega^l_q phi_i(xi_kf(q))
+};
+
 struct Adapt {
+  LevelRules lq;
   int n_levels;
   int Nl[8];
   int Nprev0;  // basis size of degree level_M[0]-1 (indicator band at the lowest level)
@@ -101,6 +111,12 @@ struct DualLaunch {
   const int32_t* ncells_dev;
   int* queue;
   int row;
+  // L-BFGS history (hessian_kind 1, reading 35; ctx-owned): pairs newest first
+  double* lb_S;     // [cells][lbfgs_m][row]
+  double* lb_Y;     // [cells][lbfgs_m][row]
+  double* lb_rho;   // [cells][lbfgs_m]  1 / (s^T y)
+  int32_t* lb_cnt;  // [cells] stored pairs
+  int32_t* lb_n;    // [cells] unknowns the pairs belong to
 };
 
 struct FluxLaunch {
@@ -145,6 +161,8 @@ struct KernelCtx {
   int big_ctas;
   // adaptive degree bucketed into uniform-degree launches (north star (c); Alg. 3): per-level
   // tables (N_l, its 1D pair table, tile counts; Phi / omega Phi shared by prefix) and cell lists
+  int hessian_kind;       // 0 exact Newton (Hessian + Cholesky), 1 L-BFGS (k_dual_lbfgs, reading 35)
+  int lbfgs_m;            // L-BFGS pairs per cell
   int bucket;             // 1: one k_dual_mma launch per level over that level's cells
   Tables Tl[8];
   int32_t* lists;         // [n_levels][cells]

@@ -420,6 +420,7 @@ __global__ void __launch_bounds__(512) k_dual_warp(DualParams P) {
 #include "ipm_dual_group.cuh"
 #include "ipm_dual_mma.cuh"
 #include "ipm_dual_big.cuh"
+#include "ipm_dual_lbfgs.cuh"
 
 // ------------------------------------------------------------------------------------------------
 // flux kernel (variant B: node states from the dual kernel)
@@ -460,7 +461,13 @@ __global__ void __launch_bounds__(256) k_flux_warp(FluxParams P) {
     return A.uq + (c - A.uq_base) * Q * MS;
   };
   for (int64_t cell = A.cell0 + (int64_t)blockIdx.x * nw + warp; cell < P.mesh.cells; cell += total_warps) {
-    for (int k = lane; k < Q; k += 32) {
+    // per-level nested rules (reading 36): the update at level l^{n+1} integrates with that level's
+    // rule, at its nodes kf of the finest rule (eq. adaptiveFVUpdate)
+    const int Lq = (P.ad.lq.on && A.level_new) ? A.level_new[cell] : -1;
+    const int Qc = Lq >= 0 ? P.ad.lq.Q[Lq] : Q;
+    const int32_t* __restrict__ kfc = Lq >= 0 ? P.ad.lq.kf[Lq] : nullptr;
+    for (int kq = lane; kq < Qc; kq += 32) {
+      const int k = kfc ? kfc[kq] : kq;
       double uj[MS], r[MS], gneg[MS];
       const double* src = nodes_of(cell) + k;
 #pragma unroll
@@ -523,7 +530,7 @@ __global__ void __launch_bounds__(256) k_flux_warp(FluxParams P) {
           for (int a = 0; a < MS; ++a) r[a] += (gpos[a] - gneg[a]) * cf;
         }
       }
-      double* qk = q + k * MS;
+      double* qk = q + kq * MS;
       if (A.update_form == 1) {
 #pragma unroll
         for (int a = 0; a < MS; ++a) qk[a] = uj[a] - dt * r[a];
@@ -541,9 +548,9 @@ __global__ void __launch_bounds__(256) k_flux_warp(FluxParams P) {
       const double old = uo[rr];  // uhat_new may alias uhat_old (only this cell's entries are read)
       double out = 0.0;
       if (i < Nnew) {
-        const double* wp = sWPhiT + i * QP;
+        const double* wp = Lq >= 0 ? P.ad.lq.wphit[Lq] + i * P.ad.lq.QP[Lq] : sWPhiT + i * QP;
         double s = 0.0;
-        for (int k = 0; k < Q; ++k) s = fma(wp[k], q[k * MS + a], s);
+        for (int k = 0; k < Qc; ++k) s = fma(wp[k], q[k * MS + a], s);
         out = (A.update_form == 1) ? s : old - dt * s;
       }
       un_[rr] = out;
@@ -953,11 +960,19 @@ __global__ void k_project_ic(Tables T, int64_t cells, const double* __restrict__
     __syncwarp();
     if (!uhat) continue;
     const int Nl = (ad.n_levels > 0 && level) ? ad.Nl[level[cell]] : N;
+    const int Lq = (ad.lq.on && level) ? level[cell] : -1;  // Alg. 3 line 3: the initial level's rule
     for (int r = lane; r < N * MS; r += 32) {
       const int i = r / MS, a = r - i * MS;
       double s = 0.0;
-      if (i < Nl)
-        for (int k = 0; k < Q; ++k) s = fma(T.WPhiT[i * T.QP + k], q[k * MS + a], s);
+      if (i < Nl) {
+        if (Lq >= 0) {
+          const double* wp = ad.lq.wphit[Lq] + i * ad.lq.QP[Lq];
+          const int32_t* kf = ad.lq.kf[Lq];
+          for (int kq = 0; kq < ad.lq.Q[Lq]; ++kq) s = fma(wp[kq], q[kf[kq] * MS + a], s);
+        } else {
+          for (int k = 0; k < Q; ++k) s = fma(T.WPhiT[i * T.QP + k], q[k * MS + a], s);
+        }
+      }
       uhat[cell * N * MS + r] = s;
     }
     __syncwarp();
@@ -1274,6 +1289,45 @@ int dual_mma_dispatch(const KernelCtx& k, const DualLaunch& a, int SF) {
 static const char* g_last_dual = "";
 const char* last_dual_kernel() { return g_last_dual; }
 
+// quasi-Newton dual solve (reading 35): one warp per cell, as many warps per CTA as shared memory and
+// registers allow, one persistent CTA per SM
+template <int CL, int MS, int NR, int MH>
+static int dual_lbfgs_impl(const KernelCtx& k, const DualLaunch& a) {
+  const size_t tab = (((size_t)k.T.N * k.T.QP + (size_t)k.T.MT * k.T.KS * 32 + 1) & ~(size_t)1) * 8;
+  const size_t pw = (size_t)LbfgsLayout<MS>::per_warp(32 * NR, k.T.Q) * 8;
+  if (tab + pw > k.smem_optin) return -1;
+  int warps = (int)((k.smem_optin - tab) / pw);
+  warps = std::min(warps, IPM_LBFGS_THREADS / 32);
+  auto kern = k_dual_lbfgs<CL, MS, NR, MH>;
+  const size_t smem = tab + warps * pw;
+  int per_sm = configure(kern, warps * 32, smem);
+  if (per_sm < 1) return -1;
+  const int64_t want = (a.cells + warps - 1) / warps;
+  int grid = (int)std::min<int64_t>(want, (int64_t)k.sm_count * per_sm);
+  if (grid < 1) grid = 1;
+  DualParams P{k.T, k.mesh, k.nw, k.ad, k.cl, a, k.sc};
+  kern<<<grid, warps * 32, smem, S(k)>>>(P);
+  g_last_dual = "k_dual_lbfgs";
+  return (int)cudaGetLastError();
+}
+
+static int dual_lbfgs_dispatch(const KernelCtx& k, const DualLaunch& a) {
+  const int n = k.T.N * k.m, NR = (n + 31) / 32;
+  if (k.lbfgs_m != 8) return -1;
+  switch ((k.closure * 10 + k.m) * 10 + NR) {
+#define IPM_LCASE(CLV, MSV, NRV) \
+  case (CLV * 10 + MSV) * 10 + NRV: return dual_lbfgs_impl<CLV, MSV, NRV, 8>(k, a);
+    IPM_LCASE(CL_QUADRATIC, 1, 1)
+    IPM_LCASE(CL_BARRIER, 1, 1)
+    IPM_LCASE(CL_EULER, 3, 1)
+    IPM_LCASE(CL_EULER, 4, 1)
+    IPM_LCASE(CL_EULER, 4, 2)
+    IPM_LCASE(CL_EULER, 4, 3)
+#undef IPM_LCASE
+  }
+  return -1;
+}
+
 // cells -> per-level lists (warp-aggregated atomics; the order inside a list is irrelevant: every
 // cell's solve is independent of the others)
 __global__ void k_bucket(const int32_t* __restrict__ level, int64_t cells, int32_t* __restrict__ lists,
@@ -1312,16 +1366,18 @@ static int launch_dual_bucketed(const KernelCtx& k, const DualLaunch& a) {
     al.queue = &k.sc->lvl_queue[l];
     al.row = k.T.N * k.m;
     const int SF = (k.T.p == 2 && k.sumfact) ? (int)std::lround((std::sqrt(8.0 * kl.T.npr + 1) - 1) / 2) : 0;
-    const int rc = dual_mma_dispatch(kl, al, SF);
+    const int rc = k.hessian_kind == 1 ? dual_lbfgs_dispatch(kl, al) : dual_mma_dispatch(kl, al, SF);
     if (rc) return rc;
   }
-  g_last_dual = "k_dual_mma";
+  g_last_dual = k.hessian_kind == 1 ? "k_dual_lbfgs" : "k_dual_mma";
   return (int)cudaGetLastError();
 }
 
 int launch_dual(const KernelCtx& k, const DualLaunch& a) {
   if (a.cells == 0) return 0;
-  if (k.bucket && a.level && !a.list && !k.force_warp_kernel && !k.dual_group) return launch_dual_bucketed(k, a);
+  if (k.hessian_kind == 1 && !(k.bucket && a.level && !a.list)) return dual_lbfgs_dispatch(k, a);
+  if (k.bucket && a.level && !a.list && (k.hessian_kind == 1 || (!k.force_warp_kernel && !k.dual_group)))
+    return launch_dual_bucketed(k, a);
   // default: the DMMA-Cholesky kernel where it is instantiated; IPM_DUAL_KERNEL=group selects the
   // 4x4-register-block kernel (comparison, tests)
   if (!k.force_warp_kernel && !k.dual_group) {
@@ -1458,7 +1514,8 @@ const char* last_flux_kernel() { return g_last_flux; }
 int launch_flux(const KernelCtx& k, const FluxLaunch& a) {
   if (k.mesh.cells <= a.cell0) return 0;
   const int key = (k.flux * 10 + k.m) * 10 + k.mesh.kind;
-  const bool banded = a.uq_halo != nullptr;  // banded node states: the cell-range kernel only
+  // banded node states, or per-level rules (reading 36): the cell-range kernel only
+  const bool banded = a.uq_halo != nullptr || k.ad.lq.on;
   if (k.flux_choice == 0 && !banded) {
 #ifndef IPM_STRIP_NT
 #define IPM_STRIP_NT 512

@@ -30,7 +30,7 @@ EXPORTS = [
     "ipm_moments_from_dual", "ipm_stress_dual", "ipm_get_levels", "ipm_set_levels", "ipm_last_cell_stats",
     "ipm_get_time", "ipm_set_time", "ipm_last_kernel_ms", "ipm_enable_timing", "ipm_last_dual_kernel", "ipm_last_flux_kernel", "ipm_struct_size", "ipm_retard_stage", "ipm_retard_advance",
     "ipm_debug_phase_cycles", "ipm_step_dual", "ipm_step_flux", "ipm_halo_layout", "ipm_partition_query",
-    "ipm_get_status", "ipm_last_cell_linesearch", "ipm_node_band_rows",
+    "ipm_get_status", "ipm_last_cell_linesearch", "ipm_node_band_rows", "ipm_lbfgs_reset", "ipm_lbfgs_history",
 ]
 HIST_BUCKETS = 16  # IPM_HIST_BUCKETS
 
@@ -64,6 +64,8 @@ class ipm_config(C.Structure):
         ("reserved_ptr", C.c_void_p), ("stream", C.c_void_p),
         ("n_retard", C.c_int32), ("retard_level", C.c_int32 * 8), ("retard_eps", C.c_double * 8),
         ("quad_kind", C.c_int32), ("quad_level", C.c_int32),
+        ("hessian_kind", C.c_int32), ("lbfgs_m", C.c_int32),
+        ("level_q1d", C.c_int32 * 8),
     ]
 
 
@@ -134,6 +136,8 @@ def lib():
             "ipm_get_status": (st, [P, C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
             "ipm_last_cell_linesearch": (st, [P, I, I]),
             "ipm_node_band_rows": (st, [P, C.POINTER(C.c_int64)]),
+            "ipm_lbfgs_reset": (st, [P]),
+            "ipm_lbfgs_history": (st, [P, P, P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -242,6 +246,12 @@ def make_config(cfg: dict, mesh_arrays=None, rank=0, nranks=1, px=1, py=1):
     c.delta_dec, c.delta_inc = cfg.get("delta_dec", 0.0), cfg.get("delta_inc", 0.0)
     c.quad_kind = {"gl": 0, "cc": 1, "smolyak": 2}[cfg.get("quad", "gl")]  # quadrature (reading 33)
     c.quad_level = cfg.get("quad_level", 0)
+    # dual-solve direction (reading 35): "newton" exact Hessian (default), "lbfgs" limited-memory BFGS
+    c.hessian_kind = {"newton": 0, "lbfgs": 1}[cfg.get("hessian", "newton")]
+    c.lbfgs_m = cfg.get("lbfgs_m", 8)
+    # per-level nested Clenshaw-Curtis rules (reading 36)
+    for k, q in enumerate(cfg.get("level_q1d") or []):
+        c.level_q1d[k] = q
     retard = cfg.get("retard") or []  # refinement retardation (Alg. 4): [(eps_l, level index cap), ...]
     c.n_retard = len(retard)
     for k, (eps, lv) in enumerate(retard):
@@ -353,6 +363,19 @@ class Context:
         w, n = C.c_int32(), C.c_int64()
         check(lib().ipm_get_status(self.h, C.byref(w), C.byref(n)), "ipm_get_status")
         return w.value, n.value
+
+    def lbfgs_reset(self):
+        """forget every cell's L-BFGS pairs (hessian="lbfgs" contexts)"""
+        check(lib().ipm_lbfgs_reset(self.h), "ipm_lbfgs_reset")
+
+    def lbfgs_history(self):
+        """(S, Y [cells][lbfgs_m][N m], count [cells]) of the L-BFGS pairs, newest first"""
+        mh = self.cfg.get("lbfgs_m", 8)
+        S = self.zeros(self.cells, mh, self.N * self.m)
+        Y = self.zeros(self.cells, mh, self.N * self.m)
+        cnt = self.zeros(self.cells, dtype=self.torch.int32)
+        check(lib().ipm_lbfgs_history(self.h, _ptr(S), _ptr(Y), _ptr(cnt)), "ipm_lbfgs_history")
+        return S, Y, cnt
 
     def last_cell_linesearch(self):
         """per-cell (rejected Armijo trials, inadmissible trials) of the last dual solve"""

@@ -53,7 +53,8 @@ int main(void) {{
   O(ipm_config, delta_dec); O(ipm_config, rank); O(ipm_config, reserved_ptr); O(ipm_config, stream);
   O(ipm_ic, xs0); O(ipm_ic, state); O(ipm_step_info, newton_iters); O(ipm_step_info, worst_status);
   O(ipm_config, n_retard); O(ipm_config, retard_level); O(ipm_config, retard_eps); O(ipm_config, quad_kind);
-  O(ipm_config, quad_level);
+  O(ipm_config, quad_level); O(ipm_config, hessian_kind); O(ipm_config, lbfgs_m);
+  O(ipm_config, level_q1d);
   return 0;
 }}
 """)

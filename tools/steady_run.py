@@ -30,10 +30,16 @@ def main():
     ap.add_argument("--max-seconds", type=float, default=1500.0)
     ap.add_argument("--every", type=int, default=2000)
     ap.add_argument("--no-adaptive", action="store_true")
+    ap.add_argument("--pts", default="", help="mesh points NXxNY of the bump channel (default: BASELINE 548x183)")
+    ap.add_argument("--hessian", default="newton", choices=["newton", "lbfgs"])
     args = ap.parse_args()
     cfg = configs.get(args.config)
     if args.no_adaptive:
         cfg.pop("levels", None)
+    if args.pts:
+        nxp, nyp = (int(v) for v in args.pts.split("x"))
+        cfg["mesh"].update(nx_pts=nxp, ny_pts=nyp)
+    cfg["hessian"] = args.hessian
     m = cfg["mesh"]
     g = Context(cfg, bump_channel_mesh(m["nx_pts"], m["ny_pts"], m["seed"]))
     uhat = g.zeros()
@@ -64,7 +70,7 @@ def main():
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     rho = uhat[:, 0, 0]
-    print(json.dumps({"summary": True, "config": args.config, "cells": g.cells, "steps": n, "converged": drop <= args.drop,
+    print(json.dumps({"summary": True, "config": args.config, "hessian": args.hessian, "cells": g.cells, "steps": n, "converged": drop <= args.drop,
                       "residual_drop": drop, "target_drop": args.drop, "wall_s": wall,
                       "cell_steps_per_s": g.cells * n / wall, "adaptive": bool(g.cfg.get("levels")),
                       "mean_rho0": float(rho.mean()), "min_rho0": float(rho.min())}), flush=True)
