@@ -144,8 +144,9 @@ typedef struct {
    *     size changed starts without pairs), initial matrix I_N (x) Jbar^{-1}, Jbar = sum_k omega_k
    *     grad u_s(Lambda_k); the pairs occupy 2 lbfgs_m N m doubles per cell of device memory.
    *     Supported: lbfgs_m = 8 (0 selects 8), n = N m <= 96.  Same line search, stopping test, counts
-   *     (accepted steps) and statuses as Newton, with at most 4 max_newton steps (superlinear, not
-   *     quadratic convergence); IPM_CELL_ILLCONDITIONED = Jbar not positive definite. */
+   *     (accepted steps) and statuses as Newton; a cell not converged after max_newton quasi-Newton
+   *     steps continues with at most max_newton exact Newton steps from its iterate (its count is the
+   *     sum, its pairs are dropped); IPM_CELL_ILLCONDITIONED = Jbar not positive definite. */
   int32_t hessian_kind, lbfgs_m;
   /* per-level nested quadrature (reading 36; PAPER.md:385-398 and 625,
    * "Order 2 uses 5 quadrature points, orders 3 to 6 use 9"): level_q1d[0] > 0 gives adaptive level l

@@ -818,7 +818,8 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
     c->d_lbR = dalloc<double>(nc * mh, c->owned);
     c->d_lbC = dalloc<int32_t>(nc, c->owned);
     c->d_lbN = dalloc<int32_t>(nc, c->owned);
-    if (!c->d_lbS || !c->d_lbY || !c->d_lbR || !c->d_lbC || !c->d_lbN ||
+    k.fb_lists = dalloc<int32_t>(nc * (size_t)std::max(1, C.n_levels), c->owned);
+    if (!c->d_lbS || !c->d_lbY || !c->d_lbR || !c->d_lbC || !c->d_lbN || !k.fb_lists ||
         cudaMemset(c->d_lbC, 0, nc * 4) != cudaSuccess || cudaMemset(c->d_lbN, 0, nc * 4) != cudaSuccess) {
       ipm_destroy(c);
       return fail(IPM_ERR_CUDA, "cudaMalloc (L-BFGS history) failed");

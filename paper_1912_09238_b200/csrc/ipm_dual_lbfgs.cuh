@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(IPM_LBFGS_THREADS, 1) k_dual_lbfgs(DualParams 
         scale = sv1 + dv1;
         // ---- a7: stopping tests ---------------------------------------------------------------------
         if (crit < P.nw.tau || (P.nw.mode == 1 && l == 1)) break;
-        if (l == 4 * P.nw.max_newton) {  // reading 35: 4 max_newton quasi-Newton steps
+        if (l == P.nw.max_newton) {  // reading 35: Newton takes over (fallback pass)
           status = 1;
           break;
         }
@@ -417,19 +417,30 @@ __global__ void __launch_bounds__(IPM_LBFGS_THREADS, 1) k_dual_lbfgs(DualParams 
         }
       }
       if (lane == 0) {
-        A.lb_cnt[cell] = cnt;
+        A.lb_cnt[cell] = (status == 1 && A.fb_list != nullptr) ? 0 : cnt;
         A.lb_n[cell] = n;
       }
     }
+    // reading 35: a cell at max_newton quasi-Newton steps goes to the Newton fallback pass, which does
+    // its accounting (counts add up there) and its node states / CFL rate; its pairs are dropped
+    const bool handoff = status == 1 && A.fb_list != nullptr;
     if (lane == 0) {
-      cell_stats(A, P.sc, cell, l, status, hv, ia, crit);
-      my_iters += l;
-      if (status != 0) {
-        my_failed += 1;
-        my_worst = max(my_worst, status);
+      if (handoff) {
+        if (A.iters) A.iters[cell] = l;
+        if (A.halv) A.halv[cell] = hv;
+        if (A.inadm) A.inadm[cell] = ia;
+        A.lb_cnt[cell] = 0;
+        A.fb_list[atomicAdd(A.fb_count, 1)] = (int32_t)cell;
+      } else {
+        cell_stats(A, P.sc, cell, l, status, hv, ia, crit);
+        if (status != 0) {
+          my_failed += 1;
+          my_worst = max(my_worst, status);
+        }
       }
+      my_iters += l;
     }
-    for (int k = lane; k < Q; k += 32) {  // node states at the final iterate (variant B)
+    for (int k = lane; k < Q && !handoff; k += 32) {  // node states at the final iterate (variant B)
       double u[MS];
 #pragma unroll
       for (int a = 0; a < MS; ++a) u[a] = nb[a * Q + k];

@@ -88,6 +88,8 @@ struct StepScalars {
   unsigned long long halvings, inadm_trials;
   // adaptive degree in uniform-degree buckets: cells per level, and a work queue per level's launch
   int lvl_count[8], lvl_queue[8];
+  // reading 35: cells of the quasi-Newton pass handed to the Newton fallback, per level, and its queues
+  int fb_count[8], fb_queue[8];
 };
 constexpr int kHistBuckets = 16;
 
@@ -117,6 +119,12 @@ struct DualLaunch {
   double* lb_rho;   // [cells][lbfgs_m]  1 / (s^T y)
   int32_t* lb_cnt;  // [cells] stored pairs
   int32_t* lb_n;    // [cells] unknowns the pairs belong to
+  // reading 35's Newton fallback: k_dual_lbfgs appends the cells that reach max_newton quasi-Newton
+  // steps to fb_list (device count fb_count) and leaves their accounting to the Newton pass over that
+  // list, which runs with accumulate = 1 (per-cell counts and line-search records add up)
+  int32_t* fb_list;
+  int* fb_count;
+  int accumulate;
 };
 
 struct FluxLaunch {
@@ -163,6 +171,7 @@ struct KernelCtx {
   // tables (N_l, its 1D pair table, tile counts; Phi / omega Phi shared by prefix) and cell lists
   int hessian_kind;       // 0 exact Newton (Hessian + Cholesky), 1 L-BFGS (k_dual_lbfgs, reading 35)
   int lbfgs_m;            // L-BFGS pairs per cell
+  int32_t* fb_lists;      // [max(1, n_levels)][cells] Newton-fallback cell lists (hessian_kind 1)
   int bucket;             // 1: one k_dual_mma launch per level over that level's cells
   Tables Tl[8];
   int32_t* lists;         // [n_levels][cells]

@@ -229,6 +229,11 @@ __device__ __forceinline__ int retard_cap(const Adapt& ad, const StepScalars* sc
 // histogram and line-search counters (ipm_step_info)
 __device__ __forceinline__ void cell_stats(const DualLaunch& A, StepScalars* sc, int64_t cell, int l, int status,
                                            int hv, int ia, double crit) {
+  if (A.accumulate) {  // Newton fallback of reading 35: totals over both passes
+    if (A.iters) l += A.iters[cell];
+    if (A.halv) hv += A.halv[cell];
+    if (A.inadm) ia += A.inadm[cell];
+  }
   if (A.iters) A.iters[cell] = l;
   if (A.status) A.status[cell] = status;
   if (A.crit) A.crit[cell] = crit;
@@ -440,14 +445,20 @@ __global__ void __launch_bounds__(256) k_flux_warp(FluxParams P) {
   extern __shared__ __align__(16) double sm[];
   const int N = P.T.N, Q = P.T.Q, QP = P.T.QP;
   // basis table staged in shared memory when it fits (P.tables_in_smem), else read from L2
-  const double* sWPhiT = P.tables_in_smem ? sm : P.T.WPhiT;
-  if (P.tables_in_smem) {
+  // tables_in_smem: 1 omega Phi^T [N][QP] (scalar projection: per-level rules), 2 its A-fragment copy
+  // [MT][KS][32] (DMMA projection), 0 neither fits (read from L2)
+  const double* sWPhiT = P.tables_in_smem == 1 ? sm : P.T.WPhiT;
+  const int tabd = P.tables_in_smem == 1 ? N * QP : (P.tables_in_smem == 2 ? P.T.MT * P.T.KS * 32 : 0);
+  if (P.tables_in_smem == 1) {
     for (int t = threadIdx.x; t < N * QP; t += blockDim.x) sm[t] = P.T.WPhiT[t];
+    __syncthreads();
+  } else if (P.tables_in_smem == 2) {
+    for (int t = threadIdx.x; t < tabd; t += blockDim.x) sm[t] = P.T.WPhiF[t];
     __syncthreads();
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
-  double* q = sm + (P.tables_in_smem ? N * QP : 0) + (size_t)warp * (Q * MS + 1);
+  double* q = sm + tabd + (size_t)warp * (Q * MS + 1);
   const int nmax = N * MS;
   const double dt = P.sc->dt;
   const double gam = P.cl.gamma;
@@ -543,6 +554,42 @@ __global__ void __launch_bounds__(256) k_flux_warp(FluxParams P) {
     const int Nnew = (P.ad.n_levels > 0 && A.level_new) ? P.ad.Nl[A.level_new[cell]] : N;
     const double* uo = A.uhat_old + cell * nmax;
     double* un_ = A.uhat_new + cell * nmax;
+    if (Lq < 0 && P.tables_in_smem != 1) {
+      // projection Phi^T (omega o q) on the fp64 tensor path: C[i][a] = sum_k (omega phi_i)(xi_k) q_a(xi_k),
+      // A = omega Phi^T in A-fragment order (shared memory when it fits, else L2), B = the q rows
+      const double* __restrict__ sWF = P.tables_in_smem == 2 ? sm : P.T.WPhiF;
+      const int KS = P.T.KS, MTl = (Nnew + 7) >> 3, bk = lane & 3, bn = lane >> 2;
+      const bool bval = bn < MS;
+      for (int mt = 0; mt < MTl; ++mt) {
+        double c0 = 0.0, c1 = 0.0;
+        const double* asrc = sWF + (size_t)mt * KS * 32 + lane;
+#pragma unroll 4
+        for (int ks = 0; ks < KS; ++ks) {
+          const int k = 4 * ks + bk;
+          const double bv = (bval && k < Q) ? q[k * MS + bn] : 0.0;
+          dmma884(c0, c1, asrc[(size_t)ks * 32], bv);
+        }
+        const int i = 8 * mt + (lane >> 2);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int a = 2 * (lane & 3) + e;
+          if (a < MS && i < Nnew) {
+            const int rr = i * MS + a;
+            const double old = uo[rr];
+            const double sres = e == 0 ? c0 : c1;
+            const double out = (A.update_form == 1) ? sres : old - dt * sres;
+            un_[rr] = out;
+            if (rr == 0) my_res += P.mesh.area[cell] * fabs(out - old);
+          }
+        }
+      }
+      for (int rr = Nnew * MS + lane; rr < nmax; rr += 32) {
+        un_[rr] = 0.0;
+        if (A.lam) A.lam[cell * nmax + rr] = 0.0;  // duals truncated to the new level (Alg. 3)
+      }
+      __syncwarp();
+      continue;
+    }
     for (int rr = lane; rr < nmax; rr += 32) {
       const int i = rr / MS, a = rr - i * MS;
       const double old = uo[rr];  // uhat_new may alias uhat_old (only this cell's entries are read)
@@ -1046,6 +1093,64 @@ __global__ void k_nodes(Tables T, Mesh mesh, ClParams cp, const double* __restri
   }
 }
 
+// node states only (no h(lambda)): u_s(Phi lambda) of C cells per warp written straight to uq
+// [cell][state][node] — no per-warp node buffer (config 5: Q (m + m(m+1)/2) doubles = 120 KB per warp
+// left k_nodes one warp per SM), each basis value read once for the C cells.  Same fma order over i as
+// the dual kernels' node pass, so the states are bit-identical to the ones they write.
+template <int CL, int MS, int C>
+__global__ void __launch_bounds__(256) k_nodes_out(Tables T, Mesh mesh, ClParams cp, const double* __restrict__ lam_g,
+                                                   double* __restrict__ uq, StepScalars* sc, int tables_in_smem,
+                                                   int want_rate) {
+  extern __shared__ __align__(16) double sm[];
+  const int N = T.N, Q = T.Q, QP = T.QP, n = N * MS;
+  const double* sPhiT = tables_in_smem ? sm : T.PhiT;
+  if (tables_in_smem) {
+    for (int t = threadIdx.x; t < N * QP; t += blockDim.x) sm[t] = T.PhiT[t];
+    __syncthreads();
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  double* lam = sm + (tables_in_smem ? N * QP : 0) + (size_t)warp * (C * n);
+  double my_rate = 0.0;
+  int bad = 0;
+  for (int64_t c0 = ((int64_t)blockIdx.x * nw + warp) * C; c0 < mesh.cells; c0 += (int64_t)gridDim.x * nw * C) {
+    const int nc = (int)min((int64_t)C, mesh.cells - c0);
+    for (int r = lane; r < C * n; r += 32) lam[r] = (r < nc * n) ? lam_g[c0 * n + r] : 0.0;
+    __syncwarp();
+    for (int k = lane; k < Q; k += 32) {
+      double Lam[C][MS];
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+#pragma unroll
+        for (int a = 0; a < MS; ++a) Lam[c][a] = 0.0;
+#pragma unroll 2
+      for (int i = 0; i < N; ++i) {
+        const double ph = sPhiT[(size_t)i * QP + k];
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+#pragma unroll
+          for (int a = 0; a < MS; ++a) Lam[c][a] = fma(lam[c * n + i * MS + a], ph, Lam[c][a]);
+      }
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        if (c < nc) {
+          double u[MS], J[MS * (MS + 1) / 2], ss;
+          if (!Closure<CL, MS>::eval(Lam[c], u, J, ss, cp)) bad = 1;
+          double* o = uq + (c0 + c) * Q * MS + k;
+#pragma unroll
+          for (int a = 0; a < MS; ++a) o[a * Q] = u[a];
+          if (want_rate) my_rate = fmax(my_rate, node_rate<CL, MS>(u, mesh, c0 + c, cp.gamma));
+        }
+      }
+    }
+    __syncwarp();
+  }
+  my_rate = warp_max(my_rate);
+  if (lane == 0 && sc) {
+    if (want_rate) atomicMax(&sc->rate_bits, (unsigned long long)__double_as_longlong(my_rate));
+    if (bad) atomicMax(&sc->worst, 4);
+  }
+}
+
 // stress duals: lambda_0 = grad s(base); higher (rel|l0| + abs) 2^-|i| z; Euler: scale
 // higher modes so that max_k sum_{i>=1} lambda_{i,E} phi_i(xi_k) <= |lambda_{0,E}|/2
 template <int CL, int MS>
@@ -1354,6 +1459,7 @@ int dual_mma_dispatch(const KernelCtx& k, const DualLaunch& a, int SF);
 static int launch_dual_bucketed(const KernelCtx& k, const DualLaunch& a) {
   const int L = k.ad.n_levels;
   cudaMemsetAsync(&k.sc->lvl_count[0], 0, sizeof(int) * 16, S(k));
+  if (k.hessian_kind == 1) cudaMemsetAsync(&k.sc->fb_count[0], 0, sizeof(int) * 16, S(k));
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((a.cells + 255) / 256, (int64_t)k.sm_count * 8));
   k_bucket<<<grid, 256, 0, S(k)>>>(a.level, a.cells, k.lists, k.sc);
   for (int l = 0; l < L; ++l) {
@@ -1366,8 +1472,21 @@ static int launch_dual_bucketed(const KernelCtx& k, const DualLaunch& a) {
     al.queue = &k.sc->lvl_queue[l];
     al.row = k.T.N * k.m;
     const int SF = (k.T.p == 2 && k.sumfact) ? (int)std::lround((std::sqrt(8.0 * kl.T.npr + 1) - 1) / 2) : 0;
-    const int rc = k.hessian_kind == 1 ? dual_lbfgs_dispatch(kl, al) : dual_mma_dispatch(kl, al, SF);
-    if (rc) return rc;
+    if (k.hessian_kind == 1) {
+      al.fb_list = k.fb_lists + (int64_t)l * a.cells;
+      al.fb_count = &k.sc->fb_count[l];
+      if (const int rc = dual_lbfgs_dispatch(kl, al)) return rc;
+      // reading 35: Newton from the iterate for the cells that reached max_newton quasi-Newton steps
+      DualLaunch af = al;
+      af.list = al.fb_list;
+      af.ncells_dev = al.fb_count;
+      af.queue = &k.sc->fb_queue[l];
+      af.accumulate = 1;
+      af.fb_list = nullptr;
+      if (const int rc = dual_mma_dispatch(kl, af, SF)) return rc;
+    } else if (const int rc = dual_mma_dispatch(kl, al, SF)) {
+      return rc;
+    }
   }
   g_last_dual = k.hessian_kind == 1 ? "k_dual_lbfgs" : "k_dual_mma";
   return (int)cudaGetLastError();
@@ -1375,7 +1494,25 @@ static int launch_dual_bucketed(const KernelCtx& k, const DualLaunch& a) {
 
 int launch_dual(const KernelCtx& k, const DualLaunch& a) {
   if (a.cells == 0) return 0;
-  if (k.hessian_kind == 1 && !(k.bucket && a.level && !a.list)) return dual_lbfgs_dispatch(k, a);
+  if (k.hessian_kind == 1 && !(k.bucket && a.level && !a.list)) {
+    cudaMemsetAsync(&k.sc->fb_count[0], 0, sizeof(int) * 16, S(k));
+    DualLaunch al = a;
+    al.fb_list = k.fb_lists;
+    al.fb_count = &k.sc->fb_count[0];
+    if (const int rc = dual_lbfgs_dispatch(k, al)) return rc;
+    // reading 35: Newton from the iterate for the cells that reached max_newton quasi-Newton steps
+    DualLaunch af = a;
+    af.list = k.fb_lists;
+    af.ncells_dev = &k.sc->fb_count[0];
+    af.queue = &k.sc->fb_queue[0];
+    af.accumulate = 1;
+    af.row = a.row ? a.row : k.T.N * k.m;
+    const int SF = (k.T.p == 2 && k.sumfact) ? (int)std::lround((std::sqrt(8.0 * k.T.npr + 1) - 1) / 2) : 0;
+    int rc = (!k.force_warp_kernel && !k.dual_group) ? dual_mma_dispatch(k, af, SF) : -1;
+    if (rc == -1) return -1;  // (every L-BFGS shape has a k_dual_mma instance)
+    g_last_dual = "k_dual_lbfgs";
+    return rc;
+  }
   if (k.bucket && a.level && !a.list && (k.hessian_kind == 1 || (!k.force_warp_kernel && !k.dual_group)))
     return launch_dual_bucketed(k, a);
   // default: the DMMA-Cholesky kernel where it is instantiated; IPM_DUAL_KERNEL=group selects the
@@ -1449,8 +1586,12 @@ int launch_dual(const KernelCtx& k, const DualLaunch& a) {
 
 template <int FX, int MS, int MK>
 static int flux_impl(const KernelCtx& k, const FluxLaunch& a) {
-  const size_t tab = (size_t)k.T.N * k.T.QP * 8, pw = (size_t)(k.T.Q * MS + 1) * 8;
-  int in_smem = (tab + 4 * pw <= k.smem_optin) ? 1 : 0;
+  // per-level rules: the scalar projection with omega Phi^T (1); otherwise the DMMA projection with the
+  // A-fragment table (2), staged in shared memory when it fits next to 4 warps' buffers
+  const bool scalar = k.ad.lq.on || std::getenv("IPM_FLUX_SCALAR_PROJ");
+  const size_t tab = scalar ? (size_t)k.T.N * k.T.QP * 8 : (size_t)k.T.MT * k.T.KS * 32 * 8;
+  const size_t pw = (size_t)(k.T.Q * MS + 1) * 8;
+  int in_smem = (tab + 4 * pw <= k.smem_optin) ? (scalar ? 1 : 2) : 0;
   const size_t base = in_smem ? tab : 0;
   int warps = (int)std::min<size_t>(8, (k.smem_optin - base) / pw);
   if (warps < 1) return -1;
@@ -1654,6 +1795,19 @@ static int warm_impl(const KernelCtx& k, const double* uhat, double* lam) {
 
 template <int CL, int MS>
 static int nodes_impl(const KernelCtx& k, const double* lam, double* uhat, double* uq, int want_rate) {
+  if (!uhat && uq && !std::getenv("IPM_NODES_LEGACY")) {  // node states only: k_nodes_out
+    constexpr int C = (MS == 4) ? 4 : 2, W = 8;
+    const size_t tab = (size_t)k.T.N * k.T.QP * 8, pw = (size_t)C * k.T.N * MS * 8;
+    const int in_smem = (tab + W * pw <= k.smem_optin / 2) ? 1 : 0;  // (leave room for 2 CTAs per SM)
+    const size_t smem = (in_smem ? tab : 0) + W * pw;
+    auto kern = k_nodes_out<CL, MS, C>;
+    int per_sm = configure(kern, W * 32, smem);
+    if (per_sm < 1) return -1;
+    const int64_t want = (k.mesh.cells + W * C - 1) / (W * C);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)k.sm_count * per_sm));
+    kern<<<grid, W * 32, smem, S(k)>>>(k.T, k.mesh, k.cl, lam, uq, k.sc, in_smem, want_rate);
+    return (int)cudaGetLastError();
+  }
   using Lay = DualLayout<MS>;
   const size_t tab = (size_t)2 * k.T.N * k.T.QP * 8, pw = (size_t)(k.T.N * MS + k.T.Q * Lay::NS + 1) * 8;
   const int in_smem = (tab + 4 * pw <= k.smem_optin) ? 1 : 0;

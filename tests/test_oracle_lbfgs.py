@@ -182,3 +182,23 @@ def test_lbfgs_run_matches_newton_run(oracle_mod):
     un, _, inn = on.run(t_end=0.02, record=True)
     assert ib["steps"] == inn["steps"]
     np.testing.assert_allclose(ub, un, rtol=0, atol=1e-8 * np.abs(un[:, 0]).max())
+
+
+def test_newton_fallback_after_max_quasi_newton_steps(oracle_mod):
+    # reading 35: with the quasi-Newton cap at 3 steps most stress cells hand over to Newton; every
+    # cell still converges, to the Newton minimiser, its count is the sum and its pairs are dropped
+    cfg = configs.get("cfg3", mesh=dict(nx=4, ny=3), hessian="lbfgs", max_newton=3)
+    o = oracle_mod.Oracle(cfg)
+    on, _ = _cfg3(oracle_mod, "newton")
+    lam_s = _stress(o, cfg)
+    uhat = o.moments_from_dual_all(lam_s)
+    lam, lam_n = o.warm_start(uhat), on.warm_start(uhat)
+    it, st, cr = o.dual_solve_all(uhat, lam)
+    it_n, st_n, _ = on.dual_solve_all(uhat, lam_n)
+    assert (st == 0).all() and (cr < 1e-10).all()
+    handed = it > 3
+    assert handed.mean() > 0.5 and (it <= 3 + 3).all()
+    for j in np.nonzero(handed)[0]:
+        assert len(o.lbfgs_history(j)[0]) == 0
+    scale = np.abs(lam_s).max(axis=(0, 1))
+    assert (np.abs(lam - lam_n).max(axis=(0, 1)) / scale).max() < 1e-8
