@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--e2e-max-gb", type=float, default=16.0, help="largest state (uhat + lambda) the e2e leg pins")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=9238)
+    ap.add_argument("--no-alt", action="store_true", help="skip the L-BFGS comparison line (N=1, Newton runs)")
     ap.add_argument("--hessian", default="newton", choices=["newton", "lbfgs"],
                     help="dual-solve direction: exact Newton (the paper's method, default) or L-BFGS "
                          "(reading 35, SURVEY 8(f) NEXT-4)")
@@ -517,10 +518,69 @@ def run_ours(args):
             "gpu_launches": (4 if world == 1 else 6) * args.steps,
             "clocks": clk.summary(),
         }
+    if line is not None and world == 1 and args.hessian == "newton" and not args.no_alt:
+        del uhat, lam
+        torch.cuda.empty_cache()
+        line["lbfgs"] = run_alt_lbfgs(args, cfg, ma, dev)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return line
+
+
+def run_alt_lbfgs(args, cfg, ma, dev):
+    """The same workload, warm-up and timed steps with the quasi-Newton dual solve (reading 35,
+    SURVEY 8(f) NEXT-4: L-BFGS directions instead of the exact Hessian): a comparison line, not the
+    headline (the paper's method is Newton).  Same stress state, same device timing."""
+    import torch
+
+    from inputs.generators import STRESS_AMP, stress_state
+    from paper_1912_09238_b200 import Context
+
+    c2 = dict(cfg, hessian="lbfgs")
+    try:
+        g = Context(c2, ma)
+    except Exception as e:  # (configurations the quasi-Newton kernels do not cover)
+        return {"skipped": str(e)[:200]}
+    kind = stress_kind(cfg)
+    base, z = stress_state(kind, centres(cfg, ma), g.N, g.m, args.seed, cfg.get("gamma", 1.4))
+    amp = STRESS_AMP[kind]
+    lam = g.zeros()
+    g.ipm_stress_dual(torch.from_numpy(base).to(dev), torch.from_numpy(z).to(dev), amp[0], amp[1], lam)
+    uhat = g.zeros()
+    g.ipm_moments_from_dual(lam, uhat)
+    g.ipm_warm_start(uhat, lam)
+    g.enable_timing(True)
+    for _ in range(args.warmup):
+        g.ipm_step(uhat, lam, None, sync=False)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = g.cells * (g.Q * g.m + 2 * g.N * g.m) * 8 < 2 * l2
+    fbuf = torch.empty(2 * l2 // 4, dtype=torch.int32, device=dev) if flush else None
+    ms, iters, failed, dual_ms, flux_ms = 0.0, 0, 0, [], []
+    for k in range(args.steps):
+        if flush:
+            fbuf.fill_(k)
+        e0.record(stream)
+        info = g.ipm_step(uhat, lam, None, sync=True)
+        e1.record(stream)
+        e1.synchronize()
+        ms += e0.elapsed_time(e1)
+        iters += info.newton_iters
+        failed += info.failed_cells
+        d, f = g.last_kernel_ms()
+        dual_ms.append(d)
+        flux_ms.append(f)
+    N, m, Q = g.N, g.m, g.Q
+    dual_avg = float(np.mean(dual_ms))
+    flops = iters / args.steps * flops_lbfgs_per_iteration(N, m, Q) + g.cells * flops_initial(N, m, Q)
+    return {"hessian": "lbfgs", "what": "quasi-Newton dual solve (reading 35, PAPER.md:843), same workload and steps",
+            "value": g.cells * args.steps / (ms / 1e3), "unit": "cell-steps/s", "ms_per_step": ms / args.steps,
+            "newton_iters_per_cell_step": iters / (g.cells * args.steps), "failed_cells": int(failed),
+            "kernel": Context.last_dual_kernel(), "dual_ms_avg": dual_avg, "flux_ms_avg": float(np.mean(flux_ms)),
+            "dual_tflops": flops / (dual_avg / 1e3) / 1e12}
 
 
 def main():

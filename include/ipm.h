@@ -143,7 +143,8 @@ typedef struct {
    *     (s, y) of accepted iterates, kept in the context across (pseudo-)time steps (a cell whose basis
    *     size changed starts without pairs), initial matrix I_N (x) Jbar^{-1}, Jbar = sum_k omega_k
    *     grad u_s(Lambda_k); the pairs occupy 2 lbfgs_m N m doubles per cell of device memory.
-   *     Supported: lbfgs_m = 8 (0 selects 8), n = N m <= 96.  Same line search, stopping test, counts
+   *     Supported: lbfgs_m = 8 (0 selects 8), n = N m <= 96, or Euler 2D cells of a 3D tensor Gauss-Legendre
+   *     rule without levels with n <= 256 (config 5: CTA per cell, sum-factorised node pass).  Same line search, stopping test, counts
    *     (accepted steps) and statuses as Newton; a cell not converged after max_newton quasi-Newton
    *     steps continues with at most max_newton exact Newton steps from its iterate (its count is the
    *     sum, its pairs are dropped); IPM_CELL_ILLCONDITIONED = Jbar not positive definite. */

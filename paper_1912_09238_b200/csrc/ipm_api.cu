@@ -593,7 +593,23 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
 
   ipm::KernelCtx& k = c->k;
-  k.T = ipm::Tables{d_PhiT, d_WPhiT, d_omega, d_deg, N, Q, QP, p, d_LL, d_idx, tensor_gl ? C.q1d : 0, npr, d_WPhiF, MT, KS};
+  k.T = ipm::Tables{d_PhiT, d_WPhiT, d_omega, d_deg, N, Q, QP, p, d_LL, d_idx, tensor_gl ? C.q1d : 0, npr, d_WPhiF, MT, KS,
+                    nullptr, nullptr, 0};
+  // 1D tables of the tensor Gauss-Legendre rule (the large-cell quasi-Newton kernel's sum factorisation)
+  if (tensor_gl) {
+    std::vector<double> L1h((size_t)(C.M + 1) * C.q1d), w1hh(C.q1d);
+    for (int i = 0; i <= C.M; ++i)
+      for (int kq = 0; kq < C.q1d; ++kq) L1h[(size_t)i * C.q1d + kq] = legendre_orthonormal(i, x1[kq]);
+    for (int kq = 0; kq < C.q1d; ++kq) w1hh[kq] = 0.5 * w1[kq];
+    double *d_L1 = dalloc<double>(L1h.size(), O), *d_w1h = dalloc<double>(w1hh.size(), O);
+    if (!d_L1 || !d_w1h || up(d_L1, L1h.data(), L1h.size() * 8) || up(d_w1h, w1hh.data(), w1hh.size() * 8)) {
+      ipm_destroy(c);
+      return fail(IPM_ERR_CUDA, "1D table upload failed");
+    }
+    k.T.L1 = d_L1;
+    k.T.w1h = d_w1h;
+    k.T.npr1 = C.M + 1;
+  }
   k.mesh.kind = C.mesh_kind;
   k.mesh.F = F;
   k.mesh.cells = cells;
@@ -808,9 +824,11 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   k.hessian_kind = C.hessian_kind;
   k.lbfgs_m = C.lbfgs_m > 0 ? C.lbfgs_m : 8;
   if (C.hessian_kind == 1) {
-    if (k.lbfgs_m != 8 || N * m > 96) {
+    const bool big_ok = N * m <= 256 && p == 3 && tensor_gl && C.closure == IPM_CLOSURE_EULER && m == 4 && C.n_levels == 0;
+    if (k.lbfgs_m != 8 || (N * m > 96 && !big_ok)) {
       ipm_destroy(c);
-      return fail(IPM_ERR_UNSUPPORTED, "L-BFGS dual solve: lbfgs_m must be 8 and N m <= 96");
+      return fail(IPM_ERR_UNSUPPORTED, "L-BFGS dual solve: lbfgs_m must be 8 and N m <= 96 (or the 3D tensor-rule Euler "
+                                       "cells of config 5, N m <= 256)");
     }
     const size_t row = (size_t)N * m, mh = (size_t)k.lbfgs_m, nc = (size_t)std::max<int64_t>(cells, 1);
     c->d_lbS = dalloc<double>(nc * mh * row, c->owned);
@@ -931,7 +949,7 @@ static int halo_nodes(ipm_ctx* c, const double* d_recv) {
   ipm::KernelCtx kh = c->k;
   kh.mesh.cells = c->halo;
   double* dst = c->band_rows ? c->d_uq_halo : c->d_uq + (size_t)c->cells * c->Q * c->m;
-  return ipm::launch_nodes(kh, d_recv, nullptr, dst, 0);
+  return ipm::launch_nodes(kh, d_recv, nullptr, dst, 0, 1);
 }
 
 // the flux update over bands of rows (banded node states): per band, the node states of its rows and

@@ -337,11 +337,15 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
     return true;
   };
 
+  // cells from the work queue, or a device-built list (the Newton fallback of k_dual_lbfgs_big)
+  const int64_t ncells = A.ncells_dev ? (int64_t)*A.ncells_dev : A.cells;
+  int* const queue = A.queue ? A.queue : &P.sc->work_counter;
   for (;;) {
-    if (t == 0) ctl[0] = atomicAdd(&P.sc->work_counter, 1);
+    if (t == 0) ctl[0] = atomicAdd(queue, 1);
     __syncthreads();
-    const int64_t cell = ctl[0];
-    if (cell >= A.cells) break;
+    const int64_t ci = ctl[0];
+    if (ci >= ncells) break;
+    const int64_t cell = A.list ? (int64_t)A.list[ci] : ci;
     const int lvl = A.level ? A.level[cell] : 0;
     const int Nl = (P.ad.n_levels > 0) ? P.ad.Nl[lvl] : N;
     const int n = Nl * MS, NPl = Nl * (Nl + 1) / 2;

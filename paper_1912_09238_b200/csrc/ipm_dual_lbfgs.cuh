@@ -461,3 +461,393 @@ __global__ void __launch_bounds__(IPM_LBFGS_THREADS, 1) k_dual_lbfgs(DualParams 
     if (my_worst) atomicMax(&P.sc->worst, my_worst);
   }
 }
+
+// ---- large cells (config 5: N = 56, m = 4, n = 224, Q = 10^3, p = 3) -------------------------------------
+// The same quasi-Newton iteration (reading 35) with one CTA of NT threads per cell.  Thread t owns the
+// unknown r = t (n <= NT) and its MH pairs in registers.  The node pass and the gradient are
+// sum-factorised over the tensor Gauss-Legendre rule (the basis is a product of 1D orthonormal
+// Legendre polynomials, the weights a product of 1D weights):
+//   T1[i1 i2][k3] = sum_i3 lambda_(i1,i2,i3) L_i3(x_k3)      T2[i1][k2][k3] = sum_i2 T1[i1 i2][k3] L_i2(x_k2)
+//   Lambda(k1,k2,k3) = sum_i1 T2[i1][k2][k3] L_i1(x_k1)
+// and the transpose for g = Phi^T (omega o u) - uhat — about 35 k fmas each instead of 224 k, with
+// 1D tables in shared memory instead of the 448 KB Phi read from L2.  Everything per cell lives in
+// shared memory (~68 KB).  No adaptive levels (config 5 has none).
+template <int MS>
+struct LbfgsBigLayout {
+  // doubles: vectors [5][n], u [MS][Q], T1 [npr2][q][MS], T2 [M+1][q][q][MS], L1 [M+1][q], w1h [q],
+  // reductions [2][16][NW]; then ints: basis index of (i1, i2, i3) [(M+1)^3]
+  static __host__ __device__ int doubles(int n, int Q, int M, int q, int NW) {
+    const int npr2 = (M + 1) * (M + 2) / 2;
+    const int t1 = npr2 * q * MS, t2 = (M + 1) * q * q * MS;
+    return 5 * n + MS * Q + t1 + t2 + (M + 1) * q + q + 2 * 16 * NW + ((M + 1) * (M + 1) * (M + 1) + 1) / 2 + 8;
+  }
+};
+
+template <int CL, int MS, int MH, int NT>
+__global__ void __launch_bounds__(NT, 2) k_dual_lbfgs_big(DualParams P) {
+  extern __shared__ __align__(16) double sm[];
+  constexpr int MM = MS * (MS + 1) / 2, NW = NT / 32;
+  const int N = P.T.N, Q = P.T.Q, q = P.T.q1d, M = P.T.npr1 - 1;  // npr1 = M + 1 (1D degrees)
+  const int n = N * MS, npr2 = (M + 1) * (M + 2) / 2;
+  double* lam = sm;
+  double* lt = lam + n;
+  double* uh = lt + n;
+  double* g = uh + n;
+  double* qv = g + n;
+  double* u = qv + n;                      // [MS][Q]
+  double* T1 = u + MS * Q;                 // [npr2][q][MS]  (also R2 of the gradient)
+  double* T2 = T1 + npr2 * q * MS;         // [M+1][q][q][MS] (also R1)
+  double* L1 = T2 + (M + 1) * q * q * MS;  // [M+1][q]
+  double* w1h = L1 + (M + 1) * q;          // [q]
+  double* red = w1h + q;                   // [2][16][NW]
+  int* bidx = reinterpret_cast<int*>(red + 2 * 16 * NW);  // [(M+1)^3] -> basis index or -1
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  for (int x = t; x < (M + 1) * q; x += NT) L1[x] = P.T.L1[x];
+  for (int x = t; x < q; x += NT) w1h[x] = P.T.w1h[x];
+  for (int x = t; x < (M + 1) * (M + 1) * (M + 1); x += NT) bidx[x] = -1;
+  __syncthreads();
+  for (int i = t; i < N; i += NT) bidx[(P.T.idx[i * 3] * (M + 1) + P.T.idx[i * 3 + 1]) * (M + 1) + P.T.idx[i * 3 + 2]] = i;
+  __syncthreads();
+  // pair (i1, i2), i1 + i2 <= M, enumerated i1-major: offset of i1's row
+  auto prow = [&](int i1) { return i1 * (M + 1) - i1 * (i1 - 1) / 2; };
+  int slot = 0;
+  auto bsum = [&](double* v, int cnt) {  // block-wide sums of cnt (<= 16) values
+    double* r = red + slot * 16 * NW;
+    slot ^= 1;
+    for (int a = 0; a < cnt; ++a) {
+      const double s = warp_sum(v[a]);
+      if (lane == 0) r[a * NW + wid] = s;
+    }
+    __syncthreads();
+    for (int a = 0; a < cnt; ++a) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) s += r[a * NW + w];
+      v[a] = s;
+    }
+  };
+
+  const DualLaunch& A = P.a;
+  const int nmax = A.row ? A.row : n;
+  const int64_t ncells = A.ncells_dev ? (int64_t)*A.ncells_dev : A.cells;
+  int* const queue = A.queue ? A.queue : &P.sc->work_counter;
+  long long my_iters = 0, my_failed = 0;
+  int my_worst = 0;
+  double my_rate = 0.0;
+  __shared__ int s_ci;
+  for (;;) {
+    if (t == 0) s_ci = atomicAdd(queue, 1);
+    __syncthreads();
+    const int64_t ci = s_ci;
+    __syncthreads();
+    if (ci >= ncells) break;
+    const int64_t cell = A.list ? (int64_t)A.list[ci] : ci;
+    for (int r = t; r < n; r += NT) {
+      uh[r] = A.uhat[cell * nmax + r];
+      lam[r] = A.lam[cell * nmax + r];
+    }
+    int cnt = A.lb_cnt[cell];
+    if (A.lb_n[cell] != n) cnt = 0;
+    double S[MH], Y[MH], rho[MH];
+    const bool own = t < n;
+#pragma unroll
+    for (int i = 0; i < MH; ++i) {
+      rho[i] = (i < cnt) ? A.lb_rho[cell * MH + i] : 0.0;
+      S[i] = (i < cnt && own) ? A.lb_S[(cell * MH + i) * (int64_t)nmax + t] : 0.0;
+      Y[i] = (i < cnt && own) ? A.lb_Y[(cell * MH + i) * (int64_t)nmax + t] : 0.0;
+    }
+    __syncthreads();
+    int status = 0, l = 0, h = 0, mode = 0, hv = 0, ia = 0;
+    double crit = INFINITY, L0 = 0.0, scale = 0.0, slope = 0.0, alpha = 1.0, gold = 0.0, dreg = 0.0;
+    bool nb_is_lam = false;
+    for (;;) {
+      const double* x = (mode == 1) ? lt : lam;
+      // ---- a2 sum-factorised: stages A, B into T1, T2; stage C + closure per node ----------------------
+      for (int o = t; o < npr2 * q * MS; o += NT) {
+        const int a = o % MS, k3 = (o / MS) % q, pr = o / (MS * q);
+        int i1 = 0;
+        while (pr >= prow(i1 + 1)) ++i1;
+        const int i2 = pr - prow(i1);
+        double s = 0.0;
+        for (int i3 = 0; i3 <= M - i1 - i2; ++i3) {
+          const int bi = bidx[(i1 * (M + 1) + i2) * (M + 1) + i3];
+          s = fma(x[bi * MS + a], L1[i3 * q + k3], s);
+        }
+        T1[o] = s;
+      }
+      __syncthreads();
+      for (int o = t; o < (M + 1) * q * q * MS; o += NT) {
+        const int a = o % MS, k3 = (o / MS) % q, k2 = (o / (MS * q)) % q, i1 = o / (MS * q * q);
+        double s = 0.0;
+        for (int i2 = 0; i2 <= M - i1; ++i2) s = fma(T1[((prow(i1) + i2) * q + k3) * MS + a], L1[i2 * q + k2], s);
+        T2[o] = s;
+      }
+      __syncthreads();
+      double sv[2] = {0.0, 0.0}, jac[MM];
+#pragma unroll
+      for (int z = 0; z < MM; ++z) jac[z] = 0.0;
+      bool bad = false;
+      for (int k = t; k < Q; k += NT) {
+        const int k1 = k / (q * q), k23 = k - k1 * q * q;
+        double Lam[MS];
+#pragma unroll
+        for (int a = 0; a < MS; ++a) Lam[a] = 0.0;
+        for (int i1 = 0; i1 <= M; ++i1) {
+          const double lv = L1[i1 * q + k1];
+#pragma unroll
+          for (int a = 0; a < MS; ++a) Lam[a] = fma(T2[(i1 * q * q + k23) * MS + a], lv, Lam[a]);
+        }
+        double uk[MS], J[MM], ss;
+        if (!Closure<CL, MS>::eval(Lam, uk, J, ss, P.cl)) bad = true;
+#pragma unroll
+        for (int a = 0; a < MS; ++a) u[a * Q + k] = uk[a];
+        const double w = P.T.omega[k];
+#pragma unroll
+        for (int z = 0; z < MM; ++z) jac[z] = fma(w, J[z], jac[z]);
+        sv[0] = fma(w, ss, sv[0]);
+        sv[1] = fma(w, fabs(ss), sv[1]);
+      }
+      if (bad) sv[1] = INFINITY;
+      double red4[4] = {sv[0], sv[1], 0.0, 0.0};
+      if (own) {
+        const double v = x[t] * uh[t];
+        red4[2] = v;
+        red4[3] = fabs(v);
+      }
+      bsum(red4, 4);  // (its barrier also completes the node buffer)
+      if (mode == 2) {
+        nb_is_lam = true;
+        break;
+      }
+      const bool ok = isfinite(red4[0]) && isfinite(red4[1]);
+      const double Lt = red4[0] - red4[2];
+      bool accept;
+      if (mode == 0) {
+        if (!ok) {
+          status = 4;
+          break;
+        }
+        accept = true;
+      } else {
+        accept = ok && (Lt <= L0 + P.nw.armijo_c * alpha * slope + 1e-12 * scale);
+      }
+      bool finish = false;
+      if (accept) {
+        // ---- a3 sum-factorised: R1 (into T2), R2 (into T1), g ----------------------------------------
+        for (int o = t; o < (M + 1) * q * q * MS; o += NT) {
+          const int a = o % MS, k23 = (o / MS) % (q * q), i1 = o / (MS * q * q);
+          double s = 0.0;
+          for (int k1 = 0; k1 < q; ++k1) s = fma(w1h[k1] * L1[i1 * q + k1], u[a * Q + k1 * q * q + k23], s);
+          T2[o] = s;
+        }
+        __syncthreads();
+        for (int o = t; o < npr2 * q * MS; o += NT) {
+          const int a = o % MS, k3 = (o / MS) % q, pr = o / (MS * q);
+          int i1 = 0;
+          while (pr >= prow(i1 + 1)) ++i1;
+          const int i2 = pr - prow(i1);
+          double s = 0.0;
+          for (int k2 = 0; k2 < q; ++k2) s = fma(w1h[k2] * L1[i2 * q + k2], T2[((i1 * q + k2) * q + k3) * MS + a], s);
+          T1[o] = s;
+        }
+        __syncthreads();
+        double gr = 0.0;
+        if (own) {
+          const int i = t / MS, a = t - i * MS;
+          const int i1 = P.T.idx[i * 3], i2 = P.T.idx[i * 3 + 1], i3 = P.T.idx[i * 3 + 2];
+          double s = 0.0;
+          for (int k3 = 0; k3 < q; ++k3) s = fma(w1h[k3] * L1[i3 * q + k3], T1[((prow(i1) + i2) * q + k3) * MS + a], s);
+          gr = s - uh[t];
+          g[t] = gr;
+        }
+        double part[MS + 3];
+#pragma unroll
+        for (int a = 0; a < MS + 3; ++a) part[a] = 0.0;
+        if (own) {
+          const int a = t % MS;
+#pragma unroll
+          for (int b = 0; b < MS; ++b)
+            if (b == a) part[b] = gr * gr;
+        }
+        if (mode == 1) {  // accepted trial: the pair (reading 35), then lambda = trial
+          const double sn = own ? lt[t] - lam[t] : 0.0, yn = own ? gr - gold : 0.0;
+          part[MS] = sn * yn;
+          part[MS + 1] = sn * sn;
+          part[MS + 2] = yn * yn;
+          bsum(part, MS + 3);
+          if (part[MS] > 1e-10 * sqrt(part[MS + 1] * part[MS + 2])) {
+#pragma unroll
+            for (int i = MH - 1; i > 0; --i) {
+              rho[i] = rho[i - 1];
+              S[i] = S[i - 1];
+              Y[i] = Y[i - 1];
+            }
+            rho[0] = 1.0 / part[MS];
+            S[0] = sn;
+            Y[0] = yn;
+            cnt = cnt < MH ? cnt + 1 : MH;
+          }
+          if (own) lam[t] = lt[t];
+          ++l;
+        } else {
+          bsum(part, MS);
+        }
+        gold = gr;
+        crit = 0.0;
+#pragma unroll
+        for (int a = 0; a < MS; ++a) crit += sqrt(part[a]);
+        nb_is_lam = true;
+        L0 = Lt;
+        scale = red4[1] + red4[3];
+        if (crit < P.nw.tau || (P.nw.mode == 1 && l == 1)) break;
+        if (l == P.nw.max_newton) {  // reading 35: Newton takes over (fallback pass)
+          status = 1;
+          break;
+        }
+        // ---- L-BFGS direction: Jbar, two-loop recursion ----------------------------------------------
+        bsum(jac, MM);
+        double Lc[MS][MS];
+        bool spd = true;
+#pragma unroll
+        for (int j = 0; j < MS; ++j) {
+          double tt = jac[sym_idx<MS>(j, j)];
+#pragma unroll
+          for (int kk = 0; kk < j; ++kk) tt = fma(-Lc[j][kk], Lc[j][kk], tt);
+          if (!(tt > 0.0) || !isfinite(tt)) spd = false;
+          Lc[j][j] = sqrt(tt);
+          const double inv = 1.0 / Lc[j][j];
+#pragma unroll
+          for (int i = j + 1; i < MS; ++i) {
+            double v = jac[sym_idx<MS>(j, i)];
+#pragma unroll
+            for (int kk = 0; kk < j; ++kk) v = fma(-Lc[i][kk], Lc[j][kk], v);
+            Lc[i][j] = v * inv;
+          }
+        }
+        if (!spd) {
+          status = 2;
+          finish = true;
+        } else {
+          for (int pass = 0; pass < 2; ++pass) {
+            double qq = gr, al[MH];
+#pragma unroll
+            for (int i = 0; i < MH; ++i) {
+              al[i] = 0.0;
+              if (i < cnt) {
+                double tt[1] = {S[i] * qq};
+                bsum(tt, 1);
+                al[i] = rho[i] * tt[0];
+                qq = fma(-al[i], Y[i], qq);
+              }
+            }
+            if (own) qv[t] = qq;
+            __syncthreads();
+            double rv = 0.0;
+            if (own) {
+              const int i = t / MS, a = t - i * MS;
+              double y[MS], z[MS];
+#pragma unroll
+              for (int b = 0; b < MS; ++b) {
+                double v = qv[i * MS + b];
+#pragma unroll
+                for (int kk = 0; kk < b; ++kk) v = fma(-Lc[b][kk], y[kk], v);
+                y[b] = v / Lc[b][b];
+              }
+#pragma unroll
+              for (int b = MS - 1; b >= 0; --b) {
+                double v = y[b];
+#pragma unroll
+                for (int kk = b + 1; kk < MS; ++kk) v = fma(-Lc[kk][b], z[kk], v);
+                z[b] = v / Lc[b][b];
+              }
+#pragma unroll
+              for (int b = 0; b < MS; ++b)
+                if (b == a) rv = z[b];
+            }
+            qq = rv;
+#pragma unroll
+            for (int i = MH - 1; i >= 0; --i) {
+              if (i < cnt) {
+                double tt[1] = {Y[i] * qq};
+                bsum(tt, 1);
+                qq = fma(S[i], al[i] - rho[i] * tt[0], qq);
+              }
+            }
+            dreg = -qq;
+            double sl[1] = {own ? gr * dreg : 0.0};
+            bsum(sl, 1);
+            slope = sl[0];
+            if (slope < 0.0 || cnt == 0) break;
+            cnt = 0;  // not a descent direction (rounding): drop the history, H0 alone
+          }
+          alpha = 1.0;
+          h = 0;
+        }
+      } else {
+        nb_is_lam = false;
+        ++hv;
+        if (!ok) ++ia;
+        alpha *= 0.5;
+        if (++h > P.nw.max_halvings) {
+          status = 3;
+          finish = true;
+        }
+      }
+      if (finish) {
+        if (nb_is_lam) break;
+        mode = 2;
+      } else {
+        if (own) lt[t] = lam[t] + alpha * dreg;
+        mode = 1;
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    const bool handoff = status == 1 && A.fb_list != nullptr;
+    for (int r = t; r < nmax; r += NT) A.lam[cell * nmax + r] = (r < n) ? lam[r] : 0.0;
+#pragma unroll
+    for (int i = 0; i < MH; ++i)
+      if (i < cnt && own) {
+        A.lb_S[(cell * MH + i) * (int64_t)nmax + t] = S[i];
+        A.lb_Y[(cell * MH + i) * (int64_t)nmax + t] = Y[i];
+      }
+    if (t == 0) {
+      for (int i = 0; i < cnt; ++i) A.lb_rho[cell * MH + i] = rho[i];
+      A.lb_cnt[cell] = handoff ? 0 : cnt;
+      A.lb_n[cell] = n;
+      if (handoff) {
+        if (A.iters) A.iters[cell] = l;
+        if (A.halv) A.halv[cell] = hv;
+        if (A.inadm) A.inadm[cell] = ia;
+        A.fb_list[atomicAdd(A.fb_count, 1)] = (int32_t)cell;
+      } else {
+        cell_stats(A, P.sc, cell, l, status, hv, ia, crit);
+        if (status != 0) {
+          my_failed += 1;
+          my_worst = max(my_worst, status);
+        }
+      }
+      my_iters += l;
+    }
+    for (int k = t; k < Q && !handoff; k += NT) {  // node states at the final iterate
+      double uk[MS];
+#pragma unroll
+      for (int a = 0; a < MS; ++a) uk[a] = u[a * Q + k];
+      if (A.uq) {
+#pragma unroll
+        for (int a = 0; a < MS; ++a) A.uq[cell * Q * MS + a * Q + k] = uk[a];
+      }
+      if (A.want_rate) my_rate = fmax(my_rate, node_rate<CL, MS>(uk, P.mesh, cell, P.cl.gamma));
+    }
+    __syncthreads();
+  }
+  my_rate = warp_max(my_rate);
+  if (lane == 0) {
+    if (A.want_rate) atomicMax(&P.sc->rate_bits, (unsigned long long)__double_as_longlong(my_rate));
+    if (t == 0) {
+      if (my_iters) atomicAdd(&P.sc->newton_iters, (unsigned long long)my_iters);
+      if (my_failed) atomicAdd(&P.sc->failed, (unsigned long long)my_failed);
+      if (my_worst) atomicMax(&P.sc->worst, my_worst);
+    }
+  }
+}

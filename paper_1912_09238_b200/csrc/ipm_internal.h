@@ -27,6 +27,11 @@ struct Tables {
   //   omega_k phi_i(xi_k), i = 8 mt + l/4, k = 4 ks + l%4 (zero outside N x Q); MT = ceil(N/8), KS = ceil(Q/4)
   const double* WPhiF;
   int MT, KS;
+  // 1D tables of the tensor Gauss-Legendre rule (sum-factorised node pass of k_dual_lbfgs_big):
+  //   L1 [M+1][q1d] orthonormal Legendre L_i(x_k) = sqrt(2i+1) P_i(x_k),  w1h [q1d] = w_k / 2;  npr1 = M + 1
+  const double* L1;
+  const double* w1h;
+  int npr1;
 };
 
 // Local mesh: owned cells, face tables (F faces per cell)
@@ -198,7 +203,8 @@ int launch_project_ic(const KernelCtx& k, const double* d_region /*[R][Q][m]*/, 
 int launch_pack(const KernelCtx& k, const double* lam, const int32_t* idx, int64_t n, double* out);
 int launch_warm_start(const KernelCtx& k, const double* uhat, double* lam);
 // node pass: uhat = h(lambda) (nullable), node states uq (nullable), CFL rate into sc
-int launch_nodes(const KernelCtx& k, const double* lam, double* uhat, double* uq, int want_rate);
+// exact = 1: the dual kernels' node-pass instruction sequence (bit-identical states; halo cells)
+int launch_nodes(const KernelCtx& k, const double* lam, double* uhat, double* uq, int want_rate, int exact = 0);
 int launch_stress(const KernelCtx& k, const double* base, const double* z, double rel, double abs_, double* lam);
 
 }  // namespace ipm

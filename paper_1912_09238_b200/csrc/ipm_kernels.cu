@@ -1394,6 +1394,24 @@ int dual_mma_dispatch(const KernelCtx& k, const DualLaunch& a, int SF) {
 static const char* g_last_dual = "";
 const char* last_dual_kernel() { return g_last_dual; }
 
+// the large-cell Newton kernel (config 5): CTA per cell, L2-resident scratch; also the Newton fallback of
+// the large-cell quasi-Newton kernel (a.list)
+static int launch_big(const KernelCtx& k, const DualLaunch& a) {
+  if (!k.big_scratch || k.closure != CL_EULER || k.m != 4) return -1;
+  constexpr int NT = 512;
+  const size_t smem0 = ((size_t)5 * k.T.N * 4 + 8 * (NT / 32) + ((k.T.q1d * k.T.npr + 1) & ~1) + 8) * 8;
+  const size_t nb8 = (size_t)(k.T.N * 4 + 7) / 8;
+  const size_t hbl = (nb8 * (nb8 + 1) / 2 * 64 + 64) * 8;  // 8 x 8 blocks + Linv operand
+  const int hb_in_smem = (smem0 + hbl <= k.smem_optin) ? 1 : 0;
+  const size_t smem = smem0 + (hb_in_smem ? hbl : 0);
+  auto kern = hb_in_smem ? k_dual_big<CL_EULER, 4, NT, true> : k_dual_big<CL_EULER, 4, NT, false>;
+  configure(kern, 0, smem);
+  const int grid = (int)std::min<int64_t>(a.cells, (int64_t)k.big_ctas);
+  DualParams P{k.T, k.mesh, k.nw, k.ad, k.cl, a, k.sc};
+  kern<<<grid, NT, smem, S(k)>>>(P, k.big_scratch);
+  return (int)cudaGetLastError();
+}
+
 // quasi-Newton dual solve (reading 35): one warp per cell, as many warps per CTA as shared memory and
 // registers allow, one persistent CTA per SM
 template <int CL, int MS, int NR, int MH>
@@ -1419,6 +1437,20 @@ static int dual_lbfgs_impl(const KernelCtx& k, const DualLaunch& a) {
 static int dual_lbfgs_dispatch(const KernelCtx& k, const DualLaunch& a) {
   const int n = k.T.N * k.m, NR = (n + 31) / 32;
   if (k.lbfgs_m != 8) return -1;
+  if (n > 96) {  // large cells (config 5): CTA per cell, sum-factorised node pass over the 3D tensor rule
+    constexpr int NT = 256;
+    if (!(k.closure == CL_EULER && k.m == 4 && k.T.p == 3 && k.T.L1 && n <= NT && k.ad.n_levels == 0)) return -1;
+    const size_t smem = (size_t)LbfgsBigLayout<4>::doubles(n, k.T.Q, k.T.npr1 - 1, k.T.q1d, NT / 32) * 8;
+    if (smem > k.smem_optin) return -1;
+    auto kern = k_dual_lbfgs_big<CL_EULER, 4, 8, NT>;
+    int per_sm = configure(kern, NT, smem);
+    if (per_sm < 1) return -1;
+    const int grid = (int)std::min<int64_t>(a.cells, (int64_t)k.sm_count * per_sm);
+    DualParams P{k.T, k.mesh, k.nw, k.ad, k.cl, a, k.sc};
+    kern<<<std::max(grid, 1), NT, smem, S(k)>>>(P);
+    g_last_dual = "k_dual_lbfgs_big";
+    return (int)cudaGetLastError();
+  }
   switch ((k.closure * 10 + k.m) * 10 + NR) {
 #define IPM_LCASE(CLV, MSV, NRV) \
   case (CLV * 10 + MSV) * 10 + NRV: return dual_lbfgs_impl<CLV, MSV, NRV, 8>(k, a);
@@ -1507,10 +1539,15 @@ int launch_dual(const KernelCtx& k, const DualLaunch& a) {
     af.queue = &k.sc->fb_queue[0];
     af.accumulate = 1;
     af.row = a.row ? a.row : k.T.N * k.m;
-    const int SF = (k.T.p == 2 && k.sumfact) ? (int)std::lround((std::sqrt(8.0 * k.T.npr + 1) - 1) / 2) : 0;
-    int rc = (!k.force_warp_kernel && !k.dual_group) ? dual_mma_dispatch(k, af, SF) : -1;
-    if (rc == -1) return -1;  // (every L-BFGS shape has a k_dual_mma instance)
-    g_last_dual = "k_dual_lbfgs";
+    const char* qn = g_last_dual;
+    int rc;
+    if (k.T.N * k.m > 96) {
+      rc = launch_big(k, af);  // (k_dual_big: the Newton kernel of the large cells)
+    } else {
+      const int SF = (k.T.p == 2 && k.sumfact) ? (int)std::lround((std::sqrt(8.0 * k.T.npr + 1) - 1) / 2) : 0;
+      rc = dual_mma_dispatch(k, af, SF);  // (every warp-kernel L-BFGS shape has a k_dual_mma instance)
+    }
+    g_last_dual = qn;
     return rc;
   }
   if (k.bucket && a.level && !a.list && (k.hessian_kind == 1 || (!k.force_warp_kernel && !k.dual_group)))
@@ -1557,19 +1594,9 @@ int launch_dual(const KernelCtx& k, const DualLaunch& a) {
     }
     // cells too large for the on-chip group kernel (config 5): CTA per cell, L2-resident scratch
     if (k.big_scratch && k.closure == CL_EULER && k.m == 4) {
-      constexpr int NT = 512;
-      const size_t smem0 = ((size_t)5 * k.T.N * 4 + 8 * (NT / 32) + ((k.T.q1d * k.T.npr + 1) & ~1) + 8) * 8;
-      const size_t nb8 = (size_t)(k.T.N * 4 + 7) / 8;
-      const size_t hbl = (nb8 * (nb8 + 1) / 2 * 64 + 64) * 8;  // 8 x 8 blocks + Linv operand
-      const int hb_in_smem = (smem0 + hbl <= k.smem_optin) ? 1 : 0;
-      const size_t smem = smem0 + (hb_in_smem ? hbl : 0);
-      auto kern = hb_in_smem ? k_dual_big<CL_EULER, 4, NT, true> : k_dual_big<CL_EULER, 4, NT, false>;
-      configure(kern, 0, smem);
-      const int grid = (int)std::min<int64_t>(a.cells, (int64_t)k.big_ctas);
-      DualParams P{k.T, k.mesh, k.nw, k.ad, k.cl, a, k.sc};
-      kern<<<grid, NT, smem, S(k)>>>(P, k.big_scratch);
+      const int rc = launch_big(k, a);
       g_last_dual = "k_dual_big";
-      return (int)cudaGetLastError();
+      return rc;
     }
   }
   g_last_dual = "k_dual_warp";
@@ -1794,8 +1821,10 @@ static int warm_impl(const KernelCtx& k, const double* uhat, double* lam) {
 }
 
 template <int CL, int MS>
-static int nodes_impl(const KernelCtx& k, const double* lam, double* uhat, double* uq, int want_rate) {
-  if (!uhat && uq && !std::getenv("IPM_NODES_LEGACY")) {  // node states only: k_nodes_out
+static int nodes_impl(const KernelCtx& k, const double* lam, double* uhat, double* uq, int want_rate, int exact) {
+  // node states only: k_nodes_out; exact = 1 (halo cells of distributed contexts) keeps the dual
+  // kernels' instruction sequence (warp_eval), so a virtual-rank run equals one context bit for bit
+  if (!uhat && uq && !exact) {
     constexpr int C = (MS == 4) ? 4 : 2, W = 8;
     const size_t tab = (size_t)k.T.N * k.T.QP * 8, pw = (size_t)C * k.T.N * MS * 8;
     const int in_smem = (tab + W * pw <= k.smem_optin / 2) ? 1 : 0;  // (leave room for 2 CTAs per SM)
@@ -1845,8 +1874,8 @@ static int stress_impl(const KernelCtx& k, const double* base, const double* z, 
   return -1;
 
 int launch_warm_start(const KernelCtx& k, const double* uhat, double* lam) { IPM_DISPATCH_CL(warm_impl, uhat, lam) }
-int launch_nodes(const KernelCtx& k, const double* lam, double* uhat, double* uq, int want_rate) {
-  IPM_DISPATCH_CL(nodes_impl, lam, uhat, uq, want_rate)
+int launch_nodes(const KernelCtx& k, const double* lam, double* uhat, double* uq, int want_rate, int exact) {
+  IPM_DISPATCH_CL(nodes_impl, lam, uhat, uq, want_rate, exact)
 }
 
 __global__ void k_pack(const double* __restrict__ lam, const int32_t* __restrict__ idx, int64_t n, int row,
