@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(IPM_LBFGS_THREADS, 1) k_dual_lbfgs(DualParams 
 #pragma unroll
         for (int z = 0; z < MM; ++z) Jb[z] = warp_sum(jac[z]);
         // Cholesky of Jbar (m x m, every lane redundantly): Lc packed lower by rows
-        double Lc[MS][MS];
+        double Lc[MS][MS], Li[MS];  // Cholesky factor of Jbar and the reciprocals of its diagonal
         bool spd = true;
 #pragma unroll
         for (int j = 0; j < MS; ++j) {
@@ -273,6 +273,7 @@ __global__ void __launch_bounds__(IPM_LBFGS_THREADS, 1) k_dual_lbfgs(DualParams 
           if (!(t > 0.0) || !isfinite(t)) spd = false;
           Lc[j][j] = sqrt(t);
           const double inv = 1.0 / Lc[j][j];
+          Li[j] = inv;
 #pragma unroll
           for (int i = j + 1; i < MS; ++i) {
             double v = Jb[sym_idx<MS>(j, i)];
@@ -317,14 +318,14 @@ __global__ void __launch_bounds__(IPM_LBFGS_THREADS, 1) k_dual_lbfgs(DualParams 
                 double v = qv[i * MS + b];
 #pragma unroll
                 for (int k = 0; k < b; ++k) v = fma(-Lc[b][k], y[k], v);
-                y[b] = v / Lc[b][b];
+                y[b] = v * Li[b];
               }
 #pragma unroll
               for (int b = MS - 1; b >= 0; --b) {
                 double v = y[b];
 #pragma unroll
                 for (int k = b + 1; k < MS; ++k) v = fma(-Lc[k][b], z[k], v);
-                z[b] = v / Lc[b][b];
+                z[b] = v * Li[b];
               }
               double rv = 0.0;
 #pragma unroll
@@ -706,7 +707,7 @@ __global__ void __launch_bounds__(NT, 2) k_dual_lbfgs_big(DualParams P) {
         }
         // ---- L-BFGS direction: Jbar, two-loop recursion ----------------------------------------------
         bsum(jac, MM);
-        double Lc[MS][MS];
+        double Lc[MS][MS], Li[MS];  // Cholesky factor of Jbar and the reciprocals of its diagonal
         bool spd = true;
 #pragma unroll
         for (int j = 0; j < MS; ++j) {
@@ -716,6 +717,7 @@ __global__ void __launch_bounds__(NT, 2) k_dual_lbfgs_big(DualParams P) {
           if (!(tt > 0.0) || !isfinite(tt)) spd = false;
           Lc[j][j] = sqrt(tt);
           const double inv = 1.0 / Lc[j][j];
+          Li[j] = inv;
 #pragma unroll
           for (int i = j + 1; i < MS; ++i) {
             double v = jac[sym_idx<MS>(j, i)];
@@ -751,14 +753,14 @@ __global__ void __launch_bounds__(NT, 2) k_dual_lbfgs_big(DualParams P) {
                 double v = qv[i * MS + b];
 #pragma unroll
                 for (int kk = 0; kk < b; ++kk) v = fma(-Lc[b][kk], y[kk], v);
-                y[b] = v / Lc[b][b];
+                y[b] = v * Li[b];
               }
 #pragma unroll
               for (int b = MS - 1; b >= 0; --b) {
                 double v = y[b];
 #pragma unroll
                 for (int kk = b + 1; kk < MS; ++kk) v = fma(-Lc[kk][b], z[kk], v);
-                z[b] = v / Lc[b][b];
+                z[b] = v * Li[b];
               }
 #pragma unroll
               for (int b = 0; b < MS; ++b)
