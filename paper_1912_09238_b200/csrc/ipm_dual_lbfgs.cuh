@@ -480,7 +480,8 @@ struct LbfgsBigLayout {
   static __host__ __device__ int doubles(int n, int Q, int M, int q, int NW) {
     const int npr2 = (M + 1) * (M + 2) / 2;
     const int t1 = npr2 * q * MS, t2 = (M + 1) * q * q * MS;
-    return 5 * n + MS * Q + t1 + t2 + (M + 1) * q + q + 2 * 16 * NW + ((M + 1) * (M + 1) * (M + 1) + 1) / 2 + 8;
+    return 5 * n + MS * Q + t1 + t2 + (M + 1) * q + q + 2 * 16 * NW + ((M + 1) * (M + 1) * (M + 1) + 1) / 2 + 8 +
+           2 * 8 * n;  // + the pairs S, Y [MH <= 8][n]
   }
 };
 
@@ -502,6 +503,9 @@ __global__ void __launch_bounds__(NT, 2) k_dual_lbfgs_big(DualParams P) {
   double* w1h = L1 + (M + 1) * q;          // [q]
   double* red = w1h + q;                   // [2][16][NW]
   int* bidx = reinterpret_cast<int*>(red + 2 * 16 * NW);  // [(M+1)^3] -> basis index or -1
+  // the cell's pairs, newest first, column t owned by thread t (shared memory: registers would spill)
+  double* sS = red + 2 * 16 * NW + ((M + 1) * (M + 1) * (M + 1) + 1) / 2 + 8;  // [MH][n]
+  double* sY = sS + MH * n;
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   for (int x = t; x < (M + 1) * q; x += NT) L1[x] = P.T.L1[x];
   for (int x = t; x < q; x += NT) w1h[x] = P.T.w1h[x];
@@ -549,13 +553,15 @@ __global__ void __launch_bounds__(NT, 2) k_dual_lbfgs_big(DualParams P) {
     }
     int cnt = A.lb_cnt[cell];
     if (A.lb_n[cell] != n) cnt = 0;
-    double S[MH], Y[MH], rho[MH];
+    double rho[MH];
     const bool own = t < n;
 #pragma unroll
     for (int i = 0; i < MH; ++i) {
       rho[i] = (i < cnt) ? A.lb_rho[cell * MH + i] : 0.0;
-      S[i] = (i < cnt && own) ? A.lb_S[(cell * MH + i) * (int64_t)nmax + t] : 0.0;
-      Y[i] = (i < cnt && own) ? A.lb_Y[(cell * MH + i) * (int64_t)nmax + t] : 0.0;
+      if (own) {
+        sS[i * n + t] = (i < cnt) ? A.lb_S[(cell * MH + i) * (int64_t)nmax + t] : 0.0;
+        sY[i * n + t] = (i < cnt) ? A.lb_Y[(cell * MH + i) * (int64_t)nmax + t] : 0.0;
+      }
     }
     __syncthreads();
     int status = 0, l = 0, h = 0, mode = 0, hv = 0, ia = 0;
@@ -680,12 +686,16 @@ __global__ void __launch_bounds__(NT, 2) k_dual_lbfgs_big(DualParams P) {
 #pragma unroll
             for (int i = MH - 1; i > 0; --i) {
               rho[i] = rho[i - 1];
-              S[i] = S[i - 1];
-              Y[i] = Y[i - 1];
+              if (own) {
+                sS[i * n + t] = sS[(i - 1) * n + t];
+                sY[i * n + t] = sY[(i - 1) * n + t];
+              }
             }
             rho[0] = 1.0 / part[MS];
-            S[0] = sn;
-            Y[0] = yn;
+            if (own) {
+              sS[t] = sn;
+              sY[t] = yn;
+            }
             cnt = cnt < MH ? cnt + 1 : MH;
           }
           if (own) lam[t] = lt[t];
@@ -736,10 +746,10 @@ __global__ void __launch_bounds__(NT, 2) k_dual_lbfgs_big(DualParams P) {
             for (int i = 0; i < MH; ++i) {
               al[i] = 0.0;
               if (i < cnt) {
-                double tt[1] = {S[i] * qq};
+                double tt[1] = {own ? sS[i * n + t] * qq : 0.0};
                 bsum(tt, 1);
                 al[i] = rho[i] * tt[0];
-                qq = fma(-al[i], Y[i], qq);
+                if (own) qq = fma(-al[i], sY[i * n + t], qq);
               }
             }
             if (own) qv[t] = qq;
@@ -770,9 +780,9 @@ __global__ void __launch_bounds__(NT, 2) k_dual_lbfgs_big(DualParams P) {
 #pragma unroll
             for (int i = MH - 1; i >= 0; --i) {
               if (i < cnt) {
-                double tt[1] = {Y[i] * qq};
+                double tt[1] = {own ? sY[i * n + t] * qq : 0.0};
                 bsum(tt, 1);
-                qq = fma(S[i], al[i] - rho[i] * tt[0], qq);
+                if (own) qq = fma(sS[i * n + t], al[i] - rho[i] * tt[0], qq);
               }
             }
             dreg = -qq;
@@ -810,8 +820,8 @@ __global__ void __launch_bounds__(NT, 2) k_dual_lbfgs_big(DualParams P) {
 #pragma unroll
     for (int i = 0; i < MH; ++i)
       if (i < cnt && own) {
-        A.lb_S[(cell * MH + i) * (int64_t)nmax + t] = S[i];
-        A.lb_Y[(cell * MH + i) * (int64_t)nmax + t] = Y[i];
+        A.lb_S[(cell * MH + i) * (int64_t)nmax + t] = sS[i * n + t];
+        A.lb_Y[(cell * MH + i) * (int64_t)nmax + t] = sY[i * n + t];
       }
     if (t == 0) {
       for (int i = 0; i < cnt; ++i) A.lb_rho[cell * MH + i] = rho[i];

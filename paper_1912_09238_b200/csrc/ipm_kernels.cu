@@ -438,6 +438,7 @@ struct FluxParams {
   FluxLaunch a;
   StepScalars* sc;
   int tables_in_smem;
+  int qchunk;  // k_flux_warp, DMMA projection: nodes per chunk of the per-warp buffer (multiple of 4; 0 = Q)
 };
 
 template <int FX, int MS, int MK>
@@ -458,7 +459,10 @@ __global__ void __launch_bounds__(256) k_flux_warp(FluxParams P) {
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
-  double* q = sm + tabd + (size_t)warp * (Q * MS + 1);
+  // per-warp buffer of the nodes' residuals (or c-form states): the whole rule, or QB-node chunks that the
+  // DMMA projection consumes one after the other (config 5: Q = 1000 nodes, 32 KB per warp otherwise)
+  const int QB = (P.tables_in_smem != 1 && P.qchunk > 0 && N <= 64) ? P.qchunk : Q;
+  double* q = sm + tabd + (size_t)warp * (QB * MS + 1);
   const int nmax = N * MS;
   const double dt = P.sc->dt;
   const double gam = P.cl.gamma;
@@ -477,7 +481,17 @@ __global__ void __launch_bounds__(256) k_flux_warp(FluxParams P) {
     const int Lq = (P.ad.lq.on && A.level_new) ? A.level_new[cell] : -1;
     const int Qc = Lq >= 0 ? P.ad.lq.Q[Lq] : Q;
     const int32_t* __restrict__ kfc = Lq >= 0 ? P.ad.lq.kf[Lq] : nullptr;
-    for (int kq = lane; kq < Qc; kq += 32) {
+    const int Nnew = (P.ad.n_levels > 0 && A.level_new) ? P.ad.Nl[A.level_new[cell]] : N;
+    const bool mma = Lq < 0 && P.tables_in_smem != 1 && N <= 64;
+    const int QBc = mma ? QB : Qc;
+    // DMMA projection accumulators (row tiles mt < MTl <= 8: N <= 64)
+    const int MTl = (Nnew + 7) >> 3, bk = lane & 3, bn = lane >> 2;
+    double acc[8][2];
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+    for (int k0 = 0; k0 < Qc; k0 += QBc) {
+    const int k1 = min(Qc, k0 + QBc);
+    for (int kq = k0 + lane; kq < k1; kq += 32) {
       const int k = kfc ? kfc[kq] : kq;
       double uj[MS], r[MS], gneg[MS];
       const double* src = nodes_of(cell) + k;
@@ -541,7 +555,7 @@ __global__ void __launch_bounds__(256) k_flux_warp(FluxParams P) {
           for (int a = 0; a < MS; ++a) r[a] += (gpos[a] - gneg[a]) * cf;
         }
       }
-      double* qk = q + kq * MS;
+      double* qk = q + (kq - k0) * MS;
       if (A.update_form == 1) {
 #pragma unroll
         for (int a = 0; a < MS; ++a) qk[a] = uj[a] - dt * r[a];
@@ -551,24 +565,31 @@ __global__ void __launch_bounds__(256) k_flux_warp(FluxParams P) {
       }
     }
     __syncwarp();
-    const int Nnew = (P.ad.n_levels > 0 && A.level_new) ? P.ad.Nl[A.level_new[cell]] : N;
+    if (mma) {
+      // projection Phi^T (omega o q) on the fp64 tensor path, this chunk's k-steps: C[i][a] += sum_k
+      // (omega phi_i)(xi_k) q_a(xi_k), A = omega Phi^T in A-fragment order (shared memory when it fits,
+      // else L2), B = the chunk's q rows
+      const double* __restrict__ sWF = P.tables_in_smem == 2 ? sm : P.T.WPhiF;
+      const int KS = P.T.KS;
+      const bool bval = bn < MS;
+      for (int ks = k0 >> 2; ks < (k1 + 3) >> 2; ++ks) {
+        const int k = 4 * ks + bk;
+        const double bv = (bval && k < k1) ? q[(k - k0) * MS + bn] : 0.0;
+        const double* asrc = sWF + (size_t)ks * 32 + lane;
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt)
+          if (mt < MTl) dmma884(acc[mt][0], acc[mt][1], asrc[(size_t)mt * KS * 32], bv);
+      }
+      __syncwarp();
+    }
+    }  // node chunks
     const double* uo = A.uhat_old + cell * nmax;
     double* un_ = A.uhat_new + cell * nmax;
-    if (Lq < 0 && P.tables_in_smem != 1) {
-      // projection Phi^T (omega o q) on the fp64 tensor path: C[i][a] = sum_k (omega phi_i)(xi_k) q_a(xi_k),
-      // A = omega Phi^T in A-fragment order (shared memory when it fits, else L2), B = the q rows
-      const double* __restrict__ sWF = P.tables_in_smem == 2 ? sm : P.T.WPhiF;
-      const int KS = P.T.KS, MTl = (Nnew + 7) >> 3, bk = lane & 3, bn = lane >> 2;
-      const bool bval = bn < MS;
-      for (int mt = 0; mt < MTl; ++mt) {
-        double c0 = 0.0, c1 = 0.0;
-        const double* asrc = sWF + (size_t)mt * KS * 32 + lane;
-#pragma unroll 4
-        for (int ks = 0; ks < KS; ++ks) {
-          const int k = 4 * ks + bk;
-          const double bv = (bval && k < Q) ? q[k * MS + bn] : 0.0;
-          dmma884(c0, c1, asrc[(size_t)ks * 32], bv);
-        }
+    if (mma) {
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        if (mt >= MTl) break;
+        const double c0 = acc[mt][0], c1 = acc[mt][1];
         const int i = 8 * mt + (lane >> 2);
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
@@ -1615,9 +1636,11 @@ template <int FX, int MS, int MK>
 static int flux_impl(const KernelCtx& k, const FluxLaunch& a) {
   // per-level rules: the scalar projection with omega Phi^T (1); otherwise the DMMA projection with the
   // A-fragment table (2), staged in shared memory when it fits next to 4 warps' buffers
-  const bool scalar = k.ad.lq.on || std::getenv("IPM_FLUX_SCALAR_PROJ");
+  const bool scalar = k.ad.lq.on || std::getenv("IPM_FLUX_SCALAR_PROJ") || k.T.N > 64;
   const size_t tab = scalar ? (size_t)k.T.N * k.T.QP * 8 : (size_t)k.T.MT * k.T.KS * 32 * 8;
-  const size_t pw = (size_t)(k.T.Q * MS + 1) * 8;
+  // DMMA projection: the per-warp buffer holds chunks of at most 128 nodes
+  const int qchunk = scalar ? 0 : std::min((k.T.Q + 3) & ~3, 128);
+  const size_t pw = (size_t)((scalar ? k.T.Q : qchunk) * MS + 1) * 8;
   int in_smem = (tab + 4 * pw <= k.smem_optin) ? (scalar ? 1 : 2) : 0;
   const size_t base = in_smem ? tab : 0;
   int warps = (int)std::min<size_t>(8, (k.smem_optin - base) / pw);
@@ -1629,7 +1652,7 @@ static int flux_impl(const KernelCtx& k, const FluxLaunch& a) {
   const int64_t want = (k.mesh.cells - a.cell0 + warps - 1) / warps;
   int grid = (int)std::min<int64_t>(want, (int64_t)k.sm_count * per_sm * 4);
   if (grid < 1) grid = 1;
-  FluxParams P{k.T, k.mesh, k.cl, k.ad, a, k.sc, in_smem};
+  FluxParams P{k.T, k.mesh, k.cl, k.ad, a, k.sc, in_smem, qchunk};
   kern<<<grid, warps * 32, smem, S(k)>>>(P);
   return (int)cudaGetLastError();
 }

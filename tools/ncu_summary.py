@@ -87,6 +87,9 @@ def main():
         rd, wr = nbytes("dram__bytes_read.sum"), nbytes("dram__bytes_write.sum")
         if rd is not None and wr is not None:
             entry[f"{label}_dram_bytes_per_launch"] = rd + wr
+        pipe = num(m.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", (None,))[0])
+        if pipe is not None:
+            entry[f"{label}_fp64_pipe_active_pct"] = pipe
         dur = num(m.get("gpu__time_duration.sum", (None,))[0])
         if dur is not None:
             entry[f"{label}_ncu_ms"] = dur * {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0}.get(
