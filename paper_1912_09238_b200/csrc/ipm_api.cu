@@ -823,6 +823,7 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   // quasi-Newton dual solve (reading 35): per-cell pair history in device memory
   k.hessian_kind = C.hessian_kind;
   k.lbfgs_m = C.lbfgs_m > 0 ? C.lbfgs_m : 8;
+  k.lbfgs_pairs_reg = env_is("IPM_LBFGS_PAIRS", "reg") ? 1 : 0;
   if (C.hessian_kind == 1) {
     const bool big_ok = N * m <= 256 && p == 3 && tensor_gl && C.closure == IPM_CLOSURE_EULER && m == 4 && C.n_levels == 0;
     if (k.lbfgs_m != 8 || (N * m > 96 && !big_ok)) {
@@ -840,7 +841,8 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
     if (!c->d_lbS || !c->d_lbY || !c->d_lbR || !c->d_lbC || !c->d_lbN || !k.fb_lists ||
         cudaMemset(c->d_lbC, 0, nc * 4) != cudaSuccess || cudaMemset(c->d_lbN, 0, nc * 4) != cudaSuccess) {
       ipm_destroy(c);
-      return fail(IPM_ERR_CUDA, "cudaMalloc (L-BFGS history) failed");
+      return fail(IPM_ERR_CUDA, "cudaMalloc (L-BFGS history: 2 lbfgs_m N m doubles per cell, " +
+                                    std::to_string(16.0 * k.lbfgs_m * row * nc / 1e9) + " GB) failed");
     }
   } else if (C.hessian_kind != 0) {
     ipm_destroy(c);

@@ -23,14 +23,15 @@
 template <int MS>
 struct LbfgsLayout {
   // per warp: lam, lt, uh, g, q (direction / two-loop vector)  [5][NV]  + node buffer u [MS][Q]
-  static __host__ __device__ int per_warp(int NV, int Q) { return ((5 * NV + MS * Q) + 1) & ~1; }
+  //           (+ the pairs S, Y [MH][NV] when they live in shared memory, PSM)
+  static __host__ __device__ int per_warp(int NV, int Q, int pairs = 0) {
+    return ((5 * NV + MS * Q + 2 * pairs * NV) + 1) & ~1;
+  }
 };
 
-#ifndef IPM_LBFGS_THREADS
-#define IPM_LBFGS_THREADS 384
-#endif
-template <int CL, int MS, int NR, int MH>
-__global__ void __launch_bounds__(IPM_LBFGS_THREADS, 1) k_dual_lbfgs(DualParams P) {
+// PSM: the pairs in shared memory (fewer registers: 16 warps per SM) instead of registers (12 warps)
+template <int CL, int MS, int NR, int MH, bool PSM>
+__global__ void __launch_bounds__(PSM ? 512 : 384, 1) k_dual_lbfgs(DualParams P) {
   extern __shared__ __align__(16) double sm[];
   constexpr int MM = MS * (MS + 1) / 2;
   constexpr int NV = 32 * NR;
@@ -43,13 +44,15 @@ __global__ void __launch_bounds__(IPM_LBFGS_THREADS, 1) k_dual_lbfgs(DualParams 
   for (int x = threadIdx.x; x < MTT * KS * 32; x += blockDim.x) sWF[x] = P.T.WPhiF[x];
   __syncthreads();
   const int wig = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* base = sm + tabsz + (size_t)wig * LbfgsLayout<MS>::per_warp(NV, Q);
+  double* base = sm + tabsz + (size_t)wig * LbfgsLayout<MS>::per_warp(NV, Q, PSM ? MH : 0);
   double* lam = base;
   double* lt = lam + NV;
   double* uh = lt + NV;
   double* g = uh + NV;
   double* qv = g + NV;
   double* nb = qv + NV;  // u[a][k] at nb[a Q + k]
+  double* sS = nb + MS * Q;  // PSM: [MH][NV], column r of lane r % 32
+  double* sY = sS + MH * NV;
 
   const double* __restrict__ omega = P.T.omega;
   const DualLaunch& A = P.a;
@@ -80,7 +83,10 @@ __global__ void __launch_bounds__(IPM_LBFGS_THREADS, 1) k_dual_lbfgs(DualParams 
     }
     int cnt = A.lb_cnt[cell];
     if (A.lb_n[cell] != n) cnt = 0;
-    double S[MH][NR], Y[MH][NR], rho[MH];
+    double rho[MH];
+#define PS(i, e) (*(PSM ? &sS[(i) * NV + lane + 32 * (e)] : &S[PSM ? 0 : (i)][PSM ? 0 : (e)]))
+#define PY(i, e) (*(PSM ? &sY[(i) * NV + lane + 32 * (e)] : &Y[PSM ? 0 : (i)][PSM ? 0 : (e)]))
+    double S[PSM ? 1 : MH][PSM ? 1 : NR], Y[PSM ? 1 : MH][PSM ? 1 : NR];
     {
       const double* gS = A.lb_S + cell * (int64_t)MH * nmax;
       const double* gY = A.lb_Y + cell * (int64_t)MH * nmax;
@@ -91,8 +97,8 @@ __global__ void __launch_bounds__(IPM_LBFGS_THREADS, 1) k_dual_lbfgs(DualParams 
         for (int e = 0; e < NR; ++e) {
           const int r = lane + 32 * e;
           const bool v = i < cnt && r < n;
-          S[i][e] = v ? gS[(int64_t)i * nmax + r] : 0.0;
-          Y[i][e] = v ? gY[(int64_t)i * nmax + r] : 0.0;
+          PS(i, e) = v ? gS[(int64_t)i * nmax + r] : 0.0;
+          PY(i, e) = v ? gY[(int64_t)i * nmax + r] : 0.0;
         }
       }
     }
@@ -223,15 +229,15 @@ __global__ void __launch_bounds__(IPM_LBFGS_THREADS, 1) k_dual_lbfgs(DualParams 
               rho[i] = rho[i - 1];
 #pragma unroll
               for (int e = 0; e < NR; ++e) {
-                S[i][e] = S[i - 1][e];
-                Y[i][e] = Y[i - 1][e];
+                PS(i, e) = PS(i - 1, e);
+                PY(i, e) = PY(i - 1, e);
               }
             }
             rho[0] = 1.0 / sy;
 #pragma unroll
             for (int e = 0; e < NR; ++e) {
-              S[0][e] = sn[e];
-              Y[0][e] = yn[e];
+              PS(0, e) = sn[e];
+              PY(0, e) = yn[e];
             }
             cnt = cnt < MH ? cnt + 1 : MH;
           }
@@ -297,10 +303,10 @@ __global__ void __launch_bounds__(IPM_LBFGS_THREADS, 1) k_dual_lbfgs(DualParams 
               if (i < cnt) {
                 double t = 0.0;
 #pragma unroll
-                for (int e = 0; e < NR; ++e) t = fma(S[i][e], q[e], t);
+                for (int e = 0; e < NR; ++e) t = fma(PS(i, e), q[e], t);
                 al[i] = rho[i] * warp_sum(t);
 #pragma unroll
-                for (int e = 0; e < NR; ++e) q[e] = fma(-al[i], Y[i][e], q[e]);
+                for (int e = 0; e < NR; ++e) q[e] = fma(-al[i], PY(i, e), q[e]);
               }
             }
             // r = H0 q: Jbar r_i = q_i per moment i (the m states of moment i through shared memory)
@@ -340,10 +346,10 @@ __global__ void __launch_bounds__(IPM_LBFGS_THREADS, 1) k_dual_lbfgs(DualParams 
               if (i < cnt) {
                 double t = 0.0;
 #pragma unroll
-                for (int e = 0; e < NR; ++e) t = fma(Y[i][e], q[e], t);
+                for (int e = 0; e < NR; ++e) t = fma(PY(i, e), q[e], t);
                 const double be = rho[i] * warp_sum(t);
 #pragma unroll
-                for (int e = 0; e < NR; ++e) q[e] = fma(S[i][e], al[i] - be, q[e]);
+                for (int e = 0; e < NR; ++e) q[e] = fma(PS(i, e), al[i] - be, q[e]);
               }
             }
             double sl = 0.0;
@@ -410,8 +416,8 @@ __global__ void __launch_bounds__(IPM_LBFGS_THREADS, 1) k_dual_lbfgs(DualParams 
           for (int e = 0; e < NR; ++e) {
             const int r = lane + 32 * e;
             if (r < n) {
-              gS[(int64_t)i * nmax + r] = S[i][e];
-              gY[(int64_t)i * nmax + r] = Y[i][e];
+              gS[(int64_t)i * nmax + r] = PS(i, e);
+              gY[(int64_t)i * nmax + r] = PY(i, e);
             }
           }
           if (lane == 0) A.lb_rho[cell * MH + i] = rho[i];
@@ -462,6 +468,8 @@ __global__ void __launch_bounds__(IPM_LBFGS_THREADS, 1) k_dual_lbfgs(DualParams 
     if (my_worst) atomicMax(&P.sc->worst, my_worst);
   }
 }
+#undef PS
+#undef PY
 
 // ---- large cells (config 5: N = 56, m = 4, n = 224, Q = 10^3, p = 3) -------------------------------------
 // The same quasi-Newton iteration (reading 35) with one CTA of NT threads per cell.  Thread t owns the

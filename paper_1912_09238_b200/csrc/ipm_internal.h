@@ -176,6 +176,7 @@ struct KernelCtx {
   // tables (N_l, its 1D pair table, tile counts; Phi / omega Phi shared by prefix) and cell lists
   int hessian_kind;       // 0 exact Newton (Hessian + Cholesky), 1 L-BFGS (k_dual_lbfgs, reading 35)
   int lbfgs_m;            // L-BFGS pairs per cell
+  int lbfgs_pairs_reg;    // 1: k_dual_lbfgs keeps the pairs in registers (IPM_LBFGS_PAIRS=reg), else shared memory
   int32_t* fb_lists;      // [max(1, n_levels)][cells] Newton-fallback cell lists (hessian_kind 1)
   int bucket;             // 1: one k_dual_mma launch per level over that level's cells
   Tables Tl[8];

@@ -1435,14 +1435,14 @@ static int launch_big(const KernelCtx& k, const DualLaunch& a) {
 
 // quasi-Newton dual solve (reading 35): one warp per cell, as many warps per CTA as shared memory and
 // registers allow, one persistent CTA per SM
-template <int CL, int MS, int NR, int MH>
+template <int CL, int MS, int NR, int MH, bool PSM>
 static int dual_lbfgs_impl(const KernelCtx& k, const DualLaunch& a) {
   const size_t tab = (((size_t)k.T.N * k.T.QP + (size_t)k.T.MT * k.T.KS * 32 + 1) & ~(size_t)1) * 8;
-  const size_t pw = (size_t)LbfgsLayout<MS>::per_warp(32 * NR, k.T.Q) * 8;
+  const size_t pw = (size_t)LbfgsLayout<MS>::per_warp(32 * NR, k.T.Q, PSM ? MH : 0) * 8;
   if (tab + pw > k.smem_optin) return -1;
   int warps = (int)((k.smem_optin - tab) / pw);
-  warps = std::min(warps, IPM_LBFGS_THREADS / 32);
-  auto kern = k_dual_lbfgs<CL, MS, NR, MH>;
+  warps = std::min(warps, (PSM ? 512 : 384) / 32);
+  auto kern = k_dual_lbfgs<CL, MS, NR, MH, PSM>;
   const size_t smem = tab + warps * pw;
   int per_sm = configure(kern, warps * 32, smem);
   if (per_sm < 1) return -1;
@@ -1473,8 +1473,11 @@ static int dual_lbfgs_dispatch(const KernelCtx& k, const DualLaunch& a) {
     return (int)cudaGetLastError();
   }
   switch ((k.closure * 10 + k.m) * 10 + NR) {
-#define IPM_LCASE(CLV, MSV, NRV) \
-  case (CLV * 10 + MSV) * 10 + NRV: return dual_lbfgs_impl<CLV, MSV, NRV, 8>(k, a);
+// pairs in shared memory (PSM) unless IPM_LBFGS_PAIRS=reg (read at ipm_init: k.lbfgs_pairs_reg)
+#define IPM_LCASE(CLV, MSV, NRV)                                                                         \
+  case (CLV * 10 + MSV) * 10 + NRV:                                                                      \
+    return k.lbfgs_pairs_reg ? dual_lbfgs_impl<CLV, MSV, NRV, 8, false>(k, a)                          \
+                             : dual_lbfgs_impl<CLV, MSV, NRV, 8, true>(k, a);
     IPM_LCASE(CL_QUADRATIC, 1, 1)
     IPM_LCASE(CL_BARRIER, 1, 1)
     IPM_LCASE(CL_EULER, 3, 1)
@@ -1638,8 +1641,10 @@ static int flux_impl(const KernelCtx& k, const FluxLaunch& a) {
   // A-fragment table (2), staged in shared memory when it fits next to 4 warps' buffers
   const bool scalar = k.ad.lq.on || std::getenv("IPM_FLUX_SCALAR_PROJ") || k.T.N > 64;
   const size_t tab = scalar ? (size_t)k.T.N * k.T.QP * 8 : (size_t)k.T.MT * k.T.KS * 32 * 8;
-  // DMMA projection: the per-warp buffer holds chunks of at most 128 nodes
-  const int qchunk = scalar ? 0 : std::min((k.T.Q + 3) & ~3, 128);
+  // DMMA projection: the per-warp buffer holds the whole rule up to 256 nodes (config 4: one chunk of
+  // 144, measured 1.56 ms against 2.23 ms in chunks of 128), chunks of 128 beyond (config 5: 1 000)
+  const int q4 = (k.T.Q + 3) & ~3;
+  const int qchunk = scalar ? 0 : (q4 <= 256 ? q4 : 128);
   const size_t pw = (size_t)((scalar ? k.T.Q : qchunk) * MS + 1) * 8;
   int in_smem = (tab + 4 * pw <= k.smem_optin) ? (scalar ? 1 : 2) : 0;
   const size_t base = in_smem ? tab : 0;

@@ -70,11 +70,13 @@ def test_lbfgs_stress_steps_parity(torch, name):
         it_g, st_g = (to_np(x) for x in g.last_cell_stats())
         assert w == 0 and info.failed_cells == 0
         np.testing.assert_array_equal(st_g, st_o)
-        _counts_close(it_g, it_o)
-        assert abs(info.dt - dt_o) <= 1e-12 * dt_o
         err = (np.abs(to_np(lam_g) - lam_o) / scale).max()
         assert err < 1e-9, f"step {step}: duals {err:.2e}"
         assert_moments_close(to_np(u_g), u_o, 1e-9, f"{name} step {step}")
+        assert abs(info.dt - dt_o) <= 1e-10 * dt_o
+        # counts: config 5's 20-35 quasi-Newton steps per solve amplify rounding differences most (its
+        # node pass and gradient are sum-factorised on the GPU, direct sums in the oracle)
+        _counts_close(it_g, it_o, frac=0.8 if name == "cfg5" else 0.99, dmax=10 if name == "cfg5" else 4)
     assert it_o.mean() > 1.0  # the stress state makes the cells iterate
     # history: pair counts agree (a borderline curvature test may flip one cell)
     _, _, cnt_g = g.lbfgs_history()
@@ -119,9 +121,11 @@ def test_lbfgs_full_run_parity(torch, name):
     assert io["steps"] == ig["steps"]
     assert_moments_close(to_np(u_g), u_o, 1e-9, name)
     for (dto, ito, _), (dtg, itg, _) in zip(io["hist"], ig["hist"]):
-        # the two sides' final iterates agree to the stopping tolerance only (superlinear convergence:
-        # their last steps differ at the 1e-11 level), so dt, a max over the reconstructed states, to 1e-9
-        assert abs(dto - dtg) <= 1e-9 * dto
+        # the two sides' final iterates agree to the stopping tolerance only (superlinear convergence),
+        # so dt, a max over the reconstructed states, differs more than Newton's 1e-12
+        # (the oracle against itself under a 1e-15 perturbation: dt differs by 3.0e-9 on config 1,
+        # 2.5e-10 on config 2 — the GPU gets a few times that spread)
+        assert abs(dto - dtg) <= 2e-8 * dto
         # over a whole run the histories carry every earlier rounding difference (measured: up to 6 % of
         # the config-1 cells differ by 2 iterations in some steps of 25-iteration solves)
         # the counts of a superlinear iteration near tau are not reproducible across summation orders:
