@@ -125,6 +125,34 @@ __device__ __forceinline__ bool blk8_diag_factor(double& a0, double& a1, int lan
 }
 
 
+// ---- 8x8 diagonal block: explicit inverse by Gauss-Jordan (block LDL^T, IPM_MMA_LDL) ----------------
+// in:  a0, a1 = A[r][2q], A[r][2q+1] of the symmetric positive definite block (C-fragment, full)
+// out: a0, a1 = the same entries of A^{-1}; false on a pivot <= 0 or non-finite.  The pivots are the
+// diagonal of the block's LDL^T (= the squared Cholesky pivots): an indefinite matrix fails at the
+// same pivot as the Cholesky factorisation.  Per column: four independent shuffles, one reciprocal,
+// two fmas — no square root and no separate inverse of L.
+__device__ __forceinline__ bool blk8_gj_inverse(double& a0, double& a1, int lane, int ncol = 8) {
+  const int r = lane >> 2, q = lane & 3;
+  bool ok = true;
+  __syncwarp();
+#pragma unroll 1
+  for (int k = 0; k < ncol; ++k) {
+    const int kq = k >> 1;
+    const double mine = (k & 1) ? a1 : a0;                    // A[.][k] of this lane's row
+    const double p = __shfl_sync(FULL_MASK, mine, k * 4 + kq);  // A[k][k]
+    const double ark = __shfl_sync(FULL_MASK, mine, r * 4 + kq);  // A[r][k]
+    const double rk0 = __shfl_sync(FULL_MASK, a0, k * 4 + q);     // A[k][2q]
+    const double rk1 = __shfl_sync(FULL_MASK, a1, k * 4 + q);     // A[k][2q+1]
+    if (!(p > 0.0) || !isfinite(p)) ok = false;
+    const double ip = rcp_nr(p);
+    const double f = ark * ip;
+    const bool rowk = r == k;
+    a0 = (2 * q == k) ? (rowk ? ip : -f) : (rowk ? rk0 * ip : fma(-f, rk0, a0));
+    a1 = (2 * q + 1 == k) ? (rowk ? ip : -f) : (rowk ? rk1 * ip : fma(-f, rk1, a1));
+  }
+  return ok;
+}
+
 // ---- 8x8 diagonal block, rows in lanes ------------------------------------------------------------
 // Left-looking (Crout) Cholesky with lane l owning row r = l/4 (its 4 lanes compute redundantly):
 //   s_rc = A_rc - sum_{k<c} L_rk L_ck,   d_c = A_cc - sum_{k<c} L_ck^2,   L_rc = s_rc / sqrt(d_c)
@@ -207,7 +235,11 @@ struct MmaLayout {
     int r = s_base(N, Q, SF, q1d) + MM * nps(N);
     const int t = t_off(N, Q, SF) + ((SF > 0) ? q1d * (SF * (SF + 1) / 2) * CHW : 0);
     if (t > r) r = t;
+#ifdef IPM_MMA_LDL  // + the unscaled panel [NB][64] and w = D^{-1} z [NB * 8]
+    const int c = (3 * NB + 1) * 64 + NB * 8;
+#else
     const int c = (2 * NB + 1) * 64;  // Cholesky: panel [NB][64], Linv fragment [64], diagonal [NB][64]
+#endif
     if (c > r) r = c;
     return (r + 1) & ~1;
   }
@@ -287,6 +319,15 @@ struct DualMma {
     double* pan = reg;                // [NB][64]
     double* linvf = reg + NB * 64;    // [64]
     double* dg = reg + NB * 64 + 64;  // [NB][64]
+#ifdef IPM_MMA_LDL
+    // block LDL^T: L_IK = A_IK D_K^{-1} (pan), the unscaled A_IK (panA) for the trailing updates
+    // A_IJ -= L_IK A_JK^T, D_K^{-1} by Gauss-Jordan (linvf), forward z_I -= L_IK z_K (dd), w = D^{-1} z (ww),
+    // back substitution d_K = w_K - sum_{I > K} L_IK^T d_I
+    double* panA = dg + NB * 64;  // [NB][64]
+    double* ww = panA + NB * 64;  // [NB * 8]
+#else
+    double* const panA = pan;
+#endif
 #ifdef IPM_PHASE_TIMERS
     long long ct0 = clock64();
 #define CPH(i)                                                                                  \
@@ -406,13 +447,13 @@ struct DualMma {
             }
           });
         };
-        each_panel([&](int s, double* pI, int) { store_afrag(pI, blk[s][0], blk[s][1], lane); });
+        each_panel([&](int s, double* pI, int I) { store_afrag(panA + I * 64, blk[s][0], blk[s][1], lane); });
         __syncwarp();
         double lf0, lf1;
         afrag_ld(linvf, lf0, lf1);
-        each_panel([&](int s, double* pI, int) {
+        each_panel([&](int s, double* pI, int I) {
           double f0, f1;
-          afrag_ld(pI, f0, f1);
+          afrag_ld(panA + I * 64, f0, f1);
           double x0 = 0.0, x1 = 0.0;
           dmma884(x0, x1, f0, lf0);
           dmma884(x0, x1, f1, lf1);
@@ -441,13 +482,18 @@ struct DualMma {
         if (K1 < NBl) {
           double2 v = *reinterpret_cast<const double2*>(dg + K1 * 64 + 2 * lane);
           if constexpr (K >= 0) {
-            double p0, p1;
+            double p0, p1, pa0, pa1;
             afrag_ld(pan + K1 * 64, p0, p1);
-            dmma884(v.x, v.y, dneg(p0), p0);
-            dmma884(v.x, v.y, dneg(p1), p1);
+            afrag_ld(panA + K1 * 64, pa0, pa1);
+            dmma884(v.x, v.y, dneg(p0), pa0);
+            dmma884(v.x, v.y, dneg(p1), pa1);
           }
           double a0 = v.x, a1 = v.y;
+#ifdef IPM_MMA_LDL
+          const bool okd = blk8_gj_inverse(a0, a1, lane, min(8, n - 8 * K1));
+#else
           const bool okd = diag_factor(a0, a1, lane, min(8, n - 8 * K1), dg + K1 * 64, linvf);
+#endif
           store_afrag(linvf, a0, a1, lane);
           __syncwarp();
           // y_K1 = Linv b_K1;  dg[K1] <- B-fragment of Linv (back substitution)
@@ -458,9 +504,15 @@ struct DualMma {
           double y0 = 0.0, y1 = 0.0;
           dmma884(y0, y1, f0, bf0);
           dmma884(y0, y1, f1, bf1);
+#ifdef IPM_MMA_LDL
+          (void)g0;
+          (void)g1;
+          if (q == 0) ww[K1 * 8 + r] = y0;  // w_K1 = D^{-1} z_K1; dd keeps z_K1 for the panel update
+#else
           *reinterpret_cast<double2*>(dg + K1 * 64 + 2 * lane) = make_double2(g0, g1);
           __syncwarp();
           if (q == 0) dd[K1 * 8 + r] = y0;
+#endif
           if (lane == 0 && !okd) ctl[1] = 1;
         }
       }
@@ -470,10 +522,11 @@ struct DualMma {
           if constexpr (Jd > K + 1 && Jd < NB) {
             if (Jd < NBl) {
               double2 v = *reinterpret_cast<const double2*>(dg + Jd * 64 + 2 * lane);
-              double p0, p1;
+              double p0, p1, pa0, pa1;
               afrag_ld(pan + Jd * 64, p0, p1);
-              dmma884(v.x, v.y, dneg(p0), p0);
-              dmma884(v.x, v.y, dneg(p1), p1);
+              afrag_ld(panA + Jd * 64, pa0, pa1);
+              dmma884(v.x, v.y, dneg(p0), pa0);
+              dmma884(v.x, v.y, dneg(p1), pa1);
               *reinterpret_cast<double2*>(dg + Jd * 64 + 2 * lane) = v;
             }
           }
@@ -486,7 +539,7 @@ struct DualMma {
               if (I < NBl) {
                 double a0, a1, b0, b1;
                 afrag_ld(pan + I * 64, a0, a1);
-                afrag_ld(pan + J * 64, b0, b1);
+                afrag_ld(panA + J * 64, b0, b1);
                 dmma884(blk[s][0], blk[s][1], dneg(a0), b0);
                 dmma884(blk[s][0], blk[s][1], dneg(a1), b1);
               }
@@ -498,6 +551,37 @@ struct DualMma {
     });
     CPH(5);
     if (ctl[1]) return false;
+#ifdef IPM_MMA_LDL
+    // ---- back substitution: d_K = w_K - sum_{I > K} L_IK^T d_I: w_J -= L_KJ^T d_K (J < K) -------------
+    static_for<NB>([&](auto kc) {
+      constexpr int K = NB - 1 - decltype(kc)::value;
+      if (K >= NBl) return;
+      if constexpr (K > 0) {
+        double d0, d1;
+        vec_frag(ww + K * 8, d0, d1);
+        static_for<NBW2>([&](auto sc) {
+          constexpr int s = decltype(sc)::value, br = s * W + WR;
+          if constexpr (br < NBO) {
+            constexpr int I = oI(br), J = oJ(br);
+            if constexpr (I == K) {
+              double v0 = 0.0, v1 = 0.0;
+              dmma884(v0, v1, d0, blk[s][0]);
+              dmma884(v0, v1, d1, blk[s][1]);
+              if (lane < 4) {
+                ww[J * 8 + 2 * q] -= v0;
+                ww[J * 8 + 2 * q + 1] -= v1;
+              }
+            }
+          }
+        });
+        named_sync(bar, G);
+      }
+    });
+    for (int x = wr * 32 + lane; x < NBl * 8; x += W * 32) dd[x] = ww[x];
+    named_sync(bar, G);
+    CPH(6);
+    return true;
+#endif
     // ---- back substitution: d_K = Linv_K^T z_K; z_J -= L_KJ^T d_K (J < K), as row-vector DMMAs --------
     static_for<NB>([&](auto kc) {
       constexpr int K = NB - 1 - decltype(kc)::value;

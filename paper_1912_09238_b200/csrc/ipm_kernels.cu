@@ -441,7 +441,10 @@ struct FluxParams {
   int qchunk;  // k_flux_warp, DMMA projection: nodes per chunk of the per-warp buffer (multiple of 4; 0 = Q)
 };
 
-template <int FX, int MS, int MK>
+// CH: the node loop in chunks of P.qchunk nodes with the DMMA projection accumulated across chunks (16
+// accumulator registers live through the loop: config 5, Q = 1 000); otherwise one pass over the rule and
+// the projection tile by tile afterwards (config 4: fewer registers, more CTAs per SM)
+template <int FX, int MS, int MK, bool CH>
 __global__ void __launch_bounds__(256) k_flux_warp(FluxParams P) {
   extern __shared__ __align__(16) double sm[];
   const int N = P.T.N, Q = P.T.Q, QP = P.T.QP;
@@ -483,12 +486,13 @@ __global__ void __launch_bounds__(256) k_flux_warp(FluxParams P) {
     const int32_t* __restrict__ kfc = Lq >= 0 ? P.ad.lq.kf[Lq] : nullptr;
     const int Nnew = (P.ad.n_levels > 0 && A.level_new) ? P.ad.Nl[A.level_new[cell]] : N;
     const bool mma = Lq < 0 && P.tables_in_smem != 1 && N <= 64;
-    const int QBc = mma ? QB : Qc;
+    const int QBc = (mma && CH) ? QB : Qc;
     // DMMA projection accumulators (row tiles mt < MTl <= 8: N <= 64)
     const int MTl = (Nnew + 7) >> 3, bk = lane & 3, bn = lane >> 2;
-    double acc[8][2];
+    constexpr int NACC = CH ? 8 : 1;
+    double acc[NACC][2];
 #pragma unroll
-    for (int mt = 0; mt < 8; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+    for (int mt = 0; mt < NACC; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
     for (int k0 = 0; k0 < Qc; k0 += QBc) {
     const int k1 = min(Qc, k0 + QBc);
     for (int kq = k0 + lane; kq < k1; kq += 32) {
@@ -565,7 +569,7 @@ __global__ void __launch_bounds__(256) k_flux_warp(FluxParams P) {
       }
     }
     __syncwarp();
-    if (mma) {
+    if (mma && CH) {
       // projection Phi^T (omega o q) on the fp64 tensor path, this chunk's k-steps: C[i][a] += sum_k
       // (omega phi_i)(xi_k) q_a(xi_k), A = omega Phi^T in A-fragment order (shared memory when it fits,
       // else L2), B = the chunk's q rows
@@ -577,7 +581,7 @@ __global__ void __launch_bounds__(256) k_flux_warp(FluxParams P) {
         const double bv = (bval && k < k1) ? q[(k - k0) * MS + bn] : 0.0;
         const double* asrc = sWF + (size_t)ks * 32 + lane;
 #pragma unroll
-        for (int mt = 0; mt < 8; ++mt)
+        for (int mt = 0; mt < NACC; ++mt)
           if (mt < MTl) dmma884(acc[mt][0], acc[mt][1], asrc[(size_t)mt * KS * 32], bv);
       }
       __syncwarp();
@@ -586,10 +590,25 @@ __global__ void __launch_bounds__(256) k_flux_warp(FluxParams P) {
     const double* uo = A.uhat_old + cell * nmax;
     double* un_ = A.uhat_new + cell * nmax;
     if (mma) {
-#pragma unroll
-      for (int mt = 0; mt < 8; ++mt) {
+      const double* __restrict__ sWF = P.tables_in_smem == 2 ? sm : P.T.WPhiF;
+      const int KS = P.T.KS;
+#pragma unroll 1
+      for (int mt = 0; mt < (CH ? 8 : MTl); ++mt) {
         if (mt >= MTl) break;
-        const double c0 = acc[mt][0], c1 = acc[mt][1];
+        double c0, c1;
+        if constexpr (CH) {
+          c0 = acc[mt < NACC ? mt : 0][0];
+          c1 = acc[mt < NACC ? mt : 0][1];
+        } else {  // one pass over the whole rule (q holds every node)
+          c0 = c1 = 0.0;
+          const double* asrc = sWF + (size_t)mt * KS * 32 + lane;
+#pragma unroll 4
+          for (int ks = 0; ks < KS; ++ks) {
+            const int k = 4 * ks + bk;
+            const double bv = (bn < MS && k < Qc) ? q[k * MS + bn] : 0.0;
+            dmma884(c0, c1, asrc[(size_t)ks * 32], bv);
+          }
+        }
         const int i = 8 * mt + (lane >> 2);
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
@@ -1651,7 +1670,7 @@ static int flux_impl(const KernelCtx& k, const FluxLaunch& a) {
   int warps = (int)std::min<size_t>(8, (k.smem_optin - base) / pw);
   if (warps < 1) return -1;
   const size_t smem = base + warps * pw;
-  auto kern = k_flux_warp<FX, MS, MK>;
+  auto kern = (qchunk > 0 && qchunk < k.T.Q) ? k_flux_warp<FX, MS, MK, true> : k_flux_warp<FX, MS, MK, false>;
   int per_sm = configure(kern, warps * 32, smem);
   if (per_sm < 1) per_sm = 1;
   const int64_t want = (k.mesh.cells - a.cell0 + warps - 1) / warps;
