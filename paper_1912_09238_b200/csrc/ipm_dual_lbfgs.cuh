@@ -30,15 +30,18 @@ struct LbfgsLayout {
 };
 
 // PSM: the pairs in shared memory (fewer registers: 16 warps per SM) instead of registers (12 warps)
-template <int CL, int MS, int NR, int MH, bool PSM>
+// QC, NC: compile-time Q and N of the launch (0 = from the tables at run time), as k_dual_mma's
+// fixed-shape instances (loop bounds and tile counts fold to constants)
+template <int CL, int MS, int NR, int MH, bool PSM, int QC = 0, int NC = 0>
 __global__ void __launch_bounds__(PSM ? 512 : 384, 1) k_dual_lbfgs(DualParams P) {
   extern __shared__ __align__(16) double sm[];
   constexpr int MM = MS * (MS + 1) / 2;
   constexpr int NV = 32 * NR;
-  const int N = P.T.N, Q = P.T.Q, QP = P.T.QP, KS = P.T.KS;
+  const int N = NC ? NC : P.T.N, Q = QC ? QC : P.T.Q;
+  const int QP = QC ? ((QC % 2) ? QC : QC + 1) : P.T.QP, KS = QC ? (QC + 3) / 4 : P.T.KS;
   double* sPhiT = sm;
   double* sWF = sm + N * QP;  // [MT][KS][32]
-  const int MTT = P.T.MT;
+  const int MTT = NC ? (NC + 7) / 8 : P.T.MT;
   const int tabsz = (N * QP + MTT * KS * 32 + 1) & ~1;
   for (int x = threadIdx.x; x < N * QP; x += blockDim.x) sPhiT[x] = P.T.PhiT[x];
   for (int x = threadIdx.x; x < MTT * KS * 32; x += blockDim.x) sWF[x] = P.T.WPhiF[x];
@@ -70,7 +73,7 @@ __global__ void __launch_bounds__(PSM ? 512 : 384, 1) k_dual_lbfgs(DualParams P)
     if (ci >= ncells) break;
     const int64_t cell = A.list ? (int64_t)A.list[ci] : (int64_t)ci;
     const int lvl = A.level ? A.level[cell] : 0;
-    const int Nl = (P.ad.n_levels > 0 && !A.list) ? P.ad.Nl[lvl] : N;
+    const int Nl = NC ? NC : ((P.ad.n_levels > 0 && !A.list) ? P.ad.Nl[lvl] : N);
     const int n = Nl * MS;
     // ---- load the cell: uhat, lambda, the L-BFGS history (pairs of another size are dropped) ----
     {

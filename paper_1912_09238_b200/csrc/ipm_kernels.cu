@@ -1454,14 +1454,14 @@ static int launch_big(const KernelCtx& k, const DualLaunch& a) {
 
 // quasi-Newton dual solve (reading 35): one warp per cell, as many warps per CTA as shared memory and
 // registers allow, one persistent CTA per SM
-template <int CL, int MS, int NR, int MH, bool PSM>
+template <int CL, int MS, int NR, int MH, bool PSM, int QC = 0, int NC = 0>
 static int dual_lbfgs_impl(const KernelCtx& k, const DualLaunch& a) {
   const size_t tab = (((size_t)k.T.N * k.T.QP + (size_t)k.T.MT * k.T.KS * 32 + 1) & ~(size_t)1) * 8;
   const size_t pw = (size_t)LbfgsLayout<MS>::per_warp(32 * NR, k.T.Q, PSM ? MH : 0) * 8;
   if (tab + pw > k.smem_optin) return -1;
   int warps = (int)((k.smem_optin - tab) / pw);
   warps = std::min(warps, (PSM ? 512 : 384) / 32);
-  auto kern = k_dual_lbfgs<CL, MS, NR, MH, PSM>;
+  auto kern = k_dual_lbfgs<CL, MS, NR, MH, PSM, QC, NC>;
   const size_t smem = tab + warps * pw;
   int per_sm = configure(kern, warps * 32, smem);
   if (per_sm < 1) return -1;
@@ -1490,6 +1490,17 @@ static int dual_lbfgs_dispatch(const KernelCtx& k, const DualLaunch& a) {
     kern<<<std::max(grid, 1), NT, smem, S(k)>>>(P);
     g_last_dual = "k_dual_lbfgs_big";
     return (int)cudaGetLastError();
+  }
+  // the BASELINE shapes: compile-time Q, N instances (launches of one basis size)
+  if (!k.lbfgs_pairs_reg && !k.mma_generic && (k.ad.n_levels == 0 || a.list) && k.closure == CL_EULER && k.m == 4) {
+#define IPM_LFCASE(NRV, QV, NV) \
+  if (NR == NRV && k.T.Q == QV && k.T.N == NV) return dual_lbfgs_impl<CL_EULER, 4, NRV, 8, true, QV, NV>(k, a);
+    IPM_LFCASE(2, 100, 15)  // config 3
+    IPM_LFCASE(1, 144, 6)   // config 4 levels (degrees 2-5)
+    IPM_LFCASE(2, 144, 10)
+    IPM_LFCASE(2, 144, 15)
+    IPM_LFCASE(3, 144, 21)
+#undef IPM_LFCASE
   }
   switch ((k.closure * 10 + k.m) * 10 + NR) {
 // pairs in shared memory (PSM) unless IPM_LBFGS_PAIRS=reg (read at ipm_init: k.lbfgs_pairs_reg)
