@@ -1491,17 +1491,8 @@ static int dual_lbfgs_dispatch(const KernelCtx& k, const DualLaunch& a) {
     g_last_dual = "k_dual_lbfgs_big";
     return (int)cudaGetLastError();
   }
-  // the BASELINE shapes: compile-time Q, N instances (launches of one basis size)
-  if (!k.lbfgs_pairs_reg && !k.mma_generic && (k.ad.n_levels == 0 || a.list) && k.closure == CL_EULER && k.m == 4) {
-#define IPM_LFCASE(NRV, QV, NV) \
-  if (NR == NRV && k.T.Q == QV && k.T.N == NV) return dual_lbfgs_impl<CL_EULER, 4, NRV, 8, true, QV, NV>(k, a);
-    IPM_LFCASE(2, 100, 15)  // config 3
-    IPM_LFCASE(1, 144, 6)   // config 4 levels (degrees 2-5)
-    IPM_LFCASE(2, 144, 10)
-    IPM_LFCASE(2, 144, 15)
-    IPM_LFCASE(3, 144, 21)
-#undef IPM_LFCASE
-  }
+  // (compile-time Q, N instances of this kernel, as k_dual_mma has, measured 8 % slower on config 3 and
+  // 4 % on config 4: r02u_*_lbfgs_fixed.json — the generic instance is the product path)
   switch ((k.closure * 10 + k.m) * 10 + NR) {
 // pairs in shared memory (PSM) unless IPM_LBFGS_PAIRS=reg (read at ipm_init: k.lbfgs_pairs_reg)
 #define IPM_LCASE(CLV, MSV, NRV)                                                                         \

@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--no-adaptive", action="store_true")
     ap.add_argument("--pts", default="", help="mesh points NXxNY of the bump channel (default: BASELINE 548x183)")
     ap.add_argument("--hessian", default="newton", choices=["newton", "lbfgs"])
+    ap.add_argument("--newton", default="", choices=["", "full", "one_step"], help="override the config's mode")
     args = ap.parse_args()
     cfg = configs.get(args.config)
     if args.no_adaptive:
@@ -40,6 +41,8 @@ def main():
         nxp, nyp = (int(v) for v in args.pts.split("x"))
         cfg["mesh"].update(nx_pts=nxp, ny_pts=nyp)
     cfg["hessian"] = args.hessian
+    if args.newton:
+        cfg["newton"] = args.newton
     m = cfg["mesh"]
     g = Context(cfg, bump_channel_mesh(m["nx_pts"], m["ny_pts"], m["seed"]))
     uhat = g.zeros()
@@ -70,7 +73,8 @@ def main():
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     rho = uhat[:, 0, 0]
-    print(json.dumps({"summary": True, "config": args.config, "hessian": args.hessian, "cells": g.cells, "steps": n, "converged": drop <= args.drop,
+    print(json.dumps({"summary": True, "config": args.config, "hessian": args.hessian, "newton": cfg["newton"],
+                      "cells": g.cells, "steps": n, "converged": drop <= args.drop,
                       "residual_drop": drop, "target_drop": args.drop, "wall_s": wall,
                       "cell_steps_per_s": g.cells * n / wall, "adaptive": bool(g.cfg.get("levels")),
                       "mean_rho0": float(rho.mean()), "min_rho0": float(rho.min())}), flush=True)
