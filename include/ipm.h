@@ -315,6 +315,16 @@ IPM_API ipm_status ipm_step_dual(ipm_ctx *c, const double *d_uhat, double *d_lam
                                  uint64_t *d_rate);
 IPM_API ipm_status ipm_step_flux(ipm_ctx *c, double *d_uhat, double *d_lambda, const double *d_recvbuf,
                                  const uint64_t *d_rate, double t_end, ipm_step_info *info);
+/* ipm_step_dual in two parts, so that the halo exchange overlaps the interior dual solves:
+ *   ipm_step_dual_boundary  begins the step, solves the owned cells adjacent to a peer, packs d_sendbuf;
+ *   (caller)                starts the send / receive of the per-peer slices (asynchronous);
+ *   ipm_step_dual_interior  solves the remaining owned cells, copies the local CFL rate to d_rate;
+ *   (caller)                waits for the receives, all-reduces d_rate with MAX; then ipm_step_flux.
+ * Results equal ipm_step_dual bit for bit (every cell's solve is independent of the launch it is in).
+ * Contexts with adaptive levels, or the comparison dual kernels (IPM_DUAL_KERNEL=group|warp), solve
+ * every cell in the boundary part (the interior part then only copies the rate). */
+IPM_API ipm_status ipm_step_dual_boundary(ipm_ctx *c, const double *d_uhat, double *d_lambda, double *d_sendbuf);
+IPM_API ipm_status ipm_step_dual_interior(ipm_ctx *c, const double *d_uhat, double *d_lambda, uint64_t *d_rate);
 /* peers (ascending rank) with per-peer send / receive cell counts; arrays sized npeers */
 IPM_API ipm_status ipm_halo_layout(const ipm_ctx *c, int32_t *npeers, int64_t *nsend, int64_t *nrecv,
                                    int32_t *h_peers, int32_t *h_send_count, int32_t *h_recv_count);

@@ -319,6 +319,10 @@ struct ipm_ctx {
   // per-level nested rules (reading 36): each level's tables on its own nodes (no sum factorisation
   // tables; the bucketed launches add them)
   ipm::Tables lq_tables[8] = {};
+  // distributed contexts: the owned cells adjacent to a peer (boundary) and the others (interior), local
+  // indices ascending, for ipm_step_dual_boundary / ipm_step_dual_interior
+  int32_t *d_bnd = nullptr, *d_int = nullptr;
+  int64_t n_bnd = 0, n_int = 0;
 };
 
 // the L-BFGS history of cells [r0, ...) for a dual launch (nothing for Newton contexts)
@@ -848,6 +852,22 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
     ipm_destroy(c);
     return fail(IPM_ERR_ARG, "hessian_kind must be 0 (Newton) or 1 (L-BFGS)");
   }
+  // boundary / interior cell lists (distributed contexts without adaptive levels: the list launches use the
+  // uniform-degree kernels)
+  if (nranks > 1 && C.n_levels == 0 && !c->part.send_local.empty()) {
+    std::vector<char> isb(cells, 0);
+    for (int32_t l : c->part.send_local) isb[l] = 1;
+    std::vector<int32_t> bl, il;
+    for (int64_t j = 0; j < cells; ++j) (isb[j] ? bl : il).push_back((int32_t)j);
+    c->n_bnd = (int64_t)bl.size();
+    c->n_int = (int64_t)il.size();
+    c->d_bnd = dalloc<int32_t>(std::max<size_t>(bl.size(), 1), c->owned);
+    c->d_int = dalloc<int32_t>(std::max<size_t>(il.size(), 1), c->owned);
+    if (!c->d_bnd || !c->d_int || up(c->d_bnd, bl.data(), bl.size() * 4) || up(c->d_int, il.data(), il.size() * 4)) {
+      ipm_destroy(c);
+      return fail(IPM_ERR_CUDA, "boundary / interior lists upload failed");
+    }
+  }
   *out = c;
   return IPM_OK;
 }
@@ -1029,6 +1049,61 @@ ipm_status ipm_step_dual(ipm_ctx* c, const double* d_uhat, double* d_lambda, dou
       return launch_rc(rc, "pack");
   if (d_rate) CUDA_OK(cudaMemcpyAsync(d_rate, &c->d_sc->rate_bits, 8, cudaMemcpyDeviceToDevice, c->stream));
   return IPM_OK;
+}
+
+// the dual solve of one of the two cell lists (boundary first, so its halo duals can travel while the
+// interior cells solve); part 0 also begins the step and packs the send buffer, part 1 copies the rate
+static ipm_status step_dual_part(ipm_ctx* c, const double* d_uhat, double* d_lambda, double* d_sendbuf,
+                                 uint64_t* d_rate, int part) {
+  if (!c || !d_uhat || !d_lambda) return fail(IPM_ERR_ARG, "null argument");
+  if (!c->part.send_local.empty() && !d_sendbuf && part == 0) return fail(IPM_ERR_ARG, "send buffer required");
+  ipm::KernelCtx k = c->k;
+  // the list launches need a uniform-degree dual kernel that takes cell lists (k_dual_mma, k_dual_big,
+  // the quasi-Newton kernels): otherwise part 0 solves every cell and part 1 does nothing
+  const bool split = c->d_bnd && !k.force_warp_kernel && !k.dual_group;
+  if (part == 0) {
+    if (int rc = ipm::launch_step_begin(k, c->ghost_rate)) return launch_rc(rc, "step_begin");
+    if (c->timing) cudaEventRecord(c->ev[0], c->stream);
+  }
+  if (part == 0 || split) {
+    ipm::DualLaunch a{};
+    a.uhat = d_uhat;
+    a.lam = d_lambda;
+    a.iters = c->d_iters;
+    a.status = c->d_status;
+    a.crit = c->d_crit;
+    a.halv = c->d_halv;
+    a.inadm = c->d_inadm;
+    a.uq = (c->band_rows || c->k.ad.lq.on) ? nullptr : c->d_uq;
+    a.cells = c->cells;
+    a.mode = c->cfg.newton_mode;
+    a.want_rate = 1;
+    lb_attach(c, a, 0);
+    if (split) {
+      a.list = part == 0 ? c->d_bnd : c->d_int;
+      a.cells = part == 0 ? c->n_bnd : c->n_int;
+      a.queue = part == 0 ? &c->d_sc->work_counter : &c->d_sc->work_counter2;
+      a.row = c->N * c->m;
+    }
+    if (a.cells > 0)
+      if (int rc = ipm::launch_dual(k, a)) return launch_rc(rc, "dual_solve");
+  }
+  if (part == 0 && !c->part.send_local.empty())
+    if (int rc = ipm::launch_pack(k, d_lambda, c->d_send_local, (int64_t)c->part.send_local.size(), d_sendbuf))
+      return launch_rc(rc, "pack");
+  if (part == 1) {
+    if (c->timing) cudaEventRecord(c->ev[1], c->stream);
+    if (d_rate) CUDA_OK(cudaMemcpyAsync(d_rate, &c->d_sc->rate_bits, 8, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  return IPM_OK;
+}
+
+ipm_status ipm_step_dual_boundary(ipm_ctx* c, const double* d_uhat, double* d_lambda, double* d_sendbuf) {
+  return step_dual_part(c, d_uhat, d_lambda, d_sendbuf, nullptr, 0);
+}
+
+ipm_status ipm_step_dual_interior(ipm_ctx* c, const double* d_uhat, double* d_lambda, uint64_t* d_rate) {
+  return step_dual_part(c, d_uhat, d_lambda, nullptr, d_rate, 1);
 }
 
 ipm_status ipm_step_flux(ipm_ctx* c, double* d_uhat, double* d_lambda, const double* d_recvbuf,

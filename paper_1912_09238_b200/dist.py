@@ -21,12 +21,15 @@ def _staged(t: torch.Tensor, group) -> bool:
     return t.is_cuda and dist.get_backend(group) == "gloo"
 
 
-def halo_exchange(sendbuf: torch.Tensor, recvbuf: torch.Tensor, layout: dict, group=None) -> None:
+def halo_exchange(sendbuf: torch.Tensor, recvbuf: torch.Tensor, layout: dict, group=None, async_op=False):
+    """async_op: return the requests (wait_all) so that device work queued after this call — the
+    interior dual solves — overlaps the transfer; NCCL orders the sends after the work already queued
+    on the current stream (the boundary solves and the pack)"""
     if _staged(sendbuf, group):
         rh = recvbuf.cpu()
         halo_exchange(sendbuf.cpu(), rh, layout, group)
         recvbuf.copy_(rh)
-        return
+        return []
     ops = []
     s0 = r0 = 0
     for peer, ns, nr in zip(layout["peers"], layout["send_count"], layout["recv_count"]):
@@ -36,9 +39,16 @@ def halo_exchange(sendbuf: torch.Tensor, recvbuf: torch.Tensor, layout: dict, gr
             ops.append(dist.P2POp(dist.irecv, recvbuf[r0:r0 + nr], peer, group))
         s0 += ns
         r0 += nr
-    if ops:
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
+    reqs = dist.batch_isend_irecv(ops) if ops else []
+    if async_op:
+        return reqs
+    wait_all(reqs)
+    return []
+
+
+def wait_all(reqs) -> None:
+    for req in reqs:
+        req.wait()
 
 
 def allreduce_max_(t: torch.Tensor, group=None) -> None:

@@ -31,6 +31,7 @@ EXPORTS = [
     "ipm_get_time", "ipm_set_time", "ipm_last_kernel_ms", "ipm_enable_timing", "ipm_last_dual_kernel", "ipm_last_flux_kernel", "ipm_struct_size", "ipm_retard_stage", "ipm_retard_advance",
     "ipm_debug_phase_cycles", "ipm_step_dual", "ipm_step_flux", "ipm_halo_layout", "ipm_partition_query",
     "ipm_get_status", "ipm_last_cell_linesearch", "ipm_node_band_rows", "ipm_lbfgs_reset", "ipm_lbfgs_history",
+    "ipm_step_dual_boundary", "ipm_step_dual_interior",
 ]
 HIST_BUCKETS = 16  # IPM_HIST_BUCKETS
 
@@ -138,6 +139,8 @@ def lib():
             "ipm_node_band_rows": (st, [P, C.POINTER(C.c_int64)]),
             "ipm_lbfgs_reset": (st, [P]),
             "ipm_lbfgs_history": (st, [P, P, P, P]),
+            "ipm_step_dual_boundary": (st, [P, P, P, P]),
+            "ipm_step_dual_interior": (st, [P, P, P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -414,9 +417,11 @@ class Context:
 
             if not hasattr(self, "sendbuf"):
                 self._halo_setup()
-            check(lib().ipm_step_dual(self.h, pu, pl, _ptr(self.sendbuf), _ptr(self.rate)),
-                  "ipm_step_dual")
-            dist.halo_exchange(self.sendbuf, self.recvbuf, self.halo, self.group)
+            # boundary cells first; their duals travel while the interior cells solve
+            check(lib().ipm_step_dual_boundary(self.h, pu, pl, _ptr(self.sendbuf)), "ipm_step_dual_boundary")
+            reqs = dist.halo_exchange(self.sendbuf, self.recvbuf, self.halo, self.group, async_op=True)
+            check(lib().ipm_step_dual_interior(self.h, pu, pl, _ptr(self.rate)), "ipm_step_dual_interior")
+            dist.wait_all(reqs)
             dist.allreduce_max_(self.rate, self.group)
             rc = lib().ipm_step_flux(self.h, pu, pl, _ptr(self.recvbuf), _ptr(self.rate), te,
                                      C.byref(info) if sync else None)

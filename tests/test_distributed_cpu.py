@@ -56,13 +56,22 @@ def _worker(rank, world, port, name, px, py, steps, outdir):
     layout = dict(peers=part["peers"].tolist(), send_count=part["send_count"].tolist(),
                   recv_count=part["recv_count"].tolist())
     row = o.N * o.m
+    boundary = np.unique(send)
+    interior = np.setdiff1d(own, boundary)
     for _ in range(steps):
-        for j in own:  # dual problems of the owned cells (no communication)
+        # the binding's order (ipm_step_dual_boundary / _interior): the dual problems of the cells
+        # adjacent to a peer first, their duals sent while the interior cells solve (no
+        # communication inside the dual problems)
+        for j in boundary:
             lam[j], _, _, st = o.dual_solve_cell(u[j], lam[j], cfg["newton"])
             assert st == 0
         sendbuf = torch.from_numpy(np.ascontiguousarray(lam[send].reshape(len(send), row)))
         recvbuf = torch.zeros((len(halo), row), dtype=torch.float64)
-        pdist.halo_exchange(sendbuf, recvbuf, layout)
+        reqs = pdist.halo_exchange(sendbuf, recvbuf, layout, async_op=True)
+        for j in interior:
+            lam[j], _, _, st = o.dual_solve_cell(u[j], lam[j], cfg["newton"])
+            assert st == 0
+        pdist.wait_all(reqs)
         lam[halo] = recvbuf.numpy().reshape(len(halo), o.N, o.m)
         rate = np.array([o.cell_rates(lam)[own].max()])
         bits = torch.from_numpy(rate.view(np.int64).copy())

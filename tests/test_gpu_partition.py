@@ -29,6 +29,8 @@ def torch():
 def _case(name):
     if name == "cart":
         return configs.parity_variant("cfg3"), None
+    if name == "cart_lbfgs":
+        return dict(configs.parity_variant("cfg3"), hessian="lbfgs"), None
     cfg = configs.parity_variant("cfg4")
     if name == "tri_retard":  # refinement retardation: the stage advances from the global residual
         cfg.update(delta_inc=1e-9, delta_dec=0.0, initial_level=0, retard=[(1.9e-4, 0), (1.8759e-4, 1)])
@@ -36,9 +38,13 @@ def _case(name):
     return cfg, bump_channel_mesh(m["nx_pts"], m["ny_pts"], m["seed"])
 
 
-@pytest.mark.parametrize("name,R,px,py", [("cart", 2, 2, 1), ("cart", 4, 2, 2), ("tri", 3, 0, 0),
-                                         ("tri_retard", 3, 0, 0)])
-def test_virtual_ranks_match_single_context(torch, name, R, px, py):
+@pytest.mark.parametrize("name,R,px,py,split", [("cart", 2, 2, 1, False), ("cart", 4, 2, 2, False),
+                                               ("tri", 3, 0, 0, False), ("tri_retard", 3, 0, 0, False),
+                                               ("cart", 4, 2, 2, True), ("cart_lbfgs", 2, 2, 1, True),
+                                               ("tri", 3, 0, 0, True)])
+def test_virtual_ranks_match_single_context(torch, name, R, px, py, split):
+    """split: the boundary cells' dual solves first (ipm_step_dual_boundary), the exchange, then the
+    interior cells' (ipm_step_dual_interior) — the overlap order of the binding's distributed step"""
     from paper_1912_09238_b200 import Context
     from paper_1912_09238_b200.ipm import _ptr, check, ipm_step_info, lib
 
@@ -60,7 +66,10 @@ def test_virtual_ranks_match_single_context(torch, name, R, px, py):
     L = lib()
     for _ in range(steps):
         for g, u, lam in zip(ctxs, us, lams):
-            check(L.ipm_step_dual(g.h, _ptr(u), _ptr(lam), _ptr(g.sendbuf), _ptr(g.rate)), "ipm_step_dual")
+            if split:
+                check(L.ipm_step_dual_boundary(g.h, _ptr(u), _ptr(lam), _ptr(g.sendbuf)), "ipm_step_dual_boundary")
+            else:
+                check(L.ipm_step_dual(g.h, _ptr(u), _ptr(lam), _ptr(g.sendbuf), _ptr(g.rate)), "ipm_step_dual")
         torch.cuda.synchronize()
         # exchange: slice of r's send buffer for peer p -> slice of p's receive buffer from r
         for r, g in enumerate(ctxs):
@@ -72,6 +81,10 @@ def test_virtual_ranks_match_single_context(torch, name, R, px, py):
                 assert gp.halo["recv_count"][k] == ns
                 gp.recvbuf[r0:r0 + ns].copy_(g.sendbuf[s0:s0 + ns])
                 s0 += ns
+        if split:
+            for g, u, lam in zip(ctxs, us, lams):
+                check(L.ipm_step_dual_interior(g.h, _ptr(u), _ptr(lam), _ptr(g.rate)), "ipm_step_dual_interior")
+            torch.cuda.synchronize()
         rate = torch.stack([g.rate for g in ctxs]).max()
         for g in ctxs:
             g.rate.copy_(rate.reshape(1))
