@@ -491,16 +491,19 @@ struct LbfgsBigLayout {
   static __host__ __device__ int doubles(int n, int Q, int M, int q, int NW) {
     const int npr2 = (M + 1) * (M + 2) / 2;
     const int t1 = npr2 * q * MS, t2 = (M + 1) * q * q * MS;
-    return 5 * n + MS * Q + t1 + t2 + (M + 1) * q + q + 2 * 16 * NW + ((M + 1) * (M + 1) * (M + 1) + 1) / 2 + 8 +
-           2 * 8 * n;  // + the pairs S, Y [MH <= 8][n]
+    return 5 * n + MS * Q + t1 + t2 + 2 * (M + 1) * q + q + 2 * 16 * NW + ((M + 1) * (M + 1) * (M + 1) + 1) / 2 + 8 +
+           2 * 8 * n;  // + the pairs S, Y [MH <= 8][n]; WL1 [M+1][q] = (w_k / 2) L_i(x_k)
   }
 };
 
-template <int CL, int MS, int MH, int NT>
+// Q1, MD: compile-time 1D points and degree (config 5: 10, 5; 0 = from the tables): the stage loops'
+// index arithmetic (divisions by q, m) folds to constants
+template <int CL, int MS, int MH, int NT, int Q1 = 0, int MD = 0>
 __global__ void __launch_bounds__(NT, 2) k_dual_lbfgs_big(DualParams P) {
   extern __shared__ __align__(16) double sm[];
   constexpr int MM = MS * (MS + 1) / 2, NW = NT / 32;
-  const int N = P.T.N, Q = P.T.Q, q = P.T.q1d, M = P.T.npr1 - 1;  // npr1 = M + 1 (1D degrees)
+  const int q = Q1 ? Q1 : P.T.q1d, M = MD ? MD : P.T.npr1 - 1;  // npr1 = M + 1 (1D degrees)
+  const int N = MD ? (MD + 1) * (MD + 2) * (MD + 3) / 6 : P.T.N, Q = Q1 ? Q1 * Q1 * Q1 : P.T.Q;
   const int n = N * MS, npr2 = (M + 1) * (M + 2) / 2;
   double* lam = sm;
   double* lt = lam + n;
@@ -512,7 +515,9 @@ __global__ void __launch_bounds__(NT, 2) k_dual_lbfgs_big(DualParams P) {
   double* T2 = T1 + npr2 * q * MS;         // [M+1][q][q][MS] (also R1)
   double* L1 = T2 + (M + 1) * q * q * MS;  // [M+1][q]
   double* w1h = L1 + (M + 1) * q;          // [q]
-  double* red = w1h + q;                   // [2][16][NW]
+  double* WL1 = w1h + q;                   // [M+1][q] (w_k / 2) L_i(x_k): the gradient stages' 1D table
+  // [2][16][NW], 16-byte aligned (double2 reads of the partials); the layout has slack for it
+  double* red = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(WL1 + (M + 1) * q) + 15) & ~(uintptr_t)15);
   int* bidx = reinterpret_cast<int*>(red + 2 * 16 * NW);  // [(M+1)^3] -> basis index or -1
   // the cell's pairs, newest first, column t owned by thread t (shared memory: registers would spill)
   double* sS = red + 2 * 16 * NW + ((M + 1) * (M + 1) * (M + 1) + 1) / 2 + 8;  // [MH][n]
@@ -520,6 +525,7 @@ __global__ void __launch_bounds__(NT, 2) k_dual_lbfgs_big(DualParams P) {
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   for (int x = t; x < (M + 1) * q; x += NT) L1[x] = P.T.L1[x];
   for (int x = t; x < q; x += NT) w1h[x] = P.T.w1h[x];
+  for (int x = t; x < (M + 1) * q; x += NT) WL1[x] = P.T.w1h[x % q] * P.T.L1[x];
   for (int x = t; x < (M + 1) * (M + 1) * (M + 1); x += NT) bidx[x] = -1;
   __syncthreads();
   for (int i = t; i < N; i += NT) bidx[(P.T.idx[i * 3] * (M + 1) + P.T.idx[i * 3 + 1]) * (M + 1) + P.T.idx[i * 3 + 2]] = i;
@@ -538,7 +544,10 @@ __global__ void __launch_bounds__(NT, 2) k_dual_lbfgs_big(DualParams P) {
     for (int a = 0; a < cnt; ++a) {
       double s = 0.0;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) s += r[a * NW + w];
+      for (int w = 0; w < NW; w += 2) {
+        const double2 x = *reinterpret_cast<const double2*>(r + a * NW + w);
+        s += x.x + x.y;
+      }
       v[a] = s;
     }
   };
@@ -655,7 +664,7 @@ __global__ void __launch_bounds__(NT, 2) k_dual_lbfgs_big(DualParams P) {
         for (int o = t; o < (M + 1) * q * q * MS; o += NT) {
           const int a = o % MS, k23 = (o / MS) % (q * q), i1 = o / (MS * q * q);
           double s = 0.0;
-          for (int k1 = 0; k1 < q; ++k1) s = fma(w1h[k1] * L1[i1 * q + k1], u[a * Q + k1 * q * q + k23], s);
+          for (int k1 = 0; k1 < q; ++k1) s = fma(WL1[i1 * q + k1], u[a * Q + k1 * q * q + k23], s);
           T2[o] = s;
         }
         __syncthreads();
@@ -665,7 +674,7 @@ __global__ void __launch_bounds__(NT, 2) k_dual_lbfgs_big(DualParams P) {
           while (pr >= prow(i1 + 1)) ++i1;
           const int i2 = pr - prow(i1);
           double s = 0.0;
-          for (int k2 = 0; k2 < q; ++k2) s = fma(w1h[k2] * L1[i2 * q + k2], T2[((i1 * q + k2) * q + k3) * MS + a], s);
+          for (int k2 = 0; k2 < q; ++k2) s = fma(WL1[i2 * q + k2], T2[((i1 * q + k2) * q + k3) * MS + a], s);
           T1[o] = s;
         }
         __syncthreads();
@@ -674,7 +683,7 @@ __global__ void __launch_bounds__(NT, 2) k_dual_lbfgs_big(DualParams P) {
           const int i = t / MS, a = t - i * MS;
           const int i1 = P.T.idx[i * 3], i2 = P.T.idx[i * 3 + 1], i3 = P.T.idx[i * 3 + 2];
           double s = 0.0;
-          for (int k3 = 0; k3 < q; ++k3) s = fma(w1h[k3] * L1[i3 * q + k3], T1[((prow(i1) + i2) * q + k3) * MS + a], s);
+          for (int k3 = 0; k3 < q; ++k3) s = fma(WL1[i3 * q + k3], T1[((prow(i1) + i2) * q + k3) * MS + a], s);
           gr = s - uh[t];
           g[t] = gr;
         }

@@ -1482,7 +1482,9 @@ static int dual_lbfgs_dispatch(const KernelCtx& k, const DualLaunch& a) {
     if (!(k.closure == CL_EULER && k.m == 4 && k.T.p == 3 && k.T.L1 && n <= NT && k.ad.n_levels == 0)) return -1;
     const size_t smem = (size_t)LbfgsBigLayout<4>::doubles(n, k.T.Q, k.T.npr1 - 1, k.T.q1d, NT / 32) * 8;
     if (smem > k.smem_optin) return -1;
-    auto kern = k_dual_lbfgs_big<CL_EULER, 4, 8, NT>;
+    // config 5's shape (q1d 10, degree 5, p = 3) at compile time
+    auto kern = (k.T.q1d == 10 && k.T.npr1 == 6) ? k_dual_lbfgs_big<CL_EULER, 4, 8, NT, 10, 5>
+                                                 : k_dual_lbfgs_big<CL_EULER, 4, 8, NT>;
     int per_sm = configure(kern, NT, smem);
     if (per_sm < 1) return -1;
     const int grid = (int)std::min<int64_t>(a.cells, (int64_t)k.sm_count * per_sm);
