@@ -25,9 +25,10 @@ def main():
     ap.add_argument("names", nargs="*", default=["cfg1", "cfg2", "cfg3"])
     ap.add_argument("--nx", type=int, default=0)
     ap.add_argument("--steps", type=int, default=0, help="cap on the number of steps (0: to t_end)")
+    ap.add_argument("--hessian", default="newton", choices=["newton", "lbfgs"])
     args = ap.parse_args()
     for name in args.names:
-        cfg = configs.get(name)
+        cfg = configs.get(name, hessian=args.hessian)
         if args.nx and cfg["mesh"]["kind"] == "cart2d":
             cfg["mesh"].update(nx=args.nx, ny=args.nx)
         ma = None
@@ -58,7 +59,7 @@ def main():
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
         rho = uhat[:, 0, 0]
-        out = {"config": name, "cells": g.cells, "steps": n, "t": t, "wall_s": wall,
+        out = {"config": name, "hessian": args.hessian, "cells": g.cells, "steps": n, "t": t, "wall_s": wall,
                "cell_steps_per_s": g.cells * n / wall, "newton_iters_per_cell_step": iters / max(1, g.cells * n),
                "mean_rho0": float(rho.mean()), "min_rho0": float(rho.min()), "dual_kernel": Context.last_dual_kernel()}
         if t_end is None:
