@@ -90,113 +90,7 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
       v[a] = s;
     }
   };
-  // sum-factorised node pass and gradient over the 3D tensor Gauss-Legendre rule (config 5, as
-  // k_dual_lbfgs_big): Lambda = Phi lambda by three 1D stages and Phi^T (omega o u) by their transpose,
-  // the stages in the (then dead) Hessian stage region of the scratch slice and the 1D tables in shared
-  // memory — instead of reading the 448 KB Phi tables from L2 twice per iteration
-  const bool sfe = HBS && P.T.L1 != nullptr && pdim == 3 && P.ad.n_levels == 0;
-  const int Md = sfe ? P.T.npr1 - 1 : 0, npr2 = (Md + 1) * (Md + 2) / 2;
-  double* sL1 = linvf + 64;               // [M+1][q1]
-  double* sWL1 = sL1 + (Md + 1) * q1;     // [M+1][q1] (w_k / 2) L_i(x_k)
-  int* sbidx = reinterpret_cast<int*>(sWL1 + (Md + 1) * q1);  // [(M+1)^3] basis index of (i1, i2, i3)
-  double* T1s = T1;                        // [npr2][q1][MS]
-  double* T2s = T1 + ((npr2 * q1 * MS + 1) & ~1);  // [M+1][q1][q1][MS]
-  if (sfe) {
-    for (int x = t; x < (Md + 1) * q1; x += NT) {
-      sL1[x] = P.T.L1[x];
-      sWL1[x] = P.T.w1h[x % q1] * P.T.L1[x];
-    }
-    for (int x = t; x < (Md + 1) * (Md + 1) * (Md + 1); x += NT) sbidx[x] = -1;
-    __syncthreads();
-    for (int i = t; i < N; i += NT)
-      sbidx[(P.T.idx[i * 3] * (Md + 1) + P.T.idx[i * 3 + 1]) * (Md + 1) + P.T.idx[i * 3 + 2]] = i;
-    __syncthreads();
-  }
-  auto prow = [&](int i1) { return i1 * (Md + 1) - i1 * (i1 - 1) / 2; };
-  auto eval_sf = [&](const double* x, double& s1, double& s2) -> bool {
-    for (int o = t; o < npr2 * q1 * MS; o += NT) {
-      const int a = o % MS, k3 = (o / MS) % q1, pr = o / (MS * q1);
-      int i1 = 0;
-      while (pr >= prow(i1 + 1)) ++i1;
-      const int i2 = pr - prow(i1);
-      double sacc = 0.0;
-      for (int i3 = 0; i3 <= Md - i1 - i2; ++i3)
-        sacc = fma(x[sbidx[(i1 * (Md + 1) + i2) * (Md + 1) + i3] * MS + a], sL1[i3 * q1 + k3], sacc);
-      T1s[o] = sacc;
-    }
-    __syncthreads();
-    for (int o = t; o < (Md + 1) * q1 * q1 * MS; o += NT) {
-      const int a = o % MS, k3 = (o / MS) % q1, k2 = (o / (MS * q1)) % q1, i1 = o / (MS * q1 * q1);
-      double sacc = 0.0;
-      for (int i2 = 0; i2 <= Md - i1; ++i2)
-        sacc = fma(T1s[((prow(i1) + i2) * q1 + k3) * MS + a], sL1[i2 * q1 + k2], sacc);
-      T2s[o] = sacc;
-    }
-    __syncthreads();
-    double v[2] = {0.0, 0.0};
-    bool bad = false;
-    for (int k = t; k < Q; k += NT) {
-      const int k1 = k / (q1 * q1), k23 = k - k1 * q1 * q1;
-      double Lam[MS];
-#pragma unroll
-      for (int a = 0; a < MS; ++a) Lam[a] = 0.0;
-      for (int i1 = 0; i1 <= Md; ++i1) {
-        const double lv = sL1[i1 * q1 + k1];
-#pragma unroll
-        for (int a = 0; a < MS; ++a) Lam[a] = fma(T2s[(i1 * q1 * q1 + k23) * MS + a], lv, Lam[a]);
-      }
-      double u[MS], J[MM], ss;
-      if (!Closure<CL, MS>::eval(Lam, u, J, ss, P.cl)) bad = true;
-      double* row = nb + (size_t)k * NS;
-#pragma unroll
-      for (int a = 0; a < MS; ++a) row[a] = u[a];
-#pragma unroll
-      for (int z = 0; z < MM; ++z) row[MS + z] = J[z];
-      v[0] = fma(omega[k], ss, v[0]);
-      v[1] = fma(omega[k], fabs(ss), v[1]);
-    }
-    if (bad) v[1] = INFINITY;
-    bsum(v, 2);
-    s1 = v[0];
-    s2 = v[1];
-    return isfinite(v[0]) && isfinite(v[1]);
-  };
-  auto grad_sf = [&]() -> double {
-    const int n = N * MS;
-    for (int o = t; o < (Md + 1) * q1 * q1 * MS; o += NT) {  // R1[i1][k2][k3][a]
-      const int a = o % MS, k23 = (o / MS) % (q1 * q1), i1 = o / (MS * q1 * q1);
-      double sacc = 0.0;
-      for (int k1 = 0; k1 < q1; ++k1) sacc = fma(sWL1[i1 * q1 + k1], nb[(size_t)(k1 * q1 * q1 + k23) * NS + a], sacc);
-      T2s[o] = sacc;
-    }
-    __syncthreads();
-    for (int o = t; o < npr2 * q1 * MS; o += NT) {  // R2[i1 i2][k3][a]
-      const int a = o % MS, k3 = (o / MS) % q1, pr = o / (MS * q1);
-      int i1 = 0;
-      while (pr >= prow(i1 + 1)) ++i1;
-      const int i2 = pr - prow(i1);
-      double sacc = 0.0;
-      for (int k2 = 0; k2 < q1; ++k2) sacc = fma(sWL1[i2 * q1 + k2], T2s[((i1 * q1 + k2) * q1 + k3) * MS + a], sacc);
-      T1s[o] = sacc;
-    }
-    __syncthreads();
-    double part[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int r = t; r < n; r += NT) {
-      const int i = r / MS, a = r - i * MS;
-      const int i1 = P.T.idx[i * 3], i2 = P.T.idx[i * 3 + 1], i3 = P.T.idx[i * 3 + 2];
-      double sacc = 0.0;
-      for (int k3 = 0; k3 < q1; ++k3) sacc = fma(sWL1[i3 * q1 + k3], T1s[((prow(i1) + i2) * q1 + k3) * MS + a], sacc);
-      const double gr = sacc - uh[r];
-      g[r] = gr;
-      part[a] = fma(gr, gr, part[a]);
-    }
-    bsum(part, MS);
-    double crit = 0.0;
-    for (int a = 0; a < MS; ++a) crit += sqrt(part[a]);
-    return crit;
-  };
   auto eval = [&](const double* lamv, int Nl, double& s1, double& s2) -> bool {
-    if (sfe) return eval_sf(lamv, s1, s2);
     double v[2] = {0.0, 0.0};
     bool bad = false;
     for (int k = t; k < Q; k += NT) {
@@ -225,7 +119,6 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
     return isfinite(v[0]) && isfinite(v[1]);
   };
   auto grad = [&](int Nl) -> double {
-    if (sfe) return grad_sf();
     const int n = Nl * MS;
     double part[4] = {0.0, 0.0, 0.0, 0.0};
     if (HBS && ((Nl + 7) >> 3) <= 8) {

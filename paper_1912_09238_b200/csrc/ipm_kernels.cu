@@ -1442,11 +1442,8 @@ static int launch_big(const KernelCtx& k, const DualLaunch& a) {
   const size_t smem0 = ((size_t)5 * k.T.N * 4 + 8 * (NT / 32) + ((k.T.q1d * k.T.npr + 1) & ~1) + 8) * 8;
   const size_t nb8 = (size_t)(k.T.N * 4 + 7) / 8;
   const size_t hbl = (nb8 * (nb8 + 1) / 2 * 64 + 64) * 8;  // 8 x 8 blocks + Linv operand
-  // + the 1D tables of the sum-factorised node pass (3D tensor rule): L1, (w/2) L1, basis index table
-  const int Md = k.T.npr1 - 1;
-  const size_t sft = (k.T.L1 && k.T.p == 3) ? ((size_t)2 * (Md + 1) * k.T.q1d + ((Md + 1) * (Md + 1) * (Md + 1) + 1) / 2 + 2) * 8 : 0;
-  const int hb_in_smem = (smem0 + hbl + sft <= k.smem_optin) ? 1 : 0;
-  const size_t smem = smem0 + (hb_in_smem ? hbl + sft : 0);
+  const int hb_in_smem = (smem0 + hbl <= k.smem_optin) ? 1 : 0;
+  const size_t smem = smem0 + (hb_in_smem ? hbl : 0);
   auto kern = hb_in_smem ? k_dual_big<CL_EULER, 4, NT, true> : k_dual_big<CL_EULER, 4, NT, false>;
   configure(kern, 0, smem);
   const int grid = (int)std::min<int64_t>(a.cells, (int64_t)k.big_ctas);
