@@ -712,6 +712,7 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   k.mma_groups = std::getenv("IPM_MMA_GROUPS") ? std::max(1, std::atoi(std::getenv("IPM_MMA_GROUPS"))) : 0;
   k.group_t1 = env_is("IPM_GROUP_T", "1") ? 1 : 0;
   k.flux_choice = env_is("IPM_FLUX_KERNEL", "cart") ? 1 : env_is("IPM_FLUX_KERNEL", "warp") ? 2 : 0;
+  k.flux_scalar_proj = std::getenv("IPM_FLUX_SCALAR_PROJ") ? 1 : 0;
   // per-level nested rules (reading 36): every level's own tables (Phi^T, omega Phi^T, the A-fragment
   // copy, omega) on its Q_l nodes, and the node indices into the finest rule for the flux
   if (level_rules) {

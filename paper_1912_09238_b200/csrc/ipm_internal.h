@@ -170,6 +170,7 @@ struct KernelCtx {
   int mma_groups;    // > 0: cap on the groups per CTA of k_dual_mma
   int group_t1;      // 1: one Hessian block per thread in k_dual_group
   int flux_choice;   // 0 default (strip when applicable), 1 cart, 2 warp
+  int flux_scalar_proj;  // 1: k_flux_warp projects with scalar dot products (IPM_FLUX_SCALAR_PROJ, comparison)
   double* big_scratch;    // per-CTA scratch of the large-cell dual kernel (config 5), or null
   int big_ctas;
   // adaptive degree bucketed into uniform-degree launches (north star (c); Alg. 3): per-level

@@ -1662,7 +1662,7 @@ template <int FX, int MS, int MK>
 static int flux_impl(const KernelCtx& k, const FluxLaunch& a) {
   // per-level rules: the scalar projection with omega Phi^T (1); otherwise the DMMA projection with the
   // A-fragment table (2), staged in shared memory when it fits next to 4 warps' buffers
-  const bool scalar = k.ad.lq.on || std::getenv("IPM_FLUX_SCALAR_PROJ") || k.T.N > 64;
+  const bool scalar = k.ad.lq.on || k.flux_scalar_proj || k.T.N > 64;
   const size_t tab = scalar ? (size_t)k.T.N * k.T.QP * 8 : (size_t)k.T.MT * k.T.KS * 32 * 8;
   // DMMA projection: the per-warp buffer holds the whole rule up to 256 nodes (config 4: one chunk of
   // 144, measured 1.56 ms against 2.23 ms in chunks of 128), chunks of 128 beyond (config 5: 1 000)
