@@ -576,7 +576,9 @@ def run_alt_lbfgs(args, cfg, ma, dev):
     N, m, Q = g.N, g.m, g.Q
     dual_avg = float(np.mean(dual_ms))
     flops = iters / args.steps * flops_lbfgs_per_iteration(N, m, Q) + g.cells * flops_initial(N, m, Q)
-    return {"hessian": "lbfgs", "what": "quasi-Newton dual solve (reading 35, PAPER.md:843), same workload and steps",
+    return {"hessian": "lbfgs", "what": "quasi-Newton dual solve (reading 35, PAPER.md:843), same workload and steps; "
+                                         "it pays far from the warm start (this stress state, One-Shot), not on "
+                                         "smooth time stepping from the IC (DESIGN.md §8 full runs)",
             "value": g.cells * args.steps / (ms / 1e3), "unit": "cell-steps/s", "ms_per_step": ms / args.steps,
             "newton_iters_per_cell_step": iters / (g.cells * args.steps), "failed_cells": int(failed),
             "kernel": Context.last_dual_kernel(), "dual_ms_avg": dual_avg, "flux_ms_avg": float(np.mean(flux_ms)),
