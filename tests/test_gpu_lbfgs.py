@@ -174,3 +174,26 @@ def test_lbfgs_matches_newton_solution(torch):
     assert w == 0 and nf == 0
     gb.lbfgs_reset()
     assert int(gb.lbfgs_history()[2].sum()) == 0
+
+
+def test_lbfgs_step_host_matches_device_step(torch):
+    """ipm_step_host (chunked copy/solve ranges: L-BFGS histories and the Newton-fallback lists of
+    each range offset into the context's arrays) equals ipm_step bit for bit"""
+    from paper_1912_09238_b200 import Context
+
+    cfg = dict(configs.get("cfg3", mesh=dict(nx=17, ny=13)), hessian="lbfgs", max_newton=12)
+    ga, gb = Context(cfg), Context(cfg)
+    import oracle
+
+    o = oracle.Oracle(cfg)
+    _, _, u = _stress_both(torch, ga, o, cfg, None, seed=41)
+    lam = ga.zeros()
+    ga.ipm_warm_start(u, lam)
+    ref_u, ref_l = u.clone(), lam.clone()
+    h_u, h_l = u.cpu().pin_memory(), lam.cpu().pin_memory()
+    d_u, d_l = gb.zeros(), gb.zeros()
+    for _ in range(3):
+        ia = ga.ipm_step(ref_u, ref_l)
+        ib = gb.ipm_step_host(h_u, h_l, d_u, d_l, None, nchunks=7)
+        assert ia.newton_iters == ib.newton_iters and ia.dt == ib.dt and ia.failed_cells == 0
+    assert torch.equal(h_u, ref_u.cpu()) and torch.equal(h_l, ref_l.cpu())
