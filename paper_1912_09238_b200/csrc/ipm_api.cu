@@ -323,6 +323,8 @@ struct ipm_ctx {
   // indices ascending, for ipm_step_dual_boundary / ipm_step_dual_interior
   int32_t *d_bnd = nullptr, *d_int = nullptr;
   int64_t n_bnd = 0, n_int = 0;
+  // triangle meshes: the flux kernel's processing order (Morton order of the owned cells' centroids)
+  int32_t* d_order = nullptr;
 };
 
 // the L-BFGS history of cells [r0, ...) for a dual launch (nothing for Newton contexts)
@@ -853,6 +855,16 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
     ipm_destroy(c);
     return fail(IPM_ERR_ARG, "hessian_kind must be 0 (Newton) or 1 (L-BFGS)");
   }
+  if (C.mesh_kind == IPM_MESH_TRI && cells > 0 && !std::getenv("IPM_FLUX_INDEX_ORDER")) {
+    std::vector<int32_t> ord;
+    ipm::morton_order(std::vector<double>(Lm.cx.begin(), Lm.cx.begin() + cells),
+                      std::vector<double>(Lm.cy.begin(), Lm.cy.begin() + cells), ord);
+    c->d_order = dalloc<int32_t>(ord.size(), c->owned);
+    if (!c->d_order || up(c->d_order, ord.data(), ord.size() * 4)) {
+      ipm_destroy(c);
+      return fail(IPM_ERR_CUDA, "flux order upload failed");
+    }
+  }
   // boundary / interior cell lists (distributed contexts without adaptive levels: the list launches use the
   // uniform-degree kernels)
   if (nranks > 1 && C.n_levels == 0 && !c->part.send_local.empty()) {
@@ -1011,6 +1023,7 @@ ipm_status ipm_flux_update(ipm_ctx* c, const double* d_lambda, const double* d_u
   }
   if (int rc = ipm::launch_dt(k, -1.0, dt, c->cfg.cfl)) return launch_rc(rc, "dt");
   ipm::FluxLaunch f{c->d_uq, d_uhat_old, d_uhat_new, nullptr, nullptr, c->cfg.update_form, c->cfg.cfl};
+  f.order = c->d_order;
   if (c->band_rows) {
     if (int rc = band_flux(c, d_lambda, f)) return launch_rc(rc, "flux (bands)");
   } else if (int rc = ipm::launch_flux(k, f)) {
@@ -1117,6 +1130,7 @@ ipm_status ipm_step_flux(ipm_ctx* c, double* d_uhat, double* d_lambda, const dou
   if (int rc = ipm::launch_dt(k, t_end, -1.0, c->cfg.cfl)) return launch_rc(rc, "dt");
   const int32_t* lvl_new = c->cfg.n_levels > 0 ? c->d_level_new : nullptr;
   ipm::FluxLaunch f{c->d_uq, d_uhat, d_uhat, lvl_new, d_lambda, c->cfg.update_form, c->cfg.cfl};
+  f.order = c->d_order;
   if (c->timing) cudaEventRecord(c->ev[2], c->stream);
   // per-level nested rules (reading 36): every owned cell's states at every node of the finest rule
   // from its duals at its old level (the flux of a cell at level l reads the nodes of Q_l)

@@ -34,6 +34,8 @@ struct Partition {
 };
 
 bool build_mesh(const ipm_config& C, MeshTables& M, std::string& err);
+// cells in Morton order of their centroids (a processing order, not a renumbering)
+void morton_order(const std::vector<double>& cx, const std::vector<double>& cy, std::vector<int32_t>& order);
 bool build_partition(const ipm_config& C, const MeshTables& G, int rank, int nranks, Partition& P, std::string& err);
 // local face tables of a partition (neighbours remapped to local / halo indices)
 void local_tables(const MeshTables& G, const Partition& P, MeshTables& L);

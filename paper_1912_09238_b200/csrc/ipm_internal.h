@@ -145,6 +145,9 @@ struct FluxLaunch {
   // c >= n_owned at uq_halo + (c - n_owned) Q m
   int64_t cell0, uq_base, n_owned;
   const double* uq_halo;
+  // processing order of the cells (k_flux_warp on triangle meshes: Morton order of the centroids, so the
+  // node states of a cell's neighbours are read while still in L2; nullable = index order)
+  const int32_t* order;
 };
 
 // Everything a launcher needs.

@@ -478,7 +478,8 @@ __global__ void __launch_bounds__(256) k_flux_warp(FluxParams P) {
     if (A.uq_halo && c >= A.n_owned) return A.uq_halo + (c - A.n_owned) * Q * MS;
     return A.uq + (c - A.uq_base) * Q * MS;
   };
-  for (int64_t cell = A.cell0 + (int64_t)blockIdx.x * nw + warp; cell < P.mesh.cells; cell += total_warps) {
+  for (int64_t idx = A.cell0 + (int64_t)blockIdx.x * nw + warp; idx < P.mesh.cells; idx += total_warps) {
+    const int64_t cell = A.order ? (int64_t)A.order[idx] : idx;
     // per-level nested rules (reading 36): the update at level l^{n+1} integrates with that level's
     // rule, at its nodes kf of the finest rule (eq. adaptiveFVUpdate)
     const int Lq = (P.ad.lq.on && A.level_new) ? A.level_new[cell] : -1;

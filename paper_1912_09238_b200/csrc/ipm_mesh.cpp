@@ -130,6 +130,29 @@ static uint64_t morton2(uint32_t x, uint32_t y) {
   return spread(x) | (spread(y) << 1);
 }
 
+// processing order of cells by the Morton code of their centroids (neighbours close in time: their node
+// states are reused from L2 by the flux kernel)
+void morton_order(const std::vector<double>& cx, const std::vector<double>& cy, std::vector<int32_t>& order) {
+  const int64_t n = (int64_t)cx.size();
+  order.resize(n);
+  if (n == 0) return;
+  double x0 = cx[0], x1 = cx[0], y0 = cy[0], y1 = cy[0];
+  for (int64_t j = 0; j < n; ++j) {
+    x0 = std::min(x0, cx[j]);
+    x1 = std::max(x1, cx[j]);
+    y0 = std::min(y0, cy[j]);
+    y1 = std::max(y1, cy[j]);
+  }
+  std::vector<std::pair<uint64_t, int64_t>> key(n);
+  for (int64_t j = 0; j < n; ++j) {
+    const uint32_t qx = (uint32_t)std::lround((cx[j] - x0) / std::max(x1 - x0, 1e-300) * 65535.0);
+    const uint32_t qy = (uint32_t)std::lround((cy[j] - y0) / std::max(y1 - y0, 1e-300) * 65535.0);
+    key[j] = {morton2(qx, qy), j};
+  }
+  std::sort(key.begin(), key.end());
+  for (int64_t s = 0; s < n; ++s) order[s] = (int32_t)key[s].second;
+}
+
 bool build_partition(const ipm_config& C, const MeshTables& G, int rank, int nranks, Partition& P,
                      std::string& err) {
   if (nranks < 1 || rank < 0 || rank >= nranks) return err = "rank / nranks", false;

@@ -9,3 +9,5 @@ IPM_DIST_BACKEND=gloo timeout 900 python bench.py --gpus 2 --steps 2 --warmup 3 
 IPM_DIST_BACKEND=gloo timeout 900 python bench.py --gpus 2 --hessian lbfgs --steps 2 --warmup 3 --nx 256 --no-e2e > gpurun_out/r02ac_multirank_gloo_2_lbfgs.json 2>&1
 bash tools/profile_round.sh r02ac
 IPM_LIB=paper_1912_09238_b200/libipm_prof.so timeout 300 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-alt > gpurun_out/r02ac_strip_prof.txt 2>&1
+timeout 600 python bench.py --config cfg4 --no-cpu-baseline --no-e2e --no-alt > gpurun_out/r02ac_cfg4_morton.json 2>&1
+IPM_FLUX_INDEX_ORDER=1 timeout 600 python bench.py --config cfg4 --no-cpu-baseline --no-e2e --no-alt > gpurun_out/r02ac_cfg4_index_order.json 2>&1
