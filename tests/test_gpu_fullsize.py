@@ -66,7 +66,8 @@ def test_dual_solve_full_size_sampled(torch, name, nx):
     g.ipm_dual_solve(u, lam, "full", it, st)
     torch.cuda.synchronize()
     rng = np.random.default_rng(5)
-    cells = np.sort(rng.choice(g.cells, size=N_SAMPLE if name == "cfg3" else 12, replace=False))
+    # SURVEY 8(c) protocol: 1 000 sampled cells of the full config-3 mesh
+    cells = np.sort(rng.choice(g.cells, size=1000 if name == "cfg3" else 12, replace=False))
     o, u_o, lam_o = _oracle_cells(cfg, base, z, amp, cells)
     it_o, st_o, _ = o.dual_solve_all(u_o, lam_o)
     lg, itg, stg = to_np(lam)[cells], to_np(it)[cells], to_np(st)[cells]
@@ -163,3 +164,39 @@ def test_cfg4_full_mesh_one_shot_sampled(torch):
         err = (np.abs(un[c] - new_o[0]) / sc).max()
         assert err < 1e-9, (c, err)
         checked += 1
+
+
+def test_dual_solve_cfg5_baseline_size_sampled(torch):
+    """config 5 at its BASELINE size (4096^2 = 16.8 M cells, n = 224, Q = 1 000, banded node states) on
+    one GPU: one full-Newton dual solve of the whole mesh from the seeded stress state, 64 sampled
+    cells against the oracle (sampled cells at 4096^2); two state arrays as bench.py"""
+    from paper_1912_09238_b200 import Context
+
+    cfg = configs.get("cfg5")
+    g = Context(cfg)
+    base, z, amp = stress_inputs(cfg, seed=78)
+    rng = np.random.default_rng(6)
+    cells = np.sort(rng.choice(g.cells, size=64, replace=False))
+    zs, bs = z[cells].copy(), base[cells].copy()
+    lam = g.zeros()
+    d_b, d_z = torch.from_numpy(base).cuda(), torch.from_numpy(z).cuda()
+    del z
+    g.ipm_stress_dual(d_b, d_z, amp[0], amp[1], lam)
+    del d_b, d_z
+    torch.cuda.empty_cache()
+    u = g.zeros()
+    g.ipm_moments_from_dual(lam, u)
+    g.ipm_warm_start(u, lam)
+    it = g.zeros(g.cells, dtype=torch.int32)
+    st = g.zeros(g.cells, dtype=torch.int32)
+    g.ipm_dual_solve(u, lam, "full", it, st)
+    torch.cuda.synchronize()
+    assert int((st != 0).sum()) == 0
+    o, u_o, lam_o = _oracle_cells(cfg, bs, zs, amp, np.arange(len(cells)))
+    it_o, st_o, _ = o.dual_solve_all(u_o, lam_o)
+    idx = torch.from_numpy(cells).cuda()
+    lg, itg = to_np(lam[idx]), to_np(it[idx])
+    assert (st_o == 0).all()
+    assert np.abs(itg - it_o).max() <= 1
+    scale = np.abs(lam_o).max(axis=(0, 1))
+    assert (np.abs(lg - lam_o) / scale).max() < 1e-9
