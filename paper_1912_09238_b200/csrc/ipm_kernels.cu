@@ -444,8 +444,11 @@ struct FluxParams {
 // CH: the node loop in chunks of P.qchunk nodes with the DMMA projection accumulated across chunks (16
 // accumulator registers live through the loop: config 5, Q = 1 000); otherwise one pass over the rule and
 // the projection tile by tile afterwards (config 4: fewer registers, more CTAs per SM)
+#ifndef IPM_FLUXW_MINB
+#define IPM_FLUXW_MINB 1  // CTAs per SM the register allocation must allow (A/B: 3)
+#endif
 template <int FX, int MS, int MK, bool CH>
-__global__ void __launch_bounds__(256) k_flux_warp(FluxParams P) {
+__global__ void __launch_bounds__(256, IPM_FLUXW_MINB) k_flux_warp(FluxParams P) {
   extern __shared__ __align__(16) double sm[];
   const int N = P.T.N, Q = P.T.Q, QP = P.T.QP;
   // basis table staged in shared memory when it fits (P.tables_in_smem), else read from L2

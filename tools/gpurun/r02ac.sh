@@ -11,3 +11,4 @@ bash tools/profile_round.sh r02ac
 IPM_LIB=paper_1912_09238_b200/libipm_prof.so timeout 300 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-alt > gpurun_out/r02ac_strip_prof.txt 2>&1
 timeout 600 python bench.py --config cfg4 --no-cpu-baseline --no-e2e --no-alt > gpurun_out/r02ac_cfg4_morton.json 2>&1
 IPM_FLUX_INDEX_ORDER=1 timeout 600 python bench.py --config cfg4 --no-cpu-baseline --no-e2e --no-alt > gpurun_out/r02ac_cfg4_index_order.json 2>&1
+BENCH_ARGS="--config cfg4 --no-alt" bash tools/ab_bench.sh "" fw3 "" fw3 > gpurun_out/r02ac_ab_fluxwarp_minb3.txt 2>&1
