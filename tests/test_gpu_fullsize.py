@@ -191,11 +191,26 @@ def test_dual_solve_cfg5_baseline_size_sampled(torch):
     st = g.zeros(g.cells, dtype=torch.int32)
     g.ipm_dual_solve(u, lam, "full", it, st)
     torch.cuda.synchronize()
-    assert int((st != 0).sum()) == 0
+    idx = torch.from_numpy(cells).cuda()
+    lg, itg, stg = to_np(lam[idx]), to_np(it[idx]), to_np(st[idx])
+    # the stress state's tail holds a handful of cells whose full-Newton solve does not converge (r02ac:
+    # 4 of 16.8 M); those must fail in the oracle as well (status parity), all others converge
+    bad = to_np(torch.nonzero(st != 0).flatten())
+    assert len(bad) <= 16, f"{len(bad)} non-converged cells"
+    if len(bad):
+        st_bad = to_np(st[torch.from_numpy(bad).cuda()])
+        del u, lam, it, st
+        torch.cuda.empty_cache()
+        base_b, z_b, _ = stress_inputs(cfg, seed=78)
+        zb, bb = z_b[bad].copy(), base_b[bad].copy()
+        del base_b, z_b
+        ob, ub, lb = _oracle_cells(cfg, bb, zb, amp, np.arange(len(bad)))
+        _, st_ob, _ = ob.dual_solve_all(ub, lb)
+        st_ob = np.asarray(st_ob)
+        assert (st_ob != 0).all(), f"cells {bad.tolist()}: GPU statuses {st_bad.tolist()}, oracle {st_ob.tolist()}"
     o, u_o, lam_o = _oracle_cells(cfg, bs, zs, amp, np.arange(len(cells)))
     it_o, st_o, _ = o.dual_solve_all(u_o, lam_o)
-    idx = torch.from_numpy(cells).cuda()
-    lg, itg = to_np(lam[idx]), to_np(it[idx])
+    assert (np.asarray(st_o) == np.asarray(stg)).all()
     assert (st_o == 0).all()
     assert np.abs(itg - it_o).max() <= 1
     scale = np.abs(lam_o).max(axis=(0, 1))
