@@ -203,6 +203,20 @@ __device__ __forceinline__ bool blk8_factor_rows(double& a0, double& a1, int lan
   return ok;
 }
 
+// Stored 8 x 8 blocks of the fragment exchange (pan, panA, linvf): row r at MMA_ROW(r) = 8 r + 4 (r / 2),
+// block extent 76, stride MMA_BS = 80.  The skew of 4 doubles every second row makes the A-fragment loads (lane:
+// row l/4, columns l%4 and l%4 + 4) conflict-free — with the plain r * 8 rows, rows r and r + 2 of a
+// half-warp fell into the same banks (2-way conflicts, ncu r02q: 5.1 G excess shared wavefronts per
+// launch) — and keeps the B-fragment loads (column-wise) and the double2 C-fragment stores
+// conflict-free; both offsets of a fragment still differ by an immediate (+4 / +40 doubles).
+#ifdef IPM_MMA_BLK64  // A/B: the unskewed layout
+#define MMA_ROW(r) ((r) * 8)
+#define MMA_BS 64
+#else
+#define MMA_ROW(r) ((r) * 8 + 4 * ((r) >> 1))
+#define MMA_BS 80
+#endif
+
 template <int MS>
 struct MmaLayout {
   static constexpr int MM = MS * (MS + 1) / 2;
@@ -213,6 +227,10 @@ struct MmaLayout {
   //                      [T chunk q1 x NPR x CHW] at offset TO (SF only)
   // S may overlap the dead part of the node buffer chunk by chunk (see s_base)
   static __host__ __device__ int npp(int N) { return N * (N + 1) / 2; }
+  // stage-2 work list of the sum factorisation (SF > 0): pairs grouped two by two with a common 1D pair
+  // index pr2, slots [2 * NEMAX] ints + the pr2 histogram [npr] + the entry count, in doubles
+  static __host__ __device__ int nemax(int N, int npr) { return (N * (N + 1) / 2 + npr) / 2 + 1; }
+  static __host__ __device__ int pairlist_doubles(int N, int npr) { return (nemax(N, npr) + (npr + 2) / 2 + 1) & ~1; }
   // row stride of S[ab][pair]: odd, so the gather's rows (different ab) fall into different banks
   static __host__ __device__ int nps(int N) { return npp(N) | 1; }
   static __host__ __device__ int node(int Q) { return Q * (MS + MM); }
@@ -236,9 +254,9 @@ struct MmaLayout {
     const int t = t_off(N, Q, SF) + ((SF > 0) ? q1d * (SF * (SF + 1) / 2) * CHW : 0);
     if (t > r) r = t;
 #ifdef IPM_MMA_LDL  // + the unscaled panel [NB][64] and w = D^{-1} z [NB * 8]
-    const int c = (3 * NB + 1) * 64 + NB * 8;
+    const int c = (2 * NB + 1) * MMA_BS + NB * 64 + NB * 8;
 #else
-    const int c = (2 * NB + 1) * 64;  // Cholesky: panel [NB][64], Linv fragment [64], diagonal [NB][64]
+    const int c = (NB + 1) * MMA_BS + NB * 64;  // Cholesky: panel [NB][BS], Linv fragment [BS], diagonal [NB][64]
 #endif
     if (c > r) r = c;
     return (r + 1) & ~1;
@@ -277,7 +295,7 @@ struct DualMma {
   // block storage in shared memory for fragment exchange: row-major, element (r, c) at r*8 + c.
   // (An XOR swizzle that also removes the 2-way conflicts of the A/B-fragment loads measured 3 %
   // slower: the extra index arithmetic costs more than the conflicts.)
-  __device__ static int bpos(int r, int c) { return r * 8 + c; }
+  __device__ static int bpos(int r, int c) { return MMA_ROW(r) + c; }
   __device__ static void store_afrag(double* dst, double c0, double c1, int lane) {
     const int r = lane >> 2, q = lane & 3;
     double2* p = reinterpret_cast<double2*>(dst + bpos(r, 2 * q));
@@ -316,15 +334,15 @@ struct DualMma {
                                     int lane, int bar) {
     constexpr int wr = WR;
     const int r = lane >> 2, q = lane & 3;
-    double* pan = reg;                // [NB][64]
-    double* linvf = reg + NB * 64;    // [64]
-    double* dg = reg + NB * 64 + 64;  // [NB][64]
+    double* pan = reg;                          // [NB][MMA_BS]
+    double* linvf = reg + NB * MMA_BS;          // [MMA_BS]
+    double* dg = reg + NB * MMA_BS + MMA_BS;    // [NB][64] (C-fragment order, lane-contiguous)
 #ifdef IPM_MMA_LDL
     // block LDL^T: L_IK = A_IK D_K^{-1} (pan), the unscaled A_IK (panA) for the trailing updates
     // A_IJ -= L_IK A_JK^T, D_K^{-1} by Gauss-Jordan (linvf), forward z_I -= L_IK z_K (dd), w = D^{-1} z (ww),
     // back substitution d_K = w_K - sum_{I > K} L_IK^T d_I
-    double* panA = dg + NB * 64;  // [NB][64]
-    double* ww = panA + NB * 64;  // [NB * 8]
+    double* panA = dg + NB * 64;      // [NB][MMA_BS]
+    double* ww = panA + NB * MMA_BS;  // [NB * 8]
 #else
     double* const panA = pan;
 #endif
@@ -442,18 +460,18 @@ struct DualMma {
             if constexpr (br < NBO) {
               constexpr int I = oI(br), J = oJ(br);
               if constexpr (J == K) {
-                if (I < NBl) fn(s, pan + I * 64, I);
+                if (I < NBl) fn(s, pan + I * MMA_BS, I);
               }
             }
           });
         };
-        each_panel([&](int s, double* pI, int I) { store_afrag(panA + I * 64, blk[s][0], blk[s][1], lane); });
+        each_panel([&](int s, double* pI, int I) { store_afrag(panA + I * MMA_BS, blk[s][0], blk[s][1], lane); });
         __syncwarp();
         double lf0, lf1;
         afrag_ld(linvf, lf0, lf1);
         each_panel([&](int s, double* pI, int I) {
           double f0, f1;
-          afrag_ld(panA + I * 64, f0, f1);
+          afrag_ld(panA + I * MMA_BS, f0, f1);
           double x0 = 0.0, x1 = 0.0;
           dmma884(x0, x1, f0, lf0);
           dmma884(x0, x1, f1, lf1);
@@ -483,8 +501,8 @@ struct DualMma {
           double2 v = *reinterpret_cast<const double2*>(dg + K1 * 64 + 2 * lane);
           if constexpr (K >= 0) {
             double p0, p1, pa0, pa1;
-            afrag_ld(pan + K1 * 64, p0, p1);
-            afrag_ld(panA + K1 * 64, pa0, pa1);
+            afrag_ld(pan + K1 * MMA_BS, p0, p1);
+            afrag_ld(panA + K1 * MMA_BS, pa0, pa1);
             dmma884(v.x, v.y, dneg(p0), pa0);
             dmma884(v.x, v.y, dneg(p1), pa1);
           }
@@ -523,8 +541,8 @@ struct DualMma {
             if (Jd < NBl) {
               double2 v = *reinterpret_cast<const double2*>(dg + Jd * 64 + 2 * lane);
               double p0, p1, pa0, pa1;
-              afrag_ld(pan + Jd * 64, p0, p1);
-              afrag_ld(panA + Jd * 64, pa0, pa1);
+              afrag_ld(pan + Jd * MMA_BS, p0, p1);
+              afrag_ld(panA + Jd * MMA_BS, pa0, pa1);
               dmma884(v.x, v.y, dneg(p0), pa0);
               dmma884(v.x, v.y, dneg(p1), pa1);
               *reinterpret_cast<double2*>(dg + Jd * 64 + 2 * lane) = v;
@@ -538,8 +556,8 @@ struct DualMma {
             if constexpr (J > K) {
               if (I < NBl) {
                 double a0, a1, b0, b1;
-                afrag_ld(pan + I * 64, a0, a1);
-                afrag_ld(panA + J * 64, b0, b1);
+                afrag_ld(pan + I * MMA_BS, a0, a1);
+                afrag_ld(panA + J * MMA_BS, b0, b1);
                 dmma884(blk[s][0], blk[s][1], dneg(a0), b0);
                 dmma884(blk[s][0], blk[s][1], dneg(a1), b1);
               }
@@ -669,13 +687,31 @@ __global__ void __launch_bounds__(IPM_MMA_THREADS) k_dual_mma(DualParams P) {
   // per pair p = i(i+1)/2 + j: the 1D pair indices (pr1, pr2) of the sum factorisation, packed
   int* sPR = (int*)(sWF + MTT * KS * 32);
   const int NPT = N * (N + 1) / 2;
-  const int tabsz = 2 * N * QP + ((SF > 0) ? ((q1 * NPR + 1) & ~1) : 0) + MTT * KS * 32 + ((NPT + 3) / 4) * 2;
+  // the sum factorisation's first-stage B operand LL[k2][pr2] in B-fragment order [KSs][NTs][32 lanes]
+  // (read per lane as LL[k2 * NPR + pr] its rows k2 = 4ks + lane%4 fell 4-way onto the same banks)
+  constexpr int NTS1 = (NPR + 7) / 8;
+  const int KSS1 = (SF > 0) ? (q1 + 3) / 4 : 0;
+  double* sLLF = sm + 2 * N * QP + ((SF > 0) ? ((q1 * NPR + 1) & ~1) : 0) + MTT * KS * 32 + ((NPT + 3) / 4) * 2;
+  // stage-2 work list: slot 2e, 2e+1 of entry e = two pairs with the same pr2 (p | pr1 << 12 | pr2 << 20; -1
+  // empty), so one thread forms both from one read of the T row (r02ac: the per-pair T reads were 10 % of
+  // the kernel's shared-memory wavefronts)
+  const int NEMAX = Lay::nemax(N, NPR);
+  int* sSlot = (int*)(sLLF + KSS1 * NTS1 * 32);
+  int* sHist = sSlot + 2 * NEMAX;  // [NPR] + the entry count
+  const int tabsz = 2 * N * QP + ((SF > 0) ? ((q1 * NPR + 1) & ~1) : 0) + MTT * KS * 32 + ((NPT + 3) / 4) * 2 +
+                    KSS1 * NTS1 * 32 + ((SF > 0) ? Lay::pairlist_doubles(N, NPR) : 0);
   for (int x = threadIdx.x; x < N * QP; x += blockDim.x) {
     sPhiT[x] = P.T.PhiT[x];
     sWPhiT[x] = P.T.WPhiT[x];
   }
-  if (SF > 0)
+  if (SF > 0) {
     for (int x = threadIdx.x; x < q1 * NPR; x += blockDim.x) sLL[x] = P.T.LL[x];
+    for (int x = threadIdx.x; x < KSS1 * NTS1 * 32; x += blockDim.x) {
+      const int ln = x & 31, nt = (x >> 5) % NTS1, ks = (x >> 5) / NTS1;
+      const int k2 = 4 * ks + (ln & 3), pr = 8 * nt + (ln >> 2);
+      sLLF[x] = (k2 < q1 && pr < NPR) ? P.T.LL[k2 * NPR + pr] : 0.0;
+    }
+  }
   for (int x = threadIdx.x; x < MTT * KS * 32; x += blockDim.x) sWF[x] = P.T.WPhiF[x];
   if constexpr (SF > 0) {
     for (int p = threadIdx.x; p < NPT; p += blockDim.x) {
@@ -686,6 +722,24 @@ __global__ void __launch_bounds__(IPM_MMA_THREADS) k_dual_mma(DualParams P) {
       if (a1 > b1) { const int x = a1; a1 = b1; b1 = x; }
       if (a2 > b2) { const int x = a2; a2 = b2; b2 = x; }
       sPR[p] = (a1 * SF - a1 * (a1 - 1) / 2 + (b1 - a1)) | ((a2 * SF - a2 * (a2 - 1) / 2 + (b2 - a2)) << 16);
+    }
+    for (int x = threadIdx.x; x < 2 * NEMAX; x += blockDim.x) sSlot[x] = -1;
+    for (int x = threadIdx.x; x < NPR; x += blockDim.x) sHist[x] = 0;
+    __syncthreads();
+    for (int p = threadIdx.x; p < NPT; p += blockDim.x) atomicAdd(&sHist[sPR[p] >> 16], 1);
+    __syncthreads();
+    // padded order: pairs sorted by (pr2, p), every pr2 group padded to an even length
+    for (int p = threadIdx.x; p < NPT; p += blockDim.x) {
+      const int pr2 = sPR[p] >> 16;
+      int pos = 0;
+      for (int q = 0; q < pr2; ++q) pos += (sHist[q] + 1) & ~1;
+      for (int p2 = 0; p2 < p; ++p2) pos += (sPR[p2] >> 16) == pr2;
+      sSlot[pos] = p | ((sPR[p] & 0xffff) << 12) | (pr2 << 20);
+    }
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int q = 0; q < NPR; ++q) tot += (sHist[q] + 1) & ~1;
+      sHist[NPR] = tot / 2;
     }
   }
   __syncthreads();
@@ -766,11 +820,7 @@ __global__ void __launch_bounds__(IPM_MMA_THREADS) k_dual_mma(DualParams P) {
               const int k2 = 4 * ks + lq;  // A column / B row of this lane
               const double av = (rok && k2 < q1) ? jrow[k2] : 0.0;
 #pragma unroll
-              for (int nt = 0; nt < NTs; ++nt) {
-                const int pr = 8 * nt + lr;
-                const double bv = (k2 < q1 && pr < NPR) ? sLL[k2 * NPR + pr] : 0.0;
-                dmma884(acc[nt][0], acc[nt][1], av, bv);
-              }
+              for (int nt = 0; nt < NTs; ++nt) dmma884(acc[nt][0], acc[nt][1], av, sLLF[(ks * NTs + nt) * 32 + lane]);
             }
             // C-fragment (row 8mt + lr, columns 8nt + 2lq + e) -> T[k1][pr2][c]
             if (rok) {
@@ -786,22 +836,33 @@ __global__ void __launch_bounds__(IPM_MMA_THREADS) k_dual_mma(DualParams P) {
         }
         gsync();
         // stage 2: S[ab0+c][pair] = sum_k1 LL[k1][pr1] T[k1][pr2][c]
+        const int NE = sHist[NPR];
 #pragma unroll 1
-        for (int p = t; p < NPl; p += G) {
-          const int prp = sPR[p], pr1 = prp & 0xffff, pr2 = prp >> 16;
-          double acc[CHW];
+        for (int e = t; e < NE; e += G) {
+          const int sa = sSlot[2 * e], sb = sSlot[2 * e + 1];
+          const int pa = sa & 0xfff, pr1a = (sa >> 12) & 0xff, pr2 = sa >> 20;
+          const bool hb = sb >= 0;
+          const int pb = sb & 0xfff, pr1b = hb ? (sb >> 12) & 0xff : pr1a;
+          double acc[CHW], acb[CHW];
 #pragma unroll
-          for (int c = 0; c < CHW; ++c) acc[c] = 0.0;
+          for (int c = 0; c < CHW; ++c) acc[c] = acb[c] = 0.0;
 #pragma unroll 2
           for (int k1 = 0; k1 < q1; ++k1) {
-            const double lv = sLL[k1 * NPR + pr1];
+            const double la = sLL[k1 * NPR + pr1a], lb = sLL[k1 * NPR + pr1b];
             const double* Tk = Tt + (k1 * NPR + pr2) * CHW;
 #pragma unroll
-            for (int c = 0; c < CHW; ++c) acc[c] = fma(lv, Tk[c], acc[c]);
+            for (int c = 0; c < CHW; ++c) {
+              const double tv = Tk[c];
+              acc[c] = fma(la, tv, acc[c]);
+              acb[c] = fma(lb, tv, acb[c]);
+            }
           }
 #pragma unroll
           for (int c = 0; c < CHW; ++c)
-            if (c < nab) Sx[(ab0 + c) * npp + p] = acc[c];
+            if (c < nab) {
+              if (pa < NPl) Sx[(ab0 + c) * npp + pa] = acc[c];
+              if (hb && pb < NPl) Sx[(ab0 + c) * npp + pb] = acb[c];
+            }
         }
         gsync();  // T chunk is rewritten by the next chunk; S complete after the last
       }

@@ -444,11 +444,14 @@ struct FluxParams {
 // CH: the node loop in chunks of P.qchunk nodes with the DMMA projection accumulated across chunks (16
 // accumulator registers live through the loop: config 5, Q = 1 000); otherwise one pass over the rule and
 // the projection tile by tile afterwards (config 4: fewer registers, more CTAs per SM)
+// Launch bound: the single-pass instance is built for 3 CTAs per SM (80 registers, no spills; 140
+// registers and one CTA per SM otherwise): config 4 flux 2.49 -> 1.25 ms (r02ac_ab_fluxwarp_minb3.txt);
+// the chunked instance keeps its registers (80 would spill ~600 bytes).
 #ifndef IPM_FLUXW_MINB
-#define IPM_FLUXW_MINB 1  // CTAs per SM the register allocation must allow (A/B: 3)
+#define IPM_FLUXW_MINB 3  // CTAs per SM of the single-pass instance (A/B: 1)
 #endif
 template <int FX, int MS, int MK, bool CH>
-__global__ void __launch_bounds__(256, IPM_FLUXW_MINB) k_flux_warp(FluxParams P) {
+__global__ void __launch_bounds__(256, CH ? 1 : IPM_FLUXW_MINB) k_flux_warp(FluxParams P) {
   extern __shared__ __align__(16) double sm[];
   const int N = P.T.N, Q = P.T.Q, QP = P.T.QP;
   // basis table staged in shared memory when it fits (P.tables_in_smem), else read from L2
@@ -1379,7 +1382,9 @@ static int dual_mma_impl(const KernelCtx& k, const DualLaunch& a) {
   constexpr int G = 32 * W;
   const int npr = SF * (SF + 1) / 2;
   const size_t tab = ((size_t)2 * k.T.N * k.T.QP + (SF > 0 ? ((k.T.q1d * npr + 1) & ~1) : 0) +
-                      (size_t)k.T.MT * k.T.KS * 32 + ((size_t)k.T.N * (k.T.N + 1) / 2 + 3) / 4 * 2) * 8;
+                      (size_t)k.T.MT * k.T.KS * 32 + ((size_t)k.T.N * (k.T.N + 1) / 2 + 3) / 4 * 2 +
+                      (SF > 0 ? (size_t)((k.T.q1d + 3) / 4) * ((npr + 7) / 8) * 32 : 0) +  // + sLLF
+                      (SF > 0 ? (size_t)Lay::pairlist_doubles(k.T.N, npr) : 0)) * 8;    // + stage-2 list
   const size_t pg = (size_t)Lay::per_group(k.T.N, k.T.Q, W, SF, k.T.q1d, NB) * 8;
   if (tab + pg > k.smem_optin) return -1;
   int groups = (int)((k.smem_optin - tab) / pg);
