@@ -39,6 +39,20 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
   // same element of consecutive blocks hit different banks (a 128-byte block stride would put them all
   // in one bank)
 #define SW(pb, x) (HBS ? ((x) ^ ((pb) & 15)) : (x))
+  // HBS 8 x 8 blocks (and linvf): element (r, c) at r * 8 + (c ^ 4 (r & 2)) — the two column halves of
+  // rows 2, 3, 6, 7 swapped, so the A/B-fragment loads (lane: row l/4, columns l%4 and l%4 + 4) of a
+  // half-warp spread over all banks (plain rows put rows r and r + 2 on the same banks: 2-way
+  // conflicts); the double2 C-fragment accesses stay aligned and conflict-free
+//   and the whole element index XOR (2 b) & 14 for block b (a bijection inside the block that keeps both
+//   properties), so that the Hessian scatter (one thread per basis pair, consecutive lanes in
+//   consecutive blocks 64 doubles apart) spreads over 8 bank groups instead of hitting one
+#ifdef IPM_BIG_NOSWZ
+#define BE8(r, c) ((r) * 8 + (c))
+#define BX(b) 0
+#else
+#define BE8(r, c) ((r) * 8 + ((c) ^ (((r) & 2) << 1)))
+#define BX(b) ((int)(((b) * 2) & 14))
+#endif
   extern __shared__ __align__(16) double sm[];
   const int N = P.T.N, Q = P.T.Q, QP = P.T.QP;
   const double* __restrict__ PhiT = P.T.PhiT;
@@ -213,7 +227,7 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
         const double v = acc[a <= b ? sym_idx<MS>(a, b) : sym_idx<MS>(b, a)];
         if constexpr (HBS) {
           const int R = I * MS + a, C = J * MS + b, bi = R >> 3, bj = C >> 3;
-          Hb[(size_t)(bi * (bi + 1) / 2 + bj) * 64 + (R & 7) * 8 + (C & 7)] = v;
+          Hb[(size_t)(bi * (bi + 1) / 2 + bj) * 64 + (BE8(R & 7, C & 7) ^ BX(bi * (bi + 1) / 2 + bj))] = v;
         } else {
           Hb[(size_t)p * TB + BIDX(a, b)] = v;
         }
@@ -234,17 +248,19 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
     constexpr int NWp = NT / 32;
     const int NBl = (n + 7) >> 3, r = lane >> 2, q = lane & 3;
     auto blk = [&](int I, int J) -> double* { return Hb + (size_t)(I * (I + 1) / 2 + J) * 64; };
+    auto bg = [&](int I, int J) -> int { return BX(I * (I + 1) / 2 + J); };
     // diagonal block K (warp 0): L_KK by quad shuffles, Linv_K (into linvf and the diagonal slot),
     // y_K = Linv_K b_K
     auto diag = [&](int K) {
       double* D = blk(K, K);
-      double a0 = D[r * 8 + 2 * q], a1 = D[r * 8 + 2 * q + 1];
+      const int gD = bg(K, K);
+      double a0 = D[BE8(r, 2 * q) ^ gD], a1 = D[(BE8(r, 2 * q) ^ gD) + 1];
       const bool ok = blk8_diag_factor(a0, a1, lane, min(8, n - 8 * K));
       __syncwarp();
-      *reinterpret_cast<double2*>(linvf + r * 8 + 2 * q) = make_double2(a0, a1);
-      *reinterpret_cast<double2*>(D + r * 8 + 2 * q) = make_double2(a0, a1);
+      *reinterpret_cast<double2*>(linvf + BE8(r, 2 * q)) = make_double2(a0, a1);
+      *reinterpret_cast<double2*>(D + (BE8(r, 2 * q) ^ gD)) = make_double2(a0, a1);
       __syncwarp();
-      const double f0 = linvf[r * 8 + q], f1 = linvf[r * 8 + q + 4];
+      const double f0 = linvf[BE8(r, q)], f1 = linvf[BE8(r, q + 4)];
       const double b0 = lane < 4 ? dd[K * 8 + lane] : 0.0, b1 = lane < 4 ? dd[K * 8 + 4 + lane] : 0.0;
       double y0 = 0.0, y1 = 0.0;
       dmma884(y0, y1, f0, b0);
@@ -256,14 +272,16 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
     // A_IJ -= L_IK L_JK^T for the row I, columns J in [j0, j1]
     auto row_update = [&](int K, int I, int j0, int j1) {
       const double* Lik = blk(I, K);
-      const double a0 = dneg(Lik[r * 8 + q]), a1 = dneg(Lik[r * 8 + q + 4]);
+      const int gik = bg(I, K);
+      const double a0 = dneg(Lik[BE8(r, q) ^ gik]), a1 = dneg(Lik[BE8(r, q + 4) ^ gik]);
       for (int J = j0; J <= j1; ++J) {
         const double* Ljk = blk(J, K);
         double* C = blk(I, J);
-        double2 c = *reinterpret_cast<const double2*>(C + r * 8 + 2 * q);
-        dmma884(c.x, c.y, a0, Ljk[r * 8 + q]);
-        dmma884(c.x, c.y, a1, Ljk[r * 8 + q + 4]);
-        *reinterpret_cast<double2*>(C + r * 8 + 2 * q) = c;
+        const int gjk = bg(J, K), gij = bg(I, J);
+        double2 c = *reinterpret_cast<const double2*>(C + (BE8(r, 2 * q) ^ gij));
+        dmma884(c.x, c.y, a0, Ljk[BE8(r, q) ^ gjk]);
+        dmma884(c.x, c.y, a1, Ljk[BE8(r, q + 4) ^ gjk]);
+        *reinterpret_cast<double2*>(C + (BE8(r, 2 * q) ^ gij)) = c;
       }
     };
     if (t == 0) ctl[1] = 0;
@@ -272,19 +290,20 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
     for (int K = 0; K < NBl; ++K) {
       if (ctl[1]) return false;
       {  // panel: L_IK = A_IK Linv_K^T, b_I -= L_IK y_K
-        const double lf0 = linvf[r * 8 + q], lf1 = linvf[r * 8 + q + 4];
+        const double lf0 = linvf[BE8(r, q)], lf1 = linvf[BE8(r, q + 4)];
         const double yf0 = lane < 4 ? dd[K * 8 + lane] : 0.0, yf1 = lane < 4 ? dd[K * 8 + 4 + lane] : 0.0;
         for (int I = K + 1 + wid; I < NBl; I += NWp) {
           double* B = blk(I, K);
-          double f0 = B[r * 8 + q], f1 = B[r * 8 + q + 4];
+          const int gB = bg(I, K);
+          double f0 = B[BE8(r, q) ^ gB], f1 = B[BE8(r, q + 4) ^ gB];
           double x0 = 0.0, x1 = 0.0;
           dmma884(x0, x1, f0, lf0);
           dmma884(x0, x1, f1, lf1);
           __syncwarp();
-          *reinterpret_cast<double2*>(B + r * 8 + 2 * q) = make_double2(x0, x1);
+          *reinterpret_cast<double2*>(B + (BE8(r, 2 * q) ^ gB)) = make_double2(x0, x1);
           __syncwarp();
-          f0 = B[r * 8 + q];
-          f1 = B[r * 8 + q + 4];
+          f0 = B[BE8(r, q) ^ gB];
+          f1 = B[BE8(r, q + 4) ^ gB];
           double v0 = 0.0, v1 = 0.0;
           dmma884(v0, v1, f0, yf0);
           dmma884(v0, v1, f1, yf1);
@@ -309,10 +328,11 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
     for (int K = NBl - 1; K >= 0; --K) {
       if (wid == 0) {
         const double* D = blk(K, K);
+        const int gD = bg(K, K);
         const double z0 = lane < 4 ? dd[K * 8 + lane] : 0.0, z1 = lane < 4 ? dd[K * 8 + 4 + lane] : 0.0;
         double v0 = 0.0, v1 = 0.0;
-        dmma884(v0, v1, z0, D[q * 8 + r]);
-        dmma884(v0, v1, z1, D[(q + 4) * 8 + r]);
+        dmma884(v0, v1, z0, D[BE8(q, r) ^ gD]);
+        dmma884(v0, v1, z1, D[BE8(q + 4, r) ^ gD]);
         __syncwarp();
         if (lane < 4) {
           dd[K * 8 + 2 * q] = v0;
@@ -324,9 +344,10 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
       const double d0 = lane < 4 ? dd[K * 8 + lane] : 0.0, d1 = lane < 4 ? dd[K * 8 + 4 + lane] : 0.0;
       for (int J = wid; J < K; J += NWp) {
         const double* L = blk(K, J);
+        const int gL = bg(K, J);
         double v0 = 0.0, v1 = 0.0;
-        dmma884(v0, v1, d0, L[q * 8 + r]);
-        dmma884(v0, v1, d1, L[(q + 4) * 8 + r]);
+        dmma884(v0, v1, d0, L[BE8(q, r) ^ gL]);
+        dmma884(v0, v1, d1, L[BE8(q + 4, r) ^ gL]);
         if (lane < 4) {
           dd[J * 8 + 2 * q] -= v0;
           dd[J * 8 + 2 * q + 1] -= v1;
@@ -542,7 +563,7 @@ __global__ void __launch_bounds__(NT) k_dual_big(DualParams P, double* __restric
             for (int e = t; e < NBl * 64; e += NT) {
               const int J = e >> 6, rr = (e >> 3) & 7, cc = e & 7;
               const int R = 8 * I + rr, C = 8 * J + cc;
-              if (R >= n || C >= n) Hb[(size_t)(I * (I + 1) / 2 + J) * 64 + rr * 8 + cc] = (R == C) ? 1.0 : 0.0;
+              if (R >= n || C >= n) Hb[(size_t)(I * (I + 1) / 2 + J) * 64 + (BE8(rr, cc) ^ BX(I * (I + 1) / 2 + J))] = (R == C) ? 1.0 : 0.0;
             }
           }
           for (int r = t; r < NBl * 8; r += NT) dd[r] = (r < n) ? -g[r] : 0.0;

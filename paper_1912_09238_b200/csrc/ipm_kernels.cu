@@ -450,8 +450,11 @@ struct FluxParams {
 #ifndef IPM_FLUXW_MINB
 #define IPM_FLUXW_MINB 3  // CTAs per SM of the single-pass instance (A/B: 1)
 #endif
+#ifndef IPM_FLUXW_MINB_CH
+#define IPM_FLUXW_MINB_CH 2  // CTAs per SM of the chunked instance (128 registers)
+#endif
 template <int FX, int MS, int MK, bool CH>
-__global__ void __launch_bounds__(256, CH ? 1 : IPM_FLUXW_MINB) k_flux_warp(FluxParams P) {
+__global__ void __launch_bounds__(256, CH ? IPM_FLUXW_MINB_CH : IPM_FLUXW_MINB) k_flux_warp(FluxParams P) {
   extern __shared__ __align__(16) double sm[];
   const int N = P.T.N, Q = P.T.Q, QP = P.T.QP;
   // basis table staged in shared memory when it fits (P.tables_in_smem), else read from L2

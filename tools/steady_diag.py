@@ -33,12 +33,15 @@ def main():
     ap.add_argument("--window", type=int, default=20000)
     ap.add_argument("--snap", type=int, default=1000)
     ap.add_argument("--out", default="gpurun_out/steady_diag")
+    ap.add_argument("--cfl", type=float, default=0.0, help="pseudo-time CFL number (default: the config's)")
     args = ap.parse_args()
     cfg = configs.get("cfg4")
     if args.pts:
         nxp, nyp = (int(v) for v in args.pts.split("x"))
         cfg["mesh"].update(nx_pts=nxp, ny_pts=nyp)
     cfg["hessian"] = args.hessian
+    if args.cfl > 0:
+        cfg["cfl"] = args.cfl
     m = cfg["mesh"]
     vert, tri, tags = bump_channel_mesh(m["nx_pts"], m["ny_pts"], m["seed"])
     g = Context(cfg, (vert, tri, tags))
