@@ -480,6 +480,7 @@ __global__ void __launch_bounds__(PSM ? 512 : 384, 1) k_dual_lbfgs(DualParams P)
 // sum-factorised over the tensor Gauss-Legendre rule (the basis is a product of 1D orthonormal
 // Legendre polynomials, the weights a product of 1D weights):
 //   T1[i1 i2][k3] = sum_i3 lambda_(i1,i2,i3) L_i3(x_k3)      T2[i1][k2][k3] = sum_i2 T1[i1 i2][k3] L_i2(x_k2)
+//   (stored state-major: T1[i1 i2][a][k3], T2[i1][a][k2][k3])
 //   Lambda(k1,k2,k3) = sum_i1 T2[i1][k2][k3] L_i1(x_k1)
 // and the transpose for g = Phi^T (omega o u) - uhat — about 35 k fmas each instead of 224 k, with
 // 1D tables in shared memory instead of the 448 KB Phi read from L2.  Everything per cell lives in
@@ -511,8 +512,11 @@ __global__ void __launch_bounds__(NT, 2) k_dual_lbfgs_big(DualParams P) {
   double* g = uh + n;
   double* qv = g + n;
   double* u = qv + n;                      // [MS][Q]
-  double* T1 = u + MS * Q;                 // [npr2][q][MS]  (also R2 of the gradient)
-  double* T2 = T1 + npr2 * q * MS;         // [M+1][q][q][MS] (also R1)
+  // stage buffers state-major (a before the node index), so that consecutive threads, which walk the
+  // node index, read consecutive doubles (with the state innermost the node pass read T2 at a 4-double
+  // stride: 4-way bank conflicts)
+  double* T1 = u + MS * Q;                 // [npr2][MS][q]  (also R2 of the gradient)
+  double* T2 = T1 + npr2 * q * MS;         // [M+1][MS][q][q] (also R1)
   double* L1 = T2 + (M + 1) * q * q * MS;  // [M+1][q]
   double* w1h = L1 + (M + 1) * q;          // [q]
   double* WL1 = w1h + q;                   // [M+1][q] (w_k / 2) L_i(x_k): the gradient stages' 1D table
@@ -591,7 +595,7 @@ __global__ void __launch_bounds__(NT, 2) k_dual_lbfgs_big(DualParams P) {
       const double* x = (mode == 1) ? lt : lam;
       // ---- a2 sum-factorised: stages A, B into T1, T2; stage C + closure per node ----------------------
       for (int o = t; o < npr2 * q * MS; o += NT) {
-        const int a = o % MS, k3 = (o / MS) % q, pr = o / (MS * q);
+        const int k3 = o % q, a = (o / q) % MS, pr = o / (MS * q);
         int i1 = 0;
         while (pr >= prow(i1 + 1)) ++i1;
         const int i2 = pr - prow(i1);
@@ -604,9 +608,9 @@ __global__ void __launch_bounds__(NT, 2) k_dual_lbfgs_big(DualParams P) {
       }
       __syncthreads();
       for (int o = t; o < (M + 1) * q * q * MS; o += NT) {
-        const int a = o % MS, k3 = (o / MS) % q, k2 = (o / (MS * q)) % q, i1 = o / (MS * q * q);
+        const int k3 = o % q, k2 = (o / q) % q, a = (o / (q * q)) % MS, i1 = o / (MS * q * q);
         double s = 0.0;
-        for (int i2 = 0; i2 <= M - i1; ++i2) s = fma(T1[((prow(i1) + i2) * q + k3) * MS + a], L1[i2 * q + k2], s);
+        for (int i2 = 0; i2 <= M - i1; ++i2) s = fma(T1[((prow(i1) + i2) * MS + a) * q + k3], L1[i2 * q + k2], s);
         T2[o] = s;
       }
       __syncthreads();
@@ -622,7 +626,7 @@ __global__ void __launch_bounds__(NT, 2) k_dual_lbfgs_big(DualParams P) {
         for (int i1 = 0; i1 <= M; ++i1) {
           const double lv = L1[i1 * q + k1];
 #pragma unroll
-          for (int a = 0; a < MS; ++a) Lam[a] = fma(T2[(i1 * q * q + k23) * MS + a], lv, Lam[a]);
+          for (int a = 0; a < MS; ++a) Lam[a] = fma(T2[(i1 * MS + a) * q * q + k23], lv, Lam[a]);
         }
         double uk[MS], J[MM], ss;
         if (!Closure<CL, MS>::eval(Lam, uk, J, ss, P.cl)) bad = true;
@@ -662,19 +666,19 @@ __global__ void __launch_bounds__(NT, 2) k_dual_lbfgs_big(DualParams P) {
       if (accept) {
         // ---- a3 sum-factorised: R1 (into T2), R2 (into T1), g ----------------------------------------
         for (int o = t; o < (M + 1) * q * q * MS; o += NT) {
-          const int a = o % MS, k23 = (o / MS) % (q * q), i1 = o / (MS * q * q);
+          const int k23 = o % (q * q), a = (o / (q * q)) % MS, i1 = o / (MS * q * q);
           double s = 0.0;
           for (int k1 = 0; k1 < q; ++k1) s = fma(WL1[i1 * q + k1], u[a * Q + k1 * q * q + k23], s);
           T2[o] = s;
         }
         __syncthreads();
         for (int o = t; o < npr2 * q * MS; o += NT) {
-          const int a = o % MS, k3 = (o / MS) % q, pr = o / (MS * q);
+          const int k3 = o % q, a = (o / q) % MS, pr = o / (MS * q);
           int i1 = 0;
           while (pr >= prow(i1 + 1)) ++i1;
           const int i2 = pr - prow(i1);
           double s = 0.0;
-          for (int k2 = 0; k2 < q; ++k2) s = fma(WL1[i2 * q + k2], T2[((i1 * q + k2) * q + k3) * MS + a], s);
+          for (int k2 = 0; k2 < q; ++k2) s = fma(WL1[i2 * q + k2], T2[((i1 * MS + a) * q + k2) * q + k3], s);
           T1[o] = s;
         }
         __syncthreads();
@@ -683,7 +687,7 @@ __global__ void __launch_bounds__(NT, 2) k_dual_lbfgs_big(DualParams P) {
           const int i = t / MS, a = t - i * MS;
           const int i1 = P.T.idx[i * 3], i2 = P.T.idx[i * 3 + 1], i3 = P.T.idx[i * 3 + 2];
           double s = 0.0;
-          for (int k3 = 0; k3 < q; ++k3) s = fma(WL1[i3 * q + k3], T1[((prow(i1) + i2) * q + k3) * MS + a], s);
+          for (int k3 = 0; k3 < q; ++k3) s = fma(WL1[i3 * q + k3], T1[((prow(i1) + i2) * MS + a) * q + k3], s);
           gr = s - uh[t];
           g[t] = gr;
         }
