@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--nx", type=int, default=0, help="override grid size (cartesian nx = ny)")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-chunks", type=int, default=64, help="ipm_step_host copy/solve ranges (e2e, N=1)")
+    ap.add_argument("--e2e-chunks", type=int, default=32, help="ipm_step_host copy/solve ranges (e2e, N=1)")
     ap.add_argument("--e2e-max-gb", type=float, default=16.0, help="largest state (uhat + lambda) the e2e leg pins")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=9238)

@@ -443,7 +443,7 @@ class Context:
         check(lib().ipm_retard_stage(self.h, C.byref(st)), "ipm_retard_stage")
         return st.value
 
-    def ipm_step_host(self, h_uhat, h_lam, d_uhat, d_lam, t_end=None, nchunks=64):
+    def ipm_step_host(self, h_uhat, h_lam, d_uhat, d_lam, t_end=None, nchunks=32):
         """One step with the state in (pinned) host tensors h_uhat / h_lam, d_uhat / d_lam device work
         buffers; copies overlapped with the dual solves in nchunks cell ranges (synchronous)."""
         info = ipm_step_info()

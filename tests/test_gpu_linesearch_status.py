@@ -6,7 +6,7 @@ ipm_last_cell_linesearch, ipm_step_info.newton_hist / halvings; the CUDA-graph s
 * an INADMISSIBLE cell is reported by ipm_get_status and keeps its level on both sides (reading 34);
 * the step statistics are consistent with the per-cell arrays;
 * the graph-replayed step (small problems) is bit-identical to the launched one;
-* ipm_step_host at 256^2 with 64 copy/solve ranges is bit-identical to ipm_step.
+* ipm_step_host at 256^2 with 32 and 64 copy/solve ranges is bit-identical to ipm_step.
 """
 import os
 
@@ -152,9 +152,10 @@ def test_graph_replay_is_bit_identical_to_launches(torch, name):
     assert out[0][2] == out[1][2]
 
 
-def test_step_host_256_64_chunks_is_bit_identical(torch):
-    """ipm_step_host (host buffers, 64 copy/solve ranges: the bench's e2e path) against ipm_step on
-    a 256^2 config-3 stress state, 2 steps"""
+@pytest.mark.parametrize("nchunks", [32, 64])
+def test_step_host_256_chunks_is_bit_identical(torch, nchunks):
+    """ipm_step_host (host buffers, 32 copy/solve ranges: the bench's e2e path, and 64) against ipm_step
+    on a 256^2 config-3 stress state, 2 steps"""
     cfg = configs.get("cfg3", mesh=dict(nx=256, ny=256))
     g, o, ma = make(cfg)
     base, z, amp = stress_inputs(cfg, seed=2, ma=ma)
@@ -171,7 +172,7 @@ def test_step_host_256_64_chunks_is_bit_identical(torch):
     h_u, h_l = u0.cpu().pin_memory(), l0.cpu().pin_memory()
     du, dl = g.zeros(), g.zeros()
     for _ in range(2):
-        info = g.ipm_step_host(h_u, h_l, du, dl, None, nchunks=64)
+        info = g.ipm_step_host(h_u, h_l, du, dl, None, nchunks=nchunks)
         assert info.failed_cells == 0
     np.testing.assert_array_equal(h_u.numpy(), to_np(u1))
     np.testing.assert_array_equal(h_l.numpy(), to_np(l1))
