@@ -600,6 +600,74 @@ struct DualMma {
     CPH(6);
     return true;
 #endif
+#ifdef IPM_MMA_BACKSUB1
+    // ---- back substitution with one group barrier per block row ------------------------------------------
+    // every warp forms d_K = Linv_K^T (z_K - sum_w p_w[K]) itself (Linv_K from its shared diagonal slot),
+    // then adds L_KJ^T d_K of its own blocks of row K to its partial sums p_WR[J]; the barrier ending the
+    // row publishes them.  The owner of K keeps d_K in dout, copied to dd at the end.  (The panel
+    // buffer is free here.)
+    {
+      constexpr int NV8 = NB * 8;
+      double* pw = pan + WR * NV8;
+      double* dout = pan + W * NV8;
+      double* dsc = pan + (W + 1) * NV8 + WR * 8;
+      for (int x = lane; x < NV8; x += 32) pw[x] = 0.0;
+      named_sync(bar, G);
+      static_for<NB>([&](auto kc) {
+        constexpr int K = NB - 1 - decltype(kc)::value;
+        if (K >= NBl) return;
+        const double2 li = *reinterpret_cast<const double2*>(dg + K * 64 + 2 * lane);
+        double z0 = 0.0, z1 = 0.0;
+        if (lane < 4) {
+          z0 = dd[K * 8 + lane];
+          z1 = dd[K * 8 + 4 + lane];
+#pragma unroll
+          for (int w = 0; w < W; ++w) {
+            z0 -= pan[w * NV8 + K * 8 + lane];
+            z1 -= pan[w * NV8 + K * 8 + 4 + lane];
+          }
+        }
+        double v0 = 0.0, v1 = 0.0;
+        dmma884(v0, v1, z0, li.x);
+        dmma884(v0, v1, z1, li.y);
+        if constexpr (K % W == WR) {
+          if (lane < 4) {
+            dout[K * 8 + 2 * q] = v0;
+            dout[K * 8 + 2 * q + 1] = v1;
+          }
+        }
+        if constexpr (K > 0) {
+          if (lane < 4) {
+            dsc[2 * q] = v0;
+            dsc[2 * q + 1] = v1;
+          }
+          __syncwarp();
+          double d0, d1;
+          vec_frag(dsc, d0, d1);
+          static_for<NBW2>([&](auto sc) {
+            constexpr int s = decltype(sc)::value, br = s * W + WR;
+            if constexpr (br < NBO) {
+              constexpr int I = oI(br), J = oJ(br);
+              if constexpr (I == K) {
+                double w0 = 0.0, w1 = 0.0;
+                dmma884(w0, w1, d0, blk[s][0]);
+                dmma884(w0, w1, d1, blk[s][1]);
+                if (lane < 4) {
+                  pw[J * 8 + 2 * q] += w0;
+                  pw[J * 8 + 2 * q + 1] += w1;
+                }
+              }
+            }
+          });
+        }
+        named_sync(bar, G);
+      });
+      for (int x = WR * 32 + lane; x < NBl * 8; x += W * 32) dd[x] = dout[x];
+      named_sync(bar, G);
+    }
+    CPH(6);
+    return true;
+#endif
     // ---- back substitution: d_K = Linv_K^T z_K; z_J -= L_KJ^T d_K (J < K), as row-vector DMMAs --------
     static_for<NB>([&](auto kc) {
       constexpr int K = NB - 1 - decltype(kc)::value;
