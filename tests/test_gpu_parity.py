@@ -270,3 +270,41 @@ def test_uniform_state_bit_exact(torch):
         info = g.ipm_step(u, lam)
         assert info.newton_iters == 0
     assert torch.equal(u, u0)
+
+
+@pytest.mark.parametrize("deltas", [(1e-4, 1e-5), (1e-9, 1e-12)])
+def test_adaptive_levels_stepwise_exact(torch, deltas):
+    """Alg. 3 line 15 (readings 19-20, 34) step by step: after every step the GPU's
+    levels equal the oracle's except on borderline cells, whose oracle indicator S (computed from the
+    oracle's lambda at the old level) lies within 1e-6 relative of delta_inc or delta_dec (a decision
+    taken by floating point on both sides); the GPU is then reset to the oracle's levels so one flip
+    cannot cascade.  The second pair of thresholds forces level changes (the check is not vacuous)."""
+    d_inc, d_dec = deltas
+    cfg = dict(configs.parity_variant("cfg4"), delta_inc=d_inc, delta_dec=d_dec)
+    g, o, _ = ctx_and_oracle(cfg)
+    u_o = o.project_ic()
+    l_o = o.warm_start(u_o)
+    u_g, l_g = g.zeros(), g.zeros()
+    g.ipm_project_ic(u_g)
+    g.ipm_warm_start(u_g, l_g)
+    changed = borderline = 0
+    for step in range(10):
+        lv_old = o.levels()
+        w, _, st, _, _ = o.step(u_o, l_o)
+        assert w == 0
+        info = g.ipm_step(u_g, l_g)
+        assert info.failed_cells == 0
+        lv_o, lv_g = o.levels(), to_np(g.levels())
+        changed += int((lv_o != lv_old).sum())
+        for j in np.nonzero(lv_o != lv_g)[0]:
+            h, ok = o.moments_from_dual(l_o[j], o.Nl[lv_old[j]])
+            assert ok
+            S = o.indicator(int(lv_old[j]), h)
+            near = min(abs(S - d_inc) / d_inc, abs(S - d_dec) / max(d_dec, 1e-300))
+            assert near <= 1e-6, f"step {step} cell {j}: levels {lv_o[j]} vs {lv_g[j]}, S = {S:.6e}"
+            borderline += 1
+        if borderline:
+            g.set_levels(torch.from_numpy(lv_o).to(u_g.device))
+        assert_moments_close(to_np(u_g), u_o, 1e-9, f"cfg4 step {step}")
+    if d_inc < 1e-6:
+        assert changed > 0
