@@ -521,13 +521,58 @@ static void spec_state(const orc_ctx *c, const orc_state_spec *s, const double *
   prim_to_cons(c, q, u);
 }
 
-/* ghost state at node k for boundary tag t (reading 16) */
+/* characteristic far-field ghost state (reading 37; Riemann invariants of the Euler equations along
+ * the outward normal n, the textbook non-reflecting far-field treatment of the paper's far-field
+ * boundaries): with v_n the normal velocity and c the sound speed,
+ *   R+ = v_n + 2c/(gamma-1) leaves the domain (taken from the interior state ui),
+ *   R- = v_n - 2c/(gamma-1) enters it (taken from the free stream uf);
+ * v_nb = (R+ + R-)/2, c_b = (gamma-1)(R+ - R-)/4; entropy p/rho^gamma and tangential velocity from
+ * the upwind side (free stream where v_nb < 0, interior otherwise).  Supersonic normal flow in the
+ * interior (|v_n| >= c): inflow takes the free stream, outflow the interior state.  2D Euler only. */
+static void farfield_ghost(double gamma, const double *ui, const double *uf, const double *n, double *ug) {
+  double qi[4], qf[4];
+  const double *us[2] = {ui, uf};
+  double *qs[2] = {qi, qf};
+  for (int s = 0; s < 2; ++s) { /* primitives rho, vx, vy, p */
+    const double *u = us[s];
+    double *q = qs[s];
+    q[0] = u[0];
+    q[1] = u[1] / u[0];
+    q[2] = u[2] / u[0];
+    q[3] = (gamma - 1.0) * (u[3] - 0.5 * u[0] * (q[1] * q[1] + q[2] * q[2]));
+  }
+  double vni = qi[1] * n[0] + qi[2] * n[1], vnf = qf[1] * n[0] + qf[2] * n[1];
+  double ci = sqrt(gamma * qi[3] / qi[0]), cf = sqrt(gamma * qf[3] / qf[0]);
+  if (vni <= -ci) { memcpy(ug, uf, 4 * sizeof(double)); return; }
+  if (vni >= ci) { memcpy(ug, ui, 4 * sizeof(double)); return; }
+  double rp = vni + 2.0 * ci / (gamma - 1.0), rm = vnf - 2.0 * cf / (gamma - 1.0);
+  double vnb = 0.5 * (rp + rm), cb = 0.25 * (gamma - 1.0) * (rp - rm);
+  const double *qu = vnb < 0.0 ? qf : qi; /* upwind side */
+  double ent = qu[3] / pow(qu[0], gamma);
+  double vnu = qu[1] * n[0] + qu[2] * n[1];
+  double vt[2] = {qu[1] - vnu * n[0], qu[2] - vnu * n[1]};
+  double rho = pow(cb * cb / (gamma * ent), 1.0 / (gamma - 1.0));
+  double p = rho * cb * cb / gamma;
+  double vx = vt[0] + vnb * n[0], vy = vt[1] + vnb * n[1];
+  ug[0] = rho;
+  ug[1] = rho * vx;
+  ug[2] = rho * vy;
+  ug[3] = p / (gamma - 1.0) + 0.5 * rho * (vx * vx + vy * vy);
+}
+
+void orc_farfield_ghost(double gamma, const double *ui, const double *uf, const double *n, double *ug) {
+  farfield_ghost(gamma, ui, uf, n, ug);
+}
+
+/* ghost state at node k for boundary tag t (reading 16; FARFIELD: reading 37) */
 static void ghost_state(const orc_ctx *c, int tag, int k, const double *uin, const double *n,
                         double *ug) {
   int m = c->m;
   int kind = c->P.bc_kind[tag];
   if (kind == ORC_BC_STATE) {
     memcpy(ug, c->bc_u + ((size_t)tag * c->Q + k) * m, sizeof(double) * m);
+  } else if (kind == ORC_BC_FARFIELD) {
+    farfield_ghost(c->P.gamma, uin, c->bc_u + ((size_t)tag * c->Q + k) * m, n, ug);
   } else if (kind == ORC_BC_SLIP) {
     int d = m - 2;
     double mn = 0.0;
@@ -700,7 +745,7 @@ orc_ctx *orc_create(const orc_problem *P) {
   build_geometry(c);
   c->bc_u = (double *)calloc((size_t)4 * Q * c->m, sizeof(double));
   for (int t = 0; t < 4; ++t)
-    if (P->bc_kind[t] == ORC_BC_STATE)
+    if (P->bc_kind[t] == ORC_BC_STATE || P->bc_kind[t] == ORC_BC_FARFIELD)
       for (int k = 0; k < Q; ++k) spec_state(c, &P->bc_state[t], c->xi + k * p, c->bc_u + ((size_t)t * Q + k) * c->m);
   c->level = (int32_t *)calloc(c->cells, sizeof(int32_t));
   c->n_levels = P->n_levels;
@@ -1341,7 +1386,11 @@ static double cell_rate(const orc_ctx *c, const double *U, int j) {
       int nb = c->nbr[j * F + f];
       if (nb >= 0) continue;
       double ug[4];
-      ghost_state(c, -1 - nb, k, u, c->nrm + (j * F + f) * 2, ug);
+      /* reading 37: a far-field face enters the rate with its free-stream state */
+      if (P->bc_kind[-1 - nb] == ORC_BC_FARFIELD)
+        memcpy(ug, c->bc_u + ((size_t)(-1 - nb) * Q + k) * m, sizeof(double) * m);
+      else
+        ghost_state(c, -1 - nb, k, u, c->nrm + (j * F + f) * 2, ug);
       double rg = state_rate(c, ug, j);
       if (rg > rate) rate = rg;
     }
@@ -1349,7 +1398,7 @@ static double cell_rate(const orc_ctx *c, const double *U, int j) {
   if (c->lq_on)
     for (int f = 0; f < F; ++f) {
       int nb = c->nbr[j * F + f];
-      if (nb >= 0 || P->bc_kind[-1 - nb] != ORC_BC_STATE) continue;
+      if (nb >= 0 || (P->bc_kind[-1 - nb] != ORC_BC_STATE && P->bc_kind[-1 - nb] != ORC_BC_FARFIELD)) continue;
       for (int k = 0; k < Q; ++k) {
         double rg = state_rate(c, c->bc_u + ((size_t)(-1 - nb) * Q + k) * m, j);
         if (rg > rate) rate = rg;

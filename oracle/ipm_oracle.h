@@ -31,7 +31,9 @@ enum { ORC_FLUX_LF_GLOBAL = 0, ORC_FLUX_HLL = 1, ORC_FLUX_RUSANOV = 2 };
 /* meshes */
 enum { ORC_MESH_1D = 0, ORC_MESH_CART2D = 1, ORC_MESH_TRI = 2 };
 /* boundary conditions (ghost states at quadrature nodes, reading 16) */
-enum { ORC_BC_TRANSMISSIVE = 0, ORC_BC_STATE = 1, ORC_BC_SLIP = 2 };
+enum { ORC_BC_TRANSMISSIVE = 0, ORC_BC_STATE = 1, ORC_BC_SLIP = 2, ORC_BC_FARFIELD = 3 };
+/* characteristic far-field ghost (reading 37): ui interior, uf free stream, n outward unit normal */
+void orc_farfield_ghost(double gamma, const double *ui, const double *uf, const double *n, double *ug);
 /* state specs (primitive states, possibly xi-dependent) */
 enum { ORC_SPEC_AFFINE = 0, ORC_SPEC_FREESTREAM = 1 };
 /* IC kinds */

@@ -22,7 +22,7 @@ HDR = os.path.join(HERE, "ipm_oracle.h")
 CLOSURE = {"quadratic": 0, "barrier": 1, "euler": 2}
 FLUX = {"lf_global": 0, "hll": 1, "rusanov": 2}
 MESH = {"1d": 0, "cart2d": 1, "tri": 2}
-BC = {"transmissive": 0, "state": 1, "slip": 2}
+BC = {"transmissive": 0, "state": 1, "slip": 2, "farfield": 3}
 IC = {"uniform": 0, "step1d": 1, "quad2d": 2}
 NEWTON = {"full": 0, "one_step": 1}
 UPDATE = {"conservative": 0, "paper_c": 1}
@@ -105,6 +105,7 @@ def lib():
             "orc_project_ic": (None, [P, C.POINTER(ICSpec), D]),
             "orc_warm_start": (None, [P, D, D]),
             "orc_indicator": (C.c_double, [P, C.c_int, D]),
+            "orc_farfield_ghost": (None, [C.c_double, D, D, D, D]),
             "orc_set_levels": (None, [P, I]), "orc_get_levels": (None, [P, I]),
             "orc_retard_stage": (C.c_int, [P]),
             "orc_problem_size": (C.c_size_t, []),
@@ -131,6 +132,14 @@ def lib():
 
 def _d(a):
     return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def farfield_ghost(gamma, ui, uf, n):
+    """characteristic far-field ghost state (reading 37) of interior ui, free stream uf, outward normal n"""
+    ui, uf, n = (np.ascontiguousarray(x, np.float64) for x in (ui, uf, n))
+    ug = np.zeros(4)
+    lib().orc_farfield_ghost(float(gamma), _d(ui), _d(uf), _d(n), _d(ug))
+    return ug
 
 
 def _i(a):
