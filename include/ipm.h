@@ -75,7 +75,11 @@ typedef enum {
 } ipm_flux;
 
 typedef enum { IPM_MESH_1D = 0, IPM_MESH_CART2D = 1, IPM_MESH_TRI = 2 } ipm_mesh_kind;
-typedef enum { IPM_BC_TRANSMISSIVE = 0, IPM_BC_STATE = 1, IPM_BC_SLIP = 2 } ipm_bc_kind;
+/* IPM_BC_FARFIELD: characteristic far-field ghost (reading 37) from the
+ * interior node state and the free stream bc_state: Riemann invariants along the outward normal.
+ * Triangle meshes with m = 4 only (ipm_init returns IPM_ERR_ARG otherwise); the CFL rate takes the
+ * free-stream state at such faces. */
+typedef enum { IPM_BC_TRANSMISSIVE = 0, IPM_BC_STATE = 1, IPM_BC_SLIP = 2, IPM_BC_FARFIELD = 3 } ipm_bc_kind;
 typedef enum { IPM_NEWTON_FULL = 0, IPM_NEWTON_ONE_STEP = 1 } ipm_newton_mode;
 typedef enum { IPM_UPDATE_CONSERVATIVE = 0, IPM_UPDATE_PAPER_C = 1 } ipm_update_form;
 typedef enum { IPM_IC_UNIFORM = 0, IPM_IC_STEP1D = 1, IPM_IC_QUAD2D = 2 } ipm_ic_kind;

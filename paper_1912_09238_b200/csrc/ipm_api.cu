@@ -388,6 +388,11 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   if (C.n_levels < 0 || C.n_levels > 8) return fail(IPM_ERR_ARG, "n_levels in [0, 8]");
   if (C.n_levels > 0 && C.level_M[C.n_levels - 1] != C.M) return fail(IPM_ERR_ARG, "level_M[last] must equal M");
   if (C.n_retard < 0 || C.n_retard > 8) return fail(IPM_ERR_ARG, "n_retard must be in [0, 8]");
+  for (int t = 0; t < 4; ++t) {
+    if (C.bc_kind[t] < IPM_BC_TRANSMISSIVE || C.bc_kind[t] > IPM_BC_FARFIELD) return fail(IPM_ERR_ARG, "bad bc_kind");
+    if (C.bc_kind[t] == IPM_BC_FARFIELD && (C.mesh_kind != IPM_MESH_TRI || C.m != 4 || C.closure != IPM_CLOSURE_EULER))
+      return fail(IPM_ERR_ARG, "far-field boundaries: triangle meshes, 2D Euler only (reading 37)");
+  }
   // per-level nested rules (reading 36): a nested ladder of tensor Clenshaw-Curtis rules, the finest
   // being the context's rule
   const bool level_rules = C.n_levels > 0 && C.level_q1d[0] > 0;
@@ -516,7 +521,7 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
   // boundary ghost states per node and their CFL contribution
   std::vector<double> ghost((size_t)4 * Q * m, 0.0);
   for (int t = 0; t < 4; ++t)
-    if (C.bc_kind[t] == IPM_BC_STATE)
+    if (C.bc_kind[t] == IPM_BC_STATE || C.bc_kind[t] == IPM_BC_FARFIELD)  // FARFIELD: the free stream
       for (int k = 0; k < Q; ++k)
         HostPrim::eval(C.bc_state[t], &c->xi[(size_t)k * p], p, m, C.gamma, &ghost[((size_t)t * Q + k) * m]);
   double grate = 0.0;
@@ -525,7 +530,7 @@ ipm_status ipm_init(const ipm_config* cfg, ipm_ctx** out) {
       const int nb = G.nbr[j * F + f];
       if (nb >= 0) continue;
       const int tag = -1 - nb;
-      if (C.bc_kind[tag] != IPM_BC_STATE) continue;
+      if (C.bc_kind[tag] != IPM_BC_STATE && C.bc_kind[tag] != IPM_BC_FARFIELD) continue;  // reading 37
       for (int k = 0; k < Q; ++k) {
         const double* ug = &ghost[((size_t)tag * Q + k) * m];
         double r;

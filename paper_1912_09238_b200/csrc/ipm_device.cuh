@@ -268,4 +268,39 @@ struct NumFlux<FX_RUSANOV, MS> {
   }
 };
 
+// Characteristic far-field ghost state (reading 37), 2D Euler: the
+// outgoing Riemann invariant v_n + 2c/(g-1) from the interior node state ui, the incoming one
+// v_n - 2c/(g-1) from the free-stream node state uf; entropy p/rho^g and tangential velocity from the
+// upwind side; supersonic normal flow in the interior takes uf (inflow) or ui (outflow).  n: outward unit
+// normal.  Full-precision sqrt / pow (parity with the oracle's libm at 1e-12).
+__device__ __forceinline__ void farfield_ghost(double g, const double* ui, const double* uf, const double* n,
+                                               double* ug) {
+  const double ri = ui[0], vxi = ui[1] / ri, vyi = ui[2] / ri;
+  const double pi = (g - 1.0) * (ui[3] - 0.5 * ri * (vxi * vxi + vyi * vyi));
+  const double rf = uf[0], vxf = uf[1] / rf, vyf = uf[2] / rf;
+  const double pf = (g - 1.0) * (uf[3] - 0.5 * rf * (vxf * vxf + vyf * vyf));
+  const double vni = vxi * n[0] + vyi * n[1], vnf = vxf * n[0] + vyf * n[1];
+  const double ci = sqrt(g * pi / ri), cf = sqrt(g * pf / rf);
+  if (vni <= -ci || vni >= ci) {
+    const double* src = vni <= -ci ? uf : ui;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) ug[a] = src[a];
+    return;
+  }
+  const double igm = 1.0 / (g - 1.0);
+  const double rp = vni + 2.0 * ci * igm, rm = vnf - 2.0 * cf * igm;
+  const double vnb = 0.5 * (rp + rm), cb = 0.25 * (g - 1.0) * (rp - rm);
+  const bool in = vnb < 0.0;
+  const double ru = in ? rf : ri, vxu = in ? vxf : vxi, vyu = in ? vyf : vyi, pu = in ? pf : pi;
+  const double ent = pu / pow(ru, g);
+  const double vnu = vxu * n[0] + vyu * n[1];
+  const double vx = (vxu - vnu * n[0]) + vnb * n[0], vy = (vyu - vnu * n[1]) + vnb * n[1];
+  const double rho = pow(cb * cb / (g * ent), igm);
+  const double p = rho * cb * cb / g;
+  ug[0] = rho;
+  ug[1] = rho * vx;
+  ug[2] = rho * vy;
+  ug[3] = p * igm + 0.5 * rho * (vx * vx + vy * vy);
+}
+
 }  // namespace ipm

@@ -536,6 +536,8 @@ __global__ void __launch_bounds__(256, CH ? IPM_FLUXW_MINB_CH : IPM_FLUXW_MINB) 
             const double* gs = P.mesh.ghost + ((int64_t)tag * Q + k) * MS;
 #pragma unroll
             for (int a = 0; a < MS; ++a) un[a] = gs[a];
+          } else if (MS == 4 && kind == 3) {  // characteristic far field (reading 37; triangles only)
+            farfield_ghost(gam, uj, P.mesh.ghost + ((int64_t)tag * Q + k) * MS, nv, un);
           } else if (kind == 2 && MS > 1) {
             // slip wall: mirror the normal momentum about the outward normal
             const double sgn = (MK == MK_TRI || (f & 1)) ? 1.0 : -1.0;
@@ -723,6 +725,8 @@ __global__ void __launch_bounds__(256) k_sc_update(FluxParams P, const double* _
             const double* gs = P.mesh.ghost + ((int64_t)tag * Q + k) * MS;
 #pragma unroll
             for (int a = 0; a < MS; ++a) un[a] = gs[a];
+          } else if (MS == 4 && kind == 3) {  // characteristic far field (reading 37; triangles only)
+            farfield_ghost(gam, uj, P.mesh.ghost + ((int64_t)tag * Q + k) * MS, nv, un);
           } else if (kind == 2 && MS > 1) {  // slip wall: mirror the normal momentum
             const double sgn = (MK == MK_TRI || (f & 1)) ? 1.0 : -1.0;
             const double on[2] = {nv[0] * sgn, nv[1] * sgn};

@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("IPM_LIB", os.path.join(HERE, "libipm.so"))
 CLOSURE = {"quadratic": 0, "barrier": 1, "euler": 2}
 FLUX = {"lf_global": 0, "hll": 1, "rusanov": 2}
 MESH = {"1d": 0, "cart2d": 1, "tri": 2}
-BC = {"transmissive": 0, "state": 1, "slip": 2}
+BC = {"transmissive": 0, "state": 1, "slip": 2, "farfield": 3}
 NEWTON = {"full": 0, "one_step": 1}
 UPDATE = {"conservative": 0, "paper_c": 1}
 IC = {"uniform": 0, "step1d": 1, "quad2d": 2}

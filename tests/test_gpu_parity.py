@@ -308,3 +308,43 @@ def test_adaptive_levels_stepwise_exact(torch, deltas):
         assert_moments_close(to_np(u_g), u_o, 1e-9, f"cfg4 step {step}")
     if d_inc < 1e-6:
         assert changed > 0
+
+
+def _farfield(cfg):
+    cfg = dict(cfg)
+    cfg["bc"] = [("farfield", s) if k == "state" else (k, s) for k, s in cfg["bc"]]
+    return cfg
+
+
+def test_farfield_cfg4_parity(torch):
+    """Reading 37 (characteristic far-field ghosts at the bump channel's inlet and outlet) on the GPU
+    (k_flux_warp) against the oracle: One-Shot adaptive config 4, 15 pseudo-steps, from a perturbed
+    state so that the interior node states differ from the free stream at the boundary"""
+    cfg = _farfield(configs.parity_variant("cfg4"))
+    g, o, ma = ctx_and_oracle(cfg)
+    base, z, amp = stress_inputs(cfg, 37, ma)
+    lam_o = o.stress_dual(base, z, amp)
+    u0 = o.moments_from_dual_all(lam_o)
+    u_o, l_o, io = o.run(n_steps=15, uhat=u0.copy(), lam=lam_o.copy(), record=True)
+    u_g = torch.from_numpy(u0.copy()).cuda()
+    l_g = torch.from_numpy(lam_o.copy()).cuda()
+    _, _, ig = g.run(uhat=u_g, lam=l_g, n_steps=15, record=True)
+    assert (o.levels() != to_np(g.levels())).mean() < 0.01
+    assert_moments_close(to_np(u_g), u_o, 1e-9, "cfg4 farfield")
+    for (dto, ito, ro), (dtg, itg, rg) in zip(io["hist"], ig["hist"]):
+        assert abs(dto - dtg) <= 1e-12 * dto
+        assert np.abs(ito - itg).max() <= 1
+        assert abs(ro - rg) <= 1e-9 * max(ro, 1e-300)
+    # the far-field ghosts differ from the Dirichlet ones on this state: the runs must differ
+    cfg_d = configs.parity_variant("cfg4")
+    od = __import__("oracle").Oracle(cfg_d, ma)
+    u_d, _, _ = od.run(n_steps=15, uhat=u0.copy(), lam=lam_o.copy())
+    assert np.abs(u_d - u_o).max() > 1e-6
+
+
+def test_farfield_refused_off_triangles(torch):
+    from paper_1912_09238_b200 import Context, IPMError
+
+    cfg = _farfield(dict(configs.parity_variant("cfg3"), bc=[("state", configs.parity_variant("cfg4")["bc"][1][1])] * 4))
+    with pytest.raises(IPMError):
+        Context(cfg)

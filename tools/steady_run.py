@@ -32,6 +32,8 @@ def main():
     ap.add_argument("--no-adaptive", action="store_true")
     ap.add_argument("--pts", default="", help="mesh points NXxNY of the bump channel (default: BASELINE 548x183)")
     ap.add_argument("--hessian", default="newton", choices=["newton", "lbfgs"])
+    ap.add_argument("--farfield", action="store_true",
+                    help="characteristic far-field ghosts at the inlet and outlet (reading 37) instead of Dirichlet")
     ap.add_argument("--newton", default="", choices=["", "full", "one_step"], help="override the config's mode")
     args = ap.parse_args()
     cfg = configs.get(args.config)
@@ -41,6 +43,8 @@ def main():
         nxp, nyp = (int(v) for v in args.pts.split("x"))
         cfg["mesh"].update(nx_pts=nxp, ny_pts=nyp)
     cfg["hessian"] = args.hessian
+    if args.farfield:
+        cfg["bc"] = [("farfield", sp) if k == "state" else (k, sp) for k, sp in cfg["bc"]]
     if args.newton:
         cfg["newton"] = args.newton
     m = cfg["mesh"]
