@@ -272,7 +272,7 @@ struct NumFlux<FX_RUSANOV, MS> {
 // outgoing Riemann invariant v_n + 2c/(g-1) from the interior node state ui, the incoming one
 // v_n - 2c/(g-1) from the free-stream node state uf; entropy p/rho^g and tangential velocity from the
 // upwind side; supersonic normal flow in the interior takes uf (inflow) or ui (outflow).  n: outward unit
-// normal.  Full-precision sqrt / pow (parity with the oracle's libm at 1e-12).
+// normal.  Full-precision sqrt / pow (no fast approximations: the host libm's results to ~1 ulp).
 __device__ __forceinline__ void farfield_ghost(double g, const double* ui, const double* uf, const double* n,
                                                double* ug) {
   const double ri = ui[0], vxi = ui[1] / ri, vyi = ui[2] / ri;
