@@ -318,9 +318,11 @@ def _farfield(cfg):
 
 def test_farfield_cfg4_parity(torch):
     """Reading 37 (characteristic far-field ghosts at the bump channel's inlet and outlet) on the GPU
-    (k_flux_warp) against the oracle: One-Shot adaptive config 4, 15 pseudo-steps, from a perturbed
-    state so that the interior node states differ from the free stream at the boundary"""
+    (k_flux_warp) against the oracle: One-Shot config 4, 15 pseudo-steps, from the seeded stress state
+    so that the interior node states differ from the free stream at the boundary (whole basis in
+    every cell, as in the stress parity tests: the stress duals carry every mode)"""
     cfg = _farfield(configs.parity_variant("cfg4"))
+    cfg["levels"] = None
     g, o, ma = ctx_and_oracle(cfg)
     base, z, amp = stress_inputs(cfg, 37, ma)
     lam_o = o.stress_dual(base, z, amp)
@@ -329,14 +331,13 @@ def test_farfield_cfg4_parity(torch):
     u_g = torch.from_numpy(u0.copy()).cuda()
     l_g = torch.from_numpy(lam_o.copy()).cuda()
     _, _, ig = g.run(uhat=u_g, lam=l_g, n_steps=15, record=True)
-    assert (o.levels() != to_np(g.levels())).mean() < 0.01
     assert_moments_close(to_np(u_g), u_o, 1e-9, "cfg4 farfield")
     for (dto, ito, ro), (dtg, itg, rg) in zip(io["hist"], ig["hist"]):
         assert abs(dto - dtg) <= 1e-12 * dto
         assert np.abs(ito - itg).max() <= 1
         assert abs(ro - rg) <= 1e-9 * max(ro, 1e-300)
     # the far-field ghosts differ from the Dirichlet ones on this state: the runs must differ
-    cfg_d = configs.parity_variant("cfg4")
+    cfg_d = dict(configs.parity_variant("cfg4"), levels=None)
     od = __import__("oracle").Oracle(cfg_d, ma)
     u_d, _, _ = od.run(n_steps=15, uhat=u0.copy(), lam=lam_o.copy())
     assert np.abs(u_d - u_o).max() > 1e-6
