@@ -453,7 +453,10 @@ struct FluxParams {
 #ifndef IPM_FLUXW_MINB_CH
 #define IPM_FLUXW_MINB_CH 2  // CTAs per SM of the chunked instance (128 registers)
 #endif
-template <int FX, int MS, int MK, bool CH>
+// FF: the instance with the characteristic far-field branch (reading 37), launched only when a boundary
+// tag asks for it: inlined into the common instance it cost config 4 1.22 -> 1.49 ms (r02ao) under the
+// 80-register bound
+template <int FX, int MS, int MK, bool CH, bool FF = false>
 __global__ void __launch_bounds__(256, CH ? IPM_FLUXW_MINB_CH : IPM_FLUXW_MINB) k_flux_warp(FluxParams P) {
   extern __shared__ __align__(16) double sm[];
   const int N = P.T.N, Q = P.T.Q, QP = P.T.QP;
@@ -536,7 +539,7 @@ __global__ void __launch_bounds__(256, CH ? IPM_FLUXW_MINB_CH : IPM_FLUXW_MINB) 
             const double* gs = P.mesh.ghost + ((int64_t)tag * Q + k) * MS;
 #pragma unroll
             for (int a = 0; a < MS; ++a) un[a] = gs[a];
-          } else if (MS == 4 && kind == 3) {  // characteristic far field (reading 37; triangles only)
+          } else if (FF && MS == 4 && kind == 3) {  // characteristic far field (reading 37; triangles only)
             farfield_ghost(gam, uj, P.mesh.ghost + ((int64_t)tag * Q + k) * MS, nv, un);
           } else if (kind == 2 && MS > 1) {
             // slip wall: mirror the normal momentum about the outward normal
@@ -1690,7 +1693,13 @@ static int flux_impl(const KernelCtx& k, const FluxLaunch& a) {
   int warps = (int)std::min<size_t>(8, (k.smem_optin - base) / pw);
   if (warps < 1) return -1;
   const size_t smem = base + warps * pw;
-  auto kern = (qchunk > 0 && qchunk < k.T.Q) ? k_flux_warp<FX, MS, MK, true> : k_flux_warp<FX, MS, MK, false>;
+  const bool ch = qchunk > 0 && qchunk < k.T.Q;
+  void (*kern)(FluxParams) = ch ? k_flux_warp<FX, MS, MK, true> : k_flux_warp<FX, MS, MK, false>;
+  if constexpr (MS == 4 && MK == MK_TRI) {
+    bool ff = false;
+    for (int t = 0; t < 4; ++t) ff = ff || k.mesh.bc_kind[t] == 3;
+    if (ff) kern = ch ? k_flux_warp<FX, MS, MK, true, true> : k_flux_warp<FX, MS, MK, false, true>;
+  }
   int per_sm = configure(kern, warps * 32, smem);
   if (per_sm < 1) per_sm = 1;
   const int64_t want = (k.mesh.cells - a.cell0 + warps - 1) / warps;
